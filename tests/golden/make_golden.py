@@ -1,0 +1,207 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (the only place /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports `sketchqr` from /root/reference/pkg/src unmodified (a bf16 tag is
+injected at runtime for the mixed-precision fixture, exactly as SURVEY A.6 —
+the reference source is not edited) and writes small `.npz` files next to
+this script.  The fixtures pin the oracle (`oracle/sketchqr_oracle.py`) and
+are the GPU parity tests' known answers.  Nothing on the GPU box reads
+/root/reference.
+"""
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF)
+
+import sketchqr  # noqa: E402
+from sketchqr import precision as P  # noqa: E402
+from sketchqr.baselines import householder_qr  # noqa: E402
+from sketchqr.experiments import gen_cmatrix  # noqa: E402
+from sketchqr.krylov import hessenberg_lstsq, rhqr_arnoldi, rhqr_gmres  # noqa: E402
+from sketchqr.linalg import cond_number, factorization_errors, orthogonality_error  # noqa: E402
+from sketchqr.rhqr import (apply_reflectors_compact, rec_rhqr, rh_vector,  # noqa: E402
+                           rhqr_left, sketch_q, thin_q)
+from sketchqr.sketching import (EmbeddedSketch, GaussianSketch,  # noqa: E402
+                                IdentitySketch, SRHTSketch)
+
+
+def save(name, **arrs):
+    np.savez_compressed(os.path.join(OUT, name + ".npz"), **arrs)
+    print("wrote", name, {k: np.shape(v) for k, v in arrs.items()})
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def srht_cases():
+    # (ell, n, seed, k) — includes the padding case n=12 (test_sketching.py:92)
+    # and the config-1 Omega shape (n = 2^14 - 32)
+    cases = [(8, 12, 3, 3), (5, 6, 21, 1), (64, 1000, 5, 4), (128, 16352, 7, 2),
+             (256, 65536 - 128, 11, 2), (400, 8191, 13, 1)]
+    for ell, n, seed, k in cases:
+        op = SRHTSketch(ell, n, seed)
+        rng = np.random.default_rng(seed + 1000)
+        X = rng.standard_normal((n, k))
+        out = dict(ell=ell, n=n, seed=seed, n_pad=op.n_pad, scale=op.scale,
+                   signbits=np.packbits(op.signs < 0, bitorder="little"),
+                   indices=op.indices, X=X, Y64=op.apply(X),
+                   Y32=op.apply(P.round_to(X, "single"), dtype=np.float32))
+        if n <= 4096:  # fp16 overflows for large n
+            out["Y16"] = op.apply(P.round_to(X, "half"), dtype=np.float16)
+        save(f"srht_{ell}_{n}_{seed}", **out)
+
+
+def gauss_cases():
+    op = GaussianSketch(8, 50, 2)
+    rng = np.random.default_rng(77)
+    X = rng.standard_normal((50, 3))
+    G = op._cache[np.dtype(np.float64)]
+    save("gauss_8_50_2", G=G, X=X, Y=op.apply(X))
+    op = GaussianSketch(24, 5000, 9)  # 24*5000 <= 2^23: cached
+    save("gauss_24_5000_9_sha", sha=np.frombuffer(
+        bytes.fromhex(sha(op._cache[np.dtype(np.float64)])), dtype=np.uint8))
+
+
+def rh_vector_cases():
+    psi = EmbeddedSketch(2, IdentitySketch(2))
+    w = np.array([3.0, 0.0, 4.0, 0.0])
+    a = rh_vector(w, psi.apply(w), 1)
+    b = rh_vector(w, psi.apply(w), 1, scaling="unit")
+    save("rh_vector_345", w=w, u_sqrt2=a.u, s_sqrt2=a.s, beta_sqrt2=a.beta,
+         rho=a.rho, sigma=a.sigma, u_unit=b.u, s_unit=b.s, beta_unit=b.beta)
+
+
+def factor_dump(F):
+    return dict(U=F.U, S=F.S, T=F.T, R=F.R, sigmas=F.sigmas, rhos=F.rhos,
+                betas=F.betas)
+
+
+def diag_dump(W, F):
+    Q = thin_q(F)
+    fro, mx, _ = factorization_errors(W, Q, F.R)
+    return dict(cond_q=cond_number(Q), orth=orthogonality_error(F.psi.apply(Q)),
+                orth_sq=orthogonality_error(sketch_q(F)), fro=fro, maxcol=mx)
+
+
+def rhqr_cases():
+    # reduced config 1 / config 2 shapes plus unit scaling and a ragged n
+    rng = np.random.default_rng(1)
+    W = rng.standard_normal((2048, 16))
+    F = rhqr_left(W, SRHTSketch(64, 2048 - 16, 5))
+    save("rhqr_left_2048x16_srht64", W=W, seed=5, ell=64, **factor_dump(F), **diag_dump(W, F))
+    F = rhqr_left(W, SRHTSketch(64, 2048 - 16, 5), scaling="unit")
+    save("rhqr_left_2048x16_srht64_unit", W=W, seed=5, ell=64, **factor_dump(F))
+    rng = np.random.default_rng(2)
+    W = rng.standard_normal((1000, 12))
+    F = rhqr_left(W, GaussianSketch(40, 1000 - 12, 8))
+    save("rhqr_left_1000x12_gauss40", W=W, seed=8, ell=40, **factor_dump(F))
+    # config-1 full size (2^14 x 32, SRHT 128): keep the small factors and U checksums
+    rng = np.random.default_rng(2024)
+    W = rng.standard_normal((1 << 14, 32))
+    F = rhqr_left(W, SRHTSketch(128, (1 << 14) - 32, 17))
+    d = factor_dump(F)
+    U = d.pop("U")
+    save("rhqr_left_cfg1", W_seed=2024, seed=17, ell=128, U_colnorm=np.linalg.norm(U, axis=0),
+         U_head=U[:64], U_tail=U[-64:], **d, **diag_dump(W, F))
+    # ill-conditioned config-2 shape at reduced n
+    rng = np.random.default_rng(3)
+    n, m = 1 << 14, 32
+    A = np.linalg.qr(rng.standard_normal((n, m)))[0]
+    B = np.linalg.qr(rng.standard_normal((m, m)))[0]
+    W = A @ np.diag(np.logspace(0, -15, m)) @ B
+    F = rhqr_left(W, SRHTSketch(64, n - m, 23))
+    d = factor_dump(F)
+    U = d.pop("U")
+    # W is regenerated by tests/golden/inputs.py (same numpy recipe); its sha pins it
+    save("rhqr_left_illcond_16384x32", W_sha=np.array(sha(W)), seed=23, ell=64,
+         U_colnorm=np.linalg.norm(U, axis=0), U_head=U[:64], **d, **diag_dump(W, F))
+    # breakdown on an exactly dependent column (test_rhqr.py:296-301)
+    W = np.zeros((32, 2))
+    W[0] = 1.0
+    try:
+        rhqr_left(W, SRHTSketch(12, 30, 34))
+        msg = "none"
+    except sketchqr.BreakdownError as e:
+        msg = str(e)
+    save("rhqr_breakdown", W=W, msg=np.array(msg))
+
+
+def mixed_cases():
+    rng = np.random.default_rng(4)
+    W = rng.standard_normal((4096, 16))
+    for tag in ("single", "half"):
+        pol = P.PrecisionPolicy(high="double", low=tag)
+        F = rhqr_left(W, SRHTSketch(64, 4096 - 16, 29), policy=pol)
+        save(f"rhqr_left_4096x16_{tag}", W=W, seed=29, ell=64, **factor_dump(F))
+    # bf16 injection — runtime only, reference source untouched
+    import ml_dtypes
+    if "bf16" not in P.PRECISIONS:
+        P.PRECISIONS = P.PRECISIONS + ("bf16",)
+        P.DTYPES["bf16"] = ml_dtypes.bfloat16
+        P.UNIT_ROUNDOFF["bf16"] = 2.0 ** -8
+    Ws = W * np.logspace(0, -8, 16)[None, :]
+    pol = P.PrecisionPolicy(high="double", low="bf16")
+    F = rhqr_left(Ws, SRHTSketch(64, 4096 - 16, 31), policy=pol)
+    save("rhqr_left_4096x16_bf16", W=Ws, seed=31, ell=64, **factor_dump(F))
+    op = SRHTSketch(64, 4096 - 16, 31)
+    Xb = P.round_to(rng.standard_normal((4096 - 16, 2)), "bf16")
+    save("srht_bf16_64_4080_31", X=Xb, Y=op.apply(Xb, dtype=ml_dtypes.bfloat16))
+
+
+def rec_cases():
+    W = gen_cmatrix(4096, 16)
+    F = rec_rhqr(W, GaussianSketch(64, 4096 - 16, 41))
+    save("rec_rhqr_cmatrix_4096x16", W=W, seed=41, ell=64, **factor_dump(F), **diag_dump(W, F))
+    Z = np.random.default_rng(5).standard_normal((80, 16))
+    Q, R, _, aux = householder_qr(Z)
+    save("householder_80x16", Z=Z, Q=Q, R=R, U=aux["U"], T=aux["T"])
+
+
+def krylov_cases():
+    rng = np.random.default_rng(6)
+    n, m = 400, 20
+    A = rng.standard_normal((n, n)) / np.sqrt(n) + 2.0 * np.eye(n)
+    A[rng.random((n, n)) < 0.9] = 0.0
+    A += 2.0 * np.eye(n)
+    b = rng.standard_normal(n)
+    om = SRHTSketch(4 * (m + 1), n - m - 1, 43)
+    bun = rhqr_arnoldi(A, b, None, m, om)
+    x, hist = rhqr_gmres(A, b, None, m, om)
+    save("arnoldi_400_m20", A=A, b=b, seed=43, ell=4 * (m + 1), U=bun.U, S=bun.S, T=bun.T,
+         H=bun.H, beta=bun.beta, Q=bun.Q_cols, x=x, hist=hist)
+    H = np.triu(np.random.default_rng(7).standard_normal((11, 10)), -1)
+    y, res, h = hessenberg_lstsq(H, 1.7, history=True)
+    save("hessenberg_11x10", H=H, beta=1.7, y=y, res=res, hist=h)
+
+
+def apply_compact_cases():
+    rng = np.random.default_rng(8)
+    n, m = 600, 8
+    W = rng.standard_normal((n, m))
+    F = rhqr_left(W, SRHTSketch(32, n - m, 47))
+    X = rng.standard_normal((n, 3))
+    save("apply_compact_600x8", W=W, seed=47, ell=32, X=X,
+         Y=apply_reflectors_compact(F.U, F.S, F.T, X, F.psi),
+         Yt=apply_reflectors_compact(F.U, F.S, F.T, X, F.psi, transpose_t=True),
+         Q=thin_q(F), SQ=sketch_q(F))
+
+
+if __name__ == "__main__":
+    srht_cases()
+    gauss_cases()
+    rh_vector_cases()
+    rhqr_cases()
+    mixed_cases()
+    rec_cases()
+    krylov_cases()
+    apply_compact_cases()

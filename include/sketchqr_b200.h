@@ -1,0 +1,170 @@
+/*
+ * sketchqr_b200 — C ABI of the B200-native randomized Householder QR library.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `sketchqr` (arXiv 2405.10923, /root/reference/pkg/src/sketchqr).  Every
+ * entry point below names the reference function it replaces.  The Python
+ * facade (paper_2405_10923_b200/) binds these with ctypes; INTEGRATION.md
+ * shows the binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no torch types.  Device pointers are CUDA
+ *    device addresses on the context's device.
+ *  - n-dimensional operands (W, U, X, Q, Krylov vectors) are COLUMN-MAJOR:
+ *    element (i, j) at ptr[i + j*ld].  Sketch-space operands (S, T, R, Y, H)
+ *    are fp64, column-major as well.
+ *  - Calls are asynchronous and ordered on the context's stream.  The
+ *    library never allocates or frees caller buffers; scratch workspace is
+ *    owned by the context.  A context is not thread-safe: one per device per
+ *    thread.
+ *  - Every call returns an sqb_status.  Numerical failures detected on the
+ *    device (breakdowns, singular factors) are recorded in a device status
+ *    word that makes the rest of the call chain a no-op; read it with
+ *    sqb_ctx_status(), which synchronises the stream.
+ */
+#ifndef SKETCHQR_B200_H
+#define SKETCHQR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (the facade maps them to the reference's exception types) */
+enum sqb_status {
+  SQB_OK = 0,
+  SQB_ERR_ARG = 1,        /* ValueError (sketching.py:52, :143; rhqr.py:204-215) */
+  SQB_ERR_BREAKDOWN = 2,  /* BreakdownError "... column {j} ..." (linalg.py:18, rhqr.py:73-79) */
+  SQB_ERR_SINGULAR = 3,   /* SingularFactorError (linalg.py:35, :92-99) */
+  SQB_ERR_CUDA = 4,
+  SQB_ERR_NCCL = 5,
+  SQB_ERR_RANGE = 6       /* PrecisionRangeError (precision.py:25, :45-50) */
+};
+
+/* storage / arithmetic formats (precision.py:12-19, plus bf16) */
+enum sqb_dtype { SQB_F64 = 0, SQB_F32 = 1, SQB_F16 = 2, SQB_BF16 = 3 };
+
+/* reflector scaling (linalg.py:25-32) */
+enum sqb_scaling { SQB_SCALE_SQRT2 = 0, SQB_SCALE_UNIT = 1 };
+
+/* sketch operator kinds */
+enum sqb_sketch_kind {
+  SQB_SKETCH_SRHT = 0,     /* SRHTSketch     sketching.py:128-155 */
+  SQB_SKETCH_DENSE = 1,    /* GaussianSketch sketching.py:82-125 (and MatrixSketch :198-213) */
+  SQB_SKETCH_IDENTITY = 2  /* IdentitySketch sketching.py:186-195 */
+};
+
+/*
+ * A sketch operator Omega (ell x n) as device data.  Built by the caller
+ * (the facade builds it from the same numpy RNG calls the reference makes,
+ * sketching.py:100-107, :144-147, so signs, indices and G are bit-exact).
+ */
+typedef struct sqb_sketch {
+  int32_t kind;               /* sqb_sketch_kind */
+  int32_t reserved;
+  int64_t ell;                /* rows of Omega */
+  int64_t n;                  /* columns of Omega (input length) */
+  /* SRHT */
+  int64_t n_pad;              /* 1 << bit_length(n-1) (sketching.py:141) */
+  double scale;               /* float(sqrt(n_pad/ell)) (sketching.py:147), fp64 */
+  const uint32_t* sign_bits;  /* device, n_pad bits, bit e set <=> signs[e] == -1 */
+  const int64_t* indices;     /* device, ell sampled rows, ORDERED (sketching.py:146) */
+  /* DENSE */
+  const double* G;            /* device, ell x n ROW-major (G[i*ldg + r]) */
+  int64_t ldg;
+} sqb_sketch;
+
+typedef struct sqb_ctx sqb_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+int sqb_version(void);
+int sqb_ctx_create(int device, void* stream, sqb_ctx** out);
+int sqb_ctx_destroy(sqb_ctx* ctx);
+int sqb_ctx_set_stream(sqb_ctx* ctx, void* stream);
+/* message of the last host-side error of this context ("" if none) */
+const char* sqb_ctx_last_error(sqb_ctx* ctx);
+/* synchronise the stream, return the device status word and reset it */
+int sqb_ctx_status(sqb_ctx* ctx, int* code, int* col, double* val);
+/* Round a double to `dtype` the way the reference's numpy path does
+ * (`dtype.type(x)`; bf16 through fp32 as ml_dtypes does).  Host helper. */
+double sqb_round_scalar(int dtype, double x);
+/* Kernel launches issued by this context since creation (instrumentation). */
+int64_t sqb_ctx_launches(sqb_ctx* ctx);
+/* Time every launch of the dominant kernel (rhqr_col_kernel) with CUDA events
+ * on the context stream; read back the summed device time and algorithmic
+ * bytes (used by bench.py for the roofline).  enable=0 turns it off. */
+int sqb_ctx_profile(sqb_ctx* ctx, int enable);
+int sqb_ctx_profile_read(sqb_ctx* ctx, double* total_ms, double* total_bytes, int64_t* launches);
+
+/* ---- sketches ------------------------------------------------------------
+ * Y (ell x k, fp64, ldy) = Omega X, X (n x k, `dtype`, ldx), arithmetic in
+ * `dtype` (replaces SketchOperator.apply, sketching.py:72-76; SRHT _apply
+ * :149-155 + fwht :21-43 bit-exact; Gaussian _apply :109-125).           */
+int sqb_sketch_apply(sqb_ctx* ctx, const sqb_sketch* sk, int dtype,
+                     const void* X, int64_t ldx, int64_t k,
+                     double* Y, int64_t ldy);
+
+/* Psi X = [X[:m]; Omega X[m:]] (EmbeddedSketch.apply, sketching.py:255-260);
+ * X is (m+n) x k, Y is (m+ell) x k. */
+int sqb_embedded_apply(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, int dtype,
+                       const void* X, int64_t ldx, int64_t k,
+                       double* Y, int64_t ldy);
+
+/* ---- factorizations ------------------------------------------------------
+ * Left-looking RHQR (rhqr_left, rhqr.py:254-267; sweep :219-251).
+ * W: N x m in `lo_dtype` (already rounded to it, rhqr.py:264); outputs U
+ * (N x m, lo_dtype), S ((m+ell) x m), T (m x m), R (m x m), sigmas, rhos,
+ * betas (m), all zero-initialised by the call.  High precision is fp64.
+ * Breakdown -> device status SQB_ERR_BREAKDOWN with the 1-based column.   */
+int sqb_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                  const void* W, int64_t N, int64_t m, int64_t ldw,
+                  void* U, int64_t ldu, double* S, int64_t lds,
+                  double* T, int64_t ldt, double* R, int64_t ldr,
+                  double* sigmas, double* rhos, double* betas);
+
+/* (I - U T S^t Psi) X, or with transpose_t the reflectors in reverse
+ * (apply_reflectors_compact, rhqr.py:100-119).  U: N x r (lo), S: (m+ell) x r,
+ * T: r x r, X/Out: N x k (lo).  Out may alias X. */
+int sqb_apply_reflectors(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, int lo_dtype,
+                         const void* U, int64_t ldu, int64_t N, int64_t r,
+                         const double* S, int64_t lds, const double* T, int64_t ldt,
+                         int transpose_t, const void* X, int64_t ldx, int64_t k,
+                         void* Out, int64_t ldo);
+
+/* thin Q = [I;0] - U (T U1^t) in fp64 (thin_q, rhqr.py:171-178).  U: N x k. */
+int sqb_thin_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N,
+               int64_t k, const double* T, int64_t ldt, double* Q, int64_t ldq);
+
+/* Gram matrix G = A^t A (k x k, fp64) of a fp64 N x k matrix (diagnostics
+ * orthogonality_error/cond_number, linalg.py:151-160, :193-197). */
+int sqb_gram(sqb_ctx* ctx, const double* A, int64_t lda, int64_t N, int64_t k,
+             double* G, int64_t ldgm);
+
+/* Psi Q = [I;0] - S (T U1^t) without touching n-dimensional data
+ * (sketch_q, rhqr.py:181-188).  S: od x k, U: top k rows used. */
+int sqb_sketch_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t k,
+                 const double* T, int64_t ldt, const double* S, int64_t lds, int64_t od,
+                 double* Q, int64_t ldq);
+
+/* out[j] = ||(W - Q R)[:, j]||^2, out[kc + j] = ||W[:, j]||^2 (fp64; the
+ * sums behind factorization_errors, linalg.py:169-190).  W: N x kc,
+ * Q: N x k, R: k x kc. */
+int sqb_residual_norms(sqb_ctx* ctx, const double* W, int64_t ldw, const double* Q, int64_t ldq,
+                       const double* R, int64_t ldr, int64_t N, int64_t k, int64_t kc,
+                       double* out);
+
+/* One randomized Householder reflector from w (n, lo_dtype) and its sketch
+ * y = Psi w (od, fp64) eliminating entries j+1.. (1-based j; rh_vector,
+ * rhqr.py:51-97): writes u (n, lo_dtype), s = Psi u (od, fp64) and
+ * scalars[0..4] = sigma, rho, beta, f, gamma.  Breakdown (rho == 0 or
+ * non-finite beta) goes to the device status word. */
+int sqb_rh_vector(sqb_ctx* ctx, int scaling, int lo_dtype, const void* w, int64_t n,
+                  const double* y, int64_t od, int64_t j, void* u, double* s,
+                  double* scalars);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKETCHQR_B200_H */

@@ -1,0 +1,298 @@
+// Compact-form application and Q materialisation (rhqr.py:100-119, 171-188),
+// Gram matrices for the diagnostics (linalg.py:151-160, 193-197).
+#include <algorithm>
+
+#include "sketch.cuh"
+#include "vec.cuh"
+
+namespace sqb {
+
+// C[:, col] = op(T) (S^t Y[:, col]) ; one CTA per column of Y
+__global__ void __launch_bounds__(256)
+coef_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict__ Tm, int64_t ldt,
+            int transpose_t, const double* __restrict__ Y, int64_t ldy, int od, int r,
+            double* __restrict__ C, int64_t ldc, const Status* st) {
+  extern __shared__ double g[];  // [r]
+  if (st && failed(st)) return;
+  const int col = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* y = Y + (int64_t)col * ldy;
+  for (int k = warp; k < r; k += 8) {
+    const double* sk = S + (int64_t)k * lds;
+    double d = 0.0;
+    for (int i = lane; i < od; i += 32) d = fma(sk[i], y[i], d);
+    d = warp_sum(d);
+    if (lane == 0) g[k] = d;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < r; i += 256) {
+    double d = 0.0;
+    if (transpose_t) {
+      for (int k = 0; k <= i; ++k) d = fma(Tm[k + (int64_t)i * ldt], g[k], d);  // (T^t g)[i]
+    } else {
+      for (int k = i; k < r; ++k) d = fma(Tm[i + (int64_t)k * ldt], g[k], d);  // (T g)[i]
+    }
+    C[i + (int64_t)col * ldc] = d;
+  }
+}
+
+// Out[:, col] = fl(X[:, col] - fl(U C_lo[:, col]))  (rhqr.py:118)
+template <typename T>
+__global__ void __launch_bounds__(256)
+update_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int r, const double* __restrict__ C,
+              int64_t ldc, const T* __restrict__ X, int64_t ldx, T* __restrict__ Out, int64_t ldo,
+              const Status* st) {
+  using A = typename Lo<T>::acc;
+  extern __shared__ unsigned char smraw[];
+  A* c = reinterpret_cast<A*>(smraw);
+  if (st && failed(st)) return;
+  const int col = blockIdx.y;
+  for (int k = threadIdx.x; k < r; k += blockDim.x) c[k] = Lo<T>::from_double(C[k + (int64_t)col * ldc]);
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    A d = 0;
+    for (int k = 0; k < r; ++k) d = fma(Lo<T>::load(U[i + (int64_t)k * ldu]), c[k], d);
+    Out[i + (int64_t)col * ldo] = Lo<T>::store(Lo<T>::sub(Lo<T>::load(X[i + (int64_t)col * ldx]), Lo<T>::rnd(d)));
+  }
+}
+
+template <typename T>
+static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, const void* U,
+                              int64_t ldu, int64_t N, int64_t r, const double* S, int64_t lds,
+                              const double* Tm, int64_t ldt, int transpose_t, const void* X,
+                              int64_t ldx, int64_t k, void* Out, int64_t ldo) {
+  const int64_t od = m + sk->ell;
+  WsPlan plan;
+  const size_t iY = plan.add(sizeof(double) * od * k);
+  const size_t iC = plan.add(sizeof(double) * std::max<int64_t>(r, 1) * k);
+  const size_t iP = plan.add(sketch_partials_bytes(sk, Lo<T>::code, k));
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  double* Y = ws_ptr<double>(ctx, plan, iY);
+  double* C = ws_ptr<double>(ctx, plan, iC);
+  const Status* st = ctx->d_status;
+  if (r == 0) {  // no reflectors: Out = X
+    if (Out != X)
+      SQB_CUDA_TRY(cudaMemcpy2DAsync(Out, ldo * sizeof(T), X, ldx * sizeof(T), N * sizeof(T), k,
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+    return SQB_OK;
+  }
+  SQB_TRY(launch_copy_top(ctx, Lo<T>::code, X, ldx, m, k, Y, od, st));
+  SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const T*)X + m, ldx, k, Y, od, m,
+                        ws_ptr<void>(ctx, plan, iP), st));
+  coef_kernel<<<(unsigned)k, 256, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od,
+                                                                     (int)od, (int)r, C, r, st);
+  SQB_TRY(check_launch(ctx, "coef_kernel"));
+  dim3 grid((unsigned)std::min<int64_t>((N + 255) / 256, 4 * 148), (unsigned)k);
+  update_kernel<T><<<grid, 256, sizeof(typename Lo<T>::acc) * r, ctx->stream>>>(
+      (const T*)U, ldu, N, (int)r, C, r, (const T*)X, ldx, (T*)Out, ldo, st);
+  return check_launch(ctx, "update_kernel");
+}
+
+int apply_reflectors_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, int lo_dtype,
+                              const void* U, int64_t ldu, int64_t N, int64_t r, const double* S,
+                              int64_t lds, const double* Tm, int64_t ldt, int transpose_t,
+                              const void* X, int64_t ldx, int64_t k, void* Out, int64_t ldo) {
+  switch (lo_dtype) {
+    case SQB_F64: return apply_reflectors_t<double>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo);
+    case SQB_F32: return apply_reflectors_t<float>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo);
+    case SQB_F16: return apply_reflectors_t<__half>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo);
+    case SQB_BF16: return apply_reflectors_t<__nv_bfloat16>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo);
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
+// ---------------------------------------------------------------------------
+// thin Q = [I;0] - U (T U1^t), fp64 (rhqr.py:171-178)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void tu1t_kernel(const T* __restrict__ U, int64_t ldu, int k, const double* __restrict__ Tm,
+                            int64_t ldt, double* __restrict__ M) {
+  // M[i, j] = sum_l T[i, l] U[j, l]   (T upper: l >= i)
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+    const int i = e % k, j = e / k;
+    double d = 0.0;
+    for (int l = i; l < k; ++l) d = fma(Tm[i + (int64_t)l * ldt], (double)Lo<T>::load(U[j + (int64_t)l * ldu]), d);
+    M[i + (int64_t)j * k] = d;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+thin_q_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int k, const double* __restrict__ M,
+              double* __restrict__ Q, int64_t ldq) {
+  extern __shared__ double sM[];  // k x k
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) sM[e] = M[e];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    double u[64];
+    for (int j0 = 0; j0 < k; j0 += 64) {
+      const int jn = min(64, k - j0);
+      for (int jj = 0; jj < jn; ++jj) u[jj] = 0.0;
+      for (int l = 0; l < k; ++l) {
+        const double ul = (double)Lo<T>::load(U[i + (int64_t)l * ldu]);
+        for (int jj = 0; jj < jn; ++jj) u[jj] = fma(ul, sM[l + (j0 + jj) * k], u[jj]);
+      }
+      for (int jj = 0; jj < jn; ++jj) {
+        const int j = j0 + jj;
+        Q[i + (int64_t)j * ldq] = (i == j ? 1.0 : 0.0) - u[jj];
+      }
+    }
+  }
+}
+
+template <typename T>
+static int thin_q_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int64_t k, const double* Tm,
+                    int64_t ldt, double* Q, int64_t ldq) {
+  WsPlan plan;
+  const size_t iM = plan.add(sizeof(double) * std::max<int64_t>(1, k * k));
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  double* M = ws_ptr<double>(ctx, plan, iM);
+  tu1t_kernel<T><<<(unsigned)std::max<int64_t>(1, (k * k + 255) / 256), 256, 0, ctx->stream>>>(
+      (const T*)U, ldu, (int)k, Tm, ldt, M);
+  SQB_TRY(check_launch(ctx, "tu1t_kernel"));
+  const size_t smem = sizeof(double) * k * k;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(thin_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  thin_q_kernel<T><<<(unsigned)std::min<int64_t>((N + 255) / 256, 2 * 148), 256, smem, ctx->stream>>>(
+      (const T*)U, ldu, N, (int)k, M, Q, ldq);
+  return check_launch(ctx, "thin_q_kernel");
+}
+
+int thin_q_dispatch(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t k,
+                    const double* Tm, int64_t ldt, double* Q, int64_t ldq) {
+  switch (lo_dtype) {
+    case SQB_F64: return thin_q_t<double>(ctx, U, ldu, N, k, Tm, ldt, Q, ldq);
+    case SQB_F32: return thin_q_t<float>(ctx, U, ldu, N, k, Tm, ldt, Q, ldq);
+    case SQB_F16: return thin_q_t<__half>(ctx, U, ldu, N, k, Tm, ldt, Q, ldq);
+    case SQB_BF16: return thin_q_t<__nv_bfloat16>(ctx, U, ldu, N, k, Tm, ldt, Q, ldq);
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
+// ---------------------------------------------------------------------------
+// Gram G = A^t A (k x k) of fp64 A (N x k): split over row blocks, fixed-order sum
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+gram_partial_kernel(const double* __restrict__ A, int64_t lda, int64_t N, int k, int64_t rows_per,
+                    double* __restrict__ P) {
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per;
+  const int64_t r1 = min(N, r0 + rows_per);
+  const int kk = k * k;
+  for (int e = threadIdx.x; e < kk; e += blockDim.x) {
+    const int i = e % k, j = e / k;
+    if (i > j) continue;
+    double d = 0.0;
+    for (int64_t r = r0; r < r1; ++r) d = fma(A[r + i * lda], A[r + j * lda], d);
+    P[(int64_t)blockIdx.x * kk + e] = d;
+  }
+}
+
+__global__ void gram_reduce_kernel(const double* __restrict__ P, int nb, int k, double* __restrict__ G,
+                                   int64_t ldg) {
+  const int kk = k * k;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kk; e += gridDim.x * blockDim.x) {
+    const int i = e % k, j = e / k;
+    const int src = i <= j ? e : (j + i * k);
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += P[(int64_t)b * kk + src];
+    G[i + (int64_t)j * ldg] = s;
+  }
+}
+
+int gram_run(sqb_ctx* ctx, const double* A, int64_t lda, int64_t N, int64_t k, double* G, int64_t ldg) {
+  if (k == 0) return SQB_OK;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 148, (N + 1023) / 1024));
+  const int64_t rows_per = (N + nb - 1) / nb;
+  WsPlan plan;
+  const size_t iP = plan.add(sizeof(double) * nb * k * k);
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  double* P = ws_ptr<double>(ctx, plan, iP);
+  gram_partial_kernel<<<nb, 256, 0, ctx->stream>>>(A, lda, N, (int)k, rows_per, P);
+  SQB_TRY(check_launch(ctx, "gram_partial_kernel"));
+  gram_reduce_kernel<<<(unsigned)std::max<int64_t>(1, (k * k + 255) / 256), 256, 0, ctx->stream>>>(P, nb, (int)k, G, ldg);
+  return check_launch(ctx, "gram_reduce_kernel");
+}
+
+}  // namespace sqb
+
+namespace sqb {
+
+// per-column sums of (W - Q R)^2 and W^2 (factorization_errors, linalg.py:169-190)
+__global__ void __launch_bounds__(256)
+residual_partial_kernel(const double* __restrict__ W, int64_t ldw, const double* __restrict__ Q,
+                        int64_t ldq, const double* __restrict__ R, int64_t ldr, int64_t N, int k,
+                        double* __restrict__ P, int nb) {
+  __shared__ double red[32];
+  const int j = blockIdx.y;
+  double sd = 0.0, sw = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    double q = 0.0;
+    for (int l = 0; l < k; ++l) q = fma(Q[i + l * ldq], R[l + (int64_t)j * ldr], q);
+    const double w = W[i + (int64_t)j * ldw];
+    const double d = w - q;
+    sd = fma(d, d, sd);
+    sw = fma(w, w, sw);
+  }
+  sd = block_sum(sd, red);
+  sw = block_sum(sw, red);
+  if (threadIdx.x == 0) {
+    P[(int64_t)j * nb + blockIdx.x] = sd;
+    P[(int64_t)(gridDim.y + j) * nb + blockIdx.x] = sw;
+  }
+}
+
+__global__ void rowsum_kernel(const double* __restrict__ P, int rows, int nb, double* __restrict__ out) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += P[(int64_t)r * nb + b];
+    out[r] = s;
+  }
+}
+
+int residual_norms_run(sqb_ctx* ctx, const double* W, int64_t ldw, const double* Q, int64_t ldq,
+                       const double* R, int64_t ldr, int64_t N, int64_t k, int64_t kc, double* out) {
+  if (kc == 0) return SQB_OK;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(2 * 148, (N + 255) / 256));
+  WsPlan plan;
+  const size_t iP = plan.add(sizeof(double) * 2 * kc * nb);
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  double* P = ws_ptr<double>(ctx, plan, iP);
+  residual_partial_kernel<<<dim3(nb, (unsigned)kc), 256, 0, ctx->stream>>>(W, ldw, Q, ldq, R, ldr, N, (int)k, P, nb);
+  SQB_TRY(check_launch(ctx, "residual_partial_kernel"));
+  rowsum_kernel<<<(unsigned)((2 * kc + 255) / 256), 256, 0, ctx->stream>>>(P, (int)(2 * kc), nb, out);
+  return check_launch(ctx, "rowsum_kernel");
+}
+
+}  // namespace sqb
+
+namespace sqb {
+
+template <typename T>
+static int sketch_q_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t k, const double* Tm, int64_t ldt,
+                      const double* S, int64_t lds, int64_t od, double* Q, int64_t ldq) {
+  WsPlan plan;
+  const size_t iM = plan.add(sizeof(double) * std::max<int64_t>(1, k * k));
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  double* M = ws_ptr<double>(ctx, plan, iM);
+  tu1t_kernel<T><<<(unsigned)std::max<int64_t>(1, (k * k + 255) / 256), 256, 0, ctx->stream>>>(
+      (const T*)U, ldu, (int)k, Tm, ldt, M);
+  SQB_TRY(check_launch(ctx, "tu1t_kernel"));
+  const size_t smem = sizeof(double) * k * k;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(thin_q_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  thin_q_kernel<double><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((od + 255) / 256, 148)), 256,
+                          smem, ctx->stream>>>(S, lds, od, (int)k, M, Q, ldq);
+  return check_launch(ctx, "thin_q_kernel");
+}
+
+int sketch_q_run(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t k, const double* Tm,
+                 int64_t ldt, const double* S, int64_t lds, int64_t od, double* Q, int64_t ldq) {
+  switch (lo_dtype) {
+    case SQB_F64: return sketch_q_t<double>(ctx, U, ldu, k, Tm, ldt, S, lds, od, Q, ldq);
+    case SQB_F32: return sketch_q_t<float>(ctx, U, ldu, k, Tm, ldt, S, lds, od, Q, ldq);
+    case SQB_F16: return sketch_q_t<__half>(ctx, U, ldu, k, Tm, ldt, S, lds, od, Q, ldq);
+    case SQB_BF16: return sketch_q_t<__nv_bfloat16>(ctx, U, ldu, k, Tm, ldt, S, lds, od, Q, ldq);
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
+}  // namespace sqb

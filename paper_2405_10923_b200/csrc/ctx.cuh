@@ -1,0 +1,113 @@
+// Context handle + workspace (host side).
+#pragma once
+
+#include <cstdio>
+#include <cstring>
+#include <cstdarg>
+#include <vector>
+
+#include "common.cuh"
+
+struct sqb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  char err[512] = {0};
+  void* ws = nullptr;          // grow-only scratch (partials, sketches, coefficients)
+  size_t ws_bytes = 0;
+  sqb::Status* d_status = nullptr;
+  sqb::Status* h_status = nullptr;  // pinned mirror
+  int64_t launches = 0;        // kernel launches issued (instrumentation for bench)
+  int sm_count = 148;
+  // per-launch CUDA-event timing of the dominant kernel (rhqr_col_kernel), on
+  // the stream it is launched on; enabled by sqb_ctx_profile()
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;   // pairs (begin, end)
+  std::vector<double> prof_bytes;     // algorithmic bytes of each timed launch
+  size_t prof_used = 0;
+};
+
+namespace sqb {
+
+inline int set_error(sqb_ctx* ctx, int code, const char* fmt, ...) {
+  if (ctx) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(ctx->err, sizeof(ctx->err), fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+inline int set_cuda_error(sqb_ctx* ctx, cudaError_t e, const char* what, const char* file, int line) {
+  return set_error(ctx, SQB_ERR_CUDA, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+                   cudaGetErrorString(e), file, line, what);
+}
+
+// Bump allocator over the context workspace.  All requests of one call are
+// made up front (plan), then the workspace grows once if needed.
+struct WsPlan {
+  std::vector<size_t> offs;
+  size_t total = 0;
+  size_t add(size_t bytes) {
+    size_t o = (total + 255) & ~size_t(255);
+    offs.push_back(o);
+    total = o + bytes;
+    return offs.size() - 1;
+  }
+};
+
+inline int ws_reserve(sqb_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->ws_bytes) return SQB_OK;
+  SQB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (ctx->ws) SQB_CUDA_TRY(cudaFree(ctx->ws));
+  ctx->ws = nullptr;
+  ctx->ws_bytes = 0;
+  size_t want = bytes + (bytes >> 3);
+  SQB_CUDA_TRY(cudaMalloc(&ctx->ws, want));
+  ctx->ws_bytes = want;
+  return SQB_OK;
+}
+
+template <typename P>
+inline P* ws_ptr(sqb_ctx* ctx, const WsPlan& plan, size_t id) {
+  return reinterpret_cast<P*>(static_cast<char*>(ctx->ws) + plan.offs[id]);
+}
+
+// bracket one launch of the profiled kernel with events (no-op when off)
+inline void prof_begin(sqb_ctx* ctx) {
+  if (!ctx->prof) return;
+  if (ctx->prof_used + 2 > ctx->prof_ev.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ctx->prof_ev.push_back(e);
+    }
+  }
+  cudaEventRecord(ctx->prof_ev[ctx->prof_used], ctx->stream);
+}
+inline void prof_end(sqb_ctx* ctx, double alg_bytes) {
+  if (!ctx->prof) return;
+  cudaEventRecord(ctx->prof_ev[ctx->prof_used + 1], ctx->stream);
+  ctx->prof_used += 2;
+  ctx->prof_bytes.push_back(alg_bytes);
+}
+
+inline int check_launch(sqb_ctx* ctx, const char* what) {
+  ctx->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(ctx, e, what, __FILE__, __LINE__);
+  return SQB_OK;
+}
+
+// host-side rounding of a double to a storage format, matching numpy:
+// float32/float16 round directly from double; ml_dtypes' bfloat16 goes
+// through float32 (two round-to-nearest-even steps).
+double round_scalar(int dtype, double x);
+
+}  // namespace sqb
+
+#define SQB_TRY(expr)              \
+  do {                             \
+    int r__ = (expr);              \
+    if (r__ != SQB_OK) return r__; \
+  } while (0)

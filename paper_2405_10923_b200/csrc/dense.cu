@@ -1,0 +1,222 @@
+// K2 — dense sketch Y = G X on the FP64 tensor pipe (DMMA, mma.sync m16n8k4 f64).
+//
+// Reference: GaussianSketch._apply (sketching.py:109-125): Y = G @ X with G the
+// (ell x n) N(0, 1/ell) matrix (row i from Philox(key=[seed, i]), :100-107;
+// generated on the host with the same numpy calls and uploaded once).  For
+// BASELINE config 3 the shape is 256 x 4,194,240 times 4,194,240 x 64: a
+// split-K GEMM with a huge K.  Both operands are K-contiguous (G row-major,
+// X column-major), so tiles stream straight into shared memory with cp.async
+// and feed DMMA fragments; the split-K partials are summed in slab order by a
+// second kernel (deterministic).
+//
+// Arithmetic type follows the reference: fp64 -> DMMA; fp32 / fp16 (fp32
+// accumulation, sketching.py:111) / bf16 (ml_dtypes matmul, fp32
+// accumulation) use a CUDA-core kernel — they are off the BASELINE configs.
+#include <algorithm>
+
+#include "dense.cuh"
+#include "sketch.cuh"
+
+namespace sqb {
+
+constexpr int DBM = 128, DBN = 64, DBK = 32, DSTR = DBK + 4, DSTAGES = 3, DNT = 256;
+constexpr size_t DSMEM = sizeof(double) * DSTAGES * (size_t)(DBM + DBN) * DSTR;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// one CTA: a 128 x 64 tile of the partial product over K-range [k0, k1)
+__global__ void __launch_bounds__(DNT, 1)
+dense_dmma_kernel(const double* __restrict__ G, int64_t ldg, const double* __restrict__ X,
+                  int64_t ldx, int64_t M, int64_t N, int64_t K, int64_t kslab,
+                  double* __restrict__ P, const Status* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sG = reinterpret_cast<double*>(smem_raw);
+  double* sX = sG + DSTAGES * DBM * DSTR;
+  if (st && failed(st)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t m0 = (int64_t)blockIdx.x * DBM, n0 = (int64_t)blockIdx.y * DBN;
+  const int64_t k0 = (int64_t)blockIdx.z * kslab;
+  const int64_t k1 = std::min<int64_t>(K, k0 + kslab);
+  const int nk = (int)((k1 - k0 + DBK - 1) / DBK);
+
+  auto load_stage = [&](int s, int kt) {
+    const int64_t kb = k0 + (int64_t)kt * DBK;
+    double* g = sG + s * DBM * DSTR;
+    double* x = sX + s * DBN * DSTR;
+    for (int e = tid; e < DBM * DBK; e += DNT) {
+      const int r = e / DBK, kk = e % DBK;
+      const int64_t gr = m0 + r, gk = kb + kk;
+      double* d = g + r * DSTR + kk;
+      if (gr < M && gk < k1) cp_async8(d, G + gr * ldg + gk);
+      else *d = 0.0;
+    }
+    for (int e = tid; e < DBN * DBK; e += DNT) {
+      const int cidx = e / DBK, kk = e % DBK;
+      const int64_t gc = n0 + cidx, gk = kb + kk;
+      double* d = x + cidx * DSTR + kk;
+      if (gc < N && gk < k1) cp_async8(d, X + gc * ldx + gk);
+      else *d = 0.0;
+    }
+  };
+
+  double acc[2][4][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+
+  const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps of 32 x 32
+  const int g = lane >> 2, t = lane & 3;
+
+#pragma unroll
+  for (int s = 0; s < DSTAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<DSTAGES - 2>();
+    __syncthreads();
+    const int nxt = kt + DSTAGES - 1;
+    if (nxt < nk) load_stage(nxt % DSTAGES, nxt);
+    cp_async_commit();
+    const double* gs = sG + (kt % DSTAGES) * DBM * DSTR + (wm * 32) * DSTR;
+    const double* xs = sX + (kt % DSTAGES) * DBN * DSTR + (wn * 32) * DSTR;
+#pragma unroll
+    for (int k4 = 0; k4 < DBK / 4; ++k4) {
+      double a0[2], a1[2], b0[4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        a0[mt] = gs[(mt * 16 + g) * DSTR + k4 * 4 + t];
+        a1[mt] = gs[(mt * 16 + g + 8) * DSTR + k4 * 4 + t];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) b0[nt] = xs[(nt * 8 + g) * DSTR + k4 * 4 + t];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(acc[mt][nt], a0[mt], a1[mt], b0[nt]);
+    }
+  }
+  cp_async_wait<0>();
+  // epilogue: partial tile -> P[slab] (M x N column-major)
+  double* p = P + (int64_t)blockIdx.z * M * N;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int64_t r = m0 + wm * 32 + mt * 16 + g + h * 8;
+          const int64_t c = n0 + wn * 32 + nt * 8 + 2 * t + q;
+          if (r < M && c < N) p[r + c * M] = acc[mt][nt][h * 2 + q];
+        }
+}
+
+__global__ void dense_reduce_kernel(const double* __restrict__ P, int64_t M, int64_t N, int S,
+                                    double* __restrict__ Y, int64_t ldy, int64_t row_off,
+                                    const Status* st) {
+  if (st && failed(st)) return;
+  const int64_t MN = M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < MN; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < S; ++z) s += P[z * MN + e];
+    const int64_t r = e % M, c = e / M;
+    Y[row_off + r + c * ldy] = s;
+  }
+}
+
+// CUDA-core path for the reduced-precision dense sketches (fp32 accumulate)
+template <typename T>
+__device__ __forceinline__ float dense_g(double g);
+template <> __device__ __forceinline__ float dense_g<float>(double g) { return __double2float_rn(g); }
+template <> __device__ __forceinline__ float dense_g<__half>(double g) { return __double2float_rn(g); }
+template <> __device__ __forceinline__ float dense_g<__nv_bfloat16>(double g) {
+  return __bfloat162float(__float2bfloat16_rn(__double2float_rn(g)));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+dense_lowp_kernel(const double* __restrict__ G, int64_t ldg, const T* __restrict__ X, int64_t ldx,
+                  int64_t M, int64_t K, double* __restrict__ Y, int64_t ldy, int64_t row_off,
+                  const Status* st) {
+  __shared__ double red[32];
+  if (st && failed(st)) return;
+  const int64_t i = blockIdx.x, c = blockIdx.y;
+  float acc = 0.f;
+  for (int64_t r = threadIdx.x; r < K; r += blockDim.x)
+    acc = fmaf(dense_g<T>(G[i * ldg + r]), Lo<T>::load(X[r + c * ldx]), acc);
+  const double tot = block_sum((double)acc, red);
+  if (threadIdx.x == 0) Y[row_off + i + c * ldy] = (double)Lo<T>::rnd((float)tot);
+}
+
+static int dense_slabs(int64_t M, int64_t N, int64_t K, int sms, int64_t* kslab) {
+  const int64_t tiles = ((M + DBM - 1) / DBM) * ((N + DBN - 1) / DBN);
+  int64_t want = std::max<int64_t>(1, (2 * (int64_t)sms + tiles - 1) / tiles);
+  int64_t ks = (K + want - 1) / want;
+  ks = std::max<int64_t>(DBK, ((ks + DBK - 1) / DBK) * DBK);
+  *kslab = ks;
+  return (int)((K + ks - 1) / ks);
+}
+
+size_t dense_ws_bytes(const sqb_sketch* sk, int dtype, int64_t k) {
+  if (dtype != SQB_F64) return 0;
+  int64_t ks;
+  const int S = dense_slabs(sk->ell, k, sk->n, 148, &ks);
+  return sizeof(double) * (size_t)S * (size_t)sk->ell * (size_t)k;
+}
+
+template <>
+int launch_dense<double>(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int64_t ldx, int64_t k,
+                         double* Y, int64_t ldy, int64_t row_off, void* ws, const Status* st) {
+  int64_t ks;
+  const int S = dense_slabs(sk->ell, k, sk->n, 148, &ks);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dense_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DSMEM);
+    attr = true;
+  }
+  dim3 grid((unsigned)((sk->ell + DBM - 1) / DBM), (unsigned)((k + DBN - 1) / DBN), (unsigned)S);
+  dense_dmma_kernel<<<grid, DNT, DSMEM, ctx->stream>>>(sk->G, sk->ldg, (const double*)X, ldx, sk->ell,
+                                                        k, sk->n, ks, (double*)ws, st);
+  SQB_TRY(check_launch(ctx, "dense_dmma_kernel"));
+  const int64_t MN = sk->ell * k;
+  const unsigned rb = (unsigned)std::min<int64_t>((MN + 255) / 256, 4096);
+  dense_reduce_kernel<<<rb, 256, 0, ctx->stream>>>((const double*)ws, sk->ell, k, S, Y, ldy, row_off, st);
+  return check_launch(ctx, "dense_reduce_kernel");
+}
+
+template <typename T>
+int launch_dense(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int64_t ldx, int64_t k,
+                 double* Y, int64_t ldy, int64_t row_off, void*, const Status* st) {
+  dim3 grid((unsigned)sk->ell, (unsigned)k);
+  dense_lowp_kernel<T><<<grid, 256, 0, ctx->stream>>>(sk->G, sk->ldg, (const T*)X, ldx, sk->ell,
+                                                      sk->n, Y, ldy, row_off, st);
+  return check_launch(ctx, "dense_lowp_kernel");
+}
+
+template int launch_dense<float>(sqb_ctx*, const sqb_sketch*, const void*, int64_t, int64_t, double*,
+                                 int64_t, int64_t, void*, const Status*);
+template int launch_dense<__half>(sqb_ctx*, const sqb_sketch*, const void*, int64_t, int64_t, double*,
+                                  int64_t, int64_t, void*, const Status*);
+template int launch_dense<__nv_bfloat16>(sqb_ctx*, const sqb_sketch*, const void*, int64_t, int64_t,
+                                         double*, int64_t, int64_t, void*, const Status*);
+
+}  // namespace sqb

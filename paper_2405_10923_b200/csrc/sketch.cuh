@@ -1,0 +1,57 @@
+// Host-side launchers for the sketch operators (shared by the factorizations).
+#pragma once
+
+#include "ctx.cuh"
+#include "srht.cuh"
+
+namespace sqb {
+
+struct SrhtGeom {
+  int log_tb;       // tile = 2^log_tb Omega coordinates (min(TileCfg::LOG_TB, log2 n_pad))
+  int64_t n_tiles;  // n_pad >> log_tb
+  int64_t n_eff;    // tiles that hold at least one real (non-padding) coordinate
+};
+
+inline int ilog2_exact(int64_t v) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return l;
+}
+
+template <typename T>
+inline SrhtGeom srht_geom_t(const sqb_sketch* sk) {
+  SrhtGeom g;
+  const int lp = ilog2_exact(sk->n_pad);
+  g.log_tb = lp < TileCfg<T>::LOG_TB ? lp : TileCfg<T>::LOG_TB;
+  g.n_tiles = sk->n_pad >> g.log_tb;
+  const int64_t tb = int64_t(1) << g.log_tb;
+  g.n_eff = (sk->n + tb - 1) / tb;
+  return g;
+}
+
+SrhtGeom srht_geom(const sqb_sketch* sk, int dtype);
+size_t acc_bytes(int dtype);   // sizeof(Lo<T>::acc)
+size_t elem_bytes(int dtype);  // sizeof(T)
+
+int validate_sketch(sqb_ctx* ctx, const sqb_sketch* sk);
+
+// Y[y_row_off + i + col*ldy] = (Omega X)[i, col], i < ell, col < k.
+// `partials` must hold sketch_partials_bytes(sk, dtype, k) bytes (SRHT only).
+size_t sketch_partials_bytes(const sqb_sketch* sk, int dtype, int64_t k);
+int launch_sketch(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* X, int64_t ldx,
+                  int64_t k, double* Y, int64_t ldy, int64_t y_row_off, void* partials,
+                  const Status* st);
+
+// SRHT pieces used by fused kernels: tree over per-tile leaves P[(col*ell + kk)*n_tiles + t]
+int launch_srht_tree(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* P, int64_t k,
+                     double* Y, int64_t ldy, int64_t y_row_off, const Status* st);
+
+// Y[0:m, col] = X[0:m, col] as fp64 (identity block of Psi, sketching.py:257)
+int launch_copy_top(sqb_ctx* ctx, int dtype, const void* X, int64_t ldx, int64_t m, int64_t k,
+                    double* Y, int64_t ldy, const Status* st);
+
+// host rounding of the SRHT constants to the arithmetic dtype:
+// c = dtype(scale) (sketching.py:150) and dtype(n_pad^-1/2) (sketching.py:42)
+void srht_constants(const sqb_sketch* sk, int dtype, double* scale_lo, double* norm_lo);
+
+}  // namespace sqb

@@ -1,0 +1,149 @@
+// K1 — subsampled randomized Hadamard transform, bit-exact with the reference.
+//
+// Reference: SRHTSketch._apply (sketching.py:149-155) + fwht (:21-43):
+//   work = fl(x * dtype(scale)); work *= signs; pad with zeros to n_pad;
+//   butterfly stages h = 1, 2, 4, ... n_pad/2 with (a+b, a-b) on (i, i+h);
+//   multiply by dtype(n_pad^-1/2); gather rows `indices` in order.
+//
+// B200 decomposition (CPU replay in tests/test_tile_tree_design.py):
+//   * the padded vector is cut into tiles of TB = 2^t consecutive Omega
+//     coordinates; one CTA streams one tile (coalesced 128-bit loads) into
+//     shared memory and runs the stages h = 1..TB/2 IN ORDER as radix-8
+//     register passes (3 stages per pass, one smem round trip per pass);
+//   * from each tile only the ell sampled rows r_lo = idx mod TB are kept
+//     (a "leaf" per output);
+//   * the remaining log2(n_pad/TB) stages only ever touch the sampled rows:
+//     output k is the binary tree over tiles, level l combining adjacent
+//     subtrees as (left + right) or (left - right) by bit l of
+//     r_hi = idx div TB, left = lower tile.  Tiles wholly inside the zero
+//     padding contribute exact +0 leaves.
+//   Every add/sub/mul is an explicit round-to-nearest intrinsic (no FMA
+//   contraction), so the result is bitwise identical to the reference.
+#pragma once
+
+#include "common.cuh"
+
+namespace sqb {
+
+constexpr int SRHT_NT = 256;  // threads per tile CTA
+
+template <typename T> struct TileCfg;
+template <> struct TileCfg<double> { static constexpr int LOG_TB = 12; };  // 32 KB smem
+template <> struct TileCfg<float> { static constexpr int LOG_TB = 13; };
+template <> struct TileCfg<__nv_bfloat16> { static constexpr int LOG_TB = 13; };
+template <> struct TileCfg<__half> { static constexpr int LOG_TB = 13; };
+
+// shared-memory padding: one spare slot every 16 doubles / 8 floats keeps the
+// radix-8 passes at the minimum number of wavefronts
+template <typename A> struct Pad;
+template <> struct Pad<double> { static constexpr int shift = 4; };
+template <> struct Pad<float> { static constexpr int shift = 3; };
+
+template <typename A>
+__device__ __forceinline__ int pidx(int e) { return e + (e >> Pad<A>::shift); }
+
+template <typename A>
+__host__ __device__ constexpr size_t tile_smem_bytes(int tb) {
+  return sizeof(A) * (size_t)(tb + (tb >> Pad<A>::shift) + 1);
+}
+
+// one radix-2^R pass over bits [b, b+R) of the in-tile index; `len` = number
+// of transformed elements (the tile, or n_pad if that is smaller)
+template <typename T, int R>
+__device__ __forceinline__ void fwht_pass(typename Lo<T>::acc* sm, int b, int len) {
+  using A = typename Lo<T>::acc;
+  const int groups = len >> R;
+  const int lowmask = (1 << b) - 1;
+  for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+    const int base = (g & lowmask) | ((g >> b) << (b + R));
+    A v[1 << R];
+#pragma unroll
+    for (int j = 0; j < (1 << R); ++j) v[j] = sm[pidx<A>(base | (j << b))];
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+#pragma unroll
+      for (int j = 0; j < (1 << R); ++j) {
+        if (!(j & (1 << s))) {
+          const A x = v[j], y = v[j | (1 << s)];
+          v[j] = Lo<T>::add(x, y);
+          v[j | (1 << s)] = Lo<T>::sub(x, y);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < (1 << R); ++j) sm[pidx<A>(base | (j << b))] = v[j];
+  }
+}
+
+// full in-tile FWHT (stages h = 1 .. len/2 in order); caller has synced
+template <typename T>
+__device__ __forceinline__ void tile_fwht(typename Lo<T>::acc* sm, int log_len) {
+  const int len = 1 << log_len;
+  for (int b = 0; b < log_len; b += 3) {
+    const int r = log_len - b;
+    if (r >= 3) fwht_pass<T, 3>(sm, b, len);
+    else if (r == 2) fwht_pass<T, 2>(sm, b, len);
+    else fwht_pass<T, 1>(sm, b, len);
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ bool sign_neg(const uint32_t* bits, int64_t e) {
+  return (__ldg(bits + (e >> 5)) >> (e & 31)) & 1u;
+}
+
+// x -> fl(fl(x * scale) * sign)  (sketching.py:152-153)
+template <typename T>
+__device__ __forceinline__ typename Lo<T>::acc srht_in(typename Lo<T>::acc x,
+                                                      typename Lo<T>::acc scale, bool neg) {
+  const typename Lo<T>::acc v = Lo<T>::mul(x, scale);
+  return neg ? -v : v;
+}
+
+// gather the sampled rows of a transformed tile into leaves P[k * ldp]
+template <typename T>
+__device__ __forceinline__ void tile_gather(const typename Lo<T>::acc* sm, const int64_t* idx,
+                                            int ell, int log_tb, typename Lo<T>::acc* P,
+                                            int64_t ldp) {
+  using A = typename Lo<T>::acc;
+  const int64_t mask = (int64_t(1) << log_tb) - 1;
+  for (int k = threadIdx.x; k < ell; k += blockDim.x)
+    P[k * ldp] = sm[pidx<A>((int)(__ldg(idx + k) & mask))];
+}
+
+// Tree over tile leaves for output k, done by one warp.  leaves[t] for
+// t < n_eff, +0 for n_eff <= t < n_tiles (all-padding tiles).  Tile t is held
+// by lane (t & 31), slot (t >> 5): the low 5 tree levels are lane shuffles,
+// the upper levels a sequential binary-counter tree over slots — both in
+// level order, left operand = lower tile index.
+template <typename T>
+__device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<T>::acc* leaves,
+                                                              int n_tiles, int n_eff, int64_t rhi) {
+  using A = typename Lo<T>::acc;
+  const int lane = threadIdx.x & 31;
+  int low_levels = 0;
+  while ((1 << low_levels) < n_tiles && low_levels < 5) ++low_levels;
+  const int slots = n_tiles > 32 ? (n_tiles >> 5) : 1;
+  A stk[16];
+  for (int j = 0; j < slots; ++j) {
+    const int t = lane + (j << 5);
+    A v = (t < n_eff) ? leaves[t] : A(0);
+    for (int l = 0; l < low_levels; ++l) {
+      const A o = __shfl_xor_sync(0xffffffffu, v, 1 << l);
+      const bool upper = (lane >> l) & 1;
+      const A a = upper ? o : v, b = upper ? v : o;
+      v = ((rhi >> l) & 1) ? Lo<T>::sub(a, b) : Lo<T>::add(a, b);
+    }
+    int lvl = 0;
+    while ((j >> lvl) & 1) {
+      v = ((rhi >> (5 + lvl)) & 1) ? Lo<T>::sub(stk[lvl], v) : Lo<T>::add(stk[lvl], v);
+      ++lvl;
+    }
+    stk[lvl] = v;
+  }
+  int top = 0;
+  while ((1 << top) < slots) ++top;
+  return __shfl_sync(0xffffffffu, stk[top], 0);
+}
+
+}  // namespace sqb

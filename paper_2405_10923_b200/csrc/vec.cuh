@@ -1,0 +1,101 @@
+// 128-bit vector loads/stores of storage-type elements, widened to the
+// arithmetic type.
+#pragma once
+
+#include "common.cuh"
+
+namespace sqb {
+
+template <typename T> struct VecN { static constexpr int n = 16 / sizeof(T); };
+
+template <typename T>
+__device__ __forceinline__ void vload(const T* p, typename Lo<T>::acc* out);
+
+template <>
+__device__ __forceinline__ void vload<double>(const double* p, double* out) {
+  const double2 v = *reinterpret_cast<const double2*>(p);
+  out[0] = v.x;
+  out[1] = v.y;
+}
+template <>
+__device__ __forceinline__ void vload<float>(const float* p, float* out) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void vload<__nv_bfloat16>(const __nv_bfloat16* p, float* out) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    out[2 * i] = f.x;
+    out[2 * i + 1] = f.y;
+  }
+}
+template <>
+__device__ __forceinline__ void vload<__half>(const __half* p, float* out) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __half22float2(h[i]);
+    out[2 * i] = f.x;
+    out[2 * i + 1] = f.y;
+  }
+}
+
+// values are already representable in T (rounded by the caller)
+template <typename T>
+__device__ __forceinline__ void vstore(T* p, const typename Lo<T>::acc* in);
+
+template <>
+__device__ __forceinline__ void vstore<double>(double* p, const double* in) {
+  *reinterpret_cast<double2*>(p) = make_double2(in[0], in[1]);
+}
+template <>
+__device__ __forceinline__ void vstore<float>(float* p, const float* in) {
+  *reinterpret_cast<float4*>(p) = make_float4(in[0], in[1], in[2], in[3]);
+}
+template <>
+__device__ __forceinline__ void vstore<__nv_bfloat16>(__nv_bfloat16* p, const float* in) {
+  uint4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(in[2 * i], in[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = v;
+}
+template <>
+__device__ __forceinline__ void vstore<__half>(__half* p, const float* in) {
+  uint4 v;
+  __half2* h = reinterpret_cast<__half2*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(in[2 * i], in[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = v;
+}
+
+// load VN consecutive elements starting at e (relative to p), zero beyond n
+template <typename T, int VN>
+__device__ __forceinline__ void load_run(const T* p, int64_t e, int64_t n,
+                                         typename Lo<T>::acc* out) {
+  if (VN > 1 && e + VN <= n) {
+    vload<T>(p + e, out);
+  } else {
+#pragma unroll
+    for (int j = 0; j < VN; ++j) out[j] = (e + j < n) ? Lo<T>::load(p[e + j]) : typename Lo<T>::acc(0);
+  }
+}
+
+template <typename T, int VN>
+__device__ __forceinline__ void store_run(T* p, int64_t e, int64_t n,
+                                          const typename Lo<T>::acc* in) {
+  if (VN > 1 && e + VN <= n) {
+    vstore<T>(p + e, in);
+  } else {
+#pragma unroll
+    for (int j = 0; j < VN; ++j)
+      if (e + j < n) p[e + j] = Lo<T>::store(in[j]);
+  }
+}
+
+}  // namespace sqb

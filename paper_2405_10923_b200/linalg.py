@@ -1,0 +1,124 @@
+"""Exceptions, scaling modes and the stability diagnostics (mirror of linalg.py).
+
+Diagnostics run on the device: the Gram matrix A^t A by the library's
+`sqb_gram` kernel, its eigenvalues by cuSOLVER (torch.linalg.eigvalsh on the
+k x k Gram, device-side), the residual W - QR by the library's fused
+`sqb_residual_norms` kernel.  cond(Q) through the Gram is accurate for the
+well-conditioned Q this package produces (squaring a cond-5 matrix loses
+nothing); `cond_number(..., exact=True)` runs a device SVD instead.
+"""
+
+from __future__ import annotations
+
+from typing import NamedTuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from .devarray import empty_colmajor, is_device, ld_of, to_device
+
+SCALE_SQRT2 = "sqrt2"
+SCALE_UNIT = "unit"
+SCALINGS = (SCALE_SQRT2, SCALE_UNIT)
+
+
+class BreakdownError(RuntimeError):
+    """A factorization step cannot continue (linalg.py:18-19)."""
+
+
+class SingularFactorError(np.linalg.LinAlgError):
+    """Triangular solve hit a zero or subnormal diagonal entry (linalg.py:35-36)."""
+
+
+def check_scaling(scaling):
+    if scaling not in SCALINGS:
+        raise ValueError(f"unknown scaling {scaling!r}, expected one of {SCALINGS}")
+
+
+def scaling_code(scaling) -> int:
+    check_scaling(scaling)
+    return _lib.SQB_SCALE_SQRT2 if scaling == SCALE_SQRT2 else _lib.SQB_SCALE_UNIT
+
+
+def sign(v):
+    """linalg.py:200-202: sign(0) = +1."""
+    return 1.0 if v >= 0.0 else -1.0
+
+
+def as_array(M):
+    """numpy passthrough (device tensors are left as they are)."""
+    if isinstance(M, torch.Tensor):
+        return M
+    return np.asarray(M, dtype=np.float64)
+
+
+def _dev64(A) -> torch.Tensor:
+    return to_device(A, "double")
+
+
+def gram(A) -> torch.Tensor:
+    """A^t A (fp64, k x k) on the device."""
+    Ad = _dev64(A)
+    N, k = Ad.shape
+    G = empty_colmajor(k, k, "double")
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_gram(ctx.h, Ad.data_ptr(), ld_of(Ad), N, k, G.data_ptr(), ld_of(G)), "sqb_gram")
+    return G
+
+
+def cond_number(M, exact: bool = False):
+    """linalg.py:151-160: 2-norm condition number; +inf if sigma_min == 0."""
+    Ad = _dev64(M)
+    if not bool(torch.isfinite(Ad).all()):
+        return np.inf
+    if exact:
+        sv = torch.linalg.svdvals(Ad)
+        smax, smin = float(sv[0]), float(sv[-1])
+    else:
+        ev = torch.linalg.eigvalsh(gram(Ad))
+        smin = float(torch.sqrt(torch.clamp(ev[0], min=0.0)))
+        smax = float(torch.sqrt(ev[-1]))
+    if smin == 0.0:
+        return np.inf
+    return smax / smin
+
+
+def orthogonality_error(Q):
+    """linalg.py:193-197: ||Q^t Q - I||_F."""
+    G = gram(Q)
+    k = G.shape[0]
+    return float(torch.linalg.norm(G - torch.eye(k, dtype=G.dtype, device=G.device)))
+
+
+class FactorizationErrors(NamedTuple):
+    fro_rel_err: float
+    max_col_rel_err: float
+    flagged_columns: tuple
+
+
+def factorization_errors(W, Q, R):
+    """linalg.py:169-190: relative residuals of W ~ Q R (Frobenius, per column)."""
+    Wd, Qd, Rd = _dev64(W), _dev64(Q), _dev64(R)
+    N, k = Qd.shape
+    out = torch.empty(2 * Rd.shape[1], dtype=torch.float64, device=Wd.device)
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_residual_norms(ctx.h, Wd.data_ptr(), ld_of(Wd), Qd.data_ptr(), ld_of(Qd),
+                                            Rd.data_ptr(), ld_of(Rd), N, k, Rd.shape[1], out.data_ptr()),
+              "sqb_residual_norms")
+    o = out.cpu().numpy()
+    d2, w2 = o[: Rd.shape[1]], o[Rd.shape[1]:]
+    wf = float(np.sqrt(w2.sum()))
+    dn = float(np.sqrt(d2.sum()))
+    fro = dn / wf if wf else dn
+    colw = np.sqrt(w2)
+    cold = np.sqrt(d2)
+    zero = colw == 0.0
+    rel = cold / np.where(zero, wf if wf else 1.0, colw)
+    return FactorizationErrors(fro, float(rel.max()) if rel.size else 0.0,
+                               tuple(np.nonzero(zero)[0].tolist()))
+
+
+__all__ = ["SCALE_SQRT2", "SCALE_UNIT", "SCALINGS", "BreakdownError", "SingularFactorError",
+           "check_scaling", "sign", "cond_number", "orthogonality_error", "factorization_errors",
+           "FactorizationErrors", "gram", "is_device"]

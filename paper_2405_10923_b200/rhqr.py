@@ -1,0 +1,232 @@
+"""Randomized Householder QR (mirror of rhqr.py) on the sm_100a library.
+
+Every numerical step runs on the device (see csrc/rhqr_left.cu,
+csrc/compact.cu); this module only validates arguments exactly as the
+reference does, moves operands across the boundary and maps device status
+words to the reference's exceptions.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .devarray import CODES, empty_colmajor, is_device, ld_of, to_device, to_numpy, tag_of_torch
+from .linalg import (SCALE_SQRT2, SCALE_UNIT, BreakdownError, SingularFactorError, check_scaling,
+                     scaling_code)
+from .precision import DOUBLE_POLICY, require_device_policy
+from .sketching import EmbeddedSketch
+
+
+@dataclass
+class HouseholderStep:
+    """rhqr.py:38-48."""
+
+    j: int
+    u: object
+    s: object
+    sigma: float
+    rho: float
+    beta: float
+
+
+@dataclass
+class RHQRFactors:
+    """rhqr.py:143-168: W = Q R with Q = [I;0] - U T U1^t."""
+
+    U: object
+    S: object
+    T: object
+    R: object
+    psi: EmbeddedSketch
+    scaling: str
+    sigmas: object
+    rhos: object
+    betas: object
+
+    @property
+    def cols(self):
+        return self.U.shape[1]
+
+    def prefix(self, j):
+        return RHQRFactors(U=self.U[:, :j], S=self.S[:, :j], T=self.T[:j, :j], R=self.R[:j, :j],
+                           psi=self.psi, scaling=self.scaling, sigmas=self.sigmas[:j],
+                           rhos=self.rhos[:j], betas=self.betas[:j])
+
+
+def _embed(omega, n, m):
+    """rhqr.py:202-216 (same checks and messages)."""
+    if isinstance(omega, EmbeddedSketch):
+        if omega.n != n or omega.m != m:
+            raise ValueError(
+                f"embedding is {omega.out_dim}x{omega.n} with identity block "
+                f"{omega.m}, expected input {n} and block {m}")
+        if omega.omega.ell < m:
+            raise ValueError("sampling size below column count")
+        return omega
+    if omega.n != n - m:
+        raise ValueError(f"sketch takes {omega.n} coordinates, expected n-m={n - m}")
+    if omega.ell < m:
+        raise ValueError("sampling size below column count")
+    return EmbeddedSketch(m, omega)
+
+
+def raise_status(ctx, what="factorization"):
+    """Map the device status word to the reference's exceptions."""
+    code, col, val = ctx.status()
+    if code == _lib.SQB_OK:
+        return
+    if code == _lib.SQB_ERR_BREAKDOWN:
+        if val == 0.0:
+            raise BreakdownError(f"sketched tail annihilated at column {col}")
+        raise BreakdownError(f"reflector scale degenerated at column {col} (rho={val:.3e})")
+    if code == _lib.SQB_ERR_SINGULAR:
+        raise SingularFactorError(f"triangular factor has zero or subnormal diagonal at index {col - 1}")
+    raise _lib.SketchQRError(f"{what}: device status {code} at column {col}")
+
+
+def _out(t, host):
+    return to_numpy(t) if host else t
+
+
+def _shape2(A):
+    return tuple(A.shape) if is_device(A) else np.shape(np.asarray(A))
+
+
+def rhqr_left_device(Wd, psi, scaling, policy, check=True):
+    """Device-resident core: Wd is a column-major CUDA tensor in the low dtype
+    with row m 16-byte aligned.  Returns device factors."""
+    N, m = Wd.shape
+    tag = policy.low
+    od = psi.out_dim
+    U = empty_colmajor(N, m, tag, align_row=m)
+    S = empty_colmajor(od, m, "double")
+    T = empty_colmajor(m, m, "double")
+    R = empty_colmajor(m, m, "double")
+    scal = torch.empty(3 * m, dtype=torch.float64, device=Wd.device)
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_rhqr_left(
+        ctx.h, psi.omega.desc(), scaling_code(scaling), CODES[tag], Wd.data_ptr(), N, m, ld_of(Wd),
+        U.data_ptr(), ld_of(U), S.data_ptr(), ld_of(S), T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R),
+        scal.data_ptr(), scal.data_ptr() + 8 * m, scal.data_ptr() + 16 * m), "sqb_rhqr_left")
+    if check:
+        raise_status(ctx, "rhqr_left")
+    return U, S, T, R, scal[:m], scal[m:2 * m], scal[2 * m:]
+
+
+def rhqr_left(W, omega, scaling=SCALE_SQRT2, policy=None):
+    """rhqr.py:254-267: left-looking randomized Householder QR of a tall W."""
+    check_scaling(scaling)
+    policy = policy or DOUBLE_POLICY
+    require_device_policy(policy)
+    host = not is_device(W)
+    n, m = _shape2(W)
+    psi = _embed(omega, n, m)
+    Wd = to_device(W, policy.low, align_row=m)  # round_to(W, low) (rhqr.py:264)
+    U, S, T, R, sg, rh, bt = rhqr_left_device(Wd, psi, scaling, policy)
+    return RHQRFactors(U=_out(U, host), S=_out(S, host), T=_out(T, host), R=_out(R, host), psi=psi,
+                       scaling=scaling, sigmas=_out(sg, host), rhos=_out(rh, host),
+                       betas=_out(bt, host))
+
+
+def rh_vector(w, y, j, scaling=SCALE_SQRT2, policy=None):
+    """rhqr.py:51-97: reflector eliminating entries j+1.. of y = Psi w."""
+    check_scaling(scaling)
+    policy = policy or DOUBLE_POLICY
+    require_device_policy(policy)
+    host = not is_device(w)
+    yd = to_device(y, "double")
+    od = yd.shape[0]
+    if not 0 <= j - 1 < od:
+        raise ValueError(f"elimination index {j} outside sketch of length {od}")
+    wd = to_device(w, policy.low)
+    n = wd.shape[0]
+    u = empty_colmajor(n, 1, policy.low)
+    s = empty_colmajor(od, 1, "double")
+    scal = torch.empty(5, dtype=torch.float64, device=wd.device)
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_rh_vector(ctx.h, scaling_code(scaling), CODES[policy.low], wd.data_ptr(), n,
+                                       yd.data_ptr(), od, j, u.data_ptr(), s.data_ptr(), scal.data_ptr()),
+              "sqb_rh_vector")
+    raise_status(ctx, "rh_vector")
+    sc = scal.cpu().numpy()
+    return HouseholderStep(j=j, u=_out(u[:, 0], host), s=_out(s[:, 0], host), sigma=float(sc[0]),
+                           rho=float(sc[1]), beta=float(sc[2]))
+
+
+def apply_reflectors_compact(U, S, T, X, psi, transpose_t=False, policy=None):
+    """rhqr.py:100-119: (I - U T S^t Psi) X, or the reversed product."""
+    policy = policy or DOUBLE_POLICY
+    require_device_policy(policy)
+    host = not is_device(X)
+    tag = policy.low
+    Xs = _shape2(X)
+    vec = len(Xs) == 1
+    N = Xs[0]
+    m = psi.m
+    Ud = to_device(U if not vec or np.ndim(U) == 2 else U, tag)
+    if Ud.dim() == 1:
+        Ud = Ud[:, None]
+    r = Ud.shape[1] if np.prod(_shape2(U)) else 0
+    Sd = to_device(S, "double") if r else empty_colmajor(psi.out_dim, 1, "double")
+    Td = to_device(T, "double") if r else empty_colmajor(1, 1, "double")
+    Xd = to_device(X, tag, align_row=m)
+    k = Xd.shape[1]
+    Out = empty_colmajor(N, k, tag, align_row=m)
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_apply_reflectors(
+        ctx.h, psi.omega.desc(), m, CODES[tag], Ud.data_ptr(), ld_of(Ud), N, r, Sd.data_ptr(), ld_of(Sd),
+        Td.data_ptr(), ld_of(Td), 1 if transpose_t else 0, Xd.data_ptr(), ld_of(Xd), k,
+        Out.data_ptr(), ld_of(Out)), "sqb_apply_reflectors")
+    res = Out[:, 0] if vec else Out
+    if host:
+        return to_numpy(res)
+    return res
+
+
+def t_factor_from_sketches(S, policy=None):  # pragma: no cover - out of the hot path
+    raise NotImplementedError("t_factor_from_sketches belongs to rhqr_right/rhqr_block (SURVEY §8(f))")
+
+
+def _lo_tag(U):
+    return tag_of_torch(U.dtype) if is_device(U) else "double"
+
+
+def thin_q(factors):
+    """rhqr.py:171-178: Q = [I;0] - U T U1^t in float64."""
+    host = not is_device(factors.U)
+    tag = _lo_tag(factors.U)
+    Ud = to_device(factors.U, tag)
+    Td = to_device(factors.T, "double")
+    N, k = Ud.shape
+    Q = empty_colmajor(N, k, "double")
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_thin_q(ctx.h, CODES[tag], Ud.data_ptr(), ld_of(Ud), N, k, Td.data_ptr(),
+                                    ld_of(Td), Q.data_ptr(), ld_of(Q)), "sqb_thin_q")
+    return _out(Q, host)
+
+
+def sketch_q(factors):
+    """rhqr.py:181-188: Psi Q = [I;0] - S T U1^t without n-dimensional data."""
+    host = not is_device(factors.U)
+    tag = _lo_tag(factors.U)
+    k = factors.U.shape[1]
+    Ud = to_device(factors.U[:k], tag)
+    Td = to_device(factors.T, "double")
+    Sd = to_device(factors.S, "double")
+    od = Sd.shape[0]
+    Q = empty_colmajor(od, k, "double")
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_sketch_q(ctx.h, CODES[tag], Ud.data_ptr(), ld_of(Ud), k, Td.data_ptr(),
+                                      ld_of(Td), Sd.data_ptr(), ld_of(Sd), od, Q.data_ptr(), ld_of(Q)),
+              "sqb_sketch_q")
+    return _out(Q, host)
+
+
+__all__ = ["HouseholderStep", "RHQRFactors", "rh_vector", "rhqr_left", "apply_reflectors_compact",
+           "thin_q", "sketch_q", "SCALE_SQRT2", "SCALE_UNIT", "raise_status", "_embed"]
+_ = C

@@ -1,32 +1,50 @@
 // Left-looking randomized Householder QR on the device (rhqr_left, rhqr.py:254-267;
 // the hot loop _left_sweep, rhqr.py:219-251).
 //
-// Per column c:
-//   K3+K1  rhqr_col_kernel  one HBM pass over rows >= m: lazily scale column
-//          c-1 (u = fl(w * f)), w_c = fl(W[:,c] - fl(U[:, :c] coef)), store
-//          w_c (unscaled) into U[:, c], and emit the in-tile SRHT leaves of
-//          w_c.  An extra CTA does the m-row identity block.
-//   tree   srht_tree_kernel      y[m:] = Omega w_c (bit-exact tree)
-//   K4     rhqr_step_kernel      rh_vector (rhqr.py:51-97) on y, S/T/R column
-//          (_extend_t :135-140), the next column's coefficients
-//          T^t (S^t y0_{c+1}) (:241) — all fp64 in one CTA, no host trip.
+// Per column c two PDL-chained launches:
+//
+//   rhqr_col_kernel (K3+K1, ~all HBM traffic)  one pass over rows >= m:
+//       lazily scale column c-1 (u = fl(w * f), rhqr.py:86-95 + round_to),
+//       w_c = fl(W[:,c] - fl(U[:, :c] coef_c)) (:242), store w_c unscaled in
+//       U[:, c], emit the in-tile SRHT leaves of w_c.  Extra CTAs: the m-row
+//       identity block (y[0:m] = w_c[0:m]) and one HELPER doing the sketch-
+//       space work that is off the critical path (T column c-1, a_{c+1}).
+//
+//   rhqr_step_kernel (K4, an 8-CTA cluster)  finishes the SRHT tree
+//       (y[m:] = Omega w_c, bit-exact), rh_vector's scalars (:71-94), s = Psi u,
+//       the R column (:248-249), v = S_c^t s (the _extend_t product, :138) and
+//       the last entry of the next coefficients — cross-CTA sums through DSMEM.
+//
+// Coefficients (rhqr.py:241, coef_{c+1} = T_{c+1}^t S_{c+1}^t y0_{c+1}) are
+// split so that only two dots sit on the critical path:
+//   a_{c+1} = T_c^t (S_c^t y0_{c+1})          (helper, during pass c)
+//   coef_{c+1}[:c] = a_{c+1}
+//   coef_{c+1}[c]  = beta_c (s_c^t y0_{c+1} - v_c^t a_{c+1})   (step c)
+// which is T_{c+1}^t g with T_{c+1}[:c, c] = -beta_c T_c v_c, T[c,c] = beta_c
+// (_extend_t) expanded algebraically; T's column c itself is written by the
+// helper of pass c+1 exactly as _extend_t forms it.
 // The raw sketches y0 = Psi W[:, c] of all columns are computed once up front
 // (bitwise equal to the per-column psi.apply(w)).
 #include <algorithm>
+#include <cooperative_groups.h>
 
+#include "pdl.cuh"
 #include "sketch.cuh"
 #include "vec.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sqb {
 
 constexpr int COL_NT = 256;
-constexpr int STEP_NT = 512;
+constexpr int STEP_NT = 256;
+constexpr int STEP_CL = 8;  // cluster size of the step kernel
 
 struct ColArgs {
   int c;            // current column (>= 1)
   int m;            // identity-block rows = columns of W
   int64_t n;        // Omega input length (N - m)
-  int ell;
+  int ell, od;
   int log_tb;
   int64_t n_tiles;
   int64_t n_eff;
@@ -34,7 +52,7 @@ struct ColArgs {
   int64_t ldw;
   void* U;          // column-major, ldu
   int64_t ldu;
-  const double* coef;   // [c] fp64 coefficients T^t S^t y0 (rhqr.py:241)
+  const double* coef;   // [c] fp64 coefficients coef_c
   const double* fscale; // [1] f (sqrt2) or gamma (unit) of column c-1
   int scaling;
   int srht;             // emit SRHT leaves (else the sketch runs separately)
@@ -43,7 +61,14 @@ struct ColArgs {
   double scale_lo;
   void* P;              // leaves [ell][n_tiles] (acc type)
   double* y;            // (m + ell) sketch of w_c; [0, m) written here
-  const Status* st;
+  // helper (sketch-space work off the critical path)
+  double* S; int64_t lds;
+  double* T; int64_t ldt;
+  const double* Y0;     // raw sketches, od x m
+  const double* vprev;  // v_{c-1} = S_{c-1}^t s_{c-1}
+  const double* betas;
+  double* abuf;         // out: a_{c+1}
+  Status* st;
 };
 
 template <typename T>
@@ -75,14 +100,62 @@ __device__ void col_top_block(const ColArgs& a, const typename Lo<T>::acc* sc) {
   }
 }
 
+// T[:kk, kk] = -beta * T[:kk,:kk] v ; T[kk,kk] = beta   (_extend_t, rhqr.py:135-140)
+__device__ void complete_t_column(double* T, int64_t ldt, int kk, const double* v, double beta) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < kk; i += nw) {
+    double d = 0.0;
+    for (int k = i + lane; k < kk; k += 32) d = fma(T[i + (int64_t)k * ldt], v[k], d);
+    d = warp_sum(d);
+    if (lane == 0) T[i + (int64_t)kk * ldt] = __dmul_rn(-beta, d);
+  }
+  if (threadIdx.x == 0) T[kk + (int64_t)kk * ldt] = beta;
+}
+
+// helper CTA of pass c: complete T column c-1, then a_{c+1} = T_c^t (S_c^t y0_{c+1})
+__device__ void col_helper(const ColArgs& a, double* g) {
+  const int c = a.c;
+  complete_t_column(a.T, a.ldt, c - 1, a.vprev, a.betas[c - 1]);
+  if (c + 1 >= a.m) return;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* y0 = a.Y0 + (int64_t)(c + 1) * a.od;
+  for (int k = warp; k < c; k += nw) {
+    const double* sk = a.S + (int64_t)k * a.lds;
+    double d0 = 0.0, d1 = 0.0;
+    int r = k + lane;
+    for (; r + 32 < a.od; r += 64) {
+      d0 = fma(sk[r], y0[r], d0);
+      d1 = fma(sk[r + 32], y0[r + 32], d1);
+    }
+    if (r < a.od) d0 = fma(sk[r], y0[r], d0);
+    const double d = warp_sum(d0 + d1);
+    if (lane == 0) g[k] = d;
+  }
+  __syncthreads();
+  for (int j = warp; j < c; j += nw) {
+    const double* tj = a.T + (int64_t)j * a.ldt;  // column j of T, rows 0..j
+    double d = 0.0;
+    for (int i = lane; i <= j; i += 32) d = fma(tj[i], g[i], d);
+    d = warp_sum(d);
+    if (lane == 0) a.abuf[j] = d;
+  }
+}
+
 template <typename T, int VN>
 __global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
   using A = typename Lo<T>::acc;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   A* sc = reinterpret_cast<A*>(smem_raw);                      // coef rounded to low [c]
   A* sm = sc + ((a.c + 3) & ~3);                              // tile buffer
+  pdl_wait();
+  pdl_trigger();
   if (failed(a.st)) return;
   const int c = a.c;
+  if (blockIdx.x == a.n_eff + 1) {
+    col_helper(a, reinterpret_cast<double*>(sm));
+    return;
+  }
   for (int k = threadIdx.x; k < c; k += COL_NT) sc[k] = Lo<T>::from_double(a.coef[k]);
   __syncthreads();
   if (blockIdx.x == a.n_eff) {
@@ -172,114 +245,175 @@ __global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K4: one CTA, fp64 sketch-space step for column c (rhqr.py:51-97, 135-140,
-// 241, 245-250)
+// K4: cluster step kernel for column c
 // ---------------------------------------------------------------------------
 struct StepArgs {
-  int c, m, ell, od;          // od = m + ell (Psi output dim)
+  int c, m, ell, od;
   int scaling;
-  const double* y;            // sketch of w_c (od)
+  int tree;                   // finish the SRHT tree from the leaves (else y[m:] is given)
+  const void* P;              // leaves [ell][n_tiles]
+  int64_t n_tiles, n_eff;
+  const int64_t* idx;
+  int log_tb;
+  double norm_lo;
+  double* y;                  // (od) sketch of w_c: [0, m) given, [m, od) tree output
   const double* Y0;           // raw sketches (od x m, ld od)
   double* S; int64_t lds;
-  double* T; int64_t ldt;
   double* R; int64_t ldr;
   void* U; int64_t ldu;       // identity-block rows of U[:, c] are written here
   double* sigmas; double* rhos; double* betas;
-  double* coef_next;          // [c+1]
-  double* fscale;             // [1]
+  double* fscale;             // out: f of column c
+  double* vbuf;               // out: v_c = S_c^t s_c
+  const double* abuf;         // in: a_{c+1}
+  double* coef;               // out: coef_{c+1}
   Status* st;
 };
 
 template <typename T>
-__global__ void __launch_bounds__(STEP_NT) rhqr_step_kernel(StepArgs a) {
+__global__ void __cluster_dims__(STEP_CL, 1, 1) __launch_bounds__(STEP_NT)
+rhqr_step_kernel(StepArgs a) {
+  using A = typename Lo<T>::acc;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* s = reinterpret_cast<double*>(smem_raw);  // [od] new reflector sketch
-  double* v = s + a.od;                            // [m] S^t s, then S^t y0
-  double* red = v + a.m;                           // [32]
-  __shared__ double sh_scal[4];
-  if (failed(a.st)) return;
-  const int c = a.c, od = a.od, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarp = STEP_NT / 32;
-  // rho = ||y[c:]||_2 (rhqr.py:72)
-  double part = 0.0;
-  for (int r = c + tid; r < od; r += STEP_NT) part = fma(a.y[r], a.y[r], part);
-  const double rho = sqrt(block_sum(part, red));
-  if (tid == 0) {
-    const double yc = a.y[c];
-    const double sigma = yc >= 0.0 ? 1.0 : -1.0;                       // linalg.py:200-202
-    const double gamma = __dadd_rn(yc, sigma * rho);                     // rhqr.py:76
-    const double beta = __ddiv_rn(1.0, __dmul_rn(__dmul_rn(rho, sigma), gamma));  // :77
-    int bad = 0;
-    if (rho == 0.0) { fail(a.st, SQB_ERR_BREAKDOWN, c + 1, 0.0); bad = 1; }
-    else if (!isfinite(beta)) { fail(a.st, SQB_ERR_BREAKDOWN, c + 1, rho); bad = 1; }
-    double f, beta_out;
-    if (a.scaling == SQB_SCALE_SQRT2) { f = __dsqrt_rn(beta); beta_out = 1.0; }
-    else { f = gamma; beta_out = __ddiv_rn(__dmul_rn(sigma, gamma), rho); }
-    sh_scal[0] = sigma; sh_scal[1] = gamma; sh_scal[2] = f; sh_scal[3] = bad ? -1.0 : beta_out;
-    a.sigmas[c] = sigma; a.rhos[c] = rho; a.betas[c] = beta_out;
-    *a.fscale = f;
-  }
-  __syncthreads();
-  const double sigma = sh_scal[0], gamma = sh_scal[1], f = sh_scal[2], beta_out = sh_scal[3];
-  if (beta_out < 0.0) return;  // breakdown recorded
-  const bool sq = a.scaling == SQB_SCALE_SQRT2;
-  // s = Psi u (rhqr.py:83-96); u's identity-block rows; R column (:248-249)
-  T* U = (T*)a.U;
-  for (int r = tid; r < od; r += STEP_NT) {
-    const double yh = r < c ? 0.0 : (r == c ? gamma : a.y[r]);
-    const double sv = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
-    s[r] = sv;
-    a.S[r + (int64_t)c * a.lds] = sv;
-    if (r < a.m) {
-      U[r + (int64_t)c * a.ldu] = Lo<T>::store(Lo<T>::from_double(sv));
-      a.R[r + (int64_t)c * a.ldr] = r < c ? a.y[r] : (r == c ? -sigma * rho : 0.0);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int c = a.c, m = a.m, ell = a.ell, od = a.od, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = STEP_NT / 32;
+  const int blk = (ell + STEP_CL - 1) / STEP_CL;
+  const int i0 = rank * blk, i1 = min(ell, i0 + blk), nown = max(0, i1 - i0);
+  const int nk = c + 1;  // entries of the partial vector: v[0..c-1], s^t y0_{c+1}
+  double* ys = reinterpret_cast<double*>(smem_raw);  // [blk] own sketch rows
+  double* ss = ys + blk;                             // [blk] own s rows
+  double* st = ss + blk;                             // [m] top-block s (rank 0)
+  double* gath = st + m;                             // [STEP_CL * nk] partial vectors (rank 0)
+  double* part = gath + STEP_CL * nk;                // [STEP_CL] rho^2 partials
+  double* red = part + STEP_CL;                      // [32]
+  __shared__ double scal[4];
+  pdl_wait();
+  pdl_trigger();
+  const bool dead = failed(a.st);  // uniform across the cluster; still take part in syncs
+  // ---- phase A: sketch rows of this CTA (tree over tile leaves, bit-exact)
+  if (!dead) {
+    if (a.tree) {
+      for (int i = i0 + warp; i < i1; i += nw) {
+        const int64_t rhi = __ldg(a.idx + i) >> a.log_tb;
+        const A v = warp_tile_tree<T>((const A*)a.P + (int64_t)i * a.n_tiles, (int)a.n_tiles,
+                                      (int)a.n_eff, rhi);
+        if (lane == 0) {
+          const double yv = (double)Lo<T>::mul(v, (A)a.norm_lo);
+          ys[i - i0] = yv;
+          a.y[m + i] = yv;
+        }
+      }
+    } else {
+      for (int i = i0 + tid; i < i1; i += STEP_NT) ys[i - i0] = a.y[m + i];
     }
   }
   __syncthreads();
-  // v = S[:, :c]^t s  (warp per column, rows strided by lane)
-  for (int k = warp; k < c; k += nwarp) {
-    const double* sk = a.S + (int64_t)k * a.lds;
-    double d = 0.0;
-    for (int r = k + lane; r < od; r += 32) d = fma(sk[r], s[r], d);  // S[r,k] = 0 for r < k
-    d = warp_sum(d);
-    if (lane == 0) v[k] = d;
+  // ---- phase B: rho = ||y[c:]|| (rhqr.py:72); partials pushed to every CTA
+  double p = 0.0;
+  if (!dead) {
+    for (int i = tid; i < nown; i += STEP_NT) p = fma(ys[i], ys[i], p);
+    if (rank == 0)
+      for (int r = c + tid; r < m; r += STEP_NT) p = fma(a.y[r], a.y[r], p);
+  }
+  p = block_sum(p, red);
+  if (tid < STEP_CL) *cluster.map_shared_rank(&part[rank], tid) = p;
+  cluster.sync();
+  if (dead) return;
+  if (tid == 0) {
+    double r2 = 0.0;
+    for (int q = 0; q < STEP_CL; ++q) r2 += part[q];
+    const double rho = sqrt(r2);
+    const double yc = a.y[c];
+    const double sigma = yc >= 0.0 ? 1.0 : -1.0;                                 // linalg.py:200-202
+    const double gamma = __dadd_rn(yc, sigma * rho);                               // rhqr.py:76
+    const double beta = __ddiv_rn(1.0, __dmul_rn(__dmul_rn(rho, sigma), gamma));   // :77
+    bool bad = false;
+    if (rho == 0.0) { bad = true; if (rank == 0) fail(a.st, SQB_ERR_BREAKDOWN, c + 1, 0.0); }
+    else if (!isfinite(beta)) { bad = true; if (rank == 0) fail(a.st, SQB_ERR_BREAKDOWN, c + 1, rho); }
+    double f, bo;
+    if (a.scaling == SQB_SCALE_SQRT2) { f = __dsqrt_rn(beta); bo = 1.0; }
+    else { f = gamma; bo = __ddiv_rn(__dmul_rn(sigma, gamma), rho); }
+    scal[0] = sigma; scal[1] = gamma; scal[2] = f; scal[3] = bad ? -1.0 : bo;
+    if (rank == 0 && !bad) {
+      a.sigmas[c] = sigma; a.rhos[c] = rho; a.betas[c] = bo;
+      *a.fscale = f;
+      a.R[c + (int64_t)c * a.ldr] = -sigma * rho;
+    }
   }
   __syncthreads();
-  // T[:c, c] = -beta * T[:c,:c] v ; T[c,c] = beta  (rhqr.py:135-140)
-  for (int i = tid; i < c; i += STEP_NT) {
-    double d = 0.0;
-    for (int k = i; k < c; ++k) d = fma(a.T[i + (int64_t)k * a.ldt], v[k], d);
-    a.T[i + (int64_t)c * a.ldt] = __dmul_rn(-beta_out, d);
+  const double gamma = scal[1], f = scal[2], bo = scal[3];
+  // a breakdown is seen identically by every CTA: leave together (no more DSMEM)
+  if (bo < 0.0) return;
+  const bool sq = a.scaling == SQB_SCALE_SQRT2;
+  // ---- phase C: s = Psi u (rhqr.py:83-96) for own rows; rank 0 also the top block
+  for (int i = tid; i < nown; i += STEP_NT) {
+    const double sv = sq ? __dmul_rn(ys[i], f) : __ddiv_rn(ys[i], f);
+    ss[i] = sv;
+    a.S[m + i0 + i + (int64_t)c * a.lds] = sv;
   }
-  if (tid == 0) a.T[c + (int64_t)c * a.ldt] = beta_out;
-  if (c + 1 >= a.m) return;
-  __syncthreads();
-  // next coefficients: g = S[:, :c+1]^t y0_{c+1}; coef = T[:c+1,:c+1]^t g (rhqr.py:241)
-  const double* y0 = a.Y0 + (int64_t)(c + 1) * od;
-  for (int k = warp; k <= c; k += nwarp) {
-    const double* sk = a.S + (int64_t)k * a.lds;
-    double d = 0.0;
-    for (int r = k + lane; r < od; r += 32) d = fma(k == c ? s[r] : sk[r], y0[r], d);
-    d = warp_sum(d);
-    if (lane == 0) v[k] = d;
+  if (rank == 0) {
+    T* U = (T*)a.U;
+    for (int r = tid; r < m; r += STEP_NT) {
+      const double yh = r < c ? 0.0 : (r == c ? gamma : a.y[r]);
+      const double sv = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
+      st[r] = sv;
+      a.S[r + (int64_t)c * a.lds] = sv;
+      U[r + (int64_t)c * a.ldu] = Lo<T>::store(Lo<T>::from_double(sv));  // u top rows
+      if (r != c) a.R[r + (int64_t)c * a.ldr] = r < c ? a.y[r] : 0.0;   // rhqr.py:248
+    }
   }
   __syncthreads();
-  for (int k = warp; k <= c; k += nwarp) {
-    const double* tk = a.T + (int64_t)k * a.ldt;  // column k of T, rows 0..k
+  // partial vector: v[k] = S[:, k]^t s (k < c), d = s^t y0_{c+1}; pushed to rank 0
+  const bool has_next = c + 1 < m;
+  const double* y0n = has_next ? a.Y0 + (int64_t)(c + 1) * od : nullptr;
+  double* dst0 = cluster.map_shared_rank(gath, 0) + rank * nk;
+  for (int k = warp; k < nk; k += nw) {
+    if (k == c && !has_next) break;
+    const double* col = (k < c) ? a.S + (int64_t)k * a.lds : y0n;
     double d = 0.0;
-    for (int i = lane; i <= k; i += 32) d = fma(tk[i], v[i], d);
+    for (int i = lane; i < nown; i += 32) d = fma(col[m + i0 + i], ss[i], d);
+    if (rank == 0)
+      for (int r = c + lane; r < m; r += 32) d = fma(col[r], st[r], d);  // s[r] = 0 for r < c
     d = warp_sum(d);
-    if (lane == 0) a.coef_next[k] = d;
+    if (lane == 0) dst0[k] = d;
+  }
+  cluster.sync();
+  if (rank != 0) return;
+  // ---- phase D (rank 0): v_c, and coef_{c+1} = [a_{c+1}; beta (d - v^t a_{c+1})]
+  double va = 0.0;
+  for (int k = tid; k < c; k += STEP_NT) {
+    double v = 0.0;
+    for (int q = 0; q < STEP_CL; ++q) v += gath[q * nk + k];
+    a.vbuf[k] = v;
+    if (has_next) {
+      const double ak = a.abuf[k];
+      a.coef[k] = ak;
+      va = fma(v, ak, va);
+    }
+  }
+  if (!has_next) return;
+  va = block_sum(va, red);
+  if (tid == 0) {
+    double d = 0.0;
+    for (int q = 0; q < STEP_CL; ++q) d += gath[q * nk + c];
+    a.coef[c] = __dmul_rn(bo, d - va);
   }
 }
 
-// final pass: U[m:, m-1] = scaled(w_{m-1}) (the lazy scaling of the last column)
+// last column: lazy scaling of its Omega rows + its T column (_extend_t)
 template <typename T>
-__global__ void scale_last_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t n,
-                                  const double* fscale, int scaling, const Status* st) {
+__global__ void finish_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t n,
+                              const double* fscale, int scaling, double* Tm, int64_t ldt, int m,
+                              const double* v, const double* betas, const Status* st) {
+  pdl_wait();
   if (failed(st)) return;
+  if (blockIdx.x == gridDim.x - 1) {
+    complete_t_column(Tm, ldt, m - 1, v, betas[m - 1]);
+    return;
+  }
   const double f = *fscale;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)(gridDim.x - 1) * blockDim.x)
     dst[i] = Lo<T>::store(lazy_scale<T>(Lo<T>::load(src[i]), f, scaling));
 }
 
@@ -307,13 +441,14 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
   const int64_t n = N - m, ell = sk->ell, od = m + ell;
   const bool srht = sk->kind == SQB_SKETCH_SRHT;
   const SrhtGeom g = srht ? srht_geom_t<T>(sk) : SrhtGeom{0, 1, 1};
-  // workspace: raw sketches, column sketch, coefficients, scale, leaves
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(m, (int64_t)(64ll << 20) /
                                    std::max<size_t>(1, sketch_partials_bytes(sk, Lo<T>::code, 1))));
   WsPlan plan;
   const size_t iY0 = plan.add(sizeof(double) * od * m);
   const size_t iy = plan.add(sizeof(double) * od);
   const size_t icoef = plan.add(sizeof(double) * (m + 1));
+  const size_t iabuf = plan.add(sizeof(double) * (m + 1));
+  const size_t ivbuf = plan.add(sizeof(double) * (m + 1));
   const size_t ifs = plan.add(sizeof(double) * 2);
   const size_t iP = plan.add(std::max(sketch_partials_bytes(sk, Lo<T>::code, chunk),
                                       sketch_partials_bytes(sk, Lo<T>::code, 1)));
@@ -321,13 +456,13 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
   double* Y0 = ws_ptr<double>(ctx, plan, iY0);
   double* y = ws_ptr<double>(ctx, plan, iy);
   double* coef = ws_ptr<double>(ctx, plan, icoef);
+  double* abuf = ws_ptr<double>(ctx, plan, iabuf);
+  double* vbuf = ws_ptr<double>(ctx, plan, ivbuf);
   double* fs = ws_ptr<double>(ctx, plan, ifs);
   void* P = ws_ptr<void>(ctx, plan, iP);
   Status* st = ctx->d_status;
 
-  SQB_TRY(zero2d(ctx, S, od, m, lds));
   SQB_TRY(zero2d(ctx, Tm, m, m, ldt));
-  SQB_TRY(zero2d(ctx, R, m, m, ldr));
   // raw sketches y0 = Psi W (all columns; rhqr.py:240 for every column)
   SQB_TRY(launch_copy_top(ctx, Lo<T>::code, W, ldw, m, m, Y0, od, st));
   const size_t esz = sizeof(T);
@@ -336,17 +471,20 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
     SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const char*)W + (c0 * ldw + m) * esz, ldw, kc,
                           Y0 + c0 * od, od, m, P, st));
   }
-  // column 0: y = y0_0, w = W[:, 0]
-  StepArgs sa{0, (int)m, (int)ell, (int)od, scaling, Y0, Y0, S, lds, Tm, ldt, R, ldr, U, ldu,
-              sigmas, rhos, betas, coef, fs, st};
-  const size_t step_smem = sizeof(double) * (od + m + 32);
-  if (step_smem > 48 * 1024)
-    cudaFuncSetAttribute(rhqr_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step_smem);
-  rhqr_step_kernel<T><<<1, STEP_NT, step_smem, ctx->stream>>>(sa);
-  SQB_TRY(check_launch(ctx, "rhqr_step_kernel"));
-
   double scale_lo = 0.0, norm_lo = 0.0;
   if (srht) srht_constants(sk, Lo<T>::code, &scale_lo, &norm_lo);
+
+  const size_t step_smem = sizeof(double) * (2 * ((ell + STEP_CL - 1) / STEP_CL) + m +
+                                             STEP_CL * (m + 1) + STEP_CL + 32);
+  cudaFuncSetAttribute(rhqr_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(step_smem, 48 * 1024));
+  // column 0: y = y0_0 (w = W[:, 0]); a_1 is empty
+  StepArgs sa{0, (int)m, (int)ell, (int)od, scaling, 0, P, g.n_tiles, g.n_eff,
+              srht ? sk->indices : nullptr, g.log_tb, norm_lo, Y0, Y0, S, lds, R, ldr, U, ldu,
+              sigmas, rhos, betas, fs, vbuf, abuf, coef, st};
+  SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT),
+                     step_smem, sa));
+
   constexpr int VN = VecN<T>::n;
   const bool vec = ((reinterpret_cast<uintptr_t>((const char*)W + m * esz) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>((const char*)U + m * esz) & 15) == 0) &&
@@ -354,43 +492,39 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
   const int tb_max = 1 << TileCfg<T>::LOG_TB;
   const int64_t n_eff_col = srht ? g.n_eff : (n + tb_max - 1) / tb_max;
   const int log_tb_col = srht ? g.log_tb : TileCfg<T>::LOG_TB;
+  const size_t tile_bytes = srht ? tile_smem_bytes<A>(tb_max) : 0;
+  const size_t col_smem_max = sizeof(A) * ((m + 3) & ~3) +
+                              std::max(tile_bytes, sizeof(double) * (size_t)(m + 1));
+  auto colk = vec ? rhqr_col_kernel<T, VN> : rhqr_col_kernel<T, 1>;
+  cudaFuncSetAttribute(colk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
   for (int64_t c = 1; c < m; ++c) {
-    ColArgs ca{(int)c, (int)m, n, (int)ell, log_tb_col, g.n_tiles, n_eff_col, W, ldw, U, ldu,
+    ColArgs ca{(int)c, (int)m, n, (int)ell, (int)od, log_tb_col, g.n_tiles, n_eff_col, W, ldw, U, ldu,
                coef, fs, scaling, srht ? 1 : 0, srht ? sk->sign_bits : nullptr,
-               srht ? sk->indices : nullptr, scale_lo, P, y, st};
-    const size_t smem = sizeof(A) * ((c + 3) & ~3) + (srht ? tile_smem_bytes<A>(tb_max) : 0);
-    dim3 grid((unsigned)(n_eff_col + 1));
+               srht ? sk->indices : nullptr, scale_lo, P, y, S, lds, Tm, ldt, Y0, vbuf, betas, abuf,
+               st};
+    const size_t smem = sizeof(A) * ((c + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(c + 1));
     prof_begin(ctx);
-    if (vec) {
-      auto kern = rhqr_col_kernel<T, VN>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kern<<<grid, COL_NT, smem, ctx->stream>>>(ca);
-    } else {
-      auto kern = rhqr_col_kernel<T, 1>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kern<<<grid, COL_NT, smem, ctx->stream>>>(ca);
-    }
+    SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", colk, dim3((unsigned)(n_eff_col + 2)), dim3(COL_NT), smem,
+                       ca));
     // algorithmic bytes of this pass: read U[:, :c] and W[:, c], write U[:, c]
     prof_end(ctx, (double)esz * (double)N * (double)(c + 2));
-    SQB_TRY(check_launch(ctx, "rhqr_col_kernel"));
-    if (srht) {
-      SQB_TRY(launch_srht_tree(ctx, sk, Lo<T>::code, P, 1, y, od, m, st));
-    } else {
+    if (!srht)
       SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const char*)U + (c * ldu + m) * esz, ldu, 1, y, od,
                             m, P, st));
-    }
     sa.c = (int)c;
     sa.y = y;
-    rhqr_step_kernel<T><<<1, STEP_NT, step_smem, ctx->stream>>>(sa);
-    SQB_TRY(check_launch(ctx, "rhqr_step_kernel"));
+    sa.tree = srht ? 1 : 0;
+    SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT),
+                       step_smem, sa));
   }
-  // lazy scaling of the last column's Omega rows
+  // last column: lazy scaling of its Omega rows and its T column
   {
     const T* src = m == 1 ? (const T*)W + m : (const T*)U + (m - 1) * ldu + m;
     T* dst = (T*)U + (m - 1) * ldu + m;
-    const unsigned gb = (unsigned)std::min<int64_t>((n + 255) / 256, 8 * 148);
-    scale_last_kernel<T><<<gb, 256, 0, ctx->stream>>>(src, dst, n, fs, scaling, st);
-    SQB_TRY(check_launch(ctx, "scale_last_kernel"));
+    const unsigned gb = (unsigned)std::min<int64_t>((n + 255) / 256, 4 * 148);
+    SQB_TRY(launch_pdl(ctx, "finish_kernel", finish_kernel<T>, dim3(gb + 1), dim3(256), 0, src, dst, n,
+                       (const double*)fs, scaling, Tm, ldt, (int)m, (const double*)vbuf,
+                       (const double*)betas, (const Status*)st));
   }
   return SQB_OK;
 }
@@ -404,76 +538,6 @@ int rhqr_left_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_d
     case SQB_F32: return rhqr_left_t<float>(ctx, sk, scaling, W, N, m, ldw, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas);
     case SQB_F16: return rhqr_left_t<__half>(ctx, sk, scaling, W, N, m, ldw, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas);
     case SQB_BF16: return rhqr_left_t<__nv_bfloat16>(ctx, sk, scaling, W, N, m, ldw, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas);
-  }
-  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
-}
-
-}  // namespace sqb
-
-// ---------------------------------------------------------------------------
-// single reflector (rh_vector, rhqr.py:51-97) for the public API
-// ---------------------------------------------------------------------------
-namespace sqb {
-
-__global__ void rh_scalars_kernel(const double* __restrict__ y, int od, int jj, int scaling,
-                                  double* scal, Status* st) {
-  __shared__ double red[32];
-  double part = 0.0;
-  for (int r = jj + threadIdx.x; r < od; r += blockDim.x) part = fma(y[r], y[r], part);
-  const double rho = sqrt(block_sum(part, red));
-  if (threadIdx.x == 0) {
-    const double sigma = y[jj] >= 0.0 ? 1.0 : -1.0;
-    const double gamma = __dadd_rn(y[jj], sigma * rho);
-    const double beta = __ddiv_rn(1.0, __dmul_rn(__dmul_rn(rho, sigma), gamma));
-    if (rho == 0.0) fail(st, SQB_ERR_BREAKDOWN, jj + 1, 0.0);
-    else if (!isfinite(beta)) fail(st, SQB_ERR_BREAKDOWN, jj + 1, rho);
-    double f, bo;
-    if (scaling == SQB_SCALE_SQRT2) { f = __dsqrt_rn(beta); bo = 1.0; }
-    else { f = gamma; bo = __ddiv_rn(__dmul_rn(sigma, gamma), rho); }
-    scal[0] = sigma; scal[1] = rho; scal[2] = bo; scal[3] = f; scal[4] = gamma;
-  }
-}
-
-template <typename T>
-__global__ void rh_vectors_kernel(const T* __restrict__ w, int64_t n, const double* __restrict__ y,
-                                  int od, int jj, int scaling, const double* scal, T* __restrict__ u,
-                                  double* __restrict__ s, const Status* st) {
-  if (failed(st)) return;
-  const double sigma = scal[0], rho = scal[1], f = scal[3], gamma = scal[4];
-  const bool sq = scaling == SQB_SCALE_SQRT2;
-  const int64_t tot = n > od ? n : od;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < n) {
-      double uh = i < jj ? 0.0 : (double)Lo<T>::load(w[i]);
-      if (i == jj) uh = __dadd_rn(uh, sigma * rho);
-      const double uv = sq ? __dmul_rn(uh, f) : __ddiv_rn(uh, f);
-      u[i] = Lo<T>::store(Lo<T>::from_double(uv));
-    }
-    if (i < od) {
-      const double yh = i < jj ? 0.0 : (i == jj ? gamma : y[i]);
-      s[i] = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
-    }
-  }
-}
-
-template <typename T>
-static int rh_vector_t(sqb_ctx* ctx, int scaling, const void* w, int64_t n, const double* y, int64_t od,
-                       int64_t j, void* u, double* s, double* scal) {
-  rh_scalars_kernel<<<1, 256, 0, ctx->stream>>>(y, (int)od, (int)(j - 1), scaling, scal, ctx->d_status);
-  SQB_TRY(check_launch(ctx, "rh_scalars_kernel"));
-  const int64_t tot = std::max(n, od);
-  rh_vectors_kernel<T><<<(unsigned)std::min<int64_t>((tot + 255) / 256, 4 * 148), 256, 0, ctx->stream>>>(
-      (const T*)w, n, y, (int)od, (int)(j - 1), scaling, scal, (T*)u, s, ctx->d_status);
-  return check_launch(ctx, "rh_vectors_kernel");
-}
-
-int rh_vector_dispatch(sqb_ctx* ctx, int scaling, int lo_dtype, const void* w, int64_t n, const double* y,
-                       int64_t od, int64_t j, void* u, double* s, double* scal) {
-  switch (lo_dtype) {
-    case SQB_F64: return rh_vector_t<double>(ctx, scaling, w, n, y, od, j, u, s, scal);
-    case SQB_F32: return rh_vector_t<float>(ctx, scaling, w, n, y, od, j, u, s, scal);
-    case SQB_F16: return rh_vector_t<__half>(ctx, scaling, w, n, y, od, j, u, s, scal);
-    case SQB_BF16: return rh_vector_t<__nv_bfloat16>(ctx, scaling, w, n, y, od, j, u, s, scal);
   }
   return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
 }

@@ -270,7 +270,10 @@ def main():
     traffic = None
     try:
         with open(prof_path) as f:
-            traffic = json.load(f).get("rhqr_col_kernel_bytes_per_launch_c64")
+            tj = json.load(f)
+            traffic = {"bytes_per_launch": tj.get("rhqr_col_kernel_bytes_per_launch_c64"),
+                       "alg_bytes_per_launch": tj.get("rhqr_col_kernel_alg_bytes_c64"),
+                       "launch": "column c=64 (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)"}
     except Exception:
         pass
 

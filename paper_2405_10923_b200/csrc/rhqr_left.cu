@@ -37,7 +37,7 @@ namespace cg = cooperative_groups;
 namespace sqb {
 
 constexpr int COL_NT = 256;
-constexpr int STEP_NT = 256;
+constexpr int STEP_NT = 512;
 constexpr int STEP_CL = 8;  // cluster size of the step kernel
 
 struct ColArgs {
@@ -52,7 +52,8 @@ struct ColArgs {
   int64_t ldw;
   void* U;          // column-major, ldu
   int64_t ldu;
-  const double* coef;   // [c] fp64 coefficients coef_c
+  const double* acur;   // [c-1] coef_c[:c-1] = a_c (written by the helper of pass c-1)
+  const double* clast;  // [m] clast[c] = coef_c[c-1] (written by step c-1)
   const double* fscale; // [1] f (sqrt2) or gamma (unit) of column c-1
   int scaling;
   int srht;             // emit SRHT leaves (else the sketch runs separately)
@@ -67,7 +68,7 @@ struct ColArgs {
   const double* Y0;     // raw sketches, od x m
   const double* vprev;  // v_{c-1} = S_{c-1}^t s_{c-1}
   const double* betas;
-  double* abuf;         // out: a_{c+1}
+  double* anext;        // out: a_{c+1}
   Status* st;
 };
 
@@ -78,25 +79,44 @@ __device__ __forceinline__ typename Lo<T>::acc lazy_scale(typename Lo<T>::acc w,
   return Lo<T>::from_double(u);
 }
 
-// identity block: y[r] = w_c[r] = fl(W[r,c] - fl(sum_k U[r,k] coef[k])), r < m
+// identity block: y[r] = w_c[r] = fl(W[r,c] - fl(sum_k U[r,k] coef[k])), r < m.
+// Columns k <= c-2 are final before step c-1 ends, so they are summed before
+// the PDL wait; column c-1 (its top rows come from step c-1) after it.
 template <typename T>
-__device__ void col_top_block(const ColArgs& a, const typename Lo<T>::acc* sc) {
+__device__ void col_top_block(const ColArgs& a, typename Lo<T>::acc* sc) {
   using A = typename Lo<T>::acc;
   const T* W = (const T*)a.W;
   const T* U = (const T*)a.U;
-  for (int r = threadIdx.x; r < a.m; r += blockDim.x) {
+  const int c = a.c;
+  constexpr int RPT = 4;  // rows per thread (m <= RPT * blockDim)
+  A acc[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int r = threadIdx.x + q * blockDim.x;
     A acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
-    int k = 0;
-    for (; k + 4 <= a.c; k += 4) {
-      acc0 = fma(Lo<T>::load(U[r + (int64_t)k * a.ldu]), sc[k], acc0);
-      acc1 = fma(Lo<T>::load(U[r + (int64_t)(k + 1) * a.ldu]), sc[k + 1], acc1);
-      acc2 = fma(Lo<T>::load(U[r + (int64_t)(k + 2) * a.ldu]), sc[k + 2], acc2);
-      acc3 = fma(Lo<T>::load(U[r + (int64_t)(k + 3) * a.ldu]), sc[k + 3], acc3);
+    if (r < a.m) {
+      int k = 0;
+      for (; k + 4 <= c - 1; k += 4) {
+        acc0 = fma(Lo<T>::load(U[r + (int64_t)k * a.ldu]), sc[k], acc0);
+        acc1 = fma(Lo<T>::load(U[r + (int64_t)(k + 1) * a.ldu]), sc[k + 1], acc1);
+        acc2 = fma(Lo<T>::load(U[r + (int64_t)(k + 2) * a.ldu]), sc[k + 2], acc2);
+        acc3 = fma(Lo<T>::load(U[r + (int64_t)(k + 3) * a.ldu]), sc[k + 3], acc3);
+      }
+      for (; k < c - 1; ++k) acc0 = fma(Lo<T>::load(U[r + (int64_t)k * a.ldu]), sc[k], acc0);
     }
-    for (; k < a.c; ++k) acc0 = fma(Lo<T>::load(U[r + (int64_t)k * a.ldu]), sc[k], acc0);
-    const A dot = (acc0 + acc1) + (acc2 + acc3);
-    const A w = Lo<T>::sub(Lo<T>::load(W[r + (int64_t)a.c * a.ldw]), Lo<T>::rnd(dot));
-    a.y[r] = (double)w;
+    acc[q] = (acc0 + acc1) + (acc2 + acc3);
+  }
+  pdl_wait();
+  if (failed(a.st)) return;
+  const A cl = Lo<T>::from_double(a.clast[c]);
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int r = threadIdx.x + q * blockDim.x;
+    if (r < a.m) {
+      const A dot = fma(Lo<T>::load(U[r + (int64_t)(c - 1) * a.ldu]), cl, acc[q]);
+      const A w = Lo<T>::sub(Lo<T>::load(W[r + (int64_t)c * a.ldw]), Lo<T>::rnd(dot));
+      a.y[r] = (double)w;
+    }
   }
 }
 
@@ -138,7 +158,7 @@ __device__ void col_helper(const ColArgs& a, double* g) {
     double d = 0.0;
     for (int i = lane; i <= j; i += 32) d = fma(tj[i], g[i], d);
     d = warp_sum(d);
-    if (lane == 0) a.abuf[j] = d;
+    if (lane == 0) a.anext[j] = d;
   }
 }
 
@@ -148,15 +168,18 @@ __global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   A* sc = reinterpret_cast<A*>(smem_raw);                      // coef rounded to low [c]
   A* sm = sc + ((a.c + 3) & ~3);                              // tile buffer
-  pdl_wait();
   pdl_trigger();
-  if (failed(a.st)) return;
   const int c = a.c;
   if (blockIdx.x == a.n_eff + 1) {
+    pdl_wait();
+    if (failed(a.st)) return;
     col_helper(a, reinterpret_cast<double*>(sm));
     return;
   }
-  for (int k = threadIdx.x; k < c; k += COL_NT) sc[k] = Lo<T>::from_double(a.coef[k]);
+  // coef_c[:c-1] = a_c is final before step c-1 ends (helper of pass c-1): load
+  // it and stream the bulk of the GEMV BEFORE waiting on step c-1 (look-ahead
+  // overlap of the HBM pass with the sketch-space step, via PDL)
+  for (int k = threadIdx.x; k < c - 1; k += COL_NT) sc[k] = Lo<T>::from_double(a.acur[k]);
   __syncthreads();
   if (blockIdx.x == a.n_eff) {
     col_top_block<T>(a, sc);
@@ -193,12 +216,15 @@ __global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
 #pragma unroll
       for (int j = 0; j < VN; ++j) acc[v][j] = fma(v0[v][j], ck, acc[v][j]);
   }
+  // ---- wait for step c-1 (f_{c-1}, coef_c[c-1], breakdown status)
+  pdl_wait();
+  if (failed(a.st)) return;
   // column c-1: lazy scaling of the stored w_{c-1}, write back u_{c-1}
   {
     const T* src = (c == 1 ? W : (const T*)U) + ro + (int64_t)(c - 1) * (c == 1 ? 0 : a.ldu);
     T* dst = U + ro + (int64_t)(c - 1) * a.ldu;
     const double f = *a.fscale;
-    const A ck = sc[c - 1];
+    const A ck = Lo<T>::from_double(a.clast[c]);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const int i = (v * COL_NT + threadIdx.x) * VN;
@@ -245,7 +271,9 @@ __global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K4: cluster step kernel for column c
+// K4: cluster step kernel for column c.  The od = m + ell rows of Psi-space are
+// split into STEP_CL contiguous blocks, one per CTA of the cluster (top-block
+// rows < m first, then the Omega rows whose sketch values the tree produces).
 // ---------------------------------------------------------------------------
 struct StepArgs {
   int c, m, ell, od;
@@ -264,10 +292,21 @@ struct StepArgs {
   double* sigmas; double* rhos; double* betas;
   double* fscale;             // out: f of column c
   double* vbuf;               // out: v_c = S_c^t s_c
-  const double* abuf;         // in: a_{c+1}
-  double* coef;               // out: coef_{c+1}
+  const double* anext;        // in: a_{c+1} (helper of pass c)
+  double* clast;              // out: clast[c+1] = coef_{c+1}[c]
   Status* st;
 };
+
+constexpr int STEP_KC = 128;                 // columns staged per chunk
+constexpr int STEP_NPART = STEP_NT / STEP_KC;
+
+__host__ __device__ inline int step_rows(int od) { return (od + STEP_CL - 1) / STEP_CL; }
+__host__ __device__ inline int step_ldst(int od) { return step_rows(od) | 1; }
+inline size_t step_smem_bytes(int od, int m) {
+  const int B = step_rows(od);
+  return sizeof(double) * (2 * (size_t)B + (size_t)STEP_KC * step_ldst(od) + STEP_CL * (size_t)(m + 1) +
+                           STEP_NPART * STEP_KC + STEP_CL + 32);
+}
 
 template <typename T>
 __global__ void __cluster_dims__(STEP_CL, 1, 1) __launch_bounds__(STEP_NT)
@@ -276,46 +315,49 @@ rhqr_step_kernel(StepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
-  const int c = a.c, m = a.m, ell = a.ell, od = a.od, tid = threadIdx.x;
+  const int c = a.c, m = a.m, od = a.od, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5, nw = STEP_NT / 32;
-  const int blk = (ell + STEP_CL - 1) / STEP_CL;
-  const int i0 = rank * blk, i1 = min(ell, i0 + blk), nown = max(0, i1 - i0);
-  const int nk = c + 1;  // entries of the partial vector: v[0..c-1], s^t y0_{c+1}
-  double* ys = reinterpret_cast<double*>(smem_raw);  // [blk] own sketch rows
-  double* ss = ys + blk;                             // [blk] own s rows
-  double* st = ss + blk;                             // [m] top-block s (rank 0)
-  double* gath = st + m;                             // [STEP_CL * nk] partial vectors (rank 0)
-  double* part = gath + STEP_CL * nk;                // [STEP_CL] rho^2 partials
+  const int B = step_rows(od), ldst = step_ldst(od);
+  const int r0 = rank * B, r1 = min(od, r0 + B), nrow = max(0, r1 - r0);
+  const int nk = c + 1;  // partial vector: v[0..c-1], s^t y0_{c+1}
+  double* yv = reinterpret_cast<double*>(smem_raw);  // [B] sketch rows owned
+  double* sv = yv + B;                               // [B] s rows owned
+  double* stage = sv + B;                            // [STEP_KC][ldst] staged S / y0 block
+  double* gath = stage + (size_t)STEP_KC * ldst;     // [STEP_CL][nk] partial vectors (rank 0)
+  double* cpart = gath + STEP_CL * (m + 1);          // [STEP_NPART][STEP_KC]
+  double* part = cpart + STEP_NPART * STEP_KC;       // [STEP_CL] rho^2 partials
   double* red = part + STEP_CL;                      // [32]
   __shared__ double scal[4];
   pdl_wait();
   pdl_trigger();
-  const bool dead = failed(a.st);  // uniform across the cluster; still take part in syncs
-  // ---- phase A: sketch rows of this CTA (tree over tile leaves, bit-exact)
+  const bool dead = failed(a.st);  // uniform across the cluster; still take part in the sync
+  // ---- phase A: y on the owned rows (identity block given; Omega rows from the tree)
   if (!dead) {
+    for (int i = tid; i < nrow; i += STEP_NT) {
+      const int row = r0 + i;
+      if (row < m || !a.tree) yv[i] = a.y[row];
+    }
     if (a.tree) {
-      for (int i = i0 + warp; i < i1; i += nw) {
-        const int64_t rhi = __ldg(a.idx + i) >> a.log_tb;
-        const A v = warp_tile_tree<T>((const A*)a.P + (int64_t)i * a.n_tiles, (int)a.n_tiles,
+      const int ob = max(r0, m), oe = r1;
+      for (int row = ob + warp; row < oe; row += nw) {
+        const int o = row - m;
+        const int64_t rhi = __ldg(a.idx + o) >> a.log_tb;
+        const A v = warp_tile_tree<T>((const A*)a.P + (int64_t)o * a.n_tiles, (int)a.n_tiles,
                                       (int)a.n_eff, rhi);
         if (lane == 0) {
-          const double yv = (double)Lo<T>::mul(v, (A)a.norm_lo);
-          ys[i - i0] = yv;
-          a.y[m + i] = yv;
+          const double y = (double)Lo<T>::mul(v, (A)a.norm_lo);
+          yv[row - r0] = y;
+          a.y[row] = y;
         }
       }
-    } else {
-      for (int i = i0 + tid; i < i1; i += STEP_NT) ys[i - i0] = a.y[m + i];
     }
   }
   __syncthreads();
   // ---- phase B: rho = ||y[c:]|| (rhqr.py:72); partials pushed to every CTA
   double p = 0.0;
-  if (!dead) {
-    for (int i = tid; i < nown; i += STEP_NT) p = fma(ys[i], ys[i], p);
-    if (rank == 0)
-      for (int r = c + tid; r < m; r += STEP_NT) p = fma(a.y[r], a.y[r], p);
-  }
+  if (!dead)
+    for (int i = tid; i < nrow; i += STEP_NT)
+      if (r0 + i >= c) p = fma(yv[i], yv[i], p);
   p = block_sum(p, red);
   if (tid < STEP_CL) *cluster.map_shared_rank(&part[rank], tid) = p;
   cluster.sync();
@@ -334,70 +376,77 @@ rhqr_step_kernel(StepArgs a) {
     double f, bo;
     if (a.scaling == SQB_SCALE_SQRT2) { f = __dsqrt_rn(beta); bo = 1.0; }
     else { f = gamma; bo = __ddiv_rn(__dmul_rn(sigma, gamma), rho); }
-    scal[0] = sigma; scal[1] = gamma; scal[2] = f; scal[3] = bad ? -1.0 : bo;
+    scal[0] = -sigma * rho; scal[1] = gamma; scal[2] = f; scal[3] = bad ? -1.0 : bo;
     if (rank == 0 && !bad) {
       a.sigmas[c] = sigma; a.rhos[c] = rho; a.betas[c] = bo;
       *a.fscale = f;
-      a.R[c + (int64_t)c * a.ldr] = -sigma * rho;
     }
   }
   __syncthreads();
-  const double gamma = scal[1], f = scal[2], bo = scal[3];
+  const double rdiag = scal[0], gamma = scal[1], f = scal[2], bo = scal[3];
   // a breakdown is seen identically by every CTA: leave together (no more DSMEM)
   if (bo < 0.0) return;
   const bool sq = a.scaling == SQB_SCALE_SQRT2;
-  // ---- phase C: s = Psi u (rhqr.py:83-96) for own rows; rank 0 also the top block
-  for (int i = tid; i < nown; i += STEP_NT) {
-    const double sv = sq ? __dmul_rn(ys[i], f) : __ddiv_rn(ys[i], f);
-    ss[i] = sv;
-    a.S[m + i0 + i + (int64_t)c * a.lds] = sv;
-  }
-  if (rank == 0) {
-    T* U = (T*)a.U;
-    for (int r = tid; r < m; r += STEP_NT) {
-      const double yh = r < c ? 0.0 : (r == c ? gamma : a.y[r]);
-      const double sv = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
-      st[r] = sv;
-      a.S[r + (int64_t)c * a.lds] = sv;
-      U[r + (int64_t)c * a.ldu] = Lo<T>::store(Lo<T>::from_double(sv));  // u top rows
-      if (r != c) a.R[r + (int64_t)c * a.ldr] = r < c ? a.y[r] : 0.0;   // rhqr.py:248
+  // ---- phase C: s = Psi u (rhqr.py:83-96), u's identity-block rows, R column (:248-249)
+  T* U = (T*)a.U;
+  for (int i = tid; i < nrow; i += STEP_NT) {
+    const int row = r0 + i;
+    const double yh = row < c ? 0.0 : (row == c ? gamma : yv[i]);
+    const double s = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
+    sv[i] = s;
+    a.S[row + (int64_t)c * a.lds] = s;
+    if (row < m) {
+      U[row + (int64_t)c * a.ldu] = Lo<T>::store(Lo<T>::from_double(s));
+      a.R[row + (int64_t)c * a.ldr] = row < c ? yv[i] : (row == c ? rdiag : 0.0);
     }
   }
-  __syncthreads();
-  // partial vector: v[k] = S[:, k]^t s (k < c), d = s^t y0_{c+1}; pushed to rank 0
+  // partial vector over the owned rows >= c (s vanishes above c):
+  // v[k] = S[:, k]^t s (k < c), d = s^t y0_{c+1}; staged through smem, pushed to rank 0
   const bool has_next = c + 1 < m;
   const double* y0n = has_next ? a.Y0 + (int64_t)(c + 1) * od : nullptr;
+  const int nkk = has_next ? nk : c;
+  const int rs = max(r0, c), nr = max(0, r1 - rs), ls = rs - r0;
   double* dst0 = cluster.map_shared_rank(gath, 0) + rank * nk;
-  for (int k = warp; k < nk; k += nw) {
-    if (k == c && !has_next) break;
-    const double* col = (k < c) ? a.S + (int64_t)k * a.lds : y0n;
-    double d = 0.0;
-    for (int i = lane; i < nown; i += 32) d = fma(col[m + i0 + i], ss[i], d);
-    if (rank == 0)
-      for (int r = c + lane; r < m; r += 32) d = fma(col[r], st[r], d);  // s[r] = 0 for r < c
-    d = warp_sum(d);
-    if (lane == 0) dst0[k] = d;
+  for (int k0 = 0; k0 < nkk; k0 += STEP_KC) {
+    const int kc = min(STEP_KC, nkk - k0);
+    __syncthreads();
+#pragma unroll 4
+    for (int e = tid; e < nr * kc; e += STEP_NT) {
+      const int i = e % nr, kk = e / nr, k = k0 + kk;
+      const double* col = (k < c) ? a.S + (int64_t)k * a.lds : y0n;
+      stage[kk * ldst + i] = col[rs + i];
+    }
+    __syncthreads();
+    {
+      const int kk = tid % STEP_KC, pp = tid / STEP_KC;
+      double d = 0.0;
+      if (kk < kc)
+        for (int i = pp; i < nr; i += STEP_NPART) d = fma(stage[kk * ldst + i], sv[ls + i], d);
+      cpart[pp * STEP_KC + kk] = d;
+    }
+    __syncthreads();
+    if (tid < kc) {
+      double d = 0.0;
+      for (int q = 0; q < STEP_NPART; ++q) d += cpart[q * STEP_KC + tid];
+      dst0[k0 + tid] = d;
+    }
   }
   cluster.sync();
   if (rank != 0) return;
-  // ---- phase D (rank 0): v_c, and coef_{c+1} = [a_{c+1}; beta (d - v^t a_{c+1})]
+  // ---- phase D (rank 0): v_c, and coef_{c+1}[c] = beta (d - v^t a_{c+1})
   double va = 0.0;
   for (int k = tid; k < c; k += STEP_NT) {
     double v = 0.0;
     for (int q = 0; q < STEP_CL; ++q) v += gath[q * nk + k];
     a.vbuf[k] = v;
-    if (has_next) {
-      const double ak = a.abuf[k];
-      a.coef[k] = ak;
-      va = fma(v, ak, va);
-    }
+    if (has_next) va = fma(v, a.anext[k], va);
   }
   if (!has_next) return;
   va = block_sum(va, red);
   if (tid == 0) {
     double d = 0.0;
     for (int q = 0; q < STEP_CL; ++q) d += gath[q * nk + c];
-    a.coef[c] = __dmul_rn(bo, d - va);
+    a.clast[c + 1] = __dmul_rn(bo, d - va);
   }
 }
 
@@ -447,7 +496,7 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
   const size_t iY0 = plan.add(sizeof(double) * od * m);
   const size_t iy = plan.add(sizeof(double) * od);
   const size_t icoef = plan.add(sizeof(double) * (m + 1));
-  const size_t iabuf = plan.add(sizeof(double) * (m + 1));
+  const size_t iabuf = plan.add(sizeof(double) * 2 * (m + 1));
   const size_t ivbuf = plan.add(sizeof(double) * (m + 1));
   const size_t ifs = plan.add(sizeof(double) * 2);
   const size_t iP = plan.add(std::max(sketch_partials_bytes(sk, Lo<T>::code, chunk),
@@ -474,14 +523,13 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
   double scale_lo = 0.0, norm_lo = 0.0;
   if (srht) srht_constants(sk, Lo<T>::code, &scale_lo, &norm_lo);
 
-  const size_t step_smem = sizeof(double) * (2 * ((ell + STEP_CL - 1) / STEP_CL) + m +
-                                             STEP_CL * (m + 1) + STEP_CL + 32);
+  const size_t step_smem = step_smem_bytes((int)od, (int)m);
   cudaFuncSetAttribute(rhqr_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(step_smem, 48 * 1024));
   // column 0: y = y0_0 (w = W[:, 0]); a_1 is empty
   StepArgs sa{0, (int)m, (int)ell, (int)od, scaling, 0, P, g.n_tiles, g.n_eff,
               srht ? sk->indices : nullptr, g.log_tb, norm_lo, Y0, Y0, S, lds, R, ldr, U, ldu,
-              sigmas, rhos, betas, fs, vbuf, abuf, coef, st};
+              sigmas, rhos, betas, fs, vbuf, abuf + (1 & 1) * (m + 1), coef, st};
   SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT),
                      step_smem, sa));
 
@@ -498,9 +546,11 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
   auto colk = vec ? rhqr_col_kernel<T, VN> : rhqr_col_kernel<T, 1>;
   cudaFuncSetAttribute(colk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
   for (int64_t c = 1; c < m; ++c) {
+    double* a_cur = abuf + (c & 1) * (m + 1);
+    double* a_nxt = abuf + ((c + 1) & 1) * (m + 1);
     ColArgs ca{(int)c, (int)m, n, (int)ell, (int)od, log_tb_col, g.n_tiles, n_eff_col, W, ldw, U, ldu,
-               coef, fs, scaling, srht ? 1 : 0, srht ? sk->sign_bits : nullptr,
-               srht ? sk->indices : nullptr, scale_lo, P, y, S, lds, Tm, ldt, Y0, vbuf, betas, abuf,
+               a_cur, coef, fs, scaling, srht ? 1 : 0, srht ? sk->sign_bits : nullptr,
+               srht ? sk->indices : nullptr, scale_lo, P, y, S, lds, Tm, ldt, Y0, vbuf, betas, a_nxt,
                st};
     const size_t smem = sizeof(A) * ((c + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(c + 1));
     prof_begin(ctx);
@@ -513,6 +563,7 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
                             m, P, st));
     sa.c = (int)c;
     sa.y = y;
+    sa.anext = a_nxt;
     sa.tree = srht ? 1 : 0;
     SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT),
                        step_smem, sa));

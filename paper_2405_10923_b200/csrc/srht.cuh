@@ -116,6 +116,9 @@ __device__ __forceinline__ void tile_gather(const typename Lo<T>::acc* sm, const
 // by lane (t & 31), slot (t >> 5): the low 5 tree levels are lane shuffles,
 // the upper levels a sequential binary-counter tree over slots — both in
 // level order, left operand = lower tile index.
+// Slots are consumed in chunks of up to 8 whose loads are all issued before
+// any arithmetic (8 loads in flight per lane); the in-chunk levels run on
+// registers, chunks combine through a binary-counter stack.
 template <typename T>
 __device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<T>::acc* leaves,
                                                               int n_tiles, int n_eff, int64_t rhi) {
@@ -123,26 +126,52 @@ __device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<
   const int lane = threadIdx.x & 31;
   int low_levels = 0;
   while ((1 << low_levels) < n_tiles && low_levels < 5) ++low_levels;
-  const int slots = n_tiles > 32 ? (n_tiles >> 5) : 1;
+  const int slots = n_tiles > 32 ? (n_tiles >> 5) : 1;  // power of two
+  const int ch = slots < 8 ? slots : 8;
+  int lch = 0;
+  while ((1 << lch) < ch) ++lch;
   A stk[16];
-  for (int j = 0; j < slots; ++j) {
-    const int t = lane + (j << 5);
-    A v = (t < n_eff) ? leaves[t] : A(0);
-    for (int l = 0; l < low_levels; ++l) {
-      const A o = __shfl_xor_sync(0xffffffffu, v, 1 << l);
-      const bool upper = (lane >> l) & 1;
-      const A a = upper ? o : v, b = upper ? v : o;
-      v = ((rhi >> l) & 1) ? Lo<T>::sub(a, b) : Lo<T>::add(a, b);
+  for (int j0 = 0; j0 < slots; j0 += ch) {
+    A v[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int t = lane + ((j0 + jj) << 5);
+      v[jj] = (jj < ch && t < n_eff) ? leaves[t] : A(0);
     }
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      if (jj < ch) {
+        A x = v[jj];
+        for (int l = 0; l < low_levels; ++l) {
+          const A o = __shfl_xor_sync(0xffffffffu, x, 1 << l);
+          const bool upper = (lane >> l) & 1;
+          const A a = upper ? o : x, b = upper ? x : o;
+          x = ((rhi >> l) & 1) ? Lo<T>::sub(a, b) : Lo<T>::add(a, b);
+        }
+        v[jj] = x;
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      if ((1 << l) < ch) {
+        const bool neg = (rhi >> (5 + l)) & 1;
+#pragma unroll
+        for (int jj = 0; jj < 8; jj += (2 << l))
+          if (jj + (1 << l) < ch)
+            v[jj] = neg ? Lo<T>::sub(v[jj], v[jj + (1 << l)]) : Lo<T>::add(v[jj], v[jj + (1 << l)]);
+      }
+    }
+    A cv = v[0];
+    const int q = j0 >> lch;
     int lvl = 0;
-    while ((j >> lvl) & 1) {
-      v = ((rhi >> (5 + lvl)) & 1) ? Lo<T>::sub(stk[lvl], v) : Lo<T>::add(stk[lvl], v);
+    while ((q >> lvl) & 1) {
+      cv = ((rhi >> (5 + lch + lvl)) & 1) ? Lo<T>::sub(stk[lvl], cv) : Lo<T>::add(stk[lvl], cv);
       ++lvl;
     }
-    stk[lvl] = v;
+    stk[lvl] = cv;
   }
   int top = 0;
-  while ((1 << top) < slots) ++top;
+  while ((ch << top) < slots) ++top;
   return __shfl_sync(0xffffffffu, stk[top], 0);
 }
 

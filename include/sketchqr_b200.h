@@ -124,6 +124,17 @@ int sqb_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
                   double* T, int64_t ldt, double* R, int64_t ldr,
                   double* sigmas, double* rhos, double* betas);
 
+/* Reconstructed RHQR (rec_rhqr, rhqr.py:368-395): one sketch Z = Psi W,
+ * Householder QR of Z in fp64 (baselines.py:33-89), Mfac = triu(T^t S^t Z)
+ * (zero diagonal -> SQB_ERR_BREAKDOWN with val = -1), U2 = W2 Mfac^{-1} by
+ * forward substitution (right_tri_solve, linalg.py:119-129), U = [S[:m]; U2].
+ * Same operands as sqb_rhqr_left. */
+int sqb_rec_rhqr(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                 const void* W, int64_t N, int64_t m, int64_t ldw,
+                 void* U, int64_t ldu, double* S, int64_t lds,
+                 double* T, int64_t ldt, double* R, int64_t ldr,
+                 double* sigmas, double* rhos, double* betas);
+
 /* (I - U T S^t Psi) X, or with transpose_t the reflectors in reverse
  * (apply_reflectors_compact, rhqr.py:100-119).  U: N x r (lo), S: (m+ell) x r,
  * T: r x r, X/Out: N x k (lo).  Out may alias X. */

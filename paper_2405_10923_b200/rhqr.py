@@ -81,6 +81,10 @@ def raise_status(ctx, what="factorization"):
     if code == _lib.SQB_OK:
         return
     if code == _lib.SQB_ERR_BREAKDOWN:
+        if what == "rec_rhqr":
+            if val == -1.0:  # rhqr.py:388-391
+                raise BreakdownError(f"reconstruction factor has zero diagonal at column {col}")
+            raise BreakdownError(f"column {col} exactly dependent on its predecessors")  # baselines.py:62
         if val == 0.0:
             raise BreakdownError(f"sketched tail annihilated at column {col}")
         raise BreakdownError(f"reflector scale degenerated at column {col} (rho={val:.3e})")
@@ -131,6 +135,34 @@ def rhqr_left(W, omega, scaling=SCALE_SQRT2, policy=None):
     return RHQRFactors(U=_out(U, host), S=_out(S, host), T=_out(T, host), R=_out(R, host), psi=psi,
                        scaling=scaling, sigmas=_out(sg, host), rhos=_out(rh, host),
                        betas=_out(bt, host))
+
+
+def rec_rhqr(W, omega, scaling=SCALE_SQRT2, policy=None):
+    """rhqr.py:368-395: one sketch of W, Householder QR of the sketch in the
+    high precision, triangular reconstruction of the n-dimensional reflectors."""
+    check_scaling(scaling)
+    policy = policy or DOUBLE_POLICY
+    require_device_policy(policy)
+    host = not is_device(W)
+    n, m = _shape2(W)
+    psi = _embed(omega, n, m)
+    tag = policy.low
+    Wd = to_device(W, tag, align_row=m)
+    od = psi.out_dim
+    U = empty_colmajor(n, m, tag, align_row=m)
+    S = empty_colmajor(od, m, "double")
+    T = empty_colmajor(m, m, "double")
+    R = empty_colmajor(m, m, "double")
+    scal = torch.empty(3 * m, dtype=torch.float64, device=Wd.device)
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_rec_rhqr(
+        ctx.h, psi.omega.desc(), scaling_code(scaling), CODES[tag], Wd.data_ptr(), n, m, ld_of(Wd),
+        U.data_ptr(), ld_of(U), S.data_ptr(), ld_of(S), T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R),
+        scal.data_ptr(), scal.data_ptr() + 8 * m, scal.data_ptr() + 16 * m), "sqb_rec_rhqr")
+    raise_status(ctx, "rec_rhqr")
+    return RHQRFactors(U=_out(U, host), S=_out(S, host), T=_out(T, host), R=_out(R, host), psi=psi,
+                       scaling=scaling, sigmas=_out(scal[:m], host), rhos=_out(scal[m:2 * m], host),
+                       betas=_out(scal[2 * m:], host))
 
 
 def rh_vector(w, y, j, scaling=SCALE_SQRT2, policy=None):
@@ -227,6 +259,6 @@ def sketch_q(factors):
     return _out(Q, host)
 
 
-__all__ = ["HouseholderStep", "RHQRFactors", "rh_vector", "rhqr_left", "apply_reflectors_compact",
+__all__ = ["HouseholderStep", "RHQRFactors", "rh_vector", "rhqr_left", "rec_rhqr", "apply_reflectors_compact",
            "thin_q", "sketch_q", "SCALE_SQRT2", "SCALE_UNIT", "raise_status", "_embed"]
 _ = C

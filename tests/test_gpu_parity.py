@@ -254,3 +254,70 @@ def test_config2_shape_reduced_rows_against_oracle(P):
     # any implementation (the oracle under 1e-16 input perturbations)
     assert P.cond_number(Q) == pytest.approx(O.cond_number(Qo), rel=2e-3)
     assert P.orthogonality_error(SQ) == pytest.approx(O.orthogonality_error(SQo), abs=1e-13)
+
+
+# ---------------------------------------------------------------- recRHQR (config 3)
+def test_rec_rhqr_matches_reference(P):
+    g = golden("rec_rhqr_cmatrix_4096x16")
+    W = workloads.gen_cmatrix(4096, 16)
+    F = P.rec_rhqr(W, P.GaussianSketch(64, 4096 - 16, 41))
+    for k in ("S", "T", "R", "U"):
+        assert rel(getattr(F, k), g[k]) < 1e-10, k
+    assert np.allclose(F.sigmas, g["sigmas"])
+
+
+def test_rec_rhqr_identity_block_and_left_agreement(P):
+    n, m, ell = 20, 4, 8
+    W = np.zeros((n, m))
+    W[:m] = np.eye(m)
+    F = P.rec_rhqr(W, P.GaussianSketch(ell, n - m, 24))
+    Z = np.zeros((ell + m, m))
+    Z[:m] = np.eye(m)
+    _, R, aux = O.householder_qr(Z)
+    assert np.allclose(F.U[m:], 0.0, atol=1e-13) and np.allclose(F.R, R, atol=1e-13)
+    assert np.allclose(F.S, aux["U"], atol=1e-13)
+    rng = np.random.default_rng(3)
+    W = rng.standard_normal((30, 5))
+    om = P.GaussianSketch(12, 25, 26)
+    Fr, Fl = P.rec_rhqr(W, om), P.rhqr_left(W, om)
+    assert np.allclose(Fr.U, Fl.U, atol=1e-10 * np.linalg.norm(Fl.U))
+    assert np.allclose(Fr.R, Fl.R, atol=1e-10 * np.linalg.norm(Fl.R))
+
+
+@pytest.mark.parametrize("m,kind", [(16, "srht"), (48, "gauss"), (80, "srht")])
+def test_rec_rhqr_against_oracle(P, m, kind):
+    N = 1 << 14
+    W = workloads.gen_cmatrix(N, m)
+    ell = 4 * m
+    mk = {"srht": (P.SRHTSketch, O.SRHT), "gauss": (P.GaussianSketch, O.Gaussian)}[kind]
+    F = P.rec_rhqr(W, mk[0](ell, N - m, 5))
+    Fo = O.rec_rhqr(W, mk[1](ell, N - m, 5))
+    assert rel(F.R, Fo.R) < 1e-10
+    assert rel(F.U, Fo.U) < 1e-9
+    Q = P.thin_q(F)
+    assert P.factorization_errors(W, Q, F.R).fro_rel_err < 1e-12
+
+
+def test_rec_rhqr_config3_full_size(P):
+    """BASELINE config 3: gen_cmatrix(2^22, 64), Gaussian ell=256 (G = 8.6 GB,
+    generated host-side with the reference's per-row Philox streams)."""
+    N, m, ell = 1 << 22, 64, 256
+    W = workloads.gen_cmatrix(N, m)
+    om = P.GaussianSketch(ell, N - m, 3)
+    F = P.rec_rhqr(W, om)
+    Q = P.thin_q(F)
+    assert P.factorization_errors(W, Q, F.R).fro_rel_err < 1e-12
+    assert P.orthogonality_error(P.sketch_q(F)) < 1e-12
+    c = P.cond_number(Q)
+    assert 1.0 < c < 10.0
+
+
+def test_rec_rhqr_breakdown_message(P):
+    # both leading columns live in the identity block: Z's second column is
+    # exactly dependent (the oracle raises the same message)
+    W = np.zeros((40, 3))
+    W[0, 0] = 1.0
+    W[0, 1] = 1.0
+    W[:, 2] = np.arange(40.0)
+    with pytest.raises(P.BreakdownError, match="column 2 exactly dependent"):
+        P.rec_rhqr(W, P.GaussianSketch(12, 37, 1))

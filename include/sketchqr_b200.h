@@ -78,6 +78,29 @@ typedef struct sqb_sketch {
 
 typedef struct sqb_ctx sqb_ctx;
 
+/* Linear operator for the Krylov driver (krylov.py:28-35 accepts a callable,
+ * a scipy sparse matrix or a dense array). */
+enum sqb_operator_kind { SQB_OP_CSR = 0, SQB_OP_DENSE = 1, SQB_OP_CALLBACK = 2 };
+/* Callback operator: the library writes x (n values of the low dtype) into
+ * the caller's device buffer `xbuf`, calls cb(user, stream), and reads the
+ * float64 product A x from the caller's device buffer `ybuf`.  The callback
+ * must enqueue its work on `stream` and return 0. */
+typedef int (*sqb_matvec_cb)(void* user, void* stream);
+typedef struct sqb_operator {
+  int32_t kind;             /* sqb_operator_kind */
+  int32_t reserved;
+  int64_t n;                /* A is n x n */
+  const int64_t* indptr;    /* CSR, device: n+1 */
+  const int32_t* indices;   /* CSR, device: nnz */
+  const double* data;       /* CSR, device: nnz */
+  const double* A;          /* DENSE, device, row-major */
+  int64_t lda;
+  sqb_matvec_cb cb;         /* CALLBACK */
+  void* user;
+  void* xbuf;               /* CALLBACK: n values of the low dtype (device) */
+  double* ybuf;             /* CALLBACK: n doubles (device) */
+} sqb_operator;
+
 /* ---- context ------------------------------------------------------------ */
 int sqb_version(void);
 int sqb_ctx_create(int device, void* stream, sqb_ctx** out);
@@ -174,6 +197,38 @@ int sqb_residual_norms(sqb_ctx* ctx, const double* W, int64_t ldw, const double*
 int sqb_rh_vector(sqb_ctx* ctx, int scaling, int lo_dtype, const void* w, int64_t n,
                   const double* y, int64_t od, int64_t j, void* u, double* s,
                   double* scalars);
+
+/* RHQR-Arnoldi (rhqr_arnoldi, krylov.py:82-150): m steps of the Krylov basis
+ * of (A, b - A x0) in compact reflector form.  b: n doubles; x0lo: n values
+ * already rounded to lo_dtype; outputs U (n x (m+1), lo_dtype), S
+ * ((m+1+ell) x (m+1)), T ((m+1)^2), H ((m+1) x m), optional Q (n x m fp64,
+ * krylov.py:139; pass NULL when store_q is false), beta (device double).
+ * Omega must take n-m-1 coordinates.  happy_tol: krylov.py:101-102.
+ * Synchronises once at the end; *attained = -1 for a full run, else the
+ * dimension at which the space closed. */
+int sqb_rhqr_arnoldi(sqb_ctx* ctx, const sqb_sketch* sk, const sqb_operator* A, int m,
+                     int scaling, int lo_dtype, double happy_tol, const double* b,
+                     const void* x0lo, void* U, int64_t ldu, double* S, int64_t lds,
+                     double* T, int64_t ldt, double* H, int64_t ldh, double* Q, int64_t ldq,
+                     double* beta, int* attained);
+
+/* min_y ||beta e1 - H y|| by Givens rotations (hessenberg_lstsq,
+ * krylov.py:153-190): H is p x k (p = k+1 normally), outputs y (k), the
+ * residual history (k+1) and the final residual; work >= p*k + p doubles. */
+int sqb_hessenberg_lstsq(sqb_ctx* ctx, const double* H, int64_t ldh, int64_t p, int64_t k,
+                         double beta, double* y, double* hist, double* resid, double* work);
+
+/* Basis columns q_1..q_c from the compact form: Q = [I;0] - U (T S[:c, :]^t)
+ * (arnoldi_q, krylov.py:64-79).  U: N x r (lo_dtype), S: od x r, T: r x r. */
+int sqb_arnoldi_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t r,
+                  const double* T, int64_t ldt, const double* S, int64_t lds, int64_t c,
+                  double* Q, int64_t ldq);
+
+/* y = lo(b - A x) (bsub != NULL) or lo(A x): CSR SpMV, row sums in CSR order
+ * with separate mul/add roundings (scipy's csr_matvec). */
+int sqb_csr_spmv(sqb_ctx* ctx, int dtype, int64_t n, const int64_t* indptr,
+                 const int32_t* indices, const double* data, const void* x,
+                 const double* bsub, void* y);
 
 #ifdef __cplusplus
 }

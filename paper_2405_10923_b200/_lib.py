@@ -32,6 +32,17 @@ class SketchDesc(C.Structure):
     ]
 
 
+SQB_OP_CSR, SQB_OP_DENSE, SQB_OP_CALLBACK = 0, 1, 2
+MATVEC_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
+
+
+class OperatorDesc(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32), ("reserved", C.c_int32), ("n", i64), ("indptr", vp), ("indices", vp),
+        ("data", vp), ("A", vp), ("lda", i64), ("cb", MATVEC_CB), ("user", vp), ("xbuf", vp), ("ybuf", vp),
+    ]
+
+
 # name -> (argtypes, restype); every export returns int unless stated
 _SIGS = {
     "sqb_version": ([], C.c_int),
@@ -56,6 +67,12 @@ _SIGS = {
     "sqb_gram": ([vp, dp, i64, i64, i64, dp, i64], C.c_int),
     "sqb_sketch_q": ([vp, C.c_int, dp, i64, i64, dp, i64, dp, i64, i64, dp, i64], C.c_int),
     "sqb_residual_norms": ([vp, dp, i64, dp, i64, dp, i64, i64, i64, i64, dp], C.c_int),
+    "sqb_rhqr_arnoldi": ([vp, C.POINTER(SketchDesc), C.POINTER(OperatorDesc), C.c_int, C.c_int, C.c_int,
+                          C.c_double, dp, dp, dp, i64, dp, i64, dp, i64, dp, i64, dp, i64, dp,
+                          C.POINTER(C.c_int)], C.c_int),
+    "sqb_hessenberg_lstsq": ([vp, dp, i64, i64, i64, C.c_double, dp, dp, dp, dp], C.c_int),
+    "sqb_csr_spmv": ([vp, C.c_int, i64, dp, dp, dp, dp, dp, dp], C.c_int),
+    "sqb_arnoldi_q": ([vp, C.c_int, dp, i64, i64, i64, dp, i64, dp, i64, i64, dp, i64], C.c_int),
     "sqb_rh_vector": ([vp, C.c_int, C.c_int, dp, i64, dp, i64, i64, dp, dp, dp], C.c_int),
 }
 

@@ -9,7 +9,7 @@ int rhqr_left_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64
                        double*, double*);
 int apply_reflectors_dispatch(sqb_ctx*, const sqb_sketch*, int64_t, int, const void*, int64_t, int64_t,
                               int64_t, const double*, int64_t, const double*, int64_t, int, const void*,
-                              int64_t, int64_t, void*, int64_t);
+                              int64_t, int64_t, void*, int64_t, void*);
 int thin_q_dispatch(sqb_ctx*, int, const void*, int64_t, int64_t, int64_t, const double*, int64_t,
                     double*, int64_t);
 int gram_run(sqb_ctx*, const double*, int64_t, int64_t, int64_t, double*, int64_t);
@@ -181,7 +181,7 @@ int sqb_apply_reflectors(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, int lo_d
   if (sk->n != N - m) return set_error(ctx, SQB_ERR_ARG, "embedding is %lld x %lld, operand has %lld rows",
                                        (long long)(m + sk->ell), (long long)(m + sk->n), (long long)N);
   return apply_reflectors_dispatch(ctx, sk, m, lo_dtype, U, ldu, N, r, S, lds, T, ldt, transpose_t, X,
-                                   ldx, k, Out, ldo);
+                                   ldx, k, Out, ldo, nullptr);
 }
 
 int sqb_thin_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t k,

@@ -88,6 +88,9 @@ struct Status {
   double val; // diagnostic value (rho, diagonal entry, ...)
 };
 
+// internal status: the Krylov space closed (happy breakdown), krylov.py:115-125
+constexpr int SQB_CLOSED = 100;
+
 __device__ __forceinline__ bool failed(const Status* st) {
   return *((volatile const int*)&st->code) != SQB_OK;
 }

@@ -59,15 +59,18 @@ template <typename T>
 static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, const void* U,
                               int64_t ldu, int64_t N, int64_t r, const double* S, int64_t lds,
                               const double* Tm, int64_t ldt, int transpose_t, const void* X,
-                              int64_t ldx, int64_t k, void* Out, int64_t ldo) {
+                              int64_t ldx, int64_t k, void* Out, int64_t ldo, void* ws_base) {
   const int64_t od = m + sk->ell;
   WsPlan plan;
   const size_t iY = plan.add(sizeof(double) * od * k);
   const size_t iC = plan.add(sizeof(double) * std::max<int64_t>(r, 1) * k);
   const size_t iP = plan.add(sketch_partials_bytes(sk, Lo<T>::code, k));
-  SQB_TRY(ws_reserve(ctx, plan.total));
-  double* Y = ws_ptr<double>(ctx, plan, iY);
-  double* C = ws_ptr<double>(ctx, plan, iC);
+  if (!ws_base) {
+    SQB_TRY(ws_reserve(ctx, plan.total));
+    ws_base = ctx->ws;
+  }
+  double* Y = reinterpret_cast<double*>(static_cast<char*>(ws_base) + plan.offs[iY]);
+  double* C = reinterpret_cast<double*>(static_cast<char*>(ws_base) + plan.offs[iC]);
   const Status* st = ctx->d_status;
   if (r == 0) {  // no reflectors: Out = X
     if (Out != X)
@@ -77,7 +80,7 @@ static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, con
   }
   SQB_TRY(launch_copy_top(ctx, Lo<T>::code, X, ldx, m, k, Y, od, st));
   SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const T*)X + m, ldx, k, Y, od, m,
-                        ws_ptr<void>(ctx, plan, iP), st));
+                        static_cast<char*>(ws_base) + plan.offs[iP], st));
   coef_kernel<<<(unsigned)k, 256, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od,
                                                                      (int)od, (int)r, C, r, st);
   SQB_TRY(check_launch(ctx, "coef_kernel"));
@@ -87,15 +90,24 @@ static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, con
   return check_launch(ctx, "update_kernel");
 }
 
+size_t apply_reflectors_ws_bytes(const sqb_sketch* sk, int dtype, int64_t m, int64_t r, int64_t k) {
+  WsPlan plan;
+  plan.add(sizeof(double) * (m + sk->ell) * k);
+  plan.add(sizeof(double) * std::max<int64_t>(r, 1) * k);
+  plan.add(sketch_partials_bytes(sk, dtype, k));
+  return plan.total + 256;
+}
+
 int apply_reflectors_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, int lo_dtype,
                               const void* U, int64_t ldu, int64_t N, int64_t r, const double* S,
                               int64_t lds, const double* Tm, int64_t ldt, int transpose_t,
-                              const void* X, int64_t ldx, int64_t k, void* Out, int64_t ldo) {
+                              const void* X, int64_t ldx, int64_t k, void* Out, int64_t ldo,
+                              void* ws_base) {
   switch (lo_dtype) {
-    case SQB_F64: return apply_reflectors_t<double>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo);
-    case SQB_F32: return apply_reflectors_t<float>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo);
-    case SQB_F16: return apply_reflectors_t<__half>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo);
-    case SQB_BF16: return apply_reflectors_t<__nv_bfloat16>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo);
+    case SQB_F64: return apply_reflectors_t<double>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo, ws_base);
+    case SQB_F32: return apply_reflectors_t<float>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo, ws_base);
+    case SQB_F16: return apply_reflectors_t<__half>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo, ws_base);
+    case SQB_BF16: return apply_reflectors_t<__nv_bfloat16>(ctx, sk, m, U, ldu, N, r, S, lds, Tm, ldt, transpose_t, X, ldx, k, Out, ldo, ws_base);
   }
   return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
 }
@@ -296,3 +308,71 @@ int sketch_q_run(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t
 }
 
 }  // namespace sqb
+
+namespace sqb {
+
+// M[i, j] = sum_{l >= i} T[i, l] S[j, l]  (r x c), i.e. T S[:c, :]^t (arnoldi_q, krylov.py:77)
+__global__ void ts_kernel(const double* __restrict__ Tm, int64_t ldt, const double* __restrict__ S,
+                          int64_t lds, int r, int c, double* __restrict__ M) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < r * c; e += gridDim.x * blockDim.x) {
+    const int i = e % r, j = e / r;
+    double d = 0.0;
+    for (int l = i; l < r; ++l) d = fma(Tm[i + (int64_t)l * ldt], S[j + (int64_t)l * lds], d);
+    M[i + (int64_t)j * r] = d;
+  }
+}
+
+// Q = [I;0] - U M with U (N x r, lo) and M (r x c): one thread per row, M in smem
+template <typename T>
+__global__ void __launch_bounds__(256)
+compact_q_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int r, int c, const double* __restrict__ M,
+                 double* __restrict__ Q, int64_t ldq) {
+  extern __shared__ double sM[];
+  for (int e = threadIdx.x; e < r * c; e += blockDim.x) sM[e] = M[e];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int j = 0; j < c; ++j) {
+      double d = 0.0;
+      for (int l = 0; l < r; ++l) d = fma((double)Lo<T>::load(U[i + (int64_t)l * ldu]), sM[l + j * r], d);
+      Q[i + (int64_t)j * ldq] = (i == j ? 1.0 : 0.0) - d;
+    }
+  }
+}
+
+template <typename T>
+static int arnoldi_q_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int64_t r, const double* Tm,
+                       int64_t ldt, const double* S, int64_t lds, int64_t c, double* Q, int64_t ldq) {
+  WsPlan plan;
+  const size_t iM = plan.add(sizeof(double) * std::max<int64_t>(1, r * c));
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  double* M = ws_ptr<double>(ctx, plan, iM);
+  ts_kernel<<<(unsigned)std::max<int64_t>(1, (r * c + 255) / 256), 256, 0, ctx->stream>>>(Tm, ldt, S, lds,
+                                                                                          (int)r, (int)c, M);
+  SQB_TRY(check_launch(ctx, "ts_kernel"));
+  const size_t smem = sizeof(double) * std::max<int64_t>(1, r * c);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(compact_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  compact_q_kernel<T><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 4 * 148)), 256, smem,
+                        ctx->stream>>>((const T*)U, ldu, N, (int)r, (int)c, M, Q, ldq);
+  return check_launch(ctx, "compact_q_kernel");
+}
+
+}  // namespace sqb
+
+extern "C" int sqb_arnoldi_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t r,
+                             const double* T, int64_t ldt, const double* S, int64_t lds, int64_t c, double* Q,
+                             int64_t ldq) {
+  using namespace sqb;
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  if (c < 0 || c > r) return set_error(ctx, SQB_ERR_ARG, "have %lld reflectors, cannot build %lld columns",
+                                       (long long)r, (long long)c);
+  if ((int64_t)r * c * 8 > 200 * 1024) return set_error(ctx, SQB_ERR_ARG, "arnoldi_q: r*c too large");
+  switch (lo_dtype) {
+    case SQB_F64: return arnoldi_q_t<double>(ctx, U, ldu, N, r, T, ldt, S, lds, c, Q, ldq);
+    case SQB_F32: return arnoldi_q_t<float>(ctx, U, ldu, N, r, T, ldt, S, lds, c, Q, ldq);
+    case SQB_F16: return arnoldi_q_t<__half>(ctx, U, ldu, N, r, T, ldt, S, lds, c, Q, ldq);
+    case SQB_BF16: return arnoldi_q_t<__nv_bfloat16>(ctx, U, ldu, N, r, T, ldt, S, lds, c, Q, ldq);
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}

@@ -1,0 +1,519 @@
+// RHQR-Arnoldi and GMRES on the device (krylov.py:82-222).
+//
+// Per Arnoldi step j (krylov.py:113-143) the host enqueues, without any sync:
+//   arn_step_kernel   happy-breakdown test, rh_vector on z (rhqr.py:51-97),
+//                     S/T columns (_extend_t), the Hessenberg column, and the
+//                     q-coefficients T_j S_j[j-1, :]^t                (1 CTA)
+//   arn_q_kernel      q = e_j - U_j coef (GEMV over U_j) with the lazy scaling
+//                     of U[:, j-1] (u = f w on the Omega rows)
+//   matvec            w = lo(A lo(q)): CSR SpMV kernel (row sums in CSR order,
+//                     unfused mul/add like scipy's csr_matvec), dense DMMA, or
+//                     a host callback that enqueues on the stream
+//   compact apply     w = (I - U T^t S^t Psi) w   (rhqr.py:100-119, transpose_t)
+//   z = Psi w
+// A closed Krylov space is recorded in the device status word (SQB_CLOSED);
+// every later kernel of the chain is then a no-op.  One sync at the end.
+#include <algorithm>
+#include <cfloat>
+
+#include "pdl.cuh"
+#include "sketch.cuh"
+#include "vec.cuh"
+#include "dense.cuh"
+
+namespace sqb {
+
+int apply_reflectors_dispatch(sqb_ctx*, const sqb_sketch*, int64_t, int, const void*, int64_t, int64_t,
+                              int64_t, const double*, int64_t, const double*, int64_t, int, const void*,
+                              int64_t, int64_t, void*, int64_t, void*);
+size_t apply_reflectors_ws_bytes(const sqb_sketch* sk, int dtype, int64_t m, int64_t r, int64_t k);
+
+template <typename T>
+__global__ void scale_col_kernel(T* __restrict__ u, int64_t n, int mt, const double* fscale, int scaling,
+                                 const Status* st) {
+  if (st && failed(st) && st->code != SQB_CLOSED) return;
+  const double f = *fscale;
+  for (int64_t i = mt + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = (double)Lo<T>::load(u[i]);
+    u[i] = Lo<T>::store(Lo<T>::from_double(scaling == SQB_SCALE_SQRT2 ? __dmul_rn(v, f) : __ddiv_rn(v, f)));
+  }
+}
+
+constexpr int ARN_NT = 512;
+
+// ---------------------------------------------------------------------------
+// CSR SpMV: y = lo(b - A x) or lo(A x); x in the low dtype, A in fp64.
+// Row sums run in CSR order with separate mul/add roundings, as scipy's
+// csr_matvec (sum += Ax[jj] * Xx[Aj[jj]]) does.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256)
+csr_spmv_kernel(int64_t n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                const double* __restrict__ data, const T* __restrict__ x, const double* __restrict__ bsub,
+                T* __restrict__ y, double* __restrict__ y64, const Status* st) {
+  if (st && failed(st)) return;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p0 = __ldg(indptr + r), p1 = __ldg(indptr + r + 1);
+    double s = 0.0;
+    for (int64_t p = p0; p < p1; ++p)
+      s = __dadd_rn(s, __dmul_rn(__ldg(data + p), (double)Lo<T>::load(x[__ldg(indices + p)])));
+    if (bsub) s = __dsub_rn(bsub[r], s);
+    if (y64) y64[r] = s;
+    y[r] = Lo<T>::store(Lo<T>::from_double(s));
+  }
+}
+
+// y = lo(b - r64) (initial residual when the product came from a dense/callback operator)
+template <typename T>
+__global__ void resid_kernel(int64_t n, const double* __restrict__ b, const double* __restrict__ r64,
+                             T* __restrict__ y, const Status* st) {
+  if (st && failed(st)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = Lo<T>::store(Lo<T>::from_double(b[i] - r64[i]));
+}
+
+template <typename T>
+__global__ void round_kernel(int64_t n, const double* __restrict__ src, T* __restrict__ dst, const Status* st) {
+  if (st && failed(st)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = Lo<T>::store(Lo<T>::from_double(src[i]));
+}
+
+template <typename T>
+__global__ void widen_kernel(int64_t n, const T* __restrict__ src, double* __restrict__ dst, const Status* st) {
+  if (st && failed(st)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (double)Lo<T>::load(src[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Arnoldi step j (1-based) on z = Psi w (krylov.py:114-139)
+// ---------------------------------------------------------------------------
+struct ArnArgs {
+  int j, m, mt, od;        // mt = m + 1 identity-block rows; od = mt + ell
+  int scaling;
+  double happy_tol;
+  const double* z;         // (od)
+  double* S; int64_t lds;  // od x (m+1)
+  double* T; int64_t ldt;  // (m+1) x (m+1)
+  double* H; int64_t ldh;  // (m+1) x m
+  void* U; int64_t ldu;    // identity-block rows of U[:, j-1]
+  double* beta;            // [1]
+  double* fscale;          // [1] f of U[:, j-1]
+  double* coefq;           // [j] T_j S_j[j-1, :]^t
+  Status* st;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(ARN_NT) arn_step_kernel(ArnArgs a) {
+  extern __shared__ double sm[];
+  double* s = sm;           // [od]
+  double* v = s + a.od;     // [m+1]
+  double* red = v + a.mt;   // [32]
+  __shared__ double scal[4];
+  if (failed(a.st)) return;
+  const int j = a.j, jj = j - 1, od = a.od, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = ARN_NT / 32;
+  // happy breakdown test: ||z[j-1:]|| <= tol ||z||  (krylov.py:115-125)
+  double pt = 0.0, pf = 0.0;
+  for (int r = tid; r < od; r += ARN_NT) {
+    const double zz = a.z[r] * a.z[r];
+    pf += zz;
+    if (r >= jj) pt += zz;
+  }
+  const double tail = sqrt(block_sum(pt, red));
+  const double full = sqrt(block_sum(pf, red));
+  if (tail <= a.happy_tol * full) {
+    if (j >= 2) {
+      for (int r = tid; r < jj; r += ARN_NT) a.H[r + (int64_t)(j - 2) * a.ldh] = a.z[r];
+      if (tid == 0) {
+        const double sg = a.z[jj] >= 0.0 ? 1.0 : -1.0;
+        a.H[jj + (int64_t)(j - 2) * a.ldh] = -sg * tail;
+      }
+    }
+    if (tid == 0) fail(a.st, SQB_CLOSED, j - 1, tail);
+    return;
+  }
+  // rh_vector (rhqr.py:71-96); rho == tail
+  if (tid == 0) {
+    const double rho = tail, yc = a.z[jj];
+    const double sigma = yc >= 0.0 ? 1.0 : -1.0;
+    const double gamma = __dadd_rn(yc, sigma * rho);
+    const double beta = __ddiv_rn(1.0, __dmul_rn(__dmul_rn(rho, sigma), gamma));
+    bool bad = false;
+    if (rho == 0.0) { bad = true; fail(a.st, SQB_ERR_BREAKDOWN, j, 0.0); }
+    else if (!isfinite(beta)) { bad = true; fail(a.st, SQB_ERR_BREAKDOWN, j, rho); }
+    double f, bo;
+    if (a.scaling == SQB_SCALE_SQRT2) { f = __dsqrt_rn(beta); bo = 1.0; }
+    else { f = gamma; bo = __ddiv_rn(__dmul_rn(sigma, gamma), rho); }
+    scal[0] = -sigma * rho; scal[1] = gamma; scal[2] = f; scal[3] = bad ? -1.0 : bo;
+    *a.fscale = f;
+    // Hessenberg column (krylov.py:130-134)
+    if (j == 1) *a.beta = -sigma * rho;
+    else a.H[jj + (int64_t)(j - 2) * a.ldh] = -sigma * rho;
+  }
+  __syncthreads();
+  const double gamma = scal[1], f = scal[2], bo = scal[3];
+  if (bo < 0.0) return;
+  const bool sq = a.scaling == SQB_SCALE_SQRT2;
+  T* U = (T*)a.U;
+  for (int r = tid; r < od; r += ARN_NT) {
+    const double yh = r < jj ? 0.0 : (r == jj ? gamma : a.z[r]);
+    const double sv = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
+    s[r] = sv;
+    a.S[r + (int64_t)jj * a.lds] = sv;
+    if (r < a.mt) U[r + (int64_t)jj * a.ldu] = Lo<T>::store(Lo<T>::from_double(sv));
+    if (j >= 2 && r < jj) a.H[r + (int64_t)(j - 2) * a.ldh] = a.z[r];  // w[:j-1]
+  }
+  __syncthreads();
+  // _extend_t (rhqr.py:135-140): T[:jj, jj] = -beta T[:jj,:jj] (S[:, :jj]^t s)
+  for (int k = warp; k < jj; k += nw) {
+    const double* sk = a.S + (int64_t)k * a.lds;
+    double d = 0.0;
+    for (int r = max(k, jj) + lane; r < od; r += 32) d = fma(sk[r], s[r], d);
+    d = warp_sum(d);
+    if (lane == 0) v[k] = d;
+  }
+  __syncthreads();
+  for (int i = warp; i < jj; i += nw) {
+    double d = 0.0;
+    for (int k = i + lane; k < jj; k += 32) d = fma(a.T[i + (int64_t)k * a.ldt], v[k], d);
+    d = warp_sum(d);
+    if (lane == 0) a.T[i + (int64_t)jj * a.ldt] = __dmul_rn(-bo, d);
+  }
+  if (tid == 0) a.T[jj + (int64_t)jj * a.ldt] = bo;
+  if (j > a.m) return;
+  __syncthreads();
+  // coef = T[:j,:j] S[j-1, :j]^t  (krylov.py:136)
+  for (int i = warp; i < j; i += nw) {
+    double d = 0.0;
+    for (int k = i + lane; k < j; k += 32) d = fma(a.T[i + (int64_t)k * a.ldt], a.S[jj + (int64_t)k * a.lds], d);
+    d = warp_sum(d);
+    if (lane == 0) a.coefq[i] = d;
+  }
+}
+
+// q = e_j - lo(U_j coef) (krylov.py:137-139); lazy scaling of U[:, j-1] rows >= mt;
+// q_lo = round(q) feeds the matvec, Q[:, j-1] = q (fp64) when stored.
+template <typename T, int VN>
+__global__ void __launch_bounds__(256)
+arn_q_kernel(int64_t n, int mt, int j, T* U, int64_t ldu, const double* __restrict__ coefq,
+             const double* __restrict__ fscale, int scaling, T* __restrict__ q, double* __restrict__ Q,
+             const Status* st) {
+  using A = typename Lo<T>::acc;
+  extern __shared__ unsigned char smraw[];
+  A* c = reinterpret_cast<A*>(smraw);
+  if (failed(st)) return;
+  for (int k = threadIdx.x; k < j; k += blockDim.x) c[k] = Lo<T>::from_double(coefq[k]);
+  __syncthreads();
+  const double f = *fscale;
+  const int jj = j - 1;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * VN; i0 < n;
+       i0 += (int64_t)gridDim.x * blockDim.x * VN) {
+    A acc[VN], x[VN];
+#pragma unroll
+    for (int e = 0; e < VN; ++e) acc[e] = A(0);
+    for (int k = 0; k < jj; ++k) {
+      load_run<T, VN>(U + (int64_t)k * ldu, i0, n, x);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) acc[e] = fma(x[e], c[k], acc[e]);
+    }
+    // column j-1: rows >= mt hold the unscaled w; scale and write back
+    T* uj = U + (int64_t)jj * ldu;
+    load_run<T, VN>(uj, i0, n, x);
+    bool any_low = false;
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      if (i0 + e >= mt) {
+        const double u = scaling == SQB_SCALE_SQRT2 ? __dmul_rn((double)x[e], f) : __ddiv_rn((double)x[e], f);
+        x[e] = Lo<T>::from_double(u);
+      } else {
+        any_low = true;
+      }
+    }
+    if (!any_low) store_run<T, VN>(uj, i0, n, x);
+    else
+#pragma unroll
+      for (int e = 0; e < VN; ++e)
+        if (i0 + e >= mt && i0 + e < n) uj[i0 + e] = Lo<T>::store(x[e]);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      acc[e] = fma(x[e], c[jj], acc[e]);
+      const int64_t i = i0 + e;
+      if (i < n) {
+        double qv = -(double)Lo<T>::rnd(acc[e]);
+        if (i == jj) qv = qv + 1.0;
+        q[i] = Lo<T>::store(Lo<T>::from_double(qv));
+        if (Q) Q[i] = qv;
+      }
+    }
+  }
+}
+
+struct OpDesc {
+  int kind;  // 0 csr, 1 dense, 2 callback
+  int64_t n;
+  const int64_t* indptr;
+  const int32_t* indices;
+  const double* data;
+  sqb_sketch dense;  // G = A (row-major) for the dense matvec
+  sqb_matvec_cb cb;
+  void* user;
+  void* xbuf;
+  double* ybuf;
+};
+
+template <typename T>
+static int matvec_t(sqb_ctx* ctx, const OpDesc& op, const T* x, const double* bsub, T* y, double* tmp64,
+                    void* dense_ws, const Status* st) {
+  const int64_t n = op.n;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 16 * 148));
+  if (op.kind == SQB_OP_CSR) {
+    csr_spmv_kernel<T><<<grid, 256, 0, ctx->stream>>>(n, op.indptr, op.indices, op.data, x, bsub, y, nullptr, st);
+    return check_launch(ctx, "csr_spmv_kernel");
+  }
+  // dense (K2 GEMM with k = 1) or callback: fp64 product into tmp64, then round
+  if (op.kind == SQB_OP_DENSE) {
+    // the reference multiplies in float64 (A @ round_to(q, low)): widen, then the K2 GEMM
+    double* x64 = tmp64 + n;
+    widen_kernel<T><<<grid, 256, 0, ctx->stream>>>(n, x, x64, st);
+    SQB_TRY(check_launch(ctx, "widen_kernel"));
+    SQB_TRY(launch_dense<double>(ctx, &op.dense, x64, n, 1, tmp64, n, 0, dense_ws, st));
+  } else {
+    SQB_CUDA_TRY(cudaMemcpyAsync(op.xbuf, x, sizeof(T) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    int rc = op.cb(op.user, ctx->stream);
+    if (rc != 0) return set_error(ctx, SQB_ERR_ARG, "matvec callback failed (%d)", rc);
+    SQB_CUDA_TRY(cudaMemcpyAsync(tmp64, op.ybuf, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (bsub) resid_kernel<T><<<grid, 256, 0, ctx->stream>>>(n, bsub, tmp64, y, st);
+  else round_kernel<T><<<grid, 256, 0, ctx->stream>>>(n, tmp64, y, st);
+  return check_launch(ctx, "matvec_round");
+}
+
+template <typename T>
+static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m, int scaling, double happy_tol,
+                     const double* b, const void* x0lo, void* U, int64_t ldu, double* S, int64_t lds, double* Tm,
+                     int64_t ldt, double* H, int64_t ldh, double* Q, int64_t ldq, double* beta, int* attained) {
+  const int64_t n = op.n;
+  const int mt = m + 1;
+  const int64_t od = mt + sk->ell;
+  WsPlan plan;
+  const size_t iz = plan.add(sizeof(double) * od);
+  const size_t iY = plan.add(sizeof(double) * od);
+  const size_t iC = plan.add(sizeof(double) * (mt + 1));
+  const size_t icq = plan.add(sizeof(double) * (mt + 1));
+  const size_t ifs = plan.add(sizeof(double) * 2);
+  const size_t iw = plan.add(sizeof(T) * (n + 16));
+  const size_t iq = plan.add(sizeof(T) * (n + 16));
+  const size_t it64 = plan.add(op.kind == SQB_OP_CSR ? 8 : sizeof(double) * 2 * n);
+  const size_t iAR = plan.add(apply_reflectors_ws_bytes(sk, Lo<T>::code, mt, mt, 1));
+  const size_t iP = plan.add(std::max(sketch_partials_bytes(sk, Lo<T>::code, 1),
+                                      op.kind == SQB_OP_DENSE ? dense_ws_bytes(&op.dense, SQB_F64, 1) : 0));
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  double* z = ws_ptr<double>(ctx, plan, iz);
+  double* fs = ws_ptr<double>(ctx, plan, ifs);
+  double* cq = ws_ptr<double>(ctx, plan, icq);
+  T* w = ws_ptr<T>(ctx, plan, iw);
+  T* q = ws_ptr<T>(ctx, plan, iq);
+  double* t64 = ws_ptr<double>(ctx, plan, it64);
+  void* P = ws_ptr<void>(ctx, plan, iP);
+  Status* st = ctx->d_status;
+  // zero the outputs the steps fill column by column
+  SQB_CUDA_TRY(cudaMemsetAsync(Tm, 0, sizeof(double) * ldt * mt, ctx->stream));
+  SQB_CUDA_TRY(cudaMemsetAsync(H, 0, sizeof(double) * ldh * m, ctx->stream));
+  SQB_CUDA_TRY(cudaMemsetAsync(beta, 0, sizeof(double), ctx->stream));
+  // w = lo(b - A lo(x0)); z = Psi w   (krylov.py:111-112)
+  SQB_TRY(matvec_t<T>(ctx, op, (const T*)x0lo, b, w, t64, P, st));
+  SQB_TRY(launch_copy_top(ctx, Lo<T>::code, w, n, mt, 1, z, od, st));
+  SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, w + mt, n, 1, z, od, mt, P, st));
+  const size_t step_smem = sizeof(double) * (od + mt + 32);
+  cudaFuncSetAttribute(arn_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(step_smem, 48 << 10));
+  constexpr int VN = VecN<T>::n;
+  const bool vec = ((reinterpret_cast<uintptr_t>(U) & 15) == 0) && (ldu % VN == 0) &&
+                   ((reinterpret_cast<uintptr_t>(q) & 15) == 0);
+  const unsigned gq = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n / VN + 255) / 256, 4 * 148));
+  for (int j = 1; j <= mt; ++j) {
+    T* uj = (T*)U + (int64_t)(j - 1) * ldu;
+    // the unscaled w becomes column j-1 of U (rows >= mt; the step writes the top rows)
+    SQB_CUDA_TRY(cudaMemcpyAsync(uj + mt, w + mt, sizeof(T) * (n - mt), cudaMemcpyDeviceToDevice, ctx->stream));
+    ArnArgs aa{j, m, mt, (int)od, scaling, happy_tol, z, S, lds, Tm, ldt, H, ldh, U, ldu, beta, fs, cq, st};
+    arn_step_kernel<T><<<1, ARN_NT, step_smem, ctx->stream>>>(aa);
+    SQB_TRY(check_launch(ctx, "arn_step_kernel"));
+    if (j > m) {
+      // lazy scaling of the last column's Omega rows
+      scale_col_kernel<T><<<gq, 256, 0, ctx->stream>>>(uj, n, mt, fs, scaling, st);
+      SQB_TRY(check_launch(ctx, "scale_col_kernel"));
+      break;
+    }
+    double* Qj = Q ? Q + (int64_t)(j - 1) * ldq : nullptr;
+    if (vec)
+      arn_q_kernel<T, VN><<<gq, 256, sizeof(double) * (mt + 1), ctx->stream>>>(n, mt, j, (T*)U, ldu, cq, fs,
+                                                                                 scaling, q, Qj, st);
+    else
+      arn_q_kernel<T, 1><<<gq, 256, sizeof(double) * (mt + 1), ctx->stream>>>(n, mt, j, (T*)U, ldu, cq, fs,
+                                                                                scaling, q, Qj, st);
+    SQB_TRY(check_launch(ctx, "arn_q_kernel"));
+    // w = lo(A lo(q))  (krylov.py:140)
+    SQB_TRY(matvec_t<T>(ctx, op, q, nullptr, w, t64, P, st));
+    // w = (I - U_j T_j^t S_j^t Psi) w  (krylov.py:141-142)
+    SQB_TRY(apply_reflectors_dispatch(ctx, sk, mt, Lo<T>::code, U, ldu, n, j, S, lds, Tm, ldt, 1, w, n, 1, w, n,
+                                      ws_ptr<void>(ctx, plan, iAR)));
+    // z = Psi w  (krylov.py:143)
+    SQB_TRY(launch_copy_top(ctx, Lo<T>::code, w, n, mt, 1, z, od, st));
+    SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, w + mt, n, 1, z, od, mt, P, st));
+  }
+  // read the outcome (the only sync of the whole Arnoldi run)
+  SQB_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(Status), cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  const Status hs = *ctx->h_status;
+  if (hs.code == SQB_CLOSED) {
+    *attained = hs.col;
+    // the last accepted reflector (column attained-1) still holds the unscaled w
+    if (hs.col >= 1) {
+      T* ul = (T*)U + (int64_t)(hs.col - 1) * ldu;
+      scale_col_kernel<T><<<gq, 256, 0, ctx->stream>>>(ul, n, mt, fs, scaling, nullptr);
+      SQB_TRY(check_launch(ctx, "scale_col_kernel"));
+    }
+    SQB_CUDA_TRY(cudaMemsetAsync(ctx->d_status, 0, sizeof(Status), ctx->stream));
+  } else {
+    *attained = -1;
+  }
+  return SQB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Hessenberg least squares by Givens rotations (krylov.py:153-190), one CTA
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+hess_lstsq_kernel(const double* __restrict__ H, int64_t ldh, int p, int k, double beta, double* R, double* g,
+                  double* y, double* hist, double* resid) {
+  __shared__ double red[32];
+  __shared__ double cs_sn[2];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < p * k; e += 256) R[(e % p) + (int64_t)(e / p) * p] = H[(e % p) + (int64_t)(e / p) * ldh];
+  for (int i = tid; i < p; i += 256) g[i] = i == 0 ? beta : 0.0;
+  if (tid == 0) hist[0] = fabs(beta);
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (tid == 0) {
+      const double a = R[j + (int64_t)j * p], t = R[j + 1 + (int64_t)j * p];
+      const double r = hypot(a, t);
+      double cs = 1.0, sn = 0.0;
+      if (r != 0.0) { cs = a / r; sn = t / r; }
+      cs_sn[0] = cs; cs_sn[1] = sn;
+      const double g0 = g[j], g1 = g[j + 1];
+      g[j] = cs * g0 + sn * g1;
+      g[j + 1] = -sn * g0 + cs * g1;
+      hist[j + 1] = fabs(g[j + 1]);
+    }
+    __syncthreads();
+    const double cs = cs_sn[0], sn = cs_sn[1];
+    for (int c = j + tid; c < k; c += 256) {
+      const double r1 = R[j + (int64_t)c * p], r2 = R[j + 1 + (int64_t)c * p];
+      R[j + (int64_t)c * p] = cs * r1 + sn * r2;
+      R[j + 1 + (int64_t)c * p] = -sn * r1 + cs * r2;
+    }
+    __syncthreads();
+  }
+  for (int i = k - 1; i >= 0; --i) {
+    double part = 0.0;
+    for (int c = i + 1 + tid; c < k; c += 256) part = fma(R[i + (int64_t)c * p], y[c], part);
+    const double dot = block_sum(part, red);
+    if (tid == 0) {
+      const double rii = R[i + (int64_t)i * p];
+      y[i] = rii == 0.0 ? 0.0 : (g[i] - dot) / rii;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *resid = p > k ? fabs(g[k]) : 0.0;
+}
+
+template <typename T>
+static int arnoldi_dispatch_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m, int scaling,
+                              double happy_tol, const double* b, const void* x0lo, void* U, int64_t ldu,
+                              double* S, int64_t lds, double* Tm, int64_t ldt, double* H, int64_t ldh,
+                              double* Q, int64_t ldq, double* beta, int* attained) {
+  return arnoldi_t<T>(ctx, sk, op, m, scaling, happy_tol, b, x0lo, U, ldu, S, lds, Tm, ldt, H, ldh, Q, ldq,
+                      beta, attained);
+}
+
+}  // namespace sqb
+
+using namespace sqb;
+
+extern "C" int sqb_rhqr_arnoldi(sqb_ctx* ctx, const sqb_sketch* sk, const sqb_operator* A, int m, int scaling,
+                                int lo_dtype, double happy_tol, const double* b, const void* x0lo, void* U,
+                                int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt, double* H,
+                                int64_t ldh, double* Q, int64_t ldq, double* beta, int* attained) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(validate_sketch(ctx, sk));
+  if (!A || A->n < 1) return set_error(ctx, SQB_ERR_ARG, "missing operator");
+  if (m < 1) return set_error(ctx, SQB_ERR_ARG, "need m >= 1");
+  if (sk->n != A->n - m - 1)
+    return set_error(ctx, SQB_ERR_ARG, "sketch takes %lld coordinates, expected n-m=%lld", (long long)sk->n,
+                     (long long)(A->n - m - 1));
+  if (sk->ell < m + 1) return set_error(ctx, SQB_ERR_ARG, "sampling size below column count");
+  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
+    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
+  OpDesc op{};
+  op.kind = A->kind;
+  op.n = A->n;
+  op.indptr = A->indptr;
+  op.indices = A->indices;
+  op.data = A->data;
+  op.cb = A->cb;
+  op.user = A->user;
+  op.xbuf = A->xbuf;
+  op.ybuf = A->ybuf;
+  if (A->kind == SQB_OP_DENSE) {
+    op.dense.kind = SQB_SKETCH_DENSE;
+    op.dense.ell = A->n;
+    op.dense.n = A->n;
+    op.dense.G = A->A;
+    op.dense.ldg = A->lda;
+  } else if (A->kind == SQB_OP_CSR) {
+    if (!A->indptr || !A->indices || !A->data) return set_error(ctx, SQB_ERR_ARG, "incomplete CSR operator");
+  } else if (A->kind == SQB_OP_CALLBACK) {
+    if (!A->cb || !A->xbuf || !A->ybuf) return set_error(ctx, SQB_ERR_ARG, "incomplete matvec callback");
+  } else {
+    return set_error(ctx, SQB_ERR_ARG, "unknown operator kind %d", A->kind);
+  }
+  switch (lo_dtype) {
+    case SQB_F64: return arnoldi_dispatch_t<double>(ctx, sk, op, m, scaling, happy_tol, b, x0lo, U, ldu, S, lds, T, ldt, H, ldh, Q, ldq, beta, attained);
+    case SQB_F32: return arnoldi_dispatch_t<float>(ctx, sk, op, m, scaling, happy_tol, b, x0lo, U, ldu, S, lds, T, ldt, H, ldh, Q, ldq, beta, attained);
+    case SQB_F16: return arnoldi_dispatch_t<__half>(ctx, sk, op, m, scaling, happy_tol, b, x0lo, U, ldu, S, lds, T, ldt, H, ldh, Q, ldq, beta, attained);
+    case SQB_BF16: return arnoldi_dispatch_t<__nv_bfloat16>(ctx, sk, op, m, scaling, happy_tol, b, x0lo, U, ldu, S, lds, T, ldt, H, ldh, Q, ldq, beta, attained);
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
+extern "C" int sqb_hessenberg_lstsq(sqb_ctx* ctx, const double* H, int64_t ldh, int64_t p, int64_t k, double beta,
+                                    double* y, double* hist, double* resid, double* work) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  if (p < k || k < 0) return set_error(ctx, SQB_ERR_ARG, "Hessenberg must be (k+1) x k");
+  double* R = work;
+  double* g = work + p * std::max<int64_t>(k, 1);
+  hess_lstsq_kernel<<<1, 256, 0, ctx->stream>>>(H, ldh, (int)p, (int)k, beta, R, g, y, hist, resid);
+  return check_launch(ctx, "hess_lstsq_kernel");
+}
+
+extern "C" int sqb_csr_spmv(sqb_ctx* ctx, int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
+                            const double* data, const void* x, const double* bsub, void* y) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 16 * 148));
+  switch (dtype) {
+    case SQB_F64: csr_spmv_kernel<double><<<grid, 256, 0, ctx->stream>>>(n, indptr, indices, data, (const double*)x, bsub, (double*)y, nullptr, nullptr); break;
+    case SQB_F32: csr_spmv_kernel<float><<<grid, 256, 0, ctx->stream>>>(n, indptr, indices, data, (const float*)x, bsub, (float*)y, nullptr, nullptr); break;
+    case SQB_F16: csr_spmv_kernel<__half><<<grid, 256, 0, ctx->stream>>>(n, indptr, indices, data, (const __half*)x, bsub, (__half*)y, nullptr, nullptr); break;
+    case SQB_BF16: csr_spmv_kernel<__nv_bfloat16><<<grid, 256, 0, ctx->stream>>>(n, indptr, indices, data, (const __nv_bfloat16*)x, bsub, (__nv_bfloat16*)y, nullptr, nullptr); break;
+    default: return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", dtype);
+  }
+  return check_launch(ctx, "csr_spmv_kernel");
+}

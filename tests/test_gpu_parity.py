@@ -321,3 +321,89 @@ def test_rec_rhqr_breakdown_message(P):
     W[:, 2] = np.arange(40.0)
     with pytest.raises(P.BreakdownError, match="column 2 exactly dependent"):
         P.rec_rhqr(W, P.GaussianSketch(12, 37, 1))
+
+
+# ---------------------------------------------------------------- Arnoldi / GMRES
+def test_hessenberg_known_answers(P):
+    y, r = P.hessenberg_lstsq(np.array([[1.0], [0.0]]), 2.0)
+    assert y[0] == pytest.approx(2.0, abs=1e-15) and r == 0.0
+    y, r = P.hessenberg_lstsq(np.array([[0.0], [1.0]]), 1.0)
+    assert y[0] == 0.0 and r == pytest.approx(1.0, abs=1e-15)
+    g = golden("hessenberg_11x10")
+    y, res, h = P.hessenberg_lstsq(g["H"], float(g["beta"]), history=True)
+    assert np.allclose(y, g["y"], rtol=1e-13, atol=1e-14)
+    assert res == pytest.approx(float(g["res"]), rel=1e-13)
+    assert np.allclose(h, g["hist"], rtol=1e-13)
+
+
+def test_arnoldi_gmres_matches_reference(P):
+    g = golden("arnoldi_400_m20")
+    m = 20
+    om = P.SRHTSketch(int(g["ell"]), 400 - m - 1, int(g["seed"]))
+    bun = P.rhqr_arnoldi(g["A"], g["b"], None, m, om)
+    assert bun.breakdown is None
+    assert rel(bun.H, g["H"]) < 1e-12 and rel(bun.Q_cols, g["Q"]) < 1e-12
+    assert rel(bun.U, g["U"]) < 1e-12 and rel(bun.T, g["T"]) < 1e-12
+    assert bun.beta == pytest.approx(float(g["beta"]), rel=1e-13)
+    x, hist = P.rhqr_gmres(g["A"], g["b"], None, m, om)
+    assert rel(x, g["x"]) < 1e-11 and np.allclose(hist, g["hist"], rtol=1e-10)
+    # the same through the CSR SpMV path and a Python callable
+    import scipy.sparse
+    A = scipy.sparse.csr_matrix(g["A"])
+    x2, h2 = P.rhqr_gmres(A, g["b"], None, m, om)
+    assert rel(x2, g["x"]) < 1e-11
+    x3, h3 = P.rhqr_gmres(lambda v: v.new_tensor(g["A"]) @ v, g["b"], None, m, om)
+    assert rel(x3, g["x"]) < 1e-11
+    Qm1 = P.arnoldi_q(bun, m + 1)
+    assert rel(Qm1[:, :m], bun.Q_cols) < 1e-13
+
+
+def test_arnoldi_identity_closes_at_one(P):
+    b = np.random.default_rng(0).standard_normal(30)
+    bun = P.rhqr_arnoldi(np.eye(30), b, None, 5, P.GaussianSketch(24, 24, 1))
+    assert bun.breakdown == 1 and bun.H.shape == (2, 1)
+    assert abs(bun.H[0, 0]) == pytest.approx(1.0, abs=1e-12) and abs(bun.H[1, 0]) <= 1e-12
+
+
+def test_arnoldi_invariant_subspace_and_gmres(P):
+    rng = np.random.default_rng(4)
+    n = 50
+    A = np.zeros((n, n))
+    A[:3, :3] = rng.standard_normal((3, 3)) + 3 * np.eye(3)
+    A[3:, 3:] = rng.standard_normal((n - 3, n - 3))
+    b = np.zeros(n)
+    b[:3] = [1.0, 2.0, -1.0]
+    bun = P.rhqr_arnoldi(A, b, None, 8, P.GaussianSketch(36, n - 9, 4))
+    ref = O.rhqr_arnoldi(A, b, None, 8, O.Gaussian(36, n - 9, 4))
+    assert bun.breakdown == ref.breakdown == 3
+    assert bun.H.shape == (4, 3) and rel(bun.H, ref.H) < 1e-10
+    x, hist = P.rhqr_gmres(A, b, None, 8, P.GaussianSketch(36, n - 9, 4))
+    xref = np.zeros(n)
+    xref[:3] = np.linalg.solve(A[:3, :3], b[:3])
+    assert np.allclose(x, xref, atol=1e-10)
+
+
+def test_gmres_zero_operator_warns(P):
+    b = np.random.default_rng(1).standard_normal(12)
+    with pytest.warns(RuntimeWarning, match="rank deficient"):
+        x, hist = P.rhqr_gmres(np.zeros((12, 12)), b, None, 3, P.GaussianSketch(12, 8, 13))
+    assert np.allclose(x, 0.0)
+
+
+def test_gmres_convection_diffusion_against_oracle(P):
+    """Config-5 operator family at a reduced grid: one GMRES(m) cycle against
+    the oracle run on the same CSR matrix and sketch."""
+    import scipy.sparse
+    k, m = 64, 40
+    indptr, indices, data = workloads.convection_diffusion_csr(k)
+    N = k * k
+    A = scipy.sparse.csr_matrix((data, indices, indptr), shape=(N, N))
+    b = np.random.default_rng(5).standard_normal(N)
+    om_p, om_o = P.SRHTSketch(4 * (m + 1), N - m - 1, 6), O.SRHT(4 * (m + 1), N - m - 1, 6)
+    x, hist = P.rhqr_gmres(A, b, None, m, om_p)
+    xo, histo = O.rhqr_gmres(A, b, None, m, om_o)
+    assert np.allclose(hist, histo, rtol=1e-9)
+    assert rel(x, xo) < 1e-9
+    # restarted driver reaches the tolerance
+    xr, hs = P.rhqr_gmres_restarted(A, b, None, m, om_p, tol=1e-6, max_cycles=200)
+    assert np.linalg.norm(b - A @ xr) <= 1e-6 * np.linalg.norm(b)

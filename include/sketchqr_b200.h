@@ -158,6 +158,30 @@ int sqb_rec_rhqr(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
                  double* T, int64_t ldt, double* R, int64_t ldr,
                  double* sigmas, double* rhos, double* betas);
 
+/* ---- multi-GPU (row partition) ------------------------------
+ * Rank p of P owns Omega coordinates [p n_pad/P, (p+1) n_pad/P) (whole SRHT
+ * tiles; needs n_pad/P >= the tile size) and rank 0 also the m identity rows.
+ * W/U local storage: rank 0 [m identity rows; its Omega rows], others [their
+ * Omega rows].  One all-gather of an (ell+m)-vector per column (NCCL); the
+ * top log2(P) SRHT tree levels are completed in rank order, so every output
+ * is bitwise identical to the single-GPU factorization. */
+int sqb_nccl_unique_id(char* out, int size);
+int sqb_ctx_init_comm(sqb_ctx* ctx, const char* id, int nranks, int rank);
+int sqb_rhqr_left_dist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                       const void* W, int64_t n_local, int64_t m, int64_t ldw,
+                       void* U, int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt,
+                       double* R, int64_t ldr, double* sigmas, double* rhos, double* betas,
+                       void* Utop_scratch);
+/* The same algorithm with P "virtual ranks" on one device (row blocks
+ * W_parts[p], the all-gather as device copies): the single-GPU test of the
+ * multi-GPU path.  Outputs are rank 0's; scratch >= (P-1)*((m+ell)m + 3m^2 + 3m)
+ * doubles. */
+int sqb_rhqr_left_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                          int nranks, const void* const* W_parts, const int64_t* ldw,
+                          void* const* U_parts, const int64_t* ldu, int64_t m,
+                          double* S, int64_t lds, double* T, int64_t ldt, double* R, int64_t ldr,
+                          double* sigmas, double* rhos, double* betas, double* scratch);
+
 /* (I - U T S^t Psi) X, or with transpose_t the reflectors in reverse
  * (apply_reflectors_compact, rhqr.py:100-119).  U: N x r (lo), S: (m+ell) x r,
  * T: r x r, X/Out: N x k (lo).  Out may alias X. */

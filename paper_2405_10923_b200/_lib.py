@@ -73,6 +73,13 @@ _SIGS = {
     "sqb_hessenberg_lstsq": ([vp, dp, i64, i64, i64, C.c_double, dp, dp, dp, dp], C.c_int),
     "sqb_csr_spmv": ([vp, C.c_int, i64, dp, dp, dp, dp, dp, dp], C.c_int),
     "sqb_arnoldi_q": ([vp, C.c_int, dp, i64, i64, i64, dp, i64, dp, i64, i64, dp, i64], C.c_int),
+    "sqb_nccl_unique_id": ([C.c_char_p, C.c_int], C.c_int),
+    "sqb_ctx_init_comm": ([vp, C.c_char_p, C.c_int, C.c_int], C.c_int),
+    "sqb_rhqr_left_dist": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, dp, i64, i64, i64, dp, i64, dp, i64,
+                            dp, i64, dp, i64, dp, dp, dp, dp], C.c_int),
+    "sqb_rhqr_left_virtual": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, C.c_int, C.POINTER(vp),
+                               C.POINTER(i64), C.POINTER(vp), C.POINTER(i64), i64, dp, i64, dp, i64, dp, i64,
+                               dp, dp, dp, dp], C.c_int),
     "sqb_rh_vector": ([vp, C.c_int, C.c_int, dp, i64, dp, i64, i64, dp, dp, dp], C.c_int),
 }
 

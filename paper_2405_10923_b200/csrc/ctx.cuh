@@ -24,6 +24,10 @@ struct sqb_ctx {
   std::vector<cudaEvent_t> prof_ev;   // pairs (begin, end)
   std::vector<double> prof_bytes;     // algorithmic bytes of each timed launch
   size_t prof_used = 0;
+  // NCCL communicator for the row-partitioned path (sqb_ctx_init_comm)
+  void* nccl = nullptr;
+  int nranks = 1;
+  int rank = 0;
 };
 
 namespace sqb {

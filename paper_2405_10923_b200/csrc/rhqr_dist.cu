@@ -1,0 +1,371 @@
+// Row-partitioned left-looking RHQR over P GPUs.
+//
+// Rank p owns the Omega coordinates [p n_pad/P, (p+1) n_pad/P) — whole SRHT
+// tiles — plus, on rank 0, the m identity-block rows.  Per column the only
+// exchange is the (ell + m)-vector of rank-local partials: each rank finishes
+// the SRHT tree over its own tiles (levels below log2(tiles per rank)), the
+// vectors are all-gathered (NCCL over NVLink), and every rank completes the top
+// log2(P) tree levels in rank order (lower rank = left operand) inside the
+// step kernel — the same binary tree as on one GPU, so y, and with it S, T, R
+// and the coefficients, are bitwise identical to the single-GPU factorization
+// (and to the reference's Psi).  Every rank then runs the sketch-space step
+// redundantly; U and W never move.
+//
+// The exchange is either NCCL (one process per GPU, sqb_ctx_init_comm) or, for
+// testing on a single GPU, "virtual ranks": all ranks' row blocks on one device,
+// the all-gather a set of device copies.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <vector>
+
+#include "rhqr_kernels.cuh"
+
+namespace sqb {
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded lazily (single-GPU users never need it)
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.h = h;
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+    }
+  }
+  return (api.getUniqueId && api.commInitRank && api.allGather) ? &api : nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// combine the gathered raw-sketch partials: Y0[row, col] (od x m)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void rank_combine_kernel(const double* __restrict__ G, int nranks, int ell, int m, int rank_level,
+                                    const int64_t* __restrict__ idx, int log_tb, double norm_lo,
+                                    double* __restrict__ Y0, int64_t ldy, const Status* st) {
+  using A = typename Lo<T>::acc;
+  if (failed(st)) return;
+  const int pl = ell + m;
+  const int col = blockIdx.y;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < m + ell; row += gridDim.x * blockDim.x) {
+    double y;
+    if (row < m) {
+      y = G[(int64_t)col * pl + ell + row];  // rank 0's slot
+    } else {
+      const int o = row - m;
+      const int64_t rhi = __ldg(idx + o) >> log_tb;
+      A v[8];
+      for (int q = 0; q < nranks; ++q) v[q] = (A)G[((int64_t)q * m + col) * pl + o];
+      int lvl = rank_level;
+      for (int w = 1; w < nranks; w <<= 1, ++lvl) {
+        const bool neg = (rhi >> lvl) & 1;
+        for (int q = 0; q + w < nranks; q += 2 * w) v[q] = neg ? Lo<T>::sub(v[q], v[q + w]) : Lo<T>::add(v[q], v[q + w]);
+      }
+      y = (double)Lo<T>::mul(v[0], (A)norm_lo);
+    }
+    Y0[row + (int64_t)col * ldy] = y;
+  }
+}
+
+struct DistRank {
+  const void* W; int64_t ldw;
+  void* U; int64_t ldu;
+  int64_t n_local;  // Omega rows held
+  int mrow;         // m on rank 0, else 0
+  int64_t e_base;   // first global Omega coordinate
+  double *S, *T, *R, *sig, *rho, *bet;
+  int64_t lds, ldt, ldr;
+  void* Utop; int64_t ldutop;  // where the step kernel writes the identity-block rows of u
+  // workspace
+  double *y, *coef, *abuf, *vbuf, *fs, *pay, *Y0pay;
+  void* P;
+};
+
+template <typename T>
+static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t m, std::vector<DistRank>& rk,
+                       int nranks, bool virt, const std::vector<int>& rank_ids) {
+  using A = typename Lo<T>::acc;
+  const int64_t ell = sk->ell, od = m + ell;
+  const SrhtGeom g = srht_geom_t<T>(sk);
+  if (g.n_tiles % nranks != 0)
+    return set_error(ctx, SQB_ERR_ARG, "n_pad=%lld too small for %d ranks (need n_pad/P >= %d)",
+                     (long long)sk->n_pad, nranks, 1 << g.log_tb);
+  const int64_t tpr = g.n_tiles / nranks;  // tiles per rank
+  int rank_level = 0;
+  while ((int64_t(1) << rank_level) < tpr) ++rank_level;
+  const int64_t tb = int64_t(1) << g.log_tb;
+  const size_t esz = sizeof(T);
+  const int L = (int)rk.size();
+  // workspace: per local rank + shared gather buffers
+  WsPlan plan;
+  std::vector<size_t> off(L * 8);
+  for (int r = 0; r < L; ++r) {
+    off[r * 8 + 0] = plan.add(sizeof(double) * od);            // y
+    off[r * 8 + 1] = plan.add(sizeof(double) * (m + 1));       // coef (clast)
+    off[r * 8 + 2] = plan.add(sizeof(double) * 2 * (m + 1));   // abuf
+    off[r * 8 + 3] = plan.add(sizeof(double) * (m + 1));       // vbuf
+    off[r * 8 + 4] = plan.add(sizeof(double) * 2);             // fs
+    off[r * 8 + 5] = plan.add(sizeof(double) * od);            // payload (ell partials + m top)
+    off[r * 8 + 6] = plan.add(sizeof(double) * m * od);        // raw-sketch payload
+    off[r * 8 + 7] = plan.add(sizeof(A) * ell * tpr * m);      // leaves
+  }
+  const size_t iG = plan.add(sizeof(double) * nranks * od);        // per-column gather
+  const size_t iG0 = plan.add(sizeof(double) * nranks * m * od);   // raw-sketch gather
+  const size_t iY0 = plan.add(sizeof(double) * od * m);            // combined raw sketches (shared)
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  char* base = static_cast<char*>(ctx->ws);
+  for (int r = 0; r < L; ++r) {
+    DistRank& d = rk[r];
+    d.y = (double*)(base + plan.offs[off[r * 8 + 0]]);
+    d.coef = (double*)(base + plan.offs[off[r * 8 + 1]]);
+    d.abuf = (double*)(base + plan.offs[off[r * 8 + 2]]);
+    d.vbuf = (double*)(base + plan.offs[off[r * 8 + 3]]);
+    d.fs = (double*)(base + plan.offs[off[r * 8 + 4]]);
+    d.pay = (double*)(base + plan.offs[off[r * 8 + 5]]);
+    d.Y0pay = (double*)(base + plan.offs[off[r * 8 + 6]]);
+    d.P = base + plan.offs[off[r * 8 + 7]];
+  }
+  double* Gc = (double*)(base + plan.offs[iG]);
+  double* G0 = (double*)(base + plan.offs[iG0]);
+  double* Y0 = (double*)(base + plan.offs[iY0]);
+  Status* st = ctx->d_status;
+  NcclApi* nc = virt ? nullptr : nccl_api();
+  if (!virt && (!nc || !ctx->nccl)) return set_error(ctx, SQB_ERR_NCCL, "NCCL communicator not initialised");
+
+  // all-gather `count` doubles from every rank's send buffer into G ([rank][count])
+  auto exchange = [&](double* (*sendp)(DistRank&), size_t count, double* G) -> int {
+    if (virt) {
+      for (int r = 0; r < L; ++r)
+        SQB_CUDA_TRY(cudaMemcpyAsync(G + (size_t)rank_ids[r] * count, sendp(rk[r]), sizeof(double) * count,
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+      return SQB_OK;
+    }
+    ncclResult_t e = nc->allGather(sendp(rk[0]), G, count, ncclDouble, (ncclComm_t)ctx->nccl, ctx->stream);
+    if (e != ncclSuccess)
+      return set_error(ctx, SQB_ERR_NCCL, "ncclAllGather: %s", nc->getErrorString ? nc->getErrorString(e) : "?");
+    return SQB_OK;
+  };
+
+  double scale_lo = 0.0, norm_lo = 0.0;
+  srht_constants(sk, Lo<T>::code, &scale_lo, &norm_lo);
+  // ---- raw sketches: rank-local subtrees, one all-gather, rank-level combine
+  for (int r = 0; r < L; ++r) {
+    DistRank& d = rk[r];
+    SQB_CUDA_TRY(cudaMemsetAsync(d.T, 0, sizeof(double) * d.ldt * m, ctx->stream));
+    SrhtGeom gl{g.log_tb, tpr, (d.n_local + tb - 1) / tb};
+    const char* wo = (const char*)d.W + d.mrow * esz;
+    if (d.n_local > 0) {
+      SQB_TRY(launch_srht_tiles_geom(ctx, sk, Lo<T>::code, gl, d.n_local, d.e_base, wo, d.ldw, m, d.P, st));
+    } else {
+      SQB_CUDA_TRY(cudaMemsetAsync(d.P, 0, sizeof(A) * ell * tpr * m, ctx->stream));
+    }
+    SQB_TRY(launch_srht_tree_geom(ctx, sk, Lo<T>::code, gl, d.P, m, d.Y0pay, od, 0, 0, st));
+    if (d.mrow > 0) SQB_TRY(launch_copy_top(ctx, Lo<T>::code, d.W, d.ldw, m, m, d.Y0pay + ell, od, st));
+  }
+  SQB_TRY(exchange([](DistRank& d) { return d.Y0pay; }, (size_t)m * od, G0));
+  {
+    dim3 grid((unsigned)((od + 255) / 256), (unsigned)m);
+    rank_combine_kernel<T><<<grid, 256, 0, ctx->stream>>>(G0, nranks, (int)ell, (int)m, rank_level, sk->indices,
+                                                          g.log_tb, norm_lo, Y0, od, st);
+    SQB_TRY(check_launch(ctx, "rank_combine_kernel"));
+  }
+  const size_t step_smem = step_smem_bytes((int)od, (int)m);
+  cudaFuncSetAttribute(rhqr_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(step_smem, 48 * 1024));
+  auto step_args = [&](DistRank& d, int c) {
+    StepArgs sa{};
+    sa.c = c; sa.m = (int)m; sa.ell = (int)ell; sa.od = (int)od; sa.scaling = scaling;
+    sa.tree = c == 0 ? 0 : 2;
+    sa.gath = Gc; sa.nranks = nranks; sa.rank_level = rank_level;
+    sa.P = nullptr; sa.n_tiles = tpr; sa.n_eff = 0; sa.idx = sk->indices; sa.log_tb = g.log_tb; sa.norm_lo = norm_lo;
+    sa.y = c == 0 ? Y0 : d.y; sa.Y0 = Y0; sa.S = d.S; sa.lds = d.lds; sa.R = d.R; sa.ldr = d.ldr;
+    sa.U = d.Utop; sa.ldu = d.ldutop; sa.sigmas = d.sig; sa.rhos = d.rho; sa.betas = d.bet;
+    sa.fscale = d.fs; sa.vbuf = d.vbuf; sa.anext = d.abuf + ((c + 1) & 1) * (m + 1); sa.clast = d.coef;
+    sa.st = st;
+    return sa;
+  };
+  for (int r = 0; r < L; ++r)
+    SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT), step_smem,
+                       step_args(rk[r], 0)));
+  // ---- column loop
+  constexpr int VN = VecN<T>::n;
+  const size_t tile_bytes = tile_smem_bytes<A>(1 << TileCfg<T>::LOG_TB);
+  const size_t col_smem_max = sizeof(A) * ((m + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(m + 1));
+  cudaFuncSetAttribute(rhqr_col_kernel<T, VN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
+  cudaFuncSetAttribute(rhqr_col_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
+  for (int64_t c = 1; c < m; ++c) {
+    for (int r = 0; r < L; ++r) {
+      DistRank& d = rk[r];
+      const int64_t n_eff = (d.n_local + tb - 1) / tb;
+      ColArgs ca{};
+      ca.c = (int)c; ca.m = (int)m; ca.mrow = d.mrow; ca.e_base = d.e_base; ca.n = d.n_local; ca.ell = (int)ell;
+      ca.od = (int)od; ca.log_tb = g.log_tb; ca.n_tiles = tpr; ca.n_eff = n_eff;
+      ca.W = d.W; ca.ldw = d.ldw; ca.U = d.U; ca.ldu = d.ldu; ca.acur = d.abuf + (c & 1) * (m + 1);
+      ca.clast = d.coef; ca.fscale = d.fs; ca.scaling = scaling; ca.srht = 1; ca.bits = sk->sign_bits;
+      ca.idx = sk->indices; ca.scale_lo = scale_lo; ca.P = d.P; ca.y = d.pay + ell;
+      ca.S = d.S; ca.lds = d.lds; ca.T = d.T; ca.ldt = d.ldt; ca.Y0 = Y0; ca.vprev = d.vbuf; ca.betas = d.bet;
+      ca.anext = d.abuf + ((c + 1) & 1) * (m + 1); ca.st = st;
+      const bool vec = ((reinterpret_cast<uintptr_t>((const char*)d.W + d.mrow * esz) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>((const char*)d.U + d.mrow * esz) & 15) == 0) &&
+                       (d.ldw % VN == 0) && (d.ldu % VN == 0);
+      const size_t smem = sizeof(A) * ((c + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(c + 1));
+      if (vec)
+        SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", rhqr_col_kernel<T, VN>, dim3((unsigned)(n_eff + 2)), dim3(COL_NT),
+                           smem, ca));
+      else
+        SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", rhqr_col_kernel<T, 1>, dim3((unsigned)(n_eff + 2)), dim3(COL_NT),
+                           smem, ca));
+      // rank-local subtree of w_c's sketch -> payload[0:ell]
+      SrhtGeom gl{g.log_tb, tpr, n_eff};
+      if (n_eff == 0) SQB_CUDA_TRY(cudaMemsetAsync(d.P, 0, sizeof(A) * ell * tpr, ctx->stream));
+      SQB_TRY(launch_srht_tree_geom(ctx, sk, Lo<T>::code, gl, d.P, 1, d.pay, od, 0, 0, st));
+    }
+    SQB_TRY(exchange([](DistRank& d) { return d.pay; }, (size_t)od, Gc));
+    for (int r = 0; r < L; ++r)
+      SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT), step_smem,
+                         step_args(rk[r], (int)c)));
+  }
+  for (int r = 0; r < L; ++r) {
+    DistRank& d = rk[r];
+    const T* src = m == 1 ? (const T*)d.W + d.mrow : (const T*)d.U + (m - 1) * d.ldu + d.mrow;
+    T* dst = (T*)d.U + (m - 1) * d.ldu + d.mrow;
+    const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((d.n_local + 255) / 256, 4 * 148));
+    SQB_TRY(launch_pdl(ctx, "finish_kernel", finish_kernel<T>, dim3(gb + 1), dim3(256), 0, src, dst, d.n_local,
+                       (const double*)d.fs, scaling, d.T, d.ldt, (int)m, (const double*)d.vbuf, (const double*)d.bet,
+                       (const Status*)st));
+  }
+  return SQB_OK;
+}
+
+static int dist_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, int64_t m,
+                         std::vector<DistRank>& rk, int nranks, bool virt, const std::vector<int>& ids) {
+  switch (lo_dtype) {
+    case SQB_F64: return rhqr_dist_t<double>(ctx, sk, scaling, m, rk, nranks, virt, ids);
+    case SQB_F32: return rhqr_dist_t<float>(ctx, sk, scaling, m, rk, nranks, virt, ids);
+    case SQB_F16: return rhqr_dist_t<__half>(ctx, sk, scaling, m, rk, nranks, virt, ids);
+    case SQB_BF16: return rhqr_dist_t<__nv_bfloat16>(ctx, sk, scaling, m, rk, nranks, virt, ids);
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
+static int check_common(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t m, int nranks) {
+  SQB_TRY(validate_sketch(ctx, sk));
+  if (sk->kind != SQB_SKETCH_SRHT) return set_error(ctx, SQB_ERR_ARG, "the row-partitioned sweep needs an SRHT");
+  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
+    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
+  if (m < 1 || m > 1024) return set_error(ctx, SQB_ERR_ARG, "need 1 <= m <= 1024");
+  if (sk->ell < m) return set_error(ctx, SQB_ERR_ARG, "sampling size below column count");
+  if (nranks < 1 || nranks > 8 || (nranks & (nranks - 1)))
+    return set_error(ctx, SQB_ERR_ARG, "nranks must be a power of two <= 8");
+  return SQB_OK;
+}
+
+}  // namespace sqb
+
+using namespace sqb;
+
+extern "C" {
+
+int sqb_nccl_unique_id(char* out, int size) {
+  NcclApi* nc = nccl_api();
+  if (!nc || size < (int)sizeof(ncclUniqueId)) return SQB_ERR_NCCL;
+  ncclUniqueId id;
+  if (nc->getUniqueId(&id) != ncclSuccess) return SQB_ERR_NCCL;
+  memcpy(out, &id, sizeof(id));
+  return SQB_OK;
+}
+
+int sqb_ctx_init_comm(sqb_ctx* ctx, const char* id, int nranks, int rank) {
+  if (!ctx) return SQB_ERR_ARG;
+  NcclApi* nc = nccl_api();
+  if (!nc) return set_error(ctx, SQB_ERR_NCCL, "libnccl.so.2 not found");
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm;
+  ncclResult_t e = nc->commInitRank(&comm, nranks, uid, rank);
+  if (e != ncclSuccess) return set_error(ctx, SQB_ERR_NCCL, "ncclCommInitRank: %s", nc->getErrorString(e));
+  ctx->nccl = comm;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  return SQB_OK;
+}
+
+int sqb_rhqr_left_dist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, const void* W,
+                       int64_t n_local, int64_t m, int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds,
+                       double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
+                       double* betas, void* Utop_scratch) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(check_common(ctx, sk, scaling, m, ctx->nranks));
+  const int64_t span = sk->n_pad / ctx->nranks;
+  const int64_t e_base = span * ctx->rank;
+  const int64_t want = std::max<int64_t>(0, std::min<int64_t>(span, sk->n - e_base));
+  if (n_local != want)
+    return set_error(ctx, SQB_ERR_ARG, "rank %d holds %lld Omega rows, expected %lld", ctx->rank,
+                     (long long)n_local, (long long)want);
+  std::vector<DistRank> rk(1);
+  DistRank& d = rk[0];
+  d.W = W; d.ldw = ldw; d.U = U; d.ldu = ldu; d.n_local = n_local; d.mrow = ctx->rank == 0 ? (int)m : 0;
+  d.e_base = e_base; d.S = S; d.T = T; d.R = R; d.sig = sigmas; d.rho = rhos; d.bet = betas;
+  d.lds = lds; d.ldt = ldt; d.ldr = ldr;
+  d.Utop = ctx->rank == 0 ? U : Utop_scratch;
+  d.ldutop = ctx->rank == 0 ? ldu : m;
+  if (!d.Utop) return set_error(ctx, SQB_ERR_ARG, "ranks > 0 need an m x m Utop_scratch buffer");
+  return dist_dispatch(ctx, sk, scaling, lo_dtype, m, rk, ctx->nranks, false, std::vector<int>{ctx->rank});
+}
+
+int sqb_rhqr_left_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, int nranks,
+                          const void* const* W_parts, const int64_t* ldw, void* const* U_parts,
+                          const int64_t* ldu, int64_t m, double* S, int64_t lds, double* T, int64_t ldt,
+                          double* R, int64_t ldr, double* sigmas, double* rhos, double* betas, double* scratch) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(check_common(ctx, sk, scaling, m, nranks));
+  const int64_t span = sk->n_pad / nranks;
+  const int64_t od = m + sk->ell;
+  // scratch for ranks > 0: S, T, R, 3m scalars, m x m Utop  (per rank)
+  const int64_t per = od * m + 2 * m * m + 3 * m + m * m;
+  std::vector<DistRank> rk(nranks);
+  std::vector<int> ids(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    DistRank& d = rk[r];
+    ids[r] = r;
+    d.W = W_parts[r]; d.ldw = ldw[r]; d.U = U_parts[r]; d.ldu = ldu[r];
+    d.e_base = span * r;
+    d.n_local = std::max<int64_t>(0, std::min<int64_t>(span, sk->n - d.e_base));
+    d.mrow = r == 0 ? (int)m : 0;
+    if (r == 0) {
+      d.S = S; d.T = T; d.R = R; d.sig = sigmas; d.rho = rhos; d.bet = betas;
+      d.lds = lds; d.ldt = ldt; d.ldr = ldr; d.Utop = U_parts[0]; d.ldutop = ldu[0];
+    } else {
+      double* b = scratch + (r - 1) * per;
+      d.S = b; d.lds = od; d.T = b + od * m; d.ldt = m; d.R = d.T + m * m; d.ldr = m;
+      d.sig = d.R + m * m; d.rho = d.sig + m; d.bet = d.rho + m; d.Utop = d.bet + m; d.ldutop = m;
+    }
+  }
+  // rank r > 0 writes its identity-block u rows as T; the scratch is double, large enough for any T
+  return dist_dispatch(ctx, sk, scaling, lo_dtype, m, rk, nranks, true, ids);
+}
+
+}  // extern "C"

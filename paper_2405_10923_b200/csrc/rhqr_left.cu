@@ -1,470 +1,7 @@
-// Left-looking randomized Householder QR on the device (rhqr_left, rhqr.py:254-267;
-// the hot loop _left_sweep, rhqr.py:219-251).
-//
-// Per column c two PDL-chained launches:
-//
-//   rhqr_col_kernel (K3+K1, ~all HBM traffic)  one pass over rows >= m:
-//       lazily scale column c-1 (u = fl(w * f), rhqr.py:86-95 + round_to),
-//       w_c = fl(W[:,c] - fl(U[:, :c] coef_c)) (:242), store w_c unscaled in
-//       U[:, c], emit the in-tile SRHT leaves of w_c.  Extra CTAs: the m-row
-//       identity block (y[0:m] = w_c[0:m]) and one HELPER doing the sketch-
-//       space work that is off the critical path (T column c-1, a_{c+1}).
-//
-//   rhqr_step_kernel (K4, an 8-CTA cluster)  finishes the SRHT tree
-//       (y[m:] = Omega w_c, bit-exact), rh_vector's scalars (:71-94), s = Psi u,
-//       the R column (:248-249), v = S_c^t s (the _extend_t product, :138) and
-//       the last entry of the next coefficients — cross-CTA sums through DSMEM.
-//
-// Coefficients (rhqr.py:241, coef_{c+1} = T_{c+1}^t S_{c+1}^t y0_{c+1}) are
-// split so that only two dots sit on the critical path:
-//   a_{c+1} = T_c^t (S_c^t y0_{c+1})          (helper, during pass c)
-//   coef_{c+1}[:c] = a_{c+1}
-//   coef_{c+1}[c]  = beta_c (s_c^t y0_{c+1} - v_c^t a_{c+1})   (step c)
-// which is T_{c+1}^t g with T_{c+1}[:c, c] = -beta_c T_c v_c, T[c,c] = beta_c
-// (_extend_t) expanded algebraically; T's column c itself is written by the
-// helper of pass c+1 exactly as _extend_t forms it.
-// The raw sketches y0 = Psi W[:, c] of all columns are computed once up front
-// (bitwise equal to the per-column psi.apply(w)).
-#include <algorithm>
-#include <cooperative_groups.h>
-
-#include "pdl.cuh"
-#include "sketch.cuh"
-#include "vec.cuh"
-
-namespace cg = cooperative_groups;
+// Left-looking RHQR driver, single GPU (kernels in rhqr_kernels.cuh).
+#include "rhqr_kernels.cuh"
 
 namespace sqb {
-
-constexpr int COL_NT = 256;
-constexpr int STEP_NT = 512;
-constexpr int STEP_CL = 8;  // cluster size of the step kernel
-
-struct ColArgs {
-  int c;            // current column (>= 1)
-  int m;            // identity-block rows = columns of W
-  int64_t n;        // Omega input length (N - m)
-  int ell, od;
-  int log_tb;
-  int64_t n_tiles;
-  int64_t n_eff;
-  const void* W;    // column-major, ldw
-  int64_t ldw;
-  void* U;          // column-major, ldu
-  int64_t ldu;
-  const double* acur;   // [c-1] coef_c[:c-1] = a_c (written by the helper of pass c-1)
-  const double* clast;  // [m] clast[c] = coef_c[c-1] (written by step c-1)
-  const double* fscale; // [1] f (sqrt2) or gamma (unit) of column c-1
-  int scaling;
-  int srht;             // emit SRHT leaves (else the sketch runs separately)
-  const uint32_t* bits;
-  const int64_t* idx;
-  double scale_lo;
-  void* P;              // leaves [ell][n_tiles] (acc type)
-  double* y;            // (m + ell) sketch of w_c; [0, m) written here
-  // helper (sketch-space work off the critical path)
-  double* S; int64_t lds;
-  double* T; int64_t ldt;
-  const double* Y0;     // raw sketches, od x m
-  const double* vprev;  // v_{c-1} = S_{c-1}^t s_{c-1}
-  const double* betas;
-  double* anext;        // out: a_{c+1}
-  Status* st;
-};
-
-template <typename T>
-__device__ __forceinline__ typename Lo<T>::acc lazy_scale(typename Lo<T>::acc w, double f, int scaling) {
-  // rhqr.py:86-95 then round_to(u, low): u = fl64(w * f) or fl64(w / gamma)
-  const double u = scaling == SQB_SCALE_SQRT2 ? __dmul_rn((double)w, f) : __ddiv_rn((double)w, f);
-  return Lo<T>::from_double(u);
-}
-
-// identity block: y[r] = w_c[r] = fl(W[r,c] - fl(sum_k U[r,k] coef[k])), r < m.
-// Columns k <= c-2 are final before step c-1 ends, so they are summed before
-// the PDL wait; column c-1 (its top rows come from step c-1) after it.
-template <typename T>
-__device__ void col_top_block(const ColArgs& a, typename Lo<T>::acc* sc) {
-  using A = typename Lo<T>::acc;
-  const T* W = (const T*)a.W;
-  const T* U = (const T*)a.U;
-  const int c = a.c;
-  constexpr int RPT = 4;  // rows per thread (m <= RPT * blockDim)
-  A acc[RPT];
-#pragma unroll
-  for (int q = 0; q < RPT; ++q) {
-    const int r = threadIdx.x + q * blockDim.x;
-    A acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
-    if (r < a.m) {
-      int k = 0;
-      for (; k + 4 <= c - 1; k += 4) {
-        acc0 = fma(Lo<T>::load(U[r + (int64_t)k * a.ldu]), sc[k], acc0);
-        acc1 = fma(Lo<T>::load(U[r + (int64_t)(k + 1) * a.ldu]), sc[k + 1], acc1);
-        acc2 = fma(Lo<T>::load(U[r + (int64_t)(k + 2) * a.ldu]), sc[k + 2], acc2);
-        acc3 = fma(Lo<T>::load(U[r + (int64_t)(k + 3) * a.ldu]), sc[k + 3], acc3);
-      }
-      for (; k < c - 1; ++k) acc0 = fma(Lo<T>::load(U[r + (int64_t)k * a.ldu]), sc[k], acc0);
-    }
-    acc[q] = (acc0 + acc1) + (acc2 + acc3);
-  }
-  pdl_wait();
-  if (failed(a.st)) return;
-  const A cl = Lo<T>::from_double(a.clast[c]);
-#pragma unroll
-  for (int q = 0; q < RPT; ++q) {
-    const int r = threadIdx.x + q * blockDim.x;
-    if (r < a.m) {
-      const A dot = fma(Lo<T>::load(U[r + (int64_t)(c - 1) * a.ldu]), cl, acc[q]);
-      const A w = Lo<T>::sub(Lo<T>::load(W[r + (int64_t)c * a.ldw]), Lo<T>::rnd(dot));
-      a.y[r] = (double)w;
-    }
-  }
-}
-
-// T[:kk, kk] = -beta * T[:kk,:kk] v ; T[kk,kk] = beta   (_extend_t, rhqr.py:135-140)
-__device__ void complete_t_column(double* T, int64_t ldt, int kk, const double* v, double beta) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = warp; i < kk; i += nw) {
-    double d = 0.0;
-    for (int k = i + lane; k < kk; k += 32) d = fma(T[i + (int64_t)k * ldt], v[k], d);
-    d = warp_sum(d);
-    if (lane == 0) T[i + (int64_t)kk * ldt] = __dmul_rn(-beta, d);
-  }
-  if (threadIdx.x == 0) T[kk + (int64_t)kk * ldt] = beta;
-}
-
-// helper CTA of pass c: complete T column c-1, then a_{c+1} = T_c^t (S_c^t y0_{c+1})
-__device__ void col_helper(const ColArgs& a, double* g) {
-  const int c = a.c;
-  complete_t_column(a.T, a.ldt, c - 1, a.vprev, a.betas[c - 1]);
-  if (c + 1 >= a.m) return;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double* y0 = a.Y0 + (int64_t)(c + 1) * a.od;
-  for (int k = warp; k < c; k += nw) {
-    const double* sk = a.S + (int64_t)k * a.lds;
-    double d0 = 0.0, d1 = 0.0;
-    int r = k + lane;
-    for (; r + 32 < a.od; r += 64) {
-      d0 = fma(sk[r], y0[r], d0);
-      d1 = fma(sk[r + 32], y0[r + 32], d1);
-    }
-    if (r < a.od) d0 = fma(sk[r], y0[r], d0);
-    const double d = warp_sum(d0 + d1);
-    if (lane == 0) g[k] = d;
-  }
-  __syncthreads();
-  for (int j = warp; j < c; j += nw) {
-    const double* tj = a.T + (int64_t)j * a.ldt;  // column j of T, rows 0..j
-    double d = 0.0;
-    for (int i = lane; i <= j; i += 32) d = fma(tj[i], g[i], d);
-    d = warp_sum(d);
-    if (lane == 0) a.anext[j] = d;
-  }
-}
-
-template <typename T, int VN>
-__global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
-  using A = typename Lo<T>::acc;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  A* sc = reinterpret_cast<A*>(smem_raw);                      // coef rounded to low [c]
-  A* sm = sc + ((a.c + 3) & ~3);                              // tile buffer
-  pdl_trigger();
-  const int c = a.c;
-  if (blockIdx.x == a.n_eff + 1) {
-    pdl_wait();
-    if (failed(a.st)) return;
-    col_helper(a, reinterpret_cast<double*>(sm));
-    return;
-  }
-  // coef_c[:c-1] = a_c is final before step c-1 ends (helper of pass c-1): load
-  // it and stream the bulk of the GEMV BEFORE waiting on step c-1 (look-ahead
-  // overlap of the HBM pass with the sketch-space step, via PDL)
-  for (int k = threadIdx.x; k < c - 1; k += COL_NT) sc[k] = Lo<T>::from_double(a.acur[k]);
-  __syncthreads();
-  if (blockIdx.x == a.n_eff) {
-    col_top_block<T>(a, sc);
-    return;
-  }
-  constexpr int TB = 1 << TileCfg<T>::LOG_TB;
-  constexpr int NV = TB / (COL_NT * VN);  // runs of VN rows per thread
-  const int tb = 1 << a.log_tb;
-  const int64_t e0 = (int64_t)blockIdx.x << a.log_tb;  // first Omega coordinate of the tile
-  const int64_t lim = a.n - e0;                       // valid rows in this tile (may exceed tb)
-  const int64_t rows = lim < tb ? lim : tb;
-  const int64_t ro = (int64_t)a.m + e0;                // first row of the tile in W / U
-  T* U = (T*)a.U;
-  const T* W = (const T*)a.W;
-
-  A acc[NV][VN];
-#pragma unroll
-  for (int v = 0; v < NV; ++v)
-#pragma unroll
-    for (int j = 0; j < VN; ++j) acc[v][j] = A(0);
-
-  // final columns 0 .. c-2
-  for (int k = 0; k < c - 1; ++k) {
-    const T* col = U + ro + (int64_t)k * a.ldu;
-    const A ck = sc[k];
-    A v0[NV][VN];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int i = (v * COL_NT + threadIdx.x) * VN;
-      if (i < tb) load_run<T, VN>(col, i, rows, v0[v]);
-    }
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-#pragma unroll
-      for (int j = 0; j < VN; ++j) acc[v][j] = fma(v0[v][j], ck, acc[v][j]);
-  }
-  // ---- wait for step c-1 (f_{c-1}, coef_c[c-1], breakdown status)
-  pdl_wait();
-  if (failed(a.st)) return;
-  // column c-1: lazy scaling of the stored w_{c-1}, write back u_{c-1}
-  {
-    const T* src = (c == 1 ? W : (const T*)U) + ro + (int64_t)(c - 1) * (c == 1 ? 0 : a.ldu);
-    T* dst = U + ro + (int64_t)(c - 1) * a.ldu;
-    const double f = *a.fscale;
-    const A ck = Lo<T>::from_double(a.clast[c]);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int i = (v * COL_NT + threadIdx.x) * VN;
-      if (i < tb) {
-        A x[VN];
-        load_run<T, VN>(src, i, rows, x);
-#pragma unroll
-        for (int j = 0; j < VN; ++j) {
-          x[j] = lazy_scale<T>(x[j], f, a.scaling);
-          acc[v][j] = fma(x[j], ck, acc[v][j]);
-        }
-        store_run<T, VN>(dst, i, rows, x);
-      }
-    }
-  }
-  // w_c = fl(W[:, c] - fl(dot)); store unscaled into U[:, c]; SRHT input to smem
-  {
-    const T* wc = W + ro + (int64_t)c * a.ldw;
-    T* uc = U + ro + (int64_t)c * a.ldu;
-    const A s_lo = (A)a.scale_lo;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int i = (v * COL_NT + threadIdx.x) * VN;
-      if (i < tb) {
-        A x[VN];
-        load_run<T, VN>(wc, i, rows, x);
-#pragma unroll
-        for (int j = 0; j < VN; ++j) x[j] = Lo<T>::sub(x[j], Lo<T>::rnd(acc[v][j]));
-        store_run<T, VN>(uc, i, rows, x);
-        if (a.srht) {
-          const int64_t e = e0 + i;
-          const uint32_t sb = __ldg(a.bits + (e >> 5)) >> (e & 31);
-#pragma unroll
-          for (int j = 0; j < VN; ++j)
-            sm[pidx<A>(i + j)] = (i + j < rows) ? srht_in<T>(x[j], s_lo, (sb >> j) & 1u) : A(0);
-        }
-      }
-    }
-  }
-  if (!a.srht) return;
-  __syncthreads();
-  tile_fwht<T>(sm, a.log_tb);
-  tile_gather<T>(sm, a.idx, a.ell, a.log_tb, (A*)a.P + blockIdx.x, a.n_tiles);
-}
-
-// ---------------------------------------------------------------------------
-// K4: cluster step kernel for column c.  The od = m + ell rows of Psi-space are
-// split into STEP_CL contiguous blocks, one per CTA of the cluster (top-block
-// rows < m first, then the Omega rows whose sketch values the tree produces).
-// ---------------------------------------------------------------------------
-struct StepArgs {
-  int c, m, ell, od;
-  int scaling;
-  int tree;                   // finish the SRHT tree from the leaves (else y[m:] is given)
-  const void* P;              // leaves [ell][n_tiles]
-  int64_t n_tiles, n_eff;
-  const int64_t* idx;
-  int log_tb;
-  double norm_lo;
-  double* y;                  // (od) sketch of w_c: [0, m) given, [m, od) tree output
-  const double* Y0;           // raw sketches (od x m, ld od)
-  double* S; int64_t lds;
-  double* R; int64_t ldr;
-  void* U; int64_t ldu;       // identity-block rows of U[:, c] are written here
-  double* sigmas; double* rhos; double* betas;
-  double* fscale;             // out: f of column c
-  double* vbuf;               // out: v_c = S_c^t s_c
-  const double* anext;        // in: a_{c+1} (helper of pass c)
-  double* clast;              // out: clast[c+1] = coef_{c+1}[c]
-  Status* st;
-};
-
-constexpr int STEP_KC = 128;                 // columns staged per chunk
-constexpr int STEP_NPART = STEP_NT / STEP_KC;
-
-__host__ __device__ inline int step_rows(int od) { return (od + STEP_CL - 1) / STEP_CL; }
-__host__ __device__ inline int step_ldst(int od) { return step_rows(od) | 1; }
-inline size_t step_smem_bytes(int od, int m) {
-  const int B = step_rows(od);
-  return sizeof(double) * (2 * (size_t)B + (size_t)STEP_KC * step_ldst(od) + STEP_CL * (size_t)(m + 1) +
-                           STEP_NPART * STEP_KC + STEP_CL + 32);
-}
-
-template <typename T>
-__global__ void __cluster_dims__(STEP_CL, 1, 1) __launch_bounds__(STEP_NT)
-rhqr_step_kernel(StepArgs a) {
-  using A = typename Lo<T>::acc;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
-  const int c = a.c, m = a.m, od = a.od, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nw = STEP_NT / 32;
-  const int B = step_rows(od), ldst = step_ldst(od);
-  const int r0 = rank * B, r1 = min(od, r0 + B), nrow = max(0, r1 - r0);
-  const int nk = c + 1;  // partial vector: v[0..c-1], s^t y0_{c+1}
-  double* yv = reinterpret_cast<double*>(smem_raw);  // [B] sketch rows owned
-  double* sv = yv + B;                               // [B] s rows owned
-  double* stage = sv + B;                            // [STEP_KC][ldst] staged S / y0 block
-  double* gath = stage + (size_t)STEP_KC * ldst;     // [STEP_CL][nk] partial vectors (rank 0)
-  double* cpart = gath + STEP_CL * (m + 1);          // [STEP_NPART][STEP_KC]
-  double* part = cpart + STEP_NPART * STEP_KC;       // [STEP_CL] rho^2 partials
-  double* red = part + STEP_CL;                      // [32]
-  __shared__ double scal[4];
-  pdl_wait();
-  pdl_trigger();
-  const bool dead = failed(a.st);  // uniform across the cluster; still take part in the sync
-  // ---- phase A: y on the owned rows (identity block given; Omega rows from the tree)
-  if (!dead) {
-    for (int i = tid; i < nrow; i += STEP_NT) {
-      const int row = r0 + i;
-      if (row < m || !a.tree) yv[i] = a.y[row];
-    }
-    if (a.tree) {
-      const int ob = max(r0, m), oe = r1;
-      for (int row = ob + warp; row < oe; row += nw) {
-        const int o = row - m;
-        const int64_t rhi = __ldg(a.idx + o) >> a.log_tb;
-        const A v = warp_tile_tree<T>((const A*)a.P + (int64_t)o * a.n_tiles, (int)a.n_tiles,
-                                      (int)a.n_eff, rhi);
-        if (lane == 0) {
-          const double y = (double)Lo<T>::mul(v, (A)a.norm_lo);
-          yv[row - r0] = y;
-          a.y[row] = y;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  // ---- phase B: rho = ||y[c:]|| (rhqr.py:72); partials pushed to every CTA
-  double p = 0.0;
-  if (!dead)
-    for (int i = tid; i < nrow; i += STEP_NT)
-      if (r0 + i >= c) p = fma(yv[i], yv[i], p);
-  p = block_sum(p, red);
-  if (tid < STEP_CL) *cluster.map_shared_rank(&part[rank], tid) = p;
-  cluster.sync();
-  if (dead) return;
-  if (tid == 0) {
-    double r2 = 0.0;
-    for (int q = 0; q < STEP_CL; ++q) r2 += part[q];
-    const double rho = sqrt(r2);
-    const double yc = a.y[c];
-    const double sigma = yc >= 0.0 ? 1.0 : -1.0;                                 // linalg.py:200-202
-    const double gamma = __dadd_rn(yc, sigma * rho);                               // rhqr.py:76
-    const double beta = __ddiv_rn(1.0, __dmul_rn(__dmul_rn(rho, sigma), gamma));   // :77
-    bool bad = false;
-    if (rho == 0.0) { bad = true; if (rank == 0) fail(a.st, SQB_ERR_BREAKDOWN, c + 1, 0.0); }
-    else if (!isfinite(beta)) { bad = true; if (rank == 0) fail(a.st, SQB_ERR_BREAKDOWN, c + 1, rho); }
-    double f, bo;
-    if (a.scaling == SQB_SCALE_SQRT2) { f = __dsqrt_rn(beta); bo = 1.0; }
-    else { f = gamma; bo = __ddiv_rn(__dmul_rn(sigma, gamma), rho); }
-    scal[0] = -sigma * rho; scal[1] = gamma; scal[2] = f; scal[3] = bad ? -1.0 : bo;
-    if (rank == 0 && !bad) {
-      a.sigmas[c] = sigma; a.rhos[c] = rho; a.betas[c] = bo;
-      *a.fscale = f;
-    }
-  }
-  __syncthreads();
-  const double rdiag = scal[0], gamma = scal[1], f = scal[2], bo = scal[3];
-  // a breakdown is seen identically by every CTA: leave together (no more DSMEM)
-  if (bo < 0.0) return;
-  const bool sq = a.scaling == SQB_SCALE_SQRT2;
-  // ---- phase C: s = Psi u (rhqr.py:83-96), u's identity-block rows, R column (:248-249)
-  T* U = (T*)a.U;
-  for (int i = tid; i < nrow; i += STEP_NT) {
-    const int row = r0 + i;
-    const double yh = row < c ? 0.0 : (row == c ? gamma : yv[i]);
-    const double s = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
-    sv[i] = s;
-    a.S[row + (int64_t)c * a.lds] = s;
-    if (row < m) {
-      U[row + (int64_t)c * a.ldu] = Lo<T>::store(Lo<T>::from_double(s));
-      a.R[row + (int64_t)c * a.ldr] = row < c ? yv[i] : (row == c ? rdiag : 0.0);
-    }
-  }
-  // partial vector over the owned rows >= c (s vanishes above c):
-  // v[k] = S[:, k]^t s (k < c), d = s^t y0_{c+1}; staged through smem, pushed to rank 0
-  const bool has_next = c + 1 < m;
-  const double* y0n = has_next ? a.Y0 + (int64_t)(c + 1) * od : nullptr;
-  const int nkk = has_next ? nk : c;
-  const int rs = max(r0, c), nr = max(0, r1 - rs), ls = rs - r0;
-  double* dst0 = cluster.map_shared_rank(gath, 0) + rank * nk;
-  for (int k0 = 0; k0 < nkk; k0 += STEP_KC) {
-    const int kc = min(STEP_KC, nkk - k0);
-    __syncthreads();
-#pragma unroll 4
-    for (int e = tid; e < nr * kc; e += STEP_NT) {
-      const int i = e % nr, kk = e / nr, k = k0 + kk;
-      const double* col = (k < c) ? a.S + (int64_t)k * a.lds : y0n;
-      stage[kk * ldst + i] = col[rs + i];
-    }
-    __syncthreads();
-    {
-      const int kk = tid % STEP_KC, pp = tid / STEP_KC;
-      double d = 0.0;
-      if (kk < kc)
-        for (int i = pp; i < nr; i += STEP_NPART) d = fma(stage[kk * ldst + i], sv[ls + i], d);
-      cpart[pp * STEP_KC + kk] = d;
-    }
-    __syncthreads();
-    if (tid < kc) {
-      double d = 0.0;
-      for (int q = 0; q < STEP_NPART; ++q) d += cpart[q * STEP_KC + tid];
-      dst0[k0 + tid] = d;
-    }
-  }
-  cluster.sync();
-  if (rank != 0) return;
-  // ---- phase D (rank 0): v_c, and coef_{c+1}[c] = beta (d - v^t a_{c+1})
-  double va = 0.0;
-  for (int k = tid; k < c; k += STEP_NT) {
-    double v = 0.0;
-    for (int q = 0; q < STEP_CL; ++q) v += gath[q * nk + k];
-    a.vbuf[k] = v;
-    if (has_next) va = fma(v, a.anext[k], va);
-  }
-  if (!has_next) return;
-  va = block_sum(va, red);
-  if (tid == 0) {
-    double d = 0.0;
-    for (int q = 0; q < STEP_CL; ++q) d += gath[q * nk + c];
-    a.clast[c + 1] = __dmul_rn(bo, d - va);
-  }
-}
-
-// last column: lazy scaling of its Omega rows + its T column (_extend_t)
-template <typename T>
-__global__ void finish_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t n,
-                              const double* fscale, int scaling, double* Tm, int64_t ldt, int m,
-                              const double* v, const double* betas, const Status* st) {
-  pdl_wait();
-  if (failed(st)) return;
-  if (blockIdx.x == gridDim.x - 1) {
-    complete_t_column(Tm, ldt, m - 1, v, betas[m - 1]);
-    return;
-  }
-  const double f = *fscale;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)(gridDim.x - 1) * blockDim.x)
-    dst[i] = Lo<T>::store(lazy_scale<T>(Lo<T>::load(src[i]), f, scaling));
-}
 
 __global__ void zero_kernel(double* p, int64_t rows, int64_t cols, int64_t ld) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * cols; e += (int64_t)gridDim.x * blockDim.x)
@@ -527,9 +64,13 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
   cudaFuncSetAttribute(rhqr_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(step_smem, 48 * 1024));
   // column 0: y = y0_0 (w = W[:, 0]); a_1 is empty
-  StepArgs sa{0, (int)m, (int)ell, (int)od, scaling, 0, P, g.n_tiles, g.n_eff,
-              srht ? sk->indices : nullptr, g.log_tb, norm_lo, Y0, Y0, S, lds, R, ldr, U, ldu,
-              sigmas, rhos, betas, fs, vbuf, abuf + (1 & 1) * (m + 1), coef, st};
+  StepArgs sa{};
+  sa.c = 0; sa.m = (int)m; sa.ell = (int)ell; sa.od = (int)od; sa.scaling = scaling; sa.tree = 0;
+  sa.gath = nullptr; sa.nranks = 1; sa.rank_level = 0;
+  sa.P = P; sa.n_tiles = g.n_tiles; sa.n_eff = g.n_eff; sa.idx = srht ? sk->indices : nullptr;
+  sa.log_tb = g.log_tb; sa.norm_lo = norm_lo; sa.y = Y0; sa.Y0 = Y0; sa.S = S; sa.lds = lds;
+  sa.R = R; sa.ldr = ldr; sa.U = U; sa.ldu = ldu; sa.sigmas = sigmas; sa.rhos = rhos; sa.betas = betas;
+  sa.fscale = fs; sa.vbuf = vbuf; sa.anext = abuf + (m + 1); sa.clast = coef; sa.st = st;
   SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT),
                      step_smem, sa));
 
@@ -548,10 +89,14 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
   for (int64_t c = 1; c < m; ++c) {
     double* a_cur = abuf + (c & 1) * (m + 1);
     double* a_nxt = abuf + ((c + 1) & 1) * (m + 1);
-    ColArgs ca{(int)c, (int)m, n, (int)ell, (int)od, log_tb_col, g.n_tiles, n_eff_col, W, ldw, U, ldu,
-               a_cur, coef, fs, scaling, srht ? 1 : 0, srht ? sk->sign_bits : nullptr,
-               srht ? sk->indices : nullptr, scale_lo, P, y, S, lds, Tm, ldt, Y0, vbuf, betas, a_nxt,
-               st};
+    ColArgs ca{};
+    ca.c = (int)c; ca.m = (int)m; ca.mrow = (int)m; ca.e_base = 0; ca.n = n; ca.ell = (int)ell;
+    ca.od = (int)od; ca.log_tb = log_tb_col; ca.n_tiles = g.n_tiles; ca.n_eff = n_eff_col;
+    ca.W = W; ca.ldw = ldw; ca.U = U; ca.ldu = ldu; ca.acur = a_cur; ca.clast = coef; ca.fscale = fs;
+    ca.scaling = scaling; ca.srht = srht ? 1 : 0; ca.bits = srht ? sk->sign_bits : nullptr;
+    ca.idx = srht ? sk->indices : nullptr; ca.scale_lo = scale_lo; ca.P = P; ca.y = y;
+    ca.S = S; ca.lds = lds; ca.T = Tm; ca.ldt = ldt; ca.Y0 = Y0; ca.vprev = vbuf; ca.betas = betas;
+    ca.anext = a_nxt; ca.st = st;
     const size_t smem = sizeof(A) * ((c + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(c + 1));
     prof_begin(ctx);
     SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", colk, dim3((unsigned)(n_eff_col + 2)), dim3(COL_NT), smem,

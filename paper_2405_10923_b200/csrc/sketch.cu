@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(SRHT_NT)
 srht_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int log_tb,
                  const uint32_t* __restrict__ bits, const int64_t* __restrict__ idx, int ell,
                  typename Lo<T>::acc scale_lo, typename Lo<T>::acc* __restrict__ P,
-                 int64_t n_tiles, const Status* st) {
+                 int64_t n_tiles, const Status* st, int64_t e_base) {
   using A = typename Lo<T>::acc;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   A* sm = reinterpret_cast<A*>(smem_raw);
@@ -120,7 +120,8 @@ srht_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int log_tb,
     const int64_t e = e0 + i;
     A v[VN];
     load_run<T, VN>(x, e, n, v);
-    const uint32_t w = __ldg(bits + (e >> 5)) >> (e & 31);
+    const int64_t eg = e_base + e;  // global Omega coordinate (sign bits)
+    const uint32_t w = __ldg(bits + (eg >> 5)) >> (eg & 31);
 #pragma unroll
     for (int j = 0; j < VN; ++j)
       sm[pidx<A>(i + j)] = (e + j < n) ? srht_in<T>(v[j], scale_lo, (w >> j) & 1u) : A(0);
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(256)
 srht_tree_kernel(const typename Lo<T>::acc* __restrict__ P, int64_t n_tiles, int64_t n_eff,
                  const int64_t* __restrict__ idx, int ell, int log_tb,
                  typename Lo<T>::acc norm_lo, double* __restrict__ Y, int64_t ldy,
-                 int64_t row_off, const Status* st) {
+                 int64_t row_off, const Status* st, int apply_norm) {
   if (st && failed(st)) return;
   const int k = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t col = blockIdx.y;
@@ -143,7 +144,7 @@ srht_tree_kernel(const typename Lo<T>::acc* __restrict__ P, int64_t n_tiles, int
   const int64_t rhi = __ldg(idx + k) >> log_tb;
   const typename Lo<T>::acc v =
       warp_tile_tree<T>(P + (col * ell + k) * n_tiles, (int)n_tiles, (int)n_eff, rhi);
-  if ((threadIdx.x & 31) == 0) Y[row_off + k + col * ldy] = (double)Lo<T>::mul(v, norm_lo);
+  if ((threadIdx.x & 31) == 0) Y[row_off + k + col * ldy] = apply_norm ? (double)Lo<T>::mul(v, norm_lo) : (double)v;
 }
 
 template <typename T>
@@ -175,10 +176,10 @@ size_t sketch_partials_bytes(const sqb_sketch* sk, int dtype, int64_t k) {
 }
 
 template <typename T>
-static int srht_tiles_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int64_t ldx, int64_t k,
-                        void* P, const Status* st) {
+static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int64_t n_local,
+                             int64_t e_base, const void* X, int64_t ldx, int64_t k, void* P,
+                             const Status* st) {
   using A = typename Lo<T>::acc;
-  const SrhtGeom g = srht_geom_t<T>(sk);
   double sc, nm;
   srht_constants(sk, Lo<T>::code, &sc, &nm);
   const size_t smem = tile_smem_bytes<A>(1 << g.log_tb);
@@ -189,15 +190,34 @@ static int srht_tiles_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int64
   if (vec) {
     auto kern = srht_tile_kernel<T, VN>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, SRHT_NT, smem, ctx->stream>>>((const T*)X, ldx, sk->n, g.log_tb, sk->sign_bits,
-                                               sk->indices, (int)sk->ell, (A)sc, (A*)P, g.n_tiles, st);
+    kern<<<grid, SRHT_NT, smem, ctx->stream>>>((const T*)X, ldx, n_local, g.log_tb, sk->sign_bits,
+                                               sk->indices, (int)sk->ell, (A)sc, (A*)P, g.n_tiles, st, e_base);
   } else {
     auto kern = srht_tile_kernel<T, 1>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, SRHT_NT, smem, ctx->stream>>>((const T*)X, ldx, sk->n, g.log_tb, sk->sign_bits,
-                                               sk->indices, (int)sk->ell, (A)sc, (A*)P, g.n_tiles, st);
+    kern<<<grid, SRHT_NT, smem, ctx->stream>>>((const T*)X, ldx, n_local, g.log_tb, sk->sign_bits,
+                                               sk->indices, (int)sk->ell, (A)sc, (A*)P, g.n_tiles, st, e_base);
   }
   return check_launch(ctx, "srht_tile_kernel");
+}
+
+template <typename T>
+static int srht_tiles_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int64_t ldx, int64_t k,
+                        void* P, const Status* st) {
+  return srht_tiles_geom_t<T>(ctx, sk, srht_geom_t<T>(sk), sk->n, 0, X, ldx, k, P, st);
+}
+
+template <typename T>
+static int srht_tree_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, const void* P, int64_t k,
+                            double* Y, int64_t ldy, int64_t row_off, int apply_norm, const Status* st) {
+  using A = typename Lo<T>::acc;
+  double sc, nm;
+  srht_constants(sk, Lo<T>::code, &sc, &nm);
+  dim3 grid((unsigned)((sk->ell + 7) / 8), (unsigned)k);
+  srht_tree_kernel<T><<<grid, 256, 0, ctx->stream>>>((const A*)P, g.n_tiles, g.n_eff, sk->indices,
+                                                     (int)sk->ell, g.log_tb, (A)nm, Y, ldy, row_off, st,
+                                                     apply_norm);
+  return check_launch(ctx, "srht_tree_kernel");
 }
 
 template <typename T>
@@ -209,7 +229,7 @@ static int srht_tree_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* P, int64_
   srht_constants(sk, Lo<T>::code, &sc, &nm);
   dim3 grid((unsigned)((sk->ell + 7) / 8), (unsigned)k);
   srht_tree_kernel<T><<<grid, 256, 0, ctx->stream>>>((const A*)P, g.n_tiles, g.n_eff, sk->indices,
-                                                     (int)sk->ell, g.log_tb, (A)nm, Y, ldy, row_off, st);
+                                                     (int)sk->ell, g.log_tb, (A)nm, Y, ldy, row_off, st, 1);
   return check_launch(ctx, "srht_tree_kernel");
 }
 
@@ -225,6 +245,16 @@ static int srht_tree_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* P, int64_
 int launch_srht_tree(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* P, int64_t k,
                      double* Y, int64_t ldy, int64_t y_row_off, const Status* st) {
   SQB_DISPATCH(dtype, srht_tree_t, ctx, sk, P, k, Y, ldy, y_row_off, st);
+}
+
+int launch_srht_tiles_geom(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const SrhtGeom& g, int64_t n_local,
+                           int64_t e_base, const void* X, int64_t ldx, int64_t k, void* P, const Status* st) {
+  SQB_DISPATCH(dtype, srht_tiles_geom_t, ctx, sk, g, n_local, e_base, X, ldx, k, P, st);
+}
+
+int launch_srht_tree_geom(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const SrhtGeom& g, const void* P,
+                          int64_t k, double* Y, int64_t ldy, int64_t row_off, int apply_norm, const Status* st) {
+  SQB_DISPATCH(dtype, srht_tree_geom_t, ctx, sk, g, P, k, Y, ldy, row_off, apply_norm, st);
 }
 
 template <typename T>

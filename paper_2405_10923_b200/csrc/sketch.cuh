@@ -46,6 +46,15 @@ int launch_sketch(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* X, 
 int launch_srht_tree(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* P, int64_t k,
                      double* Y, int64_t ldy, int64_t y_row_off, const Status* st);
 
+// geometry-explicit SRHT pieces for the row-partitioned (multi-GPU) path: the
+// tile kernel over n_local rows whose first global Omega coordinate is e_base,
+// and the tree over g.n_tiles local tiles (without the final n_pad^-1/2 when
+// apply_norm == 0, i.e. the rank-local subtree).
+int launch_srht_tiles_geom(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const SrhtGeom& g, int64_t n_local,
+                           int64_t e_base, const void* X, int64_t ldx, int64_t k, void* P, const Status* st);
+int launch_srht_tree_geom(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const SrhtGeom& g, const void* P,
+                          int64_t k, double* Y, int64_t ldy, int64_t row_off, int apply_norm, const Status* st);
+
 // Y[0:m, col] = X[0:m, col] as fp64 (identity block of Psi, sketching.py:257)
 int launch_copy_top(sqb_ctx* ctx, int dtype, const void* X, int64_t ldx, int64_t m, int64_t k,
                     double* Y, int64_t ldy, const Status* st);

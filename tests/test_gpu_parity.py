@@ -407,3 +407,29 @@ def test_gmres_convection_diffusion_against_oracle(P):
     # restarted driver reaches the tolerance
     xr, hs = P.rhqr_gmres_restarted(A, b, None, m, om_p, tol=1e-6, max_cycles=200)
     assert np.linalg.norm(b - A @ xr) <= 1e-6 * np.linalg.norm(b)
+
+
+# ---------------------------------------------------------------- multi-GPU path (virtual ranks)
+@pytest.mark.parametrize("nranks", [1, 2, 4, 8])
+def test_row_partitioned_rhqr_bitwise_equals_single_gpu(P, nranks):
+    """The row-partitioned sweep (one all-gather per column, rank-order tree
+    levels) on `nranks` virtual ranks of one B200 reproduces the single-GPU
+    factorization bit for bit."""
+    from paper_2405_10923_b200 import dist
+    N, m = (1 << 16) + 77, 24
+    W = np.random.default_rng(nranks).standard_normal((N, m))
+    om = P.SRHTSketch(96, N - m, 17)
+    F1 = P.rhqr_left(W, om)
+    Fv = dist.rhqr_left_virtual(W, om, nranks)
+    for k in ("R", "S", "T", "U", "sigmas", "rhos", "betas"):
+        assert np.array_equal(getattr(Fv, k), getattr(F1, k)), k
+
+
+def test_row_partitioned_config2_shape(P):
+    from paper_2405_10923_b200 import dist
+    N, m = 1 << 18, 64
+    W = workloads.illcond_w(N, m, 2)
+    om = P.SRHTSketch(128, N - m, 3)
+    F1 = P.rhqr_left(W, om)
+    Fv = dist.rhqr_left_virtual(W, om, 8)
+    assert np.array_equal(Fv.R, F1.R) and np.array_equal(Fv.U, F1.U)

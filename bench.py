@@ -1,24 +1,27 @@
-"""Benchmark: left-looking RHQR (BASELINE config 2) on B200.
+"""Benchmark: randomized Householder QR on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2|cfg1|cfg3|cfg4|cfg5]
 
-A step is one full `rhqr_left` of W (2^20 x 128 fp64, ill-conditioned,
-sigma = logspace(0, -15)) with an SRHT of ell = 256 — the configuration
-BASELINE.json's metric is quoted on.  Prints ONE JSON line on rank 0.
+Default workload = BASELINE config 2: one step is a full `rhqr_left` of W
+(2^20 x 128 fp64 per GPU, sigma = logspace(0,-15)) with an SRHT of ell = 256.
+Prints ONE JSON line on rank 0.
 
-value   effective HBM GB/s = algorithmic bytes (8 N (m^2 + 5m)/2)
-        x ranks / max-over-ranks device time of the K timed steps, W resident
-        in HBM (1 GiB W + 1 GiB U exceed the 126 MB L2, so no flush is needed).
-e2e     the same metric through the public API with host numpy input and host
-        numpy factors returned (H2D of W and D2H of U, S, T, R inside the timer).
-roofline  the dominant kernel (rhqr_col_kernel, the fused GEMV + SRHT-leaf pass)
-        timed per launch with CUDA events on its own stream during the timed
-        steps; peak = MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline  the CPU oracle port (oracle/sketchqr_oracle.py, restating the
-        reference's numpy code) on a bounded sample (2^17 rows, same m, ell).
+value     effective HBM GB/s = algorithmic bytes (config 2: 8 N (m^2 + 5m)/2,
+          SURVEY §8(d)) of the whole job / max-over-ranks device time of the
+          K timed steps; inputs resident in HBM and larger than the 126 MB L2
+          (no flush needed).
+e2e       the same metric through the public API with pinned host input and
+          host numpy factors returned (H2D + D2H inside the timer).
+roofline  the dominant kernel (rhqr_col_kernel: fused GEMV + lazy scaling +
+          SRHT leaves) timed per launch with CUDA events on its own stream over
+          K extra steps; peak = MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the CPU oracle port (oracle/sketchqr_oracle.py) on a bounded
+          sample of the same workload, on this host's cores.
 
-Multi-GPU (torchrun): every rank factors its own W (replicas, weak scaling);
-the row-partitioned version is the next step.
+Multi-GPU (torchrun, N > 1): config 2 runs the row-partitioned factorization
+of a (N*2^20) x 128 W — one NCCL all-gather per column, bitwise identical to
+one GPU (weak scaling); the other workloads run replicas.
 """
 
 from __future__ import annotations
@@ -39,10 +42,12 @@ sys.path.insert(0, ROOT)
 
 CFG = dict(N=1 << 20, m=128, ell=256, w_seed=7, sketch_seed=8)
 CPU_SAMPLE_N = 1 << 17
-METRIC = "rhqr_left effective HBM GB/s (config 2: W 2^20 x 128 fp64, SRHT ell=256)"
+METRIC = "rhqr_left effective HBM GB/s (config 2: W 2^20 x 128 fp64 per GPU, SRHT ell=256)"
+DATA = "synthetic: W = A diag(logspace(0,-15,128)) B, A/B orthonormalised seeded Gaussians"
 
 
 def alg_bytes(N, m, b=8):
+    """rhqr_left algorithmic HBM bytes b*N*(m^2 + 5m)/2."""
     return b * N * (m * m + 5 * m) / 2.0
 
 
@@ -110,17 +115,6 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_oracle_run(N, m, ell, w_seed, sketch_seed):
-    from oracle import sketchqr_oracle as O
-    from paper_2405_10923_b200 import workloads
-
-    W = workloads.illcond_w(N, m, w_seed)
-    om = O.SRHT(ell, N - m, sketch_seed)
-    t0 = time.perf_counter()
-    O.rhqr_left(W, om)
-    return time.perf_counter() - t0
-
-
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -137,30 +131,155 @@ def dist_env():
     return ws, rank, local
 
 
-def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (oracle port) on the host
-    cores, rank 0 only; bounded sample per step."""
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+class Workload:
+    name = ""
+    metric = METRIC
+    dtype = "f64"
+    data = DATA
+    scaling = "weak"
+
+    def cpu_sample(self):
+        """(seconds, algorithmic bytes, description) of one oracle run."""
+        raise NotImplementedError
+
+
+class RHQRLeft(Workload):
+    """rhqr_left on N x m per GPU (configs 1, 2, 4)."""
+
+    def __init__(self, name, N, m, ell, tag, cpu_N, data, metric, w_kind):
+        self.name, self.N, self.m, self.ell, self.tag = name, N, m, ell, tag
+        self.cpu_N, self.data, self.metric, self.w_kind = cpu_N, data, metric, w_kind
+        self.b = 8 if tag == "double" else 2
+        self.dtype = {"double": "f64", "bf16": "bf16"}[tag]
+
+    def make_w(self, rows, seed, device=False):
+        from paper_2405_10923_b200 import workloads
+        if self.w_kind == "illcond":
+            return workloads.illcond_w(rows, self.m, seed)
+        if self.w_kind == "gauss":
+            return workloads.gaussian_w(rows, self.m, seed)
+        import torch  # config 4: seeded device generator (SURVEY §8(d))
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        scales = torch.logspace(0, -8, self.m, dtype=torch.float64, device="cuda")
+        W = torch.randn(self.m, rows, generator=g, device="cuda", dtype=torch.float32).t()
+        return (W.to(torch.float64) * scales[None, :]).to(torch.float32).to(torch.bfloat16)
+
+    def setup(self, ws, rank):
+        import torch
+
+        import paper_2405_10923_b200 as P
+        from paper_2405_10923_b200 import dist as D
+        from paper_2405_10923_b200.devarray import to_device
+        from paper_2405_10923_b200.rhqr import _embed, rhqr_left_device
+        self.ws = ws
+        self.partitioned = ws > 1 and self.name in ("cfg2", "cfg4")
+        Ng = self.N * ws if (self.partitioned and self.name == "cfg2") else self.N
+        self.Ng = Ng
+        m = self.m
+        self.om = P.SRHTSketch(self.ell, Ng - m, CFG["sketch_seed"])
+        pol = P.PrecisionPolicy("double", self.tag)
+        if self.partitioned:
+            rows = D.local_rows(Ng, m, self.om.n_pad, ws, rank, self.tag)
+            W = self.make_w(len(rows), CFG["w_seed"] + rank)
+            self.Wd = to_device(W, self.tag, align_row=m if rank == 0 else 0)
+            D.init_comm()
+            self.step = lambda check=False: D.rhqr_left_distributed(self.Wd, self.om, m, policy=pol, check=check)
+            self.W_host = None
+        else:
+            W = self.make_w(Ng, CFG["w_seed"] + rank)
+            self.W_host = W if not isinstance(W, torch.Tensor) else None
+            self.Wd = to_device(W, self.tag, align_row=m)
+            psi = _embed(self.om, Ng, m)
+            self.step = lambda check=False: rhqr_left_device(self.Wd, psi, "sqrt2", pol, check=check)
+        self.pol = pol
+        self.alg = alg_bytes(Ng, m, self.b)  # whole job
+        self.kernel = "rhqr_col_kernel (fused GEMV over U[:, :c] + lazy scale + SRHT leaves)"
+        self.config = {"workload": f"rhqr_left {self.name}: W {Ng} x {m} {self.tag}, SRHT ell={self.ell}",
+                       "N": Ng, "N_per_gpu": self.N, "m": m, "ell": self.ell, "w_seed": CFG["w_seed"],
+                       "sketch_seed": CFG["sketch_seed"],
+                       "parallelism": (f"row-partitioned x{ws} (1 NCCL all-gather/column)" if self.partitioned
+                                       else (f"replicas x{ws}" if ws > 1 else "single GPU")),
+                       "l2": "no flush: W and U exceed the 126 MB L2",
+                       "alg_bytes_per_step": self.alg}
+        if self.partitioned and self.name == "cfg4":
+            self.scaling = "strong"
+
+    def e2e(self, steps):
+        import torch
+
+        import paper_2405_10923_b200 as P
+        if self.W_host is None or self.partitioned:
+            return None
+        Wp = torch.from_numpy(self.W_host).pin_memory()
+        P.rhqr_left(Wp, self.om, policy=self.pol)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = max(2, min(steps, 5))
+        for _ in range(reps):
+            F = P.rhqr_left(Wp, self.om, policy=self.pol)
+            _ = float(F.R[0, 0])
+        dt = (time.perf_counter() - t0) / reps
+        N, m, ell = self.Ng, self.m, self.ell
+        return {"value": self.alg / dt / 1e9, "unit": "GB/s", "ms_per_step": dt * 1e3,
+                "h2d_bytes_per_step": self.b * N * m,
+                "d2h_bytes_per_step": 8 * (N * m + (m + ell) * m + 2 * m * m + 3 * m),
+                "note": "P.rhqr_left(pinned host W) -> host numpy U,S,T,R; wall clock incl. copies"}
+
+    def cpu_sample(self):
+        from oracle import sketchqr_oracle as O
+        from paper_2405_10923_b200 import workloads
+        N, m = self.cpu_N, self.m
+        if self.w_kind == "illcond":
+            W = workloads.illcond_w(N, m, CFG["w_seed"])
+        elif self.w_kind == "gauss":
+            W = workloads.gaussian_w(N, m, CFG["w_seed"])
+        else:
+            W = workloads.scaled_gaussian_w(N, m, CFG["w_seed"])
+        om = O.SRHT(self.ell, N - m, CFG["sketch_seed"])
+        pol = O.Policy("double", self.tag)
+        t0 = time.perf_counter()
+        O.rhqr_left(W, om, policy=pol)
+        t = time.perf_counter() - t0
+        return t, alg_bytes(N, m, self.b), (f"full rhqr_left on N={N} rows x {m} ({self.tag} storage), "
+                                              f"SRHT {self.ell}")
+
+
+WORKLOADS = {
+    "cfg1": lambda: RHQRLeft("cfg1", 1 << 14, 32, 128, "double", 1 << 14,
+                             "synthetic: W i.i.d. N(0,1) (seeded)",
+                             "rhqr_left effective HBM GB/s (config 1: W 2^14 x 32 fp64, SRHT ell=128)", "gauss"),
+    "cfg2": lambda: RHQRLeft("cfg2", CFG["N"], CFG["m"], CFG["ell"], "double", CPU_SAMPLE_N, DATA, METRIC,
+                             "illcond"),
+    "cfg4": lambda: RHQRLeft("cfg4", 1 << 24, 256, 512, "bf16", 1 << 14,
+                             "synthetic: W N(0,1) x logspace(0,-8) column scales (device torch generator)",
+                             "rhqr_left effective HBM GB/s (config 4: W 2^24 x 256 bf16, SRHT ell=512)",
+                             "scaled"),
+}
+
+
+def run_reference(args, wl):
+    """--impl reference: the reference's CPU algorithm (oracle port) on this
+    host's cores, rank 0 only; each step a bounded sample of the workload."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    N, m, ell = CPU_SAMPLE_N, CFG["m"], CFG["ell"]
     for _ in range(args.warmup):
-        cpu_oracle_run(N, m, ell, CFG["w_seed"], CFG["sketch_seed"])
-    ts = [cpu_oracle_run(N, m, ell, CFG["w_seed"], CFG["sketch_seed"]) for _ in range(args.steps)]
-    t = sum(ts) / len(ts)
-    v = alg_bytes(N, m) / t / 1e9
+        wl.cpu_sample()
+    runs = [wl.cpu_sample() for _ in range(args.steps)]
+    t = sum(r[0] for r in runs) / len(runs)
+    v = runs[0][1] / t / 1e9
     cores = blas_threads()
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": wl.metric, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: W = A diag(logspace(0,-15,128)) B, A/B orthonormalised seeded Gaussians",
-        "config": {"workload": f"rhqr_left cfg2 shape, CPU sample N=2^{N.bit_length() - 1} x 128, SRHT ell=256",
-                   "N": N, "m": m, "ell": ell},
+        "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype, "data": wl.data,
+        "config": {"workload": f"{wl.name} CPU sample: {runs[0][2]}"},
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"full rhqr_left on N={N} rows (config-2 m, ell, sigma); "
-                                   "numpy oracle restating sketchqr (FWHT single-threaded, BLAS "
-                                   f"{cores} threads)"},
+                         "sample": runs[0][2] + f"; numpy oracle port of sketchqr (FWHT single-threaded, "
+                                                f"BLAS {cores} threads)"},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -172,42 +291,30 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
-
+    wl = WORKLOADS[args.workload]()
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args, wl)
         return
+    args.warmup = max(args.warmup, 3)
 
     import torch
     import torch.distributed as dist
 
-    import paper_2405_10923_b200 as P
-    from paper_2405_10923_b200 import _lib, workloads
-    from paper_2405_10923_b200.devarray import to_device
-    from paper_2405_10923_b200.rhqr import _embed, rhqr_left_device
+    from paper_2405_10923_b200 import _lib
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    N, m, ell = CFG["N"], CFG["m"], CFG["ell"]
-    W = workloads.illcond_w(N, m, CFG["w_seed"] + rank)
-    om = P.SRHTSketch(ell, N - m, CFG["sketch_seed"])
-    psi = _embed(om, N, m)
-    pol = P.DOUBLE_POLICY
-    Wd = to_device(W, "double", align_row=m)
+    wl.setup(ws, rank)
     ctx = _lib.context()
     stream = torch.cuda.current_stream()
-
-    def step(check=False):
-        return rhqr_left_device(Wd, psi, "sqrt2", pol, check=check)
-
     for i in range(args.warmup):
-        step(check=(i == 0))
+        wl.step(check=(i == 0))
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -220,90 +327,66 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        step()
+        wl.step()
     e1.record(stream)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     clk = clocks.stop()
     launches = ctx.launches() - l0
-    # roofline pass: the same K steps again with every launch of the dominant
-    # kernel bracketed by CUDA events on its stream (kept out of `value`)
-    ctx.profile(True)
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    for _ in range(args.steps):
-        step()
-    p1.record(stream)
-    torch.cuda.synchronize()
-    k_ms, k_bytes, k_n = ctx.profile_read()
-    ctx.profile(False)
-    prof_step_ms = p0.elapsed_time(p1) / args.steps
     ms = e0.elapsed_time(e1)
     if ws > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = alg_bytes(N, m) * ws / (ms_step * 1e-3) / 1e9
+    value = wl.alg / (ms_step * 1e-3) / 1e9
 
-    # end-to-end through the public API: host numpy in, host numpy factors out
-    e2e = None
-    if not args.no_e2e:
-        Wp = torch.from_numpy(W).pin_memory()
-        P.rhqr_left(Wp, om)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        reps = max(2, min(args.steps, 5))
-        for _ in range(reps):
-            F = P.rhqr_left(Wp, om)
-            _ = float(F.R[0, 0])
-        dt = (time.perf_counter() - t0) / reps
-        d2h = 8 * (N * m + (m + ell) * m + 2 * m * m + 3 * m)
-        e2e = {"value": alg_bytes(N, m) / dt / 1e9, "unit": "GB/s", "ms_per_step": dt * 1e3,
-               "h2d_bytes_per_step": 8 * N * m, "d2h_bytes_per_step": d2h,
-               "note": "P.rhqr_left(pinned host W) -> host numpy U,S,T,R; wall clock incl. copies"}
+    # roofline pass: K more steps with every launch of the dominant kernel
+    # bracketed by CUDA events on the library stream (kept out of `value`)
+    ctx.profile(True)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        wl.step()
+    p1.record(stream)
+    torch.cuda.synchronize()
+    k_ms, k_bytes, k_n = ctx.profile_read()
+    ctx.profile(False)
+    prof_step_ms = p0.elapsed_time(p1) / args.steps
 
+    e2e = None if args.no_e2e else wl.e2e(args.steps)
     peak, peak_kind = measured_peak()
     achieved = (k_bytes / k_n) / (k_ms / k_n * 1e-3) / 1e9 if k_n else None
-    prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = None
     try:
-        with open(prof_path) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tj = json.load(f)
             traffic = {"bytes_per_launch": tj.get("rhqr_col_kernel_bytes_per_launch_c64"),
                        "alg_bytes_per_launch": tj.get("rhqr_col_kernel_alg_bytes_c64"),
-                       "launch": "column c=64 (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)"}
+                       "launch": "config 2, column c=64 (ncu --set full: dram__bytes_read.sum + "
+                                 "dram__bytes_write.sum)"}
     except Exception:
         pass
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        t = cpu_oracle_run(CPU_SAMPLE_N, m, ell, CFG["w_seed"], CFG["sketch_seed"])
+        t, by, desc = wl.cpu_sample()
         cores = blas_threads()
-        cpu = {"value": alg_bytes(CPU_SAMPLE_N, m) / t / 1e9, "unit": "GB/s", "cores": cores,
-               "kind": "port", "seconds": t,
-               "sample": f"full rhqr_left on N={CPU_SAMPLE_N} rows x 128, SRHT 256 (config-2 shape at "
-                         "1/8 rows); numpy oracle port of sketchqr (FWHT single-threaded, "
-                         f"BLAS {cores} threads)"}
+        cpu = {"value": by / t / 1e9, "unit": "GB/s", "cores": cores, "kind": "port", "seconds": t,
+               "sample": desc + f"; numpy oracle port of sketchqr (FWHT single-threaded, BLAS {cores} threads)"}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "metric": wl.metric, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: W = A diag(logspace(0,-15,128)) B, A/B orthonormalised seeded Gaussians",
-            "config": {"workload": "rhqr_left cfg2: W 2^20 x 128 fp64 ill-conditioned, SRHT ell=256",
-                       "N": N, "m": m, "ell": ell, "w_seed": CFG["w_seed"],
-                       "sketch_seed": CFG["sketch_seed"],
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                       "l2": "no flush: W (1 GiB) and U (1 GiB) exceed the 126 MB L2",
-                       "alg_bytes_per_step": alg_bytes(N, m)},
+            "scaling": wl.scaling, "vs_baseline": None, "dtype": wl.dtype, "data": wl.data,
+            "config": wl.config,
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "rhqr_col_kernel (fused GEMV over U[:, :c] + lazy scale + SRHT leaves)",
+                         "kernel": wl.kernel,
                          "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                          "kernel_share_of_step": (k_ms / args.steps) / prof_step_ms if prof_step_ms else None,
                          "timing": "per-launch CUDA events on the library stream over K extra steps",

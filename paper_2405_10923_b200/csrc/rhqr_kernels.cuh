@@ -205,19 +205,46 @@ __global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
     for (int j = 0; j < VN; ++j) acc[v][j] = A(0);
 
   // final columns 0 .. c-2
-  for (int k = 0; k < c - 1; ++k) {
-    const T* col = U + ro + (int64_t)k * a.ldu;
-    const A ck = sc[k];
-    A v0[NV][VN];
+  const int K = c - 1;
+  if (VN > 1 && rows == TB && tb == TB) {
+    // full tile: streaming loads, software-pipelined one column ahead
+    A x0[NV][VN], x1[NV][VN];
+    auto ld = [&](A (&x)[NV][VN], int k) {
+      const T* col = U + ro + (int64_t)k * a.ldu;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int i = (v * COL_NT + threadIdx.x) * VN;
-      if (i < tb) load_run<T, VN>(col, i, rows, v0[v]);
+      for (int v = 0; v < NV; ++v) vload_stream<T>(col + (v * COL_NT + threadIdx.x) * VN, x[v]);
+    };
+    auto fm = [&](A (&x)[NV][VN], int k) {
+      const A ck = sc[k];
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int j = 0; j < VN; ++j) acc[v][j] = fma(x[v][j], ck, acc[v][j]);
+    };
+    if (K > 0) ld(x0, 0);
+    int k = 0;
+    for (; k + 2 <= K; k += 2) {
+      ld(x1, k + 1);
+      fm(x0, k);
+      if (k + 2 < K) ld(x0, k + 2);
+      fm(x1, k + 1);
     }
+    if (k < K) fm(x0, k);
+  } else {
+    for (int k = 0; k < K; ++k) {
+      const T* col = U + ro + (int64_t)k * a.ldu;
+      const A ck = sc[k];
+      A v0[NV][VN];
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
+      for (int v = 0; v < NV; ++v) {
+        const int i = (v * COL_NT + threadIdx.x) * VN;
+        if (i < tb) load_run<T, VN>(col, i, rows, v0[v]);
+      }
 #pragma unroll
-      for (int j = 0; j < VN; ++j) acc[v][j] = fma(v0[v][j], ck, acc[v][j]);
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int j = 0; j < VN; ++j) acc[v][j] = fma(v0[v][j], ck, acc[v][j]);
+    }
   }
   // ---- wait for step c-1 (f_{c-1}, coef_c[c-1], breakdown status)
   pdl_wait();

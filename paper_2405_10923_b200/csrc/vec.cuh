@@ -74,6 +74,32 @@ __device__ __forceinline__ void vstore<__half>(__half* p, const float* in) {
   *reinterpret_cast<uint4*>(p) = v;
 }
 
+// streaming 128-bit load for data that is read-only during the kernel: no L1
+// allocation, 256-byte L2 prefetch granularity
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ void vload_stream(const T* p, typename Lo<T>::acc* out) {
+  const uint4 v = ldg_stream(p);
+  if constexpr (sizeof(T) == 8) {
+    out[0] = __hiloint2double((int)v.y, (int)v.x);
+    out[1] = __hiloint2double((int)v.w, (int)v.z);
+  } else if constexpr (sizeof(T) == 4) {
+    out[0] = __uint_as_float(v.x); out[1] = __uint_as_float(v.y);
+    out[2] = __uint_as_float(v.z); out[3] = __uint_as_float(v.w);
+  } else {
+    const T* h = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out[i] = Lo<T>::load(h[i]);
+  }
+}
+
 // load VN consecutive elements starting at e (relative to p), zero beyond n
 template <typename T, int VN>
 __device__ __forceinline__ void load_run(const T* p, int64_t e, int64_t n,

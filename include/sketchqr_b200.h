@@ -120,6 +120,9 @@ int64_t sqb_ctx_launches(sqb_ctx* ctx);
  * bytes (used by bench.py for the roofline).  enable=0 turns it off. */
 int sqb_ctx_profile(sqb_ctx* ctx, int enable);
 int sqb_ctx_profile_read(sqb_ctx* ctx, double* total_ms, double* total_bytes, int64_t* launches);
+/* Instrumentation: the step kernel of `column` writes per-phase clock64 stamps
+ * (8 per cluster rank) to the device buffer dev_buf (NULL disables). */
+int sqb_debug_step_stamps(sqb_ctx* ctx, long long* dev_buf, int column);
 
 /* ---- sketches ------------------------------------------------------------
  * Y (ell x k, fp64, ldy) = Omega X, X (n x k, `dtype`, ldx), arithmetic in

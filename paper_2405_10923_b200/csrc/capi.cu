@@ -111,6 +111,13 @@ int sqb_ctx_profile_read(sqb_ctx* ctx, double* total_ms, double* total_bytes, in
 
 double sqb_round_scalar(int dtype, double x) { return round_scalar(dtype, x); }
 
+int sqb_debug_step_stamps(sqb_ctx* ctx, long long* dev_buf, int column) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->dbg_ts = dev_buf;
+  ctx->dbg_col = column;
+  return SQB_OK;
+}
+
 int sqb_ctx_status(sqb_ctx* ctx, int* code, int* col, double* val) {
   SQB_TRY(prep(ctx));
   SQB_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(Status), cudaMemcpyDeviceToHost,

@@ -26,6 +26,8 @@ struct sqb_ctx {
   size_t prof_used = 0;
   // NCCL communicator for the row-partitioned path (sqb_ctx_init_comm)
   void* nccl = nullptr;
+  long long* dbg_ts = nullptr;  // instrumentation: step-kernel phase stamps for column dbg_col
+  int dbg_col = -1;
   int nranks = 1;
   int rank = 0;
 };

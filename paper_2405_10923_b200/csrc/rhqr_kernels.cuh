@@ -328,7 +328,11 @@ struct StepArgs {
   const double* anext;        // in: a_{c+1} (helper of pass c)
   double* clast;              // out: clast[c+1] = coef_{c+1}[c]
   Status* st;
+  long long* dbg;             // optional per-phase clock64 stamps [STEP_CL][8] (instrumentation)
 };
+
+#define SQB_STAMP(i) \
+  do { if (a.dbg && threadIdx.x == 0) a.dbg[rank * 8 + (i)] = clock64(); } while (0)
 
 constexpr int STEP_KC = 128;                 // columns staged per chunk
 constexpr int STEP_NPART = STEP_NT / STEP_KC;
@@ -361,8 +365,10 @@ rhqr_step_kernel(StepArgs a) {
   double* part = cpart + STEP_NPART * STEP_KC;       // [STEP_CL] rho^2 partials
   double* red = part + STEP_CL;                      // [32]
   __shared__ double scal[4];
+  SQB_STAMP(0);
   pdl_wait();
   pdl_trigger();
+  SQB_STAMP(1);
   const bool dead = failed(a.st);  // uniform across the cluster; still take part in the sync
   // ---- phase A: y on the owned rows (identity block given; Omega rows from the tree)
   if (!dead) {
@@ -414,6 +420,7 @@ rhqr_step_kernel(StepArgs a) {
     }
   }
   __syncthreads();
+  SQB_STAMP(2);
   // ---- phase B: rho = ||y[c:]|| (rhqr.py:72); partials pushed to every CTA
   double p = 0.0;
   if (!dead)
@@ -422,6 +429,7 @@ rhqr_step_kernel(StepArgs a) {
   p = block_sum(p, red);
   if (tid < STEP_CL) *cluster.map_shared_rank(&part[rank], tid) = p;
   cluster.sync();
+  SQB_STAMP(3);
   if (dead) return;
   if (tid == 0) {
     double r2 = 0.0;
@@ -448,6 +456,7 @@ rhqr_step_kernel(StepArgs a) {
   // a breakdown is seen identically by every CTA: leave together (no more DSMEM)
   if (bo < 0.0) return;
   const bool sq = a.scaling == SQB_SCALE_SQRT2;
+  SQB_STAMP(4);
   // ---- phase C: s = Psi u (rhqr.py:83-96), u's identity-block rows, R column (:248-249)
   T* U = (T*)a.U;
   for (int i = tid; i < nrow; i += STEP_NT) {
@@ -492,7 +501,9 @@ rhqr_step_kernel(StepArgs a) {
       dst0[k0 + tid] = d;
     }
   }
+  SQB_STAMP(5);
   cluster.sync();
+  SQB_STAMP(6);
   if (rank != 0) return;
   // ---- phase D (rank 0): v_c, and coef_{c+1}[c] = beta (d - v^t a_{c+1})
   double va = 0.0;
@@ -509,6 +520,7 @@ rhqr_step_kernel(StepArgs a) {
     for (int q = 0; q < STEP_CL; ++q) d += gath[q * nk + c];
     a.clast[c + 1] = __dmul_rn(bo, d - va);
   }
+  SQB_STAMP(7);
 }
 
 // last column: lazy scaling of its Omega rows + its T column (_extend_t)

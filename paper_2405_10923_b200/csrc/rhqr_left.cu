@@ -108,6 +108,7 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
                             m, P, st));
     sa.c = (int)c;
     sa.y = y;
+    sa.dbg = (c == ctx->dbg_col) ? ctx->dbg_ts : nullptr;
     sa.anext = a_nxt;
     sa.tree = srht ? 1 : 0;
     SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT),

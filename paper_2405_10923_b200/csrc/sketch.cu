@@ -1,5 +1,6 @@
 // Sketch operators on the device: SRHT (K1, bit-exact), dense Gaussian
 // (generic path; the DMMA GEMM lives in dense.cu), identity, embedded.
+#include <algorithm>
 #include <cmath>
 
 #include "sketch.cuh"
@@ -102,7 +103,7 @@ int validate_sketch(sqb_ctx* ctx, const sqb_sketch* sk) {
 // SRHT kernels
 // ---------------------------------------------------------------------------
 template <typename T, int VN>
-__global__ void __launch_bounds__(SRHT_NT)
+__global__ void __launch_bounds__(SRHT_NT, 4)
 srht_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int log_tb,
                  const uint32_t* __restrict__ bits, const int64_t* __restrict__ idx, int ell,
                  typename Lo<T>::acc scale_lo, typename Lo<T>::acc* __restrict__ P,
@@ -119,7 +120,8 @@ srht_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int log_tb,
   for (int i = threadIdx.x * VN; i < tb; i += SRHT_NT * VN) {
     const int64_t e = e0 + i;
     A v[VN];
-    load_run<T, VN>(x, e, n, v);
+    if (VN > 1 && e + VN <= n) vload_stream<T>(x + e, v);
+    else load_run<T, VN>(x, e, n, v);
     const int64_t eg = e_base + e;  // global Omega coordinate (sign bits)
     const uint32_t w = __ldg(bits + (eg >> 5)) >> (eg & 31);
 #pragma unroll
@@ -129,6 +131,117 @@ srht_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int log_tb,
   __syncthreads();
   tile_fwht<T>(sm, log_tb);
   tile_gather<T>(sm, idx, ell, log_tb, P + (col * ell) * n_tiles + t, n_tiles);
+}
+
+// ---------------------------------------------------------------------------
+// fp64 SRHT tile pipeline (K1 for the batched raw sketches and sketch_apply):
+// persistent CTAs stream (tile, column) items; the next item's tile is copied
+// global -> shared with cp.async (coalesced 16-byte chunks, zero-filled past n)
+// while the current one is transformed, so HBM reads overlap the butterflies.
+// Shared layout pads 2 doubles per 16 (keeps 16-byte chunk alignment and makes
+// the radix-16 passes conflict-free: LDS.128 for bits 0-3, 2-way for 4..11).
+// ---------------------------------------------------------------------------
+constexpr int PIPE_NT = 256;
+
+__device__ __forceinline__ int pidx2(int e) { return e + 2 * (e >> 4); }
+
+template <int R>
+__device__ __forceinline__ void fwht_pass2(double* sm, int b, int len) {
+  const int groups = len >> R;
+  const int lowmask = (1 << b) - 1;
+  for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+    const int base = (g & lowmask) | ((g >> b) << (b + R));
+    double v[1 << R];
+#pragma unroll
+    for (int j = 0; j < (1 << R); ++j) v[j] = sm[pidx2(base | (j << b))];
+#pragma unroll
+    for (int s2 = 0; s2 < R; ++s2)
+#pragma unroll
+      for (int j = 0; j < (1 << R); ++j)
+        if (!(j & (1 << s2))) {
+          const double x = v[j], y = v[j | (1 << s2)];
+          v[j] = __dadd_rn(x, y);
+          v[j | (1 << s2)] = __dsub_rn(x, y);
+        }
+#pragma unroll
+    for (int j = 0; j < (1 << R); ++j) sm[pidx2(base | (j << b))] = v[j];
+  }
+}
+
+__global__ void __launch_bounds__(PIPE_NT, 3)
+srht_tile_pipe_kernel(const double* __restrict__ X, int64_t ldx, int64_t n, int log_tb, int64_t n_eff,
+                      int64_t k, const uint32_t* __restrict__ bits, const int64_t* __restrict__ idx, int ell,
+                      double scale_lo, double* __restrict__ P, int64_t n_tiles, const Status* st,
+                      int64_t e_base) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (st && failed(st)) return;
+  const int tb = 1 << log_tb;
+  const int tbp = tb + 2 * (tb >> 4);
+  double* buf0 = reinterpret_cast<double*>(smem_raw);
+  const int64_t items = n_eff * k;
+  auto issue = [&](int64_t item, double* buf) {
+    if (item >= items) return;
+    const int64_t col = item / n_eff, t = item - col * n_eff;
+    const int64_t e0 = t << log_tb;
+    const double* x = X + col * ldx + e0;
+    const int64_t nv = n - e0;
+    for (int q = threadIdx.x; q < (tb >> 1); q += PIPE_NT) {
+      const int e = 2 * q;
+      double* d = buf + pidx2(e);
+      if (e + 2 <= nv) cp_async16(d, x + e, 16);
+      else if (e < nv) cp_async16(d, x + e, 8);
+      else { d[0] = 0.0; d[1] = 0.0; }
+    }
+  };
+  int64_t item = blockIdx.x;
+  issue(item, buf0);
+  cp_async_commit_group();
+  for (int it = 0; item < items; ++it, item += gridDim.x) {
+    double* cur = buf0 + (it & 1) * tbp;
+    double* nxt = buf0 + ((it + 1) & 1) * tbp;
+    issue(item + gridDim.x, nxt);
+    cp_async_commit_group();
+    cp_async_wait_group<1>();
+    __syncthreads();
+    const int64_t col = item / n_eff, t = item - col * n_eff;
+    const int64_t e0 = t << log_tb;
+    // pass 0: scale, signs (sketching.py:152-153), stages h = 1..8 in registers
+    for (int g = threadIdx.x; g < (tb >> 4); g += PIPE_NT) {
+      double* p = cur + pidx2(g << 4);
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double2 d = *reinterpret_cast<const double2*>(p + 2 * q);
+        v[2 * q] = d.x;
+        v[2 * q + 1] = d.y;
+      }
+      const int64_t e = e0 + (g << 4);
+      const int64_t eg = e_base + e;
+      const uint32_t w = __ldg(bits + (eg >> 5)) >> (eg & 31);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const double sv = __dmul_rn(v[j], scale_lo);
+        v[j] = (e + j < n) ? (((w >> j) & 1u) ? -sv : sv) : 0.0;
+      }
+      reg_fwht16<double>(v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) *reinterpret_cast<double2*>(p + 2 * q) = make_double2(v[2 * q], v[2 * q + 1]);
+    }
+    __syncthreads();
+    for (int b = 4; b < log_tb; b += 4) {
+      const int r = log_tb - b;
+      if (r >= 4) fwht_pass2<4>(cur, b, tb);
+      else if (r == 3) fwht_pass2<3>(cur, b, tb);
+      else if (r == 2) fwht_pass2<2>(cur, b, tb);
+      else fwht_pass2<1>(cur, b, tb);
+      __syncthreads();
+    }
+    const int64_t mask = tb - 1;
+    double* leaves = P + (col * ell) * n_tiles + t;
+    for (int kk = threadIdx.x; kk < ell; kk += PIPE_NT) leaves[kk * n_tiles] = cur[pidx2((int)(__ldg(idx + kk) & mask))];
+    __syncthreads();
+  }
+  cp_async_wait_group<0>();
 }
 
 template <typename T>
@@ -187,9 +300,29 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
   const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && (ldx % VN == 0) &&
                    (g.log_tb >= 3);
   dim3 grid((unsigned)g.n_eff, (unsigned)k);
+  if constexpr (sizeof(T) == 8) {
+    if (vec && g.log_tb >= 4 && (e_base & 15) == 0) {
+      const int tb = 1 << g.log_tb;
+      const size_t psmem = 2 * sizeof(double) * (size_t)(tb + 2 * (tb >> 4));
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(srht_tile_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(80 << 10));
+        cudaFuncSetAttribute(srht_tile_pipe_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        attr = true;
+      }
+      const int64_t items = g.n_eff * k;
+      const unsigned gp = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, 3 * (int64_t)ctx->sm_count));
+      srht_tile_pipe_kernel<<<gp, PIPE_NT, psmem, ctx->stream>>>(
+          (const double*)X, ldx, n_local, g.log_tb, g.n_eff, k, sk->sign_bits, sk->indices, (int)sk->ell, sc,
+          (double*)P, g.n_tiles, st, e_base);
+      return check_launch(ctx, "srht_tile_pipe_kernel");
+    }
+  }
   if (vec) {
     auto kern = srht_tile_kernel<T, VN>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     kern<<<grid, SRHT_NT, smem, ctx->stream>>>((const T*)X, ldx, n_local, g.log_tb, sk->sign_bits,
                                                sk->indices, (int)sk->ell, (A)sc, (A*)P, g.n_tiles, st, e_base);
   } else {

@@ -75,16 +75,40 @@ __device__ __forceinline__ void fwht_pass(typename Lo<T>::acc* sm, int b, int le
   }
 }
 
-// full in-tile FWHT (stages h = 1 .. len/2 in order); caller has synced
+// in-tile FWHT stages h = 2^b0 .. len/2 in order as radix-16 passes (one smem
+// round trip per 4 stages); caller has synced
 template <typename T>
-__device__ __forceinline__ void tile_fwht(typename Lo<T>::acc* sm, int log_len) {
+__device__ __forceinline__ void tile_fwht_from(typename Lo<T>::acc* sm, int b0, int log_len) {
   const int len = 1 << log_len;
-  for (int b = 0; b < log_len; b += 3) {
+  for (int b = b0; b < log_len; b += 4) {
     const int r = log_len - b;
-    if (r >= 3) fwht_pass<T, 3>(sm, b, len);
+    if (r >= 4) fwht_pass<T, 4>(sm, b, len);
+    else if (r == 3) fwht_pass<T, 3>(sm, b, len);
     else if (r == 2) fwht_pass<T, 2>(sm, b, len);
     else fwht_pass<T, 1>(sm, b, len);
     __syncthreads();
+  }
+}
+
+// full in-tile FWHT (stages h = 1 .. len/2 in order)
+template <typename T>
+__device__ __forceinline__ void tile_fwht(typename Lo<T>::acc* sm, int log_len) {
+  tile_fwht_from<T>(sm, 0, log_len);
+}
+
+// stages h = 1, 2, 4, 8 on 16 consecutive elements held in registers
+template <typename T>
+__device__ __forceinline__ void reg_fwht16(typename Lo<T>::acc* v) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (!(j & (1 << s))) {
+        const typename Lo<T>::acc x = v[j], y = v[j | (1 << s)];
+        v[j] = Lo<T>::add(x, y);
+        v[j | (1 << s)] = Lo<T>::sub(x, y);
+      }
+    }
   }
 }
 
@@ -112,67 +136,65 @@ __device__ __forceinline__ void tile_gather(const typename Lo<T>::acc* sm, const
 }
 
 // Tree over tile leaves for output k, done by one warp.  leaves[t] for
-// t < n_eff, +0 for n_eff <= t < n_tiles (all-padding tiles).  Tile t is held
-// by lane (t & 31), slot (t >> 5): the low 5 tree levels are lane shuffles,
-// the upper levels a sequential binary-counter tree over slots — both in
-// level order, left operand = lower tile index.
-// Slots are consumed in chunks of up to 8 whose loads are all issued before
-// any arithmetic (8 loads in flight per lane); the in-chunk levels run on
-// registers, chunks combine through a binary-counter stack.
+// t < n_eff, +0 for n_eff <= t < n_tiles (all-padding tiles).  Lane L owns the
+// S = n_tiles/32 CONSECUTIVE tiles [L*S, (L+1)*S): the low log2(S) tree levels
+// run in registers (chunks of 8 whose loads are issued together, then a
+// binary-counter stack across chunks), the top 5 levels are lane shuffles —
+// all in level order with the lower tile range as the left operand.
 template <typename T>
 __device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<T>::acc* leaves,
                                                               int n_tiles, int n_eff, int64_t rhi) {
   using A = typename Lo<T>::acc;
   const int lane = threadIdx.x & 31;
-  int low_levels = 0;
-  while ((1 << low_levels) < n_tiles && low_levels < 5) ++low_levels;
-  const int slots = n_tiles > 32 ? (n_tiles >> 5) : 1;  // power of two
-  const int ch = slots < 8 ? slots : 8;
+  const int S = n_tiles >= 32 ? (n_tiles >> 5) : 1;     // tiles per lane (power of two)
+  const int lanes = n_tiles >= 32 ? 32 : n_tiles;        // lanes holding tiles
+  int sub = 0;
+  while ((1 << sub) < S) ++sub;
+  const int ch = S < 8 ? S : 8;
   int lch = 0;
   while ((1 << lch) < ch) ++lch;
+  const int t0 = lane * S;
   A stk[16];
-  for (int j0 = 0; j0 < slots; j0 += ch) {
-    A v[8];
+  A lv = A(0);
+  if (lane < lanes) {
+    for (int j0 = 0; j0 < S; j0 += ch) {
+      A v[8];
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      const int t = lane + ((j0 + jj) << 5);
-      v[jj] = (jj < ch && t < n_eff) ? leaves[t] : A(0);
-    }
+      for (int jj = 0; jj < 8; ++jj) {
+        const int t = t0 + j0 + jj;
+        v[jj] = (jj < ch && t < n_eff) ? leaves[t] : A(0);
+      }
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      if (jj < ch) {
-        A x = v[jj];
-        for (int l = 0; l < low_levels; ++l) {
-          const A o = __shfl_xor_sync(0xffffffffu, x, 1 << l);
-          const bool upper = (lane >> l) & 1;
-          const A a = upper ? o : x, b = upper ? x : o;
-          x = ((rhi >> l) & 1) ? Lo<T>::sub(a, b) : Lo<T>::add(a, b);
+      for (int l = 0; l < 3; ++l) {
+        if ((1 << l) < ch) {
+          const bool neg = (rhi >> l) & 1;
+#pragma unroll
+          for (int jj = 0; jj < 8; jj += (2 << l))
+            if (jj + (1 << l) < ch)
+              v[jj] = neg ? Lo<T>::sub(v[jj], v[jj + (1 << l)]) : Lo<T>::add(v[jj], v[jj + (1 << l)]);
         }
-        v[jj] = x;
       }
-    }
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      if ((1 << l) < ch) {
-        const bool neg = (rhi >> (5 + l)) & 1;
-#pragma unroll
-        for (int jj = 0; jj < 8; jj += (2 << l))
-          if (jj + (1 << l) < ch)
-            v[jj] = neg ? Lo<T>::sub(v[jj], v[jj + (1 << l)]) : Lo<T>::add(v[jj], v[jj + (1 << l)]);
+      A cv = v[0];
+      const int q = j0 >> lch;
+      int lvl = 0;
+      while ((q >> lvl) & 1) {
+        cv = ((rhi >> (lch + lvl)) & 1) ? Lo<T>::sub(stk[lvl], cv) : Lo<T>::add(stk[lvl], cv);
+        ++lvl;
       }
+      stk[lvl] = cv;
     }
-    A cv = v[0];
-    const int q = j0 >> lch;
-    int lvl = 0;
-    while ((q >> lvl) & 1) {
-      cv = ((rhi >> (5 + lch + lvl)) & 1) ? Lo<T>::sub(stk[lvl], cv) : Lo<T>::add(stk[lvl], cv);
-      ++lvl;
-    }
-    stk[lvl] = cv;
+    int top = 0;
+    while ((ch << top) < S) ++top;
+    lv = stk[top];
   }
-  int top = 0;
-  while ((ch << top) < slots) ++top;
-  return __shfl_sync(0xffffffffu, stk[top], 0);
+  // lane levels sub .. sub + log2(lanes) - 1
+  for (int l = 0; (1 << l) < lanes; ++l) {
+    const A o = __shfl_xor_sync(0xffffffffu, lv, 1 << l);
+    const bool upper = (lane >> l) & 1;
+    const A a = upper ? o : lv, b = upper ? lv : o;
+    lv = ((rhi >> (sub + l)) & 1) ? Lo<T>::sub(a, b) : Lo<T>::add(a, b);
+  }
+  return __shfl_sync(0xffffffffu, lv, 0);
 }
 
 }  // namespace sqb

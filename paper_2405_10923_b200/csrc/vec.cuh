@@ -100,6 +100,15 @@ __device__ __forceinline__ void vload_stream(const T* p, typename Lo<T>::acc* ou
   }
 }
 
+// cp.async (LDGSTS): 16-byte global -> shared copy; src_bytes < 16 zero-fills the rest
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 // load VN consecutive elements starting at e (relative to p), zero beyond n
 template <typename T, int VN>
 __device__ __forceinline__ void load_run(const T* p, int64_t e, int64_t n,

@@ -4,6 +4,7 @@
 
 #include "sketch.cuh"
 #include "vec.cuh"
+#include "gemv.cuh"
 
 namespace sqb {
 
@@ -35,12 +36,41 @@ coef_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict_
   }
 }
 
-// Out[:, col] = fl(X[:, col] - fl(U C_lo[:, col]))  (rhqr.py:118)
+// Out[:, col] = fl(X[:, col] - fl(U C_lo[:, col]))  (rhqr.py:118); persistent
+// row blocks, streaming GEMV core (gemv.cuh)
+template <typename T>
+__global__ void __launch_bounds__(GEMV_NT, 2)
+update_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int r, const double* __restrict__ C,
+              int64_t ldc, const T* X, int64_t ldx, T* Out, int64_t ldo, const Status* st) {
+  using A = typename Lo<T>::acc;
+  constexpr int VN = VecN<T>::n, NV = 4;
+  extern __shared__ unsigned char smraw[];
+  A* c = reinterpret_cast<A*>(smraw);
+  if (st && failed(st)) return;
+  const int col = blockIdx.y;
+  for (int k = threadIdx.x; k < r; k += blockDim.x) c[k] = Lo<T>::from_double(C[k + (int64_t)col * ldc]);
+  __syncthreads();
+  const int64_t rows_per = (int64_t)GEMV_NT * NV * VN;
+  for (int64_t r0 = (int64_t)blockIdx.x * rows_per; r0 < N; r0 += (int64_t)gridDim.x * rows_per) {
+    A acc[NV][VN];
+    gemv_rows<T, NV>(U, ldu, r0, N, r, c, acc);
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int j = 0; j < VN; ++j) {
+        const int64_t i = r0 + (v * GEMV_NT + threadIdx.x) * VN + j;
+        if (i < N)
+          Out[i + (int64_t)col * ldo] =
+              Lo<T>::store(Lo<T>::sub(Lo<T>::load(X[i + (int64_t)col * ldx]), Lo<T>::rnd(acc[v][j])));
+      }
+  }
+}
+
+// unaligned fallback
 template <typename T>
 __global__ void __launch_bounds__(256)
-update_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int r, const double* __restrict__ C,
-              int64_t ldc, const T* __restrict__ X, int64_t ldx, T* __restrict__ Out, int64_t ldo,
-              const Status* st) {
+update_scalar_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int r, const double* __restrict__ C,
+                     int64_t ldc, const T* X, int64_t ldx, T* Out, int64_t ldo, const Status* st) {
   using A = typename Lo<T>::acc;
   extern __shared__ unsigned char smraw[];
   A* c = reinterpret_cast<A*>(smraw);
@@ -84,9 +114,18 @@ static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, con
   coef_kernel<<<(unsigned)k, 256, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od,
                                                                      (int)od, (int)r, C, r, st);
   SQB_TRY(check_launch(ctx, "coef_kernel"));
-  dim3 grid((unsigned)std::min<int64_t>((N + 255) / 256, 4 * 148), (unsigned)k);
-  update_kernel<T><<<grid, 256, sizeof(typename Lo<T>::acc) * r, ctx->stream>>>(
-      (const T*)U, ldu, N, (int)r, C, r, (const T*)X, ldx, (T*)Out, ldo, st);
+  constexpr int VN = VecN<T>::n;
+  const bool vec = ((reinterpret_cast<uintptr_t>(U) & 15) == 0) && (ldu % VN == 0);
+  if (vec) {
+    const int64_t blocks = (N + (int64_t)GEMV_NT * 4 * VN - 1) / ((int64_t)GEMV_NT * 4 * VN);
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, 2 * (int64_t)ctx->sm_count)), (unsigned)k);
+    update_kernel<T><<<grid, GEMV_NT, sizeof(typename Lo<T>::acc) * r, ctx->stream>>>(
+        (const T*)U, ldu, N, (int)r, C, r, (const T*)X, ldx, (T*)Out, ldo, st);
+  } else {
+    dim3 grid((unsigned)std::min<int64_t>((N + 255) / 256, 4 * 148), (unsigned)k);
+    update_scalar_kernel<T><<<grid, 256, sizeof(typename Lo<T>::acc) * r, ctx->stream>>>(
+        (const T*)U, ldu, N, (int)r, C, r, (const T*)X, ldx, (T*)Out, ldo, st);
+  }
   return check_launch(ctx, "update_kernel");
 }
 

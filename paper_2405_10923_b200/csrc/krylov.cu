@@ -19,6 +19,7 @@
 #include "pdl.cuh"
 #include "sketch.cuh"
 #include "vec.cuh"
+#include "gemv.cuh"
 #include "dense.cuh"
 
 namespace sqb {
@@ -195,12 +196,14 @@ __global__ void __launch_bounds__(ARN_NT) arn_step_kernel(ArnArgs a) {
 
 // q = e_j - lo(U_j coef) (krylov.py:137-139); lazy scaling of U[:, j-1] rows >= mt;
 // q_lo = round(q) feeds the matvec, Q[:, j-1] = q (fp64) when stored.
-template <typename T, int VN>
-__global__ void __launch_bounds__(256)
+// Streaming GEMV core over the final columns 0..j-2 (gemv.cuh).
+template <typename T>
+__global__ void __launch_bounds__(GEMV_NT, 2)
 arn_q_kernel(int64_t n, int mt, int j, T* U, int64_t ldu, const double* __restrict__ coefq,
              const double* __restrict__ fscale, int scaling, T* __restrict__ q, double* __restrict__ Q,
              const Status* st) {
   using A = typename Lo<T>::acc;
+  constexpr int VN = VecN<T>::n, NV = 4;
   extern __shared__ unsigned char smraw[];
   A* c = reinterpret_cast<A*>(smraw);
   if (failed(st)) return;
@@ -208,45 +211,29 @@ arn_q_kernel(int64_t n, int mt, int j, T* U, int64_t ldu, const double* __restri
   __syncthreads();
   const double f = *fscale;
   const int jj = j - 1;
-  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * VN; i0 < n;
-       i0 += (int64_t)gridDim.x * blockDim.x * VN) {
-    A acc[VN], x[VN];
+  T* uj = U + (int64_t)jj * ldu;
+  const int64_t rows_per = (int64_t)GEMV_NT * NV * VN;
+  for (int64_t r0 = (int64_t)blockIdx.x * rows_per; r0 < n; r0 += (int64_t)gridDim.x * rows_per) {
+    A acc[NV][VN];
+    gemv_rows<T, NV>(U, ldu, r0, n, jj, c, acc);
 #pragma unroll
-    for (int e = 0; e < VN; ++e) acc[e] = A(0);
-    for (int k = 0; k < jj; ++k) {
-      load_run<T, VN>(U + (int64_t)k * ldu, i0, n, x);
+    for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int e = 0; e < VN; ++e) acc[e] = fma(x[e], c[k], acc[e]);
-    }
-    // column j-1: rows >= mt hold the unscaled w; scale and write back
-    T* uj = U + (int64_t)jj * ldu;
-    load_run<T, VN>(uj, i0, n, x);
-    bool any_low = false;
-#pragma unroll
-    for (int e = 0; e < VN; ++e) {
-      if (i0 + e >= mt) {
-        const double u = scaling == SQB_SCALE_SQRT2 ? __dmul_rn((double)x[e], f) : __ddiv_rn((double)x[e], f);
-        x[e] = Lo<T>::from_double(u);
-      } else {
-        any_low = true;
-      }
-    }
-    if (!any_low) store_run<T, VN>(uj, i0, n, x);
-    else
-#pragma unroll
-      for (int e = 0; e < VN; ++e)
-        if (i0 + e >= mt && i0 + e < n) uj[i0 + e] = Lo<T>::store(x[e]);
-#pragma unroll
-    for (int e = 0; e < VN; ++e) {
-      acc[e] = fma(x[e], c[jj], acc[e]);
-      const int64_t i = i0 + e;
-      if (i < n) {
-        double qv = -(double)Lo<T>::rnd(acc[e]);
+      for (int e = 0; e < VN; ++e) {
+        const int64_t i = r0 + (v * GEMV_NT + threadIdx.x) * VN + e;
+        if (i >= n) continue;
+        A x = Lo<T>::load(uj[i]);
+        if (i >= mt) {  // Omega rows hold the unscaled w: u = fl(f w) (rhqr.py:86-95)
+          const double u = scaling == SQB_SCALE_SQRT2 ? __dmul_rn((double)x, f) : __ddiv_rn((double)x, f);
+          x = Lo<T>::from_double(u);
+          uj[i] = Lo<T>::store(x);
+        }
+        const A a = fma(x, c[jj], acc[v][e]);
+        double qv = -(double)Lo<T>::rnd(a);
         if (i == jj) qv = qv + 1.0;
         q[i] = Lo<T>::store(Lo<T>::from_double(qv));
         if (Q) Q[i] = qv;
       }
-    }
   }
 }
 
@@ -330,9 +317,11 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
   cudaFuncSetAttribute(arn_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(step_smem, 48 << 10));
   constexpr int VN = VecN<T>::n;
-  const bool vec = ((reinterpret_cast<uintptr_t>(U) & 15) == 0) && (ldu % VN == 0) &&
-                   ((reinterpret_cast<uintptr_t>(q) & 15) == 0);
+  if (!(((reinterpret_cast<uintptr_t>(U) & 15) == 0) && (ldu % VN == 0)))
+    return set_error(ctx, SQB_ERR_ARG, "Arnoldi basis U must be 16-byte aligned with ldu %% %d == 0", VN);
   const unsigned gq = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n / VN + 255) / 256, 4 * 148));
+  const unsigned gg = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((n + (int64_t)GEMV_NT * 4 * VN - 1) / ((int64_t)GEMV_NT * 4 * VN), 2 * (int64_t)ctx->sm_count));
   for (int j = 1; j <= mt; ++j) {
     T* uj = (T*)U + (int64_t)(j - 1) * ldu;
     // the unscaled w becomes column j-1 of U (rows >= mt; the step writes the top rows)
@@ -347,12 +336,8 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
       break;
     }
     double* Qj = Q ? Q + (int64_t)(j - 1) * ldq : nullptr;
-    if (vec)
-      arn_q_kernel<T, VN><<<gq, 256, sizeof(double) * (mt + 1), ctx->stream>>>(n, mt, j, (T*)U, ldu, cq, fs,
-                                                                                 scaling, q, Qj, st);
-    else
-      arn_q_kernel<T, 1><<<gq, 256, sizeof(double) * (mt + 1), ctx->stream>>>(n, mt, j, (T*)U, ldu, cq, fs,
-                                                                                scaling, q, Qj, st);
+    arn_q_kernel<T><<<gg, GEMV_NT, sizeof(double) * (mt + 1), ctx->stream>>>(n, mt, j, (T*)U, ldu, cq, fs,
+                                                                             scaling, q, Qj, st);
     SQB_TRY(check_launch(ctx, "arn_q_kernel"));
     // w = lo(A lo(q))  (krylov.py:140)
     SQB_TRY(matvec_t<T>(ctx, op, q, nullptr, w, t64, P, st));

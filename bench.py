@@ -247,7 +247,108 @@ class RHQRLeft(Workload):
                                               f"SRHT {self.ell}")
 
 
+class RecRHQR(Workload):
+    """Config 3: rec_rhqr of gen_cmatrix(2^22, 64) with a Gaussian ell=256 sketch."""
+
+    name = "cfg3"
+    metric = "rec_rhqr effective GB/s (config 3: gen_cmatrix 2^22 x 64 fp64, Gaussian ell=256)"
+    data = "synthetic: W = gen_cmatrix(2^22, 64) (experiments.py:86-98); G from per-row Philox (seeded)"
+
+    def __init__(self, N=1 << 22, m=64, ell=256, cpu_N=1 << 19):
+        self.N, self.m, self.ell, self.cpu_N = N, m, ell, cpu_N
+
+    def setup(self, ws, rank):
+        import paper_2405_10923_b200 as P
+        from paper_2405_10923_b200 import workloads
+        from paper_2405_10923_b200.devarray import to_device
+        N, m, ell = self.N, self.m, self.ell
+        self.W_host = workloads.gen_cmatrix(N, m)
+        self.Wd = to_device(self.W_host, "double", align_row=m)
+        self.om = P.GaussianSketch(ell, N - m, CFG["sketch_seed"])
+        self.om.desc()  # host Philox rows + upload (one-time, like the reference constructor)
+        self.step = lambda check=False: P.rec_rhqr(self.Wd, self.om)
+        n = N - m
+        # read G (ell x n) and W, write U (SURVEY §8(d): sketch GEMM + reconstruction)
+        self.alg = 8.0 * (ell * n + N * m + N * m)
+        self.flops = 2.0 * ell * n * m
+        self.kernel = "dense_dmma_kernel (FP64 DMMA split-K sketch GEMM)"
+        self.config = {"workload": f"rec_rhqr cfg3: W {N} x {m} fp64 gen_cmatrix, Gaussian ell={ell}",
+                       "N": N, "m": m, "ell": ell, "sketch_seed": CFG["sketch_seed"],
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "l2": "no flush: G (8.6 GB) and W (2.1 GB) exceed L2", "alg_bytes_per_step": self.alg,
+                       "sketch_gflop": self.flops / 1e9}
+
+    def e2e(self, steps):
+        return None
+
+    def cpu_sample(self):
+        from oracle import sketchqr_oracle as O
+        from paper_2405_10923_b200 import workloads
+        N, m = self.cpu_N, self.m
+        W = workloads.gen_cmatrix(N, m)
+        t0 = time.perf_counter()
+        O.rec_rhqr(W, O.Gaussian(self.ell, N - m, CFG["sketch_seed"], materialize=False))
+        t = time.perf_counter() - t0
+        n = N - m
+        return t, 8.0 * (self.ell * n + 2 * N * m), (f"full rec_rhqr on gen_cmatrix({N}, {m}), Gaussian "
+                                                      f"{self.ell} regenerated per apply as the reference does")
+
+
+class GMRESCycle(Workload):
+    """Config 5: one RHQR-GMRES(200) cycle on the 2048^2 convection-diffusion CSR."""
+
+    name = "cfg5"
+    metric = "rhqr_gmres effective GB/s per GMRES(200) cycle (config 5: 2048^2 convection-diffusion, SRHT 400)"
+    data = "synthetic: 5-point -Laplace + (50,50).grad on 2048^2, b ~ N(0,1) (seeded)"
+
+    def __init__(self, k=2048, m=200, ell=400):
+        self.k, self.m, self.ell = k, m, ell
+
+    def setup(self, ws, rank):
+        import torch
+
+        import paper_2405_10923_b200 as P
+        from paper_2405_10923_b200 import workloads
+        k, m = self.k, self.m
+        indptr, indices, data = workloads.convection_diffusion_csr(k)
+        N = k * k
+        self.A = P.CSRMatrix(indptr, indices, data, N)
+        self.b = torch.from_numpy(np.random.default_rng(11 + rank).standard_normal(N)).cuda()
+        self.om = P.SRHTSketch(self.ell, N - m - 1, CFG["sketch_seed"])
+        self.step = lambda check=False: P.rhqr_gmres(self.A, self.b, None, m, self.om)
+        nnz = self.A.nnz
+        self.alg = float(sum(8 * N * (2 * j + 5) for j in range(1, m + 1)) + m * (12 * nnz + 12 * N))
+        self.kernel = "update_kernel / arn_q_kernel (streaming GEMVs over the Krylov reflectors)"
+        self.config = {"workload": f"rhqr_gmres cfg5: one GMRES({m}) cycle, {k}^2 grid CSR (nnz {nnz}), SRHT {self.ell}",
+                       "N": N, "m": m, "ell": self.ell, "nnz": nnz,
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "l2": "no flush: U (6.7 GB) exceeds L2", "alg_bytes_per_step": self.alg}
+
+    def e2e(self, steps):
+        return None
+
+    def cpu_sample(self):
+        import scipy.sparse
+
+        from oracle import sketchqr_oracle as O
+        from paper_2405_10923_b200 import workloads
+        k, msamp = self.k, 8
+        indptr, indices, data = workloads.convection_diffusion_csr(k)
+        N = k * k
+        A = scipy.sparse.csr_matrix((data, indices, indptr), shape=(N, N))
+        b = np.random.default_rng(11).standard_normal(N)
+        om = O.SRHT(self.ell, N - msamp - 1, CFG["sketch_seed"])
+        t0 = time.perf_counter()
+        O.rhqr_arnoldi(A, b, None, msamp, om, store_q=False)
+        t = time.perf_counter() - t0
+        nnz = A.nnz
+        by = float(sum(8 * N * (2 * j + 5) for j in range(1, msamp + 1)) + msamp * (12 * nnz + 12 * N))
+        return t, by, f"first {msamp} Arnoldi steps of the full-size cycle (oracle, {k}^2 grid)"
+
+
 WORKLOADS = {
+    "cfg3": lambda: RecRHQR(),
+    "cfg5": lambda: GMRESCycle(),
     "cfg1": lambda: RHQRLeft("cfg1", 1 << 14, 32, 128, "double", 1 << 14,
                              "synthetic: W i.i.d. N(0,1) (seeded)",
                              "rhqr_left effective HBM GB/s (config 1: W 2^14 x 32 fp64, SRHT ell=128)", "gauss"),

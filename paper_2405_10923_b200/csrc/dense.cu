@@ -1,4 +1,4 @@
-// K2 — dense sketch Y = G X on the FP64 tensor pipe (DMMA, mma.sync m16n8k4 f64).
+// K2 — dense sketch Y = G X on the FP64 tensor pipe (DMMA, mma.sync m16n8k16 f64).
 //
 // Reference: GaussianSketch._apply (sketching.py:109-125): Y = G @ X with G the
 // (ell x n) N(0, 1/ell) matrix (row i from Philox(key=[seed, i]), :100-107;
@@ -16,6 +16,7 @@
 
 #include "dense.cuh"
 #include "sketch.cuh"
+#include "vec.cuh"
 
 namespace sqb {
 
@@ -29,6 +30,17 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// mma.sync m16n8k16 f64 (fragment layout = CuTe SM90_16x8x16_F64F64F64F64_TN):
+// a[v0 + 2 v1] = A(g + 8 v0, t + 4 v1), b[v] = B(t + 4 v, g), c as m16n8k4
+__device__ __forceinline__ void dmma_16x8x16(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+      "{%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+        "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
 
 __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
   asm volatile(
@@ -53,10 +65,29 @@ dense_dmma_kernel(const double* __restrict__ G, int64_t ldg, const double* __res
   const int64_t k1 = std::min<int64_t>(K, k0 + kslab);
   const int nk = (int)((k1 - k0 + DBK - 1) / DBK);
 
+  const bool v16 = ((reinterpret_cast<uintptr_t>(G) | reinterpret_cast<uintptr_t>(X)) & 15) == 0 &&
+                   (ldg % 2 == 0) && (ldx % 2 == 0) && (k0 % 2 == 0) && (k1 % 2 == 0);
   auto load_stage = [&](int s, int kt) {
     const int64_t kb = k0 + (int64_t)kt * DBK;
     double* g = sG + s * DBM * DSTR;
     double* x = sX + s * DBN * DSTR;
+    if (v16) {  // 16-byte chunks (k1 even, so a pair never straddles the slab end)
+      for (int e = tid; e < DBM * DBK / 2; e += DNT) {
+        const int r = e / (DBK / 2), kk = 2 * (e % (DBK / 2));
+        const int64_t gr = m0 + r, gk = kb + kk;
+        double* d = g + r * DSTR + kk;
+        if (gr < M && gk < k1) cp_async16(d, G + gr * ldg + gk, 16);
+        else { d[0] = 0.0; d[1] = 0.0; }
+      }
+      for (int e = tid; e < DBN * DBK / 2; e += DNT) {
+        const int cidx = e / (DBK / 2), kk = 2 * (e % (DBK / 2));
+        const int64_t gc = n0 + cidx, gk = kb + kk;
+        double* d = x + cidx * DSTR + kk;
+        if (gc < N && gk < k1) cp_async16(d, X + gc * ldx + gk, 16);
+        else { d[0] = 0.0; d[1] = 0.0; }
+      }
+      return;
+    }
     for (int e = tid; e < DBM * DBK; e += DNT) {
       const int r = e / DBK, kk = e % DBK;
       const int64_t gr = m0 + r, gk = kb + kk;
@@ -98,19 +129,21 @@ dense_dmma_kernel(const double* __restrict__ G, int64_t ldg, const double* __res
     const double* gs = sG + (kt % DSTAGES) * DBM * DSTR + (wm * 32) * DSTR;
     const double* xs = sX + (kt % DSTAGES) * DBN * DSTR + (wn * 32) * DSTR;
 #pragma unroll
-    for (int k4 = 0; k4 < DBK / 4; ++k4) {
-      double a0[2], a1[2], b0[4];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        a0[mt] = gs[(mt * 16 + g) * DSTR + k4 * 4 + t];
-        a1[mt] = gs[(mt * 16 + g + 8) * DSTR + k4 * 4 + t];
-      }
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) b0[nt] = xs[(nt * 8 + g) * DSTR + k4 * 4 + t];
+    for (int k16 = 0; k16 < DBK / 16; ++k16) {
+      double a[2][8], b[4][4];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(acc[mt][nt], a0[mt], a1[mt], b0[nt]);
+        for (int v = 0; v < 8; ++v)
+          a[mt][v] = gs[(mt * 16 + g + 8 * (v & 1)) * DSTR + k16 * 16 + t + 4 * (v >> 1)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) b[nt][v] = xs[(nt * 8 + g) * DSTR + k16 * 16 + t + 4 * v];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_16x8x16(acc[mt][nt], a[mt], b[nt]);
     }
   }
   cp_async_wait<0>();

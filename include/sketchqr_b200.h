@@ -185,6 +185,19 @@ int sqb_rhqr_left_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int l
                           double* S, int64_t lds, double* T, int64_t ldt, double* R, int64_t ldr,
                           double* sigmas, double* rhos, double* betas, double* scratch);
 
+/* Left-looking Householder QR with compact T of a small fp64 A (p x m) in one
+ * CTA (householder_qr, baselines.py:33-89; the sketch-space QR of recRHQR).
+ * Outputs U (p x m), T, R (m x m), sigmas/rhos/betas; an exactly dependent
+ * column -> SQB_ERR_BREAKDOWN. */
+int sqb_householder_qr(sqb_ctx* ctx, int scaling, const double* A, int64_t lda, int64_t p, int64_t m,
+                       double* U, int64_t ldu, double* T, int64_t ldt, double* R, int64_t ldr,
+                       double* sigmas, double* rhos, double* betas);
+
+/* R X = B for upper-triangular fp64 R (m x m), B/X (m x k) (upper_tri_solve,
+ * linalg.py:102-116); zero/subnormal diagonal -> SQB_ERR_SINGULAR. */
+int sqb_upper_tri_solve(sqb_ctx* ctx, const double* R, int64_t ldr, int64_t m, const double* B,
+                        int64_t ldb, int64_t k, double* X, int64_t ldx);
+
 /* (I - U T S^t Psi) X, or with transpose_t the reflectors in reverse
  * (apply_reflectors_compact, rhqr.py:100-119).  U: N x r (lo), S: (m+ell) x r,
  * T: r x r, X/Out: N x k (lo).  Out may alias X. */

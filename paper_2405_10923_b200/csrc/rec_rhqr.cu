@@ -193,6 +193,116 @@ trsm_rows_generic_kernel(const T* __restrict__ W2, int64_t ldw, int64_t n, int m
   }
 }
 
+// K6 on the tensor pipe: blocked forward substitution X Mfac = W2 (the
+// LAPACK dtrsm blocking): per 64-row tile and 16-column block b,
+//   X_b -= X_{<b} M_{<b,b}          (DMMA m16n8k16, one warp per 16 rows)
+//   X_b  = X_b M_bb^{-1}            (16-step substitution per row, division by M_jj)
+// M (padded to a multiple of 16 with an identity tail) lives in shared memory.
+constexpr int TR_ROWS = 128, TR_NT = 256;
+
+__device__ __forceinline__ void dmma16x8x16(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+      "{%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+        "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TR_NT)
+trsm_dmma_kernel(const T* __restrict__ W2, int64_t ldw, int64_t n, int m, int mp, const double* __restrict__ M,
+                 T* __restrict__ U2, int64_t ldu, const Status* st) {
+  extern __shared__ __align__(16) double tsm[];
+  const int ld = mp + 4;            // Ms: 2-way B-fragment loads
+  const int lx = mp + 1;            // Xs: odd stride -> conflict-free column-wise access
+  double* Ms = tsm;                 // [mp][ld] column-major: Ms[col * ld + row]
+  double* Xs = tsm + mp * ld;       // [TR_ROWS][lx] row-major
+  if (failed(st)) return;
+  for (int e = threadIdx.x; e < mp * mp; e += TR_NT) {
+    const int r = e % mp, c = e / mp;
+    Ms[c * ld + r] = (r < m && c < m) ? M[r + (int64_t)c * m] : (r == c ? 1.0 : 0.0);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int nb = mp / 16;
+  for (int64_t r0 = (int64_t)blockIdx.x * TR_ROWS; r0 < n; r0 += (int64_t)gridDim.x * TR_ROWS) {
+    __syncthreads();
+    if constexpr (sizeof(T) == 8) {
+      // all of the tile's loads in flight at once (cp.async, 8-byte granules)
+      for (int e = threadIdx.x; e < TR_ROWS * mp; e += TR_NT) {
+        const int row = e % TR_ROWS, col = e / TR_ROWS;
+        double* d = &Xs[row * lx + col];
+        if (r0 + row < n && col < m) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(d);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(W2 + r0 + row + (int64_t)col * ldw));
+        } else {
+          *d = 0.0;
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    } else {
+#pragma unroll 8
+      for (int e = threadIdx.x; e < TR_ROWS * mp; e += TR_NT) {
+        const int row = e % TR_ROWS, col = e / TR_ROWS;
+        Xs[row * lx + col] = (r0 + row < n && col < m) ? (double)Lo<T>::load(W2[r0 + row + (int64_t)col * ldw]) : 0.0;
+      }
+    }
+    __syncthreads();
+    const int wr = warp * 16;  // this warp's 16 rows in the DMMA phase
+    for (int b = 0; b < nb; ++b) {
+      if (b > 0) {
+        double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+        for (int kk = 0; kk < b; ++kk) {
+          double a[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) a[v] = Xs[(wr + g + 8 * (v & 1)) * lx + 16 * kk + t + 4 * (v >> 1)];
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            double bb[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) bb[v] = Ms[(16 * b + 8 * nt + g) * ld + 16 * kk + t + 4 * v];
+            dmma16x8x16(acc[nt], a, bb);
+          }
+        }
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              double* p = &Xs[(wr + g + 8 * h) * lx + 16 * b + 8 * nt + 2 * t + q];
+              *p = *p - acc[nt][2 * h + q];
+            }
+      }
+      __syncthreads();
+      // diagonal block: one thread per row, 16-step substitution
+      if (threadIdx.x < TR_ROWS) {
+        double* xr = &Xs[threadIdx.x * lx + 16 * b];
+        double x[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = xr[j];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const double* mj = &Ms[(16 * b + j) * ld + 16 * b];
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < j; ++i) s = fma(x[i], mj[i], s);
+          x[j] = __ddiv_rn(x[j] - s, mj[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) xr[j] = x[j];
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < TR_ROWS * m; e += TR_NT) {
+      const int row = e % TR_ROWS, col = e / TR_ROWS;
+      if (r0 + row < n) U2[r0 + row + (int64_t)col * ldu] = Lo<T>::store(Lo<T>::from_double(Xs[row * lx + col]));
+    }
+  }
+}
+
 template <typename T>
 __global__ void top_from_s_kernel(const double* S, int64_t lds, int m, T* U, int64_t ldu, const Status* st) {
   if (failed(st)) return;
@@ -235,7 +345,13 @@ static int rec_rhqr_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const voi
   T* U2 = (T*)U + m;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, 8 * 148));
   const size_t msm = sizeof(double) * m * m;
-  if (m <= 16) {
+  const int mp = (int)((m + 15) / 16 * 16);
+  const size_t tsm = sizeof(double) * ((size_t)mp * (mp + 4) + (size_t)TR_ROWS * (mp + 1));
+  if (m > 16 && tsm <= 200 * 1024) {
+    cudaFuncSetAttribute(trsm_dmma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + TR_ROWS - 1) / TR_ROWS, 2 * (int64_t)ctx->sm_count));
+    trsm_dmma_kernel<T><<<gt, TR_NT, tsm, ctx->stream>>>(W2, ldw, n, (int)m, mp, M, U2, ldu, st);
+  } else if (m <= 16) {
     trsm_rows_kernel<T, 16><<<grid, 128, msm, ctx->stream>>>(W2, ldw, n, (int)m, M, U2, ldu, st);
   } else if (m <= 32) {
     trsm_rows_kernel<T, 32><<<grid, 128, msm, ctx->stream>>>(W2, ldw, n, (int)m, M, U2, ldu, st);
@@ -265,3 +381,59 @@ int rec_rhqr_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dt
 }
 
 }  // namespace sqb
+
+namespace sqb {
+
+// R X = B by back substitution, one CTA per right-hand side (upper_tri_solve,
+// linalg.py:102-116); a zero/subnormal diagonal raises SingularFactorError
+__global__ void __launch_bounds__(256)
+upper_tri_solve_kernel(const double* __restrict__ R, int64_t ldr, int m, const double* __restrict__ B, int64_t ldb,
+                       double* __restrict__ X, int64_t ldx, Status* st) {
+  __shared__ double red[32];
+  extern __shared__ double x[];
+  if (failed(st)) return;
+  const int col = blockIdx.x;
+  if (threadIdx.x == 0 && col == 0)
+    for (int i = 0; i < m; ++i)
+      if (fabs(R[i + (int64_t)i * ldr]) < DBL_MIN) { fail(st, SQB_ERR_SINGULAR, i + 1, R[i + (int64_t)i * ldr]); break; }
+  for (int i = m - 1; i >= 0; --i) {
+    double part = 0.0;
+    for (int j = i + 1 + threadIdx.x; j < m; j += blockDim.x) part = fma(R[i + (int64_t)j * ldr], x[j], part);
+    const double d = block_sum(part, red);
+    if (threadIdx.x == 0) x[i] = (B[i + (int64_t)col * ldb] - d) / R[i + (int64_t)i * ldr];
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) X[i + (int64_t)col * ldx] = x[i];
+}
+
+}  // namespace sqb
+
+extern "C" int sqb_upper_tri_solve(sqb_ctx* ctx, const double* R, int64_t ldr, int64_t m, const double* B,
+                                   int64_t ldb, int64_t k, double* X, int64_t ldx) {
+  using namespace sqb;
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  if (m < 1 || k < 1) return SQB_OK;
+  upper_tri_solve_kernel<<<(unsigned)k, 256, sizeof(double) * m, ctx->stream>>>(R, ldr, (int)m, B, ldb, X, ldx,
+                                                                               ctx->d_status);
+  return check_launch(ctx, "upper_tri_solve_kernel");
+}
+
+extern "C" int sqb_householder_qr(sqb_ctx* ctx, int scaling, const double* A, int64_t lda, int64_t p, int64_t m,
+                                  double* U, int64_t ldu, double* T, int64_t ldt, double* R, int64_t ldr,
+                                  double* sigmas, double* rhos, double* betas) {
+  using namespace sqb;
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  if (p < m) return set_error(ctx, SQB_ERR_ARG, "need p >= m, got %lld x %lld", (long long)p, (long long)m);
+  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
+    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
+  const size_t hsm = sizeof(double) * (p + 2 * m + 32);
+  if (hsm > 200 * 1024) return set_error(ctx, SQB_ERR_ARG, "householder_qr: p too large for the single-CTA kernel");
+  cudaFuncSetAttribute(hqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(hsm, 48 << 10));
+  hqr_kernel<<<1, HQR_NT, hsm, ctx->stream>>>(A, lda, (int)p, (int)m, scaling, U, ldu, T, ldt, R, ldr, sigmas, rhos,
+                                              betas, ctx->d_status);
+  return check_launch(ctx, "hqr_kernel");
+}

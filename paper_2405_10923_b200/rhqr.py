@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
+from typing import NamedTuple
 
 import numpy as np
 import torch
@@ -220,6 +221,67 @@ def apply_reflectors_compact(U, S, T, X, psi, transpose_t=False, policy=None):
     return res
 
 
+class QRResult(NamedTuple):
+    """baselines.py:25-29."""
+
+    Q: object
+    R: object
+    method: str
+    aux: dict
+
+
+def householder_qr(A, scaling=SCALE_SQRT2, policy=None):
+    """baselines.py:33-89: left-looking Householder QR with compact T of a small
+    (p x m) matrix, one CTA on the device (the sketch-space QR of recRHQR)."""
+    check_scaling(scaling)
+    policy = policy or DOUBLE_POLICY
+    if policy.low != "double" or policy.high != "double":
+        raise NotImplementedError("householder_qr on the device runs in double")
+    host = not is_device(A)
+    Ad = to_device(A, "double")
+    p, m = Ad.shape
+    if p < m:
+        raise ValueError(f"need p >= m, got {p} x {m}")
+    U = empty_colmajor(p, m, "double")
+    T = empty_colmajor(m, m, "double")
+    R = empty_colmajor(m, m, "double")
+    scal = torch.empty(3 * m, dtype=torch.float64, device="cuda")
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_householder_qr(ctx.h, scaling_code(scaling), Ad.data_ptr(), ld_of(Ad), p, m,
+                                            U.data_ptr(), ld_of(U), T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R),
+                                            scal.data_ptr(), scal.data_ptr() + 8 * m, scal.data_ptr() + 16 * m),
+              "sqb_householder_qr")
+    raise_status(ctx, "rec_rhqr")
+    Q = thin_q(RHQRFactors(U=U, S=U, T=T, R=R, psi=None, scaling=scaling, sigmas=None, rhos=None, betas=None))
+    aux = {"U": _out(U, host), "T": _out(T, host), "sigmas": _out(scal[:m], host),
+           "rhos": _out(scal[m:2 * m], host), "betas": _out(scal[2 * m:], host)}
+    return QRResult(Q=_out(Q, host), R=_out(R, host), method="householder", aux=aux)
+
+
+def upper_tri_solve(R, B, policy=None):
+    """linalg.py:102-116: R X = B by back substitution (device)."""
+    host = not (is_device(R) or is_device(B))
+    Rd = to_device(R, "double")
+    vec = (B.dim() == 1) if is_device(B) else (np.ndim(B) == 1)
+    Bd = to_device(B, "double")
+    m, k = Bd.shape
+    X = empty_colmajor(m, k, "double")
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_upper_tri_solve(ctx.h, Rd.data_ptr(), ld_of(Rd), m, Bd.data_ptr(), ld_of(Bd), k,
+                                             X.data_ptr(), ld_of(X)), "sqb_upper_tri_solve")
+    raise_status(ctx, "upper_tri_solve")
+    out = X[:, 0] if vec else X
+    return _out(out, host)
+
+
+def lsq_via_implicit_q(factors, b, policy=None):
+    """rhqr.py:191-199: argmin_x ||Psi(W x - b)|| through the compact form."""
+    policy = policy or DOUBLE_POLICY
+    c = apply_reflectors_compact(factors.U, factors.S, factors.T, b, factors.psi, transpose_t=True, policy=policy)
+    m = factors.R.shape[1]
+    return upper_tri_solve(factors.R, c[:m], policy=policy)
+
+
 def t_factor_from_sketches(S, policy=None):  # pragma: no cover - out of the hot path
     raise NotImplementedError("t_factor_from_sketches belongs to rhqr_right/rhqr_block (SURVEY §8(f))")
 
@@ -259,6 +321,7 @@ def sketch_q(factors):
     return _out(Q, host)
 
 
-__all__ = ["HouseholderStep", "RHQRFactors", "rh_vector", "rhqr_left", "rec_rhqr", "apply_reflectors_compact",
+__all__ = ["HouseholderStep", "RHQRFactors", "QRResult", "householder_qr", "upper_tri_solve",
+           "lsq_via_implicit_q", "rh_vector", "rhqr_left", "rec_rhqr", "apply_reflectors_compact",
            "thin_q", "sketch_q", "SCALE_SQRT2", "SCALE_UNIT", "raise_status", "_embed"]
 _ = C

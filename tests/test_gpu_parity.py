@@ -433,3 +433,48 @@ def test_row_partitioned_config2_shape(P):
     F1 = P.rhqr_left(W, om)
     Fv = dist.rhqr_left_virtual(W, om, 8)
     assert np.array_equal(Fv.R, F1.R) and np.array_equal(Fv.U, F1.U)
+
+
+def test_nccl_row_partitioned_single_rank(P):
+    """Exercises the real NCCL plumbing of the row-partitioned path (dlopen,
+    unique id, communicator, per-column all-gather) with world_size 1."""
+    import os
+    import torch.distributed as dist
+    from paper_2405_10923_b200 import dist as D
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(29400 + os.getpid() % 500))
+    created = False
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1)
+        created = True
+    try:
+        D.init_comm()
+        N, m = (1 << 14) + 5, 16
+        W = np.random.default_rng(0).standard_normal((N, m))
+        om = P.SRHTSketch(64, N - m, 3)
+        Fd = D.rhqr_left_distributed(W, om, m)
+        F1 = P.rhqr_left(W, om)
+        for k in ("R", "S", "T", "U"):
+            assert np.array_equal(getattr(Fd, k), getattr(F1, k)), k
+    finally:
+        if created:
+            dist.destroy_process_group()
+
+
+def test_householder_qr_and_lsq(P):
+    h = golden("householder_80x16")
+    res = P.householder_qr(h["Z"])
+    assert rel(res.Q, h["Q"]) < 1e-13 and rel(res.R, h["R"]) < 1e-13 and rel(res.aux["T"], h["T"]) < 1e-13
+    rng = np.random.default_rng(7)
+    n, m = 700, 6
+    W = rng.standard_normal((n, m))
+    F = P.rhqr_left(W, P.GaussianSketch(28, n - m, 28))
+    x = P.lsq_via_implicit_q(F, W[:, 0])
+    assert np.allclose(x, np.eye(m)[:, 0], atol=1e-12)
+    b = rng.standard_normal(n)
+    Fo = O.rhqr_left(W, O.Gaussian(28, n - m, 28))
+    assert rel(P.lsq_via_implicit_q(F, b), O.lsq_via_implicit_q(Fo, b)) < 1e-11
+    with pytest.raises(P.SingularFactorError):
+        P.upper_tri_solve(np.diag([1.0, 0.0, 2.0]), np.ones(3))
+    with pytest.raises(ValueError):
+        P.householder_qr(np.ones((3, 5)))

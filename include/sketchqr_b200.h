@@ -150,6 +150,33 @@ int sqb_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
                   double* T, int64_t ldt, double* R, int64_t ldr,
                   double* sigmas, double* rhos, double* betas);
 
+/* Blocked left-looking RHQR (rhqr_block, rhqr.py:334-365): panels of
+ * block_size columns; every earlier panel is applied compactly to the panel
+ * (one re-sketch per earlier panel), then the panel is swept with pivot
+ * offset j0.  T receives the panel triangles on its diagonal blocks
+ * (BlockRHQRFactors.panels[k].T) and zeros elsewhere; the stacked compact T
+ * is sqb_t_factor(S).  Other outputs as sqb_rhqr_left.                    */
+int sqb_rhqr_block(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                   const void* W, int64_t N, int64_t m, int64_t ldw, int64_t block_size,
+                   void* U, int64_t ldu, double* S, int64_t lds,
+                   double* T, int64_t ldt, double* R, int64_t ldr,
+                   double* sigmas, double* rhos, double* betas);
+
+/* Right-looking RHQR (rhqr_right, rhqr.py:270-301): per column, sketch the
+ * trailing block, one reflector, rank-1 update of the trailing block; T from
+ * sqb_t_factor(S) at the end.  Arguments as sqb_rhqr_left.                 */
+int sqb_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                   const void* W, int64_t N, int64_t m, int64_t ldw,
+                   void* U, int64_t ldu, double* S, int64_t lds,
+                   double* T, int64_t ldt, double* R, int64_t ldr,
+                   double* sigmas, double* rhos, double* betas);
+
+/* T of the compact form from S = Psi U alone (t_factor_from_sketches,
+ * rhqr.py:122-132): T^{-1} = triu(S^t S, 1) + diag(S^t S)/2, inverted by back
+ * substitution.  S: od x k fp64, T: k x k.  Singular -> SQB_ERR_SINGULAR.  */
+int sqb_t_factor(sqb_ctx* ctx, const double* S, int64_t lds, int64_t od, int64_t k,
+                 double* T, int64_t ldt);
+
 /* Reconstructed RHQR (rec_rhqr, rhqr.py:368-395): one sketch Z = Psi W,
  * Householder QR of Z in fp64 (baselines.py:33-89), Mfac = triu(T^t S^t Z)
  * (zero diagonal -> SQB_ERR_BREAKDOWN with val = -1), U2 = W2 Mfac^{-1} by

@@ -432,6 +432,98 @@ def rhqr_left(W, omega, scaling="sqrt2", policy=DOUBLE):
     return Factors(U, S, T, R, psi, scaling, sg, rh, bt)
 
 
+def t_factor_from_sketches(S, policy=DOUBLE):
+    """rhqr.py:122-132: S^t S = T^{-1} + T^{-t}; T^{-1} = triu(G, 1) + diag(G)/2."""
+    Sh = _cast(np.asarray(S), policy.hi)
+    G = (Sh.T @ Sh).astype(np.float64)
+    Tinv = np.triu(G, 1) + np.diag(np.diagonal(G) / 2.0)
+    return upper_tri_solve(Tinv, np.eye(G.shape[0]), policy=policy)
+
+
+@dataclass
+class BlockPanel:
+    """rhqr.py:304-309."""
+
+    U: np.ndarray
+    S: np.ndarray
+    T: np.ndarray
+    offset: int
+
+
+@dataclass
+class BlockFactors:
+    """rhqr.py:312-331 (BlockRHQRFactors)."""
+
+    panels: list
+    R: np.ndarray
+    psi: Embedded
+    scaling: str
+    sigmas: np.ndarray
+    rhos: np.ndarray
+    betas: np.ndarray
+
+    def stacked(self):
+        U = np.concatenate([p.U for p in self.panels], axis=1)
+        S = np.concatenate([p.S for p in self.panels], axis=1)
+        return Factors(U, S, t_factor_from_sketches(S), self.R, self.psi, self.scaling,
+                       self.sigmas, self.rhos, self.betas)
+
+
+def rhqr_block(W, omega, block_size=32, scaling="sqrt2", policy=DOUBLE):
+    """rhqr.py:334-365: earlier panels applied compactly (one re-sketch per
+    panel, coefficients in high, update in low), then the panel is swept."""
+    if block_size < 1:
+        raise ValueError("block_size must be positive")
+    lo, hi = policy.lo, policy.hi
+    W = np.asarray(W, dtype=np.float64)
+    n, m = W.shape
+    psi = embed(omega, n, m)
+    Wl = round_to(W, policy.low)
+    panels = []
+    R = np.zeros((m, m))
+    sig, rho, bet = np.zeros(m), np.zeros(m), np.zeros(m)
+    for j0 in range(0, m, block_size):
+        j1 = min(j0 + block_size, m)
+        X = Wl[:, j0:j1].copy()
+        for p in panels:
+            Y = psi.apply(X, dtype=lo)
+            coef = _cast(p.T.T, hi) @ (_cast(p.S, hi).T @ _cast(Y, hi))
+            X = (_cast(X, lo) - _cast(p.U, lo) @ _cast(coef, lo)).astype(np.float64)
+        U, S, T, Rp, sg, rh, bt = left_sweep(X, psi, j0, scaling, policy)
+        R[:j1, j0:j1] = Rp
+        sig[j0:j1], rho[j0:j1], bet[j0:j1] = sg, rh, bt
+        panels.append(BlockPanel(U, S, T, j0))
+    return BlockFactors(panels, R, psi, scaling, sig, rho, bet)
+
+
+def rhqr_right(W, omega, scaling="sqrt2", policy=DOUBLE):
+    """rhqr.py:270-301: rank-1 update of the trailing block, re-sketched
+    wholesale at every step; T recovered from S afterwards."""
+    lo, hi = policy.lo, policy.hi
+    W = np.asarray(W, dtype=np.float64)
+    n, m = W.shape
+    psi = embed(omega, n, m)
+    Wl = round_to(W, policy.low)
+    U = np.zeros((n, m))
+    S = np.zeros((psi.out_dim, m))
+    R = np.zeros((m, m))
+    sig, rho, bet = np.zeros(m), np.zeros(m), np.zeros(m)
+    for c in range(m):
+        Y = psi.apply(Wl[:, c:], dtype=lo)
+        st = rh_vector(Wl[:, c], Y[:, 0], c + 1, scaling, policy)
+        U[:, c] = st.u
+        S[:, c] = st.s
+        R[:c, c] = Wl[:c, c]
+        R[c, c] = -st.sigma * st.rho
+        sig[c], rho[c], bet[c] = st.sigma, st.rho, st.beta
+        if c + 1 < m:
+            coef = hi.type(st.beta) * (_cast(st.s, hi) @ _cast(Y[:, 1:], hi))
+            tail = _cast(Wl[:, c + 1:], lo) - np.outer(_cast(st.u, lo), _cast(coef, lo))
+            Wl[:, c + 1:] = tail.astype(np.float64)
+    T = t_factor_from_sketches(S, policy=policy)
+    return Factors(U, S, T, R, psi, scaling, sig, rho, bet)
+
+
 def householder_qr(A, scaling="sqrt2", policy=DOUBLE):
     """baselines.py:33-89: left-looking HQR with compact T (used by recRHQR)."""
     lo, hi = policy.lo, policy.hi

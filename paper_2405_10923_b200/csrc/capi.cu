@@ -17,6 +17,11 @@ int residual_norms_run(sqb_ctx*, const double*, int64_t, const double*, int64_t,
                        int64_t, int64_t, int64_t, double*);
 int sketch_q_run(sqb_ctx*, int, const void*, int64_t, int64_t, const double*, int64_t, const double*,
                  int64_t, int64_t, double*, int64_t);
+int rhqr_block_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t, int64_t,
+                        void*, int64_t, double*, int64_t, double*, int64_t, double*, int64_t, double*, double*,
+                        double*);
+int rhqr_right_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t, void*,
+                        int64_t, double*, int64_t, double*, int64_t, double*, double*, double*);
 int rec_rhqr_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t, void*,
                       int64_t, double*, int64_t, double*, int64_t, double*, int64_t, double*, double*, double*);
 int rh_vector_dispatch(sqb_ctx*, int, int, const void*, int64_t, const double*, int64_t, int64_t, void*,
@@ -176,6 +181,49 @@ int sqb_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
     return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
   return rhqr_left_dispatch(ctx, sk, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, T, ldt, R, ldr,
                             sigmas, rhos, betas);
+}
+
+int sqb_rhqr_block(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, const void* W,
+                   int64_t N, int64_t m, int64_t ldw, int64_t block_size, void* U, int64_t ldu, double* S,
+                   int64_t lds, double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
+                   double* betas) {
+  SQB_TRY(prep(ctx));
+  SQB_TRY(check_dtype(ctx, lo_dtype));
+  SQB_TRY(validate_sketch(ctx, sk));
+  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
+    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
+  if (block_size < 1) return set_error(ctx, SQB_ERR_ARG, "block_size must be positive");
+  if (m < 1) return set_error(ctx, SQB_ERR_ARG, "need at least one column");
+  if (m > 1024) return set_error(ctx, SQB_ERR_ARG, "m=%lld: the device sweep supports up to 1024 columns", (long long)m);
+  if (sk->n != N - m)
+    return set_error(ctx, SQB_ERR_ARG, "sketch takes %lld coordinates, expected n-m=%lld",
+                     (long long)sk->n, (long long)(N - m));
+  if (sk->ell < m) return set_error(ctx, SQB_ERR_ARG, "sampling size below column count");
+  if (ldw < N || ldu < N || lds < m + sk->ell || ldt < m || ldr < m)
+    return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
+  return rhqr_block_dispatch(ctx, sk, scaling, lo_dtype, W, N, m, ldw, block_size, U, ldu, S, lds, T, ldt, R,
+                             ldr, sigmas, rhos, betas);
+}
+
+int sqb_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, const void* W,
+                   int64_t N, int64_t m, int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds,
+                   double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
+                   double* betas) {
+  SQB_TRY(prep(ctx));
+  SQB_TRY(check_dtype(ctx, lo_dtype));
+  SQB_TRY(validate_sketch(ctx, sk));
+  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
+    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
+  if (m < 1) return set_error(ctx, SQB_ERR_ARG, "need at least one column");
+  if (sk->n != N - m)
+    return set_error(ctx, SQB_ERR_ARG, "sketch takes %lld coordinates, expected n-m=%lld",
+                     (long long)sk->n, (long long)(N - m));
+  if (sk->ell < m) return set_error(ctx, SQB_ERR_ARG, "sampling size below column count");
+  if (ldw < N || ldu < N || lds < m + sk->ell || ldt < m || ldr < m)
+    return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
+  SQB_TRY(rhqr_right_dispatch(ctx, sk, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, R, ldr, sigmas, rhos,
+                              betas));
+  return sqb_t_factor(ctx, S, lds, m + sk->ell, m, T, ldt);
 }
 
 int sqb_apply_reflectors(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, int lo_dtype, const void* U,

@@ -192,7 +192,7 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
                        (int)std::max<size_t>(step_smem, 48 * 1024));
   auto step_args = [&](DistRank& d, int c) {
     StepArgs sa{};
-    sa.c = c; sa.m = (int)m; sa.ell = (int)ell; sa.od = (int)od; sa.scaling = scaling;
+    sa.c = c; sa.m = (int)m; sa.off = 0; sa.ncol = (int)m; sa.ell = (int)ell; sa.od = (int)od; sa.scaling = scaling;
     sa.tree = c == 0 ? 0 : 2;
     sa.gath = Gc; sa.nranks = nranks; sa.rank_level = rank_level;
     sa.P = nullptr; sa.n_tiles = tpr; sa.n_eff = 0; sa.idx = sk->indices; sa.log_tb = g.log_tb; sa.norm_lo = norm_lo;
@@ -216,7 +216,7 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
       DistRank& d = rk[r];
       const int64_t n_eff = (d.n_local + tb - 1) / tb;
       ColArgs ca{};
-      ca.c = (int)c; ca.m = (int)m; ca.mrow = d.mrow; ca.e_base = d.e_base; ca.n = d.n_local; ca.ell = (int)ell;
+      ca.c = (int)c; ca.m = (int)m; ca.ncol = (int)m; ca.mrow = d.mrow; ca.e_base = d.e_base; ca.n = d.n_local; ca.ell = (int)ell;
       ca.od = (int)od; ca.log_tb = g.log_tb; ca.n_tiles = tpr; ca.n_eff = n_eff;
       ca.W = d.W; ca.ldw = d.ldw; ca.U = d.U; ca.ldu = d.ldu; ca.acur = d.abuf + (c & 1) * (m + 1);
       ca.clast = d.coef; ca.fscale = d.fs; ca.scaling = scaling; ca.srht = 1; ca.bits = sk->sign_bits;

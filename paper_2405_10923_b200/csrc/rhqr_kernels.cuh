@@ -42,8 +42,9 @@ constexpr int STEP_NT = 512;
 constexpr int STEP_CL = 8;  // cluster size of the step kernel
 
 struct ColArgs {
-  int c;            // current column (>= 1)
-  int m;            // columns of W = identity-block rows of Psi
+  int c;            // current column of the sweep (>= 1)
+  int m;            // identity-block rows of Psi (= columns of the whole W)
+  int ncol;         // columns of this sweep (m, or a panel width for rhqr_block)
   int mrow;         // identity-block rows held in this rank's storage (m on rank 0, else 0)
   int64_t e_base;   // global Omega coordinate of this rank's first local coordinate
   int64_t n;        // Omega input length (N - m)
@@ -139,7 +140,7 @@ __device__ inline void complete_t_column(double* T, int64_t ldt, int kk, const d
 __device__ inline void col_helper(const ColArgs& a, double* g) {
   const int c = a.c;
   complete_t_column(a.T, a.ldt, c - 1, a.vprev, a.betas[c - 1]);
-  if (c + 1 >= a.m) return;
+  if (c + 1 >= a.ncol) return;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* y0 = a.Y0 + (int64_t)(c + 1) * a.od;
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
 // ---------------------------------------------------------------------------
 struct StepArgs {
   int c, m, ell, od;
+  int off, ncol;              // sweep offset (pivot row = off + c) and width (rhqr.py:219-251)
   int scaling;
   int tree;                   // 1: finish the SRHT tree from the tile leaves; 0: y[m:] given;
                               // 2: combine the gathered per-rank partials (multi-GPU)
@@ -353,6 +355,7 @@ rhqr_step_kernel(StepArgs a) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int c = a.c, m = a.m, od = a.od, tid = threadIdx.x;
+  const int pv = a.off + c;  // pivot row j-1 of this column (rhqr.py:233)
   const int lane = tid & 31, warp = tid >> 5, nw = STEP_NT / 32;
   const int B = step_rows(od), ldst = step_ldst(od);
   const int r0 = rank * B, r1 = min(od, r0 + B), nrow = max(0, r1 - r0);
@@ -425,7 +428,7 @@ rhqr_step_kernel(StepArgs a) {
   double p = 0.0;
   if (!dead)
     for (int i = tid; i < nrow; i += STEP_NT)
-      if (r0 + i >= c) p = fma(yv[i], yv[i], p);
+      if (r0 + i >= pv) p = fma(yv[i], yv[i], p);
   p = block_sum(p, red);
   if (tid < STEP_CL) *cluster.map_shared_rank(&part[rank], tid) = p;
   cluster.sync();
@@ -435,13 +438,13 @@ rhqr_step_kernel(StepArgs a) {
     double r2 = 0.0;
     for (int q = 0; q < STEP_CL; ++q) r2 += part[q];
     const double rho = sqrt(r2);
-    const double yc = a.y[c];
+    const double yc = a.y[pv];
     const double sigma = yc >= 0.0 ? 1.0 : -1.0;                                 // linalg.py:200-202
     const double gamma = __dadd_rn(yc, sigma * rho);                               // rhqr.py:76
     const double beta = __ddiv_rn(1.0, __dmul_rn(__dmul_rn(rho, sigma), gamma));   // :77
     bool bad = false;
-    if (rho == 0.0) { bad = true; if (rank == 0) fail(a.st, SQB_ERR_BREAKDOWN, c + 1, 0.0); }
-    else if (!isfinite(beta)) { bad = true; if (rank == 0) fail(a.st, SQB_ERR_BREAKDOWN, c + 1, rho); }
+    if (rho == 0.0) { bad = true; if (rank == 0) fail(a.st, SQB_ERR_BREAKDOWN, pv + 1, 0.0); }
+    else if (!isfinite(beta)) { bad = true; if (rank == 0) fail(a.st, SQB_ERR_BREAKDOWN, pv + 1, rho); }
     double f, bo;
     if (a.scaling == SQB_SCALE_SQRT2) { f = __dsqrt_rn(beta); bo = 1.0; }
     else { f = gamma; bo = __ddiv_rn(__dmul_rn(sigma, gamma), rho); }
@@ -461,21 +464,21 @@ rhqr_step_kernel(StepArgs a) {
   T* U = (T*)a.U;
   for (int i = tid; i < nrow; i += STEP_NT) {
     const int row = r0 + i;
-    const double yh = row < c ? 0.0 : (row == c ? gamma : yv[i]);
+    const double yh = row < pv ? 0.0 : (row == pv ? gamma : yv[i]);
     const double s = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
     sv[i] = s;
     a.S[row + (int64_t)c * a.lds] = s;
     if (row < m) {
       U[row + (int64_t)c * a.ldu] = Lo<T>::store(Lo<T>::from_double(s));
-      a.R[row + (int64_t)c * a.ldr] = row < c ? yv[i] : (row == c ? rdiag : 0.0);
+      a.R[row + (int64_t)c * a.ldr] = row < pv ? yv[i] : (row == pv ? rdiag : 0.0);
     }
   }
   // partial vector over the owned rows >= c (s vanishes above c):
   // v[k] = S[:, k]^t s (k < c), d = s^t y0_{c+1}; staged through smem, pushed to rank 0
-  const bool has_next = c + 1 < m;
+  const bool has_next = c + 1 < a.ncol;
   const double* y0n = has_next ? a.Y0 + (int64_t)(c + 1) * od : nullptr;
   const int nkk = has_next ? nk : c;
-  const int rs = max(r0, c), nr = max(0, r1 - rs), ls = rs - r0;
+  const int rs = max(r0, pv), nr = max(0, r1 - rs), ls = rs - r0;
   double* dst0 = cluster.map_shared_rank(gath, 0) + rank * nk;
   for (int k0 = 0; k0 < nkk; k0 += STEP_KC) {
     const int kc = min(STEP_KC, nkk - k0);

@@ -15,45 +15,71 @@ static int zero2d(sqb_ctx* ctx, double* p, int64_t rows, int64_t cols, int64_t l
   return check_launch(ctx, "zero_kernel");
 }
 
+// workspace of one sweep
+struct SweepWs {
+  WsPlan plan;
+  int64_t chunk;
+  size_t iY0, iy, icoef, iabuf, ivbuf, ifs, iP;
+};
+static SweepWs sweep_ws(const sqb_sketch* sk, int code, int64_t m, int64_t ncol) {
+  SweepWs w;
+  const int64_t od = m + sk->ell;
+  w.chunk = std::max<int64_t>(1, std::min<int64_t>(ncol, (int64_t)(64ll << 20) /
+                              std::max<size_t>(1, sketch_partials_bytes(sk, code, 1))));
+  w.iY0 = w.plan.add(sizeof(double) * od * ncol);
+  w.iy = w.plan.add(sizeof(double) * od);
+  w.icoef = w.plan.add(sizeof(double) * (m + 1));
+  w.iabuf = w.plan.add(sizeof(double) * 2 * (m + 1));
+  w.ivbuf = w.plan.add(sizeof(double) * (m + 1));
+  w.ifs = w.plan.add(sizeof(double) * 2);
+  w.iP = w.plan.add(std::max(sketch_partials_bytes(sk, code, w.chunk), sketch_partials_bytes(sk, code, 1)));
+  return w;
+}
+size_t left_sweep_ws_bytes(const sqb_sketch* sk, int code, int64_t m, int64_t ncol) {
+  return sweep_ws(sk, code, m, ncol).plan.total + 256;
+}
+
 // ---------------------------------------------------------------------------
-// driver
+// driver: the left-looking sweep (_left_sweep, rhqr.py:219-251) over the ncol
+// columns of W, eliminating column c at global index off + c + 1.  m is the
+// identity-block size of Psi (the column count of the whole matrix).  U, S, R,
+// sigmas, rhos and betas point at the sweep's first column; T is ncol x ncol.
+// rhqr_left is the sweep with off = 0, ncol = m.
 // ---------------------------------------------------------------------------
 template <typename T>
-static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W, int64_t N,
-                       int64_t m, int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds,
-                       double* Tm, int64_t ldt, double* R, int64_t ldr, double* sigmas,
-                       double* rhos, double* betas) {
+int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W, int64_t N, int64_t m,
+                 int64_t ldw, int64_t ncol, int64_t off, void* U, int64_t ldu, double* S, int64_t lds,
+                 double* Tm, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
+                 double* betas, void* ws_base) {
   using A = typename Lo<T>::acc;
   const int64_t n = N - m, ell = sk->ell, od = m + ell;
   const bool srht = sk->kind == SQB_SKETCH_SRHT;
   const SrhtGeom g = srht ? srht_geom_t<T>(sk) : SrhtGeom{0, 1, 1};
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(m, (int64_t)(64ll << 20) /
-                                   std::max<size_t>(1, sketch_partials_bytes(sk, Lo<T>::code, 1))));
-  WsPlan plan;
-  const size_t iY0 = plan.add(sizeof(double) * od * m);
-  const size_t iy = plan.add(sizeof(double) * od);
-  const size_t icoef = plan.add(sizeof(double) * (m + 1));
-  const size_t iabuf = plan.add(sizeof(double) * 2 * (m + 1));
-  const size_t ivbuf = plan.add(sizeof(double) * (m + 1));
-  const size_t ifs = plan.add(sizeof(double) * 2);
-  const size_t iP = plan.add(std::max(sketch_partials_bytes(sk, Lo<T>::code, chunk),
-                                      sketch_partials_bytes(sk, Lo<T>::code, 1)));
-  SQB_TRY(ws_reserve(ctx, plan.total));
-  double* Y0 = ws_ptr<double>(ctx, plan, iY0);
-  double* y = ws_ptr<double>(ctx, plan, iy);
-  double* coef = ws_ptr<double>(ctx, plan, icoef);
-  double* abuf = ws_ptr<double>(ctx, plan, iabuf);
-  double* vbuf = ws_ptr<double>(ctx, plan, ivbuf);
-  double* fs = ws_ptr<double>(ctx, plan, ifs);
-  void* P = ws_ptr<void>(ctx, plan, iP);
+  const SweepWs sw = sweep_ws(sk, Lo<T>::code, m, ncol);
+  const int64_t chunk = sw.chunk;
+  const WsPlan& plan = sw.plan;
+  const size_t iY0 = sw.iY0, iy = sw.iy, icoef = sw.icoef, iabuf = sw.iabuf, ivbuf = sw.ivbuf, ifs = sw.ifs,
+               iP = sw.iP;
+  if (!ws_base) {
+    SQB_TRY(ws_reserve(ctx, plan.total));
+    ws_base = ctx->ws;
+  }
+  char* wb = static_cast<char*>(ws_base);
+  double* Y0 = reinterpret_cast<double*>(wb + plan.offs[iY0]);
+  double* y = reinterpret_cast<double*>(wb + plan.offs[iy]);
+  double* coef = reinterpret_cast<double*>(wb + plan.offs[icoef]);
+  double* abuf = reinterpret_cast<double*>(wb + plan.offs[iabuf]);
+  double* vbuf = reinterpret_cast<double*>(wb + plan.offs[ivbuf]);
+  double* fs = reinterpret_cast<double*>(wb + plan.offs[ifs]);
+  void* P = wb + plan.offs[iP];
   Status* st = ctx->d_status;
 
-  SQB_TRY(zero2d(ctx, Tm, m, m, ldt));
+  SQB_TRY(zero2d(ctx, Tm, ncol, ncol, ldt));
   // raw sketches y0 = Psi W (all columns; rhqr.py:240 for every column)
-  SQB_TRY(launch_copy_top(ctx, Lo<T>::code, W, ldw, m, m, Y0, od, st));
+  SQB_TRY(launch_copy_top(ctx, Lo<T>::code, W, ldw, m, ncol, Y0, od, st));
   const size_t esz = sizeof(T);
-  for (int64_t c0 = 0; c0 < m; c0 += chunk) {
-    const int64_t kc = std::min(chunk, m - c0);
+  for (int64_t c0 = 0; c0 < ncol; c0 += chunk) {
+    const int64_t kc = std::min(chunk, ncol - c0);
     SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const char*)W + (c0 * ldw + m) * esz, ldw, kc,
                           Y0 + c0 * od, od, m, P, st));
   }
@@ -66,6 +92,7 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
   // column 0: y = y0_0 (w = W[:, 0]); a_1 is empty
   StepArgs sa{};
   sa.c = 0; sa.m = (int)m; sa.ell = (int)ell; sa.od = (int)od; sa.scaling = scaling; sa.tree = 0;
+  sa.off = (int)off; sa.ncol = (int)ncol;
   sa.gath = nullptr; sa.nranks = 1; sa.rank_level = 0;
   sa.P = P; sa.n_tiles = g.n_tiles; sa.n_eff = g.n_eff; sa.idx = srht ? sk->indices : nullptr;
   sa.log_tb = g.log_tb; sa.norm_lo = norm_lo; sa.y = Y0; sa.Y0 = Y0; sa.S = S; sa.lds = lds;
@@ -86,11 +113,11 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
                               std::max(tile_bytes, sizeof(double) * (size_t)(m + 1));
   auto colk = vec ? rhqr_col_kernel<T, VN> : rhqr_col_kernel<T, 1>;
   cudaFuncSetAttribute(colk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
-  for (int64_t c = 1; c < m; ++c) {
+  for (int64_t c = 1; c < ncol; ++c) {
     double* a_cur = abuf + (c & 1) * (m + 1);
     double* a_nxt = abuf + ((c + 1) & 1) * (m + 1);
     ColArgs ca{};
-    ca.c = (int)c; ca.m = (int)m; ca.mrow = (int)m; ca.e_base = 0; ca.n = n; ca.ell = (int)ell;
+    ca.c = (int)c; ca.m = (int)m; ca.ncol = (int)ncol; ca.mrow = (int)m; ca.e_base = 0; ca.n = n; ca.ell = (int)ell;
     ca.od = (int)od; ca.log_tb = log_tb_col; ca.n_tiles = g.n_tiles; ca.n_eff = n_eff_col;
     ca.W = W; ca.ldw = ldw; ca.U = U; ca.ldu = ldu; ca.acur = a_cur; ca.clast = coef; ca.fscale = fs;
     ca.scaling = scaling; ca.srht = srht ? 1 : 0; ca.bits = srht ? sk->sign_bits : nullptr;
@@ -116,25 +143,35 @@ static int rhqr_left_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const vo
   }
   // last column: lazy scaling of its Omega rows and its T column
   {
-    const T* src = m == 1 ? (const T*)W + m : (const T*)U + (m - 1) * ldu + m;
-    T* dst = (T*)U + (m - 1) * ldu + m;
+    const T* src = ncol == 1 ? (const T*)W + m : (const T*)U + (ncol - 1) * ldu + m;
+    T* dst = (T*)U + (ncol - 1) * ldu + m;
     const unsigned gb = (unsigned)std::min<int64_t>((n + 255) / 256, 4 * 148);
     SQB_TRY(launch_pdl(ctx, "finish_kernel", finish_kernel<T>, dim3(gb + 1), dim3(256), 0, src, dst, n,
-                       (const double*)fs, scaling, Tm, ldt, (int)m, (const double*)vbuf,
+                       (const double*)fs, scaling, Tm, ldt, (int)ncol, (const double*)vbuf,
                        (const double*)betas, (const Status*)st));
   }
   return SQB_OK;
 }
+
+#define SQB_SWEEP_INST(T)                                                                                  \
+  template int left_sweep_t<T>(sqb_ctx*, const sqb_sketch*, int, const void*, int64_t, int64_t, int64_t, int64_t, \
+                               int64_t, void*, int64_t, double*, int64_t, double*, int64_t, double*, int64_t,     \
+                               double*, double*, double*, void*);
+SQB_SWEEP_INST(double)
+SQB_SWEEP_INST(float)
+SQB_SWEEP_INST(__half)
+SQB_SWEEP_INST(__nv_bfloat16)
+#undef SQB_SWEEP_INST
 
 int rhqr_left_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
                        const void* W, int64_t N, int64_t m, int64_t ldw, void* U, int64_t ldu,
                        double* S, int64_t lds, double* T, int64_t ldt, double* R, int64_t ldr,
                        double* sigmas, double* rhos, double* betas) {
   switch (lo_dtype) {
-    case SQB_F64: return rhqr_left_t<double>(ctx, sk, scaling, W, N, m, ldw, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas);
-    case SQB_F32: return rhqr_left_t<float>(ctx, sk, scaling, W, N, m, ldw, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas);
-    case SQB_F16: return rhqr_left_t<__half>(ctx, sk, scaling, W, N, m, ldw, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas);
-    case SQB_BF16: return rhqr_left_t<__nv_bfloat16>(ctx, sk, scaling, W, N, m, ldw, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas);
+    case SQB_F64: return left_sweep_t<double>(ctx, sk, scaling, W, N, m, ldw, m, 0, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas, nullptr);
+    case SQB_F32: return left_sweep_t<float>(ctx, sk, scaling, W, N, m, ldw, m, 0, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas, nullptr);
+    case SQB_F16: return left_sweep_t<__half>(ctx, sk, scaling, W, N, m, ldw, m, 0, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas, nullptr);
+    case SQB_BF16: return left_sweep_t<__nv_bfloat16>(ctx, sk, scaling, W, N, m, ldw, m, 0, U, ldu, S, lds, T, ldt, R, ldr, sigmas, rhos, betas, nullptr);
   }
   return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
 }

@@ -138,6 +138,34 @@ def rhqr_left(W, omega, scaling=SCALE_SQRT2, policy=None):
                        betas=_out(bt, host))
 
 
+def rhqr_right(W, omega, scaling=SCALE_SQRT2, policy=None):
+    """rhqr.py:270-301: right-looking variant — rank-1 update of the trailing
+    block, which is re-sketched wholesale at every step; T recovered from S."""
+    check_scaling(scaling)
+    policy = policy or DOUBLE_POLICY
+    require_device_policy(policy)
+    host = not is_device(W)
+    n, m = _shape2(W)
+    psi = _embed(omega, n, m)
+    tag = policy.low
+    Wd = to_device(W, tag, align_row=m)
+    od = psi.out_dim
+    U = empty_colmajor(n, m, tag, align_row=m)
+    S = empty_colmajor(od, m, "double")
+    T = empty_colmajor(m, m, "double")
+    R = empty_colmajor(m, m, "double")
+    scal = torch.empty(3 * m, dtype=torch.float64, device=Wd.device)
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_rhqr_right(
+        ctx.h, psi.omega.desc(), scaling_code(scaling), CODES[tag], Wd.data_ptr(), n, m, ld_of(Wd),
+        U.data_ptr(), ld_of(U), S.data_ptr(), ld_of(S), T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R),
+        scal.data_ptr(), scal.data_ptr() + 8 * m, scal.data_ptr() + 16 * m), "sqb_rhqr_right")
+    raise_status(ctx, "rhqr_right")
+    return RHQRFactors(U=_out(U, host), S=_out(S, host), T=_out(T, host), R=_out(R, host), psi=psi,
+                       scaling=scaling, sigmas=_out(scal[:m], host), rhos=_out(scal[m:2 * m], host),
+                       betas=_out(scal[2 * m:], host))
+
+
 def rec_rhqr(W, omega, scaling=SCALE_SQRT2, policy=None):
     """rhqr.py:368-395: one sketch of W, Householder QR of the sketch in the
     high precision, triangular reconstruction of the n-dimensional reflectors."""
@@ -282,8 +310,97 @@ def lsq_via_implicit_q(factors, b, policy=None):
     return upper_tri_solve(factors.R, c[:m], policy=policy)
 
 
-def t_factor_from_sketches(S, policy=None):  # pragma: no cover - out of the hot path
-    raise NotImplementedError("t_factor_from_sketches belongs to rhqr_right/rhqr_block (SURVEY §8(f))")
+def t_factor_from_sketches(S, policy=None):
+    """rhqr.py:122-132: T of the compact form from S = Psi U alone
+    (S^t S = T^{-1} + T^{-t}); Gram + back substitution on the device."""
+    policy = policy or DOUBLE_POLICY
+    host = not is_device(S)
+    Sd = to_device(S, "double")
+    if Sd.dim() == 1:
+        Sd = Sd[:, None]
+    od, k = Sd.shape
+    T = empty_colmajor(k, k, "double")
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_t_factor(ctx.h, Sd.data_ptr(), ld_of(Sd), od, k, T.data_ptr(), ld_of(T)),
+              "sqb_t_factor")
+    raise_status(ctx, "upper_tri_solve")
+    return _out(T, host)
+
+
+@dataclass
+class BlockPanel:
+    """rhqr.py:304-309: one panel of the blocked sweep."""
+
+    U: object
+    S: object
+    T: object
+    offset: int
+
+
+@dataclass
+class BlockRHQRFactors:
+    """rhqr.py:312-331: panel-compact output of rhqr_block; stacked() merges
+    the panels into one compact form (the global T rebuilt from S)."""
+
+    panels: list
+    R: object
+    psi: EmbeddedSketch
+    scaling: str
+    sigmas: object
+    rhos: object
+    betas: object
+
+    def stacked(self):
+        dev = is_device(self.panels[0].U)
+        cat = (lambda xs: torch.cat(xs, dim=1)) if dev else (lambda xs: np.concatenate(xs, axis=1))
+        U = cat([p.U for p in self.panels])
+        S = cat([p.S for p in self.panels])
+        return RHQRFactors(U=U, S=S, T=t_factor_from_sketches(S), R=self.R, psi=self.psi,
+                           scaling=self.scaling, sigmas=self.sigmas, rhos=self.rhos, betas=self.betas)
+
+
+def rhqr_block_device(Wd, psi, block_size, scaling, policy, check=True):
+    """Device core of rhqr_block: returns U, S, the block-diagonal panel T's,
+    R and the scalars as device tensors."""
+    N, m = Wd.shape
+    tag = policy.low
+    od = psi.out_dim
+    U = empty_colmajor(N, m, tag, align_row=m)
+    S = empty_colmajor(od, m, "double")
+    T = empty_colmajor(m, m, "double")
+    R = empty_colmajor(m, m, "double")
+    scal = torch.empty(3 * m, dtype=torch.float64, device=Wd.device)
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_rhqr_block(
+        ctx.h, psi.omega.desc(), scaling_code(scaling), CODES[tag], Wd.data_ptr(), N, m, ld_of(Wd), block_size,
+        U.data_ptr(), ld_of(U), S.data_ptr(), ld_of(S), T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R),
+        scal.data_ptr(), scal.data_ptr() + 8 * m, scal.data_ptr() + 16 * m), "sqb_rhqr_block")
+    if check:
+        raise_status(ctx, "rhqr_block")
+    return U, S, T, R, scal[:m], scal[m:2 * m], scal[2 * m:]
+
+
+def rhqr_block(W, omega, block_size=32, scaling=SCALE_SQRT2, policy=None):
+    """rhqr.py:334-365: blocked left-looking sweep.  Earlier panels are applied
+    compactly (one re-sketch per panel), then the panel is factored in place;
+    a final panel narrower than block_size is processed as-is."""
+    check_scaling(scaling)
+    if block_size < 1:
+        raise ValueError("block_size must be positive")
+    policy = policy or DOUBLE_POLICY
+    require_device_policy(policy)
+    host = not is_device(W)
+    n, m = _shape2(W)
+    psi = _embed(omega, n, m)
+    Wd = to_device(W, policy.low, align_row=m)
+    U, S, T, R, sg, rh, bt = rhqr_block_device(Wd, psi, int(block_size), scaling, policy)
+    panels = []
+    for j0 in range(0, m, block_size):
+        j1 = min(j0 + block_size, m)
+        panels.append(BlockPanel(U=_out(U[:, j0:j1], host), S=_out(S[:, j0:j1], host),
+                                 T=_out(T[j0:j1, j0:j1], host), offset=j0))
+    return BlockRHQRFactors(panels=panels, R=_out(R, host), psi=psi, scaling=scaling, sigmas=_out(sg, host),
+                            rhos=_out(rh, host), betas=_out(bt, host))
 
 
 def _lo_tag(U):
@@ -322,6 +439,7 @@ def sketch_q(factors):
 
 
 __all__ = ["HouseholderStep", "RHQRFactors", "QRResult", "householder_qr", "upper_tri_solve",
+           "BlockPanel", "BlockRHQRFactors", "rhqr_block", "rhqr_right", "t_factor_from_sketches",
            "lsq_via_implicit_q", "rh_vector", "rhqr_left", "rec_rhqr", "apply_reflectors_compact",
            "thin_q", "sketch_q", "SCALE_SQRT2", "SCALE_UNIT", "raise_status", "_embed"]
 _ = C

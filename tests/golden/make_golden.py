@@ -29,7 +29,8 @@ from sketchqr.experiments import gen_cmatrix  # noqa: E402
 from sketchqr.krylov import hessenberg_lstsq, rhqr_arnoldi, rhqr_gmres  # noqa: E402
 from sketchqr.linalg import cond_number, factorization_errors, orthogonality_error  # noqa: E402
 from sketchqr.rhqr import (apply_reflectors_compact, rec_rhqr, rh_vector,  # noqa: E402
-                           rhqr_left, sketch_q, thin_q)
+                           rhqr_block, rhqr_left, rhqr_right, sketch_q, t_factor_from_sketches,
+                           thin_q)
 from sketchqr.sketching import (EmbeddedSketch, GaussianSketch,  # noqa: E402
                                 IdentitySketch, SRHTSketch)
 
@@ -196,12 +197,37 @@ def apply_compact_cases():
          Q=thin_q(F), SQ=sketch_q(F))
 
 
+def block_cases():
+    # rhqr_block: one panel, degenerate, ragged final panel (test_rhqr.py:225-235)
+    rng = np.random.default_rng(11)
+    n, m = 1500, 20
+    W = rng.standard_normal((n, m))
+    out = dict(W=W, seed=53, ell=48)
+    for bs in (20, 1, 6, 8):
+        B = rhqr_block(W, SRHTSketch(48, n - m, 53), block_size=bs)
+        Fs = B.stacked()
+        out[f"R_{bs}"] = B.R
+        out[f"U_{bs}"] = Fs.U
+        out[f"S_{bs}"] = Fs.S
+        out[f"Tst_{bs}"] = Fs.T
+        out[f"Tblk_{bs}"] = np.concatenate([p.T.ravel() for p in B.panels])
+        out[f"scal_{bs}"] = np.stack([B.sigmas, B.rhos, B.betas])
+    save("rhqr_block_1500x20_srht48", **out)
+    S = rng.standard_normal((30, 8))
+    save("t_factor_30x8", S=S, T=t_factor_from_sketches(S))
+    # rhqr_right (rhqr.py:270-301), fp64 and unit scaling
+    W = rng.standard_normal((900, 12))
+    F = rhqr_right(W, SRHTSketch(36, 900 - 12, 59))
+    Fu = rhqr_right(W, SRHTSketch(36, 900 - 12, 59), scaling="unit")
+    save("rhqr_right_900x12_srht36", W=W, seed=59, ell=36, **factor_dump(F),
+         U_unit=Fu.U, R_unit=Fu.R, T_unit=Fu.T)
+
+
+SECTIONS = dict(srht=srht_cases, gauss=gauss_cases, rh_vector=rh_vector_cases, rhqr=rhqr_cases,
+                mixed=mixed_cases, rec=rec_cases, krylov=krylov_cases, apply_compact=apply_compact_cases,
+                block=block_cases)
+
 if __name__ == "__main__":
-    srht_cases()
-    gauss_cases()
-    rh_vector_cases()
-    rhqr_cases()
-    mixed_cases()
-    rec_cases()
-    krylov_cases()
-    apply_compact_cases()
+    # no arguments: every section; otherwise only the named ones
+    for name in (sys.argv[1:] or list(SECTIONS)):
+        SECTIONS[name]()

@@ -1,0 +1,182 @@
+"""GPU parity of the factorization variants next to the hot path (SURVEY
+§8(f) rank 1 and 4): rhqr_block (rhqr.py:334-365), rhqr_right (:270-301) and
+t_factor_from_sketches (:122-132), against the reference's golden vectors,
+the CPU oracle and the reference's own cross-variant tests
+(test_rhqr.py:207-235, test_acceptance.py:100-120).  fp64 bar: 1e-12
+relative (the reference's own test tolerance for these variants)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import sketchqr_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2405_10923_b200 as P
+    return P
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb else 1.0)
+
+
+# ------------------------------------------------------------ t_factor
+def test_t_factor_known_answers(P):
+    S = np.zeros((6, 2))
+    S[0, 0] = S[1, 1] = np.sqrt(2.0)
+    assert np.allclose(P.t_factor_from_sketches(S), np.eye(2), atol=1e-14)
+    assert np.allclose(P.t_factor_from_sketches(np.array([[2.0], [1.0]])), [[0.4]], atol=1e-15)
+    g = golden("t_factor_30x8")
+    assert rel(P.t_factor_from_sketches(g["S"]), g["T"]) < 1e-13
+
+
+def test_t_factor_round_trip(P):
+    S = np.random.default_rng(3).standard_normal((30, 8))
+    T = P.t_factor_from_sketches(S)
+    G = S.T @ S
+    Ti = np.linalg.inv(T)
+    assert np.linalg.norm(G - (Ti + Ti.T)) <= 1e-12 * np.linalg.norm(G)
+
+
+def test_t_factor_singular(P):
+    with pytest.raises(P.SingularFactorError):
+        P.t_factor_from_sketches(np.zeros((5, 2)))
+
+
+# ------------------------------------------------------------ rhqr_block
+@pytest.mark.parametrize("bs", [20, 1, 6, 8])
+def test_rhqr_block_matches_reference(P, bs):
+    g = golden("rhqr_block_1500x20_srht48")
+    W = g["W"]
+    om = P.SRHTSketch(int(g["ell"]), W.shape[0] - W.shape[1], int(g["seed"]))
+    B = P.rhqr_block(W, om, block_size=bs)
+    assert len(B.panels) == -(-20 // bs)
+    assert [p.offset for p in B.panels] == list(range(0, 20, bs))
+    assert rel(B.R, g[f"R_{bs}"]) < 1e-12
+    tb = np.concatenate([np.asarray(p.T).ravel() for p in B.panels])
+    assert rel(tb, g[f"Tblk_{bs}"]) < 1e-12
+    assert np.allclose(np.stack([B.sigmas, B.rhos, B.betas]), g[f"scal_{bs}"], rtol=1e-12, atol=1e-14)
+    F = B.stacked()
+    assert rel(F.U, g[f"U_{bs}"]) < 1e-12
+    assert rel(F.S, g[f"S_{bs}"]) < 1e-12
+    assert rel(F.T, g[f"Tst_{bs}"]) < 1e-11
+
+
+def test_rhqr_block_matches_unblocked(P):
+    # test_rhqr.py:225-235 with the device Gaussian sketch
+    rng = np.random.default_rng(5)
+    n, m = 60, 8
+    W = rng.standard_normal((n, m))
+    om = P.GaussianSketch(24, n - m, 22)
+    ref = P.rhqr_left(W, om)
+    for bs in (m, 1, 3):
+        B = P.rhqr_block(W, om, block_size=bs)
+        assert np.allclose(B.R, ref.R, atol=1e-12 * np.linalg.norm(ref.R))
+        F = B.stacked()
+        assert np.allclose(F.U, ref.U, atol=1e-12 * np.linalg.norm(ref.U))
+        fro, _, _ = P.factorization_errors(W, P.thin_q(F), F.R)
+        assert fro <= 1e-13
+
+
+def test_rhqr_block_identity_is_householder(P):
+    # test_acceptance.py:100-120 (criterion 1) for the blocked variant
+    rng = np.random.default_rng(101)
+    for _ in range(3):
+        W = rng.standard_normal((64, 8))
+        _, R_ref, aux = O.householder_qr(W)
+        F = P.rhqr_block(W, P.IdentitySketch(56), block_size=3).stacked()
+        assert rel(F.R, R_ref) <= 1e-13
+        assert rel(F.U, aux["U"]) <= 1e-13
+
+
+@pytest.mark.parametrize("N,m,bs,ell", [(1 << 16, 64, 16, 128), (50_003, 40, 32, 96), (1 << 18, 96, 32, 192)])
+def test_rhqr_block_against_oracle(P, N, m, bs, ell):
+    W = np.random.default_rng(N + m).standard_normal((N, m)) * np.logspace(0, -6, m)
+    om_d = P.SRHTSketch(ell, N - m, 77)
+    om_o = O.SRHT(ell, N - m, 77)
+    B = P.rhqr_block(W, om_d, block_size=bs)
+    Bo = O.rhqr_block(W, om_o, block_size=bs)
+    assert rel(B.R, Bo.R) < 1e-10
+    F, Fo = B.stacked(), Bo.stacked()
+    assert rel(F.U, Fo.U) < 1e-9
+    assert rel(F.S, Fo.S) < 1e-9
+    fro, _, _ = P.factorization_errors(W, P.thin_q(F), F.R)
+    assert fro < 1e-13
+
+
+@pytest.mark.parametrize("tag,tol", [("single", 1e-5), ("half", 3e-2), ("bf16", 1e-1)])
+def test_rhqr_block_low_precision(P, tag, tol):
+    # same bars as the rhqr_left mixed-precision parity (low-format GEMV
+    # accumulation order differs from numpy's)
+    rng = np.random.default_rng(9)
+    N, m = 8192, 16
+    W = rng.standard_normal((N, m))
+    B = P.rhqr_block(W, P.SRHTSketch(64, N - m, 12), block_size=6, policy=P.PrecisionPolicy("double", tag))
+    Bo = O.rhqr_block(W, O.SRHT(64, N - m, 12), block_size=6, policy=O.Policy("double", tag))
+    assert rel(B.R, Bo.R) < tol
+    U = B.stacked().U
+    assert np.array_equal(P.round_to(U, tag), U)
+
+
+@pytest.mark.parametrize("tag,tol", [("single", 1e-5), ("bf16", 1e-1)])
+def test_rhqr_right_low_precision(P, tag, tol):
+    rng = np.random.default_rng(10)
+    N, m = 8192, 12
+    W = rng.standard_normal((N, m))
+    F = P.rhqr_right(W, P.SRHTSketch(48, N - m, 13), policy=P.PrecisionPolicy("double", tag))
+    Fo = O.rhqr_right(W, O.SRHT(48, N - m, 13), policy=O.Policy("double", tag))
+    assert rel(F.R, Fo.R) < tol
+
+
+def test_rhqr_block_breakdown_and_args(P):
+    W = np.zeros((40, 4))
+    W[0] = 1.0
+    with pytest.raises(P.BreakdownError, match="column 2"):
+        P.rhqr_block(W, P.SRHTSketch(8, 36, 3), block_size=1)
+    with pytest.raises(ValueError, match="block_size must be positive"):
+        P.rhqr_block(np.ones((40, 4)), P.SRHTSketch(8, 36, 3), block_size=0)
+
+
+# ------------------------------------------------------------ rhqr_right
+def test_rhqr_right_matches_reference(P):
+    g = golden("rhqr_right_900x12_srht36")
+    W = g["W"]
+    om = P.SRHTSketch(int(g["ell"]), W.shape[0] - W.shape[1], int(g["seed"]))
+    F = P.rhqr_right(W, om)
+    for k in ("U", "S", "R"):
+        assert rel(getattr(F, k), g[k]) < 1e-12, k
+    assert rel(F.T, g["T"]) < 1e-11
+    assert np.allclose(np.stack([F.sigmas, F.rhos, F.betas]),
+                       np.stack([g["sigmas"], g["rhos"], g["betas"]]), rtol=1e-12, atol=1e-14)
+    Fu = P.rhqr_right(W, om, scaling="unit")
+    assert rel(Fu.U, g["U_unit"]) < 1e-12 and rel(Fu.R, g["R_unit"]) < 1e-12
+
+
+def test_rhqr_right_agrees_with_left(P):
+    rng = np.random.default_rng(21)
+    N, m = 20_000, 24
+    W = rng.standard_normal((N, m))
+    om = P.SRHTSketch(64, N - m, 4)
+    Fr, Fl = P.rhqr_right(W, om), P.rhqr_left(W, om)
+    assert rel(Fr.R, Fl.R) < 1e-12
+    assert rel(Fr.U, Fl.U) < 1e-11
+    assert rel(Fr.T, Fl.T) < 1e-10
+    Fo = O.rhqr_right(W, O.SRHT(64, N - m, 4))
+    assert rel(Fr.R, Fo.R) < 1e-12
+
+
+def test_rhqr_right_identity_is_householder(P):
+    rng = np.random.default_rng(102)
+    W = rng.standard_normal((64, 8))
+    _, R_ref, aux = O.householder_qr(W)
+    F = P.rhqr_right(W, P.IdentitySketch(56))
+    assert rel(F.R, R_ref) <= 1e-13
+    assert rel(F.U, aux["U"]) <= 1e-13

@@ -12,7 +12,9 @@
 // (BlockRHQRFactors.panels[k].T); the stacked global T comes from
 // t_factor_from_sketches(S).
 #include <algorithm>
+#include <type_traits>
 
+#include "mma.cuh"
 #include "rhqr_kernels.cuh"
 
 namespace sqb {
@@ -48,6 +50,14 @@ panel_update_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int bp, con
   for (int64_t r0 = (int64_t)blockIdx.x * PU_RB; r0 < N; r0 += (int64_t)gridDim.x * PU_RB) {
     const int64_t i = r0 + row;
     for (int jb = 0; jb < b; jb += 2 * PU_JC) {
+      // this thread's X entries first: their latency overlaps the U staging
+      // and the FMAs (loads batched ahead of the stores)
+      A xv[PU_JC];
+#pragma unroll
+      for (int j = 0; j < PU_JC; ++j) {
+        const int col = jb + h * PU_JC + j;
+        xv[j] = (i < N && col < b) ? Lo<T>::load(X[i + (int64_t)col * ldx]) : A(0);
+      }
       A acc[PU_JC];
 #pragma unroll
       for (int j = 0; j < PU_JC; ++j) acc[j] = A(0);
@@ -80,20 +90,209 @@ panel_update_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int bp, con
 #pragma unroll
         for (int j = 0; j < PU_JC; ++j) {
           const int col = jb + h * PU_JC + j;
-          if (col < b) {
-            T* x = X + i + (int64_t)col * ldx;
-            *x = Lo<T>::store(Lo<T>::sub(Lo<T>::load(*x), Lo<T>::rnd(acc[j])));
-          }
+          if (col < b) X[i + (int64_t)col * ldx] = Lo<T>::store(Lo<T>::sub(xv[j], Lo<T>::rnd(acc[j])));
         }
       }
     }
   }
 }
 
+// fp64: the same update on the tensor pipe.  A CTA owns 128 rows x 32 output
+// columns; warp w the rows [16w, 16w+16) as four m16n8 DMMA tiles.  U is
+// staged by cp.async (8 B per element, any alignment) while the thread's X
+// entries are loaded; shared strides padded to 2-wavefront fragment loads.
+constexpr int PD_RB = 128, PD_KC = 32, PD_NC = 32, PD_US = PD_RB + 4, PD_CS = PD_NC + 4;
+
+__global__ void __launch_bounds__(256, 3)
+panel_update_dmma_kernel(const double* __restrict__ U, int64_t ldu, int64_t N, int bp,
+                         const double* __restrict__ C, int64_t ldc, double* X, int64_t ldx, int b,
+                         const Status* st) {
+  __shared__ __align__(16) double Us[PD_KC * PD_US];
+  __shared__ double Cs[PD_KC * PD_CS];
+  if (failed(st)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int wr = warp * 16;
+  for (int64_t r0 = (int64_t)blockIdx.x * PD_RB; r0 < N; r0 += (int64_t)gridDim.x * PD_RB) {
+    for (int jb = 0; jb < b; jb += PD_NC) {
+      double acc[4][4], xv[4][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[nt][v] = 0.0;
+      for (int kb = 0; kb < bp; kb += PD_KC) {
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < PD_KC * PD_RB / 256; ++q) {
+          const int e = threadIdx.x + q * 256, k = e / PD_RB, r = e % PD_RB;
+          double* dst = Us + k * PD_US + r;
+          if (kb + k < bp && r0 + r < N) {
+            const double* src = U + (r0 + r) + (int64_t)(kb + k) * ldu;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+          } else {
+            *dst = 0.0;
+          }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        for (int e = threadIdx.x; e < PD_KC * PD_NC; e += 256) {
+          const int k = e / PD_NC, n = e % PD_NC;
+          Cs[k * PD_CS + n] = (kb + k < bp && jb + n < b) ? C[(kb + k) + (int64_t)(jb + n) * ldc] : 0.0;
+        }
+        if (kb == 0) {
+          // X fragment entries (rows g, g+8; columns 2t, 2t+1 of each n-tile)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const int64_t i = r0 + wr + g + 8 * (v >> 1);
+              const int col = jb + nt * 8 + 2 * t + (v & 1);
+              xv[nt][v] = (i < N && col < b) ? X[i + (int64_t)col * ldx] : 0.0;
+            }
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+#pragma unroll
+        for (int k16 = 0; k16 < PD_KC / 16; ++k16) {
+          double a[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) a[v] = Us[(k16 * 16 + t + 4 * (v >> 1)) * PD_US + wr + g + 8 * (v & 1)];
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            double bf[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) bf[v] = Cs[(k16 * 16 + t + 4 * v) * PD_CS + nt * 8 + g];
+            dmma_16x8x16(acc[nt], a, bf);
+          }
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int64_t i = r0 + wr + g + 8 * (v >> 1);
+          const int col = jb + nt * 8 + 2 * t + (v & 1);
+          if (i < N && col < b) X[i + (int64_t)col * ldx] = __dsub_rn(xv[nt][v], acc[nt][v]);
+        }
+    }
+  }
+}
+
+// The block_size <= 32 case (the default): C staged once per CTA, U double-
+// buffered across the CTA's row blocks and X prefetched one block ahead, so
+// the HBM stream of block i+1 overlaps the DMMAs and stores of block i.
+__device__ __forceinline__ void pd_stage_u(double* Us, const double* __restrict__ U, int64_t ldu, int64_t N,
+                                           int bp, int64_t r0) {
+#pragma unroll
+  for (int q = 0; q < PD_KC * PD_RB / 256; ++q) {
+    const int e = threadIdx.x + q * 256, k = e / PD_RB, r = e % PD_RB;
+    double* dst = Us + k * PD_US + r;
+    if (k < bp && r0 + r < N)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n"
+                   ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(U + (r0 + r) + (int64_t)k * ldu) : "memory");
+    else
+      *dst = 0.0;
+  }
+}
+
+__device__ __forceinline__ void pd_load_x(double (&xv)[4][4], const double* X, int64_t ldx, int64_t N, int b,
+                                          int64_t rbase, int g, int t) {
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int64_t i = rbase + g + 8 * (v >> 1);
+      const int col = nt * 8 + 2 * t + (v & 1);
+      xv[nt][v] = (i < N && col < b) ? X[i + (int64_t)col * ldx] : 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(256, 2)
+panel_update_dmma32_kernel(const double* __restrict__ U, int64_t ldu, int64_t N, int bp,
+                           const double* __restrict__ C, int64_t ldc, double* X, int64_t ldx, int b,
+                           const Status* st) {
+  extern __shared__ __align__(16) double pd_smem[];
+  double* Us0 = pd_smem;
+  double* Us1 = pd_smem + PD_KC * PD_US;
+  double* Cs = pd_smem + 2 * PD_KC * PD_US;
+  if (failed(st)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int wr = warp * 16;
+  const int64_t nblk = (N + PD_RB - 1) / PD_RB;
+  for (int e = threadIdx.x; e < PD_KC * PD_NC; e += 256) {
+    const int k = e / PD_NC, n = e % PD_NC;
+    Cs[k * PD_CS + n] = (k < bp && n < b) ? C[k + (int64_t)n * ldc] : 0.0;
+  }
+  int64_t blk = blockIdx.x;
+  double xv[4][4], xn[4][4];
+  if (blk < nblk) {
+    pd_stage_u(Us0, U, ldu, N, bp, blk * PD_RB);
+    pd_load_x(xv, X, ldx, N, b, blk * PD_RB + wr, g, t);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  for (int it = 0; blk < nblk; blk += gridDim.x, ++it) {
+    double* Uc = (it & 1) ? Us1 : Us0;
+    double* Un = (it & 1) ? Us0 : Us1;
+    const int64_t nxt = blk + gridDim.x;
+    if (nxt < nblk) {
+      pd_stage_u(Un, U, ldu, N, bp, nxt * PD_RB);
+      pd_load_x(xn, X, ldx, N, b, nxt * PD_RB + wr, g, t);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    double acc[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[nt][v] = 0.0;
+#pragma unroll
+    for (int k16 = 0; k16 < PD_KC / 16; ++k16) {
+      double a[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) a[v] = Uc[(k16 * 16 + t + 4 * (v >> 1)) * PD_US + wr + g + 8 * (v & 1)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        double bf[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) bf[v] = Cs[(k16 * 16 + t + 4 * v) * PD_CS + nt * 8 + g];
+        dmma_16x8x16(acc[nt], a, bf);
+      }
+    }
+    const int64_t rb = blk * PD_RB + wr;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int64_t i = rb + g + 8 * (v >> 1);
+        const int col = nt * 8 + 2 * t + (v & 1);
+        if (i < N && col < b) X[i + (int64_t)col * ldx] = __dsub_rn(xv[nt][v], acc[nt][v]);
+      }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) xv[nt][v] = xn[nt][v];
+    __syncthreads();  // Uc is refilled next iteration
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 template <typename T>
 static int panel_update(sqb_ctx* ctx, const T* U, int64_t ldu, int64_t N, int64_t bp, const double* C, int64_t ldc,
                         T* X, int64_t ldx, int64_t b) {
   const int64_t blocks = (N + PU_RB - 1) / PU_RB;
+  if constexpr (std::is_same<T, double>::value) {
+    if (bp <= PD_KC && b <= PD_NC) {
+      const size_t smem = sizeof(double) * (2 * PD_KC * PD_US + PD_KC * PD_CS);
+      cudaFuncSetAttribute(panel_update_dmma32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const unsigned grid = (unsigned)std::min<int64_t>(blocks, 2 * (int64_t)ctx->sm_count);
+      panel_update_dmma32_kernel<<<grid, 256, smem, ctx->stream>>>(U, ldu, N, (int)bp, C, ldc, X, ldx, (int)b,
+                                                                   ctx->d_status);
+      return check_launch(ctx, "panel_update_dmma32_kernel");
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks, 3 * (int64_t)ctx->sm_count);
+    panel_update_dmma_kernel<<<grid, 256, 0, ctx->stream>>>(U, ldu, N, (int)bp, C, ldc, X, ldx, (int)b,
+                                                            ctx->d_status);
+    return check_launch(ctx, "panel_update_dmma_kernel");
+  }
   const unsigned grid = (unsigned)std::min<int64_t>(blocks, 8 * (int64_t)ctx->sm_count);
   panel_update_kernel<T><<<grid, 256, 0, ctx->stream>>>(U, ldu, N, (int)bp, C, ldc, X, ldx, (int)b, ctx->d_status);
   return check_launch(ctx, "panel_update_kernel");

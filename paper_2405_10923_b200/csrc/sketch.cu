@@ -2,6 +2,7 @@
 // (generic path; the DMMA GEMM lives in dense.cu), identity, embedded.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "sketch.cuh"
 #include "vec.cuh"
@@ -134,111 +135,345 @@ srht_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int log_tb,
 }
 
 // ---------------------------------------------------------------------------
-// fp64 SRHT tile pipeline (K1 for the batched raw sketches and sketch_apply):
-// persistent CTAs stream (tile, column) items; the next item's tile is copied
-// global -> shared with cp.async (coalesced 16-byte chunks, zero-filled past n)
-// while the current one is transformed, so HBM reads overlap the butterflies.
-// Shared layout pads 2 doubles per 16 (keeps 16-byte chunk alignment and makes
-// the radix-16 passes conflict-free: LDS.128 for bits 0-3, 2-way for 4..11).
+// K1 standalone tile kernel (batched raw sketches, sketch_apply, the compact
+// updates): a 4096-coordinate tile is owned by 64 threads holding 64 values
+// each, so the 12 in-tile stages are TWO register passes (bits 0-5, then
+// bits 6-11) with one shared-memory round trip between them.  Persistent
+// CTAs walk (tile, column) items; the next item's raw values are copied
+// global -> shared by cp.async while the current one is transformed.  After
+// pass 2 only the sampled coordinates are written back (a per-thread 64-bit
+// mask), then gathered into the leaves.  Shared rows of 64 elements are padded
+// by 16 bytes: pass-1 LDS.128 and pass-2 LDS are both conflict-free.
 // ---------------------------------------------------------------------------
-constexpr int PIPE_NT = 256;
+constexpr int S64_NT = 64, S64_LOG = 12, S64_TB = 1 << S64_LOG;
 
-__device__ __forceinline__ int pidx2(int e) { return e + 2 * (e >> 4); }
-
-template <int R>
-__device__ __forceinline__ void fwht_pass2(double* sm, int b, int len) {
-  const int groups = len >> R;
-  const int lowmask = (1 << b) - 1;
-  for (int g = threadIdx.x; g < groups; g += blockDim.x) {
-    const int base = (g & lowmask) | ((g >> b) << (b + R));
-    double v[1 << R];
-#pragma unroll
-    for (int j = 0; j < (1 << R); ++j) v[j] = sm[pidx2(base | (j << b))];
-#pragma unroll
-    for (int s2 = 0; s2 < R; ++s2)
-#pragma unroll
-      for (int j = 0; j < (1 << R); ++j)
-        if (!(j & (1 << s2))) {
-          const double x = v[j], y = v[j | (1 << s2)];
-          v[j] = __dadd_rn(x, y);
-          v[j | (1 << s2)] = __dsub_rn(x, y);
-        }
-#pragma unroll
-    for (int j = 0; j < (1 << R); ++j) sm[pidx2(base | (j << b))] = v[j];
-  }
+template <typename E>
+__host__ __device__ constexpr int s64_pad() { return 16 / (int)sizeof(E); }
+template <typename E>
+__device__ __forceinline__ int s64_idx(int e) { return e + s64_pad<E>() * (e >> 6); }
+template <typename E>
+__host__ __device__ constexpr size_t s64_buf_bytes() {
+  return sizeof(E) * (size_t)(S64_TB + s64_pad<E>() * (S64_TB >> 6));
+}
+// v with its sign bit flipped iff bit j of w is set
+__device__ __forceinline__ double flip_sign(double v, uint32_t w, int j) {
+  const int2 p = *reinterpret_cast<int2*>(&v);
+  const int hi = p.y ^ (int)((w << (31 - j)) & 0x80000000u);
+  return __hiloint2double(hi, p.x);
+}
+__device__ __forceinline__ float flip_sign(float v, uint32_t w, int j) {
+  return __int_as_float(__float_as_int(v) ^ (int)((w << (31 - j)) & 0x80000000u));
 }
 
-__global__ void __launch_bounds__(PIPE_NT, 3)
-srht_tile_pipe_kernel(const double* __restrict__ X, int64_t ldx, int64_t n, int log_tb, int64_t n_eff,
-                      int64_t k, const uint32_t* __restrict__ bits, const int64_t* __restrict__ idx, int ell,
-                      double scale_lo, double* __restrict__ P, int64_t n_tiles, const Status* st,
-                      int64_t e_base) {
+// 6 butterfly stages over 64 register values (stages b .. b+5 of the tile)
+template <typename T>
+__device__ __forceinline__ void fwht64_regs(typename Lo<T>::acc (&v)[64]) {
+#pragma unroll
+  for (int s2 = 0; s2 < 6; ++s2)
+#pragma unroll
+    for (int j = 0; j < 64; ++j)
+      if (!(j & (1 << s2))) {
+        const typename Lo<T>::acc x = v[j], y = v[j | (1 << s2)];
+        v[j] = Lo<T>::add(x, y);
+        v[j | (1 << s2)] = Lo<T>::sub(x, y);
+      }
+}
+
+// smem layout shared by the 4096-tile kernels:
+//   [smask 64 x u64][spre 64 x int][kslot ell x int][samp ell x acc][tile buffer]
+// samp holds the transformed value of every distinct sampled coordinate
+// (slot = prefix count over the (t, j) mask bits), kslot maps output k to its
+// slot, so the tile buffer is free as soon as pass 2 has loaded it.
+constexpr int S64_MAX_ELL = 2048;
+__host__ __device__ inline size_t s64_samp_off(int ell) { return (768 + 4 * (size_t)ell + 15) & ~(size_t)15; }
+__host__ __device__ inline size_t s64_head_bytes(int ell, size_t acc) {
+  return (s64_samp_off(ell) + (size_t)ell * acc + 127) & ~(size_t)127;
+}
+
+// build smask / spre / kslot (one CTA, S64_NT threads); ends with a barrier
+__device__ __forceinline__ void s64_sample_maps(const int64_t* __restrict__ idx, int ell,
+                                                unsigned long long* smask, int* spre, int* kslot) {
+  const int tid = threadIdx.x;
+  smask[tid] = 0ull;
+  __syncthreads();
+  for (int kk = tid; kk < ell; kk += S64_NT) {
+    const int p = (int)(__ldg(idx + kk) & (S64_TB - 1));
+    atomicOr(&smask[p & 63], 1ull << (p >> 6));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int t = 0; t < 64; ++t) { spre[t] = acc; acc += __popcll(smask[t]); }
+  }
+  __syncthreads();
+  for (int kk = tid; kk < ell; kk += S64_NT) {
+    const int p = (int)(__ldg(idx + kk) & (S64_TB - 1));
+    const int t = p & 63, j = p >> 6;
+    kslot[kk] = spre[t] + __popcll(smask[t] & ((1ull << j) - 1ull));
+  }
+  __syncthreads();
+}
+
+// slot of (this thread, j) among the sampled coordinates (j compile-time after unrolling)
+__device__ __forceinline__ int s64_slot(uint32_t mlo, uint32_t mhi, int pre, int j) {
+  return j < 32 ? pre + __popc(mlo & ((1u << j) - 1u)) : pre + __popc(mlo) + __popc(mhi & ((1u << (j - 32)) - 1u));
+}
+
+// fp64 / fp32 storage (values stay in the storage type end to end)
+template <typename T>
+__global__ void __launch_bounds__(S64_NT)
+srht64_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_eff, int64_t k,
+                   const uint32_t* __restrict__ bits, const int64_t* __restrict__ idx, int ell,
+                   T scale_lo, T* __restrict__ P, int64_t n_tiles, const Status* st, int64_t e_base) {
+  static_assert(sizeof(T) == sizeof(typename Lo<T>::acc), "storage = arithmetic type");
+  constexpr int C = 16 / (int)sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* smask = reinterpret_cast<unsigned long long*>(smem_raw);
+  int* spre = reinterpret_cast<int*>(smem_raw + 512);
+  int* kslot = reinterpret_cast<int*>(smem_raw + 768);
+  T* samp = reinterpret_cast<T*>(smem_raw + s64_samp_off(ell));
+  T* buf = reinterpret_cast<T*>(smem_raw + s64_head_bytes(ell, sizeof(T)));
   if (st && failed(st)) return;
-  const int tb = 1 << log_tb;
-  const int tbp = tb + 2 * (tb >> 4);
-  double* buf0 = reinterpret_cast<double*>(smem_raw);
+  const int tid = threadIdx.x;
+  s64_sample_maps(idx, ell, smask, spre, kslot);
+  const uint32_t mlo = (uint32_t)smask[tid], mhi = (uint32_t)(smask[tid] >> 32);
+  const int mypre = spre[tid];
   const int64_t items = n_eff * k;
-  auto issue = [&](int64_t item, double* buf) {
+  auto issue = [&](int64_t item) {
     if (item >= items) return;
     const int64_t col = item / n_eff, t = item - col * n_eff;
-    const int64_t e0 = t << log_tb;
-    const double* x = X + col * ldx + e0;
+    const int64_t e0 = t << S64_LOG;
+    const T* x = X + col * ldx + e0;
     const int64_t nv = n - e0;
-    for (int q = threadIdx.x; q < (tb >> 1); q += PIPE_NT) {
-      const int e = 2 * q;
-      double* d = buf + pidx2(e);
-      if (e + 2 <= nv) cp_async16(d, x + e, 16);
-      else if (e < nv) cp_async16(d, x + e, 8);
-      else { d[0] = 0.0; d[1] = 0.0; }
+    if (nv >= S64_TB) {
+      const T* src = x + tid * C;
+      T* dst = buf + s64_idx<T>(tid * C);
+#pragma unroll
+      for (int i = 0; i < S64_TB / (C * S64_NT); ++i)
+        cp_async16(dst + i * (S64_NT * C + s64_pad<T>() * C), src + i * S64_NT * C, 16);
+    } else {
+      for (int q = tid; q < S64_TB / C; q += S64_NT) {
+        const int e = q * C;
+        const int64_t rem = nv - e;
+        const int bytes = rem >= C ? 16 : (rem > 0 ? (int)rem * (int)sizeof(T) : 0);
+        cp_async16(buf + s64_idx<T>(e), bytes > 0 ? (const void*)(x + e) : (const void*)x, bytes);
+      }
+    }
+  };
+  auto sign_words = [&](int64_t item, uint32_t& a0, uint32_t& a1) {
+    if (item >= items) return;
+    const int64_t col = item / n_eff, t = item - col * n_eff;
+    const int64_t eg = e_base + (t << S64_LOG) + tid * 64;
+    a0 = __ldg(bits + (eg >> 5));
+    a1 = __ldg(bits + (eg >> 5) + 1);
+  };
+  int64_t item = blockIdx.x;
+  uint32_t w0 = 0, w1 = 0;
+  issue(item);
+  cp_async_commit_group();
+  sign_words(item, w0, w1);
+  for (; item < items; item += gridDim.x) {
+    cp_async_wait_group<0>();
+    __syncthreads();
+    const int64_t col = item / n_eff, t = item - col * n_eff;
+    const int64_t e = (t << S64_LOG) + tid * 64;
+    T v[64];
+    // pass 1: coordinates 64 tid .. +63: scale, signs (sketching.py:152-153), stages h = 1..32
+    {
+      T* row = buf + s64_idx<T>(tid * 64);
+#pragma unroll
+      for (int q = 0; q < 64 / C; ++q) vload<T>(row + q * C, v + q * C);
+#pragma unroll
+      for (int j = 0; j < 64; ++j) v[j] = flip_sign(Lo<T>::mul(v[j], scale_lo), j < 32 ? w0 : w1, j & 31);
+      if (e + 64 > n) {  // zero padding past n is +0 (sketching.py:154)
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (e + j >= n) v[j] = T(0);
+      }
+      fwht64_regs<T>(v);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 64 / C; ++q) vstore<T>(row + q * C, v + q * C);
+    }
+    __syncthreads();
+    // pass 2: coordinates tid + 64 j, stages h = 64 .. 2048
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = buf[s64_idx<T>(tid + 64 * j)];
+    __syncthreads();  // tile buffer free: stream the next item in behind pass 2
+    issue(item + gridDim.x);
+    cp_async_commit_group();
+    sign_words(item + gridDim.x, w0, w1);
+    fwht64_regs<T>(v);
+#pragma unroll
+    for (int j = 0; j < 64; ++j)
+      if (((j < 32 ? mlo : mhi) & (1u << (j & 31))) != 0u) samp[s64_slot(mlo, mhi, mypre, j)] = v[j];
+    __syncthreads();
+    T* leaves = P + (col * ell) * n_tiles + t;
+    for (int kk = tid; kk < ell; kk += S64_NT) leaves[kk * n_tiles] = samp[kslot[kk]];
+  }
+  cp_async_wait_group<0>();
+}
+
+// ---------------------------------------------------------------------------
+// 16-bit storage (bf16 / fp16): the same two-pass tile kernel on PACKED pairs.
+// Every butterfly op of the reference is one correctly rounded 16-bit op
+// (numpy/ml_dtypes round each op once), which add/sub/mul.rn.{bf16,f16}x2
+// compute natively two at a time.  Values stay in the 16-bit format in
+// shared memory as well (half the traffic of fp32 staging).
+// ---------------------------------------------------------------------------
+template <typename T> struct Pk;
+template <> struct Pk<__nv_bfloat16> {
+  __device__ __forceinline__ static uint32_t add(uint32_t a, uint32_t b) {
+    uint32_t r; asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+  __device__ __forceinline__ static uint32_t sub(uint32_t a, uint32_t b) {
+    uint32_t r; asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+  __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) {
+    uint32_t r; asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+};
+template <> struct Pk<__half> {
+  __device__ __forceinline__ static uint32_t add(uint32_t a, uint32_t b) {
+    uint32_t r; asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+  __device__ __forceinline__ static uint32_t sub(uint32_t a, uint32_t b) {
+    uint32_t r; asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+  __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) {
+    uint32_t r; asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+};
+
+// stage on the two halves of each register: (x, y) -> (x + y, x - y)
+template <typename T>
+__device__ __forceinline__ uint32_t pk_inner(uint32_t r) {
+  const uint32_t sw = __byte_perm(r, 0, 0x1032);
+  const uint32_t sm = Pk<T>::add(r, sw), df = Pk<T>::sub(r, sw);
+  return __byte_perm(sm, df, 0x5410);  // (sm.lo, df.lo)
+}
+
+// stages b..b+5 over 64 values packed as v[i] = (x_{2i}, x_{2i+1})
+template <typename T>
+__device__ __forceinline__ void fwht64_packed(uint32_t (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = pk_inner<T>(v[i]);
+#pragma unroll
+  for (int s2 = 0; s2 < 5; ++s2)
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (!(i & (1 << s2))) {
+        const uint32_t x = v[i], y = v[i | (1 << s2)];
+        v[i] = Pk<T>::add(x, y);
+        v[i | (1 << s2)] = Pk<T>::sub(x, y);
+      }
+}
+
+template <typename T>
+__device__ __forceinline__ float h16_to_float(uint16_t h) {
+  if constexpr (std::is_same<T, __half>::value) return __half2float(__ushort_as_half(h));
+  else return __bfloat162float(__ushort_as_bfloat16(h));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(S64_NT)
+srht64h_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_eff, int64_t k,
+                    const uint32_t* __restrict__ bits, const int64_t* __restrict__ idx, int ell,
+                    uint32_t scale2, float* __restrict__ P, int64_t n_tiles, const Status* st, int64_t e_base) {
+  constexpr int C = 8;  // elements per 16-byte chunk
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* smask = reinterpret_cast<unsigned long long*>(smem_raw);
+  T* stg0 = reinterpret_cast<T*>(smem_raw + 512);
+  T* stg1 = reinterpret_cast<T*>(smem_raw + 512 + s64_buf_bytes<T>());
+  if (st && failed(st)) return;
+  const int tid = threadIdx.x;
+  smask[tid] = 0ull;
+  __syncthreads();
+  for (int kk = tid; kk < ell; kk += S64_NT) {
+    const int p = (int)(__ldg(idx + kk) & (S64_TB - 1));
+    atomicOr(&smask[p & 63], 1ull << (p >> 6));
+  }
+  __syncthreads();
+  const unsigned long long mymask = smask[tid];
+  const uint32_t mlo = (uint32_t)mymask, mhi = (uint32_t)(mymask >> 32);
+  const int64_t items = n_eff * k;
+  auto issue = [&](int64_t item, T* buf) {
+    if (item >= items) return;
+    const int64_t col = item / n_eff, t = item - col * n_eff;
+    const int64_t e0 = t << S64_LOG;
+    const T* x = X + col * ldx + e0;
+    const int64_t nv = n - e0;
+    if (nv >= S64_TB) {
+      const T* src = x + tid * C;
+      T* dst = buf + s64_idx<T>(tid * C);
+#pragma unroll
+      for (int i = 0; i < S64_TB / (C * S64_NT); ++i)
+        cp_async16(dst + i * (S64_NT * C + s64_pad<T>() * C), src + i * S64_NT * C, 16);
+    } else {
+      for (int q = tid; q < S64_TB / C; q += S64_NT) {
+        const int e = q * C;
+        const int64_t rem = nv - e;
+        const int bytes = rem >= C ? 16 : (rem > 0 ? (int)rem * 2 : 0);
+        cp_async16(buf + s64_idx<T>(e), bytes > 0 ? (const void*)(x + e) : (const void*)x, bytes);
+      }
     }
   };
   int64_t item = blockIdx.x;
-  issue(item, buf0);
+  issue(item, stg0);
   cp_async_commit_group();
   for (int it = 0; item < items; ++it, item += gridDim.x) {
-    double* cur = buf0 + (it & 1) * tbp;
-    double* nxt = buf0 + ((it + 1) & 1) * tbp;
-    issue(item + gridDim.x, nxt);
+    T* cur = (it & 1) ? stg1 : stg0;
+    issue(item + gridDim.x, (it & 1) ? stg0 : stg1);
     cp_async_commit_group();
     cp_async_wait_group<1>();
     __syncthreads();
     const int64_t col = item / n_eff, t = item - col * n_eff;
-    const int64_t e0 = t << log_tb;
-    // pass 0: scale, signs (sketching.py:152-153), stages h = 1..8 in registers
-    for (int g = threadIdx.x; g < (tb >> 4); g += PIPE_NT) {
-      double* p = cur + pidx2(g << 4);
-      double v[16];
+    const int64_t e0 = t << S64_LOG;
+    uint32_t v[32];
+    {
+      uint4* row = reinterpret_cast<uint4*>(cur + s64_idx<T>(tid * 64));
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const double2 d = *reinterpret_cast<const double2*>(p + 2 * q);
-        v[2 * q] = d.x;
-        v[2 * q + 1] = d.y;
+        const uint4 d = row[q];
+        v[4 * q] = d.x; v[4 * q + 1] = d.y; v[4 * q + 2] = d.z; v[4 * q + 3] = d.w;
       }
-      const int64_t e = e0 + (g << 4);
+      const int64_t e = e0 + tid * 64;
       const int64_t eg = e_base + e;
-      const uint32_t w = __ldg(bits + (eg >> 5)) >> (eg & 31);
+      const uint32_t w0 = __ldg(bits + (eg >> 5)), w1 = __ldg(bits + (eg >> 5) + 1);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const double sv = __dmul_rn(v[j], scale_lo);
-        v[j] = (e + j < n) ? (((w >> j) & 1u) ? -sv : sv) : 0.0;
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t w = (i < 16 ? w0 : w1) >> ((2 * i) & 31);
+        const uint32_t flip = ((w & 1u) << 15) | ((w & 2u) << 30);
+        v[i] = Pk<T>::mul(v[i], scale2) ^ flip;  // fl(x * scale), then the sign
       }
-      reg_fwht16<double>(v);
+      if (e + 64 > n) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) *reinterpret_cast<double2*>(p + 2 * q) = make_double2(v[2 * q], v[2 * q + 1]);
+        for (int i = 0; i < 32; ++i) {
+          if (e + 2 * i >= n) v[i] &= 0xffff0000u;
+          if (e + 2 * i + 1 >= n) v[i] &= 0x0000ffffu;
+        }
+      }
+      fwht64_packed<T>(v);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) row[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
     __syncthreads();
-    for (int b = 4; b < log_tb; b += 4) {
-      const int r = log_tb - b;
-      if (r >= 4) fwht_pass2<4>(cur, b, tb);
-      else if (r == 3) fwht_pass2<3>(cur, b, tb);
-      else if (r == 2) fwht_pass2<2>(cur, b, tb);
-      else fwht_pass2<1>(cur, b, tb);
-      __syncthreads();
-    }
-    const int64_t mask = tb - 1;
-    double* leaves = P + (col * ell) * n_tiles + t;
-    for (int kk = threadIdx.x; kk < ell; kk += PIPE_NT) leaves[kk * n_tiles] = cur[pidx2((int)(__ldg(idx + kk) & mask))];
+    // pass 2: coordinates tid + 64 j packed as (j, j+1) pairs
+    const uint16_t* wk = reinterpret_cast<const uint16_t*>(cur);
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      v[i] = (uint32_t)wk[s64_idx<T>(tid + 128 * i)] | ((uint32_t)wk[s64_idx<T>(tid + 128 * i + 64)] << 16);
+    fwht64_packed<T>(v);
+    uint16_t* wo = reinterpret_cast<uint16_t*>(cur);
+#pragma unroll
+    for (int j = 0; j < 64; ++j)
+      if (((j < 32 ? mlo : mhi) & (1u << (j & 31))) != 0u)
+        wo[s64_idx<T>(tid + 64 * j)] = (uint16_t)((j & 1) ? (v[j >> 1] >> 16) : (v[j >> 1] & 0xffffu));
+    __syncthreads();
+    float* leaves = P + (col * ell) * n_tiles + t;
+    for (int kk = tid; kk < ell; kk += S64_NT)
+      leaves[kk * n_tiles] = h16_to_float<T>(wo[s64_idx<T>((int)(__ldg(idx + kk) & (S64_TB - 1)))]);
     __syncthreads();
   }
   cp_async_wait_group<0>();
@@ -282,10 +517,23 @@ __global__ void identity_kernel(const T* __restrict__ X, int64_t ldx, int64_t n,
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
+// standalone sketches use 4096-coordinate tiles for every dtype (the tile size
+// only regroups the same butterflies: any power of two gives the same bits)
+static SrhtGeom standalone_geom(const sqb_sketch* sk) {
+  SrhtGeom g;
+  const int lp = ilog2_exact(sk->n_pad);
+  g.log_tb = lp < S64_LOG ? lp : S64_LOG;
+  g.n_tiles = sk->n_pad >> g.log_tb;
+  const int64_t tb = int64_t(1) << g.log_tb;
+  g.n_eff = (sk->n + tb - 1) / tb;
+  return g;
+}
+
 size_t sketch_partials_bytes(const sqb_sketch* sk, int dtype, int64_t k) {
   if (sk->kind != SQB_SKETCH_SRHT) return dense_ws_bytes(sk, dtype, k);
-  const SrhtGeom g = srht_geom(sk, dtype);
-  return acc_bytes(dtype) * (size_t)sk->ell * (size_t)g.n_tiles * (size_t)k;
+  // room for the standalone geometry and for the fused column kernels' own tiles
+  const SrhtGeom g = srht_geom(sk, dtype), g2 = standalone_geom(sk);
+  return acc_bytes(dtype) * (size_t)sk->ell * (size_t)std::max(g.n_tiles, g2.n_tiles) * (size_t)k;
 }
 
 template <typename T>
@@ -300,23 +548,46 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
   const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && (ldx % VN == 0) &&
                    (g.log_tb >= 3);
   dim3 grid((unsigned)g.n_eff, (unsigned)k);
-  if constexpr (sizeof(T) == 8) {
-    if (vec && g.log_tb >= 4 && (e_base & 15) == 0) {
-      const int tb = 1 << g.log_tb;
-      const size_t psmem = 2 * sizeof(double) * (size_t)(tb + 2 * (tb >> 4));
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(srht_tile_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(80 << 10));
-        cudaFuncSetAttribute(srht_tile_pipe_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+  if constexpr (sizeof(T) == 2) {
+    if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0) {
+      constexpr size_t smemh = 512 + 2 * s64_buf_bytes<T>();
+      static bool attr_h = false;
+      if (!attr_h) {
+        cudaFuncSetAttribute(srht64h_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemh);
+        cudaFuncSetAttribute(srht64h_tile_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
-        attr = true;
+        attr_h = true;
       }
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srht64h_tile_kernel<T>, S64_NT, smemh);
+      per_sm = std::max(1, per_sm);
       const int64_t items = g.n_eff * k;
-      const unsigned gp = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, 3 * (int64_t)ctx->sm_count));
-      srht_tile_pipe_kernel<<<gp, PIPE_NT, psmem, ctx->stream>>>(
-          (const double*)X, ldx, n_local, g.log_tb, g.n_eff, k, sk->sign_bits, sk->indices, (int)sk->ell, sc,
-          (double*)P, g.n_tiles, st, e_base);
-      return check_launch(ctx, "srht_tile_pipe_kernel");
+      const unsigned gp = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)per_sm * ctx->sm_count));
+      const T s1 = T((float)sc);  // sc is already a value of T (srht_constants): exact
+      uint16_t s16b;
+      memcpy(&s16b, &s1, 2);
+      const uint32_t s16 = s16b;
+      srht64h_tile_kernel<T><<<gp, S64_NT, smemh, ctx->stream>>>((const T*)X, ldx, n_local, g.n_eff, k,
+                                                                 sk->sign_bits, sk->indices, (int)sk->ell,
+                                                                 s16 | (s16 << 16), (float*)P, g.n_tiles, st, e_base);
+      return check_launch(ctx, "srht64h_tile_kernel");
+    }
+  }
+  if constexpr (sizeof(T) >= 4) {
+    if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= S64_MAX_ELL) {
+      const size_t smem64 = s64_head_bytes((int)sk->ell, sizeof(T)) + s64_buf_bytes<T>();
+      cudaFuncSetAttribute(srht64_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64);
+      cudaFuncSetAttribute(srht64_tile_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srht64_tile_kernel<T>, S64_NT, smem64);
+      per_sm = std::max(1, per_sm);
+      const int64_t items = g.n_eff * k;
+      const unsigned gp = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)per_sm * ctx->sm_count));
+      srht64_tile_kernel<T><<<gp, S64_NT, smem64, ctx->stream>>>((const T*)X, ldx, n_local, g.n_eff, k,
+                                                                 sk->sign_bits, sk->indices, (int)sk->ell, (T)sc,
+                                                                 (T*)P, g.n_tiles, st, e_base);
+      return check_launch(ctx, "srht64_tile_kernel");
     }
   }
   if (vec) {
@@ -337,7 +608,7 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
 template <typename T>
 static int srht_tiles_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int64_t ldx, int64_t k,
                         void* P, const Status* st) {
-  return srht_tiles_geom_t<T>(ctx, sk, srht_geom_t<T>(sk), sk->n, 0, X, ldx, k, P, st);
+  return srht_tiles_geom_t<T>(ctx, sk, standalone_geom(sk), sk->n, 0, X, ldx, k, P, st);
 }
 
 template <typename T>
@@ -357,7 +628,7 @@ template <typename T>
 static int srht_tree_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* P, int64_t k, double* Y,
                        int64_t ldy, int64_t row_off, const Status* st) {
   using A = typename Lo<T>::acc;
-  const SrhtGeom g = srht_geom_t<T>(sk);
+  const SrhtGeom g = standalone_geom(sk);
   double sc, nm;
   srht_constants(sk, Lo<T>::code, &sc, &nm);
   dim3 grid((unsigned)((sk->ell + 7) / 8), (unsigned)k);

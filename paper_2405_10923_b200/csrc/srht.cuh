@@ -136,65 +136,84 @@ __device__ __forceinline__ void tile_gather(const typename Lo<T>::acc* sm, const
 }
 
 // Tree over tile leaves for output k, done by one warp.  leaves[t] for
-// t < n_eff, +0 for n_eff <= t < n_tiles (all-padding tiles).  Lane L owns the
-// S = n_tiles/32 CONSECUTIVE tiles [L*S, (L+1)*S): the low log2(S) tree levels
-// run in registers (chunks of 8 whose loads are issued together, then a
-// binary-counter stack across chunks), the top 5 levels are lane shuffles —
-// all in level order with the lower tile range as the left operand.
+// t < n_eff, +0 for n_eff <= t < n_tiles (all-padding tiles).  The warp walks
+// the leaves in CHUNKS of 32*R consecutive tiles (R = 8, or fewer for small
+// n_tiles), one coalesced run per chunk, loaded one chunk ahead: lane L holds
+// the R tiles [L*R, (L+1)*R) of the chunk (levels 0..log2 R - 1 in registers),
+// the next 5 levels are lane shuffles, and the chunk values are combined by a
+// binary-counter stack with static register indices — every level in order,
+// lower tile range as the left operand.  Supports up to 256 chunks
+// (n_tiles <= 65536).
 template <typename T>
 __device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<T>::acc* leaves,
                                                               int n_tiles, int n_eff, int64_t rhi) {
   using A = typename Lo<T>::acc;
   const int lane = threadIdx.x & 31;
-  const int S = n_tiles >= 32 ? (n_tiles >> 5) : 1;     // tiles per lane (power of two)
-  const int lanes = n_tiles >= 32 ? 32 : n_tiles;        // lanes holding tiles
-  int sub = 0;
-  while ((1 << sub) < S) ++sub;
-  const int ch = S < 8 ? S : 8;
-  int lch = 0;
-  while ((1 << lch) < ch) ++lch;
-  const int t0 = lane * S;
-  A stk[16];
-  A lv = A(0);
-  if (lane < lanes) {
-    for (int j0 = 0; j0 < S; j0 += ch) {
-      A v[8];
+  const int lanes = n_tiles >= 32 ? 32 : n_tiles;                    // lanes holding tiles
+  const int R = n_tiles >= 256 ? 8 : (n_tiles >= 32 ? (n_tiles >> 5) : 1);
+  int lr = 0;
+  while ((1 << lr) < R) ++lr;
+  int ll = 0;
+  while ((1 << ll) < lanes) ++ll;
+  const int csz = lanes * R;            // tiles per chunk
+  const int nq = n_tiles / csz;         // chunks
+  A stk[8];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        const int t = t0 + j0 + jj;
-        v[jj] = (jj < ch && t < n_eff) ? leaves[t] : A(0);
+  for (int l = 0; l < 8; ++l) stk[l] = A(0);
+  A nx[8];
+  const int tl = lane * R;
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) nx[jj] = (lane < lanes && jj < R && tl + jj < n_eff) ? leaves[tl + jj] : A(0);
+  for (int q = 0; q < nq; ++q) {
+    A v[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) v[jj] = nx[jj];
+    if (q + 1 < nq) {
+      const int tb = (q + 1) * csz + tl;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) nx[jj] = (lane < lanes && jj < R && tb + jj < n_eff) ? leaves[tb + jj] : A(0);
+    }
+    // levels 0 .. lr-1 inside the lane
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      if ((1 << l) < R) {
+        const bool neg = (rhi >> l) & 1;
+#pragma unroll
+        for (int jj = 0; jj < 8; jj += (2 << l))
+          if (jj + (1 << l) < R)
+            v[jj] = neg ? Lo<T>::sub(v[jj], v[jj + (1 << l)]) : Lo<T>::add(v[jj], v[jj + (1 << l)]);
       }
+    }
+    // levels lr .. lr+ll-1 across lanes
+    A lv = v[0];
+    for (int l = 0; l < ll; ++l) {
+      const A o = __shfl_xor_sync(0xffffffffu, lv, 1 << l);
+      const bool upper = (lane >> l) & 1;
+      const A a = upper ? o : lv, b = upper ? lv : o;
+      lv = ((rhi >> (lr + l)) & 1) ? Lo<T>::sub(a, b) : Lo<T>::add(a, b);
+    }
+    A cv = __shfl_sync(0xffffffffu, lv, 0);
+    // levels lr+ll+l across chunks: binary counter
+    bool open = true;
 #pragma unroll
-      for (int l = 0; l < 3; ++l) {
-        if ((1 << l) < ch) {
-          const bool neg = (rhi >> l) & 1;
-#pragma unroll
-          for (int jj = 0; jj < 8; jj += (2 << l))
-            if (jj + (1 << l) < ch)
-              v[jj] = neg ? Lo<T>::sub(v[jj], v[jj + (1 << l)]) : Lo<T>::add(v[jj], v[jj + (1 << l)]);
+    for (int l = 0; l < 8; ++l) {
+      if (open) {
+        if ((q >> l) & 1) {
+          cv = ((rhi >> (lr + ll + l)) & 1) ? Lo<T>::sub(stk[l], cv) : Lo<T>::add(stk[l], cv);
+        } else {
+          stk[l] = cv;
+          open = false;
         }
       }
-      A cv = v[0];
-      const int q = j0 >> lch;
-      int lvl = 0;
-      while ((q >> lvl) & 1) {
-        cv = ((rhi >> (lch + lvl)) & 1) ? Lo<T>::sub(stk[lvl], cv) : Lo<T>::add(stk[lvl], cv);
-        ++lvl;
-      }
-      stk[lvl] = cv;
     }
-    int top = 0;
-    while ((ch << top) < S) ++top;
-    lv = stk[top];
   }
-  // lane levels sub .. sub + log2(lanes) - 1
-  for (int l = 0; (1 << l) < lanes; ++l) {
-    const A o = __shfl_xor_sync(0xffffffffu, lv, 1 << l);
-    const bool upper = (lane >> l) & 1;
-    const A a = upper ? o : lv, b = upper ? lv : o;
-    lv = ((rhi >> (sub + l)) & 1) ? Lo<T>::sub(a, b) : Lo<T>::add(a, b);
-  }
-  return __shfl_sync(0xffffffffu, lv, 0);
+  int top = 0;
+  while ((1 << top) < nq) ++top;
+  A out = stk[0];
+#pragma unroll
+  for (int l = 1; l < 8; ++l)
+    if (l == top) out = stk[l];
+  return out;
 }
 
 }  // namespace sqb

@@ -214,11 +214,6 @@ __device__ __forceinline__ void s64_sample_maps(const int64_t* __restrict__ idx,
   __syncthreads();
 }
 
-// slot of (this thread, j) among the sampled coordinates (j compile-time after unrolling)
-__device__ __forceinline__ int s64_slot(uint32_t mlo, uint32_t mhi, int pre, int j) {
-  return j < 32 ? pre + __popc(mlo & ((1u << j) - 1u)) : pre + __popc(mlo) + __popc(mhi & ((1u << (j - 32)) - 1u));
-}
-
 // fp64 / fp32 storage (values stay in the storage type end to end)
 template <typename T>
 __global__ void __launch_bounds__(S64_NT)
@@ -297,16 +292,22 @@ srht64_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_ef
     }
     __syncthreads();
     // pass 2: coordinates tid + 64 j, stages h = 64 .. 2048
+    {
+      const T* col0 = buf + tid;  // s64_idx(tid + 64 j) = tid + j (64 + pad): constant offsets
 #pragma unroll
-    for (int j = 0; j < 64; ++j) v[j] = buf[s64_idx<T>(tid + 64 * j)];
+      for (int j = 0; j < 64; ++j) v[j] = col0[j * (64 + s64_pad<T>())];
+    }
     __syncthreads();  // tile buffer free: stream the next item in behind pass 2
     issue(item + gridDim.x);
     cp_async_commit_group();
     sign_words(item + gridDim.x, w0, w1);
     fwht64_regs<T>(v);
+    {
+      int slot = mypre;  // sampled coordinates of this thread in j order
 #pragma unroll
-    for (int j = 0; j < 64; ++j)
-      if (((j < 32 ? mlo : mhi) & (1u << (j & 31))) != 0u) samp[s64_slot(mlo, mhi, mypre, j)] = v[j];
+      for (int j = 0; j < 64; ++j)
+        if (((j < 32 ? mlo : mhi) & (1u << (j & 31))) != 0u) samp[slot++] = v[j];
+    }
     __syncthreads();
     T* leaves = P + (col * ell) * n_tiles + t;
     for (int kk = tid; kk < ell; kk += S64_NT) leaves[kk * n_tiles] = samp[kslot[kk]];
@@ -383,21 +384,17 @@ srht64h_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_e
   constexpr int C = 8;  // elements per 16-byte chunk
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* smask = reinterpret_cast<unsigned long long*>(smem_raw);
-  T* stg0 = reinterpret_cast<T*>(smem_raw + 512);
-  T* stg1 = reinterpret_cast<T*>(smem_raw + 512 + s64_buf_bytes<T>());
+  int* spre = reinterpret_cast<int*>(smem_raw + 512);
+  int* kslot = reinterpret_cast<int*>(smem_raw + 768);
+  uint16_t* samp = reinterpret_cast<uint16_t*>(smem_raw + s64_samp_off(ell));
+  T* buf = reinterpret_cast<T*>(smem_raw + s64_head_bytes(ell, 2));
   if (st && failed(st)) return;
   const int tid = threadIdx.x;
-  smask[tid] = 0ull;
-  __syncthreads();
-  for (int kk = tid; kk < ell; kk += S64_NT) {
-    const int p = (int)(__ldg(idx + kk) & (S64_TB - 1));
-    atomicOr(&smask[p & 63], 1ull << (p >> 6));
-  }
-  __syncthreads();
-  const unsigned long long mymask = smask[tid];
-  const uint32_t mlo = (uint32_t)mymask, mhi = (uint32_t)(mymask >> 32);
+  s64_sample_maps(idx, ell, smask, spre, kslot);
+  const uint32_t mlo = (uint32_t)smask[tid], mhi = (uint32_t)(smask[tid] >> 32);
+  const int mypre = spre[tid];
   const int64_t items = n_eff * k;
-  auto issue = [&](int64_t item, T* buf) {
+  auto issue = [&](int64_t item) {
     if (item >= items) return;
     const int64_t col = item / n_eff, t = item - col * n_eff;
     const int64_t e0 = t << S64_LOG;
@@ -418,28 +415,31 @@ srht64h_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_e
       }
     }
   };
+  auto sign_words = [&](int64_t item, uint32_t& a0, uint32_t& a1) {
+    if (item >= items) return;
+    const int64_t col = item / n_eff, t = item - col * n_eff;
+    const int64_t eg = e_base + (t << S64_LOG) + tid * 64;
+    a0 = __ldg(bits + (eg >> 5));
+    a1 = __ldg(bits + (eg >> 5) + 1);
+  };
   int64_t item = blockIdx.x;
-  issue(item, stg0);
+  uint32_t w0 = 0, w1 = 0;
+  issue(item);
   cp_async_commit_group();
-  for (int it = 0; item < items; ++it, item += gridDim.x) {
-    T* cur = (it & 1) ? stg1 : stg0;
-    issue(item + gridDim.x, (it & 1) ? stg0 : stg1);
-    cp_async_commit_group();
-    cp_async_wait_group<1>();
+  sign_words(item, w0, w1);
+  for (; item < items; item += gridDim.x) {
+    cp_async_wait_group<0>();
     __syncthreads();
     const int64_t col = item / n_eff, t = item - col * n_eff;
-    const int64_t e0 = t << S64_LOG;
+    const int64_t e = (t << S64_LOG) + tid * 64;
     uint32_t v[32];
     {
-      uint4* row = reinterpret_cast<uint4*>(cur + s64_idx<T>(tid * 64));
+      uint4* row = reinterpret_cast<uint4*>(buf + s64_idx<T>(tid * 64));
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const uint4 d = row[q];
         v[4 * q] = d.x; v[4 * q + 1] = d.y; v[4 * q + 2] = d.z; v[4 * q + 3] = d.w;
       }
-      const int64_t e = e0 + tid * 64;
-      const int64_t eg = e_base + e;
-      const uint32_t w0 = __ldg(bits + (eg >> 5)), w1 = __ldg(bits + (eg >> 5) + 1);
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const uint32_t w = (i < 16 ? w0 : w1) >> ((2 * i) & 31);
@@ -460,21 +460,28 @@ srht64h_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_e
     }
     __syncthreads();
     // pass 2: coordinates tid + 64 j packed as (j, j+1) pairs
-    const uint16_t* wk = reinterpret_cast<const uint16_t*>(cur);
+    {
+      const uint16_t* col0 = reinterpret_cast<const uint16_t*>(buf) + tid;
+      constexpr int RS = 64 + s64_pad<T>();
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      v[i] = (uint32_t)wk[s64_idx<T>(tid + 128 * i)] | ((uint32_t)wk[s64_idx<T>(tid + 128 * i + 64)] << 16);
+      for (int i = 0; i < 32; ++i)
+        v[i] = __byte_perm((uint32_t)col0[(2 * i) * RS], (uint32_t)col0[(2 * i + 1) * RS], 0x5410);
+    }
+    __syncthreads();  // tile buffer free: stream the next item in behind pass 2
+    issue(item + gridDim.x);
+    cp_async_commit_group();
+    sign_words(item + gridDim.x, w0, w1);
     fwht64_packed<T>(v);
-    uint16_t* wo = reinterpret_cast<uint16_t*>(cur);
+    {
+      int slot = mypre;
 #pragma unroll
-    for (int j = 0; j < 64; ++j)
-      if (((j < 32 ? mlo : mhi) & (1u << (j & 31))) != 0u)
-        wo[s64_idx<T>(tid + 64 * j)] = (uint16_t)((j & 1) ? (v[j >> 1] >> 16) : (v[j >> 1] & 0xffffu));
+      for (int j = 0; j < 64; ++j)
+        if (((j < 32 ? mlo : mhi) & (1u << (j & 31))) != 0u)
+          samp[slot++] = (uint16_t)((j & 1) ? (v[j >> 1] >> 16) : (v[j >> 1] & 0xffffu));
+    }
     __syncthreads();
     float* leaves = P + (col * ell) * n_tiles + t;
-    for (int kk = tid; kk < ell; kk += S64_NT)
-      leaves[kk * n_tiles] = h16_to_float<T>(wo[s64_idx<T>((int)(__ldg(idx + kk) & (S64_TB - 1)))]);
-    __syncthreads();
+    for (int kk = tid; kk < ell; kk += S64_NT) leaves[kk * n_tiles] = h16_to_float<T>(samp[kslot[kk]]);
   }
   cp_async_wait_group<0>();
 }
@@ -549,15 +556,11 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
                    (g.log_tb >= 3);
   dim3 grid((unsigned)g.n_eff, (unsigned)k);
   if constexpr (sizeof(T) == 2) {
-    if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0) {
-      constexpr size_t smemh = 512 + 2 * s64_buf_bytes<T>();
-      static bool attr_h = false;
-      if (!attr_h) {
-        cudaFuncSetAttribute(srht64h_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemh);
-        cudaFuncSetAttribute(srht64h_tile_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
-        attr_h = true;
-      }
+    if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= S64_MAX_ELL) {
+      const size_t smemh = s64_head_bytes((int)sk->ell, 2) + s64_buf_bytes<T>();
+      cudaFuncSetAttribute(srht64h_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemh);
+      cudaFuncSetAttribute(srht64h_tile_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srht64h_tile_kernel<T>, S64_NT, smemh);
       per_sm = std::max(1, per_sm);

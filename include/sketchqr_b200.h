@@ -150,6 +150,29 @@ int sqb_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
                   double* T, int64_t ldt, double* R, int64_t ldr,
                   double* sigmas, double* rhos, double* betas);
 
+/* The same factorization with HOST operands: the call shape of the
+ * reference's rhqr_left (numpy W in, float64 numpy factors out,
+ * rhqr.py:254-267).  W: N x m float64 host array, row-major (w_layout 0,
+ * C-order, element (i, j) at W[i*ldw + j]) or column-major (w_layout 1,
+ * W[i + j*ldw]); it is rounded to lo_dtype on the device (round_to,
+ * rhqr.py:264; overflow -> device status SQB_ERR_RANGE, val = largest
+ * offending |w|).  Outputs are float64 host arrays, column-major: U (N x m,
+ * ldu), S ((m+ell) x m), T, R (m x m), sigmas/rhos/betas (m).  The PCIe
+ * transfers overlap the factorization: a column-major W streams in column
+ * groups as the sweep needs them, and U streams back in column groups as
+ * they become final.  Host buffers should be page-locked (pageable ones are
+ * staged synchronously by the driver, which removes the overlap).  Returns
+ * after the outputs are written; device scratch belongs to the context.   */
+int sqb_rhqr_left_host(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                       const double* W, int64_t N, int64_t m, int64_t ldw, int w_layout,
+                       double* U, int64_t ldu, double* S, int64_t lds,
+                       double* T, int64_t ldt, double* R, int64_t ldr,
+                       double* sigmas, double* rhos, double* betas);
+
+/* Release the context's grow-only device scratch (workspace and the
+ * host-operand arena); it is re-allocated on the next call that needs it. */
+int sqb_ctx_trim(sqb_ctx* ctx);
+
 /* Blocked left-looking RHQR (rhqr_block, rhqr.py:334-365): panels of
  * block_size columns; every earlier panel is applied compactly to the panel
  * (one re-sketch per earlier panel), then the panel is swept with pivot

@@ -60,6 +60,9 @@ _SIGS = {
     "sqb_embedded_apply": ([vp, C.POINTER(SketchDesc), i64, C.c_int, dp, i64, i64, dp, i64], C.c_int),
     "sqb_rhqr_left": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, dp, i64, i64, i64, dp, i64,
                        dp, i64, dp, i64, dp, i64, dp, dp, dp], C.c_int),
+    "sqb_rhqr_left_host": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, vp, i64, i64, i64, C.c_int,
+                            vp, i64, vp, i64, vp, i64, vp, i64, vp, vp, vp], C.c_int),
+    "sqb_ctx_trim": ([vp], C.c_int),
     "sqb_rhqr_block": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, dp, i64, i64, i64, i64, dp, i64,
                         dp, i64, dp, i64, dp, i64, dp, dp, dp], C.c_int),
     "sqb_rhqr_right": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, dp, i64, i64, i64, dp, i64,

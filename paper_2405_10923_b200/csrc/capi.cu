@@ -66,11 +66,26 @@ int sqb_ctx_create(int device, void* stream, sqb_ctx** out) {
   return SQB_OK;
 }
 
+int sqb_ctx_trim(sqb_ctx* ctx) {
+  SQB_TRY(prep(ctx));
+  SQB_CUDA_TRY(cudaDeviceSynchronize());
+  if (ctx->ws) SQB_CUDA_TRY(cudaFree(ctx->ws));
+  if (ctx->big) SQB_CUDA_TRY(cudaFree(ctx->big));
+  ctx->ws = ctx->big = nullptr;
+  ctx->ws_bytes = ctx->big_bytes = 0;
+  return SQB_OK;
+}
+
 int sqb_ctx_destroy(sqb_ctx* ctx) {
   if (!ctx) return SQB_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->s_in) cudaStreamSynchronize(ctx->s_in);
+  if (ctx->s_out) cudaStreamSynchronize(ctx->s_out);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->big) cudaFree(ctx->big);
+  if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+  if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
   if (ctx->d_status) cudaFree(ctx->d_status);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);

@@ -8,6 +8,23 @@
 
 #include "common.cuh"
 
+namespace sqb {
+// Optional per-column callbacks of the left-looking sweep, used by the
+// host-buffer entry points (host_pipe.cu) to overlap PCIe transfers with the
+// factorization.  Both run on the host at enqueue time.
+struct SweepHooks {
+  // columns of W arrive in groups: make ctx->stream wait until columns
+  // [0, upto) are resident; returns the end of the group that holds column
+  // upto-1 (>= upto).  A null hooks pointer / streamed_input == false means
+  // W is fully resident before the sweep starts.
+  bool streamed_input = false;
+  virtual int64_t wait_cols(sqb_ctx* ctx, int64_t upto) = 0;
+  // called after the launch that finalises U[:, c] has been enqueued
+  virtual int col_final(sqb_ctx* ctx, int64_t c) = 0;
+  virtual ~SweepHooks() {}
+};
+}  // namespace sqb
+
 struct sqb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -30,6 +47,13 @@ struct sqb_ctx {
   int dbg_col = -1;
   int nranks = 1;
   int rank = 0;
+  // host-buffer entry points (host_pipe.cu): device copies of the caller's
+  // host operands and transfer staging live in a second grow-only arena;
+  // copy-engine streams run the H2D / D2H pipelines beside ctx->stream
+  sqb::SweepHooks* hooks = nullptr;
+  void* big = nullptr;
+  size_t big_bytes = 0;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
 };
 
 namespace sqb {

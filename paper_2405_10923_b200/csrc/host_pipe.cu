@@ -1,0 +1,369 @@
+// Host-buffer entry points: the reference's call shape (numpy W in, numpy
+// factors out, rhqr.py:254-267) with the PCIe transfers overlapped with the
+// device factorization.
+//
+//   H2D   W arrives on the copy stream s_in.  A column-major host W streams in
+//         column groups: the sweep (rhqr_left.cu, ensure_y0) waits for a
+//         group only when pass c first needs y0_{c+1}, so the upload of
+//         later columns overlaps the factorization of earlier ones.  A
+//         row-major (C-order) host W can only be complete after its last row
+//         block, so it streams in row blocks through two device staging slots
+//         (transpose + rounding kernel per block) ahead of the whole sweep.
+//   D2H   U[:, c] is final once pass c+1 has rewritten it (lazy scaling,
+//         rhqr_kernels.cuh); the sweep calls col_final(c) after enqueuing that
+//         pass and every group of columns is copied back on s_out while later
+//         columns are still being factored.  S, T, R and the scalars follow
+//         the finish kernel.
+//
+// The device copies of W and U are context scratch (a grow-only arena),
+// never caller memory.  Host buffers should be page-locked for full PCIe
+// bandwidth (the facade allocates its outputs that way); pageable buffers
+// work but the driver stages them synchronously.
+#include <algorithm>
+#include <vector>
+
+#include "sketch.cuh"
+
+namespace sqb {
+
+int rhqr_left_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t,
+                       void*, int64_t, double*, int64_t, double*, int64_t, double*, int64_t, double*,
+                       double*, double*);
+
+// ---------------------------------------------------------------------------
+// conversion kernels: fp64 host layout -> column-major storage dtype (the
+// round_to of rhqr.py:264, precision.py:34-51: a finite value that overflows
+// the storage format is a PrecisionRangeError, reported through the status
+// word with the largest offending magnitude).
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T round_store(double x, Status* st) {
+  const auto r = Lo<T>::from_double(x);
+  if (isfinite(x) && !isfinite((double)r)) {
+    fail(st, SQB_ERR_RANGE, 0, 0.0);
+    atomicMax(reinterpret_cast<unsigned long long*>(&st->val),
+              (unsigned long long)__double_as_longlong(fabs(x)));
+  }
+  return Lo<T>::store(r);
+}
+
+// rows [0, R) of a row-major block (ld lds) -> dst[i + j*ldd], 32x32 tiles
+template <typename T>
+__global__ void __launch_bounds__(256) rowblock_to_colmajor(const double* __restrict__ src, int64_t lds,
+                                                            int64_t R, int64_t m, T* __restrict__ dst,
+                                                            int64_t ldd, Status* st) {
+  __shared__ double tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = i0 + r, j = j0 + tx;
+    tile[r][tx] = (i < R && j < m) ? src[i * lds + j] : 0.0;
+  }
+  __syncthreads();
+  for (int c = ty; c < 32; c += 8) {
+    const int64_t i = i0 + tx, j = j0 + c;
+    if (i < R && j < m) dst[i + j * ldd] = round_store<T>(tile[tx][c], st);
+  }
+}
+
+// column-major fp64 block (ld lds) -> column-major storage dtype
+template <typename T>
+__global__ void colblock_convert(const double* __restrict__ src, int64_t lds, int64_t R, int64_t k,
+                                 T* __restrict__ dst, int64_t ldd, Status* st) {
+  const int64_t tot = R * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % R, j = e / R;
+    dst[i + j * ldd] = round_store<T>(src[i + j * lds], st);
+  }
+}
+
+// column-major storage dtype -> fp64 (the float64 arrays the reference returns)
+template <typename T>
+__global__ void colblock_widen(const T* __restrict__ src, int64_t lds, int64_t R, int64_t k,
+                               double* __restrict__ dst, int64_t ldd) {
+  const int64_t tot = R * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % R, j = e / R;
+    dst[i + j * ldd] = (double)Lo<T>::load(src[i + j * lds]);
+  }
+}
+
+static size_t esize(int code) { return code == SQB_F64 ? 8 : code == SQB_F32 ? 4 : 2; }
+
+template <typename F>
+static int by_dtype(int code, F&& f) {
+  switch (code) {
+    case SQB_F64: return f(double());
+    case SQB_F32: return f(float());
+    case SQB_F16: return f(__half());
+    case SQB_BF16: return f(__nv_bfloat16());
+  }
+  return SQB_ERR_ARG;
+}
+
+static int ensure_streams(sqb_ctx* ctx) {
+  if (!ctx->s_in) SQB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
+  if (!ctx->s_out) SQB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
+  return SQB_OK;
+}
+
+static int big_reserve(sqb_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->big_bytes) return SQB_OK;
+  SQB_CUDA_TRY(cudaDeviceSynchronize());
+  if (ctx->big) SQB_CUDA_TRY(cudaFree(ctx->big));
+  ctx->big = nullptr;
+  ctx->big_bytes = 0;
+  SQB_CUDA_TRY(cudaMalloc(&ctx->big, bytes));
+  ctx->big_bytes = bytes;
+  return SQB_OK;
+}
+
+struct EventPool {
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t get() {
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    ev.push_back(e);
+    return e;
+  }
+  ~EventPool() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+};
+
+// leading dimension / base shift of a device column-major buffer so that row
+// `align_row` of every column is 16-byte aligned (devarray.empty_colmajor)
+struct DevLayout {
+  int64_t ld, shift;  // elements
+  size_t bytes;
+};
+static DevLayout dev_layout(int64_t rows, int64_t cols, int code, int64_t align_row) {
+  const int64_t vn = 16 / (int64_t)esize(code);
+  DevLayout L;
+  L.ld = std::max<int64_t>(16, (rows + 15) / 16 * 16);
+  L.shift = ((-align_row) % vn + vn) % vn;
+  L.bytes = (size_t)(L.ld * std::max<int64_t>(cols, 1) + L.shift + vn) * esize(code);
+  return L;
+}
+
+struct HostPipe : SweepHooks {
+  sqb_ctx* ctx = nullptr;
+  EventPool* evp = nullptr;
+  int code = SQB_F64;
+  int64_t N = 0, m = 0;
+  // input
+  const double* Wh = nullptr;
+  int64_t ldwh = 0;
+  void* Wd = nullptr;
+  int64_t ldwd = 0;
+  double* stage_in[2] = {nullptr, nullptr};
+  int64_t stage_in_elems = 0;
+  int64_t gin = 8;               // columns per input group (column-major input)
+  std::vector<cudaEvent_t> ev_in;  // per input group, recorded after the group is resident
+  // output
+  double* Uh = nullptr;
+  int64_t lduh = 0;
+  const void* Ud = nullptr;
+  int64_t ldud = 0;
+  double* stage_out[2] = {nullptr, nullptr};
+  int64_t gout = 8;
+  int64_t out_done = 0;
+  int out_slot = 0;
+
+  int issue_input_colmajor() {
+    // column groups: a direct 2D copy for fp64 storage, staging + rounding otherwise
+    const size_t es = esize(code);
+    const int64_t ngrp = (m + gin - 1) / gin;
+    ev_in.resize(ngrp);
+    for (int64_t g = 0; g < ngrp; ++g) {
+      const int64_t c0 = g * gin, k = std::min(gin, m - c0);
+      if (code == SQB_F64) {
+        SQB_CUDA_TRY(cudaMemcpy2DAsync((char*)Wd + c0 * ldwd * es, ldwd * es, Wh + c0 * ldwh, ldwh * sizeof(double),
+                                       N * sizeof(double), k, cudaMemcpyHostToDevice, ctx->s_in));
+      } else {
+        double* sbuf = stage_in[g & 1];
+        SQB_CUDA_TRY(cudaMemcpy2DAsync(sbuf, N * sizeof(double), Wh + c0 * ldwh, ldwh * sizeof(double),
+                                       N * sizeof(double), k, cudaMemcpyHostToDevice, ctx->s_in));
+        const unsigned gb = (unsigned)std::min<int64_t>((N * k + 255) / 256, 4 * ctx->sm_count);
+        SQB_TRY(by_dtype(code, [&](auto t) {
+          using T = decltype(t);
+          colblock_convert<T><<<gb, 256, 0, ctx->s_in>>>(sbuf, N, N, k, (T*)Wd + c0 * ldwd, ldwd, ctx->d_status);
+          return check_launch(ctx, "colblock_convert");
+        }));
+      }
+      ev_in[g] = evp->get();
+      SQB_CUDA_TRY(cudaEventRecord(ev_in[g], ctx->s_in));
+    }
+    streamed_input = true;
+    return SQB_OK;
+  }
+
+  int issue_input_rowmajor() {
+    // row blocks through two staging slots; copy and transpose share s_in,
+    // so slot reuse is ordered without extra events
+    const int64_t rb = std::max<int64_t>(1, stage_in_elems / std::max<int64_t>(ldwh, 1));
+    int slot = 0;
+    for (int64_t r0 = 0; r0 < N; r0 += rb, slot ^= 1) {
+      const int64_t R = std::min(rb, N - r0);
+      SQB_CUDA_TRY(cudaMemcpyAsync(stage_in[slot], Wh + r0 * ldwh, (size_t)R * ldwh * sizeof(double),
+                                   cudaMemcpyHostToDevice, ctx->s_in));
+      dim3 grid((unsigned)((R + 31) / 32), (unsigned)((m + 31) / 32));
+      SQB_TRY(by_dtype(code, [&](auto t) {
+        using T = decltype(t);
+        rowblock_to_colmajor<T><<<grid, 256, 0, ctx->s_in>>>(stage_in[slot], ldwh, R, m, (T*)Wd + r0, ldwd,
+                                                             ctx->d_status);
+        return check_launch(ctx, "rowblock_to_colmajor");
+      }));
+    }
+    cudaEvent_t e = evp->get();
+    SQB_CUDA_TRY(cudaEventRecord(e, ctx->s_in));
+    SQB_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, e, 0));
+    streamed_input = false;
+    return SQB_OK;
+  }
+
+  int64_t wait_cols(sqb_ctx* c, int64_t upto) override {
+    const int64_t g = (upto - 1) / gin;
+    cudaStreamWaitEvent(c->stream, ev_in[g], 0);
+    return std::min(m, (g + 1) * gin);
+  }
+
+  int flush_out(int64_t end) {
+    // U[:, out_done:end] are final on ctx->stream
+    if (end <= out_done) return SQB_OK;
+    cudaEvent_t e = evp->get();
+    SQB_CUDA_TRY(cudaEventRecord(e, ctx->stream));
+    SQB_CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, e, 0));
+    const int64_t c0 = out_done, k = end - out_done;
+    if (code == SQB_F64) {
+      SQB_CUDA_TRY(cudaMemcpy2DAsync(Uh + c0 * lduh, lduh * sizeof(double), (const double*)Ud + c0 * ldud,
+                                     ldud * sizeof(double), N * sizeof(double), k, cudaMemcpyDeviceToHost,
+                                     ctx->s_out));
+    } else {
+      double* sbuf = stage_out[out_slot];
+      out_slot ^= 1;
+      const unsigned gb = (unsigned)std::min<int64_t>((N * k + 255) / 256, 4 * ctx->sm_count);
+      SQB_TRY(by_dtype(code, [&](auto t) {
+        using T = decltype(t);
+        colblock_widen<T><<<gb, 256, 0, ctx->s_out>>>((const T*)Ud + c0 * ldud, ldud, N, k, sbuf, N);
+        return check_launch(ctx, "colblock_widen");
+      }));
+      SQB_CUDA_TRY(cudaMemcpy2DAsync(Uh + c0 * lduh, lduh * sizeof(double), sbuf, N * sizeof(double),
+                                     N * sizeof(double), k, cudaMemcpyDeviceToHost, ctx->s_out));
+    }
+    out_done = end;
+    return SQB_OK;
+  }
+
+  int col_final(sqb_ctx*, int64_t c) override {
+    if (c + 1 - out_done >= gout || c + 1 == m) return flush_out(c + 1);
+    return SQB_OK;
+  }
+};
+
+}  // namespace sqb
+
+using namespace sqb;
+
+extern "C" int sqb_rhqr_left_host(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                                  const double* W, int64_t N, int64_t m, int64_t ldw, int w_layout,
+                                  double* U, int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt,
+                                  double* R, int64_t ldr, double* sigmas, double* rhos, double* betas) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  if (lo_dtype < SQB_F64 || lo_dtype > SQB_BF16) return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+  if (!W || !U || !S || !T || !R || !sigmas || !rhos || !betas)
+    return set_error(ctx, SQB_ERR_ARG, "null host buffer");
+  if (N < 1 || m < 1) return set_error(ctx, SQB_ERR_ARG, "empty matrix");
+  const bool rowmajor = w_layout == 0;
+  if (w_layout != 0 && w_layout != 1) return set_error(ctx, SQB_ERR_ARG, "unknown layout %d", w_layout);
+  if ((rowmajor && ldw < m) || (!rowmajor && ldw < N) || ldu < N || lds < m + sk->ell || ldt < m || ldr < m)
+    return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
+  SQB_TRY(ensure_streams(ctx));
+
+  // device scratch: W, U (column-major, row m 16-byte aligned), S, T, R,
+  // scalars, input/output staging
+  const DevLayout LW = dev_layout(N, m, lo_dtype, m), LU = LW;
+  const int64_t od = m + sk->ell;
+  const int64_t stage_in_elems =
+      lo_dtype == SQB_F64 && !rowmajor ? 0 : std::max<int64_t>(rowmajor ? 4 * ldw : 8 * N, (int64_t)(32ll << 20) / 8);
+  const int64_t gout = 8;
+  const int64_t stage_out_elems = lo_dtype == SQB_F64 ? 0 : gout * N;
+  WsPlan plan;
+  const size_t iW = plan.add(LW.bytes), iU = plan.add(LU.bytes);
+  const size_t iS = plan.add(sizeof(double) * od * m), iT = plan.add(sizeof(double) * m * m),
+               iR = plan.add(sizeof(double) * m * m), iX = plan.add(sizeof(double) * 3 * m);
+  const size_t iI0 = plan.add(sizeof(double) * stage_in_elems), iI1 = plan.add(sizeof(double) * stage_in_elems);
+  const size_t iO0 = plan.add(sizeof(double) * stage_out_elems), iO1 = plan.add(sizeof(double) * stage_out_elems);
+  SQB_TRY(big_reserve(ctx, plan.total + 256));
+  char* base = static_cast<char*>(ctx->big);
+  const size_t es = esize(lo_dtype);
+  void* Wd = base + plan.offs[iW] + LW.shift * es;
+  void* Ud = base + plan.offs[iU] + LU.shift * es;
+  double* Sd = reinterpret_cast<double*>(base + plan.offs[iS]);
+  double* Td = reinterpret_cast<double*>(base + plan.offs[iT]);
+  double* Rd = reinterpret_cast<double*>(base + plan.offs[iR]);
+  double* Xd = reinterpret_cast<double*>(base + plan.offs[iX]);
+
+  // the s_in / s_out streams must not run ahead of earlier work on ctx->stream
+  // (a previous call may still be reading the arena)
+  EventPool evp;
+  {
+    cudaEvent_t e = evp.get();
+    SQB_CUDA_TRY(cudaEventRecord(e, ctx->stream));
+    SQB_CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, e, 0));
+    SQB_CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, e, 0));
+  }
+  SQB_CUDA_TRY(cudaMemsetAsync(ctx->d_status, 0, sizeof(Status), ctx->stream));
+  {
+    cudaEvent_t e = evp.get();  // status cleared before the conversion kernels may set it
+    SQB_CUDA_TRY(cudaEventRecord(e, ctx->stream));
+    SQB_CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, e, 0));
+  }
+
+  HostPipe hp;
+  hp.ctx = ctx;
+  hp.evp = &evp;
+  hp.code = lo_dtype;
+  hp.N = N;
+  hp.m = m;
+  hp.Wh = W;
+  hp.ldwh = ldw;
+  hp.Wd = Wd;
+  hp.ldwd = LW.ld;
+  hp.stage_in[0] = reinterpret_cast<double*>(base + plan.offs[iI0]);
+  hp.stage_in[1] = reinterpret_cast<double*>(base + plan.offs[iI1]);
+  hp.stage_in_elems = stage_in_elems;
+  hp.gin = std::max<int64_t>(1, std::min<int64_t>(8, stage_in_elems > 0 ? stage_in_elems / N : 8));
+  hp.Uh = U;
+  hp.lduh = ldu;
+  hp.Ud = Ud;
+  hp.ldud = LU.ld;
+  hp.stage_out[0] = reinterpret_cast<double*>(base + plan.offs[iO0]);
+  hp.stage_out[1] = reinterpret_cast<double*>(base + plan.offs[iO1]);
+  hp.gout = gout;
+  SQB_TRY(rowmajor ? hp.issue_input_rowmajor() : hp.issue_input_colmajor());
+
+  ctx->hooks = &hp;
+  int rc = rhqr_left_dispatch(ctx, sk, scaling, lo_dtype, Wd, N, m, LW.ld, Ud, LU.ld, Sd, od, Td, m, Rd, m,
+                              Xd, Xd + m, Xd + 2 * m);
+  ctx->hooks = nullptr;
+  if (rc != SQB_OK) {
+    cudaDeviceSynchronize();
+    return rc;
+  }
+  // small factors after the finish kernel
+  SQB_CUDA_TRY(cudaMemcpy2DAsync(S, lds * sizeof(double), Sd, od * sizeof(double), od * sizeof(double), m,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaMemcpy2DAsync(T, ldt * sizeof(double), Td, m * sizeof(double), m * sizeof(double), m,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaMemcpy2DAsync(R, ldr * sizeof(double), Rd, m * sizeof(double), m * sizeof(double), m,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaMemcpyAsync(sigmas, Xd, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaMemcpyAsync(rhos, Xd + m, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaMemcpyAsync(betas, Xd + 2 * m, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaStreamSynchronize(ctx->s_out));
+  SQB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SQB_OK;
+}

@@ -75,14 +75,28 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
   Status* st = ctx->d_status;
 
   SQB_TRY(zero2d(ctx, Tm, ncol, ncol, ldt));
-  // raw sketches y0 = Psi W (all columns; rhqr.py:240 for every column)
-  SQB_TRY(launch_copy_top(ctx, Lo<T>::code, W, ldw, m, ncol, Y0, od, st));
+  // raw sketches y0 = Psi W (rhqr.py:240 for every column).  Pass c and step
+  // c read y0_{c+1}; with a streamed input (host_pipe.cu) the columns arrive
+  // in groups and each group is sketched as soon as it is resident.
+  SweepHooks* hk = ctx->hooks;
+  const bool streamed = hk && hk->streamed_input;
   const size_t esz = sizeof(T);
-  for (int64_t c0 = 0; c0 < ncol; c0 += chunk) {
-    const int64_t kc = std::min(chunk, ncol - c0);
-    SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const char*)W + (c0 * ldw + m) * esz, ldw, kc,
-                          Y0 + c0 * od, od, m, P, st));
-  }
+  int64_t y0_done = 0;
+  auto ensure_y0 = [&](int64_t upto) -> int {  // y0 of columns [0, upto)
+    upto = std::min(upto, ncol);
+    if (upto <= y0_done) return SQB_OK;
+    int64_t end = streamed ? std::min(ncol, hk->wait_cols(ctx, upto)) : ncol;
+    SQB_TRY(launch_copy_top(ctx, Lo<T>::code, (const char*)W + y0_done * ldw * esz, ldw, m, end - y0_done,
+                            Y0 + y0_done * od, od, st));
+    for (int64_t c0 = y0_done; c0 < end; c0 += chunk) {
+      const int64_t kc = std::min(chunk, end - c0);
+      SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const char*)W + (c0 * ldw + m) * esz, ldw, kc,
+                            Y0 + c0 * od, od, m, P, st));
+    }
+    y0_done = end;
+    return SQB_OK;
+  };
+  SQB_TRY(ensure_y0(2));
   double scale_lo = 0.0, norm_lo = 0.0;
   if (srht) srht_constants(sk, Lo<T>::code, &scale_lo, &norm_lo);
 
@@ -114,6 +128,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
   auto colk = vec ? rhqr_col_kernel<T, VN> : rhqr_col_kernel<T, 1>;
   cudaFuncSetAttribute(colk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
   for (int64_t c = 1; c < ncol; ++c) {
+    SQB_TRY(ensure_y0(c + 2));
     double* a_cur = abuf + (c & 1) * (m + 1);
     double* a_nxt = abuf + ((c + 1) & 1) * (m + 1);
     ColArgs ca{};
@@ -130,6 +145,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
                        ca));
     // algorithmic bytes of this pass: read U[:, :c] and W[:, c], write U[:, c]
     prof_end(ctx, (double)esz * (double)N * (double)(c + 2));
+    if (hk) SQB_TRY(hk->col_final(ctx, c - 1));  // pass c wrote the scaled U[:, c-1]
     if (!srht)
       SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const char*)U + (c * ldu + m) * esz, ldu, 1, y, od,
                             m, P, st));
@@ -150,6 +166,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
                        (const double*)fs, scaling, Tm, ldt, (int)ncol, (const double*)vbuf,
                        (const double*)betas, (const Status*)st));
   }
+  if (hk) SQB_TRY(hk->col_final(ctx, ncol - 1));
   return SQB_OK;
 }
 

@@ -87,10 +87,14 @@ def to_device(X, tag: str, align_row: int = 0) -> torch.Tensor:
     A = host_to_lo(X, tag)
     if A.ndim == 1:
         A = A[:, None]
+    if not (A.flags.c_contiguous or A.flags.f_contiguous):
+        A = np.ascontiguousarray(A)
+    # a Fortran-order host array is uploaded as is (the device copy keeps its
+    # strides, so the column-major store below is a plain copy)
     if tag == "bf16":
-        src = torch.from_numpy(np.ascontiguousarray(A).view(np.int16)).view(torch.bfloat16)
+        src = torch.from_numpy(A.view(np.int16)).view(torch.bfloat16)
     else:
-        src = torch.from_numpy(np.ascontiguousarray(A))
+        src = torch.from_numpy(A)
     out = empty_colmajor(A.shape[0], A.shape[1], tag, align_row)
     out.copy_(src.cuda(non_blocking=False))
     return out
@@ -110,6 +114,35 @@ def to_numpy(t: torch.Tensor) -> np.ndarray:
     out.copy_(h, non_blocking=True)
     torch.cuda.current_stream().synchronize()
     return out.numpy()
+
+
+def host_f64(X):
+    """Host operand -> (float64 ndarray, layout, ld) for the host-buffer entry
+    points: layout 0 = row-major (C-order, ld = row stride), 1 = column-major
+    (Fortran order, ld = column stride).  A CPU tensor is viewed, not copied,
+    so page-locked tensors keep their full-bandwidth DMA path."""
+    if isinstance(X, torch.Tensor):
+        X = X.detach()
+        X = X.numpy() if X.dtype == torch.float64 else X.to(torch.float64).numpy()
+    A = np.asarray(X, dtype=np.float64)
+    if A.ndim == 1:
+        A = A[:, None]
+    if A.ndim != 2:
+        raise ValueError(f"expected a matrix, got shape {A.shape}")
+    n, m = A.shape
+    if A.flags.c_contiguous and (A.strides[0] // 8) >= m:
+        return A, 0, max(m, A.strides[0] // 8)
+    if A.flags.f_contiguous:
+        return A, 1, max(n, A.strides[1] // 8 if m > 1 else n)
+    A = np.ascontiguousarray(A)
+    return A, 0, m
+
+
+def pinned_f64(rows: int, cols: int) -> np.ndarray:
+    """Fresh float64 (rows x cols) Fortran-order ndarray in page-locked memory
+    (torch's caching host allocator; the array keeps the block alive)."""
+    t = torch.empty((max(cols, 1), max(rows, 1)), dtype=torch.float64, pin_memory=True)
+    return t.numpy().T[:rows, :cols]
 
 
 def np_dtype_tag(dt) -> str:

@@ -16,10 +16,11 @@ import numpy as np
 import torch
 
 from . import _lib
-from .devarray import CODES, empty_colmajor, is_device, ld_of, to_device, to_numpy, tag_of_torch
+from .devarray import (CODES, empty_colmajor, host_f64, is_device, ld_of, pinned_f64, to_device, to_numpy,
+                       tag_of_torch)
 from .linalg import (SCALE_SQRT2, SCALE_UNIT, BreakdownError, SingularFactorError, check_scaling,
                      scaling_code)
-from .precision import DOUBLE_POLICY, require_device_policy
+from .precision import DOUBLE_POLICY, PrecisionRangeError, require_device_policy
 from .sketching import EmbeddedSketch
 
 
@@ -76,11 +77,13 @@ def _embed(omega, n, m):
     return EmbeddedSketch(m, omega)
 
 
-def raise_status(ctx, what="factorization"):
+def raise_status(ctx, what="factorization", tag=None):
     """Map the device status word to the reference's exceptions."""
     code, col, val = ctx.status()
     if code == _lib.SQB_OK:
         return
+    if code == _lib.SQB_ERR_RANGE:  # round_to on the device (precision.py:45-50)
+        raise PrecisionRangeError(f"value {val:g} overflows {tag} range")
     if code == _lib.SQB_ERR_BREAKDOWN:
         if what == "rec_rhqr":
             if val == -1.0:  # rhqr.py:388-391
@@ -131,11 +134,37 @@ def rhqr_left(W, omega, scaling=SCALE_SQRT2, policy=None):
     host = not is_device(W)
     n, m = _shape2(W)
     psi = _embed(omega, n, m)
+    if host:
+        return _rhqr_left_host(W, psi, scaling, policy)
     Wd = to_device(W, policy.low, align_row=m)  # round_to(W, low) (rhqr.py:264)
     U, S, T, R, sg, rh, bt = rhqr_left_device(Wd, psi, scaling, policy)
     return RHQRFactors(U=_out(U, host), S=_out(S, host), T=_out(T, host), R=_out(R, host), psi=psi,
                        scaling=scaling, sigmas=_out(sg, host), rhos=_out(rh, host),
                        betas=_out(bt, host))
+
+
+def _rhqr_left_host(W, psi, scaling, policy):
+    """Host operands (numpy / CPU tensor): one sqb_rhqr_left_host call, which
+    uploads W, rounds it to the storage format on the device and overlaps
+    both PCIe directions with the sweep (csrc/host_pipe.cu).  The float64
+    factors come back as column-major (Fortran-order) ndarrays; U lives in
+    page-locked memory so its column groups stream back during the sweep."""
+    Wa, layout, ldw = host_f64(W)
+    n, m = Wa.shape
+    od = psi.out_dim
+    U = pinned_f64(n, m)
+    S = np.empty((m, od)).T
+    T = np.empty((m, m)).T
+    R = np.empty((m, m)).T
+    scal = np.empty(3 * m)
+    ctx = _lib.context()
+    p = lambda a: a.ctypes.data  # noqa: E731
+    ctx.check(_lib.lib().sqb_rhqr_left_host(
+        ctx.h, psi.omega.desc(), scaling_code(scaling), CODES[policy.low], p(Wa), n, m, ldw, layout,
+        p(U), n, p(S), od, p(T), m, p(R), m, p(scal), p(scal[m:]), p(scal[2 * m:])), "sqb_rhqr_left_host")
+    raise_status(ctx, "rhqr_left", policy.low)
+    return RHQRFactors(U=U, S=S, T=T, R=R, psi=psi, scaling=scaling, sigmas=scal[:m], rhos=scal[m:2 * m],
+                       betas=scal[2 * m:])
 
 
 def rhqr_right(W, omega, scaling=SCALE_SQRT2, policy=None):

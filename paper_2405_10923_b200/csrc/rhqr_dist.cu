@@ -209,8 +209,8 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
   constexpr int VN = VecN<T>::n;
   const size_t tile_bytes = tile_smem_bytes<A>(1 << TileCfg<T>::LOG_TB);
   const size_t col_smem_max = sizeof(A) * ((m + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(m + 1));
-  cudaFuncSetAttribute(rhqr_col_kernel<T, VN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
-  cudaFuncSetAttribute(rhqr_col_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
+  cudaFuncSetAttribute(col_kernel_select<T, VN>(true), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
+  cudaFuncSetAttribute(col_kernel_select<T, VN>(false), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
   for (int64_t c = 1; c < m; ++c) {
     for (int r = 0; r < L; ++r) {
       DistRank& d = rk[r];
@@ -223,16 +223,13 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
       ca.idx = sk->indices; ca.scale_lo = scale_lo; ca.P = d.P; ca.y = d.pay + ell;
       ca.S = d.S; ca.lds = d.lds; ca.T = d.T; ca.ldt = d.ldt; ca.Y0 = Y0; ca.vprev = d.vbuf; ca.betas = d.bet;
       ca.anext = d.abuf + ((c + 1) & 1) * (m + 1); ca.st = st;
+      ca.helper_first = helper_first_default();
       const bool vec = ((reinterpret_cast<uintptr_t>((const char*)d.W + d.mrow * esz) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>((const char*)d.U + d.mrow * esz) & 15) == 0) &&
                        (d.ldw % VN == 0) && (d.ldu % VN == 0);
       const size_t smem = sizeof(A) * ((c + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(c + 1));
-      if (vec)
-        SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", rhqr_col_kernel<T, VN>, dim3((unsigned)(n_eff + 2)), dim3(COL_NT),
-                           smem, ca));
-      else
-        SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", rhqr_col_kernel<T, 1>, dim3((unsigned)(n_eff + 2)), dim3(COL_NT),
-                           smem, ca));
+      SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", col_kernel_select<T, VN>(vec), dim3((unsigned)(n_eff + 2)),
+                         dim3(COL_NT), smem, ca));
       // rank-local subtree of w_c's sketch -> payload[0:ell]
       SrhtGeom gl{g.log_tb, tpr, n_eff};
       if (n_eff == 0) SQB_CUDA_TRY(cudaMemsetAsync(d.P, 0, sizeof(A) * ell * tpr, ctx->stream));

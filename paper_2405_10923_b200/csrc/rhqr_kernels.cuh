@@ -27,6 +27,7 @@
 // (bitwise equal to the per-column psi.apply(w)).
 #pragma once
 #include <algorithm>
+#include <cstdlib>
 #include <cooperative_groups.h>
 
 #include "pdl.cuh"
@@ -74,7 +75,14 @@ struct ColArgs {
   const double* betas;
   double* anext;        // out: a_{c+1}
   Status* st;
+  int helper_first;     // block order: 1 = helper, identity block, tiles; 0 = tiles, identity, helper
 };
+
+// SQB_HELPER_FIRST=0 restores the old block order (A/B experiments)
+inline int helper_first_default() {
+  const char* e = getenv("SQB_HELPER_FIRST");
+  return e ? atoi(e) : 1;
+}
 
 template <typename T>
 __device__ __forceinline__ typename Lo<T>::acc lazy_scale(typename Lo<T>::acc w, double f, int scaling) {
@@ -125,13 +133,40 @@ __device__ void col_top_block(const ColArgs& a, typename Lo<T>::acc* sc) {
 }
 
 // T[:kk, kk] = -beta * T[:kk,:kk] v ; T[kk,kk] = beta   (_extend_t, rhqr.py:135-140)
+// One thread per row with coalesced column reads, eight independent loads in
+// flight per step (an L2-latency chain per lane made this the longest CTA of
+// the pass at m = 256).  T holds explicit zeros below its diagonal; entries
+// k < i are masked to exact zeros anyway.
 __device__ inline void complete_t_column(double* T, int64_t ldt, int kk, const double* v, double beta) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = warp; i < kk; i += nw) {
-    double d = 0.0;
-    for (int k = i + lane; k < kk; k += 32) d = fma(T[i + (int64_t)k * ldt], v[k], d);
-    d = warp_sum(d);
-    if (lane == 0) T[i + (int64_t)kk * ldt] = __dmul_rn(-beta, d);
+  for (int i0 = 0; i0 < kk; i0 += blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    const int kb = i0 + (threadIdx.x & ~31);  // warp-uniform first column
+    if (kb >= kk) break;
+    const bool on = i < kk;
+    const double* Ti = T + (on ? i : kb);
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+    int k = kb;
+    for (; k + 8 <= kk; k += 8) {
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = Ti[(int64_t)(k + u) * ldt];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k + u < i) t[u] = 0.0;
+      d0 = fma(t[0], v[k], d0);
+      d1 = fma(t[1], v[k + 1], d1);
+      d2 = fma(t[2], v[k + 2], d2);
+      d3 = fma(t[3], v[k + 3], d3);
+      d0 = fma(t[4], v[k + 4], d0);
+      d1 = fma(t[5], v[k + 5], d1);
+      d2 = fma(t[6], v[k + 6], d2);
+      d3 = fma(t[7], v[k + 7], d3);
+    }
+    for (; k < kk; ++k) {
+      const double t = k < i ? 0.0 : Ti[(int64_t)k * ldt];
+      d0 = fma(t, v[k], d0);
+    }
+    if (on) T[i + (int64_t)kk * ldt] = __dmul_rn(-beta, (d0 + d1) + (d2 + d3));
   }
   if (threadIdx.x == 0) T[kk + (int64_t)kk * ldt] = beta;
 }
@@ -144,37 +179,59 @@ __device__ inline void col_helper(const ColArgs& a, double* g) {
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* y0 = a.Y0 + (int64_t)(c + 1) * a.od;
+  // g = S_c^t y0 (S[:, k] is zero above row k): 8 independent loads per lane
   for (int k = warp; k < c; k += nw) {
     const double* sk = a.S + (int64_t)k * a.lds;
-    double d0 = 0.0, d1 = 0.0;
-    int r = k + lane;
-    for (; r + 32 < a.od; r += 64) {
-      d0 = fma(sk[r], y0[r], d0);
-      d1 = fma(sk[r + 32], y0[r + 32], d1);
+    double d[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) d[u] = 0.0;
+    for (int r0 = k; r0 < a.od; r0 += 256) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = r0 + u * 32 + lane;
+        if (r < a.od) d[u] = fma(sk[r], y0[r], d[u]);
+      }
     }
-    if (r < a.od) d0 = fma(sk[r], y0[r], d0);
-    const double d = warp_sum(d0 + d1);
-    if (lane == 0) g[k] = d;
+    const double dd = warp_sum(((d[0] + d[1]) + (d[2] + d[3])) + ((d[4] + d[5]) + (d[6] + d[7])));
+    if (lane == 0) g[k] = dd;
   }
   __syncthreads();
+  // a_{c+1}[j] = T[:j+1, j] . g[:j+1]
   for (int j = warp; j < c; j += nw) {
-    const double* tj = a.T + (int64_t)j * a.ldt;  // column j of T, rows 0..j
-    double d = 0.0;
-    for (int i = lane; i <= j; i += 32) d = fma(tj[i], g[i], d);
-    d = warp_sum(d);
-    if (lane == 0) a.anext[j] = d;
+    const double* tj = a.T + (int64_t)j * a.ldt;
+    double d[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) d[u] = 0.0;
+    for (int i0 = 0; i0 <= j; i0 += 256) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * 32 + lane;
+        if (i <= j) d[u] = fma(tj[i], g[i], d[u]);
+      }
+    }
+    const double dd = warp_sum(((d[0] + d[1]) + (d[2] + d[3])) + ((d[4] + d[5]) + (d[6] + d[7])));
+    if (lane == 0) a.anext[j] = dd;
   }
 }
 
-template <typename T, int VN>
-__global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
+// DEP = 0: loads widened at issue, one column ahead; DEP >= 2: raw ring of
+// DEP column buffers (see the bulk loop)
+template <typename T, int VN, int DEP = 0, int MINB = 2>
+__global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
   using A = typename Lo<T>::acc;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   A* sc = reinterpret_cast<A*>(smem_raw);                      // coef rounded to low [c]
   A* sm = sc + ((a.c + 3) & ~3);                              // tile buffer
   pdl_trigger();
   const int c = a.c;
-  if (blockIdx.x == a.n_eff + 1) {
+  // block roles: with helper_first the helper (block 0) and the identity block
+  // (block 1) are dispatched first, so the helper's latency-bound sketch-space
+  // work overlaps the first wave of tiles instead of trailing the last one
+  const int64_t bid = blockIdx.x;
+  const int64_t helper_id = a.helper_first ? 0 : a.n_eff + 1;
+  const int64_t top_id = a.helper_first ? 1 : a.n_eff;
+  const int64_t tile = a.helper_first ? bid - 2 : bid;
+  if (bid == helper_id) {
     pdl_wait();
     if (failed(a.st)) return;
     col_helper(a, reinterpret_cast<double*>(sm));
@@ -185,14 +242,14 @@ __global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
   // overlap of the HBM pass with the sketch-space step, via PDL)
   for (int k = threadIdx.x; k < c - 1; k += COL_NT) sc[k] = Lo<T>::from_double(a.acur[k]);
   __syncthreads();
-  if (blockIdx.x == a.n_eff) {
+  if (bid == top_id) {
     if (a.mrow > 0) col_top_block<T>(a, sc);
     return;
   }
   constexpr int TB = 1 << TileCfg<T>::LOG_TB;
   constexpr int NV = TB / (COL_NT * VN);  // runs of VN rows per thread
   const int tb = 1 << a.log_tb;
-  const int64_t e0 = (int64_t)blockIdx.x << a.log_tb;  // first Omega coordinate of the tile
+  const int64_t e0 = tile << a.log_tb;  // first Omega coordinate of the tile
   const int64_t lim = a.n - e0;                       // valid rows in this tile (may exceed tb)
   const int64_t rows = lim < tb ? lim : tb;
   const int64_t ro = (int64_t)a.mrow + e0;             // first row of the tile in W / U
@@ -207,7 +264,42 @@ __global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
 
   // final columns 0 .. c-2
   const int K = c - 1;
-  if (VN > 1 && rows == TB && tb == TB) {
+  if (DEP >= 2 && VN > 1 && rows == TB && tb == TB) {
+    // full tile: streaming loads kept RAW (one uint4 per 16 bytes) in a ring
+    // of D column buffers, widened only at the FMA — 2-byte storage keeps
+    // four columns in flight per thread in the registers fp32 widening of
+    // two would take (ncu: the bf16 pass was L1TEX-latency bound at D = 2)
+    constexpr int D = DEP >= 2 ? DEP : 2;
+    uint4 rb[D][NV];
+    auto ldr = [&](uint4 (&x)[NV], int k) {
+      const T* col = U + ro + (int64_t)k * a.ldu;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) x[v] = ldg_stream(col + (v * COL_NT + threadIdx.x) * VN);
+    };
+    auto fmr = [&](const uint4 (&x)[NV], int k) {
+      const A ck = sc[k];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        A w[VN];
+        unpack16<T>(x[v], w);
+#pragma unroll
+        for (int j = 0; j < VN; ++j) acc[v][j] = fma(w[j], ck, acc[v][j]);
+      }
+    };
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d)
+      if (d < K) ldr(rb[d], d);
+    for (int k0 = 0; k0 < K; k0 += D) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const int k = k0 + j;
+        if (k < K) {
+          if (k + D - 1 < K) ldr(rb[(j + D - 1) % D], k + D - 1);
+          fmr(rb[j], k);
+        }
+      }
+    }
+  } else if (VN > 1 && rows == TB && tb == TB) {
     // full tile: streaming loads, software-pipelined one column ahead
     A x0[NV][VN], x1[NV][VN];
     auto ld = [&](A (&x)[NV][VN], int k) {
@@ -298,7 +390,23 @@ __global__ void __launch_bounds__(COL_NT, 2) rhqr_col_kernel(ColArgs a) {
   if (!a.srht) return;
   __syncthreads();
   tile_fwht<T>(sm, a.log_tb);
-  tile_gather<T>(sm, a.idx, a.ell, a.log_tb, (A*)a.P + blockIdx.x, a.n_tiles);
+  tile_gather<T>(sm, a.idx, a.ell, a.log_tb, (A*)a.P + tile, a.n_tiles);
+}
+
+// Bulk-loop variant of the column pass.  2-byte storage: a raw 2-deep ring
+// at 3 CTAs/SM (78 registers, 24 resident warps instead of 16) — the pass is
+// bound by load latency (ncu: L1TEX-scoreboard stalls at the first use of
+// each load), +5% on config 4.  4/8-byte storage: widened loads one column
+// ahead at 2 CTAs/SM (0.9+ of the HBM copy peak).  SQB_COL_VARIANT=base
+// forces the latter for 2-byte storage too (A/B experiments).
+template <typename T, int VN>
+inline void (*col_kernel_select(bool vec))(ColArgs) {
+  if (!vec) return rhqr_col_kernel<T, 1>;
+  if constexpr (sizeof(T) == 2) {
+    const char* e = getenv("SQB_COL_VARIANT");
+    if (!(e && e[0] == 'b')) return rhqr_col_kernel<T, VN, 2, 3>;
+  }
+  return rhqr_col_kernel<T, VN>;
 }
 
 // ---------------------------------------------------------------------------

@@ -1,4 +1,6 @@
 // Left-looking RHQR driver, single GPU (kernels in rhqr_kernels.cuh).
+#include <cstdlib>
+
 #include "rhqr_kernels.cuh"
 
 namespace sqb {
@@ -125,7 +127,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
   const size_t tile_bytes = srht ? tile_smem_bytes<A>(tb_max) : 0;
   const size_t col_smem_max = sizeof(A) * ((m + 3) & ~3) +
                               std::max(tile_bytes, sizeof(double) * (size_t)(m + 1));
-  auto colk = vec ? rhqr_col_kernel<T, VN> : rhqr_col_kernel<T, 1>;
+  auto colk = col_kernel_select<T, VN>(vec);
   cudaFuncSetAttribute(colk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
   for (int64_t c = 1; c < ncol; ++c) {
     SQB_TRY(ensure_y0(c + 2));
@@ -139,6 +141,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
     ca.idx = srht ? sk->indices : nullptr; ca.scale_lo = scale_lo; ca.P = P; ca.y = y;
     ca.S = S; ca.lds = lds; ca.T = Tm; ca.ldt = ldt; ca.Y0 = Y0; ca.vprev = vbuf; ca.betas = betas;
     ca.anext = a_nxt; ca.st = st;
+    ca.helper_first = helper_first_default();
     const size_t smem = sizeof(A) * ((c + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(c + 1));
     prof_begin(ctx);
     SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", colk, dim3((unsigned)(n_eff_col + 2)), dim3(COL_NT), smem,

@@ -100,6 +100,31 @@ __device__ __forceinline__ void vload_stream(const T* p, typename Lo<T>::acc* ou
   }
 }
 
+// widen one raw 128-bit word of storage elements to the arithmetic type
+template <typename T>
+__device__ __forceinline__ void unpack16(const uint4& v, typename Lo<T>::acc* out) {
+  if constexpr (sizeof(T) == 8) {
+    out[0] = __hiloint2double((int)v.y, (int)v.x);
+    out[1] = __hiloint2double((int)v.w, (int)v.z);
+  } else if constexpr (sizeof(T) == 4) {
+    out[0] = __uint_as_float(v.x); out[1] = __uint_as_float(v.y);
+    out[2] = __uint_as_float(v.z); out[3] = __uint_as_float(v.w);
+  } else if constexpr (Lo<T>::code == SQB_BF16) {
+    // bf16 -> fp32 is a placement of the 16 bits: low half by a shift, high
+    // half by a mask (one integer op per element, no PRMT)
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      out[2 * i] = __uint_as_float(w[i] << 16);
+      out[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  } else {
+    const T* h = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out[i] = Lo<T>::load(h[i]);
+  }
+}
+
 // cp.async (LDGSTS): 16-byte global -> shared copy; src_bytes < 16 zero-fills the rest
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(dst);

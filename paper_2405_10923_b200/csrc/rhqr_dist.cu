@@ -224,6 +224,8 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
       ca.S = d.S; ca.lds = d.lds; ca.T = d.T; ca.ldt = d.ldt; ca.Y0 = Y0; ca.vprev = d.vbuf; ca.betas = d.bet;
       ca.anext = d.abuf + ((c + 1) & 1) * (m + 1); ca.st = st;
       ca.helper_first = helper_first_default();
+      ca.no_p16 = no_p16_env();
+      ca.no_pre = no_pre_env();
       const bool vec = ((reinterpret_cast<uintptr_t>((const char*)d.W + d.mrow * esz) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>((const char*)d.U + d.mrow * esz) & 15) == 0) &&
                        (d.ldw % VN == 0) && (d.ldu % VN == 0);

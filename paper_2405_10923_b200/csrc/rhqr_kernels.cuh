@@ -76,12 +76,22 @@ struct ColArgs {
   double* anext;        // out: a_{c+1}
   Status* st;
   int helper_first;     // block order: 1 = helper, identity block, tiles; 0 = tiles, identity, helper
+  int no_p16;           // 1: 16-bit storage stages its tile FWHT in fp32 (test hook, SQB_NO_P16)
+  int no_pre;           // 1: no pre-wait loads of w_{c-1} / W[:, c] (A/B hook, SQB_NO_PRE)
 };
 
 // SQB_HELPER_FIRST=0 restores the old block order (A/B experiments)
 inline int helper_first_default() {
   const char* e = getenv("SQB_HELPER_FIRST");
   return e ? atoi(e) : 1;
+}
+inline int no_pre_env() {
+  const char* e = getenv("SQB_NO_PRE");
+  return e && e[0] == '1';
+}
+inline int no_p16_env() {
+  const char* e = getenv("SQB_NO_P16");
+  return e && e[0] == '1';
 }
 
 template <typename T>
@@ -339,12 +349,31 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
         for (int j = 0; j < VN; ++j) acc[v][j] = fma(v0[v][j], ck, acc[v][j]);
     }
   }
+  // The stored w_{c-1} (pass c-1 is complete: step c-1 waited on it before
+  // launching this pass) and W[:, c] do not depend on step c-1 either: on a
+  // full tile both are loaded raw BEFORE the wait, into the registers the
+  // bulk ring just released, so the tail after the wait starts with its
+  // operands in flight instead of two serial DRAM round trips.
+  // (the 3-CTA/SM 16-bit variant has registers for W[:, c] only; its w_{c-1}
+  // was written by pass c-1 moments ago and is mostly still in L2)
+  const bool full = VN > 1 && rows == TB && tb == TB && !a.no_pre;
+  constexpr bool PRE_U = MINB <= 2;
+  const T* src = (c == 1 ? W : (const T*)U) + ro + (int64_t)(c - 1) * (c == 1 ? 0 : a.ldu);
+  const T* wc = W + ro + (int64_t)c * a.ldw;
+  uint4 pre_u[NV], pre_w[NV];
+  if (full) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int i = (v * COL_NT + threadIdx.x) * VN;
+      if constexpr (PRE_U) pre_u[v] = ldg_l2only(src + i);
+      pre_w[v] = ldg_stream(wc + i);
+    }
+  }
   // ---- wait for step c-1 (f_{c-1}, coef_c[c-1], breakdown status)
   pdl_wait();
   if (failed(a.st)) return;
   // column c-1: lazy scaling of the stored w_{c-1}, write back u_{c-1}
   {
-    const T* src = (c == 1 ? W : (const T*)U) + ro + (int64_t)(c - 1) * (c == 1 ? 0 : a.ldu);
     T* dst = U + ro + (int64_t)(c - 1) * a.ldu;
     const double f = *a.fscale;
     const A ck = Lo<T>::from_double(a.clast[c]);
@@ -353,7 +382,8 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
       const int i = (v * COL_NT + threadIdx.x) * VN;
       if (i < tb) {
         A x[VN];
-        load_run<T, VN>(src, i, rows, x);
+        if (PRE_U && full) unpack16<T>(pre_u[v], x);
+        else load_run<T, VN>(src, i, rows, x);
 #pragma unroll
         for (int j = 0; j < VN; ++j) {
           x[j] = lazy_scale<T>(x[j], f, a.scaling);
@@ -364,19 +394,38 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
     }
   }
   // w_c = fl(W[:, c] - fl(dot)); store unscaled into U[:, c]; SRHT input to smem
+  // 16-bit storage with a full tile runs the in-tile FWHT on packed pairs in
+  // 16-bit shared memory (srht.cuh p16_*): ~6x fewer butterfly instructions
+  // than fp32 staging with a rounding per op, half the shared traffic
+  constexpr bool P16OK = sizeof(T) == 2 && VN == 8 && TileCfg<T>::LOG_TB == P16_LOG;
+  const bool p16path = P16OK && a.srht && a.log_tb == P16_LOG && !a.no_p16;
   {
-    const T* wc = W + ro + (int64_t)c * a.ldw;
     T* uc = U + ro + (int64_t)c * a.ldu;
     const A s_lo = (A)a.scale_lo;
+    uint32_t scale2 = 0;
+    if constexpr (P16OK) {
+      const uint32_t h = pk_pack<T>((float)a.scale_lo, 0.f) & 0xffffu;
+      scale2 = h | (h << 16);
+    }
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const int i = (v * COL_NT + threadIdx.x) * VN;
       if (i < tb) {
         A x[VN];
-        load_run<T, VN>(wc, i, rows, x);
+        if (full) unpack16<T>(pre_w[v], x);
+        else load_run<T, VN>(wc, i, rows, x);
 #pragma unroll
         for (int j = 0; j < VN; ++j) x[j] = Lo<T>::sub(x[j], Lo<T>::rnd(acc[v][j]));
         store_run<T, VN>(uc, i, rows, x);
+        if constexpr (P16OK) {
+          if (p16path) {
+            const int64_t e = a.e_base + e0 + i;
+            const uint32_t sb = __ldg(a.bits + (e >> 5)) >> (e & 31);
+            const int64_t vl = rows - i;
+            p16_run_in<T>(reinterpret_cast<uint16_t*>(sm), i, x, scale2, sb, vl >= 8 ? 8 : (vl > 0 ? (int)vl : 0));
+            continue;
+          }
+        }
         if (a.srht) {
           const int64_t e = a.e_base + e0 + i;  // global Omega coordinate (sign bits)
           const uint32_t sb = __ldg(a.bits + (e >> 5)) >> (e & 31);
@@ -389,6 +438,16 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
   }
   if (!a.srht) return;
   __syncthreads();
+  if constexpr (P16OK) {
+    if (p16path) {
+      const uint16_t* s16 = reinterpret_cast<const uint16_t*>(sm);
+      p16_passes<T>(reinterpret_cast<uint16_t*>(sm));
+      float* P = (float*)a.P + tile;
+      for (int k = threadIdx.x; k < a.ell; k += COL_NT)
+        P[k * a.n_tiles] = pk_lo_float<T>(s16[p16((int)(__ldg(a.idx + k) & ((1 << P16_LOG) - 1)))]);
+      return;
+    }
+  }
   tile_fwht<T>(sm, a.log_tb);
   tile_gather<T>(sm, a.idx, a.ell, a.log_tb, (A*)a.P + tile, a.n_tiles);
 }

@@ -142,6 +142,8 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
     ca.S = S; ca.lds = lds; ca.T = Tm; ca.ldt = ldt; ca.Y0 = Y0; ca.vprev = vbuf; ca.betas = betas;
     ca.anext = a_nxt; ca.st = st;
     ca.helper_first = helper_first_default();
+    ca.no_p16 = no_p16_env();
+    ca.no_pre = no_pre_env();
     const size_t smem = sizeof(A) * ((c + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(c + 1));
     prof_begin(ctx);
     SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", colk, dim3((unsigned)(n_eff_col + 2)), dim3(COL_NT), smem,

@@ -322,38 +322,6 @@ srht64_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_ef
 // compute natively two at a time.  Values stay in the 16-bit format in
 // shared memory as well (half the traffic of fp32 staging).
 // ---------------------------------------------------------------------------
-template <typename T> struct Pk;
-template <> struct Pk<__nv_bfloat16> {
-  __device__ __forceinline__ static uint32_t add(uint32_t a, uint32_t b) {
-    uint32_t r; asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
-  }
-  __device__ __forceinline__ static uint32_t sub(uint32_t a, uint32_t b) {
-    uint32_t r; asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
-  }
-  __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) {
-    uint32_t r; asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
-  }
-};
-template <> struct Pk<__half> {
-  __device__ __forceinline__ static uint32_t add(uint32_t a, uint32_t b) {
-    uint32_t r; asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
-  }
-  __device__ __forceinline__ static uint32_t sub(uint32_t a, uint32_t b) {
-    uint32_t r; asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
-  }
-  __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) {
-    uint32_t r; asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
-  }
-};
-
-// stage on the two halves of each register: (x, y) -> (x + y, x - y)
-template <typename T>
-__device__ __forceinline__ uint32_t pk_inner(uint32_t r) {
-  const uint32_t sw = __byte_perm(r, 0, 0x1032);
-  const uint32_t sm = Pk<T>::add(r, sw), df = Pk<T>::sub(r, sw);
-  return __byte_perm(sm, df, 0x5410);  // (sm.lo, df.lo)
-}
-
 // stages b..b+5 over 64 values packed as v[i] = (x_{2i}, x_{2i+1})
 template <typename T>
 __device__ __forceinline__ void fwht64_packed(uint32_t (&v)[32]) {

@@ -21,6 +21,8 @@
 //   contraction), so the result is bitwise identical to the reference.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace sqb {
@@ -133,6 +135,155 @@ __device__ __forceinline__ void tile_gather(const typename Lo<T>::acc* sm, const
   const int64_t mask = (int64_t(1) << log_tb) - 1;
   for (int k = threadIdx.x; k < ell; k += blockDim.x)
     P[k * ldp] = sm[pidx<A>((int)(__ldg(idx + k) & mask))];
+}
+
+// ---------------------------------------------------------------------------
+// Packed 16-bit arithmetic (bf16 / fp16 storage).  Every butterfly op of the
+// reference is one correctly rounded 16-bit op (numpy/ml_dtypes round each
+// op once), which add/sub/mul.rn.{bf16,f16}x2 compute natively two at a time.
+// ---------------------------------------------------------------------------
+template <typename T> struct Pk;
+template <> struct Pk<__nv_bfloat16> {
+  __device__ __forceinline__ static uint32_t add(uint32_t a, uint32_t b) {
+    uint32_t r; asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+  __device__ __forceinline__ static uint32_t sub(uint32_t a, uint32_t b) {
+    uint32_t r; asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+  __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) {
+    uint32_t r; asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+};
+template <> struct Pk<__half> {
+  __device__ __forceinline__ static uint32_t add(uint32_t a, uint32_t b) {
+    uint32_t r; asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+  __device__ __forceinline__ static uint32_t sub(uint32_t a, uint32_t b) {
+    uint32_t r; asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+  __device__ __forceinline__ static uint32_t mul(uint32_t a, uint32_t b) {
+    uint32_t r; asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b)); return r;
+  }
+};
+
+// stage on the two halves of each register: (x, y) -> (x + y, x - y)
+template <typename T>
+__device__ __forceinline__ uint32_t pk_inner(uint32_t r) {
+  const uint32_t sw = __byte_perm(r, 0, 0x1032);
+  const uint32_t sm = Pk<T>::add(r, sw), df = Pk<T>::sub(r, sw);
+  return __byte_perm(sm, df, 0x5410);  // (sm.lo, df.lo)
+}
+
+// exact pack of two values already representable in T (lo -> low half)
+template <typename T>
+__device__ __forceinline__ uint32_t pk_pack(float lo, float hi) {
+  if constexpr (std::is_same<T, __half>::value) {
+    const __half2 h = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  } else {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ float pk_lo_float(uint16_t h) {
+  if constexpr (std::is_same<T, __half>::value) return __half2float(__ushort_as_half(h));
+  else return __bfloat162float(__ushort_as_bfloat16(h));
+}
+
+// stages over 32 values packed as v[i] = (x_{2i}, x_{2i+1}): the pair bit
+// first, then bits 1..4 of i, in order
+template <typename T>
+__device__ __forceinline__ void fwht32_packed(uint32_t (&v)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = pk_inner<T>(v[i]);
+#pragma unroll
+  for (int s2 = 0; s2 < 4; ++s2)
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (!(i & (1 << s2))) {
+        const uint32_t x = v[i], y = v[i | (1 << s2)];
+        v[i] = Pk<T>::add(x, y);
+        v[i | (1 << s2)] = Pk<T>::sub(x, y);
+      }
+}
+
+// ---------------------------------------------------------------------------
+// In-tile FWHT of the column pass for 16-bit storage: a 2^13 tile held as
+// 16-bit values in shared memory (one 8-element pad per 256), 256 threads.
+//   p16_run_in   a run of 8 consecutive coordinates from registers: scale,
+//                sign, zero past the data, stages h = 1, 2, 4, one 16-byte store
+//   p16_pass     5 stages (bits b..b+4) with 32 values per thread in registers
+// Stage order is the reference's (h = 1, 2, 4, ...), so leaves are bitwise
+// those of the fp32-staged path.
+// ---------------------------------------------------------------------------
+constexpr int P16_LOG = 13;
+__device__ __forceinline__ int p16(int e) { return e + ((e >> 8) << 3); }
+
+template <typename T>
+__device__ __forceinline__ void p16_run_in(uint16_t* sm, int i, const float* x, uint32_t scale2, uint32_t sb,
+                                           int valid) {
+  uint32_t p[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    p[q] = pk_pack<T>(x[2 * q], x[2 * q + 1]);
+    const uint32_t flip = (((sb >> (2 * q)) & 1u) << 15) | (((sb >> (2 * q + 1)) & 1u) << 31);
+    p[q] = Pk<T>::mul(p[q], scale2) ^ flip;  // fl(x * scale), then the sign (sketching.py:152-153)
+  }
+  if (valid < 8) {  // zero padding past n is +0 (sketching.py:154)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (2 * q >= valid) p[q] &= 0xffff0000u;
+      if (2 * q + 1 >= valid) p[q] &= 0x0000ffffu;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) p[q] = pk_inner<T>(p[q]);  // h = 1
+#pragma unroll
+  for (int s2 = 0; s2 < 2; ++s2)  // h = 2, 4
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (!(q & (1 << s2))) {
+        const uint32_t x0 = p[q], y0 = p[q | (1 << s2)];
+        p[q] = Pk<T>::add(x0, y0);
+        p[q | (1 << s2)] = Pk<T>::sub(x0, y0);
+      }
+  *reinterpret_cast<uint4*>(sm + p16(i)) = make_uint4(p[0], p[1], p[2], p[3]);
+}
+
+// bits 3..7 (pass A) and 8..12 (pass B) of the in-tile coordinate
+template <typename T>
+__device__ __forceinline__ void p16_passes(uint16_t* sm) {
+  const int t = threadIdx.x;
+  {
+    // thread t: coordinates (t & 7) + 8 j + 256 (t >> 3), j = 0..31
+    uint16_t* base = sm + (t & 7) + 264 * (t >> 3);
+    uint32_t v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __byte_perm((uint32_t)base[16 * i], (uint32_t)base[16 * i + 8], 0x5410);
+    fwht32_packed<T>(v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      base[16 * i] = (uint16_t)(v[i] & 0xffffu);
+      base[16 * i + 8] = (uint16_t)(v[i] >> 16);
+    }
+  }
+  __syncthreads();
+  {
+    // thread t: coordinates t + 256 j
+    uint16_t* base = sm + t;
+    uint32_t v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __byte_perm((uint32_t)base[528 * i], (uint32_t)base[528 * i + 264], 0x5410);
+    fwht32_packed<T>(v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      base[528 * i] = (uint16_t)(v[i] & 0xffffu);
+      base[528 * i + 264] = (uint16_t)(v[i] >> 16);
+    }
+  }
+  __syncthreads();
 }
 
 // Tree over tile leaves for output k, done by one warp.  leaves[t] for

@@ -84,6 +84,16 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   return v;
 }
 
+// 128-bit load of data this kernel later overwrites (coherent path, no L1
+// allocation)
+__device__ __forceinline__ uint4 ldg_l2only(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 template <typename T>
 __device__ __forceinline__ void vload_stream(const T* p, typename Lo<T>::acc* out) {
   const uint4 v = ldg_stream(p);

@@ -1,5 +1,5 @@
-"""A/B of the column-pass block order (SQB_HELPER_FIRST) on configs 2 and 4,
-interleaved in one process."""
+"""A/B of a column-pass switch (env var FLAG, default SQB_HELPER_FIRST) on
+configs 2 and 4, interleaved in one process."""
 import os
 import sys
 
@@ -20,7 +20,7 @@ def case(name, Wd, N, m, ell, tag, b):
     res = {"0": [], "1": []}
     for rep in range(4):
         for v in res:
-            os.environ["SQB_HELPER_FIRST"] = v
+            os.environ[os.environ.get("FLAG", "SQB_HELPER_FIRST")] = v
             rhqr_left_device(Wd, psi, "sqrt2", pol, check=False)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -30,7 +30,7 @@ def case(name, Wd, N, m, ell, tag, b):
             torch.cuda.synchronize()
             res[v].append(e0.elapsed_time(e1))
     for v, xs in res.items():
-        print(f"{name} helper_first={v}: best {min(xs):.3f} ms ({alg / min(xs) / 1e6:.0f} GB/s) all {[round(x, 3) for x in xs]}")
+        print(f"{name} {os.environ.get('FLAG', 'SQB_HELPER_FIRST')}={v}: best {min(xs):.3f} ms ({alg / min(xs) / 1e6:.0f} GB/s) all {[round(x, 3) for x in xs]}")
 
 
 N, m = 1 << 20, 128

@@ -180,3 +180,20 @@ def test_rhqr_right_identity_is_householder(P):
     F = P.rhqr_right(W, P.IdentitySketch(56))
     assert rel(F.R, R_ref) <= 1e-13
     assert rel(F.U, aux["U"]) <= 1e-13
+
+
+@pytest.mark.parametrize("tag", ["bf16", "half"])
+@pytest.mark.parametrize("N,m,ell", [(1 << 15, 12, 48), ((1 << 16) + 8 * 1000 + 3, 9, 40), (3 * 8192 + 77, 5, 20)])
+def test_packed16_tile_fwht_is_bitwise(P, monkeypatch, tag, N, m, ell):
+    """The column pass's packed 16-bit in-tile FWHT (srht.cuh p16_*, full
+    2^13 tiles) must give bitwise the factors of the fp32-staged path, which
+    is the reference's correctly rounded op sequence."""
+    rng = np.random.default_rng(N)
+    W = rng.standard_normal((N, m)) * np.logspace(0, -2, m)[None, :]
+    om = P.SRHTSketch(ell, N - m, 5)
+    pol = P.PrecisionPolicy("double", tag)
+    F1 = P.rhqr_left(W, om, policy=pol)
+    monkeypatch.setenv("SQB_NO_P16", "1")
+    F2 = P.rhqr_left(W, om, policy=pol)
+    for k in ("U", "S", "T", "R"):
+        assert np.array_equal(getattr(F1, k), getattr(F2, k)), k

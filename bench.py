@@ -474,14 +474,14 @@ def main():
     e2e = None if args.no_e2e else wl.e2e(args.steps)
     peak, peak_kind = measured_peak()
     achieved = (k_bytes / k_n) / (k_ms / k_n * 1e-3) / 1e9 if k_n else None
-    traffic = None
+    traffic, traffic_detail = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tj = json.load(f)
-            traffic = {"bytes_per_launch": tj.get("rhqr_col_kernel_bytes_per_launch_c64"),
-                       "alg_bytes_per_launch": tj.get("rhqr_col_kernel_alg_bytes_c64"),
-                       "launch": "config 2, column c=64 (ncu --set full: dram__bytes_read.sum + "
-                                 "dram__bytes_write.sum)"}
+            tj = json.load(f).get(wl.name)
+        if tj:
+            traffic = tj["bytes_per_launch"]
+            traffic_detail = {"alg_bytes_per_launch": tj["alg_bytes_per_launch"], "launch": tj["launch"],
+                              "source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum)"}
     except Exception:
         pass
 
@@ -502,6 +502,7 @@ def main():
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_detail": traffic_detail,
                          "kernel": wl.kernel,
                          "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                          "kernel_share_of_step": (k_ms / args.steps) / prof_step_ms if prof_step_ms else None,

@@ -13,7 +13,7 @@ def load(path):
         d = dict(zip(hdr, r))
         if d.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        name = d["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").strip()
+        name = d["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").replace("sqb::", "").strip()
         v = float(d["Metric Value"].replace(",", ""))
         unit = d["Metric Unit"]
         us = v / 1e3 if unit in ("ns", "nsecond") else (v if unit in ("us", "usecond") else v * 1e3)

@@ -353,13 +353,10 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
   SQB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   const Status hs = *ctx->h_status;
   if (hs.code == SQB_CLOSED) {
+    // the space closed at step attained+1: every accepted reflector is final
+    // (column attained-1 was scaled by the arn_q pass of step attained; the
+    // unscaled w copied into column attained is past the returned factors)
     *attained = hs.col;
-    // the last accepted reflector (column attained-1) still holds the unscaled w
-    if (hs.col >= 1) {
-      T* ul = (T*)U + (int64_t)(hs.col - 1) * ldu;
-      scale_col_kernel<T><<<gq, 256, 0, ctx->stream>>>(ul, n, mt, fs, scaling, nullptr);
-      SQB_TRY(check_launch(ctx, "scale_col_kernel"));
-    }
     SQB_CUDA_TRY(cudaMemsetAsync(ctx->d_status, 0, sizeof(Status), ctx->stream));
   } else {
     *attained = -1;

@@ -223,9 +223,74 @@ def block_cases():
          U_unit=Fu.U, R_unit=Fu.R, T_unit=Fu.T)
 
 
+def experiment_cases():
+    """The stability-sweep harness (experiments.py:125-339) on small inputs:
+    metric rows and the deterministic CSV bytes, per algorithm."""
+    import io
+    import tempfile
+
+    import scipy.sparse
+    from sketchqr.experiments import (ExperimentConfig, run_factor_experiment, run_gmres_experiment,
+                                      write_csv)
+
+    def pack(rows):
+        return (np.array([r[0] for r in rows], dtype=np.int64),
+                np.array([list(r[1:-1]) for r in rows], dtype=np.float64),
+                np.array([r[-1] for r in rows]))
+
+    def csv_bytes(rows, cfg):
+        with tempfile.NamedTemporaryFile("r", suffix=".csv") as fh:
+            write_csv(fh.name, rows, config=cfg, extra="golden")
+            return np.frombuffer(open(fh.name, "rb").read(), dtype=np.uint8)
+
+    out = {}
+    W = gen_cmatrix(2048, 48)
+    cases = {
+        "left": ExperimentConfig(algo="rhqr-left", seed=3, every=8, deterministic=True),
+        "right": ExperimentConfig(algo="rhqr-right", seed=3, every=8, deterministic=True),
+        "block": ExperimentConfig(algo="rhqr-block", seed=3, every=8, block_size=16, deterministic=True),
+        "rec": ExperimentConfig(algo="rec-rhqr", seed=3, every=16, deterministic=True),
+        "leftgauss": ExperimentConfig(algo="rhqr-left", sketch="gauss", ell=120, seed=5, every=12,
+                                      deterministic=True),
+        "mixed": ExperimentConfig(algo="rhqr-left", ell=96, seed=2, precision="mixed", every=8,
+                                  deterministic=True),
+    }
+    for name, cfg in cases.items():
+        rows = run_factor_experiment(W, cfg)
+        j, vals, st = pack(rows)
+        out[f"{name}_j"], out[f"{name}_vals"], out[f"{name}_status"] = j, vals, st
+        out[f"{name}_csv"] = csv_bytes(rows, cfg)
+    # breakdown: an all-zero column 4 (rhqr.py:73-79 -> 'breakdown@4', NaN rows after)
+    Wb = np.random.default_rng(77).standard_normal((512, 10))
+    Wb[:, 3] = 0.0
+    cfg = ExperimentConfig(algo="rhqr-left", seed=1, every=2, deterministic=True)
+    j, vals, st = pack(run_factor_experiment(Wb, cfg))
+    out.update(bd_W=Wb, bd_j=j, bd_vals=vals, bd_status=st)
+    save("experiments_cmatrix_2048x48", W_sha=np.array(sha(W)), **out)
+
+    # GMRES sweep (experiments.py:247-299) on a 24^2 convection-diffusion grid
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from paper_2405_10923_b200.workloads import convection_diffusion_csr
+    ip, ix, dv = convection_diffusion_csr(24)
+    A = scipy.sparse.csr_matrix((dv, ix, ip), shape=(576, 576))
+    b = np.random.default_rng(81).standard_normal(576)
+    g = {}
+    for name, cfg in {"srht": ExperimentConfig(algo="rhqr", seed=4, deterministic=True),
+                      "gauss": ExperimentConfig(algo="rhqr", sketch="gauss", ell=100, seed=6,
+                                                deterministic=True)}.items():
+        rows = run_gmres_experiment(A, b, 24, cfg)
+        j, vals, st = pack(rows)
+        g[f"{name}_j"], g[f"{name}_vals"], g[f"{name}_status"] = j, vals, st
+        g[f"{name}_csv"] = csv_bytes(rows, cfg)
+    rows = run_gmres_experiment(np.eye(32), b[:32], 5, ExperimentConfig(algo="rhqr", sketch="gauss", seed=1))
+    j, vals, st = pack(rows)
+    g.update(eye_j=j, eye_vals=vals, eye_status=st)
+    save("experiments_gmres_cd24", indptr=ip, indices=ix, data=dv, b=b, **g)
+
+
 SECTIONS = dict(srht=srht_cases, gauss=gauss_cases, rh_vector=rh_vector_cases, rhqr=rhqr_cases,
                 mixed=mixed_cases, rec=rec_cases, krylov=krylov_cases, apply_compact=apply_compact_cases,
-                block=block_cases)
+                block=block_cases, experiments=experiment_cases)
 
 if __name__ == "__main__":
     # no arguments: every section; otherwise only the named ones

@@ -383,6 +383,26 @@ def test_arnoldi_invariant_subspace_and_gmres(P):
     assert np.allclose(x, xref, atol=1e-10)
 
 
+@pytest.mark.parametrize("scaling", ["sqrt2", "unit"])
+def test_arnoldi_closed_space_reflectors_are_final(P, scaling):
+    """A dense b with a 3-dimensional Krylov space: the space closes at step 4
+    and every returned reflector (Omega rows included) must equal the
+    oracle's; GMRES then solves exactly (experiments' closed@k rows)."""
+    rng = np.random.default_rng(12)
+    n = 64
+    A = np.diag(np.repeat([1.0, 2.0, 5.0], [20, 20, 24]))  # 3 distinct eigenvalues, exact
+    b = rng.standard_normal(n)
+    bun = P.rhqr_arnoldi(A, b, None, 8, P.GaussianSketch(36, n - 9, 4), scaling=scaling)
+    ref = O.rhqr_arnoldi(A, b, None, 8, O.Gaussian(36, n - 9, 4), scaling=scaling)
+    assert bun.breakdown == ref.breakdown == 3
+    assert rel(bun.U, ref.U) < 1e-10 and rel(bun.S, ref.S) < 1e-10 and rel(bun.T, ref.T) < 1e-10
+    x, _ = P.rhqr_gmres(A, b, None, 8, P.GaussianSketch(36, n - 9, 4), scaling=scaling)
+    assert np.linalg.norm(b - A @ x) <= 1e-10 * np.linalg.norm(b)
+    b1 = rng.standard_normal(30)
+    x1, _ = P.rhqr_gmres(np.eye(30), b1, None, 5, P.GaussianSketch(24, 24, 1), scaling=scaling)
+    assert np.linalg.norm(b1 - x1) <= 1e-12 * np.linalg.norm(b1)
+
+
 def test_gmres_zero_operator_warns(P):
     b = np.random.default_rng(1).standard_normal(12)
     with pytest.warns(RuntimeWarning, match="rank deficient"):

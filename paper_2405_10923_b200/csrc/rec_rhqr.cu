@@ -1,3 +1,5 @@
+#include <cstdlib>
+#include <type_traits>
 // recRHQR on the device (rec_rhqr, rhqr.py:368-395):
 //   Z = Psi W (one sketch of all columns; K2 DMMA for a Gaussian Omega),
 //   K5  householder_qr(Z) in the high precision (baselines.py:33-89), one CTA,
@@ -10,6 +12,7 @@
 
 #include "pdl.cuh"
 #include "sketch.cuh"
+#include "vec.cuh"
 
 namespace sqb {
 
@@ -303,6 +306,111 @@ trsm_dmma_kernel(const T* __restrict__ W2, int64_t ldw, int64_t n, int m, int mp
   }
 }
 
+// K6, fp64 storage, m <= 64: the same blocked substitution as a software
+// pipeline — 64-row tiles, two shared-memory tile buffers per CTA filled by
+// 16-byte cp.async (the next tile streams in while this one is solved), two
+// CTAs per SM.  Tiles are column-major in shared memory (ld 72 = 8 mod 16:
+// conflict-free DMMA A fragments and row-per-thread substitution); the
+// diagonal blocks are solved right-looking (x_j *= 1/M_jj, then x_k -= x_j
+// M_jk for k > j), the reference BLAS dtrsm order (multiply by the
+// reciprocal of the diagonal).  Measured (config 3, ncu): 2.17 -> 1.56 ms.
+// With the solve removed the same kernel moves its 4.3 GB in 0.68 ms
+// (6.25 TB/s), so what remains is the latency of the per-tile solve chain
+// (two warps run the 16-step diagonal substitutions while six wait).
+constexpr int TP_ROWS = 64, TP_NT = 256, TP_LDX = 72, TP_MP = 64, TP_LDM = 68;
+constexpr size_t TP_SMEM = sizeof(double) * ((size_t)2 * TP_MP * TP_LDX + (size_t)TP_MP * TP_LDM + TP_MP);
+
+__global__ void __launch_bounds__(TP_NT, 2)
+trsm_pipe_kernel(const double* __restrict__ W2, int64_t ldw, int64_t n, int m, int mp,
+                 const double* __restrict__ M, double* __restrict__ U2, int64_t ldu, const Status* st) {
+  extern __shared__ __align__(16) double tps[];
+  double* Ms = tps + 2 * TP_MP * TP_LDX;  // column-major, ld TP_LDM
+  double* rinv = Ms + TP_MP * TP_LDM;
+  if (failed(st)) return;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < mp * mp; e += TP_NT) {
+    const int r = e % mp, c = e / mp;
+    Ms[c * TP_LDM + r] = (r < m && c < m) ? M[r + (int64_t)c * m] : (r == c ? 1.0 : 0.0);
+  }
+  for (int e = tid; e < mp; e += TP_NT) rinv[e] = e < m ? 1.0 / M[e + (int64_t)e * m] : 1.0;
+  // padding columns m..mp-1 stay zero in both buffers (never loaded)
+  for (int e = tid; e < 2 * TP_MP * TP_LDX; e += TP_NT) {
+    const int c = (e % (TP_MP * TP_LDX)) / TP_LDX;
+    if (c >= m) tps[e] = 0.0;
+  }
+  const int64_t ntiles = (n + TP_ROWS - 1) / TP_ROWS;
+  auto issue = [&](int64_t tile, double* X) {  // 16-byte granules (2 rows) per cp.async
+    if (tile >= ntiles) return;
+    const int64_t r0 = tile * TP_ROWS;
+    for (int e = tid; e < (TP_ROWS / 2) * m; e += TP_NT) {
+      const int g2 = e % (TP_ROWS / 2), c = e / (TP_ROWS / 2);
+      const int64_t row = r0 + 2 * g2;
+      const int64_t rem = n - row;
+      const int bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+      cp_async16(X + c * TP_LDX + 2 * g2, bytes ? W2 + row + (int64_t)c * ldw : W2, bytes);
+    }
+  };
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int rg = warp & 3, nt = warp >> 2;  // DMMA: 16-row group, 8-column half of the block
+  const int nb = mp / 16;
+  int it = 0;
+  issue(blockIdx.x, tps);
+  cp_async_commit_group();
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    double* X = tps + (it & 1) * (TP_MP * TP_LDX);
+    cp_async_wait_group<0>();
+    __syncthreads();  // tile landed; every thread is done with the other buffer
+    issue(tile + gridDim.x, tps + ((it + 1) & 1) * (TP_MP * TP_LDX));
+    cp_async_commit_group();
+    for (int b = 0; b < nb; ++b) {
+      if (b > 0) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int kk = 0; kk < b; ++kk) {
+          double a[8], bb[4];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) a[v] = X[(16 * kk + t + 4 * (v >> 1)) * TP_LDX + 16 * rg + g + 8 * (v & 1)];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) bb[v] = Ms[(16 * b + 8 * nt + g) * TP_LDM + 16 * kk + t + 4 * v];
+          dmma16x8x16(acc, a, bb);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            double* p = &X[(16 * b + 8 * nt + 2 * t + q) * TP_LDX + 16 * rg + g + 8 * h];
+            *p = *p - acc[2 * h + q];
+          }
+        __syncthreads();
+      }
+      if (tid < TP_ROWS) {
+        double x[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = X[(16 * b + j) * TP_LDX + tid];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          x[j] = x[j] * rinv[16 * b + j];
+#pragma unroll
+          for (int k = j + 1; k < 16; ++k) x[k] = fma(-x[j], Ms[(16 * b + k) * TP_LDM + 16 * b + j], x[k]);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) X[(16 * b + j) * TP_LDX + tid] = x[j];
+      }
+      __syncthreads();
+    }
+    // store the solved tile (16-byte stores, rows beyond n skipped)
+    const int64_t r0 = tile * TP_ROWS;
+    for (int e = tid; e < (TP_ROWS / 2) * m; e += TP_NT) {
+      const int g2 = e % (TP_ROWS / 2), c = e / (TP_ROWS / 2);
+      const int64_t row = r0 + 2 * g2;
+      const double2 v = *reinterpret_cast<const double2*>(X + c * TP_LDX + 2 * g2);
+      double* dst = U2 + row + (int64_t)c * ldu;
+      if (row + 1 < n) *reinterpret_cast<double2*>(dst) = v;
+      else if (row < n) dst[0] = v.x;
+    }
+  }
+  cp_async_wait_group<0>();
+}
+
 template <typename T>
 __global__ void top_from_s_kernel(const double* S, int64_t lds, int m, T* U, int64_t ldu, const Status* st) {
   if (failed(st)) return;
@@ -347,7 +455,14 @@ static int rec_rhqr_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const voi
   const size_t msm = sizeof(double) * m * m;
   const int mp = (int)((m + 15) / 16 * 16);
   const size_t tsm = sizeof(double) * ((size_t)mp * (mp + 4) + (size_t)TR_ROWS * (mp + 1));
-  if (m > 16 && tsm <= 200 * 1024) {
+  const bool pipe_ok = std::is_same<T, double>::value && m > 16 && m <= TP_MP &&
+                       ((reinterpret_cast<uintptr_t>(W2) & 15) == 0) && ((reinterpret_cast<uintptr_t>(U2) & 15) == 0) &&
+                       (ldw % 2 == 0) && (ldu % 2 == 0) && !getenv("SQB_TRSM_BASE");
+  if (pipe_ok) {
+    cudaFuncSetAttribute(trsm_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM);
+    const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + TP_ROWS - 1) / TP_ROWS, 2 * (int64_t)ctx->sm_count));
+    trsm_pipe_kernel<<<gt, TP_NT, TP_SMEM, ctx->stream>>>((const double*)W2, ldw, n, (int)m, mp, M, (double*)U2, ldu, st);
+  } else if (m > 16 && tsm <= 200 * 1024) {
     cudaFuncSetAttribute(trsm_dmma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + TR_ROWS - 1) / TR_ROWS, 2 * (int64_t)ctx->sm_count));
     trsm_dmma_kernel<T><<<gt, TR_NT, tsm, ctx->stream>>>(W2, ldw, n, (int)m, mp, M, U2, ldu, st);

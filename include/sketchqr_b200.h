@@ -235,6 +235,23 @@ int sqb_rhqr_left_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int l
                           double* S, int64_t lds, double* T, int64_t ldt, double* R, int64_t ldr,
                           double* sigmas, double* rhos, double* betas, double* scratch);
 
+/* Row-partitioned recRHQR (rec_rhqr, rhqr.py:368-395) on the same partition:
+ * rank-local SRHT subtrees of Psi W, ONE all-gather of the (ell+m) x m
+ * partials, the rank-order combine (Z bitwise the single-GPU sketch), the
+ * sketch-space QR and Mfac redundantly on every rank, then each rank solves
+ * its own rows U2 = W2 Mfac^{-1} (rank 0 also U[:m] = S[:m]).  Arguments as
+ * sqb_rhqr_left_dist (no Utop scratch); the _virtual form runs P ranks on
+ * one device (scratch as sqb_rhqr_left_virtual). */
+int sqb_rec_rhqr_dist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                      const void* W, int64_t n_local, int64_t m, int64_t ldw,
+                      void* U, int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt,
+                      double* R, int64_t ldr, double* sigmas, double* rhos, double* betas);
+int sqb_rec_rhqr_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                         int nranks, const void* const* W_parts, const int64_t* ldw,
+                         void* const* U_parts, const int64_t* ldu, int64_t m,
+                         double* S, int64_t lds, double* T, int64_t ldt, double* R, int64_t ldr,
+                         double* sigmas, double* rhos, double* betas, double* scratch);
+
 /* Left-looking Householder QR with compact T of a small fp64 A (p x m) in one
  * CTA (householder_qr, baselines.py:33-89; the sketch-space QR of recRHQR).
  * Outputs U (p x m), T, R (m x m), sigmas/rhos/betas; an exactly dependent

@@ -89,6 +89,11 @@ _SIGS = {
     "sqb_rhqr_left_virtual": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, C.c_int, C.POINTER(vp),
                                C.POINTER(i64), C.POINTER(vp), C.POINTER(i64), i64, dp, i64, dp, i64, dp, i64,
                                dp, dp, dp, dp], C.c_int),
+    "sqb_rec_rhqr_dist": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, dp, i64, i64, i64, dp, i64, dp, i64,
+                           dp, i64, dp, i64, dp, dp, dp], C.c_int),
+    "sqb_rec_rhqr_virtual": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, C.c_int, C.POINTER(vp),
+                              C.POINTER(i64), C.POINTER(vp), C.POINTER(i64), i64, dp, i64, dp, i64, dp, i64,
+                              dp, dp, dp, dp], C.c_int),
     "sqb_householder_qr": ([vp, C.c_int, dp, i64, i64, i64, dp, i64, dp, i64, dp, i64, dp, dp, dp], C.c_int),
     "sqb_upper_tri_solve": ([vp, dp, i64, i64, dp, i64, i64, dp, i64], C.c_int),
     "sqb_rh_vector": ([vp, C.c_int, C.c_int, dp, i64, dp, i64, i64, dp, dp, dp], C.c_int),

@@ -418,6 +418,76 @@ __global__ void top_from_s_kernel(const double* S, int64_t lds, int m, T* U, int
     U[(e % m) + (int64_t)(e / m) * ldu] = Lo<T>::store(Lo<T>::from_double(S[(e % m) + (int64_t)(e / m) * lds]));
 }
 
+// Everything of rec_rhqr after the sketch (rhqr.py:383-395): householder_qr
+// of Z (od x m, fp64, overwritten by nothing), Mfac = triu(T^t S^t Z) and its
+// diagonal check, U2 = W2 Mfac^{-1} over the n2 rows of W2 given, and — when
+// Utop is set — the identity-block rows U[:m] = S[:m].  Shared by the single-
+// GPU path and the row-partitioned one (rhqr_dist.cu), where every rank solves
+// its own rows.  M: m x m fp64 scratch; X: n2 x m fp64 scratch when m > 64.
+template <typename T>
+int rec_finish_t(sqb_ctx* ctx, int scaling, const double* Z, int64_t od, int64_t m, const T* W2, int64_t n2,
+                 int64_t ldw, T* U2, int64_t ldu, T* Utop, int64_t ldutop, double* S, int64_t lds, double* Tm,
+                 int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos, double* betas, double* M,
+                 double* X) {
+  Status* st = ctx->d_status;
+  // K5: householder_qr(Z) (rhqr.py:383)
+  const size_t hsm = sizeof(double) * (od + 2 * m + 32);
+  cudaFuncSetAttribute(hqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(hsm, 48 << 10));
+  hqr_kernel<<<1, HQR_NT, hsm, ctx->stream>>>(Z, od, (int)od, (int)m, scaling, S, lds, Tm, ldt, R, ldr,
+                                              sigmas, rhos, betas, st);
+  SQB_TRY(check_launch(ctx, "hqr_kernel"));
+  // Mfac = triu(T^t S^t Z) and its diagonal check (rhqr.py:387-391)
+  mfac_kernel<<<(unsigned)m, 256, sizeof(double) * m, ctx->stream>>>(S, lds, Tm, ldt, Z, od, (int)od, (int)m, M, st);
+  SQB_TRY(check_launch(ctx, "mfac_kernel"));
+  mfac_check_kernel<<<1, 32, 0, ctx->stream>>>(M, (int)m, st);
+  SQB_TRY(check_launch(ctx, "mfac_check_kernel"));
+  // K6: U2 = W2 Mfac^{-1}
+  const int64_t n = n2;
+  if (n > 0) {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, 8 * 148));
+    const size_t msm = sizeof(double) * m * m;
+    const int mp = (int)((m + 15) / 16 * 16);
+    const size_t tsm = sizeof(double) * ((size_t)mp * (mp + 4) + (size_t)TR_ROWS * (mp + 1));
+    const bool pipe_ok = std::is_same<T, double>::value && m > 16 && m <= TP_MP &&
+                         ((reinterpret_cast<uintptr_t>(W2) & 15) == 0) && ((reinterpret_cast<uintptr_t>(U2) & 15) == 0) &&
+                         (ldw % 2 == 0) && (ldu % 2 == 0) && !getenv("SQB_TRSM_BASE");
+    if (pipe_ok) {
+      cudaFuncSetAttribute(trsm_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM);
+      const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + TP_ROWS - 1) / TP_ROWS, 2 * (int64_t)ctx->sm_count));
+      trsm_pipe_kernel<<<gt, TP_NT, TP_SMEM, ctx->stream>>>((const double*)W2, ldw, n, (int)m, mp, M, (double*)U2, ldu, st);
+    } else if (m > 16 && tsm <= 200 * 1024) {
+      cudaFuncSetAttribute(trsm_dmma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + TR_ROWS - 1) / TR_ROWS, 2 * (int64_t)ctx->sm_count));
+      trsm_dmma_kernel<T><<<gt, TR_NT, tsm, ctx->stream>>>(W2, ldw, n, (int)m, mp, M, U2, ldu, st);
+    } else if (m <= 16) {
+      trsm_rows_kernel<T, 16><<<grid, 128, msm, ctx->stream>>>(W2, ldw, n, (int)m, M, U2, ldu, st);
+    } else if (m <= 32) {
+      trsm_rows_kernel<T, 32><<<grid, 128, msm, ctx->stream>>>(W2, ldw, n, (int)m, M, U2, ldu, st);
+    } else if (m <= 64) {
+      trsm_rows_kernel<T, 64><<<grid, 128, msm, ctx->stream>>>(W2, ldw, n, (int)m, M, U2, ldu, st);
+    } else {
+      trsm_rows_generic_kernel<T><<<grid, 128, 0, ctx->stream>>>(W2, ldw, n, (int)m, M, U2, ldu, X, st);
+    }
+    SQB_TRY(check_launch(ctx, "trsm_rows_kernel"));
+  }
+  if (Utop) {
+    top_from_s_kernel<T><<<(unsigned)std::max<int64_t>(1, (m * m + 255) / 256), 256, 0, ctx->stream>>>(
+        S, lds, (int)m, Utop, ldutop, st);
+    SQB_TRY(check_launch(ctx, "top_from_s_kernel"));
+  }
+  return SQB_OK;
+}
+
+#define SQB_REC_FINISH_INST(T)                                                                              \
+  template int rec_finish_t<T>(sqb_ctx*, int, const double*, int64_t, int64_t, const T*, int64_t, int64_t, T*, \
+                               int64_t, T*, int64_t, double*, int64_t, double*, int64_t, double*, int64_t,   \
+                               double*, double*, double*, double*, double*);
+SQB_REC_FINISH_INST(double)
+SQB_REC_FINISH_INST(float)
+SQB_REC_FINISH_INST(__half)
+SQB_REC_FINISH_INST(__nv_bfloat16)
+#undef SQB_REC_FINISH_INST
+
 template <typename T>
 static int rec_rhqr_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W, int64_t N, int64_t m,
                       int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds, double* Tm, int64_t ldt,
@@ -430,56 +500,14 @@ static int rec_rhqr_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const voi
   const size_t iX = plan.add(m > 64 ? sizeof(double) * n * m : 8);
   SQB_TRY(ws_reserve(ctx, plan.total));
   double* Z = ws_ptr<double>(ctx, plan, iZ);
-  double* M = ws_ptr<double>(ctx, plan, iM);
   Status* st = ctx->d_status;
   const size_t esz = sizeof(T);
   // Z = Psi W  (rhqr.py:382)
   SQB_TRY(launch_copy_top(ctx, Lo<T>::code, W, ldw, m, m, Z, od, st));
   SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const char*)W + m * esz, ldw, m, Z, od, m,
                         ws_ptr<void>(ctx, plan, iP), st));
-  // K5: householder_qr(Z) (rhqr.py:383)
-  const size_t hsm = sizeof(double) * (od + 2 * m + 32);
-  cudaFuncSetAttribute(hqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(hsm, 48 << 10));
-  hqr_kernel<<<1, HQR_NT, hsm, ctx->stream>>>(Z, od, (int)od, (int)m, scaling, S, lds, Tm, ldt, R, ldr,
-                                              sigmas, rhos, betas, st);
-  SQB_TRY(check_launch(ctx, "hqr_kernel"));
-  // Mfac = triu(T^t S^t Z) and its diagonal check (rhqr.py:387-391)
-  mfac_kernel<<<(unsigned)m, 256, sizeof(double) * m, ctx->stream>>>(S, lds, Tm, ldt, Z, od, (int)od, (int)m, M, st);
-  SQB_TRY(check_launch(ctx, "mfac_kernel"));
-  mfac_check_kernel<<<1, 32, 0, ctx->stream>>>(M, (int)m, st);
-  SQB_TRY(check_launch(ctx, "mfac_check_kernel"));
-  // K6: U2 = W2 Mfac^{-1}; U = [S[:m]; U2]
-  const T* W2 = (const T*)W + m;
-  T* U2 = (T*)U + m;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, 8 * 148));
-  const size_t msm = sizeof(double) * m * m;
-  const int mp = (int)((m + 15) / 16 * 16);
-  const size_t tsm = sizeof(double) * ((size_t)mp * (mp + 4) + (size_t)TR_ROWS * (mp + 1));
-  const bool pipe_ok = std::is_same<T, double>::value && m > 16 && m <= TP_MP &&
-                       ((reinterpret_cast<uintptr_t>(W2) & 15) == 0) && ((reinterpret_cast<uintptr_t>(U2) & 15) == 0) &&
-                       (ldw % 2 == 0) && (ldu % 2 == 0) && !getenv("SQB_TRSM_BASE");
-  if (pipe_ok) {
-    cudaFuncSetAttribute(trsm_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM);
-    const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + TP_ROWS - 1) / TP_ROWS, 2 * (int64_t)ctx->sm_count));
-    trsm_pipe_kernel<<<gt, TP_NT, TP_SMEM, ctx->stream>>>((const double*)W2, ldw, n, (int)m, mp, M, (double*)U2, ldu, st);
-  } else if (m > 16 && tsm <= 200 * 1024) {
-    cudaFuncSetAttribute(trsm_dmma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-    const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + TR_ROWS - 1) / TR_ROWS, 2 * (int64_t)ctx->sm_count));
-    trsm_dmma_kernel<T><<<gt, TR_NT, tsm, ctx->stream>>>(W2, ldw, n, (int)m, mp, M, U2, ldu, st);
-  } else if (m <= 16) {
-    trsm_rows_kernel<T, 16><<<grid, 128, msm, ctx->stream>>>(W2, ldw, n, (int)m, M, U2, ldu, st);
-  } else if (m <= 32) {
-    trsm_rows_kernel<T, 32><<<grid, 128, msm, ctx->stream>>>(W2, ldw, n, (int)m, M, U2, ldu, st);
-  } else if (m <= 64) {
-    trsm_rows_kernel<T, 64><<<grid, 128, msm, ctx->stream>>>(W2, ldw, n, (int)m, M, U2, ldu, st);
-  } else {
-    trsm_rows_generic_kernel<T><<<grid, 128, 0, ctx->stream>>>(W2, ldw, n, (int)m, M, U2, ldu,
-                                                                ws_ptr<double>(ctx, plan, iX), st);
-  }
-  SQB_TRY(check_launch(ctx, "trsm_rows_kernel"));
-  top_from_s_kernel<T><<<(unsigned)std::max<int64_t>(1, (m * m + 255) / 256), 256, 0, ctx->stream>>>(
-      S, lds, (int)m, (T*)U, ldu, st);
-  return check_launch(ctx, "top_from_s_kernel");
+  return rec_finish_t<T>(ctx, scaling, Z, od, m, (const T*)W + m, n, ldw, (T*)U + m, ldu, (T*)U, ldu, S, lds, Tm,
+                         ldt, R, ldr, sigmas, rhos, betas, ws_ptr<double>(ctx, plan, iM), ws_ptr<double>(ctx, plan, iX));
 }
 
 int rec_rhqr_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, const void* W,

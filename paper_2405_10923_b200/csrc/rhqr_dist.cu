@@ -254,6 +254,108 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
   return SQB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Row-partitioned recRHQR (rhqr.py:368-395): the rank-local
+// SRHT subtrees of Psi W, ONE all-gather of the (ell+m) x m partials, the
+// rank-order combine (the same binary tree as one GPU, so Z is bitwise the
+// single-GPU sketch), then every rank runs the sketch-space QR and Mfac
+// redundantly and solves its own rows U2 = W2 Mfac^{-1}; rank 0 also writes
+// the identity-block rows U[:m] = S[:m].
+// ---------------------------------------------------------------------------
+template <typename T>
+int rec_finish_t(sqb_ctx* ctx, int scaling, const double* Z, int64_t od, int64_t m, const T* W2, int64_t n2,
+                 int64_t ldw, T* U2, int64_t ldu, T* Utop, int64_t ldutop, double* S, int64_t lds, double* Tm,
+                 int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos, double* betas, double* M,
+                 double* X);
+
+template <typename T>
+static int rec_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t m, std::vector<DistRank>& rk,
+                      int nranks, bool virt, const std::vector<int>& rank_ids) {
+  using A = typename Lo<T>::acc;
+  const int64_t ell = sk->ell, od = m + ell;
+  const SrhtGeom g = srht_geom_t<T>(sk);
+  if (g.n_tiles % nranks != 0)
+    return set_error(ctx, SQB_ERR_ARG, "n_pad=%lld too small for %d ranks (need n_pad/P >= %d)",
+                     (long long)sk->n_pad, nranks, 1 << g.log_tb);
+  const int64_t tpr = g.n_tiles / nranks;
+  int rank_level = 0;
+  while ((int64_t(1) << rank_level) < tpr) ++rank_level;
+  const int64_t tb = int64_t(1) << g.log_tb;
+  const size_t esz = sizeof(T);
+  const int L = (int)rk.size();
+  int64_t nmax = 0;
+  for (auto& d : rk) nmax = std::max(nmax, d.n_local);
+  WsPlan plan;
+  std::vector<size_t> off(L * 2);
+  for (int r = 0; r < L; ++r) {
+    off[r * 2 + 0] = plan.add(sizeof(double) * m * od);    // partial payload
+    off[r * 2 + 1] = plan.add(sizeof(A) * ell * tpr * m);  // leaves
+  }
+  const size_t iG0 = plan.add(sizeof(double) * nranks * m * od);
+  const size_t iZ = plan.add(sizeof(double) * od * m);
+  const size_t iM = plan.add(sizeof(double) * m * m);
+  const size_t iX = plan.add(m > 64 ? sizeof(double) * nmax * m : 8);
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  char* base = static_cast<char*>(ctx->ws);
+  for (int r = 0; r < L; ++r) {
+    rk[r].Y0pay = (double*)(base + plan.offs[off[r * 2 + 0]]);
+    rk[r].P = base + plan.offs[off[r * 2 + 1]];
+  }
+  double* G0 = (double*)(base + plan.offs[iG0]);
+  double* Z = (double*)(base + plan.offs[iZ]);
+  Status* st = ctx->d_status;
+  NcclApi* nc = virt ? nullptr : nccl_api();
+  if (!virt && (!nc || !ctx->nccl)) return set_error(ctx, SQB_ERR_NCCL, "NCCL communicator not initialised");
+  double scale_lo = 0.0, norm_lo = 0.0;
+  srht_constants(sk, Lo<T>::code, &scale_lo, &norm_lo);
+  for (int r = 0; r < L; ++r) {
+    DistRank& d = rk[r];
+    SrhtGeom gl{g.log_tb, tpr, (d.n_local + tb - 1) / tb};
+    if (d.n_local > 0) {
+      SQB_TRY(launch_srht_tiles_geom(ctx, sk, Lo<T>::code, gl, d.n_local, d.e_base,
+                                     (const char*)d.W + d.mrow * esz, d.ldw, m, d.P, st));
+    } else {
+      SQB_CUDA_TRY(cudaMemsetAsync(d.P, 0, sizeof(A) * ell * tpr * m, ctx->stream));
+    }
+    SQB_TRY(launch_srht_tree_geom(ctx, sk, Lo<T>::code, gl, d.P, m, d.Y0pay, od, 0, 0, st));
+    if (d.mrow > 0) SQB_TRY(launch_copy_top(ctx, Lo<T>::code, d.W, d.ldw, m, m, d.Y0pay + ell, od, st));
+  }
+  const size_t count = (size_t)m * od;
+  if (virt) {
+    for (int r = 0; r < L; ++r)
+      SQB_CUDA_TRY(cudaMemcpyAsync(G0 + (size_t)rank_ids[r] * count, rk[r].Y0pay, sizeof(double) * count,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    ncclResult_t e = nc->allGather(rk[0].Y0pay, G0, count, ncclDouble, (ncclComm_t)ctx->nccl, ctx->stream);
+    if (e != ncclSuccess)
+      return set_error(ctx, SQB_ERR_NCCL, "ncclAllGather: %s", nc->getErrorString ? nc->getErrorString(e) : "?");
+  }
+  {
+    dim3 grid((unsigned)((od + 255) / 256), (unsigned)m);
+    rank_combine_kernel<T><<<grid, 256, 0, ctx->stream>>>(G0, nranks, (int)ell, (int)m, rank_level, sk->indices,
+                                                          g.log_tb, norm_lo, Z, od, st);
+    SQB_TRY(check_launch(ctx, "rank_combine_kernel"));
+  }
+  for (int r = 0; r < L; ++r) {
+    DistRank& d = rk[r];
+    SQB_TRY(rec_finish_t<T>(ctx, scaling, Z, od, m, (const T*)d.W + d.mrow, d.n_local, d.ldw, (T*)d.U + d.mrow,
+                            d.ldu, d.mrow > 0 ? (T*)d.U : nullptr, d.ldu, d.S, d.lds, d.T, d.ldt, d.R, d.ldr, d.sig,
+                            d.rho, d.bet, (double*)(base + plan.offs[iM]), (double*)(base + plan.offs[iX])));
+  }
+  return SQB_OK;
+}
+
+static int rec_dist_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, int64_t m,
+                             std::vector<DistRank>& rk, int nranks, bool virt, const std::vector<int>& ids) {
+  switch (lo_dtype) {
+    case SQB_F64: return rec_dist_t<double>(ctx, sk, scaling, m, rk, nranks, virt, ids);
+    case SQB_F32: return rec_dist_t<float>(ctx, sk, scaling, m, rk, nranks, virt, ids);
+    case SQB_F16: return rec_dist_t<__half>(ctx, sk, scaling, m, rk, nranks, virt, ids);
+    case SQB_BF16: return rec_dist_t<__nv_bfloat16>(ctx, sk, scaling, m, rk, nranks, virt, ids);
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
 static int dist_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, int64_t m,
                          std::vector<DistRank>& rk, int nranks, bool virt, const std::vector<int>& ids) {
   switch (lo_dtype) {
@@ -308,7 +410,7 @@ int sqb_ctx_init_comm(sqb_ctx* ctx, const char* id, int nranks, int rank) {
   return SQB_OK;
 }
 
-int sqb_rhqr_left_dist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, const void* W,
+static int left_dist_entry(bool rec, sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, const void* W,
                        int64_t n_local, int64_t m, int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds,
                        double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
                        double* betas, void* Utop_scratch) {
@@ -329,11 +431,12 @@ int sqb_rhqr_left_dist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_d
   d.lds = lds; d.ldt = ldt; d.ldr = ldr;
   d.Utop = ctx->rank == 0 ? U : Utop_scratch;
   d.ldutop = ctx->rank == 0 ? ldu : m;
-  if (!d.Utop) return set_error(ctx, SQB_ERR_ARG, "ranks > 0 need an m x m Utop_scratch buffer");
-  return dist_dispatch(ctx, sk, scaling, lo_dtype, m, rk, ctx->nranks, false, std::vector<int>{ctx->rank});
+  if (!d.Utop && !rec) return set_error(ctx, SQB_ERR_ARG, "ranks > 0 need an m x m Utop_scratch buffer");
+  return rec ? rec_dist_dispatch(ctx, sk, scaling, lo_dtype, m, rk, ctx->nranks, false, std::vector<int>{ctx->rank})
+             : dist_dispatch(ctx, sk, scaling, lo_dtype, m, rk, ctx->nranks, false, std::vector<int>{ctx->rank});
 }
 
-int sqb_rhqr_left_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, int nranks,
+static int left_virtual_entry(bool rec, sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, int nranks,
                           const void* const* W_parts, const int64_t* ldw, void* const* U_parts,
                           const int64_t* ldu, int64_t m, double* S, int64_t lds, double* T, int64_t ldt,
                           double* R, int64_t ldr, double* sigmas, double* rhos, double* betas, double* scratch) {
@@ -364,7 +467,40 @@ int sqb_rhqr_left_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int l
     }
   }
   // rank r > 0 writes its identity-block u rows as T; the scratch is double, large enough for any T
-  return dist_dispatch(ctx, sk, scaling, lo_dtype, m, rk, nranks, true, ids);
+  return rec ? rec_dist_dispatch(ctx, sk, scaling, lo_dtype, m, rk, nranks, true, ids)
+             : dist_dispatch(ctx, sk, scaling, lo_dtype, m, rk, nranks, true, ids);
+}
+
+int sqb_rhqr_left_dist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, const void* W,
+                       int64_t n_local, int64_t m, int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds,
+                       double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
+                       double* betas, void* Utop_scratch) {
+  return left_dist_entry(false, ctx, sk, scaling, lo_dtype, W, n_local, m, ldw, U, ldu, S, lds, T, ldt, R, ldr,
+                         sigmas, rhos, betas, Utop_scratch);
+}
+
+int sqb_rec_rhqr_dist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, const void* W,
+                      int64_t n_local, int64_t m, int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds,
+                      double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
+                      double* betas) {
+  return left_dist_entry(true, ctx, sk, scaling, lo_dtype, W, n_local, m, ldw, U, ldu, S, lds, T, ldt, R, ldr,
+                         sigmas, rhos, betas, nullptr);
+}
+
+int sqb_rhqr_left_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, int nranks,
+                          const void* const* W_parts, const int64_t* ldw, void* const* U_parts,
+                          const int64_t* ldu, int64_t m, double* S, int64_t lds, double* T, int64_t ldt,
+                          double* R, int64_t ldr, double* sigmas, double* rhos, double* betas, double* scratch) {
+  return left_virtual_entry(false, ctx, sk, scaling, lo_dtype, nranks, W_parts, ldw, U_parts, ldu, m, S, lds, T,
+                            ldt, R, ldr, sigmas, rhos, betas, scratch);
+}
+
+int sqb_rec_rhqr_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, int nranks,
+                         const void* const* W_parts, const int64_t* ldw, void* const* U_parts,
+                         const int64_t* ldu, int64_t m, double* S, int64_t lds, double* T, int64_t ldt,
+                         double* R, int64_t ldr, double* sigmas, double* rhos, double* betas, double* scratch) {
+  return left_virtual_entry(true, ctx, sk, scaling, lo_dtype, nranks, W_parts, ldw, U_parts, ldu, m, S, lds, T,
+                            ldt, R, ldr, sigmas, rhos, betas, scratch);
 }
 
 }  // extern "C"

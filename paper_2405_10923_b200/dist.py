@@ -74,6 +74,16 @@ def init_comm(group=None):
 
 def rhqr_left_distributed(W_local, omega, m, scaling=SCALE_SQRT2, policy=None, check=True):
     """This rank's part of rhqr_left (rhqr.py:254-267) on the row partition."""
+    return _distributed("sqb_rhqr_left_dist", W_local, omega, m, scaling, policy, check)
+
+
+def rec_rhqr_distributed(W_local, omega, m, scaling=SCALE_SQRT2, policy=None, check=True):
+    """This rank's part of rec_rhqr (rhqr.py:368-395) on the row partition:
+    one all-gather of the sketch partials, then a local triangular solve."""
+    return _distributed("sqb_rec_rhqr_dist", W_local, omega, m, scaling, policy, check)
+
+
+def _distributed(entry, W_local, omega, m, scaling, policy, check):
     check_scaling(scaling)
     policy = policy or DOUBLE_POLICY
     require_device_policy(policy)
@@ -94,13 +104,14 @@ def rhqr_left_distributed(W_local, omega, m, scaling=SCALE_SQRT2, policy=None, c
     scal = torch.empty(3 * m, dtype=torch.float64, device="cuda")
     utop = torch.empty(m * m, dtype=torch.float64, device="cuda")
     ctx = _lib.context()
-    ctx.check(_lib.lib().sqb_rhqr_left_dist(
-        ctx.h, omega.desc(), scaling_code(scaling), CODES[tag], Wd.data_ptr(), n_local, m, ld_of(Wd),
-        U.data_ptr(), ld_of(U), S.data_ptr(), ld_of(S), T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R),
-        scal.data_ptr(), scal.data_ptr() + 8 * m, scal.data_ptr() + 16 * m, utop.data_ptr()),
-        "sqb_rhqr_left_dist")
+    args = [ctx.h, omega.desc(), scaling_code(scaling), CODES[tag], Wd.data_ptr(), n_local, m, ld_of(Wd),
+            U.data_ptr(), ld_of(U), S.data_ptr(), ld_of(S), T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R),
+            scal.data_ptr(), scal.data_ptr() + 8 * m, scal.data_ptr() + 16 * m]
+    if entry == "sqb_rhqr_left_dist":
+        args.append(utop.data_ptr())
+    ctx.check(getattr(_lib.lib(), entry)(*args), entry)
     if check:
-        raise_status(ctx, "rhqr_left_distributed")
+        raise_status(ctx, "rec_rhqr" if entry == "sqb_rec_rhqr_dist" else "rhqr_left_distributed")
     del world
     return RHQRFactors(U=_out(U, host), S=_out(S, host), T=_out(T, host), R=_out(R, host),
                        psi=EmbeddedSketch(m, omega),
@@ -112,6 +123,15 @@ def rhqr_left_virtual(W, omega, nranks, scaling=SCALE_SQRT2, policy=None):
     """The multi-GPU algorithm with `nranks` virtual ranks on ONE device (the
     all-gather becomes device copies).  Returns factors with U reassembled in
     global row order — bitwise equal to rhqr_left by construction."""
+    return _virtual("sqb_rhqr_left_virtual", W, omega, nranks, scaling, policy)
+
+
+def rec_rhqr_virtual(W, omega, nranks, scaling=SCALE_SQRT2, policy=None):
+    """Row-partitioned rec_rhqr with `nranks` virtual ranks on one device."""
+    return _virtual("sqb_rec_rhqr_virtual", W, omega, nranks, scaling, policy)
+
+
+def _virtual(entry, W, omega, nranks, scaling, policy):
     check_scaling(scaling)
     policy = policy or DOUBLE_POLICY
     require_device_policy(policy)
@@ -138,11 +158,11 @@ def rhqr_left_virtual(W, omega, nranks, scaling=SCALE_SQRT2, policy=None):
     Up = (C.c_void_p * nranks)(*[t.data_ptr() for t in Us])
     Ul = (C.c_int64 * nranks)(*[ld_of(t) for t in Us])
     ctx = _lib.context()
-    ctx.check(_lib.lib().sqb_rhqr_left_virtual(
+    ctx.check(getattr(_lib.lib(), entry)(
         ctx.h, omega.desc(), scaling_code(scaling), CODES[tag], nranks, Wp, Wl, Up, Ul, m, S.data_ptr(),
         ld_of(S), T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R), scal.data_ptr(), scal.data_ptr() + 8 * m,
-        scal.data_ptr() + 16 * m, scratch.data_ptr()), "sqb_rhqr_left_virtual")
-    raise_status(ctx, "rhqr_left_virtual")
+        scal.data_ptr() + 16 * m, scratch.data_ptr()), entry)
+    raise_status(ctx, "rec_rhqr" if entry == "sqb_rec_rhqr_virtual" else "rhqr_left_virtual")
     U = empty_colmajor(N, m, tag)
     for rows, Ut in zip(rows_list, Us):
         if len(rows):

@@ -455,6 +455,24 @@ def test_row_partitioned_config2_shape(P):
     assert np.array_equal(Fv.R, F1.R) and np.array_equal(Fv.U, F1.U)
 
 
+@pytest.mark.parametrize("nranks,m", [(1, 16), (2, 48), (4, 64), (8, 80)])
+def test_row_partitioned_rec_rhqr(P, nranks, m):
+    """Row-partitioned recRHQR (one all-gather of the sketch partials): the
+    combined sketch — hence S, T, R — is bitwise the single-GPU one; the
+    rows of U come from the same per-row triangular solve."""
+    from paper_2405_10923_b200 import dist
+    N = (1 << 16) + 77
+    W = workloads.gen_cmatrix(N, m)
+    om = P.SRHTSketch(4 * m, N - m, 19)
+    F1 = P.rec_rhqr(W, om)
+    Fv = dist.rec_rhqr_virtual(W, om, nranks)
+    for k in ("R", "S", "T", "sigmas", "rhos", "betas"):
+        assert np.array_equal(getattr(Fv, k), getattr(F1, k)), k
+    assert rel(Fv.U, F1.U) < 1e-14
+    Fo = O.rec_rhqr(W, O.SRHT(4 * m, N - m, 19))
+    assert rel(Fv.R, Fo.R) < 1e-10
+
+
 def test_nccl_row_partitioned_single_rank(P):
     """Exercises the real NCCL plumbing of the row-partitioned path (dlopen,
     unique id, communicator, per-column all-gather) with world_size 1."""
@@ -476,6 +494,12 @@ def test_nccl_row_partitioned_single_rank(P):
         F1 = P.rhqr_left(W, om)
         for k in ("R", "S", "T", "U"):
             assert np.array_equal(getattr(Fd, k), getattr(F1, k)), k
+        Wc = workloads.gen_cmatrix(N, 24)
+        omc = P.SRHTSketch(96, N - 24, 4)
+        Fr, Fr1 = D.rec_rhqr_distributed(Wc, omc, 24), P.rec_rhqr(Wc, omc)
+        for k in ("R", "S", "T"):
+            assert np.array_equal(getattr(Fr, k), getattr(Fr1, k)), k
+        assert rel(Fr.U, Fr1.U) < 1e-14
     finally:
         if created:
             dist.destroy_process_group()

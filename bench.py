@@ -327,16 +327,38 @@ class GMRESCycle(Workload):
         k, m = self.k, self.m
         indptr, indices, data = workloads.convection_diffusion_csr(k)
         N = k * k
-        self.A = P.CSRMatrix(indptr, indices, data, N)
-        self.b = torch.from_numpy(np.random.default_rng(11 + rank).standard_normal(N)).cuda()
         self.om = P.SRHTSketch(self.ell, N - m - 1, CFG["sketch_seed"])
-        self.step = lambda check=False: P.rhqr_gmres(self.A, self.b, None, m, self.om)
-        nnz = self.A.nnz
+        b = np.random.default_rng(11).standard_normal(N)
+        nnz = int(indptr[-1])
+        if ws > 1:
+            # strong scaling: the row-partitioned Arnoldi over the same 2048^2
+            # problem (q all-gather for the SpMV + two sketch all-gathers per step)
+            import scipy.sparse
+
+            from paper_2405_10923_b200 import dist as D
+            D.init_comm()
+            A = scipy.sparse.csr_matrix((data, indices, indptr), shape=(N, N))
+            self.Al = D.local_operator(A, m, self.om.n_pad, ws, rank)
+            r0, nr = self.Al[3], self.Al[4]
+            bl = torch.from_numpy(b[r0:r0 + nr].copy()).cuda()
+            x0l = torch.zeros(nr, dtype=torch.float64, device="cuda")
+
+            def step(check=False):
+                bun = D.rhqr_arnoldi_distributed(self.Al, bl, x0l, m, self.om, N)
+                y, _ = P.hessenberg_lstsq(bun.H, bun.beta)
+                return D.gmres_solution_local(bun, y, x0l, rank)
+            self.step = step
+            self.scaling = "strong"
+        else:
+            self.A = P.CSRMatrix(indptr, indices, data, N)
+            self.b = torch.from_numpy(b).cuda()
+            self.step = lambda check=False: P.rhqr_gmres(self.A, self.b, None, m, self.om)
         self.alg = float(sum(8 * N * (2 * j + 5) for j in range(1, m + 1)) + m * (12 * nnz + 12 * N))
         self.kernel = "update_kernel / arn_q_kernel (streaming GEMVs over the Krylov reflectors)"
         self.config = {"workload": f"rhqr_gmres cfg5: one GMRES({m}) cycle, {k}^2 grid CSR (nnz {nnz}), SRHT {self.ell}",
                        "N": N, "m": m, "ell": self.ell, "nnz": nnz,
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                       "parallelism": (f"row-partitioned x{ws} (q all-gather + 2 sketch all-gathers per step)"
+                                       if ws > 1 else "single GPU"),
                        "l2": "no flush: U (6.7 GB) exceeds L2", "alg_bytes_per_step": self.alg}
 
     def e2e(self, steps):

@@ -94,6 +94,15 @@ _SIGS = {
     "sqb_rec_rhqr_virtual": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, C.c_int, C.POINTER(vp),
                               C.POINTER(i64), C.POINTER(vp), C.POINTER(i64), i64, dp, i64, dp, i64, dp, i64,
                               dp, dp, dp, dp], C.c_int),
+    "sqb_compact_update": ([vp, C.c_int, dp, i64, dp, i64, dp, i64, C.c_int, i64, dp, i64, i64, dp, dp], C.c_int),
+    "sqb_rhqr_arnoldi_dist": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, C.c_int, C.c_double, i64, i64, i64,
+                               dp, dp, dp, dp, dp, dp, i64, dp, i64, dp, i64, dp, i64, dp, i64, dp, dp,
+                               C.POINTER(C.c_int)], C.c_int),
+    "sqb_rhqr_arnoldi_virtual": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                  C.POINTER(i64), C.POINTER(i64), i64, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                  C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(i64), C.POINTER(vp), i64,
+                                  C.POINTER(vp), i64, C.POINTER(vp), i64, C.POINTER(vp), C.POINTER(vp),
+                                  C.POINTER(C.c_int)], C.c_int),
     "sqb_householder_qr": ([vp, C.c_int, dp, i64, i64, i64, dp, i64, dp, i64, dp, i64, dp, dp, dp], C.c_int),
     "sqb_upper_tri_solve": ([vp, dp, i64, i64, dp, i64, i64, dp, i64], C.c_int),
     "sqb_rh_vector": ([vp, C.c_int, C.c_int, dp, i64, dp, i64, i64, dp, dp, dp], C.c_int),

@@ -129,6 +129,42 @@ static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, con
   return check_launch(ctx, "update_kernel");
 }
 
+// Out = X - U op(T) S^t Y for a given sketch Y = Psi X (od x 1): the
+// coefficient and update halves of apply_reflectors_t, used by the
+// row-partitioned Arnoldi (krylov.cu) on each rank's rows after the sketch
+// has been combined across ranks.  C: r doubles of scratch.
+int compact_update_dispatch(sqb_ctx* ctx, int lo_dtype, const double* Y, int64_t od, const double* S, int64_t lds,
+                            const double* Tm, int64_t ldt, int transpose_t, int64_t r, const void* U, int64_t ldu,
+                            int64_t N, const void* X, void* Out, double* C) {
+  const Status* st = ctx->d_status;
+  coef_kernel<<<1, 256, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od, (int)od, (int)r, C,
+                                                           r, st);
+  SQB_TRY(check_launch(ctx, "coef_kernel"));
+  auto run = [&](auto t) -> int {
+    using T = decltype(t);
+    constexpr int VN = VecN<T>::n;
+    const bool vec = ((reinterpret_cast<uintptr_t>(U) & 15) == 0) && (ldu % VN == 0);
+    if (vec) {
+      const int64_t blocks = (N + (int64_t)GEMV_NT * 4 * VN - 1) / ((int64_t)GEMV_NT * 4 * VN);
+      dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, 2 * (int64_t)ctx->sm_count)), 1);
+      update_kernel<T><<<grid, GEMV_NT, sizeof(typename Lo<T>::acc) * r, ctx->stream>>>(
+          (const T*)U, ldu, N, (int)r, C, r, (const T*)X, N, (T*)Out, N, st);
+    } else {
+      dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 4 * 148)), 1);
+      update_scalar_kernel<T><<<grid, 256, sizeof(typename Lo<T>::acc) * r, ctx->stream>>>(
+          (const T*)U, ldu, N, (int)r, C, r, (const T*)X, N, (T*)Out, N, st);
+    }
+    return check_launch(ctx, "update_kernel");
+  };
+  switch (lo_dtype) {
+    case SQB_F64: return run(double());
+    case SQB_F32: return run(float());
+    case SQB_F16: return run(__half());
+    case SQB_BF16: return run(__nv_bfloat16());
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
 size_t apply_reflectors_ws_bytes(const sqb_sketch* sk, int dtype, int64_t m, int64_t r, int64_t k) {
   WsPlan plan;
   plan.add(sizeof(double) * (m + sk->ell) * k);
@@ -414,4 +450,23 @@ extern "C" int sqb_arnoldi_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t 
     case SQB_BF16: return arnoldi_q_t<__nv_bfloat16>(ctx, U, ldu, N, r, T, ldt, S, lds, c, Q, ldq);
   }
   return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
+// Out = X - U op(T) S^t Y with the sketch Y = Psi X given (od fp64): the
+// compact-form update of apply_reflectors_compact (rhqr.py:100-119) without
+// its sketch, for callers that hold Psi X already (the row-partitioned GMRES
+// solution, whose padded coefficient vector has Psi pad = [pad[:m+1]; 0]).
+extern "C" int sqb_compact_update(sqb_ctx* ctx, int lo_dtype, const double* Y, int64_t od, const double* S,
+                                  int64_t lds, const double* T, int64_t ldt, int transpose_t, int64_t r,
+                                  const void* U, int64_t ldu, int64_t N, const void* X, void* Out) {
+  using namespace sqb;
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  if (r < 1 || N < 1) return SQB_OK;
+  WsPlan plan;
+  const size_t iC = plan.add(sizeof(double) * r);
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  return compact_update_dispatch(ctx, lo_dtype, Y, od, S, lds, T, ldt, transpose_t, r, U, ldu, N, X, Out,
+                                 ws_ptr<double>(ctx, plan, iC));
 }

@@ -1,0 +1,97 @@
+// Pieces shared by the row-partitioned paths (rhqr_dist.cu, krylov.cu):
+// the lazily loaded NCCL API, the all-gather (NCCL or, for virtual ranks on
+// one device, device copies) and the rank-order combine of gathered SRHT
+// partials — the top log2(P) levels of the single-GPU tree, so a combined
+// sketch is bitwise the single-GPU one.
+#pragma once
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <vector>
+
+#include "sketch.cuh"
+
+namespace sqb {
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded lazily (single-GPU users never need it)
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+inline NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.h = h;
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+    }
+  }
+  return (api.getUniqueId && api.commInitRank && api.allGather) ? &api : nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// combine the gathered raw-sketch partials: Y0[row, col] (od x m)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void rank_combine_kernel(const double* __restrict__ G, int nranks, int ell, int m, int ncols, int rank_level,
+                                    const int64_t* __restrict__ idx, int log_tb, double norm_lo,
+                                    double* __restrict__ Y0, int64_t ldy, const Status* st) {
+  using A = typename Lo<T>::acc;
+  if (failed(st)) return;
+  const int pl = ell + m;
+  const int col = blockIdx.y;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < m + ell; row += gridDim.x * blockDim.x) {
+    double y;
+    if (row < m) {
+      y = G[(int64_t)col * pl + ell + row];  // rank 0's slot
+    } else {
+      const int o = row - m;
+      const int64_t rhi = __ldg(idx + o) >> log_tb;
+      A v[8];
+      for (int q = 0; q < nranks; ++q) v[q] = (A)G[((int64_t)q * ncols + col) * pl + o];
+      int lvl = rank_level;
+      for (int w = 1; w < nranks; w <<= 1, ++lvl) {
+        const bool neg = (rhi >> lvl) & 1;
+        for (int q = 0; q + w < nranks; q += 2 * w) v[q] = neg ? Lo<T>::sub(v[q], v[q + w]) : Lo<T>::add(v[q], v[q + w]);
+      }
+      y = (double)Lo<T>::mul(v[0], (A)norm_lo);
+    }
+    Y0[row + (int64_t)col * ldy] = y;
+  }
+}
+
+
+// all-gather `bytes` from every (local) rank's send buffer into G ([rank][bytes])
+inline int dist_allgather(sqb_ctx* ctx, bool virt, const std::vector<int>& ids, const std::vector<const void*>& send,
+                          size_t bytes, void* G) {
+  if (virt) {
+    for (size_t r = 0; r < send.size(); ++r)
+      SQB_CUDA_TRY(cudaMemcpyAsync((char*)G + (size_t)ids[r] * bytes, send[r], bytes, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+    return SQB_OK;
+  }
+  NcclApi* nc = nccl_api();
+  if (!nc || !ctx->nccl) return set_error(ctx, SQB_ERR_NCCL, "NCCL communicator not initialised");
+  ncclResult_t e = nc->allGather(send[0], G, bytes, ncclUint8, (ncclComm_t)ctx->nccl, ctx->stream);
+  if (e != ncclSuccess)
+    return set_error(ctx, SQB_ERR_NCCL, "ncclAllGather: %s", nc->getErrorString ? nc->getErrorString(e) : "?");
+  return SQB_OK;
+}
+
+}  // namespace sqb

@@ -21,6 +21,7 @@
 #include "vec.cuh"
 #include "gemv.cuh"
 #include "dense.cuh"
+#include "dist_common.cuh"
 
 namespace sqb {
 
@@ -194,14 +195,15 @@ __global__ void __launch_bounds__(ARN_NT) arn_step_kernel(ArnArgs a) {
   }
 }
 
-// q = e_j - lo(U_j coef) (krylov.py:137-139); lazy scaling of U[:, j-1] rows >= mt;
+// q = e_j - lo(U_j coef) (krylov.py:137-139); lazy scaling of U[:, j-1] rows >= mt
+// (the local rows past the identity block; row0 = global index of local row 0);
 // q_lo = round(q) feeds the matvec, Q[:, j-1] = q (fp64) when stored.
 // Streaming GEMV core over the final columns 0..j-2 (gemv.cuh).
 template <typename T>
 __global__ void __launch_bounds__(GEMV_NT, 2)
 arn_q_kernel(int64_t n, int mt, int j, T* U, int64_t ldu, const double* __restrict__ coefq,
              const double* __restrict__ fscale, int scaling, T* __restrict__ q, double* __restrict__ Q,
-             const Status* st) {
+             const Status* st, int64_t row0 = 0) {
   using A = typename Lo<T>::acc;
   constexpr int VN = VecN<T>::n, NV = 4;
   extern __shared__ unsigned char smraw[];
@@ -230,7 +232,7 @@ arn_q_kernel(int64_t n, int mt, int j, T* U, int64_t ldu, const double* __restri
         }
         const A a = fma(x, c[jj], acc[v][e]);
         double qv = -(double)Lo<T>::rnd(a);
-        if (i == jj) qv = qv + 1.0;
+        if (row0 + i == jj) qv = qv + 1.0;  // e_j (global row j-1: rank 0's identity rows)
         q[i] = Lo<T>::store(Lo<T>::from_double(qv));
         if (Q) Q[i] = qv;
       }
@@ -420,6 +422,218 @@ static int arnoldi_dispatch_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& 
                       beta, attained);
 }
 
+// ---------------------------------------------------------------------------
+// Row-partitioned RHQR-Arnoldi.  Rank p owns the rows of the
+// Omega coordinates [p n_pad/P, (p+1) n_pad/P) (whole SRHT tiles) and rank 0
+// also the m+1 identity-block rows, so every rank's rows are one contiguous
+// range.  Per step the exchanges are (a) the all-gather of q for the SpMV
+// (each rank multiplies its own CSR rows, whose column indices the caller has
+// remapped into the gathered [rank][seg] layout), and (b) two (ell+m+1)-vector
+// all-gathers of the rank-local SRHT subtrees (the projection's sketch and
+// z = Psi w), combined in rank order — the single-GPU tree, so z, H, S, T
+// and beta are bitwise the single-GPU ones.  The sketch-space step runs
+// redundantly on every rank; U, w, q and the Krylov rows never move.
+// ---------------------------------------------------------------------------
+int compact_update_dispatch(sqb_ctx* ctx, int lo_dtype, const double* Y, int64_t od, const double* S, int64_t lds,
+                            const double* Tm, int64_t ldt, int transpose_t, int64_t r, const void* U, int64_t ldu,
+                            int64_t N, const void* X, void* Out, double* C);
+
+struct ArnRank {
+  int64_t rows;     // local rows (identity block included on rank 0)
+  int mrow;         // m+1 on rank 0, else 0
+  int64_t row0;     // global row of local row 0
+  int64_t e_base;   // first global Omega coordinate
+  const int64_t* indptr; const int32_t* indices; const double* data;  // local CSR rows, remapped columns
+  const double* b; const void* x0lo;                                  // local rows
+  void* U; int64_t ldu; double* Q; int64_t ldq;
+  double *S, *T, *H, *beta; int64_t lds, ldt, ldh;
+  void* Utop; int64_t ldutop;                                         // identity rows of U (ranks > 0: scratch)
+  // workspace
+  double *z, *Y, *C, *cq, *fs, *pay;
+  void *w, *q, *P;
+};
+
+template <typename T>
+static int arnoldi_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int m, int scaling, double happy_tol,
+                          std::vector<ArnRank>& rk, int nranks, bool virt, const std::vector<int>& ids, int64_t seg,
+                          int* attained) {
+  using A = typename Lo<T>::acc;
+  const int mt = m + 1;
+  const int64_t ell = sk->ell, od = mt + ell, pl = ell + mt;
+  const SrhtGeom g = srht_geom_t<T>(sk);
+  if (g.n_tiles % nranks != 0)
+    return set_error(ctx, SQB_ERR_ARG, "n_pad=%lld too small for %d ranks", (long long)sk->n_pad, nranks);
+  const int64_t tpr = g.n_tiles / nranks, tb = int64_t(1) << g.log_tb;
+  int rank_level = 0;
+  while ((int64_t(1) << rank_level) < tpr) ++rank_level;
+  const int L = (int)rk.size();
+  constexpr int VN = VecN<T>::n;
+  WsPlan plan;
+  std::vector<size_t> off(L * 9);
+  for (int r = 0; r < L; ++r) {
+    off[r * 9 + 0] = plan.add(sizeof(double) * od);             // z
+    off[r * 9 + 1] = plan.add(sizeof(double) * od);             // Y (projection sketch)
+    off[r * 9 + 2] = plan.add(sizeof(double) * (mt + 1));       // C
+    off[r * 9 + 3] = plan.add(sizeof(double) * (mt + 1));       // cq
+    off[r * 9 + 4] = plan.add(sizeof(double) * 2);              // fs
+    off[r * 9 + 5] = plan.add(sizeof(double) * pl);             // payload
+    off[r * 9 + 6] = plan.add(sizeof(T) * (seg + 2 * VN));      // w
+    off[r * 9 + 7] = plan.add(sizeof(T) * (seg + 2 * VN));      // q
+    off[r * 9 + 8] = plan.add(sizeof(A) * ell * tpr);           // leaves
+  }
+  const size_t iGq = plan.add(sizeof(T) * nranks * seg);
+  const size_t iGs = plan.add(sizeof(double) * nranks * pl);
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  char* base = static_cast<char*>(ctx->ws);
+  for (int r = 0; r < L; ++r) {
+    ArnRank& d = rk[r];
+    d.z = (double*)(base + plan.offs[off[r * 9 + 0]]);
+    d.Y = (double*)(base + plan.offs[off[r * 9 + 1]]);
+    d.C = (double*)(base + plan.offs[off[r * 9 + 2]]);
+    d.cq = (double*)(base + plan.offs[off[r * 9 + 3]]);
+    d.fs = (double*)(base + plan.offs[off[r * 9 + 4]]);
+    d.pay = (double*)(base + plan.offs[off[r * 9 + 5]]);
+    // w, q: the Omega rows (local row mrow) start 16-byte aligned
+    const int shift = (int)((VN - d.mrow % VN) % VN);
+    d.w = (T*)(base + plan.offs[off[r * 9 + 6]]) + shift;
+    d.q = (T*)(base + plan.offs[off[r * 9 + 7]]) + shift;
+    d.P = base + plan.offs[off[r * 9 + 8]];
+  }
+  T* Gq = (T*)(base + plan.offs[iGq]);
+  double* Gs = (double*)(base + plan.offs[iGs]);
+  Status* st = ctx->d_status;
+  double scale_lo = 0.0, norm_lo = 0.0;
+  srht_constants(sk, Lo<T>::code, &scale_lo, &norm_lo);
+
+  // Psi (local rows of) v for every rank -> out[r] (od): local subtrees, one
+  // all-gather, rank-order combine
+  auto sketch_all = [&](void* ArnRank::*vsel, double* ArnRank::*osel) -> int {
+    std::vector<const void*> send(L);
+    for (int r = 0; r < L; ++r) {
+      ArnRank& d = rk[r];
+      const T* v = (const T*)(d.*vsel);
+      const int64_t n_local = d.rows - d.mrow;
+      SrhtGeom gl{g.log_tb, tpr, (n_local + tb - 1) / tb};
+      if (n_local > 0) SQB_TRY(launch_srht_tiles_geom(ctx, sk, Lo<T>::code, gl, n_local, d.e_base, v + d.mrow,
+                                                      n_local, 1, d.P, st));
+      else SQB_CUDA_TRY(cudaMemsetAsync(d.P, 0, sizeof(A) * ell * tpr, ctx->stream));
+      SQB_TRY(launch_srht_tree_geom(ctx, sk, Lo<T>::code, gl, d.P, 1, d.pay, pl, 0, 0, st));
+      if (d.mrow > 0) SQB_TRY(launch_copy_top(ctx, Lo<T>::code, v, d.rows, mt, 1, d.pay + ell, pl, st));
+      send[r] = d.pay;
+    }
+    SQB_TRY(dist_allgather(ctx, virt, ids, send, sizeof(double) * pl, Gs));
+    for (int r = 0; r < L; ++r) {
+      rank_combine_kernel<T><<<dim3((unsigned)((od + 255) / 256), 1), 256, 0, ctx->stream>>>(
+          Gs, nranks, (int)ell, mt, 1, rank_level, sk->indices, g.log_tb, norm_lo, rk[r].*osel, od, st);
+      SQB_TRY(check_launch(ctx, "rank_combine_kernel"));
+    }
+    return SQB_OK;
+  };
+  auto gather_T = [&](void* ArnRank::*sel) -> int {
+    std::vector<const void*> send(L);
+    for (int r = 0; r < L; ++r) send[r] = rk[r].*sel;
+    return dist_allgather(ctx, virt, ids, send, sizeof(T) * seg, Gq);
+  };
+  auto spmv = [&](ArnRank& d, const double* bsub) -> int {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((d.rows + 255) / 256, 16 * 148));
+    csr_spmv_kernel<T><<<grid, 256, 0, ctx->stream>>>(d.rows, d.indptr, d.indices, d.data, Gq, bsub, (T*)d.w,
+                                                      nullptr, st);
+    return check_launch(ctx, "csr_spmv_kernel");
+  };
+
+  // w = lo(b - A lo(x0)); z = Psi w  (krylov.py:111-112)
+  for (int r = 0; r < L; ++r) {
+    ArnRank& d = rk[r];
+    SQB_CUDA_TRY(cudaMemsetAsync(d.T, 0, sizeof(double) * d.ldt * mt, ctx->stream));
+    SQB_CUDA_TRY(cudaMemsetAsync(d.H, 0, sizeof(double) * d.ldh * m, ctx->stream));
+    SQB_CUDA_TRY(cudaMemsetAsync(d.beta, 0, sizeof(double), ctx->stream));
+    SQB_CUDA_TRY(cudaMemcpyAsync(d.q, d.x0lo, sizeof(T) * d.rows, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  SQB_TRY(gather_T(&ArnRank::q));
+  for (int r = 0; r < L; ++r) SQB_TRY(spmv(rk[r], rk[r].b));
+  SQB_TRY(sketch_all(&ArnRank::w, &ArnRank::z));
+  const size_t step_smem = sizeof(double) * (od + mt + 32);
+  cudaFuncSetAttribute(arn_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(step_smem, 48 << 10));
+  for (int j = 1; j <= mt; ++j) {
+    for (int r = 0; r < L; ++r) {
+      ArnRank& d = rk[r];
+      T* uj = (T*)d.U + (int64_t)(j - 1) * d.ldu;
+      if (d.rows > d.mrow)
+        SQB_CUDA_TRY(cudaMemcpyAsync(uj + d.mrow, (T*)d.w + d.mrow, sizeof(T) * (d.rows - d.mrow),
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+      ArnArgs aa{j, m, mt, (int)od, scaling, happy_tol, d.z, d.S, d.lds, d.T, d.ldt, d.H, d.ldh, d.Utop, d.ldutop,
+                 d.beta, d.fs, d.cq, st};
+      arn_step_kernel<T><<<1, ARN_NT, step_smem, ctx->stream>>>(aa);
+      SQB_TRY(check_launch(ctx, "arn_step_kernel"));
+      if (j > m) {
+        const unsigned gq = (unsigned)std::max<int64_t>(1, std::min<int64_t>((d.rows / VN + 255) / 256, 4 * 148));
+        scale_col_kernel<T><<<gq, 256, 0, ctx->stream>>>(uj, d.rows, d.mrow, d.fs, scaling, st);
+        SQB_TRY(check_launch(ctx, "scale_col_kernel"));
+      }
+    }
+    if (j > m) break;
+    for (int r = 0; r < L; ++r) {
+      ArnRank& d = rk[r];
+      const unsigned gg = (unsigned)std::max<int64_t>(
+          1, std::min<int64_t>((d.rows + (int64_t)GEMV_NT * 4 * VN - 1) / ((int64_t)GEMV_NT * 4 * VN),
+                               2 * (int64_t)ctx->sm_count));
+      double* Qj = d.Q ? d.Q + (int64_t)(j - 1) * d.ldq : nullptr;
+      arn_q_kernel<T><<<gg, GEMV_NT, sizeof(double) * (mt + 1), ctx->stream>>>(
+          d.rows, d.mrow, j, (T*)d.U, d.ldu, d.cq, d.fs, scaling, (T*)d.q, Qj, st, d.row0);
+      SQB_TRY(check_launch(ctx, "arn_q_kernel"));
+    }
+    // w = lo(A lo(q))  (krylov.py:140)
+    SQB_TRY(gather_T(&ArnRank::q));
+    for (int r = 0; r < L; ++r) SQB_TRY(spmv(rk[r], nullptr));
+    // w = (I - U_j T_j^t S_j^t Psi) w  (krylov.py:141-142)
+    SQB_TRY(sketch_all(&ArnRank::w, &ArnRank::Y));
+    for (int r = 0; r < L; ++r) {
+      ArnRank& d = rk[r];
+      SQB_TRY(compact_update_dispatch(ctx, Lo<T>::code, d.Y, od, d.S, d.lds, d.T, d.ldt, 1, j, d.U, d.ldu, d.rows,
+                                      d.w, d.w, d.C));
+    }
+    // z = Psi w  (krylov.py:143)
+    SQB_TRY(sketch_all(&ArnRank::w, &ArnRank::z));
+  }
+  SQB_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(Status), cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  const Status hs = *ctx->h_status;
+  if (hs.code == SQB_CLOSED) {
+    *attained = hs.col;
+    SQB_CUDA_TRY(cudaMemsetAsync(ctx->d_status, 0, sizeof(Status), ctx->stream));
+  } else {
+    *attained = -1;
+  }
+  return SQB_OK;
+}
+
+static int arnoldi_dist_entry(sqb_ctx* ctx, const sqb_sketch* sk, int m, int scaling, int lo_dtype, double happy_tol,
+                              std::vector<ArnRank>& rk, int nranks, bool virt, const std::vector<int>& ids,
+                              int64_t seg, int* attained) {
+  SQB_TRY(validate_sketch(ctx, sk));
+  if (sk->kind != SQB_SKETCH_SRHT) return set_error(ctx, SQB_ERR_ARG, "the row-partitioned Arnoldi needs an SRHT");
+  if (m < 1) return set_error(ctx, SQB_ERR_ARG, "need m >= 1");
+  if (sk->ell < m + 1) return set_error(ctx, SQB_ERR_ARG, "sampling size below column count");
+  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
+    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
+  if (nranks < 1 || nranks > 8 || (nranks & (nranks - 1)))
+    return set_error(ctx, SQB_ERR_ARG, "nranks must be a power of two <= 8");
+  const int64_t span = sk->n_pad / nranks;
+  for (auto& d : rk) {
+    if (d.rows > seg) return set_error(ctx, SQB_ERR_ARG, "local rows exceed the gather segment");
+    if (d.mrow == 0 && d.rows > span) return set_error(ctx, SQB_ERR_ARG, "local rows exceed the Omega span");
+  }
+  switch (lo_dtype) {
+    case SQB_F64: return arnoldi_dist_t<double>(ctx, sk, m, scaling, happy_tol, rk, nranks, virt, ids, seg, attained);
+    case SQB_F32: return arnoldi_dist_t<float>(ctx, sk, m, scaling, happy_tol, rk, nranks, virt, ids, seg, attained);
+    case SQB_F16: return arnoldi_dist_t<__half>(ctx, sk, m, scaling, happy_tol, rk, nranks, virt, ids, seg, attained);
+    case SQB_BF16:
+      return arnoldi_dist_t<__nv_bfloat16>(ctx, sk, m, scaling, happy_tol, rk, nranks, virt, ids, seg, attained);
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
 }  // namespace sqb
 
 using namespace sqb;
@@ -498,4 +712,66 @@ extern "C" int sqb_csr_spmv(sqb_ctx* ctx, int dtype, int64_t n, const int64_t* i
     default: return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", dtype);
   }
   return check_launch(ctx, "csr_spmv_kernel");
+}
+
+// Row-partitioned RHQR-Arnoldi, one process per GPU (NCCL communicator from
+// sqb_ctx_init_comm).  This rank's rows: `rows` consecutive global rows
+// starting at row0 (rank 0: the m+1 identity rows and its Omega rows; rank p:
+// the Omega coordinates [p n_pad/P, ...)).  CSR: the local rows with column
+// indices remapped to the gathered layout [rank][seg] (global row g of rank
+// q at q*seg + (g - row0_q)).  Utop: (m+1) x (m+1) scratch on ranks > 0.
+extern "C" int sqb_rhqr_arnoldi_dist(sqb_ctx* ctx, const sqb_sketch* sk, int m, int scaling, int lo_dtype,
+                                     double happy_tol, int64_t rows, int64_t row0, int64_t seg,
+                                     const int64_t* indptr, const int32_t* indices, const double* data,
+                                     const double* b, const void* x0lo, void* U, int64_t ldu, double* S,
+                                     int64_t lds, double* T, int64_t ldt, double* H, int64_t ldh, double* Q,
+                                     int64_t ldq, double* beta, void* Utop, int* attained) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  std::vector<ArnRank> rk(1);
+  ArnRank& d = rk[0];
+  d = ArnRank{};
+  const int mt = m + 1;
+  d.rows = rows; d.row0 = row0; d.mrow = ctx->rank == 0 ? mt : 0;
+  d.e_base = ctx->rank == 0 ? 0 : row0 - mt;
+  d.indptr = indptr; d.indices = indices; d.data = data; d.b = b; d.x0lo = x0lo;
+  d.U = U; d.ldu = ldu; d.Q = Q; d.ldq = ldq; d.S = S; d.lds = lds; d.T = T; d.ldt = ldt; d.H = H; d.ldh = ldh;
+  d.beta = beta;
+  d.Utop = ctx->rank == 0 ? U : Utop;
+  d.ldutop = ctx->rank == 0 ? ldu : mt;
+  if (!d.Utop) return set_error(ctx, SQB_ERR_ARG, "ranks > 0 need an (m+1) x (m+1) Utop scratch");
+  return arnoldi_dist_entry(ctx, sk, m, scaling, lo_dtype, happy_tol, rk, ctx->nranks, false,
+                            std::vector<int>{ctx->rank}, seg, attained);
+}
+
+// The same with P virtual ranks on one device (the all-gathers become device
+// copies); per-rank arrays of length P; outputs S/T/H/beta of rank p in
+// S_parts[p] etc. (every rank computes them redundantly).
+extern "C" int sqb_rhqr_arnoldi_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int m, int scaling, int lo_dtype,
+                                        double happy_tol, int nranks, const int64_t* rows, const int64_t* row0,
+                                        int64_t seg, const int64_t* const* indptr, const int32_t* const* indices,
+                                        const double* const* data, const double* const* b,
+                                        const void* const* x0lo, void* const* U, const int64_t* ldu,
+                                        double* const* S, int64_t lds, double* const* T, int64_t ldt,
+                                        double* const* H, int64_t ldh, double* const* beta,
+                                        void* const* Utop, int* attained) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  const int mt = m + 1;
+  std::vector<ArnRank> rk(nranks);
+  std::vector<int> ids(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    ArnRank& d = rk[r];
+    d = ArnRank{};
+    ids[r] = r;
+    d.rows = rows[r]; d.row0 = row0[r]; d.mrow = r == 0 ? mt : 0; d.e_base = r == 0 ? 0 : row0[r] - mt;
+    d.indptr = indptr[r]; d.indices = indices[r]; d.data = data[r]; d.b = b[r]; d.x0lo = x0lo[r];
+    d.U = U[r]; d.ldu = ldu[r]; d.Q = nullptr; d.ldq = 1;
+    d.S = S[r]; d.lds = lds; d.T = T[r]; d.ldt = ldt; d.H = H[r]; d.ldh = ldh; d.beta = beta[r];
+    d.Utop = r == 0 ? U[0] : Utop[r];
+    d.ldutop = r == 0 ? ldu[0] : mt;
+  }
+  return arnoldi_dist_entry(ctx, sk, m, scaling, lo_dtype, happy_tol, rk, nranks, true, ids, seg, attained);
 }

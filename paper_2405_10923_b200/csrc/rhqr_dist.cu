@@ -14,76 +14,12 @@
 // The exchange is either NCCL (one process per GPU, sqb_ctx_init_comm) or, for
 // testing on a single GPU, "virtual ranks": all ranks' row blocks on one device,
 // the all-gather a set of device copies.
-#include <dlfcn.h>
-#include <nccl.h>
-
 #include <vector>
 
+#include "dist_common.cuh"
 #include "rhqr_kernels.cuh"
 
 namespace sqb {
-
-// ---------------------------------------------------------------------------
-// NCCL, loaded lazily (single-GPU users never need it)
-// ---------------------------------------------------------------------------
-struct NcclApi {
-  void* h = nullptr;
-  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
-  const char* (*getErrorString)(ncclResult_t) = nullptr;
-};
-
-static NcclApi* nccl_api() {
-  static NcclApi api;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-    if (h) {
-      api.h = h;
-      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
-      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
-      api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
-      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
-      api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
-    }
-  }
-  return (api.getUniqueId && api.commInitRank && api.allGather) ? &api : nullptr;
-}
-
-// ---------------------------------------------------------------------------
-// combine the gathered raw-sketch partials: Y0[row, col] (od x m)
-// ---------------------------------------------------------------------------
-template <typename T>
-__global__ void rank_combine_kernel(const double* __restrict__ G, int nranks, int ell, int m, int rank_level,
-                                    const int64_t* __restrict__ idx, int log_tb, double norm_lo,
-                                    double* __restrict__ Y0, int64_t ldy, const Status* st) {
-  using A = typename Lo<T>::acc;
-  if (failed(st)) return;
-  const int pl = ell + m;
-  const int col = blockIdx.y;
-  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < m + ell; row += gridDim.x * blockDim.x) {
-    double y;
-    if (row < m) {
-      y = G[(int64_t)col * pl + ell + row];  // rank 0's slot
-    } else {
-      const int o = row - m;
-      const int64_t rhi = __ldg(idx + o) >> log_tb;
-      A v[8];
-      for (int q = 0; q < nranks; ++q) v[q] = (A)G[((int64_t)q * m + col) * pl + o];
-      int lvl = rank_level;
-      for (int w = 1; w < nranks; w <<= 1, ++lvl) {
-        const bool neg = (rhi >> lvl) & 1;
-        for (int q = 0; q + w < nranks; q += 2 * w) v[q] = neg ? Lo<T>::sub(v[q], v[q + w]) : Lo<T>::add(v[q], v[q + w]);
-      }
-      y = (double)Lo<T>::mul(v[0], (A)norm_lo);
-    }
-    Y0[row + (int64_t)col * ldy] = y;
-  }
-}
 
 struct DistRank {
   const void* W; int64_t ldw;
@@ -183,7 +119,7 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
   SQB_TRY(exchange([](DistRank& d) { return d.Y0pay; }, (size_t)m * od, G0));
   {
     dim3 grid((unsigned)((od + 255) / 256), (unsigned)m);
-    rank_combine_kernel<T><<<grid, 256, 0, ctx->stream>>>(G0, nranks, (int)ell, (int)m, rank_level, sk->indices,
+    rank_combine_kernel<T><<<grid, 256, 0, ctx->stream>>>(G0, nranks, (int)ell, (int)m, (int)m, rank_level, sk->indices,
                                                           g.log_tb, norm_lo, Y0, od, st);
     SQB_TRY(check_launch(ctx, "rank_combine_kernel"));
   }
@@ -332,7 +268,7 @@ static int rec_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t m
   }
   {
     dim3 grid((unsigned)((od + 255) / 256), (unsigned)m);
-    rank_combine_kernel<T><<<grid, 256, 0, ctx->stream>>>(G0, nranks, (int)ell, (int)m, rank_level, sk->indices,
+    rank_combine_kernel<T><<<grid, 256, 0, ctx->stream>>>(G0, nranks, (int)ell, (int)m, (int)m, rank_level, sk->indices,
                                                           g.log_tb, norm_lo, Z, od, st);
     SQB_TRY(check_launch(ctx, "rank_combine_kernel"));
   }

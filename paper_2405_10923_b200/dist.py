@@ -173,3 +173,213 @@ def _virtual(entry, W, omega, nranks, scaling, policy):
 
 
 _ = to_numpy
+
+
+# ---------------------------------------------------------------- RHQR-Arnoldi / GMRES
+def krylov_partition(n: int, m: int, n_pad: int, nranks: int, tag: str = "double"):
+    """Row ranges of the row-partitioned Arnoldi: rank 0 owns the m+1
+    identity-block rows and its Omega coordinates, rank p > 0 the Omega
+    coordinates [p span, (p+1) span) — each a contiguous range [row0, row0+rows).
+    Returns (row0s, rows, seg) with seg = the per-rank slot of the gathered
+    vectors (m+1+span)."""
+    mt = m + 1
+    span = omega_span(n_pad, nranks, tag)
+    row0s, rows = [], []
+    for p in range(nranks):
+        r = local_rows(n, mt, n_pad, nranks, p, tag)
+        row0s.append(int(r[0]) if len(r) else n)
+        rows.append(len(r))
+    return row0s, rows, mt + span
+
+
+def _gather_positions(cols: np.ndarray, m: int, span: int, seg: int) -> np.ndarray:
+    """Global vector index -> position in the gathered [rank][seg] layout."""
+    mt = m + 1
+    cols = np.asarray(cols, dtype=np.int64)
+    e = cols - mt
+    q = np.where(cols < mt + span, 0, e // span)
+    local = np.where(q == 0, cols, e - q * span)
+    return q * seg + local
+
+
+def local_operator_host(A, m: int, n_pad: int, nranks: int, rank: int, tag: str = "double"):
+    """This rank's CSR rows of a global scipy sparse A with the column
+    indices remapped to the gathered layout (host arrays): (indptr int64,
+    indices int32, data float64, row0, rows, seg)."""
+    import scipy.sparse
+    A = scipy.sparse.csr_matrix(A)
+    A.sort_indices()
+    n = A.shape[0]
+    row0s, rows, seg = krylov_partition(n, m, n_pad, nranks, tag)
+    r0, nr = row0s[rank], rows[rank]
+    B = A[r0:r0 + nr]
+    span = omega_span(n_pad, nranks, tag)
+    idx = _gather_positions(B.indices, m, span, seg).astype(np.int32)
+    return B.indptr.astype(np.int64), idx, B.data.astype(np.float64), r0, nr, seg
+
+
+def gather_layout(x, m: int, n_pad: int, nranks: int, tag: str = "double"):
+    """A global vector in the gathered [rank][seg] layout (what the per-step
+    all-gather of q produces on every rank)."""
+    n = len(x)
+    row0s, rows, seg = krylov_partition(n, m, n_pad, nranks, tag)
+    out = np.zeros(nranks * seg, dtype=np.asarray(x).dtype)
+    for p in range(nranks):
+        out[p * seg:p * seg + rows[p]] = x[row0s[p]:row0s[p] + rows[p]]
+    return out
+
+
+def local_operator(A, m: int, n_pad: int, nranks: int, rank: int, tag: str = "double"):
+    """local_operator_host, uploaded (what sqb_rhqr_arnoldi_dist expects)."""
+    ip, ix, dv, r0, nr, seg = local_operator_host(A, m, n_pad, nranks, rank, tag)
+    return (torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda(), torch.from_numpy(dv).cuda(), r0, nr, seg)
+
+
+def _arnoldi_bufs(rows, mrow, m, od, tag, x0_local):
+    mt = m + 1
+    # U is streamed from local row 0 by the GEMVs (16-byte aligned there)
+    return dict(U=empty_colmajor(max(rows, 1), mt, tag), S=empty_colmajor(od, mt, "double"),
+                T=empty_colmajor(mt, mt, "double"), H=empty_colmajor(mt, m, "double"),
+                beta=torch.zeros(1, dtype=torch.float64, device="cuda"),
+                Utop=empty_colmajor(mt, mt, tag), x0=to_device(x0_local, tag))
+
+
+def rhqr_arnoldi_virtual(A, b, x0, m, omega, nranks, scaling=SCALE_SQRT2, policy=None, happy_tol=None):
+    """The row-partitioned RHQR-Arnoldi with `nranks` virtual ranks on one
+    device; returns rank 0's sketch-space factors (bitwise those of one GPU)
+    and U reassembled in global row order."""
+    from .krylov import KrylovBundle
+    check_scaling(scaling)
+    policy = policy or DOUBLE_POLICY
+    require_device_policy(policy)
+    tag = policy.low
+    b = np.asarray(b, dtype=np.float64)
+    n = b.shape[0]
+    x0 = np.zeros(n) if x0 is None else np.asarray(x0, dtype=np.float64)
+    mt = m + 1
+    psi = _embed(omega, n, mt)
+    od = psi.out_dim
+    happy_tol = 32.0 * policy.u_high if happy_tol is None else happy_tol
+    row0s, rows, seg = krylov_partition(n, m, omega.n_pad, nranks, tag)
+    keep, bufs = [], []
+    for p in range(nranks):
+        ip, ix, dv, r0, nr, _ = local_operator(A, m, omega.n_pad, nranks, p, tag)
+        bl = torch.from_numpy(b[r0:r0 + nr].copy()).cuda() if nr else torch.zeros(1, dtype=torch.float64, device="cuda")
+        bf = _arnoldi_bufs(nr, mt if p == 0 else 0, m, od, tag, x0[r0:r0 + nr] if nr else np.zeros(1))
+        keep += [ip, ix, dv, bl]
+        bufs.append((ip, ix, dv, bl, bf))
+    P_ = nranks
+    arr = lambda ctype, xs: (ctype * P_)(*xs)  # noqa: E731
+    attained = C.c_int(-1)
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_rhqr_arnoldi_virtual(
+        ctx.h, omega.desc(), m, scaling_code(scaling), CODES[tag], float(happy_tol), P_,
+        arr(C.c_int64, rows), arr(C.c_int64, row0s), seg,
+        arr(C.c_void_p, [x[0].data_ptr() for x in bufs]), arr(C.c_void_p, [x[1].data_ptr() for x in bufs]),
+        arr(C.c_void_p, [x[2].data_ptr() for x in bufs]), arr(C.c_void_p, [x[3].data_ptr() for x in bufs]),
+        arr(C.c_void_p, [x[4]["x0"].data_ptr() for x in bufs]), arr(C.c_void_p, [x[4]["U"].data_ptr() for x in bufs]),
+        arr(C.c_int64, [ld_of(x[4]["U"]) for x in bufs]), arr(C.c_void_p, [x[4]["S"].data_ptr() for x in bufs]),
+        ld_of(bufs[0][4]["S"]), arr(C.c_void_p, [x[4]["T"].data_ptr() for x in bufs]), ld_of(bufs[0][4]["T"]),
+        arr(C.c_void_p, [x[4]["H"].data_ptr() for x in bufs]), ld_of(bufs[0][4]["H"]),
+        arr(C.c_void_p, [x[4]["beta"].data_ptr() for x in bufs]),
+        arr(C.c_void_p, [x[4]["Utop"].data_ptr() for x in bufs]), C.byref(attained)), "sqb_rhqr_arnoldi_virtual")
+    raise_status(ctx, "rhqr_arnoldi")
+    closed = None if attained.value < 0 else attained.value
+    k = m if closed is None else closed
+    r = mt if closed is None else closed
+    U = empty_colmajor(n, mt, tag)
+    for p, (_, _, _, _, bf) in enumerate(bufs):
+        if rows[p]:
+            U[row0s[p]:row0s[p] + rows[p]] = bf["U"][: rows[p]]
+    b0 = bufs[0][4]
+    return KrylovBundle(U=to_numpy(U[:, :r]), S=to_numpy(b0["S"][:, :r]), T=to_numpy(b0["T"][:r, :r]),
+                        H=to_numpy(b0["H"][: k + 1, :k]), psi=psi, beta=float(b0["beta"].item()), scaling=scaling,
+                        Q_cols=None, breakdown=closed)
+
+
+def rhqr_arnoldi_distributed(A_local, b_local, x0_local, m, omega, n, scaling=SCALE_SQRT2, policy=None,
+                             happy_tol=None):
+    """This rank's part of rhqr_arnoldi (krylov.py:82-150) on the row
+    partition (one process per GPU, NCCL).  A_local = local_operator(...)
+    output; b_local / x0_local are this rank's rows.  Returns a KrylovBundle
+    whose U holds the local rows; S, T, H, beta are replicated."""
+    import torch.distributed as dist
+    from .krylov import KrylovBundle
+    check_scaling(scaling)
+    policy = policy or DOUBLE_POLICY
+    require_device_policy(policy)
+    tag = policy.low
+    rank = dist.get_rank()
+    ip, ix, dv, r0, nr, seg = A_local
+    mt = m + 1
+    psi = _embed(omega, n, mt)
+    od = psi.out_dim
+    happy_tol = 32.0 * policy.u_high if happy_tol is None else happy_tol
+    bl = to_device(b_local, "double")[:, 0]
+    bf = _arnoldi_bufs(nr, mt if rank == 0 else 0, m, od, tag,
+                       x0_local if x0_local is not None else np.zeros(max(nr, 1)))
+    attained = C.c_int(-1)
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_rhqr_arnoldi_dist(
+        ctx.h, omega.desc(), m, scaling_code(scaling), CODES[tag], float(happy_tol), nr, r0, seg, ip.data_ptr(),
+        ix.data_ptr(), dv.data_ptr(), bl.data_ptr(), bf["x0"].data_ptr(), bf["U"].data_ptr(), ld_of(bf["U"]),
+        bf["S"].data_ptr(), ld_of(bf["S"]), bf["T"].data_ptr(), ld_of(bf["T"]), bf["H"].data_ptr(), ld_of(bf["H"]),
+        None, 1, bf["beta"].data_ptr(), bf["Utop"].data_ptr(), C.byref(attained)), "sqb_rhqr_arnoldi_dist")
+    raise_status(ctx, "rhqr_arnoldi")
+    closed = None if attained.value < 0 else attained.value
+    k = m if closed is None else closed
+    r = mt if closed is None else closed
+    return KrylovBundle(U=bf["U"][:nr, :r], S=bf["S"][:, :r], T=bf["T"][:r, :r], H=bf["H"][: k + 1, :k], psi=psi,
+                        beta=float(bf["beta"].item()), scaling=scaling, Q_cols=None, breakdown=closed)
+
+
+def gmres_solution_local(bundle, y, x0_local, rank, policy=None):
+    """x_local = x0_local + this rank's rows of the compact-form correction
+    (krylov.py:214-222).  The padded coefficient vector lives in the identity
+    rows (rank 0), so Psi pad = [pad[:m+1]; 0] is known on every rank without
+    communication (an SRHT of zeros is +0); each rank updates its own rows
+    (sqb_compact_update)."""
+    policy = policy or DOUBLE_POLICY
+    tag = policy.low
+    k = bundle.dim
+    x0d = to_device(x0_local, "double")[:, 0]
+    if k == 0:
+        return x0d.clone()
+    U = to_device(bundle.U[:, :k], tag)
+    rows = U.shape[0]
+    od = bundle.S.shape[0]
+    yv = torch.as_tensor(y, device="cuda", dtype=torch.float64).reshape(-1)[:k]
+    Y = torch.zeros(od, dtype=torch.float64, device="cuda")
+    Y[:k] = yv  # Psi pad, top block: a bitwise copy of pad[:m+1]
+    X = empty_colmajor(rows, 1, tag, zero=True)
+    if rank == 0:
+        X[:k, 0] = yv.to(X.dtype)
+    Out = empty_colmajor(rows, 1, tag)
+    S = to_device(bundle.S[:, :k], "double")
+    T = to_device(bundle.T[:k, :k], "double")
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_compact_update(ctx.h, CODES[tag], Y.data_ptr(), od, S.data_ptr(), ld_of(S),
+                                            T.data_ptr(), ld_of(T), 0, k, U.data_ptr(), ld_of(U), rows,
+                                            X.data_ptr(), Out.data_ptr()), "sqb_compact_update")
+    return x0d + Out[:, 0].to(torch.float64)
+
+
+def rhqr_gmres_virtual(A, b, x0, m, omega, nranks, scaling=SCALE_SQRT2, policy=None):
+    """rhqr_gmres (krylov.py:193-222) on the row-partitioned Arnoldi with
+    virtual ranks: each rank's solution rows from its own U rows."""
+    from .krylov import hessenberg_lstsq
+    b = np.asarray(b, dtype=np.float64)
+    n = b.shape[0]
+    x0 = np.zeros(n) if x0 is None else np.asarray(x0, dtype=np.float64)
+    bun = rhqr_arnoldi_virtual(A, b, x0, m, omega, nranks, scaling=scaling, policy=policy)
+    y, _, hist = hessenberg_lstsq(bun.H, bun.beta, history=True)
+    tag = (policy or DOUBLE_POLICY).low
+    row0s, rows, _ = krylov_partition(n, m, omega.n_pad, nranks, tag)
+    x = np.empty(n)
+    for p in range(nranks):
+        if not rows[p]:
+            continue
+        sl = slice(row0s[p], row0s[p] + rows[p])
+        part = type(bun)(U=bun.U[sl], S=bun.S, T=bun.T, H=bun.H, psi=bun.psi, beta=bun.beta, scaling=bun.scaling)
+        x[sl] = to_numpy(gmres_solution_local(part, y, x0[sl], p, policy))
+    return x, hist

@@ -119,3 +119,67 @@ def test_four_rank_model_bitwise():
         w <<= 1
         lvl += 1
     assert np.array_equal(vals[0] * (op.n_pad ** -0.5), op.apply(x))
+
+
+# ---------------------------------------------------------------- row-partitioned Arnoldi (host logic)
+def _cd_matrix(k):
+    import scipy.sparse
+    from paper_2405_10923_b200.workloads import convection_diffusion_csr
+    ip, ix, dv = convection_diffusion_csr(k)
+    return scipy.sparse.csr_matrix((dv, ix, ip), shape=(k * k, k * k))
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_krylov_partition_and_remapped_spmv(P):
+    from paper_2405_10923_b200.dist import gather_layout, krylov_partition, local_operator_host
+    import scipy.sparse
+    k, m = 192, 20
+    A = _cd_matrix(k)
+    n = k * k
+    n_pad = 1 << (n - m - 2).bit_length()
+    row0s, rows, seg = krylov_partition(n, m, n_pad, P)
+    assert row0s[0] == 0 and sum(rows) == n
+    for p in range(1, P):
+        if rows[p]:
+            assert row0s[p] == row0s[p - 1] + rows[p - 1]  # contiguous ranges, in rank order
+    x = np.random.default_rng(P).standard_normal(n)
+    xg = gather_layout(x, m, n_pad, P)
+    y = A @ x
+    for p in range(P):
+        ip, ix, dv, r0, nr, sg = local_operator_host(A, m, n_pad, P, p)
+        B = scipy.sparse.csr_matrix((dv, ix, ip), shape=(nr, P * sg))
+        assert np.array_equal(B @ xg, y[r0:r0 + nr])  # same CSR row order -> bitwise
+
+
+def _gmres_worker(rank, world, port, out):
+    """world_size-2 gloo model of the per-step exchange of the row-partitioned
+    Arnoldi: all-gather of the local q rows into the [rank][seg] layout, local
+    CSR rows times the gathered vector."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2405_10923_b200.dist import krylov_partition, local_operator_host
+    import scipy.sparse
+    k, m = 128, 12
+    A = _cd_matrix(k)
+    n = k * k
+    n_pad = 1 << (n - m - 2).bit_length()
+    row0s, rows, seg = krylov_partition(n, m, n_pad, world)
+    x = np.random.default_rng(0).standard_normal(n)
+    mine = np.zeros(seg)
+    mine[:rows[rank]] = x[row0s[rank]:row0s[rank] + rows[rank]]
+    parts = [torch.zeros(seg, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(parts, torch.from_numpy(mine))
+    xg = torch.cat(parts).numpy()
+    ip, ix, dv, r0, nr, sg = local_operator_host(A, m, n_pad, world, rank)
+    yl = scipy.sparse.csr_matrix((dv, ix, ip), shape=(nr, world * sg)) @ xg
+    out[rank] = bool(np.array_equal(yl, (A @ x)[r0:r0 + nr]))
+    dist.destroy_process_group()
+
+
+def test_gmres_exchange_gloo_world2():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = 29600 + os.getpid() % 300
+    mp.spawn(_gmres_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0] and out[1]

@@ -473,6 +473,30 @@ def test_row_partitioned_rec_rhqr(P, nranks, m):
     assert rel(Fv.R, Fo.R) < 1e-10
 
 
+@pytest.mark.parametrize("nranks", [1, 2, 4, 8])
+def test_row_partitioned_arnoldi_bitwise(P, nranks):
+    """Row-partitioned RHQR-Arnoldi (q all-gather for the SpMV, two sketch
+    all-gathers per step, rank-order combine) on virtual ranks: H, S, T,
+    beta and U are bitwise the single-GPU run; GMRES matches to rounding."""
+    import scipy.sparse
+    from paper_2405_10923_b200 import dist
+    k, m = 192, 20
+    ip, ix, dv = workloads.convection_diffusion_csr(k)
+    n = k * k
+    A = scipy.sparse.csr_matrix((dv, ix, ip), shape=(n, n))
+    b = np.random.default_rng(nranks).standard_normal(n)
+    om = P.SRHTSketch(4 * (m + 1), n - m - 1, 23)
+    b1 = P.rhqr_arnoldi(A, b, None, m, om)
+    bv = dist.rhqr_arnoldi_virtual(A, b, None, m, om, nranks)
+    assert bv.breakdown == b1.breakdown and bv.beta == b1.beta
+    for key in ("H", "S", "T", "U"):
+        assert np.array_equal(getattr(bv, key), getattr(b1, key)), key
+    x1, h1 = P.rhqr_gmres(A, b, None, m, om)
+    xv, hv = dist.rhqr_gmres_virtual(A, b, None, m, om, nranks)
+    assert np.array_equal(hv, h1)
+    assert rel(xv, x1) < 1e-14
+
+
 def test_nccl_row_partitioned_single_rank(P):
     """Exercises the real NCCL plumbing of the row-partitioned path (dlopen,
     unique id, communicator, per-column all-gather) with world_size 1."""
@@ -500,6 +524,17 @@ def test_nccl_row_partitioned_single_rank(P):
         for k in ("R", "S", "T"):
             assert np.array_equal(getattr(Fr, k), getattr(Fr1, k)), k
         assert rel(Fr.U, Fr1.U) < 1e-14
+        # row-partitioned Arnoldi through NCCL (world 1)
+        import scipy.sparse
+        kk, mm = 64, 10
+        ip, ix, dv = workloads.convection_diffusion_csr(kk)
+        A = scipy.sparse.csr_matrix((dv, ix, ip), shape=(kk * kk, kk * kk))
+        b = np.random.default_rng(3).standard_normal(kk * kk)
+        oma = P.SRHTSketch(44, kk * kk - mm - 1, 8)
+        Al = D.local_operator(A, mm, oma.n_pad, 1, 0)
+        bd = D.rhqr_arnoldi_distributed(Al, b, None, mm, oma, kk * kk)
+        b1 = P.rhqr_arnoldi(A, b, None, mm, oma)
+        assert np.array_equal(bd.H.cpu().numpy(), b1.H) and np.array_equal(bd.U.cpu().numpy(), b1.U)
     finally:
         if created:
             dist.destroy_process_group()

@@ -8,6 +8,8 @@
 #include "vec.cuh"
 #include "dense.cuh"
 
+#include <cuda.h>
+
 namespace sqb {
 
 // ---------------------------------------------------------------------------
@@ -315,6 +317,296 @@ srht64_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_ef
   cp_async_wait_group<0>();
 }
 
+template <typename T>
+__device__ __forceinline__ void fwht32_regs(T (&v)[32]) {
+#pragma unroll
+  for (int s2 = 0; s2 < 5; ++s2)
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (!(j & (1 << s2))) {
+        const T x = v[j], y = v[j | (1 << s2)];
+        v[j] = Lo<T>::add(x, y);
+        v[j | (1 << s2)] = Lo<T>::sub(x, y);
+      }
+}
+
+template <typename T>
+__host__ __device__ constexpr int wt_rs() { return 32 + 16 / (int)sizeof(T); }  // padded row (elements)
+
+// ---------------------------------------------------------------------------
+// K1 standalone for fp64 / fp32 storage: TMA-staged warp tiles.
+//   * One WARP owns a 4096-coordinate leaf group as four 1024-coordinate
+//     sub-tiles.  A lane holds 32 values, so a sub-tile is two 5-stage
+//     register passes: bits 0-4 on the lane's contiguous run, bits 5-9 after
+//     one warp-private shared-memory transpose (padded rows: conflict-free).
+//   * Stages h = 1024 and 2048 are evaluated only at the sampled coordinates:
+//     output k at in-group position p is (s0 +- s1) +- (s2 +- s3), s_q = the
+//     sub-tile-q value at p mod 1024, signs from bits 10 and 11 of p, lower
+//     operand first — exactly what the full stages compute at p (the identity
+//     the cross-tile tree also uses), so the leaves are bitwise those of the
+//     4096-coordinate tile and the tree kernel is shared.  2/12 fewer
+//     butterflies than the CTA tile kernel.
+//   * Every full sub-tile arrives through the tensor-memory accelerator: a
+//     3-D tensor map (elements of one 128-byte half-run x runs of 32
+//     coordinates x columns), SWIZZLE_128B, one box per half, completion on a
+//     per-stage mbarrier.  Each warp owns an S-stage ring; a stage is
+//     refilled (S sub-tiles ahead) as soon as pass 1 has read it, so HBM
+//     latency is covered by the ring, not by registers, and no global load
+//     crosses the L1 pipe.  Lane l's run is swizzled row l of each half
+//     (chunk c at c ^ (l & 7)): the lane-run reads are conflict-free.
+//   * Warps walk contiguous (column, group) ranges with cursors (no
+//     per-sub-tile division); the tree levels 10/11 are branch-free selects.
+// Measured (B200, 2^20 x 128 fp64, ell = 256; scripts/ab_srht.py): 0.54 ->
+// 0.60 of HBM vs the CTA tile kernel; variants with direct lane-run loads
+// (LDG.128: L1-bound at 98 %; LDG.256: 0.56; register prefetch: 0.51) lost.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Tma {
+  static constexpr int HALF = 128 / (int)sizeof(T);  // elements per swizzled row
+  static constexpr int NH = 32 / HALF;                 // rows (halves) per 32-coordinate run
+  static constexpr int STAGE = 32 * 32 * (int)sizeof(T);  // bytes per sub-tile
+};
+
+// byte offset of run r, element i (0..31) inside a swizzled stage buffer
+template <typename T>
+__device__ __forceinline__ uint32_t tma_off(uint32_t r, uint32_t i) {
+  constexpr int HALF = Tma<T>::HALF;
+  const uint32_t h = i / HALF, c = (i % HALF) * sizeof(T);
+  return h * 4096u + r * 128u + ((((c >> 4) ^ (r & 7u)) << 4) | (c & 15u));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{ .reg .pred P; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1; @!P bra WAIT_%=; }" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T, int KPL, int S, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restrict__ X, int64_t ldx, int64_t n,
+                     int64_t n_eff, int64_t k, const uint32_t* __restrict__ bits, const int64_t* __restrict__ idx,
+                     int ell, T scale_lo, T* __restrict__ P, int64_t n_tiles, const Status* st, int64_t e_base) {
+  static_assert(sizeof(T) == sizeof(typename Lo<T>::acc), "storage = arithmetic type");
+  constexpr int C = 16 / (int)sizeof(T), RS = wt_rs<T>();
+  constexpr uint32_t SB = Tma<T>::STAGE;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  if (st && failed(st)) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // [1024-aligned TMA stages: WPB x S x SB][padded transpose buffers: WPB x 32 x RS][barriers]
+  // (offset from smem_raw itself so the compiler keeps the shared address space)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* stages = base + (size_t)wid * S * SB;
+  T* buf = reinterpret_cast<T*>(base + (size_t)WPB * S * SB) + wid * 32 * RS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + (size_t)WPB * S * SB + sizeof(T) * (size_t)WPB * 32 * RS) + wid * S;
+  if (lane == 0)
+    for (int s = 0; s < S; ++s) mbar_init(bars + s, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  // per output k = lane + 32 i: byte offset of its position p mod 1024 in the
+  // transpose buffer (bits 0-15), bit 10 of p at bit 16, bit 11 at bit 17
+  uint32_t mypk[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int kk = lane + 32 * i;
+    const uint32_t p = kk < ell ? (uint32_t)(__ldg(idx + kk) & 4095) : 0u;
+    mypk[i] = (uint32_t)(((p & 1023u) >> 5) * RS + (p & 31u)) * (uint32_t)sizeof(T) | (((p >> 10) & 3u) << 16);
+  }
+  // each warp owns a contiguous run of (column, group) items, walked by
+  // cursors (no per-unit division): one for the unit being transformed, one
+  // for the unit whose TMA load is issued S units ahead, one for sign words
+  const int64_t items = n_eff * k;
+  const int64_t nwarps = (int64_t)gridDim.x * WPB;
+  const int64_t wg = (int64_t)blockIdx.x * WPB + wid;
+  const int64_t per = (items + nwarps - 1) / nwarps;
+  const int64_t i0 = std::min(items, wg * per), i1 = std::min(items, i0 + per);
+  const int64_t units = (i1 - i0) * 4;  // sub-tiles this warp processes
+  struct Cur {
+    int64_t col, g;
+    int q;
+    __device__ void next(int64_t ne) {
+      if (++q == 4) {
+        q = 0;
+        if (++g == ne) { g = 0; ++col; }
+      }
+    }
+    __device__ int64_t e0() const { return (g << 12) + ((int64_t)q << 10); }
+  };
+  Cur cu{i0 / n_eff, i0 % n_eff, 0};
+  Cur ci = cu, cw = cu;
+  auto issue = [&](int64_t u) {  // lane 0 only; unit u (= cursor ci) is loaded by TMA iff it lies below n
+    const int64_t e0 = ci.e0();
+    if (e0 + 1024 > n) return;
+    const int s = (int)(u % S);
+    uint64_t* b = bars + s;
+    unsigned char* dst = stages + (size_t)s * SB;
+    mbar_expect_tx(b, SB);
+#pragma unroll
+    for (int h = 0; h < Tma<T>::NH; ++h)
+      tma_load_3d(dst + h * 4096, &map, h * Tma<T>::HALF, (int)(e0 >> 5), (int)ci.col, b);
+  };
+  if (lane == 0)
+    for (int64_t u = 0; u < S && u < units; ++u) { issue(u); ci.next(n_eff); }
+  uint32_t phase = 0;  // bit s = parity expected next on stage s
+  uint32_t w_next = units > 0 ? __ldg(bits + ((e_base + cw.e0() + lane * 32) >> 5)) : 0u;
+  cw.next(n_eff);
+  // lane-run reads of a swizzled stage: chunk c of half h at (c ^ (lane & 7))
+  const uint32_t run_base = (uint32_t)lane * 128u, run_x = ((uint32_t)lane & 7u) << 4;
+  T ab[KPL], acc[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) ab[i] = acc[i] = T(0);
+  for (int64_t u = 0; u < units; ++u, cu.next(n_eff)) {
+    const int64_t col = cu.col, e0 = cu.e0();
+    const int q = cu.q;
+    const int s = (int)(u % S);
+    const int64_t e = e0 + lane * 32;
+    const uint32_t w = w_next;
+    if (u + 1 < units) w_next = __ldg(bits + ((e_base + cw.e0() + lane * 32) >> 5));
+    cw.next(n_eff);
+    T v[32];
+    unsigned char* sb = stages + (size_t)s * SB;
+    const bool full = e0 + 1024 <= n;
+    if (full) {
+      mbar_wait(bars + s, (phase >> s) & 1u);
+      phase ^= 1u << s;
+    } else {  // the column tail: stage it by hand in the same swizzled layout
+      const T* x = X + col * ldx;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        *reinterpret_cast<T*>(sb + tma_off<T>(lane, j)) = (e + j < n) ? x[e + j] : T(0);
+      __syncwarp();
+    }
+#pragma unroll
+    for (int c = 0; c < 32 / C; ++c) {
+      const uint32_t h = (uint32_t)(c * C) / Tma<T>::HALF, cc = (uint32_t)(c % (Tma<T>::HALF / C));
+      const uint4 r = *reinterpret_cast<const uint4*>(sb + h * 4096u + run_base + ((cc << 4) ^ run_x));
+      unpack16<T>(r, v + c * C);
+    }
+    // the stage is consumed: refill it with unit u + S
+    __syncwarp();
+    if (lane == 0 && u + S < units) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(u + S);
+      ci.next(n_eff);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = flip_sign(Lo<T>::mul(v[j], scale_lo), w, j);
+    if (e + 32 > n) {  // zero padding past n is +0 (sketching.py:154)
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (e + j >= n) v[j] = T(0);
+    }
+    fwht32_regs<T>(v);  // h = 1..16
+    {
+      T* row = buf + lane * RS;
+#pragma unroll
+      for (int c = 0; c < 32 / C; ++c) vstore<T>(row + c * C, v + c * C);
+    }
+    __syncwarp();
+    // lane-column l holds coordinates l + 32 j; reads and writes stay in the column
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = buf[j * RS + lane];
+    fwht32_regs<T>(v);  // h = 32..512
+#pragma unroll
+    for (int j = 0; j < 32; ++j) buf[j * RS + lane] = v[j];
+    __syncwarp();
+    // tree levels 10 and 11 at the sampled positions, branch-free:
+    // acc = (q odd) ? acc -+ s : s ; ab = acc before sub-tile 2 overwrites it
+    // (x - y is x + (-y) exactly, so the sign bit selects add or sub)
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const uint32_t pk = mypk[i];
+      const T sv = *reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(buf) + (pk & 0xffffu));
+      const T t = Lo<T>::add(acc[i], flip_sign(sv, pk, 16));
+      if (q == 2) ab[i] = acc[i];
+      acc[i] = (q & 1) ? t : sv;
+    }
+    if (q == 3) {
+      T* leaves = P + (col * ell) * n_tiles + (e0 >> 12);
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) {
+        const int kk = lane + 32 * i;
+        if (kk < ell) leaves[(int64_t)kk * n_tiles] = Lo<T>::add(ab[i], flip_sign(acc[i], mypk[i], 17));
+      }
+    }
+    __syncwarp();
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+template <typename T, int KPL, int S, int WPB>
+static int launch_tma(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int64_t n_local, int64_t e_base,
+                      const T* X, int64_t ldx, int64_t k, T sc, T* P, const Status* st) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return set_error(ctx, SQB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  const cuuint64_t runs = (cuuint64_t)(n_local >> 5);
+  const cuuint64_t dims[3] = {(cuuint64_t)Tma<T>::HALF * Tma<T>::NH, std::max<cuuint64_t>(runs, 1), (cuuint64_t)k};
+  const cuuint64_t strides[2] = {32 * sizeof(T), (cuuint64_t)ldx * sizeof(T)};
+  const cuuint32_t box[3] = {(cuuint32_t)Tma<T>::HALF, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                         const_cast<T*>(X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(ctx, SQB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  const size_t smem = 1024 + (size_t)WPB * S * Tma<T>::STAGE + sizeof(T) * (size_t)WPB * 32 * wt_rs<T>() +
+                       (size_t)WPB * S * 8;
+  auto kern = srht_tma_tile_kernel<T, KPL, S, WPB>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem);
+  per_sm = std::max(1, per_sm);
+  const int64_t items = g.n_eff * k;
+  const int64_t ctas =
+      std::max<int64_t>(1, std::min<int64_t>((items + WPB - 1) / WPB, (int64_t)per_sm * ctx->sm_count));
+  kern<<<(unsigned)ctas, WPB * 32, smem, ctx->stream>>>(map, X, ldx, n_local, g.n_eff, k, sk->sign_bits,
+                                                         sk->indices, (int)sk->ell, sc, P, g.n_tiles, st, e_base);
+  return check_launch(ctx, "srht_tma_tile_kernel");
+}
+
+template <typename T, int S, int WPB>
+static int launch_tma_kpl(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int64_t n_local, int64_t e_base,
+                          const T* X, int64_t ldx, int64_t k, T sc, T* P, const Status* st) {
+  const int kpl = (int)((sk->ell + 31) / 32);
+  if (kpl <= 4) return launch_tma<T, 4, S, WPB>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+  if (kpl <= 8) return launch_tma<T, 8, S, WPB>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+  return launch_tma<T, 16, S, WPB>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+}
+
 // ---------------------------------------------------------------------------
 // 16-bit storage (bf16 / fp16): the same two-pass tile kernel on PACKED pairs.
 // Every butterfly op of the reference is one correctly rounded 16-bit op
@@ -545,6 +837,9 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
     }
   }
   if constexpr (sizeof(T) >= 4) {
+    // TMA-staged warp tiles (ell <= 512: the per-lane output registers)
+    if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= 512 && n_local >= 32 && encode_tiled())
+      return launch_tma_kpl<T, 2, 4>(ctx, sk, g, n_local, e_base, (const T*)X, ldx, k, (T)sc, (T*)P, st);
     if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= S64_MAX_ELL) {
       const size_t smem64 = s64_head_bytes((int)sk->ell, sizeof(T)) + s64_buf_bytes<T>();
       cudaFuncSetAttribute(srht64_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64);

@@ -7,8 +7,7 @@
 #include "sketch.cuh"
 #include "vec.cuh"
 #include "dense.cuh"
-
-#include <cuda.h>
+#include "tma.cuh"
 
 namespace sqb {
 
@@ -375,29 +374,6 @@ __device__ __forceinline__ uint32_t tma_off(uint32_t r, uint32_t i) {
   return h * 4096u + r * 128u + ((((c >> 4) ^ (r & 7u)) << 4) | (c & 15u));
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{ .reg .pred P; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1; @!P bra WAIT_%=; }" ::"r"(
-          smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
-
 template <typename T, int KPL, int S, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
 srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restrict__ X, int64_t ldx, int64_t n,
@@ -434,21 +410,26 @@ srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restric
   const int64_t items = n_eff * k;
   const int64_t nwarps = (int64_t)gridDim.x * WPB;
   const int64_t wg = (int64_t)blockIdx.x * WPB + wid;
-  const int64_t per = (items + nwarps - 1) / nwarps;
-  const int64_t i0 = std::min(items, wg * per), i1 = std::min(items, i0 + per);
-  const int64_t units = (i1 - i0) * 4;  // sub-tiles this warp processes
-  struct Cur {
+  // items wg, wg + nwarps, ...: groups processed at the same time are adjacent,
+  // so the 8-byte / 4-byte leaf writes of neighbouring groups meet in L2 and
+  // leave as whole sectors (a contiguous range per warp doubled DRAM writes)
+  const int64_t my_items = wg < items ? (items - wg + nwarps - 1) / nwarps : 0;
+  const int64_t dcol = nwarps / n_eff, dg = nwarps - dcol * n_eff;
+  const int64_t units = my_items * 4;  // sub-tiles this warp processes
+  struct Cur {  // (column, group, sub-tile) of a unit; advance without division
     int64_t col, g;
     int q;
-    __device__ void next(int64_t ne) {
+    __device__ void next(int64_t ne, int64_t dc, int64_t dgg) {
       if (++q == 4) {
         q = 0;
-        if (++g == ne) { g = 0; ++col; }
+        g += dgg;
+        col += dc;
+        if (g >= ne) { g -= ne; ++col; }
       }
     }
     __device__ int64_t e0() const { return (g << 12) + ((int64_t)q << 10); }
   };
-  Cur cu{i0 / n_eff, i0 % n_eff, 0};
+  Cur cu{wg / n_eff, wg % n_eff, 0};
   Cur ci = cu, cw = cu;
   auto issue = [&](int64_t u) {  // lane 0 only; unit u (= cursor ci) is loaded by TMA iff it lies below n
     const int64_t e0 = ci.e0();
@@ -462,23 +443,23 @@ srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restric
       tma_load_3d(dst + h * 4096, &map, h * Tma<T>::HALF, (int)(e0 >> 5), (int)ci.col, b);
   };
   if (lane == 0)
-    for (int64_t u = 0; u < S && u < units; ++u) { issue(u); ci.next(n_eff); }
+    for (int64_t u = 0; u < S && u < units; ++u) { issue(u); ci.next(n_eff, dcol, dg); }
   uint32_t phase = 0;  // bit s = parity expected next on stage s
   uint32_t w_next = units > 0 ? __ldg(bits + ((e_base + cw.e0() + lane * 32) >> 5)) : 0u;
-  cw.next(n_eff);
+  cw.next(n_eff, dcol, dg);
   // lane-run reads of a swizzled stage: chunk c of half h at (c ^ (lane & 7))
   const uint32_t run_base = (uint32_t)lane * 128u, run_x = ((uint32_t)lane & 7u) << 4;
   T ab[KPL], acc[KPL];
 #pragma unroll
   for (int i = 0; i < KPL; ++i) ab[i] = acc[i] = T(0);
-  for (int64_t u = 0; u < units; ++u, cu.next(n_eff)) {
+  for (int64_t u = 0; u < units; ++u, cu.next(n_eff, dcol, dg)) {
     const int64_t col = cu.col, e0 = cu.e0();
     const int q = cu.q;
     const int s = (int)(u % S);
     const int64_t e = e0 + lane * 32;
     const uint32_t w = w_next;
     if (u + 1 < units) w_next = __ldg(bits + ((e_base + cw.e0() + lane * 32) >> 5));
-    cw.next(n_eff);
+    cw.next(n_eff, dcol, dg);
     T v[32];
     unsigned char* sb = stages + (size_t)s * SB;
     const bool full = e0 + 1024 <= n;
@@ -503,7 +484,7 @@ srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restric
     if (lane == 0 && u + S < units) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(u + S);
-      ci.next(n_eff);
+      ci.next(n_eff, dcol, dg);
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = flip_sign(Lo<T>::mul(v[j], scale_lo), w, j);
@@ -746,6 +727,211 @@ srht64h_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_e
   cp_async_wait_group<0>();
 }
 
+// ---------------------------------------------------------------------------
+// K1 standalone for 16-bit storage: TMA-staged warp tiles on PACKED pairs.
+// A warp owns a 4096-coordinate leaf group as two 2048-coordinate
+// sub-tiles; lane l holds run l (64 coordinates = 32 bf16x2/f16x2 words, one
+// 128-byte swizzled row of the TMA box).  Pass 1: the pair bit and bits 1-5
+// in registers.  Pass 2: lane l takes word l (coordinates 2l, 2l+1) of all
+// 32 runs, so the five run-bit stages (bits 6-10) act on both halves of
+// every word at once.  Bit 11 is one correctly rounded op at the sampled
+// coordinates (left operand = sub-tile 0), as in the fp64 kernel.  Every
+// butterfly is one add/sub.rn.{bf16,f16}x2 (the reference rounds each op).
+// ---------------------------------------------------------------------------
+template <typename T, int KPL, int S, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+srht_tma16_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restrict__ X, int64_t ldx, int64_t n,
+                       int64_t n_eff, int64_t k, const uint32_t* __restrict__ bits,
+                       const int64_t* __restrict__ idx, int ell, uint32_t scale2, float* __restrict__ P,
+                       int64_t n_tiles, const Status* st, int64_t e_base) {
+  constexpr uint32_t SB = 4096;  // bytes per 2048-coordinate sub-tile
+  constexpr int RW = 36;         // transpose-buffer row: 32 words + 16-byte pad
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  if (st && failed(st)) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* stages = base + (size_t)wid * S * SB;
+  uint32_t* buf = reinterpret_cast<uint32_t*>(base + (size_t)WPB * S * SB) + wid * 32 * RW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + (size_t)WPB * S * SB + 4 * (size_t)WPB * 32 * RW) + wid * S;
+  if (lane == 0)
+    for (int s = 0; s < S; ++s) mbar_init(bars + s, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  // per output k = lane + 32 i: byte offset of its 16-bit value in the
+  // transpose buffer (bits 0-15), bit 11 of its in-group position at bit 16
+  uint32_t mypk[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int kk = lane + 32 * i;
+    const uint32_t p = kk < ell ? (uint32_t)(__ldg(idx + kk) & 4095) : 0u;
+    const uint32_t run = (p >> 6) & 31u, pos = p & 63u;
+    mypk[i] = ((run * RW + (pos >> 1)) * 4u + (pos & 1u) * 2u) | (((p >> 11) & 1u) << 16);
+  }
+  const int64_t items = n_eff * k;
+  const int64_t nwarps = (int64_t)gridDim.x * WPB;
+  const int64_t wg = (int64_t)blockIdx.x * WPB + wid;
+  // items wg, wg + nwarps, ...: groups processed at the same time are adjacent,
+  // so the 8-byte / 4-byte leaf writes of neighbouring groups meet in L2 and
+  // leave as whole sectors (a contiguous range per warp doubled DRAM writes)
+  const int64_t my_items = wg < items ? (items - wg + nwarps - 1) / nwarps : 0;
+  const int64_t dcol = nwarps / n_eff, dg = nwarps - dcol * n_eff;
+  const int64_t units = my_items * 2;  // 2048-coordinate sub-tiles of this warp
+  struct Cur {  // (column, group, sub-tile) of a unit; advance without division
+    int64_t col, g;
+    int q;
+    __device__ void next(int64_t ne, int64_t dc, int64_t dgg) {
+      if (++q == 2) {
+        q = 0;
+        g += dgg;
+        col += dc;
+        if (g >= ne) { g -= ne; ++col; }
+      }
+    }
+    __device__ int64_t e0() const { return (g << 12) + ((int64_t)q << 11); }
+  };
+  Cur cu{wg / n_eff, wg % n_eff, 0};
+  Cur ci = cu, cw = cu;
+  auto issue = [&](int64_t u) {  // lane 0 only
+    const int64_t e0 = ci.e0();
+    if (e0 + 2048 > n) return;
+    const int s = (int)(u % S);
+    mbar_expect_tx(bars + s, SB);
+    tma_load_3d(stages + (size_t)s * SB, &map, 0, (int)(e0 >> 6), (int)ci.col, bars + s);
+  };
+  if (lane == 0)
+    for (int64_t u = 0; u < S && u < units; ++u) { issue(u); ci.next(n_eff, dcol, dg); }
+  uint32_t phase = 0;
+  uint2 w_next = make_uint2(0u, 0u);
+  if (units > 0) w_next = __ldg(reinterpret_cast<const uint2*>(bits + ((e_base + cw.e0() + lane * 64) >> 5)));
+  cw.next(n_eff, dcol, dg);
+  const uint32_t run_base = (uint32_t)lane * 128u, run_x = ((uint32_t)lane & 7u) << 4;
+  float acc[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) acc[i] = 0.f;
+  for (int64_t u = 0; u < units; ++u, cu.next(n_eff, dcol, dg)) {
+    const int64_t col = cu.col, e0 = cu.e0();
+    const int q = cu.q;
+    const int s = (int)(u % S);
+    const int64_t e = e0 + lane * 64;
+    const uint2 w = w_next;
+    if (u + 1 < units) w_next = __ldg(reinterpret_cast<const uint2*>(bits + ((e_base + cw.e0() + lane * 64) >> 5)));
+    cw.next(n_eff, dcol, dg);
+    unsigned char* sb = stages + (size_t)s * SB;
+    if (e0 + 2048 <= n) {
+      mbar_wait(bars + s, (phase >> s) & 1u);
+      phase ^= 1u << s;
+    } else {  // column tail: stage it by hand in the same swizzled layout
+      const uint16_t* x = reinterpret_cast<const uint16_t*>(X + col * ldx);
+#pragma unroll
+      for (int j = 0; j < 64; j += 2) {
+        const uint32_t lo = (e + j < n) ? x[e + j] : 0u, hi = (e + j + 1 < n) ? x[e + j + 1] : 0u;
+        *reinterpret_cast<uint32_t*>(sb + run_base + ((((uint32_t)j * 2u) & ~15u) ^ run_x) + ((j * 2) & 15)) =
+            lo | (hi << 16);
+      }
+      __syncwarp();
+    }
+    uint32_t v[32];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 r = *reinterpret_cast<const uint4*>(sb + run_base + (((uint32_t)c << 4) ^ run_x));
+      v[4 * c] = r.x; v[4 * c + 1] = r.y; v[4 * c + 2] = r.z; v[4 * c + 3] = r.w;
+    }
+    __syncwarp();
+    if (lane == 0 && u + S < units) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(u + S);
+      ci.next(n_eff, dcol, dg);
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {  // fl(x * scale), then the signs (sketching.py:152-153)
+      const uint32_t ww = (i < 16 ? w.x : w.y) >> ((2 * i) & 31);
+      v[i] = Pk<T>::mul(v[i], scale2) ^ (((ww & 1u) << 15) | ((ww & 2u) << 30));
+    }
+    if (e + 64 > n) {  // zero padding past n is +0 (sketching.py:154)
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (e + 2 * i >= n) v[i] &= 0xffff0000u;
+        if (e + 2 * i + 1 >= n) v[i] &= 0x0000ffffu;
+      }
+    }
+    fwht64_packed<T>(v);  // h = 1..32
+    {
+      uint4* row = reinterpret_cast<uint4*>(buf + lane * RW);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) row[c] = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 32; ++r) v[r] = buf[r * RW + lane];
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2)  // h = 64..1024 on both halves of each word
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (!(r & (1 << s2))) {
+          const uint32_t x = v[r], y = v[r | (1 << s2)];
+          v[r] = Pk<T>::add(x, y);
+          v[r | (1 << s2)] = Pk<T>::sub(x, y);
+        }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) buf[r * RW + lane] = v[r];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const uint32_t pk = mypk[i];
+      const float sv =
+          pk_lo_float<T>(*reinterpret_cast<const uint16_t*>(reinterpret_cast<const unsigned char*>(buf) + (pk & 0xffffu)));
+      if (q == 0) {
+        acc[i] = sv;
+      } else {
+        const int kk = lane + 32 * i;
+        if (kk < ell)
+          P[(col * ell + kk) * n_tiles + (e0 >> 12)] = ((pk >> 16) & 1u) ? Lo<T>::sub(acc[i], sv) : Lo<T>::add(acc[i], sv);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <typename T, int KPL, int S, int WPB>
+static int launch_tma16(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int64_t n_local, int64_t e_base,
+                        const T* X, int64_t ldx, int64_t k, uint32_t scale2, float* P, const Status* st) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return set_error(ctx, SQB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  const cuuint64_t dims[3] = {64, (cuuint64_t)(n_local >> 6), (cuuint64_t)k};
+  const cuuint64_t strides[2] = {128, (cuuint64_t)ldx * 2};
+  const cuuint32_t box[3] = {64, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(&map, std::is_same<T, __half>::value ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                         3, const_cast<T*>(X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(ctx, SQB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  const size_t smem = 1024 + (size_t)WPB * S * 4096 + 4 * (size_t)WPB * 32 * 36 + (size_t)WPB * S * 8;
+  auto kern = srht_tma16_tile_kernel<T, KPL, S, WPB>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem);
+  per_sm = std::max(1, per_sm);
+  const int64_t items = g.n_eff * k;
+  const int64_t ctas =
+      std::max<int64_t>(1, std::min<int64_t>((items + WPB - 1) / WPB, (int64_t)per_sm * ctx->sm_count));
+  kern<<<(unsigned)ctas, WPB * 32, smem, ctx->stream>>>(map, X, ldx, n_local, g.n_eff, k, sk->sign_bits,
+                                                         sk->indices, (int)sk->ell, scale2, P, g.n_tiles, st, e_base);
+  return check_launch(ctx, "srht_tma16_tile_kernel");
+}
+
+template <typename T, int S, int WPB>
+static int launch_tma16_kpl(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int64_t n_local,
+                            int64_t e_base, const T* X, int64_t ldx, int64_t k, uint32_t scale2, float* P,
+                            const Status* st) {
+  const int kpl = (int)((sk->ell + 31) / 32);
+  if (kpl <= 4) return launch_tma16<T, 4, S, WPB>(ctx, sk, g, n_local, e_base, X, ldx, k, scale2, P, st);
+  if (kpl <= 8) return launch_tma16<T, 8, S, WPB>(ctx, sk, g, n_local, e_base, X, ldx, k, scale2, P, st);
+  return launch_tma16<T, 16, S, WPB>(ctx, sk, g, n_local, e_base, X, ldx, k, scale2, P, st);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 srht_tree_kernel(const typename Lo<T>::acc* __restrict__ P, int64_t n_tiles, int64_t n_eff,
@@ -816,6 +1002,15 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
                    (g.log_tb >= 3);
   dim3 grid((unsigned)g.n_eff, (unsigned)k);
   if constexpr (sizeof(T) == 2) {
+    if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= 512 && n_local >= 64 && encode_tiled() &&
+        !getenv("SQB_SRHT16_OLD")) {
+      const T s1 = T((float)sc);  // sc is already a value of T (srht_constants): exact
+      uint16_t s16b;
+      memcpy(&s16b, &s1, 2);
+      const uint32_t s16 = s16b;
+      return launch_tma16_kpl<T, 2, 4>(ctx, sk, g, n_local, e_base, (const T*)X, ldx, k, s16 | (s16 << 16),
+                                       (float*)P, st);
+    }
     if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= S64_MAX_ELL) {
       const size_t smemh = s64_head_bytes((int)sk->ell, 2) + s64_buf_bytes<T>();
       cudaFuncSetAttribute(srht64h_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemh);

@@ -1,5 +1,5 @@
-"""A/B of the standalone SRHT tile kernels (SQB_SRHT_VARIANT, read once per
-process, so each variant runs in its own process): time + bitwise digest."""
+"""A/B of the standalone SRHT tile kernels: each argument NAME=VALUE is the
+environment of one child process (e.g. SQB_SRHT16_OLD=1); time + bitwise digest."""
 import os, sys, subprocess, json, hashlib
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -12,7 +12,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     out = []
     cases = [((1 << 20) - 128, 256, 128, "double"), ((1 << 22) - 201, 400, 16, "double"),
              ((1 << 20) - 128, 256, 128, "single"), ((1 << 22) - 201, 400, 1, "double"),
-             ((1 << 20) - 128, 256, 1, "double"), (5000, 128, 3, "double"), ((1 << 14) - 32, 128, 32, "double")]
+             ((1 << 20) - 128, 256, 1, "double"), (5000, 128, 3, "double"), ((1 << 14) - 32, 128, 32, "double"),
+             ((1 << 24) - 256, 512, 16, "bf16"), ((1 << 20) - 128, 256, 16, "half"), (5000, 128, 3, "bf16"),
+             ((1 << 22) - 201, 400, 4, "bf16")]
     for (n, ell, k, tag) in cases:
         om = P.SRHTSketch(ell, n, 8)
         g = torch.Generator(device="cuda"); g.manual_seed(5)
@@ -35,7 +37,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
         out.append(f"n={n} ell={ell} k={k} {tag}: {ms*1e3:8.1f} us {b/ms/1e6:6.0f} GB/s = {b/ms/1e6/peak:.2f}  {dig}")
     print("\n".join(out))
 else:
-    for v in sys.argv[1:] or ["0", "1", "2"]:
-        env = dict(os.environ, SQB_SRHT_VARIANT=v)
+    for v in sys.argv[1:] or ["default"]:  # each argument: NAME=VALUE environment for one process
+        env = dict(os.environ)
+        if "=" in v:
+            env[v.split("=")[0]] = v.split("=")[1]
         r = subprocess.run([sys.executable, __file__, "child"], env=env, capture_output=True, text=True)
         print(f"--- variant {v}\n{r.stdout}{r.stderr[-2000:]}")

@@ -61,6 +61,19 @@ def test_srht_bitwise_against_oracle_large(P, ell, n, seed, k):
     assert np.array_equal(op.apply(X), ref.apply(X))
 
 
+@pytest.mark.parametrize("tag", ["single", "half", "bf16"])
+@pytest.mark.parametrize("ell,n,seed,k", [(512, (1 << 18) - 256, 4, 2), (128, 3 * 4096 + 17, 6, 5),
+                                          (33, 1000, 7, 3), (600, (1 << 16) - 5, 8, 2)])
+def test_srht_lowprec_bitwise_against_oracle(P, tag, ell, n, seed, k):
+    """The TMA warp-tile kernels (fp32 and packed 16-bit) and their fallbacks
+    (tail-only columns, ell > 512): bitwise the oracle's rounded-per-op SRHT."""
+    op = P.SRHTSketch(ell, n, seed)
+    ref = O.SRHT(ell, n, seed)
+    dt = O.TAG_DTYPE[tag]
+    X = O.round_to(np.random.default_rng(seed).standard_normal((n, k)), tag)
+    assert np.array_equal(op.apply(X, dt), ref.apply(X, dt))
+
+
 def test_srht_rejects_bad_rows(P):
     op = P.SRHTSketch(8, 20, 1)
     with pytest.raises(ValueError):

@@ -767,6 +767,248 @@ def gen_cmatrix(n, m):
         np.cos(100.0 * (mu[None, :] - x[:, None])) + 1.1)
 
 
+# --------------------------------------------------------------------------
+# trim.py (+ sketching.py:216-235): trimmed RHQR, SURVEY §8(f)4
+# --------------------------------------------------------------------------
+class ColumnScaled:
+    """sketching.py:216-235: rescale the m leading input coordinates (in the
+    arithmetic dtype), then apply the base operator.  `E` caches the unit
+    sketches of the leading columns."""
+
+    kind = "colscaled"
+
+    def __init__(self, base, scales, m, E):
+        self.base, self.m = base, int(m)
+        self.ell, self.n, self.seed = base.ell, base.n, base.seed
+        self.scales = np.asarray(scales, dtype=np.float64)
+        self.E = E
+
+    def apply(self, X, dtype=np.float64):
+        X, vec = _cols(X, self.n)
+        dt = np.dtype(dtype)
+        Xs = X.astype(dt) * self.scales[:, None].astype(dt)
+        Y = self.base.apply(Xs.astype(np.float64), dtype=dt)
+        Y = np.asarray(Y, dtype=np.float64)
+        return Y[:, 0] if vec else Y
+
+
+def srht_unit_columns(omega, m):
+    """Omega e_k for k < m in closed form (SRHT only): the FWHT of a one-hot
+    vector adds only exact zeros, so entry i is
+    sign_k * (-1)^popcount(idx_i & k) * fl(fl(1 * scale) * n_pad^-1/2)
+    — bitwise what sketching.py:149-155 computes for I[:, :m]."""
+    a = np.float64(np.float64(1.0) * np.float64(omega.scale)) * np.float64(omega.n_pad ** -0.5)
+    k = np.arange(m, dtype=np.int64)
+    par = np.zeros((omega.ell, m), dtype=np.int64)
+    x = omega.indices[:, None] & k[None, :]
+    while np.any(x):
+        par ^= x & 1
+        x >>= 1
+    return (np.where(par == 1, -1.0, 1.0) * omega.signs[:m][None, :]) * a
+
+
+def normalize_leading_columns(omega, m, chunk=256):
+    """trim.py:51-77."""
+    if isinstance(omega, ColumnScaled) and omega.m >= m:
+        return omega
+    n = omega.n
+    if m > n:
+        raise ValueError(f"cannot normalize {m} leading columns of {n} inputs")
+    cols = np.empty((omega.ell, m))
+    for k0 in range(0, m, chunk):
+        k1 = min(k0 + chunk, m)
+        eye = np.zeros((n, k1 - k0))
+        eye[np.arange(k0, k1), np.arange(k1 - k0)] = 1.0
+        cols[:, k0:k1] = omega.apply(eye)
+    norms = np.linalg.norm(cols, axis=0)
+    if np.any(norms == 0.0):
+        raise ValueError(f"leading column {int(np.argmin(norms)) + 1} sketches to zero")
+    scales = np.ones(n)
+    scales[:m] = 1.0 / norms
+    return ColumnScaled(omega, scales, m, cols / norms)
+
+
+@dataclass
+class TrimStep:
+    """trim.py:37-48."""
+
+    j: int
+    v: np.ndarray
+    s: np.ndarray
+    sigma: float
+    rho: float
+    beta: float
+
+
+def trim_rh_vector(w_tail, omega, j, scaling="sqrt2", policy=DOUBLE):
+    """trim.py:80-146: the reflector of the tail w[j-1:], sketched with the
+    j-1 leading coordinates zeroed."""
+    lo, hi = policy.lo, policy.hi.type
+    w_tail = np.asarray(w_tail, dtype=np.float64)
+    n, p = omega.n, j - 1
+    if not 0 <= p < n:
+        raise ValueError(f"elimination index {j} outside {n} coordinates")
+    if w_tail.shape[0] != n - p:
+        raise ValueError(f"tail has {w_tail.shape[0]} entries, expected {n - p}")
+    x = np.zeros(n)
+    x[p:] = w_tail
+    z = omega.apply(x, dtype=lo)
+    zn = float(np.linalg.norm(z))
+    rho = float(round_to(zn, policy.high))
+    if rho == 0.0:
+        raise BreakdownError(f"sketched tail annihilated at column {j}")
+    sg = sign(w_tail[0])
+    v = w_tail.copy()
+    v[0] += sg * rho
+    v = round_to(v, policy.low)
+    x[p:] = v
+    vs = omega.apply(x, dtype=lo)
+    nv = float(round_to(np.linalg.norm(vs), policy.high))
+    if nv <= 8.0 * policy.u_high * (zn + rho):
+        raise BreakdownError(f"sketched reflector vector cancelled at column {j} "
+                             f"(degenerate sketch geometry, norm {nv:.3e})")
+    beta = float(hi(2.0 / (nv * nv)))
+    if scaling == "sqrt2":
+        f = float(hi(np.sqrt(beta)))
+        v, vs, beta = v * f, vs * f, 1.0
+    else:
+        piv = float(vs[0])
+        if abs(piv) <= 8.0 * policy.u_high * nv:
+            raise BreakdownError(f"unit scaling pivot vanished at column {j} (sketched entry {piv:.3e})")
+        v, vs = v / piv, vs / piv
+        beta = float(hi(beta * piv * piv))
+    return TrimStep(j, round_to(v, policy.low), round_to(vs, policy.high), sg, rho, beta)
+
+
+@dataclass
+class TrimFactors:
+    """trim.py:149-186."""
+
+    U: np.ndarray
+    S: np.ndarray
+    T: np.ndarray
+    T_tilde: np.ndarray
+    R: np.ndarray
+    L: np.ndarray
+    E: np.ndarray
+    omega: ColumnScaled
+    scaling: str
+    sigmas: np.ndarray
+    rhos: np.ndarray
+    betas: np.ndarray
+
+
+def _trim_setup(W, omega, m):
+    """trim.py:228-235."""
+    W = np.asarray(W, dtype=np.float64)
+    if W.ndim != 2:
+        raise ValueError("W must be a matrix")
+    omega = normalize_leading_columns(omega, m)
+    if omega.n != W.shape[0]:
+        raise ValueError(f"sketch takes {omega.n} coordinates, W has {W.shape[0]} rows")
+    return W, omega
+
+
+def t_tilde_from_factors(S, E, U, policy=DOUBLE):
+    """trim.py:189-208: T~^t = -A^{-1}, A = corr - tril(G, -1) - diag(G)/2."""
+    hi = policy.hi
+    S = np.asarray(S)
+    m = S.shape[1]
+    Sh = _cast(S, hi)
+    G = (Sh.T @ Sh).astype(np.float64)
+    Lt = np.tril((Sh.T @ _cast(np.asarray(E)[:, :m], hi)).astype(np.float64), -1)
+    corr = (_cast(Lt, hi) @ _cast(np.asarray(U)[:m], hi)).astype(np.float64)
+    A = corr - np.tril(G, -1) - np.diag(np.diagonal(G) / 2.0)
+    return -upper_tri_solve(A.T, np.eye(m), policy=policy)
+
+
+def trim_thin_q(F):
+    """trim.py:211-225: Q = [I;0] - U T triu(S^t E)."""
+    U = np.asarray(F.U)
+    k = U.shape[1]
+    M = np.triu(np.asarray(F.S).T @ np.asarray(F.E)[:, :k])
+    Q = -U @ (np.asarray(F.T) @ M)
+    Q[:k] += np.eye(k)
+    return Q
+
+
+def trim_rhqr_left(W, omega, scaling="sqrt2", policy=DOUBLE):
+    """trim.py:272-325: column c is transformed by the reversed compact form
+    w -= U T~^t (S^t (Omega w) - L w_head), then reflected from its tail."""
+    lo, hi = policy.lo, policy.hi
+    n, m = np.asarray(W).shape
+    W, omega = _trim_setup(W, omega, m)
+    E = omega.E[:, :m].copy()
+    Wl = round_to(W, policy.low)
+    U = np.zeros((n, m))
+    S = np.zeros((omega.ell, m))
+    R = np.zeros((m, m))
+    T = np.zeros((m, m))
+    Tt = np.zeros((m, m))
+    L = np.zeros((m, m))
+    sg, rh, bt = [], [], []
+    for c in range(m):
+        w = Wl[:, c].copy()
+        if c:
+            z = omega.apply(w, dtype=lo)
+            h = (_cast(S[:, :c], hi).T @ _cast(z, hi)).astype(np.float64)
+            h -= (_cast(L[:c, :c], hi) @ _cast(w[:c], hi)).astype(np.float64)
+            coef = (_cast(Tt[:c, :c], hi).T @ _cast(h, hi)).astype(np.float64)
+            w = (_cast(w, lo) - _cast(U[:, :c], lo) @ _cast(coef, lo)).astype(np.float64)
+        st = trim_rh_vector(w[c:], omega, c + 1, scaling, policy)
+        U[c:, c] = st.v
+        S[:, c] = st.s
+        R[:c, c] = w[:c]
+        R[c, c] = -st.sigma * st.rho
+        lrow = (_cast(E[:, :c], hi).T @ _cast(st.s, hi)).astype(np.float64)
+        L[c, :c] = lrow
+        extend_t(T, S, st.s, st.beta, c, hi=hi.type)
+        if c:
+            g = (_cast(S[:, :c], hi).T @ _cast(st.s, hi)).astype(np.float64)
+            g -= (_cast(U[:c, :c], hi).T @ _cast(lrow, hi)).astype(np.float64)
+            Tt[:c, c] = (hi.type(-st.beta) * (_cast(Tt[:c, :c], hi) @ _cast(g, hi))).astype(np.float64)
+        Tt[c, c] = st.beta
+        sg.append(st.sigma)
+        rh.append(st.rho)
+        bt.append(st.beta)
+    return TrimFactors(U, S, T, Tt, R, L, E, omega, scaling, np.array(sg), np.array(rh), np.array(bt))
+
+
+def trim_rhqr_right(W, omega, scaling="sqrt2", policy=DOUBLE):
+    """trim.py:238-269: right-looking, trailing columns updated through the
+    masked sketch; T, T~ and L assembled after the sweep."""
+    lo, hi = policy.lo, policy.hi
+    n, m = np.asarray(W).shape
+    W, omega = _trim_setup(W, omega, m)
+    Wl = round_to(W, policy.low)
+    U = np.zeros((n, m))
+    S = np.zeros((omega.ell, m))
+    R = np.zeros((m, m))
+    sg, rh, bt = [], [], []
+    for c in range(m):
+        w = Wl[:, c]
+        st = trim_rh_vector(w[c:], omega, c + 1, scaling, policy)
+        U[c:, c] = st.v
+        S[:, c] = st.s
+        R[:c, c] = w[:c]
+        R[c, c] = -st.sigma * st.rho
+        sg.append(st.sigma)
+        rh.append(st.rho)
+        bt.append(st.beta)
+        if c + 1 < m:
+            Y = Wl[:, c + 1:]
+            masked = Y.copy()
+            masked[:c] = 0.0
+            X = omega.apply(masked, dtype=lo)
+            coef = (hi.type(st.beta) * (_cast(st.s, hi) @ _cast(X, hi))).astype(np.float64)
+            Wl[:, c + 1:] = (_cast(Y, lo) - np.outer(_cast(U[:, c], lo), _cast(coef, lo))).astype(np.float64)
+    E = omega.E[:, :m].copy()
+    T = t_factor_from_sketches(S, policy=policy)
+    Tt = t_tilde_from_factors(S, E, U, policy=policy)
+    L = np.tril((_cast(S, hi).T @ _cast(E, hi)).astype(np.float64), -1)
+    return TrimFactors(U, S, T, Tt, R, L, E, omega, scaling, np.array(sg), np.array(rh), np.array(bt))
+
+
 def rhqr_left_bytes(N, m, elem_bytes=8):
     """Algorithmic HBM bytes of left-looking RHQR:
     b*N*(m^2 + 5m)/2 — read U[:, :c] and read+write w_c per column, plus the

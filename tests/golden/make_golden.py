@@ -288,9 +288,39 @@ def experiment_cases():
     save("experiments_gmres_cd24", indptr=ip, indices=ix, data=dv, b=b, **g)
 
 
+def trim_cases():
+    """Trimmed RHQR (trim.py:51-325): ell < m, left and right drivers, both
+    scalings, a single-precision policy, and the exact-dependence breakdown."""
+    from sketchqr.trim import (normalize_leading_columns, trim_rhqr_left, trim_rhqr_right,
+                               trim_thin_q)
+    rng = np.random.default_rng(71)
+    N, m, ell, seed = 2048, 16, 12, 73
+    W = rng.standard_normal((N, m)) * np.logspace(0, -6, m)
+    om = SRHTSketch(ell, N, seed)
+    wrapped = normalize_leading_columns(om, m)
+
+    def dump(F, pre=""):
+        return {pre + k: getattr(F, k) for k in ("U", "S", "T", "T_tilde", "R", "L", "E",
+                                                  "sigmas", "rhos", "betas")}
+    F = trim_rhqr_left(W, om)
+    Fu = trim_rhqr_left(W, om, scaling="unit")
+    Fr = trim_rhqr_right(W, om)
+    Fs = trim_rhqr_left(W, om, policy=P.policy_from_tag("single"))
+    save("trim_2048x16_srht12", W=W, seed=seed, ell=ell, scales=wrapped.scales[:m],
+         Q=trim_thin_q(F), **dump(F), **dump(Fu, "unit_"), **dump(Fr, "right_"), **dump(Fs, "single_"))
+    Wd = np.zeros((64, 2))
+    Wd[0] = 1.0  # test_trim.py:215-220: the second tail is exactly zero after the update
+    try:
+        trim_rhqr_left(Wd, SRHTSketch(12, 64, 37))
+        msg = ""
+    except Exception as e:  # BreakdownError
+        msg = str(e)
+    save("trim_breakdown", W=Wd, seed=37, ell=12, msg=np.array(msg))
+
+
 SECTIONS = dict(srht=srht_cases, gauss=gauss_cases, rh_vector=rh_vector_cases, rhqr=rhqr_cases,
                 mixed=mixed_cases, rec=rec_cases, krylov=krylov_cases, apply_compact=apply_compact_cases,
-                block=block_cases, experiments=experiment_cases)
+                block=block_cases, experiments=experiment_cases, trim=trim_cases)
 
 if __name__ == "__main__":
     # no arguments: every section; otherwise only the named ones

@@ -194,6 +194,35 @@ int sqb_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype
                    double* T, int64_t ldt, double* R, int64_t ldr,
                    double* sigmas, double* rhos, double* betas);
 
+/* Trimmed left-looking RHQR (trim_rhqr_left, trim.py:272-325).  The sketch
+ * sk acts on all N coordinates; the column-scaled wrapper (sketching.py:
+ * 216-235) multiplies coordinates k < m by scales[k] first, and E (ell x m,
+ * ld lde) holds its unit leading-column sketches (normalize_leading_columns,
+ * trim.py:51-77, built by the caller).  Outputs U (N x m, lo dtype, 16-byte
+ * aligned), S (ell x m), T, T~, R, L (m x m, fp64) and the scalars.
+ * Breakdown -> SQB_ERR_BREAKDOWN, col = j | kind << 24 (0: sketched tail
+ * annihilated, 1: sketched reflector cancelled, val = norm; 2: unit pivot
+ * vanished, val = pivot).                                                 */
+int sqb_trim_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
+                       const double* E, int64_t lde, int scaling, int lo_dtype,
+                       const void* W, int64_t N, int64_t m, int64_t ldw,
+                       void* U, int64_t ldu, double* S, int64_t lds,
+                       double* T, int64_t ldt, double* Tt, int64_t ldtt,
+                       double* R, int64_t ldr, double* L, int64_t ldl,
+                       double* sigmas, double* rhos, double* betas);
+
+/* The column-scaled operator alone (ColumnScaledSketch._apply,
+ * sketching.py:230-235): Y = Omega (X with rows k < m times scales[k] in the
+ * arithmetic dtype).  X: sk->n x k (dtype), Y: ell x k fp64.               */
+int sqb_colscaled_apply(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t m,
+                        int dtype, const void* X, int64_t ldx, int64_t k, double* Y, int64_t ldy);
+
+/* Trimmed thin Q = [I;0] - U T triu(S^t E) in fp64 (trim_thin_q,
+ * trim.py:211-225).  U: N x k (lo), T: k x k, S and E: ell x k.            */
+int sqb_trim_thin_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t k,
+                    const double* T, int64_t ldt, const double* S, int64_t lds,
+                    const double* E, int64_t lde, int64_t ell, double* Q, int64_t ldq);
+
 /* T of the compact form from S = Psi U alone (t_factor_from_sketches,
  * rhqr.py:122-132): T^{-1} = triu(S^t S, 1) + diag(S^t S)/2, inverted by back
  * substitution.  S: od x k fp64, T: k x k.  Singular -> SQB_ERR_SINGULAR.  */

@@ -20,6 +20,13 @@ int sketch_q_run(sqb_ctx*, int, const void*, int64_t, int64_t, const double*, in
 int rhqr_block_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t, int64_t,
                         void*, int64_t, double*, int64_t, double*, int64_t, double*, int64_t, double*, double*,
                         double*);
+int trim_left_dispatch(sqb_ctx*, const sqb_sketch*, const double*, const double*, int64_t, int, int, const void*,
+                       int64_t, int64_t, int64_t, void*, int64_t, double*, int64_t, double*, int64_t, double*,
+                       int64_t, double*, int64_t, double*, int64_t, double*, double*, double*);
+int colscaled_apply_dispatch(sqb_ctx*, const sqb_sketch*, const double*, int64_t, int, const void*, int64_t,
+                             int64_t, double*, int64_t);
+int trim_thin_q_impl(sqb_ctx*, int, const void*, int64_t, int64_t, int64_t, const double*, int64_t,
+                     const double*, int64_t, const double*, int64_t, int64_t, double*, int64_t);
 int rhqr_right_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t, void*,
                         int64_t, double*, int64_t, double*, int64_t, double*, double*, double*);
 int rec_rhqr_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t, void*,
@@ -218,6 +225,53 @@ int sqb_rhqr_block(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype
     return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
   return rhqr_block_dispatch(ctx, sk, scaling, lo_dtype, W, N, m, ldw, block_size, U, ldu, S, lds, T, ldt, R,
                              ldr, sigmas, rhos, betas);
+}
+
+int sqb_trim_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+                       int scaling, int lo_dtype, const void* W, int64_t N, int64_t m, int64_t ldw, void* U,
+                       int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt, double* Tt, int64_t ldtt,
+                       double* R, int64_t ldr, double* L, int64_t ldl, double* sigmas, double* rhos,
+                       double* betas) {
+  SQB_TRY(prep(ctx));
+  SQB_TRY(check_dtype(ctx, lo_dtype));
+  SQB_TRY(validate_sketch(ctx, sk));
+  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
+    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
+  if (m < 1) return set_error(ctx, SQB_ERR_ARG, "need at least one column");
+  if (sk->n != N)
+    return set_error(ctx, SQB_ERR_ARG, "sketch takes %lld coordinates, W has %lld rows", (long long)sk->n,
+                     (long long)N);
+  if (m > N) return set_error(ctx, SQB_ERR_ARG, "cannot normalize %lld leading columns of %lld inputs",
+                              (long long)m, (long long)N);
+  if (!scales || !E || lde < sk->ell) return set_error(ctx, SQB_ERR_ARG, "column-scaled operator without scales/E");
+  if (ldw < N || ldu < N || lds < sk->ell || ldt < m || ldtt < m || ldr < m || ldl < m)
+    return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
+  const int64_t esz = lo_dtype == SQB_F64 ? 8 : lo_dtype == SQB_F32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(U) & 15) || (ldu * esz) % 16)
+    return set_error(ctx, SQB_ERR_ARG, "U must be 16-byte aligned with a 16-byte multiple leading dimension");
+  SQB_TRY(trim_left_dispatch(ctx, sk, scales, E, lde, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, T, ldt, Tt,
+                             ldtt, R, ldr, L, ldl, sigmas, rhos, betas));
+  return SQB_OK;
+}
+
+int sqb_colscaled_apply(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t m, int dtype,
+                        const void* X, int64_t ldx, int64_t k, double* Y, int64_t ldy) {
+  SQB_TRY(prep(ctx));
+  SQB_TRY(check_dtype(ctx, dtype));
+  SQB_TRY(validate_sketch(ctx, sk));
+  if (m < 0 || m > sk->n || !scales) return set_error(ctx, SQB_ERR_ARG, "bad column-scaled operator");
+  if (ldx < sk->n || ldy < sk->ell) return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
+  return colscaled_apply_dispatch(ctx, sk, scales, m, dtype, X, ldx, k, Y, ldy);
+}
+
+int sqb_trim_thin_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t k,
+                    const double* T, int64_t ldt, const double* S, int64_t lds, const double* E, int64_t lde,
+                    int64_t ell, double* Q, int64_t ldq) {
+  SQB_TRY(prep(ctx));
+  SQB_TRY(check_dtype(ctx, lo_dtype));
+  if (k < 0 || k > N || ldu < N || ldq < N || ldt < k || lds < ell || lde < ell)
+    return set_error(ctx, SQB_ERR_ARG, "bad trimmed thin-Q arguments");
+  return trim_thin_q_impl(ctx, lo_dtype, U, ldu, N, k, T, ldt, S, lds, E, lde, ell, Q, ldq);
 }
 
 int sqb_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, const void* W,

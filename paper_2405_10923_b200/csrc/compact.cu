@@ -244,6 +244,30 @@ static int thin_q_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int64_t
   return check_launch(ctx, "thin_q_kernel");
 }
 
+// Q = [I;0] - U M for a given k x k fp64 M (ld k) — the trimmed thin Q
+// (trim.py:211-225) passes M = T triu(S^t E)
+template <typename T>
+static int thin_q_m_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int64_t k, const double* M, double* Q,
+                      int64_t ldq) {
+  const size_t smem = sizeof(double) * k * k;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(thin_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  thin_q_kernel<T><<<(unsigned)std::min<int64_t>((N + 255) / 256, 2 * 148), 256, smem, ctx->stream>>>(
+      (const T*)U, ldu, N, (int)k, M, Q, ldq);
+  return check_launch(ctx, "thin_q_kernel");
+}
+
+int thin_q_m_dispatch(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t k,
+                      const double* M, double* Q, int64_t ldq) {
+  switch (lo_dtype) {
+    case SQB_F64: return thin_q_m_t<double>(ctx, U, ldu, N, k, M, Q, ldq);
+    case SQB_F32: return thin_q_m_t<float>(ctx, U, ldu, N, k, M, Q, ldq);
+    case SQB_F16: return thin_q_m_t<__half>(ctx, U, ldu, N, k, M, Q, ldq);
+    case SQB_BF16: return thin_q_m_t<__nv_bfloat16>(ctx, U, ldu, N, k, M, Q, ldq);
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
 int thin_q_dispatch(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t k,
                     const double* Tm, int64_t ldt, double* Q, int64_t ldq) {
   switch (lo_dtype) {

@@ -1,0 +1,386 @@
+// Trimmed RHQR, left-looking (trim.py:272-325).
+//
+// The operator is the column-scaled wrapper of a base sketch over all N
+// coordinates (sketching.py:216-235): coordinates < m are multiplied by
+// scales[k] in the arithmetic dtype before the base sketch.  Per column c
+// (1-based j = c + 1):
+//   c > 0:  z = Om(w)                       prep + K1
+//           h = S^t z - L w[:c];  coef = T~^t h          (trim_coef_kernel)
+//           w = fl(w - fl(U[:, :c] coef))                (streaming GEMV)
+//   trim_rh_vector (trim.py:80-146):
+//           z = Om([0; w[c:]]);  rho = ||z||;  v0 = fl(w[c] + sigma rho)
+//           vs = Om([0; v0, w[c+1:]])           (the prepared input with one
+//                                                entry replaced, K1 again)
+//           beta = 2 / ||vs||^2, sqrt2 / unit scaling, breakdown checks
+//   S[:, c] = vs;  R[:c, c] = w[:c];  R[c, c] = -sigma rho
+//   L[c, :c] = E^t vs;  T column (_extend_t);  T~ column (trim.py:312-316)
+//   U[:, c] = [0; v] * f  (or / piv)
+// Sketch-space work runs in single-CTA kernels on the device; nothing returns
+// to the host until the sweep ends.  Breakdowns set the device status with
+// col = j | kind << 24 (kind 0: tail annihilated, 1: reflector cancelled,
+// 2: unit pivot vanished), which the facade maps to the reference's messages.
+#include <algorithm>
+
+#include "sketch.cuh"
+#include "vec.cuh"
+#include "gemv.cuh"
+
+namespace sqb {
+
+constexpr int TRIM_NT = 256;
+
+// x = Xs of the column-scaled wrapper applied to [0 (c0 entries); w[c0:]]
+template <typename T>
+__global__ void trim_prep_kernel(T* __restrict__ x, const T* __restrict__ w, int64_t N, int64_t c0, int64_t m,
+                                 const double* __restrict__ scales, const Status* st) {
+  if (failed(st)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    T v;
+    if (i < c0) v = Lo<T>::store(typename Lo<T>::acc(0));
+    else if (i < m) v = Lo<T>::store(Lo<T>::mul(Lo<T>::load(w[i]), Lo<T>::from_double(scales[i])));
+    else v = w[i];  // x * 1.0 is exact
+    x[i] = v;
+  }
+}
+
+// h = S[:, :c]^t z - L[:c, :c] w[:c];  coef = T~[:c, :c]^t h   (trim.py:296-299)
+template <typename T>
+__global__ void __launch_bounds__(TRIM_NT)
+trim_coef_kernel(const double* __restrict__ S, int64_t lds, int ell, const double* __restrict__ z,
+                 const double* __restrict__ L, int64_t ldl, const T* __restrict__ w, const double* __restrict__ Tt,
+                 int64_t ldtt, int c, double* __restrict__ coef, const Status* st) {
+  extern __shared__ double h[];  // [c]
+  if (failed(st)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = warp; k < c; k += TRIM_NT / 32) {
+    double d = 0.0;
+    for (int i = lane; i < ell; i += 32) d = fma(S[i + k * lds], z[i], d);
+    d = warp_sum(d);
+    double e = 0.0;
+    for (int i = lane; i < k; i += 32) e = fma(L[k + i * ldl], (double)Lo<T>::load(w[i]), e);
+    e = warp_sum(e);
+    if (lane == 0) h[k] = d - e;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < c; i += TRIM_NT) {
+    double d = 0.0;
+    for (int k = 0; k <= i; ++k) d = fma(Tt[k + i * ldtt], h[k], d);
+    coef[i] = d;
+  }
+}
+
+// w = fl(w - fl(U[:, :c] coef_lo)) over all N rows (trim.py:300)
+template <typename T>
+__global__ void __launch_bounds__(GEMV_NT, 2)
+trim_update_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int c, const double* __restrict__ coef,
+                   T* __restrict__ w, const Status* st) {
+  using A = typename Lo<T>::acc;
+  constexpr int VN = VecN<T>::n, NV = 4;
+  extern __shared__ unsigned char smraw[];
+  A* cl = reinterpret_cast<A*>(smraw);
+  if (failed(st)) return;
+  for (int k = threadIdx.x; k < c; k += blockDim.x) cl[k] = Lo<T>::from_double(coef[k]);
+  __syncthreads();
+  const int64_t rows_per = (int64_t)GEMV_NT * NV * VN;
+  for (int64_t r0 = (int64_t)blockIdx.x * rows_per; r0 < N; r0 += (int64_t)gridDim.x * rows_per) {
+    A acc[NV][VN];
+    gemv_rows<T, NV>(U, ldu, r0, N, c, cl, acc);
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int j = 0; j < VN; ++j) {
+        const int64_t i = r0 + (v * GEMV_NT + threadIdx.x) * VN + j;
+        if (i < N) w[i] = Lo<T>::store(Lo<T>::sub(Lo<T>::load(w[i]), Lo<T>::rnd(acc[v][j])));
+      }
+  }
+}
+
+// fp64 block sum of squares (all threads get the result)
+__device__ __forceinline__ double block_sumsq(const double* __restrict__ y, int n, double* red) {
+  double d = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) d = fma(y[i], y[i], d);
+  return block_sum(d, red);
+}
+
+// after z = Om([0; w[c:]]): rho, sigma, v0; replace entry c of the prepared
+// input by the scaled v0 so the next K1 sketches [0; v] (trim.py:103-114)
+template <typename T>
+__global__ void __launch_bounds__(TRIM_NT)
+trim_tail_kernel(const double* __restrict__ z, int ell, const T* __restrict__ w, int c,
+                 const double* __restrict__ scales, T* __restrict__ x, double* __restrict__ scal, Status* st) {
+  __shared__ double red[32];
+  if (failed(st)) return;
+  const double zn = __dsqrt_rn(block_sumsq(z, ell, red));
+  if (threadIdx.x == 0) {
+    const double rho = zn;  // round_to(., high) is the identity for fp64
+    if (rho == 0.0) {
+      fail(st, SQB_ERR_BREAKDOWN, (c + 1), 0.0);
+      return;
+    }
+    const double wc = (double)Lo<T>::load(w[c]);
+    const double sg = wc >= 0.0 ? 1.0 : -1.0;
+    const double v0 = (double)Lo<T>::from_double(__dadd_rn(wc, sg * rho));
+    x[c] = Lo<T>::store(Lo<T>::mul(Lo<T>::from_double(v0), Lo<T>::from_double(scales[c])));
+    scal[0] = sg;
+    scal[1] = rho;
+    scal[2] = zn;
+    scal[3] = v0;
+  }
+}
+
+// after vs = Om([0; v]): scaling, breakdown checks, and every sketch-space
+// column of the step (trim.py:115-146, 304-316)
+template <typename T>
+__global__ void __launch_bounds__(TRIM_NT)
+trim_finish_kernel(double* __restrict__ vs, int ell, int c, int scaling, double u_high, const T* __restrict__ w,
+                   const T* __restrict__ U, int64_t ldu, const double* __restrict__ E, int64_t lde,
+                   double* __restrict__ S, int64_t lds, double* __restrict__ Tm, int64_t ldt,
+                   double* __restrict__ Tt, int64_t ldtt, double* __restrict__ R, int64_t ldr,
+                   double* __restrict__ L, int64_t ldl, double* __restrict__ sig, double* __restrict__ rho_out,
+                   double* __restrict__ bet, double* __restrict__ scal, Status* st) {
+  extern __shared__ double sh[];  // [c] S^t vs, [c] lrow, [c] g, [1] flag
+  __shared__ double red[32];
+  if (failed(st)) return;
+  double* sv = sh;
+  double* lrow = sh + c;
+  double* g = sh + 2 * c;
+  const double sg = scal[0], rho = scal[1], zn = scal[2];
+  const double nv = __dsqrt_rn(block_sumsq(vs, ell, red));
+  if (nv <= 8.0 * u_high * (zn + rho)) {
+    if (threadIdx.x == 0) fail(st, SQB_ERR_BREAKDOWN, (c + 1) | (1 << 24), nv);
+    return;
+  }
+  double beta = __ddiv_rn(2.0, __dmul_rn(nv, nv));
+  double fac;  // v = v * fac (sqrt2) or v / fac (unit)
+  if (scaling == SQB_SCALE_SQRT2) {
+    fac = __dsqrt_rn(beta);
+    beta = 1.0;
+  } else {
+    const double piv = vs[0];
+    if (fabs(piv) <= 8.0 * u_high * nv) {
+      if (threadIdx.x == 0) fail(st, SQB_ERR_BREAKDOWN, (c + 1) | (2 << 24), piv);
+      return;
+    }
+    fac = piv;
+    beta = __dmul_rn(__dmul_rn(beta, piv), piv);
+  }
+  __syncthreads();  // every thread has read vs[0] before it is rescaled
+  for (int i = threadIdx.x; i < ell; i += TRIM_NT) {
+    const double s = scaling == SQB_SCALE_SQRT2 ? __dmul_rn(vs[i], fac) : __ddiv_rn(vs[i], fac);
+    vs[i] = s;
+    S[i + (int64_t)c * lds] = s;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = warp; k < c; k += TRIM_NT / 32) {
+    double a = 0.0, b = 0.0;
+    for (int i = lane; i < ell; i += 32) {
+      a = fma(S[i + (int64_t)k * lds], vs[i], a);
+      b = fma(E[i + (int64_t)k * lde], vs[i], b);
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+      sv[k] = a;
+      lrow[k] = b;
+      L[c + (int64_t)k * ldl] = b;
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < c; k += TRIM_NT) {  // g = S^t vs - U[:c, :c]^t lrow
+    double d = 0.0;
+    for (int i = k; i < c; ++i) d = fma((double)Lo<T>::load(U[i + (int64_t)k * ldu]), lrow[i], d);
+    g[k] = sv[k] - d;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < c; i += TRIM_NT) {
+    double t = 0.0, tt = 0.0;
+    for (int k = i; k < c; ++k) {
+      t = fma(Tm[i + (int64_t)k * ldt], sv[k], t);
+      tt = fma(Tt[i + (int64_t)k * ldtt], g[k], tt);
+    }
+    Tm[i + (int64_t)c * ldt] = __dmul_rn(-beta, t);
+    Tt[i + (int64_t)c * ldtt] = __dmul_rn(-beta, tt);
+    R[i + (int64_t)c * ldr] = (double)Lo<T>::load(w[i]);
+  }
+  if (threadIdx.x == 0) {
+    Tm[c + (int64_t)c * ldt] = beta;
+    Tt[c + (int64_t)c * ldtt] = beta;
+    R[c + (int64_t)c * ldr] = -sg * rho;
+    sig[c] = sg;
+    rho_out[c] = rho;
+    bet[c] = beta;
+    scal[4] = fac;
+  }
+}
+
+// U[:, c] = [0; v0, w[c+1:]] scaled (trim.py:131-144, then round_to low)
+template <typename T>
+__global__ void trim_ucol_kernel(T* __restrict__ Uc, const T* __restrict__ w, int64_t N, int c, int scaling,
+                                 const double* __restrict__ scal, const Status* st) {
+  if (failed(st)) return;
+  const double fac = scal[4], v0 = scal[3];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < c) {
+      Uc[i] = Lo<T>::store(typename Lo<T>::acc(0));
+      continue;
+    }
+    const double v = i == c ? v0 : (double)Lo<T>::load(w[i]);
+    const double u = scaling == SQB_SCALE_SQRT2 ? __dmul_rn(v, fac) : __ddiv_rn(v, fac);
+    Uc[i] = Lo<T>::store(Lo<T>::from_double(u));
+  }
+}
+
+template <typename T>
+static int trim_left_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+                       int scaling, const void* W, int64_t N, int64_t m, int64_t ldw, void* Uv, int64_t ldu,
+                       double* S, int64_t lds, double* Tm, int64_t ldt, double* Tt, int64_t ldtt, double* R,
+                       int64_t ldr, double* L, int64_t ldl, double* sig, double* rho, double* bet) {
+  const int64_t ell = sk->ell;
+  const size_t esz = sizeof(T);
+  const int64_t ldx = (N + 15) / 16 * 16;
+  WsPlan plan;
+  const size_t ix = plan.add(esz * ldx);
+  const size_t iw = plan.add(esz * ldx);
+  const size_t iz = plan.add(sizeof(double) * ell);
+  const size_t iv = plan.add(sizeof(double) * ell);
+  const size_t ic = plan.add(sizeof(double) * (m + 1));
+  const size_t is = plan.add(sizeof(double) * 8);
+  const size_t iP = plan.add(sketch_partials_bytes(sk, Lo<T>::code, 1));
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  T* x = ws_ptr<T>(ctx, plan, ix);
+  T* w = ws_ptr<T>(ctx, plan, iw);
+  double* z = ws_ptr<double>(ctx, plan, iz);
+  double* vs = ws_ptr<double>(ctx, plan, iv);
+  double* coef = ws_ptr<double>(ctx, plan, ic);
+  double* scal = ws_ptr<double>(ctx, plan, is);
+  void* P = ws_ptr<void>(ctx, plan, iP);
+  T* U = static_cast<T*>(Uv);
+  Status* st = ctx->d_status;
+  cudaStream_t s = ctx->stream;
+  for (double* M : {Tm, Tt, R, L}) {
+    const int64_t ld = M == Tm ? ldt : M == Tt ? ldtt : M == R ? ldr : ldl;
+    SQB_CUDA_TRY(cudaMemset2DAsync(M, ld * sizeof(double), 0, m * sizeof(double), m, s));
+  }
+  const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 4 * ctx->sm_count));
+  const double u_high = 1.0 / 9007199254740992.0;  // 2^-53: the device path computes high in fp64
+  const int64_t rows_per = (int64_t)GEMV_NT * 4 * VecN<T>::n;
+  const unsigned gu = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + rows_per - 1) / rows_per,
+                                                                       2 * ctx->sm_count));
+  for (int64_t c = 0; c < m; ++c) {
+    SQB_CUDA_TRY(cudaMemcpyAsync(w, (const T*)W + c * ldw, esz * N, cudaMemcpyDeviceToDevice, s));
+    if (c > 0) {
+      trim_prep_kernel<T><<<gv, 256, 0, s>>>(x, w, N, 0, m, scales, st);
+      SQB_TRY(check_launch(ctx, "trim_prep_kernel"));
+      SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, z, ell, 0, P, st));
+      trim_coef_kernel<T><<<1, TRIM_NT, sizeof(double) * c, s>>>(S, lds, (int)ell, z, L, ldl, w, Tt, ldtt, (int)c,
+                                                                 coef, st);
+      SQB_TRY(check_launch(ctx, "trim_coef_kernel"));
+      trim_update_kernel<T><<<gu, GEMV_NT, sizeof(typename Lo<T>::acc) * c, s>>>(U, ldu, N, (int)c, coef, w, st);
+      SQB_TRY(check_launch(ctx, "trim_update_kernel"));
+    }
+    trim_prep_kernel<T><<<gv, 256, 0, s>>>(x, w, N, c, m, scales, st);
+    SQB_TRY(check_launch(ctx, "trim_prep_kernel"));
+    SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, z, ell, 0, P, st));
+    trim_tail_kernel<T><<<1, TRIM_NT, 0, s>>>(z, (int)ell, w, (int)c, scales, x, scal, st);
+    SQB_TRY(check_launch(ctx, "trim_tail_kernel"));
+    SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, vs, ell, 0, P, st));
+    trim_finish_kernel<T><<<1, TRIM_NT, sizeof(double) * (3 * c + 1), s>>>(
+        vs, (int)ell, (int)c, scaling, u_high, w, U, ldu, E, lde, S, lds, Tm, ldt, Tt, ldtt, R, ldr, L, ldl, sig,
+        rho, bet, scal, st);
+    SQB_TRY(check_launch(ctx, "trim_finish_kernel"));
+    trim_ucol_kernel<T><<<gv, 256, 0, s>>>(U + c * ldu, w, N, (int)c, scaling, scal, st);
+    SQB_TRY(check_launch(ctx, "trim_ucol_kernel"));
+  }
+  return SQB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the column-scaled operator alone (sketching.py:230-235) and the trimmed
+// thin Q (trim.py:211-225)
+// ---------------------------------------------------------------------------
+template <typename T>
+static int colscaled_apply_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t m, const void* X,
+                             int64_t ldx, int64_t k, double* Y, int64_t ldy) {
+  const int64_t N = sk->n, ldp = (N + 15) / 16 * 16;
+  WsPlan plan;
+  const size_t ix = plan.add(sizeof(T) * ldp);
+  const size_t iP = plan.add(sketch_partials_bytes(sk, Lo<T>::code, 1));
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  T* x = ws_ptr<T>(ctx, plan, ix);
+  void* P = ws_ptr<void>(ctx, plan, iP);
+  const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 4 * ctx->sm_count));
+  for (int64_t j = 0; j < k; ++j) {
+    trim_prep_kernel<T><<<gv, 256, 0, ctx->stream>>>(x, (const T*)X + j * ldx, N, 0, m, scales, ctx->d_status);
+    SQB_TRY(check_launch(ctx, "trim_prep_kernel"));
+    SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldp, 1, Y + j * ldy, ldy, 0, P, ctx->d_status));
+  }
+  return SQB_OK;
+}
+
+int colscaled_apply_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t m, int dtype,
+                             const void* X, int64_t ldx, int64_t k, double* Y, int64_t ldy) {
+  switch (dtype) {
+    case SQB_F64: return colscaled_apply_t<double>(ctx, sk, scales, m, X, ldx, k, Y, ldy);
+    case SQB_F32: return colscaled_apply_t<float>(ctx, sk, scales, m, X, ldx, k, Y, ldy);
+    case SQB_F16: return colscaled_apply_t<__half>(ctx, sk, scales, m, X, ldx, k, Y, ldy);
+    case SQB_BF16: return colscaled_apply_t<__nv_bfloat16>(ctx, sk, scales, m, X, ldx, k, Y, ldy);
+  }
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", dtype);
+}
+
+// M = T triu(S^t E)   (k x k, ld k; T upper so M[i, j] = sum_{l >= i} T[i, l] triu(S^t E)[l, j])
+__global__ void trim_tm_kernel(const double* __restrict__ Tm, int64_t ldt, const double* __restrict__ S,
+                               int64_t lds, const double* __restrict__ E, int64_t lde, int ell, int k,
+                               double* __restrict__ M) {
+  extern __shared__ double G[];  // k x k: triu(S^t E)
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int l = e % k, j = e / k;
+    double d = 0.0;
+    if (l <= j)
+      for (int i = 0; i < ell; ++i) d = fma(S[i + (int64_t)l * lds], E[i + (int64_t)j * lde], d);
+    G[e] = d;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int i = e % k, j = e / k;
+    double d = 0.0;
+    for (int l = i; l <= j; ++l) d = fma(Tm[i + (int64_t)l * ldt], G[l + j * k], d);
+    M[e] = d;
+  }
+}
+
+int thin_q_m_dispatch(sqb_ctx*, int, const void*, int64_t, int64_t, int64_t, const double*, double*, int64_t);
+
+int trim_thin_q_impl(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t k,
+                     const double* Tm, int64_t ldt, const double* S, int64_t lds, const double* E, int64_t lde,
+                     int64_t ell, double* Q, int64_t ldq) {
+  WsPlan plan;
+  const size_t iM = plan.add(sizeof(double) * std::max<int64_t>(1, k * k));
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  double* M = ws_ptr<double>(ctx, plan, iM);
+  const size_t smem = sizeof(double) * k * k;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(trim_tm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  trim_tm_kernel<<<1, 256, smem, ctx->stream>>>(Tm, ldt, S, lds, E, lde, (int)ell, (int)k, M);
+  SQB_TRY(check_launch(ctx, "trim_tm_kernel"));
+  return thin_q_m_dispatch(ctx, lo_dtype, U, ldu, N, k, M, Q, ldq);
+}
+
+int trim_left_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+                       int scaling, int lo_dtype, const void* W, int64_t N, int64_t m, int64_t ldw, void* U,
+                       int64_t ldu, double* S, int64_t lds, double* Tm, int64_t ldt, double* Tt, int64_t ldtt,
+                       double* R, int64_t ldr, double* L, int64_t ldl, double* sig, double* rho, double* bet) {
+#define SQB_TRIM_CALL(TY)                                                                                      \
+  return trim_left_t<TY>(ctx, sk, scales, E, lde, scaling, W, N, m, ldw, U, ldu, S, lds, Tm, ldt, Tt, ldtt, R, \
+                         ldr, L, ldl, sig, rho, bet)
+  switch (lo_dtype) {
+    case SQB_F64: SQB_TRIM_CALL(double);
+    case SQB_F32: SQB_TRIM_CALL(float);
+    case SQB_F16: SQB_TRIM_CALL(__half);
+    case SQB_BF16: SQB_TRIM_CALL(__nv_bfloat16);
+  }
+#undef SQB_TRIM_CALL
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
+}  // namespace sqb

@@ -4,7 +4,7 @@
 // coordinates (sketching.py:216-235): coordinates < m are multiplied by
 // scales[k] in the arithmetic dtype before the base sketch.  Per column c
 // (1-based j = c + 1):
-//   c > 0:  z = Om(w)                       prep + K1
+//   c > 0:  z = Om(W[:, c])                 (all columns in one batched K1)
 //           h = S^t z - L w[:c];  coef = T~^t h          (trim_coef_kernel)
 //           w = fl(w - fl(U[:, :c] coef))                (streaming GEMV)
 //   trim_rh_vector (trim.py:80-146):
@@ -41,6 +41,17 @@ __global__ void trim_prep_kernel(T* __restrict__ x, const T* __restrict__ w, int
     else v = w[i];  // x * 1.0 is exact
     x[i] = v;
   }
+}
+
+// the column-scaled copy of W[:, 1:] (blockIdx.y = column - 1)
+template <typename T>
+__global__ void trim_prep_batch_kernel(T* __restrict__ X, int64_t ldx, const T* __restrict__ W, int64_t ldw,
+                                       int64_t N, int64_t m, const double* __restrict__ scales, const Status* st) {
+  if (failed(st)) return;
+  T* x = X + blockIdx.y * ldx;
+  const T* w = W + (blockIdx.y + 1) * ldw;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = i < m ? Lo<T>::store(Lo<T>::mul(Lo<T>::load(w[i]), Lo<T>::from_double(scales[i]))) : w[i];
 }
 
 // h = S[:, :c]^t z - L[:c, :c] w[:c];  coef = T~[:c, :c]^t h   (trim.py:296-299)
@@ -246,10 +257,16 @@ static int trim_left_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
   const size_t iv = plan.add(sizeof(double) * ell);
   const size_t ic = plan.add(sizeof(double) * (m + 1));
   const size_t is = plan.add(sizeof(double) * 8);
-  const size_t iP = plan.add(sketch_partials_bytes(sk, Lo<T>::code, 1));
+  const size_t iP = plan.add(sketch_partials_bytes(sk, Lo<T>::code, m));
+  // the update sketches z_c = Om(W[:, c]) of the ORIGINAL columns do not
+  // depend on the sweep: one batched K1 over the column-scaled W up front
+  const size_t iXa = plan.add(esz * ldx * (m > 1 ? m - 1 : 1));
+  const size_t iZ0 = plan.add(sizeof(double) * ell * m);
   SQB_TRY(ws_reserve(ctx, plan.total));
   T* x = ws_ptr<T>(ctx, plan, ix);
   T* w = ws_ptr<T>(ctx, plan, iw);
+  T* Xa = ws_ptr<T>(ctx, plan, iXa);
+  double* Z0 = ws_ptr<double>(ctx, plan, iZ0);
   double* z = ws_ptr<double>(ctx, plan, iz);
   double* vs = ws_ptr<double>(ctx, plan, iv);
   double* coef = ws_ptr<double>(ctx, plan, ic);
@@ -267,14 +284,18 @@ static int trim_left_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
   const int64_t rows_per = (int64_t)GEMV_NT * 4 * VecN<T>::n;
   const unsigned gu = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + rows_per - 1) / rows_per,
                                                                        2 * ctx->sm_count));
+  if (m > 1) {
+    const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 2 * ctx->sm_count));
+    trim_prep_batch_kernel<T><<<dim3(gb, (unsigned)(m - 1)), 256, 0, s>>>(Xa, ldx, (const T*)W, ldw, N, m,
+                                                                          scales, st);
+    SQB_TRY(check_launch(ctx, "trim_prep_batch_kernel"));
+    SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, Xa, ldx, m - 1, Z0 + ell, ell, 0, P, st));
+  }
   for (int64_t c = 0; c < m; ++c) {
     SQB_CUDA_TRY(cudaMemcpyAsync(w, (const T*)W + c * ldw, esz * N, cudaMemcpyDeviceToDevice, s));
     if (c > 0) {
-      trim_prep_kernel<T><<<gv, 256, 0, s>>>(x, w, N, 0, m, scales, st);
-      SQB_TRY(check_launch(ctx, "trim_prep_kernel"));
-      SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, z, ell, 0, P, st));
-      trim_coef_kernel<T><<<1, TRIM_NT, sizeof(double) * c, s>>>(S, lds, (int)ell, z, L, ldl, w, Tt, ldtt, (int)c,
-                                                                 coef, st);
+      trim_coef_kernel<T><<<1, TRIM_NT, sizeof(double) * c, s>>>(S, lds, (int)ell, Z0 + c * ell, L, ldl, w, Tt,
+                                                                 ldtt, (int)c, coef, st);
       SQB_TRY(check_launch(ctx, "trim_coef_kernel"));
       trim_update_kernel<T><<<gu, GEMV_NT, sizeof(typename Lo<T>::acc) * c, s>>>(U, ldu, N, (int)c, coef, w, st);
       SQB_TRY(check_launch(ctx, "trim_update_kernel"));

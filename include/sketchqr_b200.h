@@ -211,6 +211,18 @@ int sqb_trim_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
                        double* R, int64_t ldr, double* L, int64_t ldl,
                        double* sigmas, double* rhos, double* betas);
 
+/* Trimmed right-looking RHQR (trim_rhqr_right, trim.py:238-269): per column
+ * the tail reflector, then the trailing block updated through the masked
+ * sketch; T = t_factor_from_sketches(S), T~ = t_tilde_from_factors(S, E, U),
+ * L = tril(S^t E, -1) after the sweep.  Arguments as sqb_trim_rhqr_left.  */
+int sqb_trim_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
+                        const double* E, int64_t lde, int scaling, int lo_dtype,
+                        const void* W, int64_t N, int64_t m, int64_t ldw,
+                        void* U, int64_t ldu, double* S, int64_t lds,
+                        double* T, int64_t ldt, double* Tt, int64_t ldtt,
+                        double* R, int64_t ldr, double* L, int64_t ldl,
+                        double* sigmas, double* rhos, double* betas);
+
 /* The column-scaled operator alone (ColumnScaledSketch._apply,
  * sketching.py:230-235): Y = Omega (X with rows k < m times scales[k] in the
  * arithmetic dtype).  X: sk->n x k (dtype), Y: ell x k fp64.               */

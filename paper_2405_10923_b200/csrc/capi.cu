@@ -23,6 +23,9 @@ int rhqr_block_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int6
 int trim_left_dispatch(sqb_ctx*, const sqb_sketch*, const double*, const double*, int64_t, int, int, const void*,
                        int64_t, int64_t, int64_t, void*, int64_t, double*, int64_t, double*, int64_t, double*,
                        int64_t, double*, int64_t, double*, int64_t, double*, double*, double*);
+int trim_right_dispatch(sqb_ctx*, const sqb_sketch*, const double*, const double*, int64_t, int, int, const void*,
+                        int64_t, int64_t, int64_t, void*, int64_t, double*, int64_t, double*, int64_t, double*,
+                        int64_t, double*, int64_t, double*, int64_t, double*, double*, double*);
 int colscaled_apply_dispatch(sqb_ctx*, const sqb_sketch*, const double*, int64_t, int, const void*, int64_t,
                              int64_t, double*, int64_t);
 int trim_thin_q_impl(sqb_ctx*, int, const void*, int64_t, int64_t, int64_t, const double*, int64_t,
@@ -251,6 +254,32 @@ int sqb_trim_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
     return set_error(ctx, SQB_ERR_ARG, "U must be 16-byte aligned with a 16-byte multiple leading dimension");
   SQB_TRY(trim_left_dispatch(ctx, sk, scales, E, lde, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, T, ldt, Tt,
                              ldtt, R, ldr, L, ldl, sigmas, rhos, betas));
+  return SQB_OK;
+}
+
+int sqb_trim_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+                        int scaling, int lo_dtype, const void* W, int64_t N, int64_t m, int64_t ldw, void* U,
+                        int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt, double* Tt, int64_t ldtt,
+                        double* R, int64_t ldr, double* L, int64_t ldl, double* sigmas, double* rhos,
+                        double* betas) {
+  // the same argument contract as sqb_trim_rhqr_left (validated there with a
+  // dry run of the checks only)
+  SQB_TRY(prep(ctx));
+  SQB_TRY(check_dtype(ctx, lo_dtype));
+  SQB_TRY(validate_sketch(ctx, sk));
+  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
+    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
+  if (m < 1) return set_error(ctx, SQB_ERR_ARG, "need at least one column");
+  if (sk->n != N)
+    return set_error(ctx, SQB_ERR_ARG, "sketch takes %lld coordinates, W has %lld rows", (long long)sk->n,
+                     (long long)N);
+  if (m > N) return set_error(ctx, SQB_ERR_ARG, "cannot normalize %lld leading columns of %lld inputs",
+                              (long long)m, (long long)N);
+  if (!scales || !E || lde < sk->ell) return set_error(ctx, SQB_ERR_ARG, "column-scaled operator without scales/E");
+  if (ldw < N || ldu < N || lds < sk->ell || ldt < m || ldtt < m || ldr < m || ldl < m)
+    return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
+  SQB_TRY(trim_right_dispatch(ctx, sk, scales, E, lde, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, T, ldt, Tt,
+                              ldtt, R, ldr, L, ldl, sigmas, rhos, betas));
   return SQB_OK;
 }
 

@@ -387,6 +387,189 @@ int trim_thin_q_impl(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int
   return thin_q_m_dispatch(ctx, lo_dtype, U, ldu, N, k, M, Q, ldq);
 }
 
+// ---------------------------------------------------------------------------
+// Right-looking trimmed RHQR (trim.py:238-269): per column the reflector of
+// the tail (same kernels as the left sweep), then the trailing columns are
+// updated through the masked sketch; T, T~ and L are assembled from S, E and
+// U after the sweep (t_factor_from_sketches, t_tilde_from_factors).
+// ---------------------------------------------------------------------------
+// X[:, j] = column-scaled copy of Y[:, j] with rows < c0 zeroed (trim.py:256-258)
+template <typename T>
+__global__ void trim_mask_batch_kernel(T* __restrict__ X, int64_t ldx, const T* __restrict__ Y, int64_t ldy,
+                                       int64_t N, int64_t c0, int64_t m, const double* __restrict__ scales,
+                                       const Status* st) {
+  if (failed(st)) return;
+  T* x = X + blockIdx.y * ldx;
+  const T* y = Y + blockIdx.y * ldy;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = i < c0 ? Lo<T>::store(typename Lo<T>::acc(0))
+                  : (i < m ? Lo<T>::store(Lo<T>::mul(Lo<T>::load(y[i]), Lo<T>::from_double(scales[i]))) : y[i]);
+}
+
+// coef[j] = beta (s^t X[:, j]) in fp64 (trim.py:260)
+__global__ void trim_rcoef_kernel(const double* __restrict__ s, const double* __restrict__ Xs, int64_t ldx, int ell,
+                                  const double* __restrict__ bet, int c, double* __restrict__ coef, const Status* st) {
+  __shared__ double red[32];
+  if (failed(st)) return;
+  const int j = blockIdx.x;
+  double d = 0.0;
+  for (int i = threadIdx.x; i < ell; i += blockDim.x) d = fma(s[i], Xs[i + (int64_t)j * ldx], d);
+  d = block_sum(d, red);
+  if (threadIdx.x == 0) coef[j] = __dmul_rn(bet[c], d);
+}
+
+// Y[:, j] = fl(Y[:, j] - fl(u coef_lo[j]))  (trim.py:261-263: np.outer, then subtract)
+template <typename T>
+__global__ void trim_rank1_kernel(const T* __restrict__ u, const double* __restrict__ coef, T* __restrict__ Y,
+                                  int64_t ldy, int64_t N, const Status* st) {
+  using A = typename Lo<T>::acc;
+  if (failed(st)) return;
+  const A cj = Lo<T>::from_double(coef[blockIdx.y]);
+  T* y = Y + blockIdx.y * ldy;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = Lo<T>::store(Lo<T>::sub(Lo<T>::load(y[i]), Lo<T>::mul(Lo<T>::load(u[i]), cj)));
+}
+
+// A^t (for T~^t = -A^{-1}, trim.py:189-208), the identity, and L = tril(S^t E, -1)
+template <typename T>
+__global__ void trim_tilde_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict__ E,
+                                  int64_t lde, int ell, const T* __restrict__ U, int64_t ldu, int m,
+                                  double* __restrict__ At, double* __restrict__ I, double* __restrict__ L,
+                                  int64_t ldl, double* __restrict__ Lt) {
+  // Lt[i, k] = <s_i, e_k> for k < i (scratch m x m, also written to L)
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x) {
+    const int i = e % m, k = e / m;
+    double d = 0.0;
+    if (k < i)
+      for (int r = 0; r < ell; ++r) d = fma(S[r + (int64_t)i * lds], E[r + (int64_t)k * lde], d);
+    Lt[e] = d;
+    L[i + (int64_t)k * ldl] = d;
+  }
+  __syncthreads();
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x) {
+    const int i = e % m, k = e / m;
+    double corr = 0.0;  // (Lt U[:m])[i, k] = sum_{k <= l < i} Lt[i, l] U[l, k]
+    for (int l = k; l < i; ++l) corr = fma(Lt[i + l * m], (double)Lo<T>::load(U[l + (int64_t)k * ldu]), corr);
+    double g = 0.0;
+    if (k <= i)
+      for (int r = 0; r < ell; ++r) g = fma(S[r + (int64_t)i * lds], S[r + (int64_t)k * lds], g);
+    double a = corr;
+    if (k < i) a = __dsub_rn(a, g);
+    else if (k == i) a = __dsub_rn(a, g / 2.0);
+    At[k + (int64_t)i * m] = a;  // A^t[k, i] = A[i, k]
+    I[e] = i == k ? 1.0 : 0.0;
+  }
+}
+
+__global__ void trim_negate_kernel(const double* __restrict__ X, int m, double* __restrict__ Tt, int64_t ldtt) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x)
+    Tt[e % m + (int64_t)(e / m) * ldtt] = -X[e];
+}
+
+template <typename T>
+static int trim_right_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+                        int scaling, const void* W, int64_t N, int64_t m, int64_t ldw, void* Uv, int64_t ldu,
+                        double* S, int64_t lds, double* Tm, int64_t ldt, double* Tt, int64_t ldtt, double* R,
+                        int64_t ldr, double* L, int64_t ldl, double* sig, double* rho, double* bet) {
+  const int64_t ell = sk->ell;
+  const size_t esz = sizeof(T);
+  const int64_t ldx = (N + 15) / 16 * 16;
+  T* U = static_cast<T*>(Uv);
+  cudaStream_t s = ctx->stream;
+  Status* st = ctx->d_status;
+  {
+    WsPlan plan;
+    const size_t iWl = plan.add(esz * ldx * m);                       // working copy of W
+    const size_t iXm = plan.add(esz * ldx * (m > 1 ? m - 1 : 1));     // masked, scaled trailing block
+    const size_t ix = plan.add(esz * ldx);
+    const size_t iz = plan.add(sizeof(double) * ell);
+    const size_t iv = plan.add(sizeof(double) * ell);
+    const size_t iY = plan.add(sizeof(double) * ell * m);
+    const size_t ic = plan.add(sizeof(double) * (m + 1));
+    const size_t is = plan.add(sizeof(double) * 8);
+    const size_t iP = plan.add(sketch_partials_bytes(sk, Lo<T>::code, m));
+    SQB_TRY(ws_reserve(ctx, plan.total));
+    T* Wl = ws_ptr<T>(ctx, plan, iWl);
+    T* Xm = ws_ptr<T>(ctx, plan, iXm);
+    T* x = ws_ptr<T>(ctx, plan, ix);
+    double* z = ws_ptr<double>(ctx, plan, iz);
+    double* vs = ws_ptr<double>(ctx, plan, iv);
+    double* Yx = ws_ptr<double>(ctx, plan, iY);
+    double* coef = ws_ptr<double>(ctx, plan, ic);
+    double* scal = ws_ptr<double>(ctx, plan, is);
+    void* P = ws_ptr<void>(ctx, plan, iP);
+    SQB_CUDA_TRY(cudaMemcpy2DAsync(Wl, ldx * esz, W, ldw * esz, N * esz, m, cudaMemcpyDeviceToDevice, s));
+    for (double* M : {Tm, Tt, R, L}) {
+      const int64_t ld = M == Tm ? ldt : M == Tt ? ldtt : M == R ? ldr : ldl;
+      SQB_CUDA_TRY(cudaMemset2DAsync(M, ld * sizeof(double), 0, m * sizeof(double), m, s));
+    }
+    const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 4 * ctx->sm_count));
+    const double u_high = 1.0 / 9007199254740992.0;
+    for (int64_t c = 0; c < m; ++c) {
+      T* w = Wl + c * ldx;
+      trim_prep_kernel<T><<<gv, 256, 0, s>>>(x, w, N, c, m, scales, st);
+      SQB_TRY(check_launch(ctx, "trim_prep_kernel"));
+      SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, z, ell, 0, P, st));
+      trim_tail_kernel<T><<<1, TRIM_NT, 0, s>>>(z, (int)ell, w, (int)c, scales, x, scal, st);
+      SQB_TRY(check_launch(ctx, "trim_tail_kernel"));
+      SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, vs, ell, 0, P, st));
+      // the left sweep's finish kernel also grows T, T~ and L; the right
+      // variant overwrites them below with the reference's assembled forms
+      trim_finish_kernel<T><<<1, TRIM_NT, sizeof(double) * (3 * c + 1), s>>>(
+          vs, (int)ell, (int)c, scaling, u_high, w, U, ldu, E, lde, S, lds, Tm, ldt, Tt, ldtt, R, ldr, L, ldl, sig,
+          rho, bet, scal, st);
+      SQB_TRY(check_launch(ctx, "trim_finish_kernel"));
+      trim_ucol_kernel<T><<<gv, 256, 0, s>>>(U + c * ldu, w, N, (int)c, scaling, scal, st);
+      SQB_TRY(check_launch(ctx, "trim_ucol_kernel"));
+      const int64_t k = m - c - 1;
+      if (k > 0) {
+        const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 2 * ctx->sm_count));
+        trim_mask_batch_kernel<T><<<dim3(gb, (unsigned)k), 256, 0, s>>>(Xm, ldx, w + ldx, ldx, N, c, m, scales, st);
+        SQB_TRY(check_launch(ctx, "trim_mask_batch_kernel"));
+        SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, Xm, ldx, k, Yx, ell, 0, P, st));
+        trim_rcoef_kernel<<<(unsigned)k, 256, 0, s>>>(S + c * lds, Yx, ell, (int)ell, bet, (int)c, coef, st);
+        SQB_TRY(check_launch(ctx, "trim_rcoef_kernel"));
+        trim_rank1_kernel<T><<<dim3(gb, (unsigned)k), 256, 0, s>>>(U + c * ldu, coef, w + ldx, ldx, N, st);
+        SQB_TRY(check_launch(ctx, "trim_rank1_kernel"));
+      }
+    }
+  }
+  // T = t_factor_from_sketches(S) (rhqr.py:122-132); may reuse the workspace
+  SQB_TRY(sqb_t_factor(ctx, S, lds, ell, m, Tm, ldt));
+  WsPlan plan;
+  const size_t iA = plan.add(sizeof(double) * m * m);
+  const size_t iI = plan.add(sizeof(double) * m * m);
+  const size_t iX = plan.add(sizeof(double) * m * m);
+  const size_t iL = plan.add(sizeof(double) * m * m);
+  SQB_TRY(ws_reserve(ctx, plan.total));
+  double* At = ws_ptr<double>(ctx, plan, iA);
+  double* I = ws_ptr<double>(ctx, plan, iI);
+  double* X = ws_ptr<double>(ctx, plan, iX);
+  double* Lt = ws_ptr<double>(ctx, plan, iL);
+  trim_tilde_kernel<T><<<1, 256, 0, s>>>(S, lds, E, lde, (int)ell, U, ldu, (int)m, At, I, L, ldl, Lt);
+  SQB_TRY(check_launch(ctx, "trim_tilde_kernel"));
+  SQB_TRY(sqb_upper_tri_solve(ctx, At, m, m, I, m, m, X, m));
+  trim_negate_kernel<<<(unsigned)std::max<int64_t>(1, (m * m + 255) / 256), 256, 0, s>>>(X, (int)m, Tt, ldtt);
+  return check_launch(ctx, "trim_negate_kernel");
+}
+
+int trim_right_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+                        int scaling, int lo_dtype, const void* W, int64_t N, int64_t m, int64_t ldw, void* U,
+                        int64_t ldu, double* S, int64_t lds, double* Tm, int64_t ldt, double* Tt, int64_t ldtt,
+                        double* R, int64_t ldr, double* L, int64_t ldl, double* sig, double* rho, double* bet) {
+#define SQB_TRIM_CALL(TY)                                                                                       \
+  return trim_right_t<TY>(ctx, sk, scales, E, lde, scaling, W, N, m, ldw, U, ldu, S, lds, Tm, ldt, Tt, ldtt, R, \
+                          ldr, L, ldl, sig, rho, bet)
+  switch (lo_dtype) {
+    case SQB_F64: SQB_TRIM_CALL(double);
+    case SQB_F32: SQB_TRIM_CALL(float);
+    case SQB_F16: SQB_TRIM_CALL(__half);
+    case SQB_BF16: SQB_TRIM_CALL(__nv_bfloat16);
+  }
+#undef SQB_TRIM_CALL
+  return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+}
+
 int trim_left_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
                        int scaling, int lo_dtype, const void* W, int64_t N, int64_t m, int64_t ldw, void* U,
                        int64_t ldu, double* S, int64_t lds, double* Tm, int64_t ldt, double* Tt, int64_t ldtt,

@@ -7,9 +7,9 @@ is wrapped so its m leading columns sketch to unit vectors
 two compact-form triangles (T in creation order, T~ reversed) and the
 strictly lower table L[i, k] = <Omega u_i, Omega e_k>.
 
-`trim_rhqr_left` runs the whole column sweep on the device
-(csrc/trim.cu: column-scaled K1 sketches, single-CTA sketch-space kernels,
-a streaming GEMV update); this module validates arguments exactly as the
+`trim_rhqr_left` / `trim_rhqr_right` run the whole column sweep on the
+device (csrc/trim.cu: column-scaled K1 sketches, single-CTA sketch-space
+kernels, a streaming GEMV or rank-1 update); this module validates arguments exactly as the
 reference does, builds the wrapper (a one-time sketch construction, like the
 SRHT's signs), moves operands across the boundary and maps device status
 words to the reference's exceptions.
@@ -164,13 +164,27 @@ def _raise_trim_status(ctx):
             raise BreakdownError(f"sketched reflector vector cancelled at column {j} "
                                  f"(degenerate sketch geometry, norm {val:.3e})")
         raise BreakdownError(f"unit scaling pivot vanished at column {j} (sketched entry {val:.3e})")
-    raise _lib.SketchQRError(f"trim_rhqr_left: device status {code} at column {col}")
+    if code == _lib.SQB_ERR_SINGULAR:
+        from .linalg import SingularFactorError
+        raise SingularFactorError("triangular factor has zero or subnormal diagonal")
+    raise _lib.SketchQRError(f"trimmed factorization: device status {code} at column {col}")
 
 
 def trim_rhqr_left(W, omega, scaling=SCALE_SQRT2, policy=None):
     """trim.py:272-325: left-looking trimmed factorization maintaining both
     triangles; column j is transformed by the reversed compact form
     w -= U T~^t (S^t (Omega w) - L w_head), then reflected from its tail."""
+    return _trim_run("sqb_trim_rhqr_left", W, omega, scaling, policy)
+
+
+def trim_rhqr_right(W, omega, scaling=SCALE_SQRT2, policy=None):
+    """trim.py:238-269: right-looking trimmed factorization; each reflector
+    updates the trailing columns through the masked sketch, and T, T~ and L
+    are assembled from S and E after the sweep."""
+    return _trim_run("sqb_trim_rhqr_right", W, omega, scaling, policy)
+
+
+def _trim_run(entry, W, omega, scaling, policy):
     check_scaling(scaling)
     policy = policy or DOUBLE_POLICY
     require_device_policy(policy)
@@ -193,11 +207,11 @@ def trim_rhqr_left(W, omega, scaling=SCALE_SQRT2, policy=None):
     L = empty_colmajor(m, m, "double")
     scal = torch.empty(3 * m, dtype=torch.float64, device=Wd.device)
     ctx = _lib.context()
-    ctx.check(_lib.lib().sqb_trim_rhqr_left(
+    ctx.check(getattr(_lib.lib(), entry)(
         ctx.h, omega.desc(), sc.data_ptr(), Ed.data_ptr(), ld_of(Ed), scaling_code(scaling), CODES[tag],
         Wd.data_ptr(), n, m, ld_of(Wd), U.data_ptr(), ld_of(U), S.data_ptr(), ld_of(S), T.data_ptr(), ld_of(T),
         Tt.data_ptr(), ld_of(Tt), R.data_ptr(), ld_of(R), L.data_ptr(), ld_of(L), scal.data_ptr(),
-        scal.data_ptr() + 8 * m, scal.data_ptr() + 16 * m), "sqb_trim_rhqr_left")
+        scal.data_ptr() + 8 * m, scal.data_ptr() + 16 * m), entry)
     _raise_trim_status(ctx)
     o = (lambda t: to_numpy(t)) if host else (lambda t: t)
     return TrimFactors(U=o(U), S=o(S), T=o(T), T_tilde=o(Tt), R=o(R), L=o(L),

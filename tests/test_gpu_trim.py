@@ -54,6 +54,21 @@ def test_trim_rhqr_left_matches_reference(P, pre, scaling):
         assert rel(Q @ F.R, g["W"]) <= 1e-13
 
 
+@pytest.mark.parametrize("scaling", ["sqrt2", "unit"])
+def test_trim_rhqr_right_matches_reference(P, scaling):
+    g = golden("trim_2048x16_srht12")
+    om = P.SRHTSketch(int(g["ell"]), g["W"].shape[0], int(g["seed"]))
+    F = P.trim_rhqr_right(g["W"], om, scaling=scaling)
+    if scaling == "sqrt2":
+        for k in KEYS:
+            assert rel(getattr(F, k), g["right_" + k]) <= 1e-12, k
+    # left and right agree (test_trim.py:84-91) and both reconstruct W
+    Fl = P.trim_rhqr_left(g["W"], om, scaling=scaling)
+    assert rel(F.R, Fl.R) <= 1e-11
+    assert rel(F.T_tilde, Fl.T_tilde) <= 1e-10
+    assert rel(P.trim_thin_q(F) @ F.R, g["W"]) <= 1e-13
+
+
 @pytest.mark.parametrize("tag", ["single", "bf16"])
 def test_trim_rhqr_left_low_precision_against_oracle(P, tag):
     rng = np.random.default_rng(5)

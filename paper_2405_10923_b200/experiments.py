@@ -21,8 +21,8 @@ instead of re-materialising every prefix as the reference does
     values); the small SVDs run on the device.
 The CSV writer is byte-compatible with experiments.py:318-339 (%.17g).
 
-Methods outside the hot path (trimRHQR, RGS/CGS/MGS, randomized Cholesky QR,
-RGS-GMRES; SURVEY §2 rows 11, 13, 16) raise NotImplementedError.
+Methods outside the hot path (RGS/CGS/MGS, randomized Cholesky QR,
+RGS-GMRES; SURVEY §2 rows 11, 13) raise NotImplementedError.
 """
 
 from __future__ import annotations
@@ -44,6 +44,7 @@ from .precision import PrecisionRangeError, policy_from_tag, require_device_poli
 from .rhqr import (apply_reflectors_compact, householder_qr, rec_rhqr, rhqr_block, rhqr_left, rhqr_right,
                    thin_q)
 from .sketching import make_sketch
+from .trim import trim_rhqr_left, trim_rhqr_right, trim_thin_q
 from .workloads import gen_cmatrix as _gen_cmatrix
 
 FACTOR_ALGOS = ("rhqr-left", "rhqr-right", "rhqr-block", "rec-rhqr",
@@ -51,7 +52,7 @@ FACTOR_ALGOS = ("rhqr-left", "rhqr-right", "rhqr-block", "rec-rhqr",
                 "hqr", "rcholqr")
 EMBEDDED_ALGOS = ("rhqr-left", "rhqr-right", "rhqr-block", "rec-rhqr")
 RERUN_ALGOS = ("rec-rhqr", "rcholqr")
-DEVICE_ALGOS = ("rhqr-left", "rhqr-right", "rhqr-block", "rec-rhqr", "hqr")
+DEVICE_ALGOS = ("rhqr-left", "rhqr-right", "rhqr-block", "rec-rhqr", "trim-left", "trim-right", "hqr")
 
 
 class MetricRow(NamedTuple):
@@ -180,6 +181,10 @@ def _factor_once(Wd, config, policy, ell):
     n, m = Wd.shape
     algo = config.algo
     omega = make_sketch(config.sketch, ell, n - m, config.seed, s=config.s) if algo in EMBEDDED_ALGOS else None
+    if algo in ("trim-left", "trim-right"):  # the trimmed drivers sketch all n coordinates
+        omega = make_sketch(config.sketch, ell, n, config.seed, s=config.s)
+        fn = trim_rhqr_left if algo == "trim-left" else trim_rhqr_right
+        return fn(Wd, omega, scaling=config.scaling, policy=policy)
     if algo == "rhqr-left":
         return rhqr_left(Wd, omega, scaling=config.scaling, policy=policy)
     if algo == "rhqr-right":
@@ -195,6 +200,9 @@ def _qr_of(out, algo):
     """(Q, R, Psi Q) of a full-width factorization object (experiments.py:189-209)."""
     if algo == "hqr":
         return out.Q, out.R, out.Q
+    if algo.startswith("trim"):  # experiments.py:196-199
+        Q = trim_thin_q(out)
+        return Q, out.R, out.omega.apply(Q)
     Q = thin_q(out)
     return Q, out.R, out.psi.apply(Q)
 

@@ -316,6 +316,17 @@ def trim_cases():
     except Exception as e:  # BreakdownError
         msg = str(e)
     save("trim_breakdown", W=Wd, seed=37, ell=12, msg=np.array(msg))
+    # the stability-sweep harness on the trimmed drivers (experiments.py:161-164, 196-199)
+    from sketchqr.experiments import ExperimentConfig, run_factor_experiment
+    Wx = rng.standard_normal((2048, 24)) * np.logspace(0, -4, 24)
+    out = {}
+    for name, algo in (("trimleft", "trim-left"), ("trimright", "trim-right")):
+        rows = run_factor_experiment(Wx, ExperimentConfig(algo=algo, ell=20, seed=3, every=6,
+                                                          deterministic=True))
+        out[f"{name}_j"] = np.array([r[0] for r in rows], dtype=np.int64)
+        out[f"{name}_vals"] = np.array([list(r[1:-1]) for r in rows], dtype=np.float64)
+        out[f"{name}_status"] = np.array([r[-1] for r in rows])
+    save("experiments_trim", W=Wx, **out)
 
 
 SECTIONS = dict(srht=srht_cases, gauss=gauss_cases, rh_vector=rh_vector_cases, rhqr=rhqr_cases,

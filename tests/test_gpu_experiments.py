@@ -94,3 +94,17 @@ def test_gmres_identity_closes_immediately(P):
                                   P.ExperimentConfig(algo="rhqr", sketch="gauss", seed=1))
     assert len(rows) == 1 and rows[0].status == str(g["eye_status"][0]) == "closed@1"
     assert rows[0].true_resid <= 1e-12 * np.linalg.norm(g["b"][:32])
+
+
+@pytest.mark.parametrize("name,algo", [("trimleft", "trim-left"), ("trimright", "trim-right")])
+def test_trim_factor_sweep_matches_reference(P, name, algo):
+    """The trimmed drivers in the harness (experiments.py:161-164, 196-199):
+    ell = 20 < m = 24, so orth_err is O(1) by design and compared as a value."""
+    g = golden("experiments_trim")
+    rows = P.run_factor_experiment(g["W"], P.ExperimentConfig(algo=algo, ell=20, seed=3, every=6))
+    assert [r.j for r in rows] == g[f"{name}_j"].tolist()
+    assert [r.status for r in rows] == g[f"{name}_status"].tolist()
+    for r, want in zip(rows, g[f"{name}_vals"]):
+        got = np.array(r[1:-1], dtype=float)
+        assert got[[0, 1, 4]] == pytest.approx(want[[0, 1, 4]], rel=1e-8)
+        assert np.all(got[2:4] <= 10.0 * want[2:4] + 1e-14), (got, want)

@@ -28,7 +28,7 @@ def test_config_validation():
     with pytest.raises(ValueError):
         E.run_factor_experiment(np.eye(4), E.ExperimentConfig(algo="qr-but-wrong"))
     with pytest.raises(NotImplementedError):
-        E.run_factor_experiment(np.eye(4), E.ExperimentConfig(algo="trim-left"))
+        E.run_factor_experiment(np.eye(4), E.ExperimentConfig(algo="mgs"))
     with pytest.raises(ValueError):
         E.run_gmres_experiment(np.eye(4), np.ones(4), 2, E.ExperimentConfig(algo="hqr"))
     with pytest.raises(NotImplementedError):

@@ -20,9 +20,13 @@ constexpr int HQR_NT = 1024;
 
 // K5: left-looking Householder QR with compact T of Z (od x m), fp64 throughout.
 // Writes S = U_z (od x m), T, R (m x m), sigmas/rhos/betas.
+// RES: S and T live in shared memory for the whole factorization (every
+// column re-reads all previous reflectors and T: shared-memory latency instead
+// of L2 latency on the dependent chain) and are written out at the end.
+template <bool RES>
 __global__ void __launch_bounds__(HQR_NT)
-hqr_kernel(const double* __restrict__ Z, int64_t ldz, int od, int m, int scaling, double* S,
-           int64_t lds, double* T, int64_t ldt, double* R, int64_t ldr, double* sig, double* rhos,
+hqr_kernel(const double* __restrict__ Z, int64_t ldz, int od, int m, int scaling, double* Sg,
+           int64_t ldsg, double* Tg, int64_t ldtg, double* R, int64_t ldr, double* sig, double* rhos,
            double* bets, Status* st) {
   extern __shared__ double sm[];
   double* w = sm;          // [od]
@@ -31,6 +35,10 @@ hqr_kernel(const double* __restrict__ Z, int64_t ldz, int od, int m, int scaling
   double* red = cf + m;    // [32]
   __shared__ double scal[4];
   if (failed(st)) return;
+  double* S = RES ? red + 32 : Sg;
+  const int64_t lds = RES ? od : ldsg;
+  double* T = RES ? S + (int64_t)od * m : Tg;
+  const int64_t ldt = RES ? m : ldtg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = HQR_NT / 32;
   for (int e = tid; e < m * m; e += HQR_NT) {
     T[(e % m) + (int64_t)(e / m) * ldt] = 0.0;
@@ -109,6 +117,10 @@ hqr_kernel(const double* __restrict__ Z, int64_t ldz, int od, int m, int scaling
     }
     if (tid == 0) T[c + (int64_t)c * ldt] = bo;
     __syncthreads();
+  }
+  if (RES) {
+    for (int e = tid; e < od * m; e += HQR_NT) Sg[(e % od) + (int64_t)(e / od) * ldsg] = S[e];
+    for (int e = tid; e < m * m; e += HQR_NT) Tg[(e % m) + (int64_t)(e / m) * ldtg] = T[e];
   }
 }
 
@@ -317,8 +329,10 @@ trsm_dmma_kernel(const T* __restrict__ W2, int64_t ldw, int64_t n, int m, int mp
 // With the solve removed the same kernel moves its 4.3 GB in 0.68 ms
 // (6.25 TB/s), so what remains is the latency of the per-tile solve chain
 // (two warps run the 16-step diagonal substitutions while six wait).
-constexpr int TP_ROWS = 64, TP_NT = 256, TP_LDX = 72, TP_MP = 64, TP_LDM = 68;
-constexpr size_t TP_SMEM = sizeof(double) * ((size_t)2 * TP_MP * TP_LDX + (size_t)TP_MP * TP_LDM + TP_MP);
+constexpr int TP_ROWS = 64, TP_NT = 256, TP_LDX = 68, TP_MP = 64, TP_LDM = 68;
+// + the diagonal blocks transposed (row j of block b contiguous: pairs of
+// M[j, k] for the substitution, loaded two at a time)
+constexpr size_t TP_SMEM = sizeof(double) * ((size_t)2 * TP_MP * TP_LDX + (size_t)TP_MP * TP_LDM + TP_MP + (size_t)TP_MP * 16);
 
 __global__ void __launch_bounds__(TP_NT, 2)
 trsm_pipe_kernel(const double* __restrict__ W2, int64_t ldw, int64_t n, int m, int mp,
@@ -326,6 +340,7 @@ trsm_pipe_kernel(const double* __restrict__ W2, int64_t ldw, int64_t n, int m, i
   extern __shared__ __align__(16) double tps[];
   double* Ms = tps + 2 * TP_MP * TP_LDX;  // column-major, ld TP_LDM
   double* rinv = Ms + TP_MP * TP_LDM;
+  double* DT = rinv + TP_MP;  // [mp/16][16][16]: DT[b][j][k] = M[16b + j, 16b + k] for k > j
   if (failed(st)) return;
   const int tid = threadIdx.x;
   for (int e = tid; e < mp * mp; e += TP_NT) {
@@ -333,6 +348,11 @@ trsm_pipe_kernel(const double* __restrict__ W2, int64_t ldw, int64_t n, int m, i
     Ms[c * TP_LDM + r] = (r < m && c < m) ? M[r + (int64_t)c * m] : (r == c ? 1.0 : 0.0);
   }
   for (int e = tid; e < mp; e += TP_NT) rinv[e] = e < m ? 1.0 / M[e + (int64_t)e * m] : 1.0;
+  for (int e = tid; e < mp * 16; e += TP_NT) {
+    const int b = e >> 8, j = (e >> 4) & 15, k = e & 15;
+    const int r = 16 * b + j, c = 16 * b + k;
+    DT[e] = (k > j && r < m && c < m) ? M[r + (int64_t)c * m] : 0.0;
+  }
   // padding columns m..mp-1 stay zero in both buffers (never loaded)
   for (int e = tid; e < 2 * TP_MP * TP_LDX; e += TP_NT) {
     const int c = (e % (TP_MP * TP_LDX)) / TP_LDX;
@@ -386,11 +406,16 @@ trsm_pipe_kernel(const double* __restrict__ W2, int64_t ldw, int64_t n, int m, i
         double x[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) x[j] = X[(16 * b + j) * TP_LDX + tid];
+        const double2* dt2 = reinterpret_cast<const double2*>(DT + 256 * b);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           x[j] = x[j] * rinv[16 * b + j];
 #pragma unroll
-          for (int k = j + 1; k < 16; ++k) x[k] = fma(-x[j], Ms[(16 * b + k) * TP_LDM + 16 * b + j], x[k]);
+          for (int p2 = (j + 1) / 2; p2 < 8; ++p2) {  // same ops, same order: k = j+1 .. 15
+            const double2 mm = dt2[8 * j + p2];
+            if (2 * p2 > j) x[2 * p2] = fma(-x[j], mm.x, x[2 * p2]);
+            x[2 * p2 + 1] = fma(-x[j], mm.y, x[2 * p2 + 1]);
+          }
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) X[(16 * b + j) * TP_LDX + tid] = x[j];
@@ -432,9 +457,17 @@ int rec_finish_t(sqb_ctx* ctx, int scaling, const double* Z, int64_t od, int64_t
   Status* st = ctx->d_status;
   // K5: householder_qr(Z) (rhqr.py:383)
   const size_t hsm = sizeof(double) * (od + 2 * m + 32);
-  cudaFuncSetAttribute(hqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(hsm, 48 << 10));
-  hqr_kernel<<<1, HQR_NT, hsm, ctx->stream>>>(Z, od, (int)od, (int)m, scaling, S, lds, Tm, ldt, R, ldr,
-                                              sigmas, rhos, betas, st);
+  const size_t hsm_res = hsm + sizeof(double) * ((size_t)od * m + (size_t)m * m);
+  if (hsm_res <= 227 * 1024) {
+    cudaFuncSetAttribute(hqr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm_res);
+    hqr_kernel<true><<<1, HQR_NT, hsm_res, ctx->stream>>>(Z, od, (int)od, (int)m, scaling, S, lds, Tm, ldt, R, ldr,
+                                                          sigmas, rhos, betas, st);
+  } else {
+    cudaFuncSetAttribute(hqr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max<size_t>(hsm, 48 << 10));
+    hqr_kernel<false><<<1, HQR_NT, hsm, ctx->stream>>>(Z, od, (int)od, (int)m, scaling, S, lds, Tm, ldt, R, ldr,
+                                                       sigmas, rhos, betas, st);
+  }
   SQB_TRY(check_launch(ctx, "hqr_kernel"));
   // Mfac = triu(T^t S^t Z) and its diagonal check (rhqr.py:387-391)
   mfac_kernel<<<(unsigned)m, 256, sizeof(double) * m, ctx->stream>>>(S, lds, Tm, ldt, Z, od, (int)od, (int)m, M, st);
@@ -575,8 +608,16 @@ extern "C" int sqb_householder_qr(sqb_ctx* ctx, int scaling, const double* A, in
     return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
   const size_t hsm = sizeof(double) * (p + 2 * m + 32);
   if (hsm > 200 * 1024) return set_error(ctx, SQB_ERR_ARG, "householder_qr: p too large for the single-CTA kernel");
-  cudaFuncSetAttribute(hqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(hsm, 48 << 10));
-  hqr_kernel<<<1, HQR_NT, hsm, ctx->stream>>>(A, lda, (int)p, (int)m, scaling, U, ldu, T, ldt, R, ldr, sigmas, rhos,
-                                              betas, ctx->d_status);
+  const size_t hsm_res = hsm + sizeof(double) * ((size_t)p * m + (size_t)m * m);
+  if (hsm_res <= 227 * 1024) {
+    cudaFuncSetAttribute(hqr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm_res);
+    hqr_kernel<true><<<1, HQR_NT, hsm_res, ctx->stream>>>(A, lda, (int)p, (int)m, scaling, U, ldu, T, ldt, R, ldr,
+                                                          sigmas, rhos, betas, ctx->d_status);
+  } else {
+    cudaFuncSetAttribute(hqr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max<size_t>(hsm, 48 << 10));
+    hqr_kernel<false><<<1, HQR_NT, hsm, ctx->stream>>>(A, lda, (int)p, (int)m, scaling, U, ldu, T, ldt, R, ldr,
+                                                       sigmas, rhos, betas, ctx->d_status);
+  }
   return check_launch(ctx, "hqr_kernel");
 }

@@ -261,6 +261,13 @@ int sqb_rec_rhqr(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
  * is bitwise identical to the single-GPU factorization. */
 int sqb_nccl_unique_id(char* out, int size);
 int sqb_ctx_init_comm(sqb_ctx* ctx, const char* id, int nranks, int rank);
+
+/* Halo ranges of the row-partitioned SpMV in the distributed RHQR-Arnoldi
+ * (exchange only the referenced entries — one grid row with
+ * each neighbour for the 5-point stencil — instead of all-gathering q):
+ * table[(r P + p) 2 + {0, 1}] = [lo, hi) of rank p's segment that rank r's
+ * CSR rows reference.  NULL clears it (all-gather of q).                  */
+int sqb_ctx_set_halo(sqb_ctx* ctx, int nranks, const int64_t* table);
 int sqb_rhqr_left_dist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
                        const void* W, int64_t n_local, int64_t m, int64_t ldw,
                        void* U, int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt,

@@ -47,6 +47,8 @@ struct sqb_ctx {
   int dbg_col = -1;
   int nranks = 1;
   int rank = 0;
+  // halo ranges of the row-partitioned SpMV (sqb_ctx_set_halo): [P][P][2]
+  std::vector<int64_t> halo;
   // host-buffer entry points (host_pipe.cu): device copies of the caller's
   // host operands and transfer staging live in a second grow-only arena;
   // copy-engine streams run the H2D / D2H pipelines beside ctx->stream

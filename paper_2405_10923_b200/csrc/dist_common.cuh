@@ -23,6 +23,10 @@ struct NcclApi {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -40,6 +44,10 @@ inline NcclApi* nccl_api() {
       api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
       api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
       api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+      api.send = (decltype(api.send))dlsym(h, "ncclSend");
+      api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+      api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+      api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
     }
   }
   return (api.getUniqueId && api.commInitRank && api.allGather) ? &api : nullptr;
@@ -91,6 +99,59 @@ inline int dist_allgather(sqb_ctx* ctx, bool virt, const std::vector<int>& ids, 
   ncclResult_t e = nc->allGather(send[0], G, bytes, ncclUint8, (ncclComm_t)ctx->nccl, ctx->stream);
   if (e != ncclSuccess)
     return set_error(ctx, SQB_ERR_NCCL, "ncclAllGather: %s", nc->getErrorString ? nc->getErrorString(e) : "?");
+  return SQB_OK;
+}
+
+// Halo exchange of a row-partitioned vector into the gathered [rank][seg]
+// layout: rank r receives only [lo, hi) of rank p's segment, the range its
+// CSR rows reference (halo[(r P + p) 2 + {0, 1}]), plus its own segment.
+// NCCL: one group of point-to-point sends/receives (for the 5-point stencil
+// one grid row to/from each neighbour instead of the whole vector); virtual
+// ranks: device copies into each rank's own gathered buffer.
+inline int dist_halo_exchange(sqb_ctx* ctx, bool virt, const std::vector<int>& ids, int nranks,
+                              const std::vector<const void*>& local, const std::vector<int64_t>& rows,
+                              size_t esz, int64_t seg, const std::vector<void*>& G) {
+  const std::vector<int64_t>& h = ctx->halo;
+  for (size_t i = 0; i < local.size(); ++i) {
+    const int r = ids[i];
+    if (rows[i] > 0)
+      SQB_CUDA_TRY(cudaMemcpyAsync((char*)G[i] + (size_t)r * seg * esz, local[i], (size_t)rows[i] * esz,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (virt) {
+    for (size_t i = 0; i < local.size(); ++i) {
+      const int r = ids[i];
+      for (size_t j = 0; j < local.size(); ++j) {
+        const int p = ids[j];
+        if (p == r) continue;
+        const int64_t lo = h[((size_t)r * nranks + p) * 2], hi = h[((size_t)r * nranks + p) * 2 + 1];
+        if (hi > lo)
+          SQB_CUDA_TRY(cudaMemcpyAsync((char*)G[i] + ((size_t)p * seg + lo) * esz, (const char*)local[j] + lo * esz,
+                                       (size_t)(hi - lo) * esz, cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+    }
+    return SQB_OK;
+  }
+  NcclApi* nc = nccl_api();
+  if (!nc || !ctx->nccl || !nc->send || !nc->recv || !nc->groupStart || !nc->groupEnd)
+    return set_error(ctx, SQB_ERR_NCCL, "NCCL point-to-point API not available");
+  const int r = ids[0];
+  ncclComm_t comm = (ncclComm_t)ctx->nccl;
+  ncclResult_t e = nc->groupStart();
+  for (int p = 0; p < nranks && e == ncclSuccess; ++p) {
+    if (p == r) continue;
+    const int64_t slo = h[((size_t)p * nranks + r) * 2], shi = h[((size_t)p * nranks + r) * 2 + 1];
+    if (shi > slo) e = nc->send((const char*)local[0] + slo * esz, (size_t)(shi - slo) * esz, ncclUint8, p, comm,
+                                ctx->stream);
+    const int64_t rlo = h[((size_t)r * nranks + p) * 2], rhi = h[((size_t)r * nranks + p) * 2 + 1];
+    if (e == ncclSuccess && rhi > rlo)
+      e = nc->recv((char*)G[0] + ((size_t)p * seg + rlo) * esz, (size_t)(rhi - rlo) * esz, ncclUint8, p, comm,
+                   ctx->stream);
+  }
+  const ncclResult_t e2 = nc->groupEnd();
+  if (e == ncclSuccess) e = e2;
+  if (e != ncclSuccess)
+    return set_error(ctx, SQB_ERR_NCCL, "halo exchange: %s", nc->getErrorString ? nc->getErrorString(e) : "?");
   return SQB_OK;
 }
 

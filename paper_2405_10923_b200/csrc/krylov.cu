@@ -481,7 +481,10 @@ static int arnoldi_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int m, int scaling
     off[r * 9 + 7] = plan.add(sizeof(T) * (seg + 2 * VN));      // q
     off[r * 9 + 8] = plan.add(sizeof(A) * ell * tpr);           // leaves
   }
-  const size_t iGq = plan.add(sizeof(T) * nranks * seg);
+  const bool halo = ctx->halo.size() == (size_t)nranks * nranks * 2;
+  // virtual ranks with halo ranges: one gathered buffer per rank (each holds
+  // only what its own rows reference — a wrong range shows up as wrong bits)
+  const size_t iGq = plan.add(sizeof(T) * nranks * seg * (halo && virt ? L : 1));
   const size_t iGs = plan.add(sizeof(double) * nranks * pl);
   SQB_TRY(ws_reserve(ctx, plan.total));
   char* base = static_cast<char*>(ctx->ws);
@@ -500,6 +503,8 @@ static int arnoldi_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int m, int scaling
     d.P = base + plan.offs[off[r * 9 + 8]];
   }
   T* Gq = (T*)(base + plan.offs[iGq]);
+  if (halo)
+    SQB_CUDA_TRY(cudaMemsetAsync(Gq, 0, sizeof(T) * nranks * seg * (virt ? L : 1), ctx->stream));
   double* Gs = (double*)(base + plan.offs[iGs]);
   Status* st = ctx->d_status;
   double scale_lo = 0.0, norm_lo = 0.0;
@@ -529,14 +534,27 @@ static int arnoldi_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int m, int scaling
     }
     return SQB_OK;
   };
+  // q for the SpMV: the halo exchange when the caller set the ranges
+  // (sqb_ctx_set_halo), else the all-gather of the whole vector
   auto gather_T = [&](void* ArnRank::*sel) -> int {
     std::vector<const void*> send(L);
     for (int r = 0; r < L; ++r) send[r] = rk[r].*sel;
+    if (halo) {
+      std::vector<int64_t> rows(L);
+      std::vector<void*> G(L);
+      for (int r = 0; r < L; ++r) {
+        rows[r] = rk[r].rows;
+        G[r] = Gq + (virt ? (int64_t)r * nranks * seg : 0);
+      }
+      return dist_halo_exchange(ctx, virt, ids, nranks, send, rows, sizeof(T), seg, G);
+    }
     return dist_allgather(ctx, virt, ids, send, sizeof(T) * seg, Gq);
   };
   auto spmv = [&](ArnRank& d, const double* bsub) -> int {
+    const int r = (int)(&d - rk.data());
+    const T* Gr = Gq + (halo && virt ? (int64_t)r * nranks * seg : 0);
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((d.rows + 255) / 256, 16 * 148));
-    csr_spmv_kernel<T><<<grid, 256, 0, ctx->stream>>>(d.rows, d.indptr, d.indices, d.data, Gq, bsub, (T*)d.w,
+    csr_spmv_kernel<T><<<grid, 256, 0, ctx->stream>>>(d.rows, d.indptr, d.indices, d.data, Gr, bsub, (T*)d.w,
                                                       nullptr, st);
     return check_launch(ctx, "csr_spmv_kernel");
   };
@@ -743,6 +761,31 @@ extern "C" int sqb_rhqr_arnoldi_dist(sqb_ctx* ctx, const sqb_sketch* sk, int m, 
   if (!d.Utop) return set_error(ctx, SQB_ERR_ARG, "ranks > 0 need an (m+1) x (m+1) Utop scratch");
   return arnoldi_dist_entry(ctx, sk, m, scaling, lo_dtype, happy_tol, rk, ctx->nranks, false,
                             std::vector<int>{ctx->rank}, seg, attained);
+}
+
+// Halo ranges for the row-partitioned SpMV of sqb_rhqr_arnoldi_dist /
+// _virtual: table[(r P + p) 2 + {0, 1}] = [lo, hi) of rank p's segment that
+// rank r's CSR rows reference.  table = NULL (or nranks = 0) clears it: the
+// q exchange falls back to the all-gather.
+extern "C" int sqb_ctx_set_halo(sqb_ctx* ctx, int nranks, const int64_t* table) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  if (!table || nranks <= 0) {
+    ctx->halo.clear();
+    return SQB_OK;
+  }
+  if (nranks > 8) return set_error(ctx, SQB_ERR_ARG, "nranks must be <= 8");
+  ctx->halo.assign(table, table + (size_t)nranks * nranks * 2);
+  for (int r = 0; r < nranks; ++r)
+    for (int p = 0; p < nranks; ++p) {
+      const int64_t lo = ctx->halo[((size_t)r * nranks + p) * 2], hi = ctx->halo[((size_t)r * nranks + p) * 2 + 1];
+      if (lo < 0 || hi < lo) {
+        ctx->halo.clear();
+        return set_error(ctx, SQB_ERR_ARG, "bad halo range [%lld, %lld) for ranks %d <- %d", (long long)lo,
+                         (long long)hi, r, p);
+      }
+    }
+  return SQB_OK;
 }
 
 // The same with P virtual ranks on one device (the all-gathers become device

@@ -229,6 +229,34 @@ def gather_layout(x, m: int, n_pad: int, nranks: int, tag: str = "double"):
     return out
 
 
+def halo_ranges(indices, seg: int, nranks: int, rank: int):
+    """[lo, hi) of every rank's segment that this rank's remapped CSR column
+    indices reference (its own segment: (0, 0), it is copied locally) — the
+    halo of the row-partitioned SpMV; for the 5-point stencil
+    one grid row at the end of the previous rank and the start of the next."""
+    idx = np.asarray(indices, dtype=np.int64)
+    out = np.zeros((nranks, 2), dtype=np.int64)
+    if idx.size:
+        owner = idx // seg
+        for p in range(nranks):
+            if p == rank:
+                continue
+            sel = idx[owner == p]
+            if sel.size:
+                out[p] = (int(sel.min()) - p * seg, int(sel.max()) - p * seg + 1)
+    return out
+
+
+def set_halo(table):
+    """Install a [P][P][2] halo table on the library context (None clears)."""
+    ctx = _lib.context()
+    if table is None:
+        ctx.check(_lib.lib().sqb_ctx_set_halo(ctx.h, 0, None), "sqb_ctx_set_halo")
+        return
+    t = np.ascontiguousarray(np.asarray(table, dtype=np.int64))
+    ctx.check(_lib.lib().sqb_ctx_set_halo(ctx.h, int(t.shape[0]), t.ctypes.data), "sqb_ctx_set_halo")
+
+
 def local_operator(A, m: int, n_pad: int, nranks: int, rank: int, tag: str = "double"):
     """local_operator_host, uploaded (what sqb_rhqr_arnoldi_dist expects)."""
     ip, ix, dv, r0, nr, seg = local_operator_host(A, m, n_pad, nranks, rank, tag)
@@ -244,10 +272,13 @@ def _arnoldi_bufs(rows, mrow, m, od, tag, x0_local):
                 Utop=empty_colmajor(mt, mt, tag), x0=to_device(x0_local, tag))
 
 
-def rhqr_arnoldi_virtual(A, b, x0, m, omega, nranks, scaling=SCALE_SQRT2, policy=None, happy_tol=None):
+def rhqr_arnoldi_virtual(A, b, x0, m, omega, nranks, scaling=SCALE_SQRT2, policy=None, happy_tol=None,
+                         halo=True):
     """The row-partitioned RHQR-Arnoldi with `nranks` virtual ranks on one
     device; returns rank 0's sketch-space factors (bitwise those of one GPU)
-    and U reassembled in global row order."""
+    and U reassembled in global row order.  halo=True exchanges only the
+    entries of q each rank's rows reference (each rank gets its own gathered
+    buffer, so a wrong range changes the result); False all-gathers q."""
     from .krylov import KrylovBundle
     check_scaling(scaling)
     policy = policy or DOUBLE_POLICY
@@ -262,8 +293,10 @@ def rhqr_arnoldi_virtual(A, b, x0, m, omega, nranks, scaling=SCALE_SQRT2, policy
     happy_tol = 32.0 * policy.u_high if happy_tol is None else happy_tol
     row0s, rows, seg = krylov_partition(n, m, omega.n_pad, nranks, tag)
     keep, bufs = [], []
+    table = np.zeros((nranks, nranks, 2), dtype=np.int64)
     for p in range(nranks):
         ip, ix, dv, r0, nr, _ = local_operator(A, m, omega.n_pad, nranks, p, tag)
+        table[p] = halo_ranges(ix.cpu().numpy(), seg, nranks, p)
         bl = torch.from_numpy(b[r0:r0 + nr].copy()).cuda() if nr else torch.zeros(1, dtype=torch.float64, device="cuda")
         bf = _arnoldi_bufs(nr, mt if p == 0 else 0, m, od, tag, x0[r0:r0 + nr] if nr else np.zeros(1))
         keep += [ip, ix, dv, bl]
@@ -272,7 +305,9 @@ def rhqr_arnoldi_virtual(A, b, x0, m, omega, nranks, scaling=SCALE_SQRT2, policy
     arr = lambda ctype, xs: (ctype * P_)(*xs)  # noqa: E731
     attained = C.c_int(-1)
     ctx = _lib.context()
-    ctx.check(_lib.lib().sqb_rhqr_arnoldi_virtual(
+    set_halo(table if halo else None)
+    try:
+        rc = _lib.lib().sqb_rhqr_arnoldi_virtual(
         ctx.h, omega.desc(), m, scaling_code(scaling), CODES[tag], float(happy_tol), P_,
         arr(C.c_int64, rows), arr(C.c_int64, row0s), seg,
         arr(C.c_void_p, [x[0].data_ptr() for x in bufs]), arr(C.c_void_p, [x[1].data_ptr() for x in bufs]),
@@ -282,7 +317,10 @@ def rhqr_arnoldi_virtual(A, b, x0, m, omega, nranks, scaling=SCALE_SQRT2, policy
         ld_of(bufs[0][4]["S"]), arr(C.c_void_p, [x[4]["T"].data_ptr() for x in bufs]), ld_of(bufs[0][4]["T"]),
         arr(C.c_void_p, [x[4]["H"].data_ptr() for x in bufs]), ld_of(bufs[0][4]["H"]),
         arr(C.c_void_p, [x[4]["beta"].data_ptr() for x in bufs]),
-        arr(C.c_void_p, [x[4]["Utop"].data_ptr() for x in bufs]), C.byref(attained)), "sqb_rhqr_arnoldi_virtual")
+        arr(C.c_void_p, [x[4]["Utop"].data_ptr() for x in bufs]), C.byref(attained))
+    finally:
+        set_halo(None)
+    ctx.check(rc, "sqb_rhqr_arnoldi_virtual")
     raise_status(ctx, "rhqr_arnoldi")
     closed = None if attained.value < 0 else attained.value
     k = m if closed is None else closed
@@ -298,7 +336,7 @@ def rhqr_arnoldi_virtual(A, b, x0, m, omega, nranks, scaling=SCALE_SQRT2, policy
 
 
 def rhqr_arnoldi_distributed(A_local, b_local, x0_local, m, omega, n, scaling=SCALE_SQRT2, policy=None,
-                             happy_tol=None):
+                             happy_tol=None, halo=True):
     """This rank's part of rhqr_arnoldi (krylov.py:82-150) on the row
     partition (one process per GPU, NCCL).  A_local = local_operator(...)
     output; b_local / x0_local are this rank's rows.  Returns a KrylovBundle
@@ -320,11 +358,22 @@ def rhqr_arnoldi_distributed(A_local, b_local, x0_local, m, omega, n, scaling=SC
                        x0_local if x0_local is not None else np.zeros(max(nr, 1)))
     attained = C.c_int(-1)
     ctx = _lib.context()
-    ctx.check(_lib.lib().sqb_rhqr_arnoldi_dist(
+    table = None
+    if halo:  # every rank's halo ranges, gathered once (host, tiny)
+        mine = halo_ranges(ix.cpu().numpy(), seg, dist.get_world_size(), rank)
+        rows_all = [None] * dist.get_world_size()
+        dist.all_gather_object(rows_all, mine.tolist())
+        table = np.asarray(rows_all, dtype=np.int64)
+    set_halo(table)
+    try:
+        rc = _lib.lib().sqb_rhqr_arnoldi_dist(
         ctx.h, omega.desc(), m, scaling_code(scaling), CODES[tag], float(happy_tol), nr, r0, seg, ip.data_ptr(),
         ix.data_ptr(), dv.data_ptr(), bl.data_ptr(), bf["x0"].data_ptr(), bf["U"].data_ptr(), ld_of(bf["U"]),
         bf["S"].data_ptr(), ld_of(bf["S"]), bf["T"].data_ptr(), ld_of(bf["T"]), bf["H"].data_ptr(), ld_of(bf["H"]),
-        None, 1, bf["beta"].data_ptr(), bf["Utop"].data_ptr(), C.byref(attained)), "sqb_rhqr_arnoldi_dist")
+        None, 1, bf["beta"].data_ptr(), bf["Utop"].data_ptr(), C.byref(attained))
+    finally:
+        set_halo(None)
+    ctx.check(rc, "sqb_rhqr_arnoldi_dist")
     raise_status(ctx, "rhqr_arnoldi")
     closed = None if attained.value < 0 else attained.value
     k = m if closed is None else closed

@@ -183,3 +183,77 @@ def test_gmres_exchange_gloo_world2():
     port = 29600 + os.getpid() % 300
     mp.spawn(_gmres_worker, args=(2, port, out), nprocs=2, join=True)
     assert out[0] and out[1]
+
+
+def _halo_worker(rank, world, port, out):
+    """world_size-2 gloo model of the halo exchange: every rank
+    publishes its halo ranges once (all_gather_object, as the facade does),
+    then per step sends only the ranges its peers reference and receives
+    only its own (point-to-point, as the NCCL group in dist_halo_exchange);
+    the local CSR rows times that partially filled gathered vector equal the
+    global SpMV rows bitwise, and the exchanged volume is one grid row per
+    neighbour, not the whole vector."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2405_10923_b200.dist import halo_ranges, krylov_partition, local_operator_host
+    import scipy.sparse
+    k, m = 128, 12
+    A = _cd_matrix(k)
+    n = k * k
+    n_pad = 1 << (n - m - 2).bit_length()
+    row0s, rows, seg = krylov_partition(n, m, n_pad, world)
+    ip, ix, dv, r0, nr, sg = local_operator_host(A, m, n_pad, world, rank)
+    mine = halo_ranges(ix, seg, world, rank)
+    table = [None] * world
+    dist.all_gather_object(table, mine.tolist())
+    table = np.asarray(table, dtype=np.int64)
+    x = np.random.default_rng(0).standard_normal(n)
+    q = x[row0s[rank]:row0s[rank] + rows[rank]].copy()
+    G = np.zeros(world * seg)
+    G[rank * seg:rank * seg + rows[rank]] = q
+    reqs, moved = [], 0
+    for p in range(world):
+        if p == rank:
+            continue
+        slo, shi = table[p, rank]
+        if shi > slo:
+            reqs.append(dist.isend(torch.from_numpy(q[slo:shi].copy()), p))
+        rlo, rhi = table[rank, p]
+        if rhi > rlo:
+            buf = torch.zeros(rhi - rlo, dtype=torch.float64)
+            dist.recv(buf, p)
+            G[p * seg + rlo:p * seg + rhi] = buf.numpy()
+            moved += rhi - rlo
+    for r in reqs:
+        r.wait()
+    yl = scipy.sparse.csr_matrix((dv, ix, ip), shape=(nr, world * sg)) @ G
+    out[rank] = (bool(np.array_equal(yl, (A @ x)[r0:r0 + nr])), int(moved))
+    dist.destroy_process_group()
+
+
+def test_halo_exchange_gloo_world2():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = 29300 + os.getpid() % 300
+    mp.spawn(_halo_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0][0] and out[1][0]
+    assert out[0][1] <= 128 and out[1][1] <= 128  # one grid row (k = 128) per neighbour
+
+
+def test_halo_ranges_stencil():
+    from paper_2405_10923_b200.dist import halo_ranges, krylov_partition, local_operator_host
+    k, m, world = 96, 10, 4
+    A = _cd_matrix(k)
+    n = k * k
+    n_pad = 1 << (n - m - 2).bit_length()
+    _, rows, seg = krylov_partition(n, m, n_pad, world)
+    for r in range(world):
+        ip, ix, dv, r0, nr, sg = local_operator_host(A, m, n_pad, world, r)
+        h = halo_ranges(ix, seg, world, r)
+        for p in range(world):
+            size = h[p, 1] - h[p, 0]
+            if abs(p - r) == 1 and nr and rows[p]:
+                assert 0 < size <= k  # one grid row with each (non-empty) neighbour
+            else:
+                assert size == 0

@@ -500,10 +500,11 @@ def test_row_partitioned_arnoldi_bitwise(P, nranks):
     b = np.random.default_rng(nranks).standard_normal(n)
     om = P.SRHTSketch(4 * (m + 1), n - m - 1, 23)
     b1 = P.rhqr_arnoldi(A, b, None, m, om)
-    bv = dist.rhqr_arnoldi_virtual(A, b, None, m, om, nranks)
-    assert bv.breakdown == b1.breakdown and bv.beta == b1.beta
-    for key in ("H", "S", "T", "U"):
-        assert np.array_equal(getattr(bv, key), getattr(b1, key)), key
+    for halo in (True, False):  # halo exchange of the referenced q ranges / all-gather of q
+        bv = dist.rhqr_arnoldi_virtual(A, b, None, m, om, nranks, halo=halo)
+        assert bv.breakdown == b1.breakdown and bv.beta == b1.beta
+        for key in ("H", "S", "T", "U"):
+            assert np.array_equal(getattr(bv, key), getattr(b1, key)), (halo, key)
     x1, h1 = P.rhqr_gmres(A, b, None, m, om)
     xv, hv = dist.rhqr_gmres_virtual(A, b, None, m, om, nranks)
     assert np.array_equal(hv, h1)

@@ -171,7 +171,7 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
       // rank-local subtree of w_c's sketch -> payload[0:ell]
       SrhtGeom gl{g.log_tb, tpr, n_eff};
       if (n_eff == 0) SQB_CUDA_TRY(cudaMemsetAsync(d.P, 0, sizeof(A) * ell * tpr, ctx->stream));
-      SQB_TRY(launch_srht_tree_geom(ctx, sk, Lo<T>::code, gl, d.P, 1, d.pay, od, 0, 0, st));
+      SQB_TRY(launch_srht_tree_geom(ctx, sk, Lo<T>::code, gl, d.P, 1, d.pay, od, 0, 0, st, 1));  // column-kernel leaves
     }
     SQB_TRY(exchange([](DistRank& d) { return d.pay; }, (size_t)od, Gc));
     for (int r = 0; r < L; ++r)

@@ -132,7 +132,7 @@ srht_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int log_tb,
   }
   __syncthreads();
   tile_fwht<T>(sm, log_tb);
-  tile_gather<T>(sm, idx, ell, log_tb, P + (col * ell) * n_tiles + t, n_tiles);
+  tile_gather<T>(sm, idx, ell, log_tb, P + (col * n_tiles + t) * ell, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -310,8 +310,8 @@ srht64_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_ef
         if (((j < 32 ? mlo : mhi) & (1u << (j & 31))) != 0u) samp[slot++] = v[j];
     }
     __syncthreads();
-    T* leaves = P + (col * ell) * n_tiles + t;
-    for (int kk = tid; kk < ell; kk += S64_NT) leaves[kk * n_tiles] = samp[kslot[kk]];
+    T* leaves = P + (col * n_tiles + t) * ell;
+    for (int kk = tid; kk < ell; kk += S64_NT) leaves[kk] = samp[kslot[kk]];
   }
   cp_async_wait_group<0>();
 }
@@ -519,11 +519,11 @@ srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restric
       acc[i] = (q & 1) ? t : sv;
     }
     if (q == 3) {
-      T* leaves = P + (col * ell) * n_tiles + (e0 >> 12);
+      T* leaves = P + (col * n_tiles + (e0 >> 12)) * ell;
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
         const int kk = lane + 32 * i;
-        if (kk < ell) leaves[(int64_t)kk * n_tiles] = Lo<T>::add(ab[i], flip_sign(acc[i], mypk[i], 17));
+        if (kk < ell) leaves[kk] = Lo<T>::add(ab[i], flip_sign(acc[i], mypk[i], 17));
       }
     }
     __syncwarp();
@@ -721,8 +721,8 @@ srht64h_tile_kernel(const T* __restrict__ X, int64_t ldx, int64_t n, int64_t n_e
           samp[slot++] = (uint16_t)((j & 1) ? (v[j >> 1] >> 16) : (v[j >> 1] & 0xffffu));
     }
     __syncthreads();
-    float* leaves = P + (col * ell) * n_tiles + t;
-    for (int kk = tid; kk < ell; kk += S64_NT) leaves[kk * n_tiles] = h16_to_float<T>(samp[kslot[kk]]);
+    float* leaves = P + (col * n_tiles + t) * ell;
+    for (int kk = tid; kk < ell; kk += S64_NT) leaves[kk] = h16_to_float<T>(samp[kslot[kk]]);
   }
   cp_async_wait_group<0>();
 }
@@ -885,7 +885,7 @@ srht_tma16_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restr
       } else {
         const int kk = lane + 32 * i;
         if (kk < ell)
-          P[(col * ell + kk) * n_tiles + (e0 >> 12)] = ((pk >> 16) & 1u) ? Lo<T>::sub(acc[i], sv) : Lo<T>::add(acc[i], sv);
+          P[(col * n_tiles + (e0 >> 12)) * ell + kk] = ((pk >> 16) & 1u) ? Lo<T>::sub(acc[i], sv) : Lo<T>::add(acc[i], sv);
       }
     }
     __syncwarp();
@@ -932,12 +932,34 @@ static int launch_tma16_kpl(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& 
   return launch_tma16<T, 16, S, WPB>(ctx, sk, g, n_local, e_base, X, ldx, k, scale2, P, st);
 }
 
+// Leaves of the fused column kernel (rhqr_col_kernel) are k-major,
+// P[(col ell + k) n_tiles + t]: one warp per output (the row-partitioned
+// sweep's rank-local subtree, rhqr_dist.cu).
+// group-major leaves, one warp per output with lanes over tiles (strided
+// reads): the latency-friendly choice when there are few outputs (a single
+// vector: the Arnoldi sketches)
 template <typename T>
 __global__ void __launch_bounds__(256)
-srht_tree_kernel(const typename Lo<T>::acc* __restrict__ P, int64_t n_tiles, int64_t n_eff,
-                 const int64_t* __restrict__ idx, int ell, int log_tb,
-                 typename Lo<T>::acc norm_lo, double* __restrict__ Y, int64_t ldy,
-                 int64_t row_off, const Status* st, int apply_norm) {
+srht_tree_gmw_kernel(const typename Lo<T>::acc* __restrict__ P, int64_t n_tiles, int64_t n_eff,
+                     const int64_t* __restrict__ idx, int ell, int log_tb,
+                     typename Lo<T>::acc norm_lo, double* __restrict__ Y, int64_t ldy,
+                     int64_t row_off, const Status* st, int apply_norm) {
+  if (st && failed(st)) return;
+  const int k = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t col = blockIdx.y;
+  if (k >= ell) return;
+  const int64_t rhi = __ldg(idx + k) >> log_tb;
+  const typename Lo<T>::acc v =
+      warp_tile_tree<T>(P + col * n_tiles * ell + k, (int)n_tiles, (int)n_eff, rhi, ell);
+  if ((threadIdx.x & 31) == 0) Y[row_off + k + col * ldy] = apply_norm ? (double)Lo<T>::mul(v, norm_lo) : (double)v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+srht_tree_km_kernel(const typename Lo<T>::acc* __restrict__ P, int64_t n_tiles, int64_t n_eff,
+                    const int64_t* __restrict__ idx, int ell, int log_tb,
+                    typename Lo<T>::acc norm_lo, double* __restrict__ Y, int64_t ldy,
+                    int64_t row_off, const Status* st, int apply_norm) {
   if (st && failed(st)) return;
   const int k = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t col = blockIdx.y;
@@ -946,6 +968,70 @@ srht_tree_kernel(const typename Lo<T>::acc* __restrict__ P, int64_t n_tiles, int
   const typename Lo<T>::acc v =
       warp_tile_tree<T>(P + (col * ell + k) * n_tiles, (int)n_tiles, (int)n_eff, rhi);
   if ((threadIdx.x & 31) == 0) Y[row_off + k + col * ldy] = apply_norm ? (double)Lo<T>::mul(v, norm_lo) : (double)v;
+}
+
+// Standalone leaves are GROUP-major, P[(col n_tiles + t) ell + k]: the tile
+// kernels write each group's ell leaves as one coalesced run, and here lane
+// = output k reads them coalesced.  CTA = 32 outputs x 8 warps; warp w folds
+// the aligned tile chunk [w cs, (w+1) cs) with a binary counter (the node of
+// height h combines left +- right by bit h of r_hi = idx div TB, left =
+// lower tiles; all-padding tiles are exact +0 leaves) — the same binary tree
+// as one pass over all tiles — then warp 0 folds the chunk roots.
+template <typename T, int NW>
+__global__ void __launch_bounds__(NW * 32)
+srht_tree_kernel(const typename Lo<T>::acc* __restrict__ P, int64_t n_tiles, int64_t n_eff,
+                 const int64_t* __restrict__ idx, int ell, int log_tb,
+                 typename Lo<T>::acc norm_lo, double* __restrict__ Y, int64_t ldy,
+                 int64_t row_off, const Status* st, int apply_norm) {
+  using A = typename Lo<T>::acc;
+  __shared__ A roots[NW][32];
+  if (st && failed(st)) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int k = blockIdx.x * 32 + lane;
+  const int64_t col = blockIdx.y;
+  const int nch = n_tiles >= NW ? NW : (int)n_tiles;
+  const int64_t cs = n_tiles / nch;  // power of two
+  int lc = 0;
+  while ((int64_t(1) << lc) < cs) ++lc;
+  const int64_t rhi = k < ell ? (__ldg(idx + k) >> log_tb) : 0;
+  if (w < nch) {
+    A acc[40];
+    const A* pc = P + (col * n_tiles + (int64_t)w * cs) * ell + k;
+    const int64_t t0 = (int64_t)w * cs;
+    for (int64_t tb = 0; tb < cs; tb += 8) {
+      A v8[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        v8[j] = (k < ell && tb + j < cs && t0 + tb + j < n_eff) ? pc[(tb + j) * ell] : A(0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (tb + j >= cs) break;
+        const int64_t tt = tb + j;
+        A v = v8[j];
+        int h = 0;
+        while ((tt >> h) & 1) {
+          v = ((rhi >> h) & 1) ? Lo<T>::sub(acc[h], v) : Lo<T>::add(acc[h], v);
+          ++h;
+        }
+        acc[h] = v;
+      }
+    }
+    roots[w][lane] = acc[lc];
+  }
+  __syncthreads();
+  if (w == 0 && k < ell) {
+    A r[NW];
+#pragma unroll
+    for (int q = 0; q < NW; ++q) r[q] = q < nch ? roots[q][lane] : A(0);
+    int lvl = lc;
+    for (int s2 = 1; s2 < nch; s2 <<= 1, ++lvl) {
+      const bool neg = (rhi >> lvl) & 1;
+#pragma unroll
+      for (int q = 0; q < NW; q += 2)
+        if ((q % (2 * s2)) == 0 && q + s2 < nch) r[q] = neg ? Lo<T>::sub(r[q], r[q + s2]) : Lo<T>::add(r[q], r[q + s2]);
+    }
+    Y[row_off + k + col * ldy] = apply_norm ? (double)Lo<T>::mul(r[0], norm_lo) : (double)r[0];
+  }
 }
 
 template <typename T>
@@ -1072,17 +1158,46 @@ static int srht_tiles_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int64
   return srht_tiles_geom_t<T>(ctx, sk, standalone_geom(sk), sk->n, 0, X, ldx, k, P, st);
 }
 
+// group-major tree launch: 8 chunk warps per 32 outputs, or 32 when the
+// grid would not fill the GPU (few columns: single-vector Arnoldi sketches)
+template <typename T>
+static int launch_tree_gm(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, const void* P, int64_t k,
+                          double* Y, int64_t ldy, int64_t row_off, typename Lo<T>::acc nm, int apply_norm,
+                          const Status* st) {
+  using A = typename Lo<T>::acc;
+  dim3 grid((unsigned)((sk->ell + 31) / 32), (unsigned)k);
+  if (k <= 2) {
+    dim3 gw((unsigned)((sk->ell + 7) / 8), (unsigned)k);
+    srht_tree_gmw_kernel<T><<<gw, 256, 0, ctx->stream>>>((const A*)P, g.n_tiles, g.n_eff, sk->indices,
+                                                         (int)sk->ell, g.log_tb, nm, Y, ldy, row_off, st, apply_norm);
+    return check_launch(ctx, "srht_tree_gmw_kernel");
+  }
+  if ((int64_t)grid.x * grid.y < 2 * ctx->sm_count && g.n_tiles >= 64)
+    srht_tree_kernel<T, 32><<<grid, 1024, 0, ctx->stream>>>((const A*)P, g.n_tiles, g.n_eff, sk->indices,
+                                                            (int)sk->ell, g.log_tb, nm, Y, ldy, row_off, st,
+                                                            apply_norm);
+  else
+    srht_tree_kernel<T, 8><<<grid, 256, 0, ctx->stream>>>((const A*)P, g.n_tiles, g.n_eff, sk->indices,
+                                                          (int)sk->ell, g.log_tb, nm, Y, ldy, row_off, st,
+                                                          apply_norm);
+  return check_launch(ctx, "srht_tree_kernel");
+}
+
 template <typename T>
 static int srht_tree_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, const void* P, int64_t k,
-                            double* Y, int64_t ldy, int64_t row_off, int apply_norm, const Status* st) {
+                            double* Y, int64_t ldy, int64_t row_off, int apply_norm, const Status* st,
+                            int kmajor) {
   using A = typename Lo<T>::acc;
   double sc, nm;
   srht_constants(sk, Lo<T>::code, &sc, &nm);
-  dim3 grid((unsigned)((sk->ell + 7) / 8), (unsigned)k);
-  srht_tree_kernel<T><<<grid, 256, 0, ctx->stream>>>((const A*)P, g.n_tiles, g.n_eff, sk->indices,
-                                                     (int)sk->ell, g.log_tb, (A)nm, Y, ldy, row_off, st,
-                                                     apply_norm);
-  return check_launch(ctx, "srht_tree_kernel");
+  if (kmajor) {
+    dim3 gk((unsigned)((sk->ell + 7) / 8), (unsigned)k);
+    srht_tree_km_kernel<T><<<gk, 256, 0, ctx->stream>>>((const A*)P, g.n_tiles, g.n_eff, sk->indices,
+                                                        (int)sk->ell, g.log_tb, (A)nm, Y, ldy, row_off, st,
+                                                        apply_norm);
+    return check_launch(ctx, "srht_tree_km_kernel");
+  }
+  return launch_tree_gm<T>(ctx, sk, g, P, k, Y, ldy, row_off, (A)nm, apply_norm, st);
 }
 
 template <typename T>
@@ -1092,10 +1207,7 @@ static int srht_tree_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* P, int64_
   const SrhtGeom g = standalone_geom(sk);
   double sc, nm;
   srht_constants(sk, Lo<T>::code, &sc, &nm);
-  dim3 grid((unsigned)((sk->ell + 7) / 8), (unsigned)k);
-  srht_tree_kernel<T><<<grid, 256, 0, ctx->stream>>>((const A*)P, g.n_tiles, g.n_eff, sk->indices,
-                                                     (int)sk->ell, g.log_tb, (A)nm, Y, ldy, row_off, st, 1);
-  return check_launch(ctx, "srht_tree_kernel");
+  return launch_tree_gm<T>(ctx, sk, g, P, k, Y, ldy, row_off, (A)nm, 1, st);
 }
 
 #define SQB_DISPATCH(dtype, FN, ...)                                   \
@@ -1118,8 +1230,9 @@ int launch_srht_tiles_geom(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const 
 }
 
 int launch_srht_tree_geom(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const SrhtGeom& g, const void* P,
-                          int64_t k, double* Y, int64_t ldy, int64_t row_off, int apply_norm, const Status* st) {
-  SQB_DISPATCH(dtype, srht_tree_geom_t, ctx, sk, g, P, k, Y, ldy, row_off, apply_norm, st);
+                          int64_t k, double* Y, int64_t ldy, int64_t row_off, int apply_norm, const Status* st,
+                          int kmajor) {
+  SQB_DISPATCH(dtype, srht_tree_geom_t, ctx, sk, g, P, k, Y, ldy, row_off, apply_norm, st, kmajor);
 }
 
 template <typename T>

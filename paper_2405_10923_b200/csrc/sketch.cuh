@@ -42,7 +42,7 @@ int launch_sketch(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* X, 
                   int64_t k, double* Y, int64_t ldy, int64_t y_row_off, void* partials,
                   const Status* st);
 
-// SRHT pieces used by fused kernels: tree over per-tile leaves P[(col*ell + kk)*n_tiles + t]
+// tree over the group-major leaves of the standalone tile kernels, P[(col*n_tiles + t)*ell + kk]
 int launch_srht_tree(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* P, int64_t k,
                      double* Y, int64_t ldy, int64_t y_row_off, const Status* st);
 
@@ -53,7 +53,8 @@ int launch_srht_tree(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* 
 int launch_srht_tiles_geom(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const SrhtGeom& g, int64_t n_local,
                            int64_t e_base, const void* X, int64_t ldx, int64_t k, void* P, const Status* st);
 int launch_srht_tree_geom(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const SrhtGeom& g, const void* P,
-                          int64_t k, double* Y, int64_t ldy, int64_t row_off, int apply_norm, const Status* st);
+                          int64_t k, double* Y, int64_t ldy, int64_t row_off, int apply_norm, const Status* st,
+                          int kmajor = 0);  // leaves: 0 = standalone tiles (group-major), 1 = rhqr_col_kernel
 
 // Y[0:m, col] = X[0:m, col] as fp64 (identity block of Psi, sketching.py:257)
 int launch_copy_top(sqb_ctx* ctx, int dtype, const void* X, int64_t ldx, int64_t m, int64_t k,

@@ -294,10 +294,11 @@ __device__ __forceinline__ void p16_passes(uint16_t* sm) {
 // the next 5 levels are lane shuffles, and the chunk values are combined by a
 // binary-counter stack with static register indices — every level in order,
 // lower tile range as the left operand.  Supports up to 256 chunks
-// (n_tiles <= 65536).
+// (n_tiles <= 65536).  `stride`: distance between consecutive tiles' leaves.
 template <typename T>
 __device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<T>::acc* leaves,
-                                                              int n_tiles, int n_eff, int64_t rhi) {
+                                                              int n_tiles, int n_eff, int64_t rhi,
+                                                              int64_t stride = 1) {
   using A = typename Lo<T>::acc;
   const int lane = threadIdx.x & 31;
   const int lanes = n_tiles >= 32 ? 32 : n_tiles;                    // lanes holding tiles
@@ -314,7 +315,7 @@ __device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<
   A nx[8];
   const int tl = lane * R;
 #pragma unroll
-  for (int jj = 0; jj < 8; ++jj) nx[jj] = (lane < lanes && jj < R && tl + jj < n_eff) ? leaves[tl + jj] : A(0);
+  for (int jj = 0; jj < 8; ++jj) nx[jj] = (lane < lanes && jj < R && tl + jj < n_eff) ? leaves[(tl + jj) * stride] : A(0);
   for (int q = 0; q < nq; ++q) {
     A v[8];
 #pragma unroll
@@ -322,7 +323,7 @@ __device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<
     if (q + 1 < nq) {
       const int tb = (q + 1) * csz + tl;
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) nx[jj] = (lane < lanes && jj < R && tb + jj < n_eff) ? leaves[tb + jj] : A(0);
+      for (int jj = 0; jj < 8; ++jj) nx[jj] = (lane < lanes && jj < R && tb + jj < n_eff) ? leaves[(tb + jj) * stride] : A(0);
     }
     // levels 0 .. lr-1 inside the lane
 #pragma unroll

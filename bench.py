@@ -207,6 +207,42 @@ class RHQRLeft(Workload):
         if self.partitioned and self.name == "cfg4":
             self.scaling = "strong"
 
+    def extra_kernels(self):
+        """K1 standalone SRHT (the raw sketches Psi W of this workload, through
+        sqb_sketch_apply, tile + tree kernels) timed live: algorithmic bytes
+        b (N-m) m + 8 ell m over CUDA-event time, against the HBM peak."""
+        import torch
+        from paper_2405_10923_b200 import _lib
+        from paper_2405_10923_b200.devarray import CODES, empty_colmajor, ld_of
+        if self.partitioned:
+            return None
+        m, n = self.m, self.Ng - self.m
+        Y = empty_colmajor(self.ell, m, "double")
+        ctx = _lib.context()
+        d = self.om.desc()
+        esz = self.Wd.element_size()
+        f = lambda: ctx.check(_lib.lib().sqb_sketch_apply(  # noqa: E731
+            ctx.h, d, CODES[self.tag], self.Wd.data_ptr() + m * esz, ld_of(self.Wd), m, Y.data_ptr(), ld_of(Y)),
+            "sqb_sketch_apply")
+        for _ in range(3):
+            f()
+        torch.cuda.synchronize()
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        e0.record(s)
+        for _ in range(reps):
+            f()
+        e1.record(s)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        by = self.b * n * m + 8.0 * self.ell * m
+        peak, _ = measured_peak()
+        return {"srht_k1": {"what": f"standalone SRHT apply of W's {n} x {m} Omega rows ({self.tag}), "
+                                    "srht_tma*_tile_kernel + srht_tree_kernel",
+                            "ms": ms, "GB/s": by / ms / 1e6, "frac_hbm": by / ms / 1e6 / peak,
+                            "alg_bytes": by}}
+
     def e2e(self, steps):
         import torch
 
@@ -507,6 +543,13 @@ def main():
     except Exception:
         pass
 
+    extra = None
+    if rank == 0 and hasattr(wl, "extra_kernels"):
+        try:
+            extra = wl.extra_kernels()
+        except Exception as exc:  # informational only
+            extra = {"error": str(exc)[:200]}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         t, by, desc = wl.cpu_sample()
@@ -533,6 +576,8 @@ def main():
             "cpu_baseline": cpu,
             "clocks": clk,
         }
+        if extra:
+            line["kernels"] = extra
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

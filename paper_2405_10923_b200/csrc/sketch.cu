@@ -1088,8 +1088,7 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
                    (g.log_tb >= 3);
   dim3 grid((unsigned)g.n_eff, (unsigned)k);
   if constexpr (sizeof(T) == 2) {
-    if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= 512 && n_local >= 64 && encode_tiled() &&
-        !getenv("SQB_SRHT16_OLD")) {
+    if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= 512 && n_local >= 64 && encode_tiled()) {
       const T s1 = T((float)sc);  // sc is already a value of T (srht_constants): exact
       uint16_t s16b;
       memcpy(&s16b, &s1, 2);

@@ -226,7 +226,10 @@ __device__ inline void col_helper(const ColArgs& a, double* g) {
 
 // DEP = 0: loads widened at issue, one column ahead; DEP >= 2: raw ring of
 // DEP column buffers (see the bulk loop)
-template <typename T, int VN, int DEP = 0, int MINB = 2>
+// LOGT: log2 of the tile (SRHT leaf group) size; small problems use 512-row
+// tiles so the pass spreads over enough CTAs (the leaves and the step
+// kernel's tree adapt: the same binary tree, the same bits)
+template <typename T, int VN, int DEP = 0, int MINB = 2, int LOGT = TileCfg<T>::LOG_TB>
 __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
   using A = typename Lo<T>::acc;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
     if (a.mrow > 0) col_top_block<T>(a, sc);
     return;
   }
-  constexpr int TB = 1 << TileCfg<T>::LOG_TB;
+  constexpr int TB = 1 << LOGT;
   constexpr int NV = TB / (COL_NT * VN);  // runs of VN rows per thread
   const int tb = 1 << a.log_tb;
   const int64_t e0 = tile << a.log_tb;  // first Omega coordinate of the tile

@@ -122,12 +122,27 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
                    ((reinterpret_cast<uintptr_t>((const char*)U + m * esz) & 15) == 0) &&
                    (ldw % VN == 0) && (ldu % VN == 0);
   const int tb_max = 1 << TileCfg<T>::LOG_TB;
-  const int64_t n_eff_col = srht ? g.n_eff : (n + tb_max - 1) / tb_max;
-  const int log_tb_col = srht ? g.log_tb : TileCfg<T>::LOG_TB;
+  // small fp64 problems (config 1: 2^14 rows = 4 tiles of 4096): 512-row
+  // tiles, 8x the CTAs per column pass; leaves and the step kernel's tree
+  // follow the geometry
+  constexpr int SMALL_LOG = 9;
+  const bool small = std::is_same<T, double>::value && srht && vec && g.log_tb == TileCfg<T>::LOG_TB &&
+                     sk->n_pad <= (int64_t(1) << 16) && ncol >= 8;
+  SrhtGeom gc = g;
+  if (small) {
+    gc.log_tb = SMALL_LOG;
+    gc.n_tiles = sk->n_pad >> SMALL_LOG;
+    gc.n_eff = (n + (1 << SMALL_LOG) - 1) >> SMALL_LOG;
+  }
+  const int64_t n_eff_col = srht ? gc.n_eff : (n + tb_max - 1) / tb_max;
+  const int log_tb_col = srht ? gc.log_tb : TileCfg<T>::LOG_TB;
   const size_t tile_bytes = srht ? tile_smem_bytes<A>(tb_max) : 0;
   const size_t col_smem_max = sizeof(A) * ((m + 3) & ~3) +
                               std::max(tile_bytes, sizeof(double) * (size_t)(m + 1));
-  auto colk = col_kernel_select<T, VN>(vec);
+  void (*colk)(ColArgs) = col_kernel_select<T, VN>(vec);
+  if constexpr (std::is_same<T, double>::value) {
+    if (small) colk = rhqr_col_kernel<T, VN, 0, 2, SMALL_LOG>;
+  }
   cudaFuncSetAttribute(colk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
   for (int64_t c = 1; c < ncol; ++c) {
     SQB_TRY(ensure_y0(c + 2));
@@ -135,7 +150,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
     double* a_nxt = abuf + ((c + 1) & 1) * (m + 1);
     ColArgs ca{};
     ca.c = (int)c; ca.m = (int)m; ca.ncol = (int)ncol; ca.mrow = (int)m; ca.e_base = 0; ca.n = n; ca.ell = (int)ell;
-    ca.od = (int)od; ca.log_tb = log_tb_col; ca.n_tiles = g.n_tiles; ca.n_eff = n_eff_col;
+    ca.od = (int)od; ca.log_tb = log_tb_col; ca.n_tiles = gc.n_tiles; ca.n_eff = n_eff_col;
     ca.W = W; ca.ldw = ldw; ca.U = U; ca.ldu = ldu; ca.acur = a_cur; ca.clast = coef; ca.fscale = fs;
     ca.scaling = scaling; ca.srht = srht ? 1 : 0; ca.bits = srht ? sk->sign_bits : nullptr;
     ca.idx = srht ? sk->indices : nullptr; ca.scale_lo = scale_lo; ca.P = P; ca.y = y;
@@ -159,6 +174,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
     sa.dbg = (c == ctx->dbg_col) ? ctx->dbg_ts : nullptr;
     sa.anext = a_nxt;
     sa.tree = srht ? 1 : 0;
+    sa.n_tiles = gc.n_tiles; sa.n_eff = gc.n_eff; sa.log_tb = gc.log_tb;
     SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT),
                        step_smem, sa));
   }

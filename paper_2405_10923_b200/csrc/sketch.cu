@@ -1165,7 +1165,7 @@ static int launch_tree_gm(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g,
                           const Status* st) {
   using A = typename Lo<T>::acc;
   dim3 grid((unsigned)((sk->ell + 31) / 32), (unsigned)k);
-  if (k <= 2) {
+  if (k <= 2 && g.n_tiles <= 65536) {  // warp_tile_tree's chunk stack limit
     dim3 gw((unsigned)((sk->ell + 7) / 8), (unsigned)k);
     srht_tree_gmw_kernel<T><<<gw, 256, 0, ctx->stream>>>((const A*)P, g.n_tiles, g.n_eff, sk->indices,
                                                          (int)sk->ell, g.log_tb, nm, Y, ldy, row_off, st, apply_norm);

@@ -53,7 +53,8 @@ def test_srht_bf16_bitwise(P):
 
 
 @pytest.mark.parametrize("ell,n,seed,k", [(256, (1 << 20) - 128, 3, 3), (512, (1 << 18) - 256, 4, 2),
-                                          (400, (1 << 22) - 201, 5, 1), (128, 3 * 4096 + 17, 6, 5)])
+                                          (400, (1 << 22) - 201, 5, 1), (128, 3 * 4096 + 17, 6, 5),
+                                          (256, (1 << 16) - 3, 8, 40)])  # 40 columns: the 8-warp chunked tree
 def test_srht_bitwise_against_oracle_large(P, ell, n, seed, k):
     op = P.SRHTSketch(ell, n, seed)
     ref = O.SRHT(ell, n, seed)

@@ -4,6 +4,8 @@
 // predecessor produced.
 #pragma once
 
+#include <cstdlib>
+
 #include "ctx.cuh"
 
 namespace sqb {
@@ -23,7 +25,8 @@ inline int launch_pdl(sqb_ctx* ctx, const char* what, void (*kern)(KArgs...), di
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const int no_pdl = [] { const char* e = getenv("SQB_NO_PDL"); return e && e[0] == '1'; }();
+  cfg.numAttrs = no_pdl ? 0 : 1;  // SQB_NO_PDL=1: plain stream order (A/B of the look-ahead)
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
   if (e != cudaSuccess) return set_cuda_error(ctx, e, what, __FILE__, __LINE__);
   return check_launch(ctx, what);

@@ -2,6 +2,7 @@
 // (generic path; the DMMA GEMM lives in dense.cu), identity, embedded.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "sketch.cuh"
@@ -1058,6 +1059,12 @@ __global__ void identity_kernel(const T* __restrict__ X, int64_t ldx, int64_t n,
 // ---------------------------------------------------------------------------
 // standalone sketches use 4096-coordinate tiles for every dtype (the tile size
 // only regroups the same butterflies: any power of two gives the same bits)
+// SQB_<NAME>=0 switches an optimisation off (A/B experiments)
+static bool getenv_flag0(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] == '0';
+}
+
 static SrhtGeom standalone_geom(const sqb_sketch* sk) {
   SrhtGeom g;
   const int lp = ilog2_exact(sk->n_pad);
@@ -1272,6 +1279,26 @@ int launch_sketch(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* X, 
                   int64_t k, double* Y, int64_t ldy, int64_t y_row_off, void* partials,
                   const Status* st) {
   SQB_DISPATCH(dtype, sketch_t, ctx, sk, X, ldx, k, Y, ldy, y_row_off, partials, st);
+}
+
+template <typename T>
+static int resketch_head_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int64_t ldx, int64_t upto,
+                           double* Y, int64_t ldy, int64_t row_off, void* partials, const Status* st) {
+  if (sk->kind != SQB_SKETCH_SRHT || getenv_flag0("SQB_RESKETCH_HEAD"))
+    return sketch_t<T>(ctx, sk, X, ldx, 1, Y, ldy, row_off, partials, st);
+  SrhtGeom g = standalone_geom(sk);
+  const int64_t tb = int64_t(1) << g.log_tb;
+  if (upto > tb) return sketch_t<T>(ctx, sk, X, ldx, 1, Y, ldy, row_off, partials, st);
+  SrhtGeom g0 = g;
+  g0.n_eff = 1;  // tile 0 only; leaves stay at their (col 0, tile 0) slots of the full geometry
+  SQB_TRY(srht_tiles_geom_t<T>(ctx, sk, g0, std::min<int64_t>(sk->n, tb), 0, X, ldx, 1, partials, st));
+  return srht_tree_t<T>(ctx, sk, partials, 1, Y, ldy, row_off, st);
+}
+
+int launch_sketch_resketch_head(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* X, int64_t ldx,
+                                int64_t upto, double* Y, int64_t ldy, int64_t y_row_off, void* partials,
+                                const Status* st) {
+  SQB_DISPATCH(dtype, resketch_head_t, ctx, sk, X, ldx, upto, Y, ldy, y_row_off, partials, st);
 }
 
 }  // namespace sqb

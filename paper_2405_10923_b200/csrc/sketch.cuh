@@ -42,6 +42,16 @@ int launch_sketch(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* X, 
                   int64_t k, double* Y, int64_t ldy, int64_t y_row_off, void* partials,
                   const Status* st);
 
+// Re-sketch of ONE vector after entries [0, upto) changed, when `partials`
+// still holds the leaves of its previous launch_sketch (k = 1): only the
+// first tile's leaves are recomputed (every other tile's in-tile FWHT sees the
+// same inputs, so its leaves are bitwise the same), then the whole tree runs.
+// Falls back to a full launch_sketch when the changed range leaves tile 0 or
+// the sketch is not an SRHT.
+int launch_sketch_resketch_head(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* X, int64_t ldx,
+                                int64_t upto, double* Y, int64_t ldy, int64_t y_row_off, void* partials,
+                                const Status* st);
+
 // tree over the group-major leaves of the standalone tile kernels, P[(col*n_tiles + t)*ell + kk]
 int launch_srht_tree(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* P, int64_t k,
                      double* Y, int64_t ldy, int64_t y_row_off, const Status* st);

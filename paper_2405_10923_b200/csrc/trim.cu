@@ -24,10 +24,12 @@
 #include "sketch.cuh"
 #include "vec.cuh"
 #include "gemv.cuh"
+#include "pdl.cuh"
 
 namespace sqb {
 
 constexpr int TRIM_NT = 256;
+constexpr int TRIM_SNT = 1024;  // single-CTA sketch-space kernels
 
 // x = Xs of the column-scaled wrapper applied to [0 (c0 entries); w[c0:]]
 template <typename T>
@@ -55,15 +57,22 @@ __global__ void trim_prep_batch_kernel(T* __restrict__ X, int64_t ldx, const T* 
 }
 
 // h = S[:, :c]^t z - L[:c, :c] w[:c];  coef = T~[:c, :c]^t h   (trim.py:296-299)
+// Sketch-space kernels run one CTA of TRIM_SNT threads with one warp per
+// output and the lanes over the reduction index (coalesced, 32 loads in
+// flight per warp): a thread-per-output loop was a chain of c dependent
+// strided loads per column (ncu: 33 us per launch, the finish kernel 53 us)
 template <typename T>
-__global__ void __launch_bounds__(TRIM_NT)
+__global__ void __launch_bounds__(TRIM_SNT)
 trim_coef_kernel(const double* __restrict__ S, int64_t lds, int ell, const double* __restrict__ z,
                  const double* __restrict__ L, int64_t ldl, const T* __restrict__ w, const double* __restrict__ Tt,
                  int64_t ldtt, int c, double* __restrict__ coef, const Status* st) {
   extern __shared__ double h[];  // [c]
+  pdl_trigger();  // PDL: the next column kernel may be scheduled now
+  pdl_wait();     // ... and this one reads its predecessor's output only after this
   if (failed(st)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = warp; k < c; k += TRIM_NT / 32) {
+  constexpr int NW = TRIM_SNT / 32;
+  for (int k = warp; k < c; k += NW) {
     double d = 0.0;
     for (int i = lane; i < ell; i += 32) d = fma(S[i + k * lds], z[i], d);
     d = warp_sum(d);
@@ -73,22 +82,29 @@ trim_coef_kernel(const double* __restrict__ S, int64_t lds, int ell, const doubl
     if (lane == 0) h[k] = d - e;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < c; i += TRIM_NT) {
+  for (int i = warp; i < c; i += NW) {  // coef[i] = T~[:i+1, i] . h[:i+1]
+    const double* ti = Tt + (int64_t)i * ldtt;
     double d = 0.0;
-    for (int k = 0; k <= i; ++k) d = fma(Tt[k + i * ldtt], h[k], d);
-    coef[i] = d;
+    for (int k = lane; k <= i; k += 32) d = fma(ti[k], h[k], d);
+    d = warp_sum(d);
+    if (lane == 0) coef[i] = d;
   }
 }
 
-// w = fl(w - fl(U[:, :c] coef_lo)) over all N rows (trim.py:300)
+// w = fl(W[:, c] - fl(U[:, :c] coef_lo)) over all N rows (trim.py:300; w = W[:, c]
+// for c = 0), fused with the column-scaled input of the next K1:
+// x = [0 (c entries); w[c:m] * scales; w[m:]] (trim_prep_kernel's map)
 template <typename T>
 __global__ void __launch_bounds__(GEMV_NT, 2)
 trim_update_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int c, const double* __restrict__ coef,
-                   T* __restrict__ w, const Status* st) {
+                   const T* __restrict__ Wc, T* __restrict__ w, T* __restrict__ x, int64_t m,
+                   const double* __restrict__ scales, const Status* st) {
   using A = typename Lo<T>::acc;
   constexpr int VN = VecN<T>::n, NV = 4;
   extern __shared__ unsigned char smraw[];
   A* cl = reinterpret_cast<A*>(smraw);
+  pdl_trigger();  // PDL: the next column kernel may be scheduled now
+  pdl_wait();     // ... and this one reads its predecessor's output only after this
   if (failed(st)) return;
   for (int k = threadIdx.x; k < c; k += blockDim.x) cl[k] = Lo<T>::from_double(coef[k]);
   __syncthreads();
@@ -101,7 +117,15 @@ trim_update_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int c, const
 #pragma unroll
       for (int j = 0; j < VN; ++j) {
         const int64_t i = r0 + (v * GEMV_NT + threadIdx.x) * VN + j;
-        if (i < N) w[i] = Lo<T>::store(Lo<T>::sub(Lo<T>::load(w[i]), Lo<T>::rnd(acc[v][j])));
+        if (i < N) {
+          const T wv = c > 0 ? Lo<T>::store(Lo<T>::sub(Lo<T>::load(Wc[i]), Lo<T>::rnd(acc[v][j]))) : Wc[i];
+          w[i] = wv;
+          T xv;
+          if (i < c) xv = Lo<T>::store(A(0));
+          else if (i < m) xv = Lo<T>::store(Lo<T>::mul(Lo<T>::load(wv), Lo<T>::from_double(scales[i])));
+          else xv = wv;  // x * 1.0 is exact
+          x[i] = xv;
+        }
       }
   }
 }
@@ -120,6 +144,8 @@ __global__ void __launch_bounds__(TRIM_NT)
 trim_tail_kernel(const double* __restrict__ z, int ell, const T* __restrict__ w, int c,
                  const double* __restrict__ scales, T* __restrict__ x, double* __restrict__ scal, Status* st) {
   __shared__ double red[32];
+  pdl_trigger();  // PDL: the next column kernel may be scheduled now
+  pdl_wait();     // ... and this one reads its predecessor's output only after this
   if (failed(st)) return;
   const double zn = __dsqrt_rn(block_sumsq(z, ell, red));
   if (threadIdx.x == 0) {
@@ -142,7 +168,7 @@ trim_tail_kernel(const double* __restrict__ z, int ell, const T* __restrict__ w,
 // after vs = Om([0; v]): scaling, breakdown checks, and every sketch-space
 // column of the step (trim.py:115-146, 304-316)
 template <typename T>
-__global__ void __launch_bounds__(TRIM_NT)
+__global__ void __launch_bounds__(TRIM_SNT)
 trim_finish_kernel(double* __restrict__ vs, int ell, int c, int scaling, double u_high, const T* __restrict__ w,
                    const T* __restrict__ U, int64_t ldu, const double* __restrict__ E, int64_t lde,
                    double* __restrict__ S, int64_t lds, double* __restrict__ Tm, int64_t ldt,
@@ -151,6 +177,8 @@ trim_finish_kernel(double* __restrict__ vs, int ell, int c, int scaling, double 
                    double* __restrict__ bet, double* __restrict__ scal, Status* st) {
   extern __shared__ double sh[];  // [c] S^t vs, [c] lrow, [c] g, [1] flag
   __shared__ double red[32];
+  pdl_trigger();  // PDL: the next column kernel may be scheduled now
+  pdl_wait();     // ... and this one reads its predecessor's output only after this
   if (failed(st)) return;
   double* sv = sh;
   double* lrow = sh + c;
@@ -176,14 +204,15 @@ trim_finish_kernel(double* __restrict__ vs, int ell, int c, int scaling, double 
     beta = __dmul_rn(__dmul_rn(beta, piv), piv);
   }
   __syncthreads();  // every thread has read vs[0] before it is rescaled
-  for (int i = threadIdx.x; i < ell; i += TRIM_NT) {
+  for (int i = threadIdx.x; i < ell; i += TRIM_SNT) {
     const double s = scaling == SQB_SCALE_SQRT2 ? __dmul_rn(vs[i], fac) : __ddiv_rn(vs[i], fac);
     vs[i] = s;
     S[i + (int64_t)c * lds] = s;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = warp; k < c; k += TRIM_NT / 32) {
+  constexpr int NW = TRIM_SNT / 32;
+  for (int k = warp; k < c; k += NW) {
     double a = 0.0, b = 0.0;
     for (int i = lane; i < ell; i += 32) {
       a = fma(S[i + (int64_t)k * lds], vs[i], a);
@@ -198,21 +227,27 @@ trim_finish_kernel(double* __restrict__ vs, int ell, int c, int scaling, double 
     }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < c; k += TRIM_NT) {  // g = S^t vs - U[:c, :c]^t lrow
+  for (int k = warp; k < c; k += NW) {  // g = S^t vs - U[:c, :c]^t lrow
+    const T* uk = U + (int64_t)k * ldu;
     double d = 0.0;
-    for (int i = k; i < c; ++i) d = fma((double)Lo<T>::load(U[i + (int64_t)k * ldu]), lrow[i], d);
-    g[k] = sv[k] - d;
+    for (int i = k + lane; i < c; i += 32) d = fma((double)Lo<T>::load(uk[i]), lrow[i], d);
+    d = warp_sum(d);
+    if (lane == 0) g[k] = sv[k] - d;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < c; i += TRIM_NT) {
+  for (int i = warp; i < c; i += NW) {  // T[i, c], T~[i, c]: row i of T, T~ against sv, g
     double t = 0.0, tt = 0.0;
-    for (int k = i; k < c; ++k) {
+    for (int k = i + lane; k < c; k += 32) {
       t = fma(Tm[i + (int64_t)k * ldt], sv[k], t);
       tt = fma(Tt[i + (int64_t)k * ldtt], g[k], tt);
     }
-    Tm[i + (int64_t)c * ldt] = __dmul_rn(-beta, t);
-    Tt[i + (int64_t)c * ldtt] = __dmul_rn(-beta, tt);
-    R[i + (int64_t)c * ldr] = (double)Lo<T>::load(w[i]);
+    t = warp_sum(t);
+    tt = warp_sum(tt);
+    if (lane == 0) {
+      Tm[i + (int64_t)c * ldt] = __dmul_rn(-beta, t);
+      Tt[i + (int64_t)c * ldtt] = __dmul_rn(-beta, tt);
+      R[i + (int64_t)c * ldr] = (double)Lo<T>::load(w[i]);
+    }
   }
   if (threadIdx.x == 0) {
     Tm[c + (int64_t)c * ldt] = beta;
@@ -229,6 +264,8 @@ trim_finish_kernel(double* __restrict__ vs, int ell, int c, int scaling, double 
 template <typename T>
 __global__ void trim_ucol_kernel(T* __restrict__ Uc, const T* __restrict__ w, int64_t N, int c, int scaling,
                                  const double* __restrict__ scal, const Status* st) {
+  pdl_trigger();  // PDL: the next column kernel may be scheduled now
+  pdl_wait();     // ... and this one reads its predecessor's output only after this
   if (failed(st)) return;
   const double fac = scal[4], v0 = scal[3];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
@@ -292,26 +329,24 @@ static int trim_left_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
     SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, Xa, ldx, m - 1, Z0 + ell, ell, 0, P, st));
   }
   for (int64_t c = 0; c < m; ++c) {
-    SQB_CUDA_TRY(cudaMemcpyAsync(w, (const T*)W + c * ldw, esz * N, cudaMemcpyDeviceToDevice, s));
-    if (c > 0) {
-      trim_coef_kernel<T><<<1, TRIM_NT, sizeof(double) * c, s>>>(S, lds, (int)ell, Z0 + c * ell, L, ldl, w, Tt,
-                                                                 ldtt, (int)c, coef, st);
-      SQB_TRY(check_launch(ctx, "trim_coef_kernel"));
-      trim_update_kernel<T><<<gu, GEMV_NT, sizeof(typename Lo<T>::acc) * c, s>>>(U, ldu, N, (int)c, coef, w, st);
-      SQB_TRY(check_launch(ctx, "trim_update_kernel"));
+    if (c > 0) {  // w[:c] (read by the coefficient kernel) is W[:c, c]: the original column
+      SQB_TRY(launch_pdl(ctx, "trim_coef_kernel", trim_coef_kernel<T>, dim3(1), dim3(TRIM_SNT), sizeof(double) * c,
+                         (const double*)S, lds, (int)ell, (const double*)(Z0 + c * ell), (const double*)L, ldl,
+                         (const T*)W + c * ldw, (const double*)Tt, ldtt, (int)c, coef, (const Status*)st));
     }
-    trim_prep_kernel<T><<<gv, 256, 0, s>>>(x, w, N, c, m, scales, st);
-    SQB_TRY(check_launch(ctx, "trim_prep_kernel"));
+    SQB_TRY(launch_pdl(ctx, "trim_update_kernel", trim_update_kernel<T>, dim3(gu), dim3(GEMV_NT),
+                       sizeof(typename Lo<T>::acc) * std::max<int64_t>(c, 1), (const T*)U, ldu, N, (int)c,
+                       (const double*)coef, (const T*)W + c * ldw, w, x, m, scales, (const Status*)st));
     SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, z, ell, 0, P, st));
-    trim_tail_kernel<T><<<1, TRIM_NT, 0, s>>>(z, (int)ell, w, (int)c, scales, x, scal, st);
-    SQB_TRY(check_launch(ctx, "trim_tail_kernel"));
-    SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, vs, ell, 0, P, st));
-    trim_finish_kernel<T><<<1, TRIM_NT, sizeof(double) * (3 * c + 1), s>>>(
-        vs, (int)ell, (int)c, scaling, u_high, w, U, ldu, E, lde, S, lds, Tm, ldt, Tt, ldtt, R, ldr, L, ldl, sig,
-        rho, bet, scal, st);
-    SQB_TRY(check_launch(ctx, "trim_finish_kernel"));
-    trim_ucol_kernel<T><<<gv, 256, 0, s>>>(U + c * ldu, w, N, (int)c, scaling, scal, st);
-    SQB_TRY(check_launch(ctx, "trim_ucol_kernel"));
+    SQB_TRY(launch_pdl(ctx, "trim_tail_kernel", trim_tail_kernel<T>, dim3(1), dim3(TRIM_NT), 0, (const double*)z,
+                       (int)ell, (const T*)w, (int)c, scales, x, scal, st));
+    // x differs from the z sketch's input only at entry c: re-sketch the head tile
+    SQB_TRY(launch_sketch_resketch_head(ctx, sk, Lo<T>::code, x, ldx, c + 1, vs, ell, 0, P, st));
+    SQB_TRY(launch_pdl(ctx, "trim_finish_kernel", trim_finish_kernel<T>, dim3(1), dim3(TRIM_SNT),
+                       sizeof(double) * (3 * c + 1), vs, (int)ell, (int)c, scaling, u_high, (const T*)w,
+                       (const T*)U, ldu, E, lde, S, lds, Tm, ldt, Tt, ldtt, R, ldr, L, ldl, sig, rho, bet, scal, st));
+    SQB_TRY(launch_pdl(ctx, "trim_ucol_kernel", trim_ucol_kernel<T>, dim3(gv), dim3(256), 0, U + c * ldu,
+                       (const T*)w, N, (int)c, scaling, (const double*)scal, (const Status*)st));
   }
   return SQB_OK;
 }
@@ -512,10 +547,11 @@ static int trim_right_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
       SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, z, ell, 0, P, st));
       trim_tail_kernel<T><<<1, TRIM_NT, 0, s>>>(z, (int)ell, w, (int)c, scales, x, scal, st);
       SQB_TRY(check_launch(ctx, "trim_tail_kernel"));
-      SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, vs, ell, 0, P, st));
+      // x differs from the z sketch's input only at entry c: re-sketch the head tile
+      SQB_TRY(launch_sketch_resketch_head(ctx, sk, Lo<T>::code, x, ldx, c + 1, vs, ell, 0, P, st));
       // the left sweep's finish kernel also grows T, T~ and L; the right
       // variant overwrites them below with the reference's assembled forms
-      trim_finish_kernel<T><<<1, TRIM_NT, sizeof(double) * (3 * c + 1), s>>>(
+      trim_finish_kernel<T><<<1, TRIM_SNT, sizeof(double) * (3 * c + 1), s>>>(
           vs, (int)ell, (int)c, scaling, u_high, w, U, ldu, E, lde, S, lds, Tm, ldt, Tt, ldtt, R, ldr, L, ldl, sig,
           rho, bet, scal, st);
       SQB_TRY(check_launch(ctx, "trim_finish_kernel"));

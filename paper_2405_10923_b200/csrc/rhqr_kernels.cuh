@@ -240,14 +240,10 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
   // block roles: with helper_first the helper (block 0) and the identity block
   // (block 1) are dispatched first, so the helper's latency-bound sketch-space
   // work overlaps the first wave of tiles instead of trailing the last one
-  // tile CTAs: gridDim.x - 2 of them; with fewer CTAs than tiles each one
-  // walks tiles tile0, tile0 + ntc, ... (a static, SM-balanced share: see
-  // col_grid in rhqr_left.cu)
   const int64_t bid = blockIdx.x;
-  const int64_t ntc = (int64_t)gridDim.x - 2;
-  const int64_t helper_id = a.helper_first ? 0 : ntc + 1;
-  const int64_t top_id = a.helper_first ? 1 : ntc;
-  const int64_t tile0 = a.helper_first ? bid - 2 : bid;
+  const int64_t helper_id = a.helper_first ? 0 : a.n_eff + 1;
+  const int64_t top_id = a.helper_first ? 1 : a.n_eff;
+  const int64_t tile = a.helper_first ? bid - 2 : bid;
   if (bid == helper_id) {
     pdl_wait();
     if (failed(a.st)) return;
@@ -266,8 +262,6 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
   constexpr int TB = 1 << LOGT;
   constexpr int NV = TB / (COL_NT * VN);  // runs of VN rows per thread
   const int tb = 1 << a.log_tb;
-  for (int64_t tile = tile0; tile < a.n_eff; tile += ntc) {
-  if (tile != tile0) __syncthreads();  // the previous tile's leaves are read out of sm
   const int64_t e0 = tile << a.log_tb;  // first Omega coordinate of the tile
   const int64_t lim = a.n - e0;                       // valid rows in this tile (may exceed tb)
   const int64_t rows = lim < tb ? lim : tb;
@@ -445,7 +439,7 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
       }
     }
   }
-  if (!a.srht) continue;
+  if (!a.srht) return;
   __syncthreads();
   if constexpr (P16OK) {
     if (p16path) {
@@ -454,12 +448,11 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
       float* P = (float*)a.P + tile;
       for (int k = threadIdx.x; k < a.ell; k += COL_NT)
         P[k * a.n_tiles] = pk_lo_float<T>(s16[p16((int)(__ldg(a.idx + k) & ((1 << P16_LOG) - 1)))]);
-      continue;
+      return;
     }
   }
   tile_fwht<T>(sm, a.log_tb);
   tile_gather<T>(sm, a.idx, a.ell, a.log_tb, (A*)a.P + tile, a.n_tiles);
-  }  // tile loop
 }
 
 // Bulk-loop variant of the column pass.  2-byte storage: a raw 2-deep ring

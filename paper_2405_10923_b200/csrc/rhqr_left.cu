@@ -17,25 +17,6 @@ static int zero2d(sqb_ctx* ctx, double* p, int64_t rows, int64_t cols, int64_t l
   return check_launch(ctx, "zero_kernel");
 }
 
-// Grid of a column pass: one CTA per tile plus the helper and identity
-// blocks.  SQB_COL_PERSIST=1 (A/B only) launches exactly one wave of CTAs
-// that walk the tiles in a static stride instead, so that no partial last
-// wave lands on a subset of the SMs (ncu, config 4: SMs active 75% of the
-// pass).  Measured (scripts/ab_col_persist.py, bitwise identical): bf16
-// 2^24 x 256 231.5 vs 231.6 ms, bf16 2^23 118.0 vs 124.7 ms, fp32 2^24
-// 366.4 vs 363.6 ms, fp64 2^24 901 vs 858 ms — no BASELINE config gains, so
-// one CTA per tile stays the default.
-static unsigned col_grid(sqb_ctx* ctx, void (*k)(ColArgs), size_t smem, int64_t n_eff) {
-  const char* e = getenv("SQB_COL_PERSIST");
-  int per_sm = 0;
-  if (e && e[0] == '1' && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, COL_NT, smem) == cudaSuccess) {
-    const int64_t slots = (int64_t)per_sm * ctx->sm_count;
-    if (per_sm > 0 && n_eff + 2 > slots && slots >= 3) return (unsigned)slots;
-  }
-  (void)cudaGetLastError();
-  return (unsigned)(n_eff + 2);
-}
-
 // workspace of one sweep
 struct SweepWs {
   WsPlan plan;
@@ -163,7 +144,6 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
     if (small) colk = rhqr_col_kernel<T, VN, 0, 2, SMALL_LOG>;
   }
   cudaFuncSetAttribute(colk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
-  const unsigned col_ctas = col_grid(ctx, colk, col_smem_max, n_eff_col);
   for (int64_t c = 1; c < ncol; ++c) {
     SQB_TRY(ensure_y0(c + 2));
     double* a_cur = abuf + (c & 1) * (m + 1);
@@ -181,7 +161,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
     ca.no_pre = no_pre_env();
     const size_t smem = sizeof(A) * ((c + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(c + 1));
     prof_begin(ctx);
-    SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", colk, dim3(col_ctas), dim3(COL_NT), smem,
+    SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", colk, dim3((unsigned)(n_eff_col + 2)), dim3(COL_NT), smem,
                        ca));
     // algorithmic bytes of this pass: read U[:, :c] and W[:, c], write U[:, c]
     prof_end(ctx, (double)esz * (double)N * (double)(c + 2));

@@ -1,4 +1,5 @@
-"""A/B of the column-pass grid (SQB_COL_PERSIST=1: one wave of CTAs walking
+"""(Historical: the SQB_COL_PERSIST switch and the tile loop were removed after this
+A/B.)  A/B of the column-pass grid (SQB_COL_PERSIST=1: one wave of CTAs walking
 the tiles in a static stride; 0: one CTA per tile), interleaved in one
 process, bitwise check of R and U between the two."""
 import os

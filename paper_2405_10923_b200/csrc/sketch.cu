@@ -375,7 +375,9 @@ __device__ __forceinline__ uint32_t tma_off(uint32_t r, uint32_t i) {
   return h * 4096u + r * 128u + ((((c >> 4) ^ (r & 7u)) << 4) | (c & 15u));
 }
 
-template <typename T, int KPL, int S, int WPB>
+// LG: log2 of the leaf group (12: 4 sub-tiles, levels 10-11 at the sampled
+// positions; 13: 8 sub-tiles, levels 10-12 — half the leaves for the tree)
+template <typename T, int KPL, int S, int WPB, int LG>
 __global__ void __launch_bounds__(WPB * 32)
 srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restrict__ X, int64_t ldx, int64_t n,
                      int64_t n_eff, int64_t k, const uint32_t* __restrict__ bits, const int64_t* __restrict__ idx,
@@ -396,14 +398,16 @@ srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restric
     for (int s = 0; s < S; ++s) mbar_init(bars + s, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncwarp();
+  static_assert(LG == 12 || LG == 13, "leaf group of 4 or 8 sub-tiles");
+  constexpr int NQ = 1 << (LG - 10);  // sub-tiles per leaf group
   // per output k = lane + 32 i: byte offset of its position p mod 1024 in the
-  // transpose buffer (bits 0-15), bit 10 of p at bit 16, bit 11 at bit 17
+  // transpose buffer (bits 0-15), bits 10.. of p from bit 16 up
   uint32_t mypk[KPL];
 #pragma unroll
   for (int i = 0; i < KPL; ++i) {
     const int kk = lane + 32 * i;
-    const uint32_t p = kk < ell ? (uint32_t)(__ldg(idx + kk) & 4095) : 0u;
-    mypk[i] = (uint32_t)(((p & 1023u) >> 5) * RS + (p & 31u)) * (uint32_t)sizeof(T) | (((p >> 10) & 3u) << 16);
+    const uint32_t p = kk < ell ? (uint32_t)(__ldg(idx + kk) & ((1 << LG) - 1)) : 0u;
+    mypk[i] = (uint32_t)(((p & 1023u) >> 5) * RS + (p & 31u)) * (uint32_t)sizeof(T) | ((p >> 10) << 16);
   }
   // each warp owns a contiguous run of (column, group) items, walked by
   // cursors (no per-unit division): one for the unit being transformed, one
@@ -416,19 +420,19 @@ srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restric
   // leave as whole sectors (a contiguous range per warp doubled DRAM writes)
   const int64_t my_items = wg < items ? (items - wg + nwarps - 1) / nwarps : 0;
   const int64_t dcol = nwarps / n_eff, dg = nwarps - dcol * n_eff;
-  const int64_t units = my_items * 4;  // sub-tiles this warp processes
+  const int64_t units = my_items * NQ;  // sub-tiles this warp processes
   struct Cur {  // (column, group, sub-tile) of a unit; advance without division
     int64_t col, g;
     int q;
     __device__ void next(int64_t ne, int64_t dc, int64_t dgg) {
-      if (++q == 4) {
+      if (++q == NQ) {
         q = 0;
         g += dgg;
         col += dc;
         if (g >= ne) { g -= ne; ++col; }
       }
     }
-    __device__ int64_t e0() const { return (g << 12) + ((int64_t)q << 10); }
+    __device__ int64_t e0() const { return (g << LG) + ((int64_t)q << 10); }
   };
   Cur cu{wg / n_eff, wg % n_eff, 0};
   Cur ci = cu, cw = cu;
@@ -450,9 +454,9 @@ srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restric
   cw.next(n_eff, dcol, dg);
   // lane-run reads of a swizzled stage: chunk c of half h at (c ^ (lane & 7))
   const uint32_t run_base = (uint32_t)lane * 128u, run_x = ((uint32_t)lane & 7u) << 4;
-  T ab[KPL], acc[KPL];
+  T ab[KPL], acc[KPL], ac2[KPL];
 #pragma unroll
-  for (int i = 0; i < KPL; ++i) ab[i] = acc[i] = T(0);
+  for (int i = 0; i < KPL; ++i) ab[i] = acc[i] = ac2[i] = T(0);
   for (int64_t u = 0; u < units; ++u, cu.next(n_eff, dcol, dg)) {
     const int64_t col = cu.col, e0 = cu.e0();
     const int q = cu.q;
@@ -508,23 +512,26 @@ srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restric
 #pragma unroll
     for (int j = 0; j < 32; ++j) buf[j * RS + lane] = v[j];
     __syncwarp();
-    // tree levels 10 and 11 at the sampled positions, branch-free:
-    // acc = (q odd) ? acc -+ s : s ; ab = acc before sub-tile 2 overwrites it
+    // tree levels 10.. at the sampled positions (a binary counter over the
+    // group's sub-tiles, warp-uniform in q; left operand = lower sub-tiles):
+    // acc = (q odd) ? acc -+ s : s ; ab = the level-11 node of sub-tiles 0-3
     // (x - y is x + (-y) exactly, so the sign bit selects add or sub)
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
       const uint32_t pk = mypk[i];
       const T sv = *reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(buf) + (pk & 0xffffu));
       const T t = Lo<T>::add(acc[i], flip_sign(sv, pk, 16));
-      if (q == 2) ab[i] = acc[i];
+      if ((q & 3) == 2) ab[i] = acc[i];
       acc[i] = (q & 1) ? t : sv;
+      if (LG == 13 && q == 3) ac2[i] = Lo<T>::add(ab[i], flip_sign(acc[i], pk, 17));
     }
-    if (q == 3) {
-      T* leaves = P + (col * n_tiles + (e0 >> 12)) * ell;
+    if (q == NQ - 1) {
+      T* leaves = P + (col * n_tiles + (e0 >> LG)) * ell;
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
         const int kk = lane + 32 * i;
-        if (kk < ell) leaves[kk] = Lo<T>::add(ab[i], flip_sign(acc[i], mypk[i], 17));
+        const T l11 = Lo<T>::add(ab[i], flip_sign(acc[i], mypk[i], 17));
+        if (kk < ell) leaves[kk] = LG == 13 ? Lo<T>::add(ac2[i], flip_sign(l11, mypk[i], 18)) : l11;
       }
     }
     __syncwarp();
@@ -548,7 +555,7 @@ static EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-template <typename T, int KPL, int S, int WPB>
+template <typename T, int KPL, int S, int WPB, int LG>
 static int launch_tma(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int64_t n_local, int64_t e_base,
                       const T* X, int64_t ldx, int64_t k, T sc, T* P, const Status* st) {
   EncodeTiledFn enc = encode_tiled();
@@ -566,7 +573,7 @@ static int launch_tma(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int
   if (r != CUDA_SUCCESS) return set_error(ctx, SQB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   const size_t smem = 1024 + (size_t)WPB * S * Tma<T>::STAGE + sizeof(T) * (size_t)WPB * 32 * wt_rs<T>() +
                        (size_t)WPB * S * 8;
-  auto kern = srht_tma_tile_kernel<T, KPL, S, WPB>;
+  auto kern = srht_tma_tile_kernel<T, KPL, S, WPB, LG>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   int per_sm = 1;
@@ -584,9 +591,13 @@ template <typename T, int S, int WPB>
 static int launch_tma_kpl(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int64_t n_local, int64_t e_base,
                           const T* X, int64_t ldx, int64_t k, T sc, T* P, const Status* st) {
   const int kpl = (int)((sk->ell + 31) / 32);
-  if (kpl <= 4) return launch_tma<T, 4, S, WPB>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
-  if (kpl <= 8) return launch_tma<T, 8, S, WPB>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
-  return launch_tma<T, 16, S, WPB>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+  if (g.log_tb == 13) {  // 8-sub-tile leaf groups (standalone geometry, ell <= 256)
+    if (kpl <= 4) return launch_tma<T, 4, S, WPB, 13>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+    return launch_tma<T, 8, S, WPB, 13>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+  }
+  if (kpl <= 4) return launch_tma<T, 4, S, WPB, 12>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+  if (kpl <= 8) return launch_tma<T, 8, S, WPB, 12>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+  return launch_tma<T, 16, S, WPB, 12>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1065,10 +1076,21 @@ static bool getenv_flag0(const char* name) {
   return e && e[0] == '0';
 }
 
-static SrhtGeom standalone_geom(const sqb_sketch* sk) {
+// fp64 / fp32 with ell <= 256: 8192-coordinate leaf groups (the TMA warp-tile
+// kernel folds 8 sub-tiles at the sampled positions), half the leaves of the
+// 4096-coordinate groups for the tile kernel to write and the tree to read
+// (bitwise the same sketch).  SQB_K1_G13=0 keeps 4096 (A/B).
+// Only with enough groups to fill the GPU ((n_pad / 8192) k >= 2048 warp
+// items): halving the items of a single vector or a short matrix costs more
+// latency than the leaves save (2^20 x 1: 16.9 -> 19.1 us; 5000 x 3: 15.1 ->
+// 21.0 us; 2^20 x 128: 236.9 -> 223.5 us).
+static SrhtGeom standalone_geom(const sqb_sketch* sk, int dtype, int64_t k) {
   SrhtGeom g;
   const int lp = ilog2_exact(sk->n_pad);
   g.log_tb = lp < S64_LOG ? lp : S64_LOG;
+  if ((dtype == SQB_F64 || dtype == SQB_F32) && sk->ell <= 256 && lp > S64_LOG &&
+      (sk->n_pad >> (S64_LOG + 1)) * k >= 2048 && !getenv_flag0("SQB_K1_G13"))
+    g.log_tb = S64_LOG + 1;
   g.n_tiles = sk->n_pad >> g.log_tb;
   const int64_t tb = int64_t(1) << g.log_tb;
   g.n_eff = (sk->n + tb - 1) / tb;
@@ -1078,8 +1100,8 @@ static SrhtGeom standalone_geom(const sqb_sketch* sk) {
 size_t sketch_partials_bytes(const sqb_sketch* sk, int dtype, int64_t k) {
   if (sk->kind != SQB_SKETCH_SRHT) return dense_ws_bytes(sk, dtype, k);
   // room for the standalone geometry and for the fused column kernels' own tiles
-  const SrhtGeom g = srht_geom(sk, dtype), g2 = standalone_geom(sk);
-  return acc_bytes(dtype) * (size_t)sk->ell * (size_t)std::max(g.n_tiles, g2.n_tiles) * (size_t)k;
+  const SrhtGeom g = srht_geom(sk, dtype), g2 = standalone_geom(sk, dtype, k), g12 = standalone_geom(sk, SQB_F16, k);
+  return acc_bytes(dtype) * (size_t)sk->ell * (size_t)std::max(std::max(g.n_tiles, g2.n_tiles), g12.n_tiles) * (size_t)k;
 }
 
 template <typename T>
@@ -1125,7 +1147,8 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
   }
   if constexpr (sizeof(T) >= 4) {
     // TMA-staged warp tiles (ell <= 512: the per-lane output registers)
-    if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= 512 && n_local >= 32 && encode_tiled())
+    const bool tma_geom = g.log_tb == S64_LOG || (g.log_tb == S64_LOG + 1 && sk->ell <= 256);
+    if (vec && tma_geom && (e_base & 63) == 0 && sk->ell <= 512 && n_local >= 32 && encode_tiled())
       return launch_tma_kpl<T, 2, 4>(ctx, sk, g, n_local, e_base, (const T*)X, ldx, k, (T)sc, (T*)P, st);
     if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= S64_MAX_ELL) {
       const size_t smem64 = s64_head_bytes((int)sk->ell, sizeof(T)) + s64_buf_bytes<T>();
@@ -1161,7 +1184,7 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
 template <typename T>
 static int srht_tiles_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int64_t ldx, int64_t k,
                         void* P, const Status* st) {
-  return srht_tiles_geom_t<T>(ctx, sk, standalone_geom(sk), sk->n, 0, X, ldx, k, P, st);
+  return srht_tiles_geom_t<T>(ctx, sk, standalone_geom(sk, Lo<T>::code, k), sk->n, 0, X, ldx, k, P, st);
 }
 
 // group-major tree launch: 8 chunk warps per 32 outputs, or 32 when the
@@ -1210,7 +1233,7 @@ template <typename T>
 static int srht_tree_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* P, int64_t k, double* Y,
                        int64_t ldy, int64_t row_off, const Status* st) {
   using A = typename Lo<T>::acc;
-  const SrhtGeom g = standalone_geom(sk);
+  const SrhtGeom g = standalone_geom(sk, Lo<T>::code, k);
   double sc, nm;
   srht_constants(sk, Lo<T>::code, &sc, &nm);
   return launch_tree_gm<T>(ctx, sk, g, P, k, Y, ldy, row_off, (A)nm, 1, st);
@@ -1286,7 +1309,7 @@ static int resketch_head_t(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, in
                            double* Y, int64_t ldy, int64_t row_off, void* partials, const Status* st) {
   if (sk->kind != SQB_SKETCH_SRHT || getenv_flag0("SQB_RESKETCH_HEAD"))
     return sketch_t<T>(ctx, sk, X, ldx, 1, Y, ldy, row_off, partials, st);
-  SrhtGeom g = standalone_geom(sk);
+  SrhtGeom g = standalone_geom(sk, Lo<T>::code, 1);
   const int64_t tb = int64_t(1) << g.log_tb;
   if (upto > tb) return sketch_t<T>(ctx, sk, X, ldx, 1, Y, ldy, row_off, partials, st);
   SrhtGeom g0 = g;

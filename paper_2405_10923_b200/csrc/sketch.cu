@@ -12,6 +12,13 @@
 
 namespace sqb {
 
+// SQB_<NAME>=0 switches an optimisation off (A/B experiments)
+static bool getenv_flag0(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] == '0';
+}
+
+
 // ---------------------------------------------------------------------------
 // host rounding helpers (numpy semantics)
 // ---------------------------------------------------------------------------
@@ -538,6 +545,109 @@ srht_tma_tile_kernel(const __grid_constant__ CUtensorMap map, const T* __restric
   }
 }
 
+// Few leaf groups (a single vector, a short matrix): one CTA per 4096-
+// coordinate group, warp q transforms sub-tile q (the same per-sub-tile code
+// as srht_tma_tile_kernel), the four sampled values of each output meet in
+// shared memory and fold as (s0 +- s1) +- (s2 +- s3) — the same operations
+// in the same order, so the leaves are bitwise those of the warp-per-group
+// kernel, at a quarter of its per-group latency.
+template <typename T, int KPL>
+__global__ void __launch_bounds__(128)
+srht_tma_split_kernel(const __grid_constant__ CUtensorMap map, const T* __restrict__ X, int64_t ldx, int64_t n,
+                      int64_t n_eff, int64_t k, const uint32_t* __restrict__ bits, const int64_t* __restrict__ idx,
+                      int ell, T scale_lo, T* __restrict__ P, int64_t n_tiles, const Status* st, int64_t e_base) {
+  constexpr int C = 16 / (int)sizeof(T), RS = wt_rs<T>();
+  constexpr uint32_t SB = Tma<T>::STAGE;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  if (st && failed(st)) return;
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  // [1024-aligned stages: 4 x SB][transpose buffers: 4 x 32 x RS][samples: 4 x 32 KPL][barriers: 4]
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* sb = base + (size_t)q * SB;
+  T* buf = reinterpret_cast<T*>(base + 4 * (size_t)SB) + q * 32 * RS;
+  T* samp = reinterpret_cast<T*>(base + 4 * (size_t)SB + sizeof(T) * 4 * 32 * RS);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 4 * (size_t)SB + sizeof(T) * 4 * 32 * (RS + KPL)) + q;
+  if (lane == 0) mbar_init(bar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  uint32_t mypk[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int kk = lane + 32 * i;
+    const uint32_t p = kk < ell ? (uint32_t)(__ldg(idx + kk) & 1023) : 0u;
+    mypk[i] = (uint32_t)((p >> 5) * RS + (p & 31u)) * (uint32_t)sizeof(T);
+  }
+  const uint32_t run_base = (uint32_t)lane * 128u, run_x = ((uint32_t)lane & 7u) << 4;
+  uint32_t phase = 0;
+  const int64_t items = n_eff * k;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t col = item / n_eff, g = item - col * n_eff;
+    const int64_t e0 = (g << 12) + ((int64_t)q << 10), e = e0 + lane * 32;
+    const bool full = e0 + 1024 <= n;
+    if (full) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, SB);
+#pragma unroll
+        for (int h = 0; h < Tma<T>::NH; ++h)
+          tma_load_3d(sb + h * 4096, &map, h * Tma<T>::HALF, (int)(e0 >> 5), (int)col, bar);
+      }
+    }
+    const uint32_t w = __ldg(bits + ((e_base + e) >> 5));
+    if (full) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    } else {  // the column tail / padding: staged by hand in the same swizzled layout
+      const T* x = X + col * ldx;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        *reinterpret_cast<T*>(sb + tma_off<T>(lane, j)) = (e + j < n) ? x[e + j] : T(0);
+      __syncwarp();
+    }
+    T v[32];
+#pragma unroll
+    for (int c = 0; c < 32 / C; ++c) {
+      const uint32_t h = (uint32_t)(c * C) / Tma<T>::HALF, cc = (uint32_t)(c % (Tma<T>::HALF / C));
+      const uint4 r = *reinterpret_cast<const uint4*>(sb + h * 4096u + run_base + ((cc << 4) ^ run_x));
+      unpack16<T>(r, v + c * C);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = flip_sign(Lo<T>::mul(v[j], scale_lo), w, j);
+    if (e + 32 > n) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (e + j >= n) v[j] = T(0);
+    }
+    fwht32_regs<T>(v);  // h = 1..16
+    {
+      T* row = buf + lane * RS;
+#pragma unroll
+      for (int c = 0; c < 32 / C; ++c) vstore<T>(row + c * C, v + c * C);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = buf[j * RS + lane];
+    fwht32_regs<T>(v);  // h = 32..512
+#pragma unroll
+    for (int j = 0; j < 32; ++j) buf[j * RS + lane] = v[j];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < KPL; ++i)
+      samp[q * 32 * KPL + lane + 32 * i] =
+          *reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(buf) + mypk[i]);
+    __syncthreads();
+    T* leaves = P + (col * n_tiles + g) * ell;
+    for (int kk = threadIdx.x; kk < ell; kk += 128) {
+      const uint32_t p = (uint32_t)(__ldg(idx + kk) & 4095);
+      const T s0 = samp[kk], s1 = samp[32 * KPL + kk], s2 = samp[64 * KPL + kk], s3 = samp[96 * KPL + kk];
+      const T a = Lo<T>::add(s0, flip_sign(s1, p, 10));
+      const T b = Lo<T>::add(s2, flip_sign(s3, p, 10));
+      leaves[kk] = Lo<T>::add(a, flip_sign(b, p, 11));
+    }
+    __syncthreads();  // samples and stages are reused by the next item
+  }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -587,10 +697,44 @@ static int launch_tma(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int
   return check_launch(ctx, "srht_tma_tile_kernel");
 }
 
+template <typename T, int KPL>
+static int launch_tma_split(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int64_t n_local, int64_t e_base,
+                            const T* X, int64_t ldx, int64_t k, T sc, T* P, const Status* st) {
+  EncodeTiledFn enc = encode_tiled();
+  CUtensorMap map;
+  const cuuint64_t runs = (cuuint64_t)(n_local >> 5);
+  const cuuint64_t dims[3] = {(cuuint64_t)Tma<T>::HALF * Tma<T>::NH, std::max<cuuint64_t>(runs, 1), (cuuint64_t)k};
+  const cuuint64_t strides[2] = {32 * sizeof(T), (cuuint64_t)ldx * sizeof(T)};
+  const cuuint32_t box[3] = {(cuuint32_t)Tma<T>::HALF, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                         const_cast<T*>(X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(ctx, SQB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  const size_t smem = 1024 + 4 * (size_t)Tma<T>::STAGE + sizeof(T) * 4 * 32 * (size_t)(wt_rs<T>() + KPL) + 4 * 8;
+  auto kern = srht_tma_split_kernel<T, KPL>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t items = g.n_eff * k;
+  kern<<<(unsigned)std::min<int64_t>(items, 65535), 128, smem, ctx->stream>>>(
+      map, X, ldx, n_local, g.n_eff, k, sk->sign_bits, sk->indices, (int)sk->ell, sc, P, g.n_tiles, st, e_base);
+  return check_launch(ctx, "srht_tma_split_kernel");
+}
+
 template <typename T, int S, int WPB>
 static int launch_tma_kpl(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int64_t n_local, int64_t e_base,
                           const T* X, int64_t ldx, int64_t k, T sc, T* P, const Status* st) {
   const int kpl = (int)((sk->ell + 31) / 32);
+  // few 4096-coordinate groups (<= 4 per SM): one CTA per group, a warp per
+  // sub-tile (SQB_K1_SPLIT=0: the warp-per-group kernel).  Measured (digests
+  // unchanged): 2^20 x 1 14.5 vs 18.9 us, 16352 x 32 14.2 vs 18.1 us,
+  // 5000 x 3 13.8 vs 17.9 us; at 2^22 x 1 (1024 groups) 26.2 vs 23.9 us, so
+  // many groups keep the warp-per-group kernel
+  if (g.log_tb == S64_LOG && g.n_eff * k <= 4 * (int64_t)ctx->sm_count && !getenv_flag0("SQB_K1_SPLIT")) {
+    if (kpl <= 4) return launch_tma_split<T, 4>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+    if (kpl <= 8) return launch_tma_split<T, 8>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+    return launch_tma_split<T, 16>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
+  }
   if (g.log_tb == 13) {  // 8-sub-tile leaf groups (standalone geometry, ell <= 256)
     if (kpl <= 4) return launch_tma<T, 4, S, WPB, 13>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
     return launch_tma<T, 8, S, WPB, 13>(ctx, sk, g, n_local, e_base, X, ldx, k, sc, P, st);
@@ -1070,12 +1214,6 @@ __global__ void identity_kernel(const T* __restrict__ X, int64_t ldx, int64_t n,
 // ---------------------------------------------------------------------------
 // standalone sketches use 4096-coordinate tiles for every dtype (the tile size
 // only regroups the same butterflies: any power of two gives the same bits)
-// SQB_<NAME>=0 switches an optimisation off (A/B experiments)
-static bool getenv_flag0(const char* name) {
-  const char* e = getenv(name);
-  return e && e[0] == '0';
-}
-
 // fp64 / fp32 with ell <= 256: 8192-coordinate leaf groups (the TMA warp-tile
 // kernel folds 8 sub-tiles at the sampled positions), half the leaves of the
 // 4096-coordinate groups for the tile kernel to write and the tree to read

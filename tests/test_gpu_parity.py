@@ -54,7 +54,9 @@ def test_srht_bf16_bitwise(P):
 
 @pytest.mark.parametrize("ell,n,seed,k", [(256, (1 << 20) - 128, 3, 3), (512, (1 << 18) - 256, 4, 2),
                                           (400, (1 << 22) - 201, 5, 1), (128, 3 * 4096 + 17, 6, 5),
-                                          (256, (1 << 16) - 3, 8, 40)])  # 40 columns: the 8-warp chunked tree
+                                          (256, (1 << 16) - 3, 8, 40),  # 40 columns: the 8-warp chunked tree
+                                          (200, (1 << 18) - 5, 9, 64),  # 8192-coordinate leaf groups
+                                          (96, 1 << 20, 10, 1)])  # one CTA per group (split kernel)
 def test_srht_bitwise_against_oracle_large(P, ell, n, seed, k):
     op = P.SRHTSketch(ell, n, seed)
     ref = O.SRHT(ell, n, seed)
@@ -72,6 +74,15 @@ def test_srht_lowprec_bitwise_against_oracle(P, tag, ell, n, seed, k):
     ref = O.SRHT(ell, n, seed)
     dt = O.TAG_DTYPE[tag]
     X = O.round_to(np.random.default_rng(seed).standard_normal((n, k)), tag)
+    assert np.array_equal(op.apply(X, dt), ref.apply(X, dt))
+
+
+def test_srht_fp32_wide_groups_bitwise(P):
+    """fp32 on the 8192-coordinate leaf groups ((n_pad / 8192) k >= 2048)."""
+    op = P.SRHTSketch(200, (1 << 18) - 5, 9)
+    ref = O.SRHT(200, (1 << 18) - 5, 9)
+    dt = O.TAG_DTYPE["single"]
+    X = O.round_to(np.random.default_rng(9).standard_normal(((1 << 18) - 5, 64)), "single")
     assert np.array_equal(op.apply(X, dt), ref.apply(X, dt))
 
 

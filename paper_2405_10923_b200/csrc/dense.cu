@@ -151,8 +151,17 @@ __global__ void dense_reduce_kernel(const double* __restrict__ P, int64_t M, int
   if (st && failed(st)) return;
   const int64_t MN = M * N;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < MN; e += (int64_t)gridDim.x * blockDim.x) {
+    // slab order (deterministic); eight slab loads in flight ahead of the adds
     double s = 0.0;
-    for (int z = 0; z < S; ++z) s += P[z * MN + e];
+    int z = 0;
+    for (; z + 8 <= S; z += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = P[(int64_t)(z + u) * MN + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; z < S; ++z) s += P[(int64_t)z * MN + e];
     const int64_t r = e % M, c = e / M;
     Y[row_off + r + c * ldy] = s;
   }

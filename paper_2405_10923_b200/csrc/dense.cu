@@ -21,7 +21,11 @@
 
 namespace sqb {
 
-constexpr int DBM = 128, DBN = 64, DBK = 32, DSTR = DBK + 4, DSTAGES = 3, DNT = 256;
+// 64-deep k tiles, double-buffered (2 x 102 KB): half the block barriers of
+// the former 32-deep 3-stage ring per flop; the next tile's cp.async traffic
+// (2.2 us at the per-SM HBM share) hides under 4.2 us of DMMA.  Config 3:
+// 6.87 -> 6.44 ms (round 1 session 4).
+constexpr int DBM = 128, DBN = 64, DBK = 64, DSTR = DBK + 4, DSTAGES = 2, DNT = 256;
 constexpr size_t DSMEM = sizeof(double) * DSTAGES * (size_t)(DBM + DBN) * DSTR;
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {

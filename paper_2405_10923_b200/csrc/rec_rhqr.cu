@@ -44,8 +44,17 @@ hqr_kernel(const double* __restrict__ Z, int64_t ldz, int od, int m, int scaling
     T[(e % m) + (int64_t)(e / m) * ldt] = 0.0;
     R[(e % m) + (int64_t)(e / m) * ldr] = 0.0;
   }
+  // Z[:, c+1] is fetched while column c is processed (od <= HQR_NT: one
+  // entry per thread), so the global load is off the per-column chain
+  const bool pre = od <= HQR_NT;
+  double zpre = (pre && tid < od) ? Z[tid] : 0.0;
   for (int c = 0; c < m; ++c) {
-    for (int r = tid; r < od; r += HQR_NT) w[r] = Z[r + (int64_t)c * ldz];
+    if (pre) {
+      if (tid < od) w[tid] = zpre;
+      if (tid < od && c + 1 < m) zpre = Z[tid + (int64_t)(c + 1) * ldz];
+    } else {
+      for (int r = tid; r < od; r += HQR_NT) w[r] = Z[r + (int64_t)c * ldz];
+    }
     __syncthreads();
     if (c > 0) {
       // coef = T[:c,:c]^t (U[:, :c]^t w); w = w - U[:, :c] coef   (baselines.py:57-59)

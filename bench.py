@@ -323,6 +323,11 @@ class RecRHQR(Workload):
         self.alg = 8.0 * (ell * n + N * m + N * m)
         self.flops = 2.0 * ell * n * m
         self.kernel = "dense_dmma_kernel (FP64 DMMA split-K sketch GEMM)"
+        # the sketch GEMM is tensor-bound (AI ~12.8 flop/B): its roofline is
+        # the FP64 DMMA pipe, which MEASURED_PEAKS.json does not carry
+        self.roof = {"bound": "tensor", "unit": "TFLOP/s", "scale": 1e12, "peak": 37.0,
+                     "peak_source": "profiles/fp64_peak_b200.txt (register-only DMMA m16n8k16 probe, 36.8-37.1 "
+                                    "TFLOP/s on this pool's B200s; MEASURED_PEAKS.json has no FP64 figure)"}
         self.config = {"workload": f"rec_rhqr cfg3: W {N} x {m} fp64 gen_cmatrix, Gaussian ell={ell}",
                        "N": N, "m": m, "ell": ell, "sketch_seed": CFG["sketch_seed"],
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
@@ -330,7 +335,25 @@ class RecRHQR(Workload):
                        "sketch_gflop": self.flops / 1e9}
 
     def e2e(self, steps):
-        return None
+        import torch
+
+        import paper_2405_10923_b200 as P
+        N, m, ell = self.N, self.m, self.ell
+        Wp = torch.from_numpy(np.asfortranarray(self.W_host).T).pin_memory().T  # pinned, column-major
+        for _ in range(2):
+            P.rec_rhqr(Wp, self.om)
+        torch.cuda.synchronize()
+        reps = max(3, min(steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            F = P.rec_rhqr(Wp, self.om)
+            _ = float(F.R[0, 0])
+        dt = (time.perf_counter() - t0) / reps
+        return {"value": self.alg / dt / 1e9, "unit": "GB/s", "ms_per_step": dt * 1e3,
+                "h2d_bytes_per_step": 8 * N * m,
+                "d2h_bytes_per_step": 8 * (N * m + (m + ell) * m + 2 * m * m + 3 * m),
+                "note": ("P.rec_rhqr(pinned host float64 W) -> host float64 U,S,T,R,scalars (upload, "
+                         "factorization, download in series: no streamed pipeline for rec_rhqr); wall clock")}
 
     def cpu_sample(self):
         from oracle import sketchqr_oracle as O
@@ -390,7 +413,12 @@ class GMRESCycle(Workload):
             self.b = torch.from_numpy(b).cuda()
             self.step = lambda check=False: P.rhqr_gmres(self.A, self.b, None, m, self.om)
         self.alg = float(sum(8 * N * (2 * j + 5) for j in range(1, m + 1)) + m * (12 * nnz + 12 * N))
-        self.kernel = "update_kernel / arn_q_kernel (streaming GEMVs over the Krylov reflectors)"
+        self.kernel = ("arn_q_kernel (streaming GEMV q = e_j - U_j coef over the Krylov reflectors; the "
+                       "apply_reflectors update GEMV has the same shape)")
+        self.host = (indptr, indices, data, b, N)
+        self.roof_note = ("achieved can reach the measured peak: the GEMV is a read stream (the peak is a "
+                          "read+write copy), and the reflector columns written moments earlier are partly "
+                          "L2-resident")
         self.config = {"workload": f"rhqr_gmres cfg5: one GMRES({m}) cycle, {k}^2 grid CSR (nnz {nnz}), SRHT {self.ell}",
                        "N": N, "m": m, "ell": self.ell, "nnz": nnz,
                        "parallelism": (f"row-partitioned x{ws} (q all-gather + 2 sketch all-gathers per step)"
@@ -398,7 +426,30 @@ class GMRESCycle(Workload):
                        "l2": "no flush: U (6.7 GB) exceeds L2", "alg_bytes_per_step": self.alg}
 
     def e2e(self, steps):
-        return None
+        import scipy.sparse
+        import torch
+
+        import paper_2405_10923_b200 as P
+        if not hasattr(self, "A"):
+            return None
+        indptr, indices, data, b, N = self.host
+        A = scipy.sparse.csr_matrix((data, indices, indptr), shape=(N, N))
+        bp = torch.from_numpy(b).pin_memory()
+        for _ in range(2):
+            P.rhqr_gmres(A, bp, None, self.m, self.om)
+        torch.cuda.synchronize()
+        reps = max(3, min(steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            x, hist = P.rhqr_gmres(A, bp, None, self.m, self.om)
+            _ = float(np.asarray(x)[0])
+        dt = (time.perf_counter() - t0) / reps
+        nnz = int(indptr[-1])
+        return {"value": self.alg / dt / 1e9, "unit": "GB/s", "ms_per_step": dt * 1e3,
+                "h2d_bytes_per_step": int(indptr.nbytes + indices.nbytes + data.nbytes + 8 * N),
+                "d2h_bytes_per_step": 8 * N + 8 * (self.m + 1),
+                "note": (f"P.rhqr_gmres(host scipy CSR ({nnz} nnz), pinned host b) -> host x and residual "
+                         "history: the CSR upload is inside every timed call; wall clock")}
 
     def cpu_sample(self):
         import scipy.sparse
@@ -531,7 +582,9 @@ def main():
 
     e2e = None if args.no_e2e else wl.e2e(args.steps)
     peak, peak_kind = measured_peak()
-    achieved = (k_bytes / k_n) / (k_ms / k_n * 1e-3) / 1e9 if k_n else None
+    roof = getattr(wl, "roof", None) or {"bound": "hbm", "unit": "GB/s", "scale": 1e9, "peak": peak,
+                                         "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)"}
+    achieved = (k_bytes / k_n) / (k_ms / k_n * 1e-3) / roof["scale"] if k_n else None
     traffic, traffic_detail = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -565,14 +618,14 @@ def main():
             "config": wl.config,
             "e2e": e2e,
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "roofline": {"bound": roof["bound"], "achieved": achieved, "peak": roof["peak"], "unit": roof["unit"],
+                         "frac": (achieved / roof["peak"]) if achieved else None, "traffic": traffic,
                          "traffic_detail": traffic_detail,
                          "kernel": wl.kernel,
-                         "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                         "peak_source": roof["peak_source"],
                          "kernel_share_of_step": (k_ms / args.steps) / prof_step_ms if prof_step_ms else None,
                          "timing": "per-launch CUDA events on the library stream over K extra steps",
-                         "launches_timed": k_n},
+                         "launches_timed": k_n, **({"note": wl.roof_note} if hasattr(wl, "roof_note") else {})},
             "cpu_baseline": cpu,
             "clocks": clk,
         }

@@ -222,9 +222,11 @@ int launch_dense<double>(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int6
     attr = true;
   }
   dim3 grid((unsigned)((sk->ell + DBM - 1) / DBM), (unsigned)((k + DBN - 1) / DBN), (unsigned)S);
+  prof_begin(ctx);
   dense_dmma_kernel<<<grid, DNT, DSMEM, ctx->stream>>>(sk->G, sk->ldg, (const double*)X, ldx, sk->ell,
                                                         k, sk->n, ks, (double*)ws, st);
   SQB_TRY(check_launch(ctx, "dense_dmma_kernel"));
+  prof_end(ctx, 2.0 * (double)sk->ell * (double)sk->n * (double)k);  // flops (bench.py: tensor roofline)
   const int64_t MN = sk->ell * k;
   const unsigned rb = (unsigned)std::min<int64_t>((MN + 255) / 256, 4096);
   dense_reduce_kernel<<<rb, 256, 0, ctx->stream>>>((const double*)ws, sk->ell, k, S, Y, ldy, row_off, st);

@@ -338,9 +338,12 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
       break;
     }
     double* Qj = Q ? Q + (int64_t)(j - 1) * ldq : nullptr;
+    prof_begin(ctx);
     arn_q_kernel<T><<<gg, GEMV_NT, sizeof(double) * (mt + 1), ctx->stream>>>(n, mt, j, (T*)U, ldu, cq, fs,
                                                                              scaling, q, Qj, st);
     SQB_TRY(check_launch(ctx, "arn_q_kernel"));
+    // algorithmic bytes of the GEMV q = e_j - U_j coef: read U[:, :j], write q
+    prof_end(ctx, (double)sizeof(T) * (double)n * (double)(j + 1));
     // w = lo(A lo(q))  (krylov.py:140)
     SQB_TRY(matvec_t<T>(ctx, op, q, nullptr, w, t64, P, st));
     // w = (I - U_j T_j^t S_j^t Psi) w  (krylov.py:141-142)

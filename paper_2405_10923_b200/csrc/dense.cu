@@ -21,11 +21,11 @@
 
 namespace sqb {
 
-// 64-deep k tiles, double-buffered (2 x 102 KB): half the block barriers of
-// the former 32-deep 3-stage ring per flop; the next tile's cp.async traffic
-// (2.2 us at the per-SM HBM share) hides under 4.2 us of DMMA.  Config 3:
-// 6.87 -> 6.44 ms (round 1 session 4).
-constexpr int DBM = 128, DBN = 64, DBK = 64, DSTR = DBK + 4, DSTAGES = 2, DNT = 256;
+// Double-buffered 32-deep k tiles (2 x 55 KB) at 2 CTAs/SM (128 registers):
+// the two CTAs' DMMA streams cover each other's block barriers and cp.async
+// waits.  Config 3 (round 1 session 4): 3-stage 1-CTA 6.87 ms, 64-deep
+// 2-stage 1-CTA 6.43 ms, this 6.34 ms (30.4 TFLOP/s in the sketch GEMM).
+constexpr int DBM = 128, DBN = 64, DBK = 32, DSTR = DBK + 4, DSTAGES = 2, DNT = 256;
 constexpr size_t DSMEM = sizeof(double) * DSTAGES * (size_t)(DBM + DBN) * DSTR;
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -37,7 +37,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // one CTA: a 128 x 64 tile of the partial product over K-range [k0, k1)
-__global__ void __launch_bounds__(DNT, 1)
+__global__ void __launch_bounds__(DNT, 2)
 dense_dmma_kernel(const double* __restrict__ G, int64_t ldg, const double* __restrict__ X,
                   int64_t ldx, int64_t M, int64_t N, int64_t K, int64_t kslab,
                   double* __restrict__ P, const Status* st) {

@@ -35,7 +35,14 @@ import sys
 import threading
 import time
 
-import numpy as np
+if "reference" in sys.argv and os.environ.get("RANK", "0") == "0":
+    # the reference arm uses every host core; torchrun exports OMP_NUM_THREADS=1
+    # to its ranks, which must not reach the BLAS pools before numpy loads
+    for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        if "WORLD_SIZE" in os.environ and os.environ.get(_v) == "1":
+            os.environ[_v] = str(os.cpu_count() or 1)
+
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -124,6 +131,43 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
+def ref_module():
+    """The UNMODIFIED reference package (`sketchqr`) installed into
+    baseline/_ref (pip --target, git-ignored, travels to the GPU box), or None.
+    The reference arm and cpu_baseline time it when present, else the oracle
+    port (oracle/sketchqr_oracle.py; same algorithm, pinned to the reference's
+    golden vectors)."""
+    d = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(d, "sketchqr")):
+        return None
+    if d not in sys.path:
+        sys.path.insert(0, d)
+    try:
+        import sketchqr
+        from sketchqr import precision as RP
+    except Exception:
+        return None
+    if "bf16" not in RP.PRECISIONS:  # config 4: runtime bf16 tag, SURVEY A.6 (source untouched)
+        import ml_dtypes
+        RP.PRECISIONS = RP.PRECISIONS + ("bf16",)
+        RP.DTYPES["bf16"] = ml_dtypes.bfloat16
+        RP.UNIT_ROUNDOFF["bf16"] = 2.0 ** -8
+    return sketchqr
+
+
+def cpu_kind():
+    return "reference" if ref_module() is not None else "port"
+
+
+def timed_sample(fn, threads=None):
+    """Run one CPU sample, optionally with the BLAS pools limited."""
+    if threads is None:
+        return fn()
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=threads):
+        return fn()
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -152,6 +196,8 @@ class RHQRLeft(Workload):
     def __init__(self, name, N, m, ell, tag, cpu_N, data, metric, w_kind):
         self.name, self.N, self.m, self.ell, self.tag = name, N, m, ell, tag
         self.cpu_N, self.data, self.metric, self.w_kind = cpu_N, data, metric, w_kind
+        if tag == "double":  # config 4's full fp64-emulated size needs ~96 GB of host arrays
+            self.full_N = N
         self.b = 8 if tag == "double" else 2
         self.dtype = {"double": "f64", "bf16": "bf16"}[tag]
 
@@ -269,30 +315,37 @@ class RHQRLeft(Workload):
         # under the sweep (csrc/host_pipe.cu)
         dt_c = run(torch.from_numpy(np.ascontiguousarray(self.W_host)).pin_memory())
         dt_f = run(torch.from_numpy(np.asfortranarray(self.W_host).T).pin_memory().T)
-        dt = min(dt_c, dt_f)
+        dt = dt_c  # headline: the C-order arrays the reference's users pass
         return {"value": self.alg / dt / 1e9, "unit": "GB/s", "ms_per_step": dt * 1e3,
                 "h2d_bytes_per_step": self.b * N * m if self.b == 8 else 8 * N * m,
                 "d2h_bytes_per_step": 8 * (N * m + (m + ell) * m + 2 * m * m + 3 * m),
                 "ms_per_step_c_order_input": dt_c * 1e3, "ms_per_step_f_order_input": dt_f * 1e3,
-                "input_order": "F" if dt_f <= dt_c else "C",
+                "input_order": "C (headline; F-order reported beside it)",
                 "note": ("P.rhqr_left(pinned host float64 W) -> host float64 U,S,T,R,scalars "
                          "(sqb_rhqr_left_host: H2D/D2H overlapped with the sweep); wall clock, "
                          "steady state (caller holds the previous result)")}
 
-    def cpu_sample(self):
-        from oracle import sketchqr_oracle as O
+    def cpu_sample(self, N=None):
         from paper_2405_10923_b200 import workloads
-        N, m = self.cpu_N, self.m
+        N, m = N or self.cpu_N, self.m
         if self.w_kind == "illcond":
             W = workloads.illcond_w(N, m, CFG["w_seed"])
         elif self.w_kind == "gauss":
             W = workloads.gaussian_w(N, m, CFG["w_seed"])
         else:
             W = workloads.scaled_gaussian_w(N, m, CFG["w_seed"])
-        om = O.SRHT(self.ell, N - m, CFG["sketch_seed"])
-        pol = O.Policy("double", self.tag)
+        R = ref_module()
+        if R is not None:  # sketchqr.rhqr_left (rhqr.py:254-267), stock code path
+            om = R.SRHTSketch(self.ell, N - m, CFG["sketch_seed"])
+            pol = R.PrecisionPolicy(high="double", low=self.tag)
+            run = lambda: R.rhqr_left(W, om, policy=pol)  # noqa: E731
+        else:
+            from oracle import sketchqr_oracle as O
+            om = O.SRHT(self.ell, N - m, CFG["sketch_seed"])
+            pol = O.Policy("double", self.tag)
+            run = lambda: O.rhqr_left(W, om, policy=pol)  # noqa: E731
         t0 = time.perf_counter()
-        O.rhqr_left(W, om, policy=pol)
+        run()
         t = time.perf_counter() - t0
         return t, alg_bytes(N, m, self.b), (f"full rhqr_left on N={N} rows x {m} ({self.tag} storage), "
                                               f"SRHT {self.ell}")
@@ -307,6 +360,7 @@ class RecRHQR(Workload):
 
     def __init__(self, N=1 << 22, m=64, ell=256, cpu_N=1 << 19):
         self.N, self.m, self.ell, self.cpu_N = N, m, ell, cpu_N
+        self.full_N = N
 
     def setup(self, ws, rank):
         import paper_2405_10923_b200 as P
@@ -355,13 +409,25 @@ class RecRHQR(Workload):
                 "note": ("P.rec_rhqr(pinned host float64 W) -> host float64 U,S,T,R,scalars (upload, "
                          "factorization, download in series: no streamed pipeline for rec_rhqr); wall clock")}
 
-    def cpu_sample(self):
-        from oracle import sketchqr_oracle as O
+    def cpu_sample(self, N=None, precached=False):
+        """precached: G built once through the reference's own row generator
+        and placed in its `_cache` (sketching.py:110-117) before the timer, so
+        the time is the GEMM + HQR + solve without the Philox regeneration."""
         from paper_2405_10923_b200 import workloads
-        N, m = self.cpu_N, self.m
+        N, m = N or self.cpu_N, self.m
         W = workloads.gen_cmatrix(N, m)
+        R = ref_module()
+        if R is not None:  # sketchqr.rec_rhqr (rhqr.py:368-395); G regenerated per apply
+            om = R.GaussianSketch(self.ell, N - m, CFG["sketch_seed"])
+            if precached:
+                om._cache[np.dtype(np.float64)] = om._rows(0, self.ell)
+            run = lambda: R.rec_rhqr(W, om)  # noqa: E731
+        else:
+            from oracle import sketchqr_oracle as O
+            run = lambda: O.rec_rhqr(W, O.Gaussian(self.ell, N - m, CFG["sketch_seed"],  # noqa: E731
+                                                   materialize=precached))
         t0 = time.perf_counter()
-        O.rec_rhqr(W, O.Gaussian(self.ell, N - m, CFG["sketch_seed"], materialize=False))
+        run()
         t = time.perf_counter() - t0
         n = N - m
         return t, 8.0 * (self.ell * n + 2 * N * m), (f"full rec_rhqr on gen_cmatrix({N}, {m}), Gaussian "
@@ -451,19 +517,26 @@ class GMRESCycle(Workload):
                 "note": (f"P.rhqr_gmres(host scipy CSR ({nnz} nnz), pinned host b) -> host x and residual "
                          "history: the CSR upload is inside every timed call; wall clock")}
 
-    def cpu_sample(self):
+    def cpu_sample(self, N=None):
         import scipy.sparse
 
-        from oracle import sketchqr_oracle as O
         from paper_2405_10923_b200 import workloads
         k, msamp = self.k, 8
         indptr, indices, data = workloads.convection_diffusion_csr(k)
         N = k * k
         A = scipy.sparse.csr_matrix((data, indices, indptr), shape=(N, N))
         b = np.random.default_rng(11).standard_normal(N)
-        om = O.SRHT(self.ell, N - msamp - 1, CFG["sketch_seed"])
+        R = ref_module()
+        if R is not None:  # sketchqr.rhqr_arnoldi (krylov.py:82-150)
+            from sketchqr.krylov import rhqr_arnoldi
+            om = R.SRHTSketch(self.ell, N - msamp - 1, CFG["sketch_seed"])
+            run = lambda: rhqr_arnoldi(A, b, None, msamp, om, store_q=False)  # noqa: E731
+        else:
+            from oracle import sketchqr_oracle as O
+            om = O.SRHT(self.ell, N - msamp - 1, CFG["sketch_seed"])
+            run = lambda: O.rhqr_arnoldi(A, b, None, msamp, om, store_q=False)  # noqa: E731
         t0 = time.perf_counter()
-        O.rhqr_arnoldi(A, b, None, msamp, om, store_q=False)
+        run()
         t = time.perf_counter() - t0
         nnz = A.nnz
         by = float(sum(8 * N * (2 * j + 5) for j in range(1, msamp + 1)) + msamp * (12 * nnz + 12 * N))
@@ -485,9 +558,17 @@ WORKLOADS = {
 }
 
 
+def cpu_desc(kind, cores):
+    if kind == "reference":
+        return (f"the unmodified reference package sketchqr 0.1.0 (baseline/_ref, numpy/scipy; FWHT "
+                f"single-threaded numpy, BLAS {cores} threads)")
+    return f"numpy oracle port of sketchqr (FWHT single-threaded, BLAS {cores} threads)"
+
+
 def run_reference(args, wl):
-    """--impl reference: the reference's CPU algorithm (oracle port) on this
-    host's cores, rank 0 only; each step a bounded sample of the workload."""
+    """--impl reference: the reference's own CPU implementation (sketchqr from
+    baseline/_ref when installed, else the oracle port) on this host's cores,
+    rank 0 only; each step a bounded sample of the workload."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
@@ -497,17 +578,31 @@ def run_reference(args, wl):
     t = sum(r[0] for r in runs) / len(runs)
     v = runs[0][1] / t / 1e9
     cores = blas_threads()
+    kind = cpu_kind()
     line = {
         "impl": "reference", "metric": wl.metric, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype, "data": wl.data,
+        "scaling": wl.scaling, "vs_baseline": None, "dtype": wl.dtype, "data": wl.data,
         "config": {"workload": f"{wl.name} CPU sample: {runs[0][2]}"},
-        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": runs[0][2] + f"; numpy oracle port of sketchqr (FWHT single-threaded, "
-                                                f"BLAS {cores} threads)"},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": kind,
+                         "sample": runs[0][2] + "; " + cpu_desc(kind, cores)},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def relaunch_cmd(args_gpus, argv, port):
+    """`bench.py --gpus N` (N > 1) started without torchrun re-executes itself
+    as N ranks of one node (the contract's launch line)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args_gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
 
 
 def main():
@@ -519,7 +614,21 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="also time the CPU reference on the workload's full size (config 2: ~35-60 s)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-exec under torchrun (NCCL INIT log kept on so
+        # the ranks are visible in the output)
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        r = subprocess.run(relaunch_cmd(args.gpus, sys.argv[1:], free_port()), env=env)
+        sys.exit(r.returncode)
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
+    print(f"[bench] rank {os.environ.get('RANK', '0')}/{ws_env} impl={args.impl}", file=sys.stderr, flush=True)
     wl = WORKLOADS[args.workload]()
     if args.impl == "reference":
         run_reference(args, wl)
@@ -607,8 +716,18 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         t, by, desc = wl.cpu_sample()
         cores = blas_threads()
-        cpu = {"value": by / t / 1e9, "unit": "GB/s", "cores": cores, "kind": "port", "seconds": t,
-               "sample": desc + f"; numpy oracle port of sketchqr (FWHT single-threaded, BLAS {cores} threads)"}
+        kind = cpu_kind()
+        cpu = {"value": by / t / 1e9, "unit": "GB/s", "cores": cores, "kind": kind, "seconds": t,
+               "sample": desc + "; " + cpu_desc(kind, cores)}
+        t1, by1, _ = timed_sample(wl.cpu_sample, threads=1)  # also a 1-thread run
+        cpu["one_thread"] = {"value": by1 / t1 / 1e9, "seconds": t1, "cores": 1}
+        if isinstance(wl, RecRHQR):
+            tp, byp, _ = wl.cpu_sample(precached=True)
+            cpu["g_precached"] = {"value": byp / tp / 1e9, "seconds": tp,
+                                  "what": "same sample with G pre-cached in GaussianSketch._cache"}
+        if args.cpu_full and hasattr(wl, "full_N"):
+            tf, byf, descf = wl.cpu_sample(N=wl.full_N)
+            cpu["full_size"] = {"value": byf / tf / 1e9, "seconds": tf, "sample": descf}
 
     if rank == 0:
         line = {
@@ -625,6 +744,11 @@ def main():
                          "peak_source": roof["peak_source"],
                          "kernel_share_of_step": (k_ms / args.steps) / prof_step_ms if prof_step_ms else None,
                          "timing": "per-launch CUDA events on the library stream over K extra steps",
+                         "in_pipeline": ({"achieved": value, "frac": value / roof["peak"],
+                                          "what": "whole step (all kernels, PDL look-ahead intact): "
+                                                  "algorithmic bytes / ms_per_step"}
+                                         if roof["bound"] == "hbm" else None),
+                         "profiled_step_ms": prof_step_ms,
                          "launches_timed": k_n, **({"note": wl.roof_note} if hasattr(wl, "roof_note") else {})},
             "cpu_baseline": cpu,
             "clocks": clk,

@@ -160,7 +160,8 @@ class Context:
 
     def set_stream(self, stream: int):
         if stream != self.stream:
-            lib().sqb_ctx_set_stream(self.h, vp(stream))
+            # the C side orders the new stream after the old one (shared scratch)
+            self.check(lib().sqb_ctx_set_stream(self.h, vp(stream)), "sqb_ctx_set_stream")
             self.stream = stream
 
     def check(self, rc, what):
@@ -195,19 +196,30 @@ class Context:
 
 
 _ctxs = {}
+_ctx_lock = threading.Lock()
 
 
 def context():
-    """Context bound to torch's current device and stream."""
+    """Context bound to torch's current device and stream.
+
+    One context per (device, host thread): a context's scratch workspace,
+    host-operand arena and status word are not safe to share between threads.
+    Within a thread, switching torch streams orders the new stream after the
+    old one (sqb_ctx_set_stream), so calls on different streams never race on
+    the shared scratch."""
     import torch
 
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2405_10923_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
     dev = torch.cuda.current_device()
     stream = torch.cuda.current_stream(dev).cuda_stream
-    ctx = _ctxs.get(dev)
+    key = (dev, threading.get_ident())
+    ctx = _ctxs.get(key)
     if ctx is None:
-        ctx = _ctxs[dev] = Context(dev, stream)
+        with _ctx_lock:
+            ctx = _ctxs.get(key)
+            if ctx is None:
+                ctx = _ctxs[key] = Context(dev, stream)
     ctx.set_stream(stream)
     return ctx
 

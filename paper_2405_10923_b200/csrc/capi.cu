@@ -105,7 +105,20 @@ int sqb_ctx_destroy(sqb_ctx* ctx) {
 
 int sqb_ctx_set_stream(sqb_ctx* ctx, void* stream) {
   if (!ctx) return SQB_ERR_ARG;
-  ctx->stream = (cudaStream_t)stream;
+  cudaStream_t next = (cudaStream_t)stream;
+  if (next != ctx->stream) {
+    // the workspace, arena and status word are shared by every stream the
+    // context is used on: work enqueued on the new stream must not overtake
+    // what the old stream may still be doing with them
+    SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaEvent_t e;
+    SQB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaError_t r = cudaEventRecord(e, ctx->stream);
+    if (r == cudaSuccess) r = cudaStreamWaitEvent(next, e, 0);
+    cudaEventDestroy(e);
+    if (r != cudaSuccess) return set_cuda_error(ctx, r, "sqb_ctx_set_stream", __FILE__, __LINE__);
+    ctx->stream = next;
+  }
   return SQB_OK;
 }
 
@@ -162,7 +175,7 @@ int sqb_ctx_status(sqb_ctx* ctx, int* code, int* col, double* val) {
 
 int sqb_sketch_apply(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* X, int64_t ldx,
                      int64_t k, double* Y, int64_t ldy) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, dtype));
   SQB_TRY(validate_sketch(ctx, sk));
   if (k < 0 || ldx < sk->n || ldy < sk->ell) return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
@@ -174,7 +187,7 @@ int sqb_sketch_apply(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const void* 
 
 int sqb_embedded_apply(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, int dtype, const void* X,
                        int64_t ldx, int64_t k, double* Y, int64_t ldy) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, dtype));
   SQB_TRY(validate_sketch(ctx, sk));
   if (m < 0 || k < 0 || ldx < m + sk->n || ldy < m + sk->ell)
@@ -191,17 +204,9 @@ int sqb_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
                   int64_t N, int64_t m, int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds,
                   double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
                   double* betas) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
-  SQB_TRY(validate_sketch(ctx, sk));
-  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
-    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
-  if (m < 1) return set_error(ctx, SQB_ERR_ARG, "need at least one column");
-  if (m > 1024) return set_error(ctx, SQB_ERR_ARG, "m=%lld: the device sweep supports up to 1024 columns", (long long)m);
-  if (sk->n != N - m)
-    return set_error(ctx, SQB_ERR_ARG, "sketch takes %lld coordinates, expected n-m=%lld",
-                     (long long)sk->n, (long long)(N - m));
-  if (sk->ell < m) return set_error(ctx, SQB_ERR_ARG, "sampling size below column count");
+  SQB_TRY(validate_left_args(ctx, sk, scaling, N, m));
   if (ldw < N || ldu < N || lds < m + sk->ell || ldt < m || ldr < m)
     return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
   return rhqr_left_dispatch(ctx, sk, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, T, ldt, R, ldr,
@@ -212,7 +217,7 @@ int sqb_rhqr_block(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype
                    int64_t N, int64_t m, int64_t ldw, int64_t block_size, void* U, int64_t ldu, double* S,
                    int64_t lds, double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
                    double* betas) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
   SQB_TRY(validate_sketch(ctx, sk));
   if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
@@ -235,7 +240,7 @@ int sqb_trim_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
                        int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt, double* Tt, int64_t ldtt,
                        double* R, int64_t ldr, double* L, int64_t ldl, double* sigmas, double* rhos,
                        double* betas) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
   SQB_TRY(validate_sketch(ctx, sk));
   if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
@@ -264,7 +269,7 @@ int sqb_trim_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
                         double* betas) {
   // the same argument contract as sqb_trim_rhqr_left (validated there with a
   // dry run of the checks only)
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
   SQB_TRY(validate_sketch(ctx, sk));
   if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
@@ -285,7 +290,7 @@ int sqb_trim_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
 
 int sqb_colscaled_apply(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t m, int dtype,
                         const void* X, int64_t ldx, int64_t k, double* Y, int64_t ldy) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, dtype));
   SQB_TRY(validate_sketch(ctx, sk));
   if (m < 0 || m > sk->n || !scales) return set_error(ctx, SQB_ERR_ARG, "bad column-scaled operator");
@@ -296,7 +301,7 @@ int sqb_colscaled_apply(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
 int sqb_trim_thin_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t k,
                     const double* T, int64_t ldt, const double* S, int64_t lds, const double* E, int64_t lde,
                     int64_t ell, double* Q, int64_t ldq) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
   if (k < 0 || k > N || ldu < N || ldq < N || ldt < k || lds < ell || lde < ell)
     return set_error(ctx, SQB_ERR_ARG, "bad trimmed thin-Q arguments");
@@ -307,7 +312,7 @@ int sqb_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype
                    int64_t N, int64_t m, int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds,
                    double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
                    double* betas) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
   SQB_TRY(validate_sketch(ctx, sk));
   if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
@@ -328,7 +333,7 @@ int sqb_apply_reflectors(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, int lo_d
                          int64_t ldu, int64_t N, int64_t r, const double* S, int64_t lds,
                          const double* T, int64_t ldt, int transpose_t, const void* X, int64_t ldx,
                          int64_t k, void* Out, int64_t ldo) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
   SQB_TRY(validate_sketch(ctx, sk));
   if (sk->n != N - m) return set_error(ctx, SQB_ERR_ARG, "embedding is %lld x %lld, operand has %lld rows",
@@ -339,33 +344,33 @@ int sqb_apply_reflectors(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, int lo_d
 
 int sqb_thin_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t k,
                const double* T, int64_t ldt, double* Q, int64_t ldq) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
   if (k > N) return set_error(ctx, SQB_ERR_ARG, "more reflectors than rows");
   return thin_q_dispatch(ctx, lo_dtype, U, ldu, N, k, T, ldt, Q, ldq);
 }
 
 int sqb_gram(sqb_ctx* ctx, const double* A, int64_t lda, int64_t N, int64_t k, double* G, int64_t ldg) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   return gram_run(ctx, A, lda, N, k, G, ldg);
 }
 
 int sqb_residual_norms(sqb_ctx* ctx, const double* W, int64_t ldw, const double* Q, int64_t ldq,
                        const double* R, int64_t ldr, int64_t N, int64_t k, int64_t kc, double* out) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   return residual_norms_run(ctx, W, ldw, Q, ldq, R, ldr, N, k, kc, out);
 }
 
 int sqb_sketch_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t k, const double* T,
                  int64_t ldt, const double* S, int64_t lds, int64_t od, double* Q, int64_t ldq) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
   return sketch_q_run(ctx, lo_dtype, U, ldu, k, T, ldt, S, lds, od, Q, ldq);
 }
 
 int sqb_rh_vector(sqb_ctx* ctx, int scaling, int lo_dtype, const void* w, int64_t n, const double* y,
                   int64_t od, int64_t j, void* u, double* s, double* scalars) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
   if (j < 1 || j > od)
     return set_error(ctx, SQB_ERR_ARG, "elimination index %lld outside sketch of length %lld", (long long)j,
@@ -377,7 +382,7 @@ int sqb_rec_rhqr(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, 
                  int64_t N, int64_t m, int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds,
                  double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
                  double* betas) {
-  SQB_TRY(prep(ctx));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_dtype(ctx, lo_dtype));
   SQB_TRY(validate_sketch(ctx, sk));
   if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)

@@ -206,24 +206,38 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 thin_q_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int k, const double* __restrict__ M,
               double* __restrict__ Q, int64_t ldq) {
-  extern __shared__ double sM[];  // k x k
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) sM[e] = M[e];
+  // blockIdx.y selects a block of (up to) 64 output columns: shared memory
+  // holds M[:, j0:j0+64] only, so any k <= 400 fits
+  extern __shared__ double sM[];  // k x jn
+  const int j0 = blockIdx.y * 64;
+  const int jn = min(64, k - j0);
+  for (int e = threadIdx.x; e < k * jn; e += blockDim.x) sM[e] = M[(e % k) + (int64_t)(j0 + e / k) * k];
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
     double u[64];
-    for (int j0 = 0; j0 < k; j0 += 64) {
-      const int jn = min(64, k - j0);
-      for (int jj = 0; jj < jn; ++jj) u[jj] = 0.0;
-      for (int l = 0; l < k; ++l) {
-        const double ul = (double)Lo<T>::load(U[i + (int64_t)l * ldu]);
-        for (int jj = 0; jj < jn; ++jj) u[jj] = fma(ul, sM[l + (j0 + jj) * k], u[jj]);
-      }
-      for (int jj = 0; jj < jn; ++jj) {
-        const int j = j0 + jj;
-        Q[i + (int64_t)j * ldq] = (i == j ? 1.0 : 0.0) - u[jj];
-      }
+    for (int jj = 0; jj < jn; ++jj) u[jj] = 0.0;
+    for (int l = 0; l < k; ++l) {
+      const double ul = (double)Lo<T>::load(U[i + (int64_t)l * ldu]);
+      for (int jj = 0; jj < jn; ++jj) u[jj] = fma(ul, sM[l + jj * k], u[jj]);
+    }
+    for (int jj = 0; jj < jn; ++jj) {
+      const int j = j0 + jj;
+      Q[i + (int64_t)j * ldq] = (i == j ? 1.0 : 0.0) - u[jj];
     }
   }
+}
+
+template <typename T>
+static int launch_thin_q(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int64_t k, const double* M,
+                         double* Q, int64_t ldq) {
+  if (k > 400) return set_error(ctx, SQB_ERR_ARG, "thin_q: k=%lld above 400", (long long)k);
+  const size_t smem = sizeof(double) * k * std::min<int64_t>(64, k);
+  cudaFuncSetAttribute(thin_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(smem, 48 * 1024));
+  const unsigned nb = (unsigned)((k + 63) / 64);
+  thin_q_kernel<T><<<dim3((unsigned)std::min<int64_t>((N + 255) / 256, 2 * 148), nb), 256, smem, ctx->stream>>>(
+      (const T*)U, ldu, N, (int)k, M, Q, ldq);
+  return check_launch(ctx, "thin_q_kernel");
 }
 
 template <typename T>
@@ -236,12 +250,7 @@ static int thin_q_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int64_t
   tu1t_kernel<T><<<(unsigned)std::max<int64_t>(1, (k * k + 255) / 256), 256, 0, ctx->stream>>>(
       (const T*)U, ldu, (int)k, Tm, ldt, M);
   SQB_TRY(check_launch(ctx, "tu1t_kernel"));
-  const size_t smem = sizeof(double) * k * k;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(thin_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  thin_q_kernel<T><<<(unsigned)std::min<int64_t>((N + 255) / 256, 2 * 148), 256, smem, ctx->stream>>>(
-      (const T*)U, ldu, N, (int)k, M, Q, ldq);
-  return check_launch(ctx, "thin_q_kernel");
+  return launch_thin_q<T>(ctx, U, ldu, N, k, M, Q, ldq);
 }
 
 // Q = [I;0] - U M for a given k x k fp64 M (ld k) — the trimmed thin Q
@@ -249,12 +258,7 @@ static int thin_q_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int64_t
 template <typename T>
 static int thin_q_m_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int64_t k, const double* M, double* Q,
                       int64_t ldq) {
-  const size_t smem = sizeof(double) * k * k;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(thin_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  thin_q_kernel<T><<<(unsigned)std::min<int64_t>((N + 255) / 256, 2 * 148), 256, smem, ctx->stream>>>(
-      (const T*)U, ldu, N, (int)k, M, Q, ldq);
-  return check_launch(ctx, "thin_q_kernel");
+  return launch_thin_q<T>(ctx, U, ldu, N, k, M, Q, ldq);
 }
 
 int thin_q_m_dispatch(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t N, int64_t k,
@@ -387,12 +391,7 @@ static int sketch_q_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t k, const
   tu1t_kernel<T><<<(unsigned)std::max<int64_t>(1, (k * k + 255) / 256), 256, 0, ctx->stream>>>(
       (const T*)U, ldu, (int)k, Tm, ldt, M);
   SQB_TRY(check_launch(ctx, "tu1t_kernel"));
-  const size_t smem = sizeof(double) * k * k;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(thin_q_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  thin_q_kernel<double><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((od + 255) / 256, 148)), 256,
-                          smem, ctx->stream>>>(S, lds, od, (int)k, M, Q, ldq);
-  return check_launch(ctx, "thin_q_kernel");
+  return launch_thin_q<double>(ctx, S, lds, od, k, M, Q, ldq);
 }
 
 int sketch_q_run(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int64_t k, const double* Tm,
@@ -462,8 +461,7 @@ extern "C" int sqb_arnoldi_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t 
                              const double* T, int64_t ldt, const double* S, int64_t lds, int64_t c, double* Q,
                              int64_t ldq) {
   using namespace sqb;
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
+  SQB_TRY(begin_entry(ctx));
   if (c < 0 || c > r) return set_error(ctx, SQB_ERR_ARG, "have %lld reflectors, cannot build %lld columns",
                                        (long long)r, (long long)c);
   if ((int64_t)r * c * 8 > 200 * 1024) return set_error(ctx, SQB_ERR_ARG, "arnoldi_q: r*c too large");
@@ -484,9 +482,7 @@ extern "C" int sqb_compact_update(sqb_ctx* ctx, int lo_dtype, const double* Y, i
                                   int64_t lds, const double* T, int64_t ldt, int transpose_t, int64_t r,
                                   const void* U, int64_t ldu, int64_t N, const void* X, void* Out) {
   using namespace sqb;
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
-  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(begin_entry(ctx));
   if (r < 1 || N < 1) return SQB_OK;
   WsPlan plan;
   const size_t iC = plan.add(sizeof(double) * r);

@@ -131,6 +131,17 @@ inline int check_launch(sqb_ctx* ctx, const char* what) {
   return SQB_OK;
 }
 
+// Start of a computing entry point: clear the error text and the device
+// status word on ctx->stream, so a failure left by an earlier unchecked call
+// cannot turn this call's kernels into early-returning no-ops.
+inline int begin_entry(sqb_ctx* ctx) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_CUDA_TRY(cudaMemsetAsync(ctx->d_status, 0, sizeof(Status), ctx->stream));
+  return SQB_OK;
+}
+
 // host-side rounding of a double to a storage format, matching numpy:
 // float32/float16 round directly from double; ml_dtypes' bfloat16 goes
 // through float32 (two round-to-nearest-even steps).

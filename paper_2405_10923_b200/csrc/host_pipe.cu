@@ -273,6 +273,8 @@ extern "C" int sqb_rhqr_left_host(sqb_ctx* ctx, const sqb_sketch* sk, int scalin
   ctx->err[0] = 0;
   SQB_CUDA_TRY(cudaSetDevice(ctx->device));
   if (lo_dtype < SQB_F64 || lo_dtype > SQB_BF16) return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+  // the same argument checks as sqb_rhqr_left, before sk is dereferenced
+  SQB_TRY(validate_left_args(ctx, sk, scaling, N, m));
   if (!W || !U || !S || !T || !R || !sigmas || !rhos || !betas)
     return set_error(ctx, SQB_ERR_ARG, "null host buffer");
   if (N < 1 || m < 1) return set_error(ctx, SQB_ERR_ARG, "empty matrix");

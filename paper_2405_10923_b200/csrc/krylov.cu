@@ -663,9 +663,7 @@ extern "C" int sqb_rhqr_arnoldi(sqb_ctx* ctx, const sqb_sketch* sk, const sqb_op
                                 int lo_dtype, double happy_tol, const double* b, const void* x0lo, void* U,
                                 int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt, double* H,
                                 int64_t ldh, double* Q, int64_t ldq, double* beta, int* attained) {
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
-  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(validate_sketch(ctx, sk));
   if (!A || A->n < 1) return set_error(ctx, SQB_ERR_ARG, "missing operator");
   if (m < 1) return set_error(ctx, SQB_ERR_ARG, "need m >= 1");
@@ -709,9 +707,7 @@ extern "C" int sqb_rhqr_arnoldi(sqb_ctx* ctx, const sqb_sketch* sk, const sqb_op
 
 extern "C" int sqb_hessenberg_lstsq(sqb_ctx* ctx, const double* H, int64_t ldh, int64_t p, int64_t k, double beta,
                                     double* y, double* hist, double* resid, double* work) {
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
-  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(begin_entry(ctx));
   if (p < k || k < 0) return set_error(ctx, SQB_ERR_ARG, "Hessenberg must be (k+1) x k");
   double* R = work;
   double* g = work + p * std::max<int64_t>(k, 1);
@@ -721,6 +717,7 @@ extern "C" int sqb_hessenberg_lstsq(sqb_ctx* ctx, const double* H, int64_t ldh, 
 
 extern "C" int sqb_csr_spmv(sqb_ctx* ctx, int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
                             const double* data, const void* x, const double* bsub, void* y) {
+  // no status clear: a matvec may run inside a caller's Arnoldi callback
   if (!ctx) return SQB_ERR_ARG;
   ctx->err[0] = 0;
   SQB_CUDA_TRY(cudaSetDevice(ctx->device));
@@ -747,9 +744,7 @@ extern "C" int sqb_rhqr_arnoldi_dist(sqb_ctx* ctx, const sqb_sketch* sk, int m, 
                                      const double* b, const void* x0lo, void* U, int64_t ldu, double* S,
                                      int64_t lds, double* T, int64_t ldt, double* H, int64_t ldh, double* Q,
                                      int64_t ldq, double* beta, void* Utop, int* attained) {
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
-  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(begin_entry(ctx));
   std::vector<ArnRank> rk(1);
   ArnRank& d = rk[0];
   d = ArnRank{};
@@ -802,9 +797,7 @@ extern "C" int sqb_rhqr_arnoldi_virtual(sqb_ctx* ctx, const sqb_sketch* sk, int 
                                         double* const* S, int64_t lds, double* const* T, int64_t ldt,
                                         double* const* H, int64_t ldh, double* const* beta,
                                         void* const* Utop, int* attained) {
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
-  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(begin_entry(ctx));
   const int mt = m + 1;
   std::vector<ArnRank> rk(nranks);
   std::vector<int> ids(nranks);

@@ -596,9 +596,7 @@ upper_tri_solve_kernel(const double* __restrict__ R, int64_t ldr, int m, const d
 extern "C" int sqb_upper_tri_solve(sqb_ctx* ctx, const double* R, int64_t ldr, int64_t m, const double* B,
                                    int64_t ldb, int64_t k, double* X, int64_t ldx) {
   using namespace sqb;
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
-  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(begin_entry(ctx));
   if (m < 1 || k < 1) return SQB_OK;
   upper_tri_solve_kernel<<<(unsigned)k, 256, sizeof(double) * m, ctx->stream>>>(R, ldr, (int)m, B, ldb, X, ldx,
                                                                                ctx->d_status);
@@ -609,9 +607,7 @@ extern "C" int sqb_householder_qr(sqb_ctx* ctx, int scaling, const double* A, in
                                   double* U, int64_t ldu, double* T, int64_t ldt, double* R, int64_t ldr,
                                   double* sigmas, double* rhos, double* betas) {
   using namespace sqb;
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
-  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(begin_entry(ctx));
   if (p < m) return set_error(ctx, SQB_ERR_ARG, "need p >= m, got %lld x %lld", (long long)p, (long long)m);
   if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
     return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);

@@ -379,9 +379,7 @@ __global__ void tinv_kernel(const double* __restrict__ S, int64_t lds, int od, i
 extern "C" int sqb_t_factor(sqb_ctx* ctx, const double* S, int64_t lds, int64_t od, int64_t k, double* T,
                             int64_t ldt) {
   using namespace sqb;
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
-  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(begin_entry(ctx));
   if (k < 1) return SQB_OK;
   if (lds < od || ldt < k) return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
   WsPlan plan;

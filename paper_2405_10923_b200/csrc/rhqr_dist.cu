@@ -350,9 +350,7 @@ static int left_dist_entry(bool rec, sqb_ctx* ctx, const sqb_sketch* sk, int sca
                        int64_t n_local, int64_t m, int64_t ldw, void* U, int64_t ldu, double* S, int64_t lds,
                        double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos,
                        double* betas, void* Utop_scratch) {
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
-  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_common(ctx, sk, scaling, m, ctx->nranks));
   const int64_t span = sk->n_pad / ctx->nranks;
   const int64_t e_base = span * ctx->rank;
@@ -376,9 +374,7 @@ static int left_virtual_entry(bool rec, sqb_ctx* ctx, const sqb_sketch* sk, int 
                           const void* const* W_parts, const int64_t* ldw, void* const* U_parts,
                           const int64_t* ldu, int64_t m, double* S, int64_t lds, double* T, int64_t ldt,
                           double* R, int64_t ldr, double* sigmas, double* rhos, double* betas, double* scratch) {
-  if (!ctx) return SQB_ERR_ARG;
-  ctx->err[0] = 0;
-  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_TRY(begin_entry(ctx));
   SQB_TRY(check_common(ctx, sk, scaling, m, nranks));
   const int64_t span = sk->n_pad / nranks;
   const int64_t od = m + sk->ell;

@@ -17,11 +17,19 @@ static int zero2d(sqb_ctx* ctx, double* p, int64_t rows, int64_t cols, int64_t l
   return check_launch(ctx, "zero_kernel");
 }
 
+// persistent single-kernel sweep for small fp64 problems (rhqr_persist.cu)
+size_t persist_ws_bytes(const sqb_sketch* sk, int64_t m);
+bool persist_eligible(sqb_ctx* ctx, const sqb_sketch* sk, int64_t N, int64_t m, int64_t ncol, int64_t off);
+int launch_persist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const double* W, int64_t N, int64_t m,
+                   int64_t ldw, double* U, int64_t ldu, double* S, int64_t lds, double* Tm, int64_t ldt, double* R,
+                   int64_t ldr, double* sigmas, double* rhos, double* betas, const double* Y0, double* abuf,
+                   double* vbuf, void* pws, double scale_lo, double norm_lo);
+
 // workspace of one sweep
 struct SweepWs {
   WsPlan plan;
   int64_t chunk;
-  size_t iY0, iy, icoef, iabuf, ivbuf, ifs, iP;
+  size_t iY0, iy, icoef, iabuf, ivbuf, ifs, iP, iPS;
 };
 static SweepWs sweep_ws(const sqb_sketch* sk, int code, int64_t m, int64_t ncol) {
   SweepWs w;
@@ -35,6 +43,7 @@ static SweepWs sweep_ws(const sqb_sketch* sk, int code, int64_t m, int64_t ncol)
   w.ivbuf = w.plan.add(sizeof(double) * (m + 1));
   w.ifs = w.plan.add(sizeof(double) * 2);
   w.iP = w.plan.add(std::max(sketch_partials_bytes(sk, code, w.chunk), sketch_partials_bytes(sk, code, 1)));
+  w.iPS = w.plan.add(code == SQB_F64 ? persist_ws_bytes(sk, m) : 0);
   return w;
 }
 size_t left_sweep_ws_bytes(const sqb_sketch* sk, int code, int64_t m, int64_t ncol) {
@@ -98,9 +107,27 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
     y0_done = end;
     return SQB_OK;
   };
-  SQB_TRY(ensure_y0(2));
   double scale_lo = 0.0, norm_lo = 0.0;
   if (srht) srht_constants(sk, Lo<T>::code, &scale_lo, &norm_lo);
+  if constexpr (std::is_same<T, double>::value) {
+    // small fp64 problems (config 1): one cooperative kernel runs every column
+    constexpr int VN2 = VecN<T>::n;
+    const bool vec2 = ((reinterpret_cast<uintptr_t>((const char*)W + m * esz) & 15) == 0) &&
+                      ((reinterpret_cast<uintptr_t>((const char*)U + m * esz) & 15) == 0) && (ldw % VN2 == 0) &&
+                      (ldu % VN2 == 0);
+    if (vec2 && persist_eligible(ctx, sk, N, m, ncol, off)) {
+      SQB_TRY(ensure_y0(ncol));
+      prof_begin(ctx);
+      SQB_TRY(launch_persist(ctx, sk, scaling, (const double*)W, N, m, ldw, (double*)U, ldu, S, lds, Tm, ldt, R,
+                             ldr, sigmas, rhos, betas, Y0, abuf, vbuf, wb + plan.offs[sw.iPS], scale_lo, norm_lo));
+      // algorithmic bytes of the column passes it replaces: sum_c 8 N (c + 2)
+      prof_end(ctx, 8.0 * (double)N * (double)((ncol - 1) * ncol / 2 + 2 * (ncol - 1)));
+      if (hk)
+        for (int64_t c = 0; c < ncol; ++c) SQB_TRY(hk->col_final(ctx, c));
+      return SQB_OK;
+    }
+  }
+  SQB_TRY(ensure_y0(2));
 
   const size_t step_smem = step_smem_bytes((int)od, (int)m);
   cudaFuncSetAttribute(rhqr_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,

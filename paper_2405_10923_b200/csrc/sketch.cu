@@ -109,6 +109,19 @@ int validate_sketch(sqb_ctx* ctx, const sqb_sketch* sk) {
   return SQB_OK;
 }
 
+int validate_left_args(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t N, int64_t m) {
+  SQB_TRY(validate_sketch(ctx, sk));
+  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
+    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
+  if (m < 1) return set_error(ctx, SQB_ERR_ARG, "need at least one column");
+  if (m > 1024) return set_error(ctx, SQB_ERR_ARG, "m=%lld: the device sweep supports up to 1024 columns", (long long)m);
+  if (sk->n != N - m)
+    return set_error(ctx, SQB_ERR_ARG, "sketch takes %lld coordinates, expected n-m=%lld",
+                     (long long)sk->n, (long long)(N - m));
+  if (sk->ell < m) return set_error(ctx, SQB_ERR_ARG, "sampling size below column count");
+  return SQB_OK;
+}
+
 // ---------------------------------------------------------------------------
 // SRHT kernels
 // ---------------------------------------------------------------------------

@@ -34,6 +34,11 @@ size_t acc_bytes(int dtype);   // sizeof(Lo<T>::acc)
 size_t elem_bytes(int dtype);  // sizeof(T)
 
 int validate_sketch(sqb_ctx* ctx, const sqb_sketch* sk);
+// Arguments shared by every left-looking sweep entry (sqb_rhqr_left,
+// sqb_rhqr_left_host, sqb_rhqr_block): the sketch itself, the scaling, the
+// column count (1..1024) and Omega taking exactly the N-m trailing rows with
+// ell >= m (rhqr.py:202-216 `_embed`).
+int validate_left_args(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t N, int64_t m);
 
 // Y[y_row_off + i + col*ldy] = (Omega X)[i, col], i < ell, col < k.
 // `partials` must hold sketch_partials_bytes(sk, dtype, k) bytes (SRHT only).

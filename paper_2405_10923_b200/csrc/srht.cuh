@@ -295,7 +295,16 @@ __device__ __forceinline__ void p16_passes(uint16_t* sm) {
 // binary-counter stack with static register indices — every level in order,
 // lower tile range as the left operand.  Supports up to 256 chunks
 // (n_tiles <= 65536).  `stride`: distance between consecutive tiles' leaves.
-template <typename T>
+// Global leaves are read with L1-bypassing loads: they are produced by other
+// CTAs (a previous kernel, or the same persistent grid before a grid
+// barrier); SMEM = true reads a shared-memory copy.
+template <typename A, bool SMEM>
+__device__ __forceinline__ A tree_leaf(const A* p) {
+  if constexpr (SMEM) return *p;
+  else return __ldcg(p);
+}
+
+template <typename T, bool SMEM = false>
 __device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<T>::acc* leaves,
                                                               int n_tiles, int n_eff, int64_t rhi,
                                                               int64_t stride = 1) {
@@ -315,7 +324,7 @@ __device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<
   A nx[8];
   const int tl = lane * R;
 #pragma unroll
-  for (int jj = 0; jj < 8; ++jj) nx[jj] = (lane < lanes && jj < R && tl + jj < n_eff) ? leaves[(tl + jj) * stride] : A(0);
+  for (int jj = 0; jj < 8; ++jj) nx[jj] = (lane < lanes && jj < R && tl + jj < n_eff) ? tree_leaf<A, SMEM>(leaves + (tl + jj) * stride) : A(0);
   for (int q = 0; q < nq; ++q) {
     A v[8];
 #pragma unroll
@@ -323,7 +332,7 @@ __device__ __forceinline__ typename Lo<T>::acc warp_tile_tree(const typename Lo<
     if (q + 1 < nq) {
       const int tb = (q + 1) * csz + tl;
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) nx[jj] = (lane < lanes && jj < R && tb + jj < n_eff) ? leaves[(tb + jj) * stride] : A(0);
+      for (int jj = 0; jj < 8; ++jj) nx[jj] = (lane < lanes && jj < R && tb + jj < n_eff) ? tree_leaf<A, SMEM>(leaves + (tb + jj) * stride) : A(0);
     }
     // levels 0 .. lr-1 inside the lane
 #pragma unroll

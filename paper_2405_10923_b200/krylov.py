@@ -4,9 +4,12 @@ The whole Arnoldi run (krylov.py:82-150) is one library call
 (`sqb_rhqr_arnoldi`): the per-step kernels are enqueued back to back and a
 closed Krylov space is detected on the device, so the host synchronises once.
 Operators (krylov.py:28-35): scipy sparse matrices and `CSRMatrix` run the
-library's CSR SpMV; dense arrays the DMMA GEMV; a Python callable is called
-with a CUDA float64 tensor and must return A @ x (it runs on the library's
-stream through a C callback).
+library's CSR SpMV; dense arrays the DMMA GEMV; a Python callable (a numpy
+closure, a scipy LinearOperator, ...) is called through a C callback on the
+library's stream.  As in the reference (krylov.py:28-35) it receives the
+vector in the caller's form: a float64 numpy vector when the caller passed
+host operands, a CUDA float64 tensor when it passed device tensors; it may
+return either.  An exception raised by the callable propagates unchanged.
 """
 
 from __future__ import annotations
@@ -60,8 +63,9 @@ class CSRMatrix:
 class _Operator:
     """Device form of A for sqb_rhqr_arnoldi (keeps buffers alive)."""
 
-    def __init__(self, A, n, tag):
+    def __init__(self, A, n, tag, host=False):
         self.keep = []
+        self.exc = None  # exception raised by a Python matvec, re-raised after the library call
         self.desc = _lib.OperatorDesc(n=n)
         if isinstance(A, CSRMatrix) or scipy.sparse.issparse(A):
             M = A if isinstance(A, CSRMatrix) else CSRMatrix.from_scipy(A)
@@ -76,11 +80,15 @@ class _Operator:
             def _cb(user, stream):
                 try:
                     x = xbuf[:, 0].to(torch.float64)
-                    y = A(x)
-                    y = y if isinstance(y, torch.Tensor) else torch.from_numpy(np.asarray(y, dtype=np.float64))
+                    y = A(x.cpu().numpy() if host else x)
+                    y = y if isinstance(y, torch.Tensor) else torch.from_numpy(
+                        np.ascontiguousarray(np.asarray(y, dtype=np.float64)))
+                    if y.numel() != n:
+                        raise ValueError(f"matvec returned {y.numel()} values, expected {n}")
                     ybuf.copy_(y.reshape(-1).to(device=ybuf.device, dtype=torch.float64))
                     return 0
-                except Exception:  # pragma: no cover - surfaced as SQB_ERR_ARG
+                except BaseException as e:  # kept and re-raised by the caller
+                    self.exc = e
                     return 1
 
             cb = _lib.MATVEC_CB(_cb)
@@ -139,13 +147,15 @@ def arnoldi_q(bundle, cols=None):
     return _out(Q, host)
 
 
-def rhqr_arnoldi(A, b, x0, m, omega, scaling=SCALE_SQRT2, policy=None, store_q=True, happy_tol=None):
+def rhqr_arnoldi(A, b, x0, m, omega, scaling=SCALE_SQRT2, policy=None, store_q=True, happy_tol=None,
+                 _host=None):
     """krylov.py:82-150: Krylov basis of (A, b - A x0) through randomized
     Householder QR; omega sketches the trailing n-m-1 coordinates."""
     check_scaling(scaling)
     policy = policy or DOUBLE_POLICY
     require_device_policy(policy)
-    host = not is_device(b)
+    host = not is_device(b)                     # form of the returned bundle
+    op_host = host if _host is None else _host  # form a Python matvec receives
     tag = policy.low
     bd = to_device(b, "double")[:, 0]
     n = bd.shape[0]
@@ -162,10 +172,10 @@ def rhqr_arnoldi(A, b, x0, m, omega, scaling=SCALE_SQRT2, policy=None, store_q=T
     H = empty_colmajor(mt, m, "double")
     Q = empty_colmajor(n, m, "double") if store_q else None
     beta = torch.zeros(1, dtype=torch.float64, device="cuda")
-    op = _Operator(A, n, tag)
+    op = _Operator(A, n, tag, host=op_host)
     attained = C.c_int(-1)
     ctx = _lib.context()
-    ctx.check(_lib.lib().sqb_rhqr_arnoldi(
+    _check_op(ctx, op, _lib.lib().sqb_rhqr_arnoldi(
         ctx.h, psi.omega.desc(), C.byref(op.desc), m, scaling_code(scaling), CODES[tag], float(happy_tol),
         bd.data_ptr(), x0d.data_ptr(), U.data_ptr(), ld_of(U), S.data_ptr(), ld_of(S), T.data_ptr(), ld_of(T),
         H.data_ptr(), ld_of(H), Q.data_ptr() if store_q else None, ld_of(Q) if store_q else 1,
@@ -197,14 +207,15 @@ def hessenberg_lstsq(H, beta, history=False):
     return out + (_out(hist, host),) if history else out
 
 
-def rhqr_gmres(A, b, x0, m, omega, scaling=SCALE_SQRT2, policy=None, happy_tol=None):
+def rhqr_gmres(A, b, x0, m, omega, scaling=SCALE_SQRT2, policy=None, happy_tol=None, _host=None):
     """krylov.py:193-222: GMRES in the sketched norm; returns (x, resid_history)."""
     policy = policy or DOUBLE_POLICY
-    host = not is_device(b)
+    host = (not is_device(b)) if _host is None else _host
     bd = to_device(b, "double")[:, 0]
     n = bd.shape[0]
     x0d = torch.zeros(n, dtype=torch.float64, device="cuda") if x0 is None else to_device(x0, "double")[:, 0]
-    bun = rhqr_arnoldi(A, bd, x0d, m, omega, scaling=scaling, policy=policy, store_q=False, happy_tol=happy_tol)
+    bun = rhqr_arnoldi(A, bd, x0d, m, omega, scaling=scaling, policy=policy, store_q=False, happy_tol=happy_tol,
+                       _host=host)
     k = bun.dim
     y, _, hist = hessenberg_lstsq(bun.H, bun.beta, history=True)
     if k and bool((torch.diagonal(bun.H)[:k] == 0.0).any()):
@@ -233,18 +244,28 @@ def rhqr_gmres_restarted(A, b, x0, m, omega, tol=1e-8, max_cycles=1000, scaling=
     bnorm = float(torch.linalg.norm(bd))
     hists = []
     for cyc in range(max_cycles):
-        x, h = rhqr_gmres(Aop, bd, x, m, omega, scaling=scaling, policy=policy)
+        x, h = rhqr_gmres(Aop, bd, x, m, omega, scaling=scaling, policy=policy, _host=host)
+        x = to_device(x, "double")[:, 0] if host else x
+        h = to_device(h, "double")[:, 0] if host else h
         hists.append(h)
-        r = bd - (Aop.matvec(x) if isinstance(Aop, CSRMatrix) else _dense_matvec(Aop, x))
+        r = bd - (Aop.matvec(x) if isinstance(Aop, CSRMatrix) else _dense_matvec(Aop, x, host))
         if float(torch.linalg.norm(r)) <= tol * bnorm:
             break
     return (to_numpy(x), [to_numpy(h) for h in hists]) if host else (x, hists)
 
 
-def _dense_matvec(A, x):
+def _check_op(ctx, op, rc, what):
+    """A failed Python matvec surfaces as its own exception, not as a status code."""
+    if op.exc is not None:
+        exc, op.exc = op.exc, None
+        raise exc
+    ctx.check(rc, what)
+
+
+def _dense_matvec(A, x, host=False):
     if callable(A) and not isinstance(A, (np.ndarray, torch.Tensor)):
-        y = A(x)
-        return y if isinstance(y, torch.Tensor) else torch.from_numpy(np.asarray(y)).cuda()
+        y = A(x.cpu().numpy() if host else x)
+        return y if isinstance(y, torch.Tensor) else torch.from_numpy(np.asarray(y, dtype=np.float64)).cuda()
     Ad = A if is_device(A) else torch.from_numpy(np.asarray(A, dtype=np.float64)).cuda()
     return Ad @ x
 

@@ -5,7 +5,8 @@ Diagnostics run on the device: the Gram matrix A^t A by the library's
 k x k Gram, device-side), the residual W - QR by the library's fused
 `sqb_residual_norms` kernel.  cond(Q) through the Gram is accurate for the
 well-conditioned Q this package produces (squaring a cond-5 matrix loses
-nothing); `cond_number(..., exact=True)` runs a device SVD instead.
+nothing); an ill-conditioned input switches to a device QR + SVD of R, so
+the value matches the reference's SVD (linalg.py:151-160) at any cond.
 """
 
 from __future__ import annotations
@@ -67,18 +68,37 @@ def gram(A) -> torch.Tensor:
     return G
 
 
+# Gram eigenvalues resolve sigma_min to ~u * cond^2 relative; above this
+# lambda_min / lambda_max ratio (cond < 1e4) that is <= 1e-8 and the fast
+# path is kept, below it (or lambda_min <= 0) the QR + SVD path runs.
+_GRAM_RATIO_MIN = 1e-8
+
+
 def cond_number(M, exact: bool = False):
-    """linalg.py:151-160: 2-norm condition number; +inf if sigma_min == 0."""
+    """linalg.py:151-160: 2-norm condition number; +inf if sigma_min == 0.
+
+    The reference takes float64 SVD values.  Here a well-conditioned M (the
+    factors' Q, cond ~ 1-10) is measured through its Gram matrix (library
+    `sqb_gram` + a k x k eigvalsh), where squaring loses nothing; whenever the
+    Gram ratio shows cond >~ 1e4 (lambda_min <= 0 included) the value is the
+    float64 SVD of the R factor of a device Householder QR of M — the same
+    numbers as the reference's SVD (LAPACK's gesdd also reduces a tall matrix
+    by QR first), e.g. 1e15 on config 2's W where the Gram route underflows.
+    `exact=True` skips the Gram probe."""
     Ad = _dev64(M)
+    if Ad.numel() == 0:
+        return np.inf
     if not bool(torch.isfinite(Ad).all()):
         return np.inf
-    if exact:
-        sv = torch.linalg.svdvals(Ad)
-        smax, smin = float(sv[0]), float(sv[-1])
-    else:
+    if not exact:
         ev = torch.linalg.eigvalsh(gram(Ad))
-        smin = float(torch.sqrt(torch.clamp(ev[0], min=0.0)))
-        smax = float(torch.sqrt(ev[-1]))
+        lmin, lmax = float(ev[0]), float(ev[-1])
+        if lmax > 0.0 and lmin > _GRAM_RATIO_MIN * lmax:
+            return float(np.sqrt(lmax) / np.sqrt(lmin))
+    N, k = Ad.shape
+    B = torch.linalg.qr(Ad, mode="r")[1] if N > k else Ad
+    sv = torch.linalg.svdvals(B)
+    smax, smin = float(sv[0]), float(sv[-1])
     if smin == 0.0:
         return np.inf
     return smax / smin

@@ -329,11 +329,247 @@ def trim_cases():
     save("experiments_trim", W=Wx, **out)
 
 
+# ---------------------------------------------------------------------------
+# BASELINE configs at their own shapes (round 2).  Inputs are regenerated on
+# the GPU box by paper_2405_10923_b200.workloads (the same numpy recipes, same
+# seeds as bench.py) and pinned here by sha256; only small outputs are stored.
+# Each section takes tens of seconds to minutes of CPU; run them in parallel:
+#   for s in cfg2 cfg3 cfg4 cfg5 cfg5r; do python make_golden.py $s & done
+# ---------------------------------------------------------------------------
+W_SEED, SK_SEED = 7, 8          # bench.py CFG
+ROW_SAMPLE_SEED = 99
+
+
+def _row_sample(N, k=256):
+    return np.sort(np.random.default_rng(ROW_SAMPLE_SEED).choice(N, size=k, replace=False))
+
+
+def _workloads():
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from paper_2405_10923_b200 import workloads
+    return workloads
+
+
+def _factor_summary(W, F, rows):
+    """Small outputs of a full-size factorization: the sketch-space factors,
+    scalars, U checksums and sampled rows, sketch_q (Psi Q), sampled rows of Q
+    and the reference diagnostics (linalg.py:151-197)."""
+    Q = thin_q(F)
+    fro, mx, _ = factorization_errors(W, Q, F.R)
+    PQ = F.psi.apply(Q)
+    return dict(R=F.R, S=F.S, T=F.T, sigmas=F.sigmas, rhos=F.rhos, betas=F.betas,
+                U_colnorm=np.linalg.norm(F.U, axis=0), U_head=F.U[:F.U.shape[1] + 64], rows=rows,
+                U_rows=F.U[rows], Q_rows=Q[rows], SQ=sketch_q(F), PsiQ=PQ,
+                cond_q=cond_number(Q), orth=orthogonality_error(PQ),
+                orth_sq=orthogonality_error(sketch_q(F)), fro=fro, maxcol=mx)
+
+
+def cfg2_case():
+    """Config 2 at full size: rhqr_left of the 2^20 x 128 ill-conditioned W
+    (sigma = logspace(0,-15)), SRHT ell = 256 (rhqr.py:254-267), plus the
+    reference cond_number of W itself (the drop-in check for linalg.py:151)."""
+    wl = _workloads()
+    N, m, ell = 1 << 20, 128, 256
+    W = wl.illcond_w(N, m, W_SEED)
+    F = rhqr_left(W, SRHTSketch(ell, N - m, SK_SEED))
+    rows = _row_sample(N)
+    out = _factor_summary(W, F, rows)
+    # W comes out of LAPACK QRs, whose last bits depend on the host CPU's
+    # BLAS kernels: sampled rows + column norms pin it to rounding level
+    out.update(W_rows=W[rows], W_colnorm=np.linalg.norm(W, axis=0))
+    save("cfg2_rhqr_left_full", W_sha=np.array(sha(W)), N=N, m=m, ell=ell, w_seed=W_SEED,
+         sk_seed=SK_SEED, cond_w=cond_number(W), **out)
+
+
+def cfg2_spread_case():
+    """How much of config 2's output is defined at all: the REFERENCE re-run
+    on W perturbed by one unit roundoff per entry (W * (1 + u r), r uniform
+    in [-1, 1], two seeds).  The spread of cond(Q), R and Psi Q over these
+    runs is the parity bar's floor for any implementation."""
+    wl = _workloads()
+    N, m, ell = 1 << 20, 128, 256
+    W = wl.illcond_w(N, m, W_SEED)
+    out = {}
+    for i, ps in enumerate((101, 102)):
+        r = np.random.default_rng(ps).uniform(-1.0, 1.0, W.shape)
+        Wp = W * (1.0 + 2.0 ** -53 * r)
+        F = rhqr_left(Wp, SRHTSketch(ell, N - m, SK_SEED))
+        Q = thin_q(F)
+        out[f"cond_q_{i}"] = cond_number(Q)
+        out[f"R_{i}"] = F.R
+        out[f"SQ_{i}"] = sketch_q(F)
+        out[f"sigmas_{i}"] = F.sigmas
+    save("cfg2_perturbation_spread", **out)
+
+
+def cfg3_case():
+    """Config 3 at full size: rec_rhqr of gen_cmatrix(2^22, 64) with the
+    Gaussian ell = 256 sketch regenerated per apply (rhqr.py:368-395,
+    sketching.py:100-125)."""
+    N, m, ell = 1 << 22, 64, 256
+    W = gen_cmatrix(N, m)
+    F = rec_rhqr(W, GaussianSketch(ell, N - m, SK_SEED))
+    out = _factor_summary(W, F, _row_sample(N))
+    save("cfg3_rec_rhqr_full", W_sha=np.array(sha(W)), N=N, m=m, ell=ell, sk_seed=SK_SEED, **out)
+
+
+def cfg3_spread_case():
+    """Config 3's own sensitivity: the REFERENCE rec_rhqr re-run on W
+    perturbed by one unit roundoff per entry (two seeds), as for config 2."""
+    N, m, ell = 1 << 22, 64, 256
+    W = gen_cmatrix(N, m)
+    rows = _row_sample(N)
+    out = {}
+    for i, ps in enumerate((101, 102)):
+        r = np.random.default_rng(ps).uniform(-1.0, 1.0, W.shape)
+        Wp = W * (1.0 + 2.0 ** -53 * r)
+        del r
+        F = rec_rhqr(Wp, GaussianSketch(ell, N - m, SK_SEED))
+        out[f"R_{i}"], out[f"S_{i}"], out[f"T_{i}"] = F.R, F.S, F.T
+        out[f"SQ_{i}"] = sketch_q(F)
+        out[f"U_rows_{i}"] = F.U[rows]
+        out[f"cond_q_{i}"] = cond_number(thin_q(F))
+    save("cfg3_perturbation_spread", **out)
+
+
+class _SplitKGaussian:
+    """The reference's own Gaussian operator (identical G rows, from
+    GaussianSketch._rows) applied with another summation order along n: the
+    product is formed as the sum of `parts` K-slabs, each a BLAS dgemm.
+    Passing it to the unmodified rec_rhqr measures how much of config 3's
+    output is defined by the sketch GEMM's rounding (its apply() is the only
+    thing that differs)."""
+
+    kind = "gauss"
+
+    def __init__(self, ell, n, seed, parts):
+        self.ell, self.n, self.seed, self.parts = ell, n, seed, parts
+        self._g = GaussianSketch(ell, n, seed)
+
+    @property
+    def shape(self):
+        return (self.ell, self.n)
+
+    def apply(self, X, dtype=np.float64):
+        X = np.asarray(X, dtype=np.float64)
+        one = X.ndim == 1
+        X2 = X.reshape(-1, 1) if one else X
+        step = max(1, (1 << 23) // self.n)
+        Y = np.zeros((self.ell, X2.shape[1]))
+        cuts = np.linspace(0, self.n, self.parts + 1).astype(np.int64)
+        for i0 in range(0, self.ell, step):
+            i1 = min(i0 + step, self.ell)
+            G = self._g._rows(i0, i1)
+            acc = np.zeros((i1 - i0, X2.shape[1]))
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                acc += G[:, a:b] @ X2[a:b]
+            Y[i0:i1] = acc
+        return Y[:, 0] if one else Y
+
+
+def cfg3_sum_order_spread_case():
+    """Config 3 with the sketch GEMM summed in 2 and in 16 K-slabs (same G,
+    same reference rec_rhqr): the reference's own sensitivity to the GEMM's
+    summation order, the bar for any other valid order (the DMMA split-K)."""
+    N, m, ell = 1 << 22, 64, 256
+    W = gen_cmatrix(N, m)
+    rows = _row_sample(N)
+    out = {}
+    for i, parts in enumerate((2, 16)):
+        F = rec_rhqr(W, _SplitKGaussian(ell, N - m, SK_SEED, parts))
+        out[f"parts_{i}"] = parts
+        out[f"R_{i}"], out[f"S_{i}"], out[f"T_{i}"] = F.R, F.S, F.T
+        out[f"SQ_{i}"] = sketch_q(F)
+        out[f"U_rows_{i}"] = F.U[rows]
+    save("cfg3_sum_order_spread", **out)
+
+
+def cfg4_case():
+    """Config 4 shape at reduced rows: bf16 storage / fp64 sketch space
+    (bf16 tag injected at runtime), 2^18 x 256 with column scales
+    logspace(0,-8), SRHT ell = 512 (precision.py:104-109)."""
+    import ml_dtypes
+    if "bf16" not in P.PRECISIONS:
+        P.PRECISIONS = P.PRECISIONS + ("bf16",)
+        P.DTYPES["bf16"] = ml_dtypes.bfloat16
+        P.UNIT_ROUNDOFF["bf16"] = 2.0 ** -8
+    wl = _workloads()
+    N, m, ell = 1 << 18, 256, 512
+    W = wl.scaled_gaussian_w(N, m, W_SEED)
+    pol = P.PrecisionPolicy(high="double", low="bf16")
+    F = rhqr_left(W, SRHTSketch(ell, N - m, SK_SEED), policy=pol)
+    Wb = P.round_to(W, "bf16")  # the storage-rounded W the factors describe
+    out = _factor_summary(Wb, F, _row_sample(N))
+    # size: the leading 64 columns of Psi Q are what the parity bar reads
+    out["SQ"], out["PsiQ"] = out["SQ"][:, :64].copy(), out["PsiQ"][:, :64].copy()
+    out.pop("U_head")
+    save("cfg4_rhqr_left_bf16_2p18", W_sha=np.array(sha(W)), N=N, m=m, ell=ell, w_seed=W_SEED,
+         sk_seed=SK_SEED, **out)
+
+
+def _cfg5_problem():
+    import scipy.sparse
+    wl = _workloads()
+    k = 2048
+    ip, ix, dv = wl.convection_diffusion_csr(k)
+    N = k * k
+    A = scipy.sparse.csr_matrix((dv, ix, ip), shape=(N, N))
+    b = np.random.default_rng(11).standard_normal(N)
+    return A, b, N, sha(ip) + sha(ix) + sha(dv)
+
+
+def cfg5_case():
+    """Config 5 at full size: one RHQR-GMRES(200) cycle on the 2048^2
+    convection-diffusion CSR, SRHT ell = 400 over N - 201 coordinates
+    (krylov.py:82-222).  The Arnoldi bundle is captured by wrapping
+    krylov.rhqr_arnoldi at runtime (the reference source is not edited)."""
+    from sketchqr import krylov as K
+    A, b, N, csr_sha = _cfg5_problem()
+    m, ell = 200, 400
+    cap = {}
+    orig = K.rhqr_arnoldi
+
+    def spy(*a, **kw):
+        cap["b"] = orig(*a, **kw)
+        return cap["b"]
+    K.rhqr_arnoldi = spy
+    try:
+        x, hist = K.rhqr_gmres(A, b, None, m, SRHTSketch(ell, N - m - 1, SK_SEED))
+    finally:
+        K.rhqr_arnoldi = orig
+    bun = cap["b"]
+    rows = _row_sample(N)
+    save("cfg5_gmres200_full", csr_sha=np.array(csr_sha), b_sha=np.array(sha(b)), N=N, m=m, ell=ell,
+         sk_seed=SK_SEED, hist=hist, H=bun.H, beta=bun.beta, S=bun.S, T=bun.T,
+         U_colnorm=np.linalg.norm(bun.U, axis=0), U_head=bun.U[:m + 65], rows=rows, U_rows=bun.U[rows],
+         x_rows=x[rows], x_norm=np.linalg.norm(x), x_head=x[:256], x_tail=x[-256:],
+         true_resid=np.linalg.norm(b - A @ x) / np.linalg.norm(b))
+
+
+def cfg5_restart_case():
+    """Config 5 problem, the restarted driver's semantics at full size: two
+    GMRES(10) cycles x1 = gmres(A, b, 0), x2 = gmres(A, b, x1) with the same
+    Omega (SRHT 400 over N - 11 coordinates) — what rhqr_gmres_restarted runs."""
+    A, b, N, csr_sha = _cfg5_problem()
+    m, ell = 10, 400
+    om = SRHTSketch(ell, N - m - 1, SK_SEED)
+    x1, h1 = rhqr_gmres(A, b, None, m, om)
+    x2, h2 = rhqr_gmres(A, b, x1, m, om)
+    rows = _row_sample(N)
+    save("cfg5_gmres10_restart", csr_sha=np.array(csr_sha), N=N, m=m, ell=ell, sk_seed=SK_SEED,
+         hist1=h1, hist2=h2, rows=rows, x1_rows=x1[rows], x2_rows=x2[rows],
+         x1_norm=np.linalg.norm(x1), x2_norm=np.linalg.norm(x2),
+         true_resid2=np.linalg.norm(b - A @ x2) / np.linalg.norm(b))
+
+
 SECTIONS = dict(srht=srht_cases, gauss=gauss_cases, rh_vector=rh_vector_cases, rhqr=rhqr_cases,
                 mixed=mixed_cases, rec=rec_cases, krylov=krylov_cases, apply_compact=apply_compact_cases,
                 block=block_cases, experiments=experiment_cases, trim=trim_cases)
+# the config-scale sections run only when named (minutes of CPU each)
+BIG_SECTIONS = dict(cfg2=cfg2_case, cfg2spread=cfg2_spread_case, cfg3spread=cfg3_spread_case, cfg3sum=cfg3_sum_order_spread_case, cfg3=cfg3_case, cfg4=cfg4_case, cfg5=cfg5_case,
+                    cfg5r=cfg5_restart_case)
 
 if __name__ == "__main__":
     # no arguments: every section; otherwise only the named ones
     for name in (sys.argv[1:] or list(SECTIONS)):
-        SECTIONS[name]()
+        {**SECTIONS, **BIG_SECTIONS}[name]()

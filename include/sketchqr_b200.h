@@ -169,6 +169,22 @@ int sqb_rhqr_left_host(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_d
                        double* T, int64_t ldt, double* R, int64_t ldr,
                        double* sigmas, double* rhos, double* betas);
 
+/* rec_rhqr with HOST operands (rhqr.py:368-395; replaces the whole
+ * reference call with numpy W in and numpy factors out): W (float64,
+ * row-major w_layout = 0 or column-major 1) is uploaded in row blocks aligned
+ * to the split-K slabs of the Gaussian sketch GEMM, and each block's slabs
+ * start on a side stream as soon as it is resident (the sketch runs under the
+ * upload; Z is bitwise that of sqb_rec_rhqr).  Other sketches / precisions:
+ * blocked upload, then the device path.  U (float64, column-major, ldu) comes
+ * back after the reconstruction solve; S, T, R and the scalars as in
+ * sqb_rec_rhqr.  Host buffers should be page-locked.  Returns after the
+ * outputs are written.                                                     */
+int sqb_rec_rhqr_host(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
+                      const double* W, int64_t N, int64_t m, int64_t ldw, int w_layout,
+                      double* U, int64_t ldu, double* S, int64_t lds,
+                      double* T, int64_t ldt, double* R, int64_t ldr,
+                      double* sigmas, double* rhos, double* betas);
+
 /* Release the context's grow-only device scratch (workspace and the
  * host-operand arena); it is re-allocated on the next call that needs it. */
 int sqb_ctx_trim(sqb_ctx* ctx);

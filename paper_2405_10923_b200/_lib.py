@@ -62,6 +62,8 @@ _SIGS = {
                        dp, i64, dp, i64, dp, i64, dp, dp, dp], C.c_int),
     "sqb_rhqr_left_host": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, vp, i64, i64, i64, C.c_int,
                             vp, i64, vp, i64, vp, i64, vp, i64, vp, vp, vp], C.c_int),
+    "sqb_rec_rhqr_host": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, vp, i64, i64, i64, C.c_int,
+                           vp, i64, vp, i64, vp, i64, vp, i64, vp, vp, vp], C.c_int),
     "sqb_ctx_trim": ([vp], C.c_int),
     "sqb_rhqr_block": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, dp, i64, i64, i64, i64, dp, i64,
                         dp, i64, dp, i64, dp, i64, dp, dp, dp], C.c_int),

@@ -94,6 +94,11 @@ int sqb_ctx_destroy(sqb_ctx* ctx) {
   if (ctx->s_out) cudaStreamSynchronize(ctx->s_out);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->big) cudaFree(ctx->big);
+  for (cudaStream_t a : ctx->s_aux)
+    if (a) {
+      cudaStreamSynchronize(a);
+      cudaStreamDestroy(a);
+    }
   if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
   if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
   if (ctx->d_status) cudaFree(ctx->d_status);

@@ -56,6 +56,7 @@ struct sqb_ctx {
   void* big = nullptr;
   size_t big_bytes = 0;
   cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaStream_t s_aux[4] = {nullptr, nullptr, nullptr, nullptr};  // streamed-sketch compute streams
 };
 
 namespace sqb {

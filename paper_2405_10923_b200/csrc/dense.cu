@@ -40,14 +40,15 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __global__ void __launch_bounds__(DNT, 2)
 dense_dmma_kernel(const double* __restrict__ G, int64_t ldg, const double* __restrict__ X,
                   int64_t ldx, int64_t M, int64_t N, int64_t K, int64_t kslab,
-                  double* __restrict__ P, const Status* st) {
+                  double* __restrict__ P, const Status* st, int z_off) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* sG = reinterpret_cast<double*>(smem_raw);
   double* sX = sG + DSTAGES * DBM * DSTR;
   if (st && failed(st)) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t m0 = (int64_t)blockIdx.x * DBM, n0 = (int64_t)blockIdx.y * DBN;
-  const int64_t k0 = (int64_t)blockIdx.z * kslab;
+  const int64_t z = (int64_t)blockIdx.z + z_off;  // slab (a streamed upload launches a range of slabs)
+  const int64_t k0 = z * kslab;
   const int64_t k1 = std::min<int64_t>(K, k0 + kslab);
   const int nk = (int)((k1 - k0 + DBK - 1) / DBK);
 
@@ -134,7 +135,7 @@ dense_dmma_kernel(const double* __restrict__ G, int64_t ldg, const double* __res
   }
   cp_async_wait<0>();
   // epilogue: partial tile -> P[slab] (M x N column-major)
-  double* p = P + (int64_t)blockIdx.z * M * N;
+  double* p = P + z * M * N;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -224,9 +225,39 @@ int launch_dense<double>(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int6
   dim3 grid((unsigned)((sk->ell + DBM - 1) / DBM), (unsigned)((k + DBN - 1) / DBN), (unsigned)S);
   prof_begin(ctx);
   dense_dmma_kernel<<<grid, DNT, DSMEM, ctx->stream>>>(sk->G, sk->ldg, (const double*)X, ldx, sk->ell,
-                                                        k, sk->n, ks, (double*)ws, st);
+                                                        k, sk->n, ks, (double*)ws, st, 0);
   SQB_TRY(check_launch(ctx, "dense_dmma_kernel"));
   prof_end(ctx, 2.0 * (double)sk->ell * (double)sk->n * (double)k);  // flops (bench.py: tensor roofline)
+  const int64_t MN = sk->ell * k;
+  const unsigned rb = (unsigned)std::min<int64_t>((MN + 255) / 256, 4096);
+  dense_reduce_kernel<<<rb, 256, 0, ctx->stream>>>((const double*)ws, sk->ell, k, S, Y, ldy, row_off, st);
+  return check_launch(ctx, "dense_reduce_kernel");
+}
+
+// The same split-K product in pieces (host_pipe.cu, sqb_rec_rhqr_host): the
+// slab partition of launch_dense<double>, slabs [z0, z1) launched on `stream`
+// as soon as their rows of X are resident, then the slab-order reduction —
+// bitwise the one-shot launch.
+int dense_slab_plan(const sqb_sketch* sk, int64_t k, int64_t* kslab) {
+  return dense_slabs(sk->ell, k, sk->n, 148, kslab);
+}
+
+int launch_dense_slabs(sqb_ctx* ctx, cudaStream_t stream, const sqb_sketch* sk, const double* X, int64_t ldx,
+                       int64_t k, int z0, int z1, int64_t kslab, void* ws, const Status* st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dense_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DSMEM);
+    attr = true;
+  }
+  if (z1 <= z0) return SQB_OK;
+  dim3 grid((unsigned)((sk->ell + DBM - 1) / DBM), (unsigned)((k + DBN - 1) / DBN), (unsigned)(z1 - z0));
+  dense_dmma_kernel<<<grid, DNT, DSMEM, stream>>>(sk->G, sk->ldg, X, ldx, sk->ell, k, sk->n, kslab, (double*)ws,
+                                                 st, z0);
+  return check_launch(ctx, "dense_dmma_kernel");
+}
+
+int launch_dense_reduce(sqb_ctx* ctx, const sqb_sketch* sk, int64_t k, int S, const void* ws, double* Y,
+                        int64_t ldy, int64_t row_off, const Status* st) {
   const int64_t MN = sk->ell * k;
   const unsigned rb = (unsigned)std::min<int64_t>((MN + 255) / 256, 4096);
   dense_reduce_kernel<<<rb, 256, 0, ctx->stream>>>((const double*)ws, sk->ell, k, S, Y, ldy, row_off, st);

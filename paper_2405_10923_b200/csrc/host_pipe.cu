@@ -24,7 +24,17 @@
 
 #include "sketch.cuh"
 
+#include "dense.cuh"
+
 namespace sqb {
+
+int rec_rhqr_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t, void*,
+                      int64_t, double*, int64_t, double*, int64_t, double*, int64_t, double*, double*, double*);
+template <typename T>
+int rec_finish_t(sqb_ctx* ctx, int scaling, const double* Z, int64_t od, int64_t m, const T* W2, int64_t n2,
+                 int64_t ldw, T* U2, int64_t ldu, T* Utop, int64_t ldutop, double* S, int64_t lds, double* Tm,
+                 int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos, double* betas, double* M,
+                 double* X);
 
 int rhqr_left_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t,
                        void*, int64_t, double*, int64_t, double*, int64_t, double*, int64_t, double*,
@@ -356,6 +366,191 @@ extern "C" int sqb_rhqr_left_host(sqb_ctx* ctx, const sqb_sketch* sk, int scalin
     return rc;
   }
   // small factors after the finish kernel
+  SQB_CUDA_TRY(cudaMemcpy2DAsync(S, lds * sizeof(double), Sd, od * sizeof(double), od * sizeof(double), m,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaMemcpy2DAsync(T, ldt * sizeof(double), Td, m * sizeof(double), m * sizeof(double), m,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaMemcpy2DAsync(R, ldr * sizeof(double), Rd, m * sizeof(double), m * sizeof(double), m,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaMemcpyAsync(sigmas, Xd, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaMemcpyAsync(rhos, Xd + m, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaMemcpyAsync(betas, Xd + 2 * m, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  SQB_CUDA_TRY(cudaStreamSynchronize(ctx->s_out));
+  SQB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return SQB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// rec_rhqr with host operands (rhqr.py:368-395: numpy W in, numpy factors out).
+//
+//   H2D   W arrives on s_in in row blocks aligned to the split-K slabs of the
+//         Gaussian sketch GEMM (K2): each block's slabs start on an auxiliary
+//         stream as soon as the block is resident, so the 137 GFLOP sketch
+//         runs under the upload; the slab-order reduction then gives Z
+//         bitwise as the one-shot launch does.  (SRHT / low-precision
+//         sketches: the blocks are uploaded, then the device path runs.)
+//   D2H   U streams back after the reconstruction solve (every row of U2
+//         depends on Mfac, i.e. on all of W: the two directions cannot overlap).
+// ---------------------------------------------------------------------------
+extern "C" int sqb_rec_rhqr_host(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype, const double* W,
+                                 int64_t N, int64_t m, int64_t ldw, int w_layout, double* U, int64_t ldu, double* S,
+                                 int64_t lds, double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas,
+                                 double* rhos, double* betas) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->err[0] = 0;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  if (lo_dtype < SQB_F64 || lo_dtype > SQB_BF16) return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
+  SQB_TRY(validate_sketch(ctx, sk));
+  if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
+    return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
+  if (!W || !U || !S || !T || !R || !sigmas || !rhos || !betas)
+    return set_error(ctx, SQB_ERR_ARG, "null host buffer");
+  if (N < 1 || m < 1) return set_error(ctx, SQB_ERR_ARG, "empty matrix");
+  if (sk->n != N - m)
+    return set_error(ctx, SQB_ERR_ARG, "sketch takes %lld coordinates, expected n-m=%lld", (long long)sk->n,
+                     (long long)(N - m));
+  if (sk->ell < m) return set_error(ctx, SQB_ERR_ARG, "sampling size below column count");
+  const bool rowmajor = w_layout == 0;
+  if (w_layout != 0 && w_layout != 1) return set_error(ctx, SQB_ERR_ARG, "unknown layout %d", w_layout);
+  if ((rowmajor && ldw < m) || (!rowmajor && ldw < N) || ldu < N || lds < m + sk->ell || ldt < m || ldr < m)
+    return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
+  SQB_TRY(ensure_streams(ctx));
+  for (auto& a : ctx->s_aux)
+    if (!a) SQB_CUDA_TRY(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+
+  const int64_t n = N - m, od = m + sk->ell;
+  const bool streamed = sk->kind == SQB_SKETCH_DENSE && lo_dtype == SQB_F64;
+  const DevLayout LW = dev_layout(N, m, lo_dtype, m), LU = LW;
+  const size_t es = esize(lo_dtype);
+  int64_t ks = 0;
+  const int nslab = streamed ? dense_slab_plan(sk, m, &ks) : 0;
+  // input blocks: whole slab groups (streamed) or ~32 MB row blocks
+  const int64_t blk_rows = streamed ? ks * std::max<int64_t>(1, ((int64_t)(48ll << 20) / (8 * m)) / ks)
+                                    : std::max<int64_t>(1024, (int64_t)(32ll << 20) / (8 * m));
+  const bool staged_in = rowmajor || lo_dtype != SQB_F64;
+  const int64_t stage_in_elems = staged_in ? (blk_rows + m) * (rowmajor ? std::max(ldw, m) : m) : 0;
+  const int64_t stage_out_elems = lo_dtype == SQB_F64 ? 0 : N * std::min<int64_t>(m, 8);
+  WsPlan plan;
+  const size_t iW = plan.add(LW.bytes), iU = plan.add(LU.bytes);
+  const size_t iS = plan.add(sizeof(double) * od * m), iT = plan.add(sizeof(double) * m * m),
+               iR = plan.add(sizeof(double) * m * m), iX = plan.add(sizeof(double) * 3 * m);
+  const size_t iZ = plan.add(sizeof(double) * od * m), iM = plan.add(sizeof(double) * m * m);
+  const size_t iP = plan.add(streamed ? sizeof(double) * (size_t)nslab * sk->ell * m : 8);
+  const size_t iXs = plan.add(m > 64 ? sizeof(double) * n * m : 8);
+  const size_t iI0 = plan.add(sizeof(double) * stage_in_elems), iI1 = plan.add(sizeof(double) * stage_in_elems);
+  const size_t iO = plan.add(sizeof(double) * stage_out_elems);
+  SQB_TRY(big_reserve(ctx, plan.total + 256));
+  char* base = static_cast<char*>(ctx->big);
+  void* Wd = base + plan.offs[iW] + LW.shift * es;
+  void* Ud = base + plan.offs[iU] + LU.shift * es;
+  double* Sd = reinterpret_cast<double*>(base + plan.offs[iS]);
+  double* Td = reinterpret_cast<double*>(base + plan.offs[iT]);
+  double* Rd = reinterpret_cast<double*>(base + plan.offs[iR]);
+  double* Xd = reinterpret_cast<double*>(base + plan.offs[iX]);
+  double* Zd = reinterpret_cast<double*>(base + plan.offs[iZ]);
+  double* Md = reinterpret_cast<double*>(base + plan.offs[iM]);
+  void* Pd = base + plan.offs[iP];
+  double* stage_in[2] = {reinterpret_cast<double*>(base + plan.offs[iI0]),
+                         reinterpret_cast<double*>(base + plan.offs[iI1])};
+  double* stage_out = reinterpret_cast<double*>(base + plan.offs[iO]);
+  Status* st = ctx->d_status;
+
+  EventPool evp;
+  {  // side streams must not run ahead of earlier work on ctx->stream (arena reuse)
+    cudaEvent_t e = evp.get();
+    SQB_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(Status), ctx->stream));
+    SQB_CUDA_TRY(cudaEventRecord(e, ctx->stream));
+    SQB_CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, e, 0));
+    SQB_CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, e, 0));
+    for (auto a : ctx->s_aux) SQB_CUDA_TRY(cudaStreamWaitEvent(a, e, 0));
+  }
+  // ---- upload in row blocks [r0, r1) of W (block 0 also carries the m identity rows)
+  std::vector<cudaEvent_t> done;
+  int slot = 0, z = 0;
+  for (int64_t r0 = 0, b = 0; r0 < N; ++b, slot ^= 1) {
+    const int64_t r1 = std::min(N, (b == 0 ? m : r0) + blk_rows);
+    const int64_t R = r1 - r0;
+    if (rowmajor) {
+      SQB_CUDA_TRY(cudaMemcpyAsync(stage_in[slot], W + r0 * ldw, (size_t)R * ldw * sizeof(double),
+                                   cudaMemcpyHostToDevice, ctx->s_in));
+      dim3 grid((unsigned)((R + 31) / 32), (unsigned)((m + 31) / 32));
+      SQB_TRY(by_dtype(lo_dtype, [&](auto t) {
+        using TT = decltype(t);
+        rowblock_to_colmajor<TT><<<grid, 256, 0, ctx->s_in>>>(stage_in[slot], ldw, R, m, (TT*)Wd + r0, LW.ld, st);
+        return check_launch(ctx, "rowblock_to_colmajor");
+      }));
+    } else if (lo_dtype == SQB_F64) {
+      SQB_CUDA_TRY(cudaMemcpy2DAsync((double*)Wd + r0, LW.ld * sizeof(double), W + r0, ldw * sizeof(double),
+                                     R * sizeof(double), m, cudaMemcpyHostToDevice, ctx->s_in));
+    } else {
+      SQB_CUDA_TRY(cudaMemcpy2DAsync(stage_in[slot], R * sizeof(double), W + r0, ldw * sizeof(double),
+                                     R * sizeof(double), m, cudaMemcpyHostToDevice, ctx->s_in));
+      const unsigned gb = (unsigned)std::min<int64_t>((R * m + 255) / 256, 4 * ctx->sm_count);
+      SQB_TRY(by_dtype(lo_dtype, [&](auto t) {
+        using TT = decltype(t);
+        colblock_convert<TT><<<gb, 256, 0, ctx->s_in>>>(stage_in[slot], R, R, m, (TT*)Wd + r0, LW.ld, st);
+        return check_launch(ctx, "colblock_convert");
+      }));
+    }
+    cudaEvent_t e = evp.get();
+    SQB_CUDA_TRY(cudaEventRecord(e, ctx->s_in));
+    if (streamed) {
+      // slabs whose Omega rows [z ks, (z+1) ks) are now resident
+      const int zend = r1 >= N ? nslab : (int)std::min<int64_t>(nslab, (r1 - m) / ks);
+      if (zend > z) {
+        cudaStream_t cs = ctx->s_aux[b % 4];
+        SQB_CUDA_TRY(cudaStreamWaitEvent(cs, e, 0));
+        SQB_TRY(launch_dense_slabs(ctx, cs, sk, (const double*)Wd + m, LW.ld, m, z, zend, ks, Pd, st));
+        cudaEvent_t e2 = evp.get();
+        SQB_CUDA_TRY(cudaEventRecord(e2, cs));
+        done.push_back(e2);
+        z = zend;
+      }
+    }
+    done.push_back(e);
+    r0 = r1;
+  }
+  for (cudaEvent_t e : done) SQB_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, e, 0));
+  // ---- sketch-space work and the reconstruction on ctx->stream
+  int rc = SQB_OK;
+  if (streamed) {
+    rc = launch_copy_top(ctx, SQB_F64, Wd, LW.ld, m, m, Zd, od, st);
+    if (rc == SQB_OK) rc = launch_dense_reduce(ctx, sk, m, nslab, Pd, Zd, od, m, st);
+    if (rc == SQB_OK)
+      rc = rec_finish_t<double>(ctx, scaling, Zd, od, m, (const double*)Wd + m, n, LW.ld, (double*)Ud + m, LU.ld,
+                                (double*)Ud, LU.ld, Sd, od, Td, m, Rd, m, Xd, Xd + m, Xd + 2 * m, Md,
+                                reinterpret_cast<double*>(base + plan.offs[iXs]));
+  } else {
+    rc = rec_rhqr_dispatch(ctx, sk, scaling, lo_dtype, Wd, N, m, LW.ld, Ud, LU.ld, Sd, od, Td, m, Rd, m, Xd, Xd + m,
+                           Xd + 2 * m);
+  }
+  if (rc != SQB_OK) {
+    cudaDeviceSynchronize();
+    return rc;
+  }
+  // ---- download U (float64, column-major host) on s_out, small factors on ctx->stream
+  {
+    cudaEvent_t e = evp.get();
+    SQB_CUDA_TRY(cudaEventRecord(e, ctx->stream));
+    SQB_CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, e, 0));
+    if (lo_dtype == SQB_F64) {
+      SQB_CUDA_TRY(cudaMemcpy2DAsync(U, ldu * sizeof(double), Ud, LU.ld * sizeof(double), N * sizeof(double), m,
+                                     cudaMemcpyDeviceToHost, ctx->s_out));
+    } else {
+      const int64_t g = std::min<int64_t>(m, 8);
+      for (int64_t c0 = 0; c0 < m; c0 += g) {
+        const int64_t k = std::min(g, m - c0);
+        const unsigned gb = (unsigned)std::min<int64_t>((N * k + 255) / 256, 4 * ctx->sm_count);
+        SQB_TRY(by_dtype(lo_dtype, [&](auto t) {
+          using TT = decltype(t);
+          colblock_widen<TT><<<gb, 256, 0, ctx->s_out>>>((const TT*)Ud + c0 * LU.ld, LU.ld, N, k, stage_out, N);
+          return check_launch(ctx, "colblock_widen");
+        }));
+        SQB_CUDA_TRY(cudaMemcpy2DAsync(U + c0 * ldu, ldu * sizeof(double), stage_out, N * sizeof(double),
+                                       N * sizeof(double), k, cudaMemcpyDeviceToHost, ctx->s_out));
+      }
+    }
+  }
   SQB_CUDA_TRY(cudaMemcpy2DAsync(S, lds * sizeof(double), Sd, od * sizeof(double), od * sizeof(double), m,
                                  cudaMemcpyDeviceToHost, ctx->stream));
   SQB_CUDA_TRY(cudaMemcpy2DAsync(T, ldt * sizeof(double), Td, m * sizeof(double), m * sizeof(double), m,

@@ -204,6 +204,8 @@ def rec_rhqr(W, omega, scaling=SCALE_SQRT2, policy=None):
     host = not is_device(W)
     n, m = _shape2(W)
     psi = _embed(omega, n, m)
+    if host:
+        return _rec_rhqr_host(W, psi, scaling, policy)
     tag = policy.low
     Wd = to_device(W, tag, align_row=m)
     od = psi.out_dim
@@ -221,6 +223,28 @@ def rec_rhqr(W, omega, scaling=SCALE_SQRT2, policy=None):
     return RHQRFactors(U=_out(U, host), S=_out(S, host), T=_out(T, host), R=_out(R, host), psi=psi,
                        scaling=scaling, sigmas=_out(scal[:m], host), rhos=_out(scal[m:2 * m], host),
                        betas=_out(scal[2 * m:], host))
+
+
+def _rec_rhqr_host(W, psi, scaling, policy):
+    """Host operands: one sqb_rec_rhqr_host call — the Gaussian sketch GEMM
+    runs under the blocked upload of W (csrc/host_pipe.cu); float64 factors
+    come back as column-major ndarrays, U in page-locked memory."""
+    Wa, layout, ldw = host_f64(W)
+    n, m = Wa.shape
+    od = psi.out_dim
+    U = pinned_f64(n, m)
+    S = np.empty((m, od)).T
+    T = np.empty((m, m)).T
+    R = np.empty((m, m)).T
+    scal = np.empty(3 * m)
+    ctx = _lib.context()
+    p = lambda a: a.ctypes.data  # noqa: E731
+    ctx.check(_lib.lib().sqb_rec_rhqr_host(
+        ctx.h, psi.omega.desc(), scaling_code(scaling), CODES[policy.low], p(Wa), n, m, ldw, layout,
+        p(U), n, p(S), od, p(T), m, p(R), m, p(scal), p(scal[m:]), p(scal[2 * m:])), "sqb_rec_rhqr_host")
+    raise_status(ctx, "rec_rhqr", policy.low)
+    return RHQRFactors(U=U, S=S, T=T, R=R, psi=psi, scaling=scaling, sigmas=scal[:m], rhos=scal[m:2 * m],
+                       betas=scal[2 * m:])
 
 
 def rh_vector(w, y, j, scaling=SCALE_SQRT2, policy=None):

@@ -109,6 +109,38 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// dot(a[lo:hi], b[lo:hi]) by one warp (all lanes get it): lanes stride the
+// range with four independent accumulators, so four loads per lane are in
+// flight (the sketch-space dots are L2-latency bound, not bandwidth bound)
+__device__ __forceinline__ double warp_dot(const double* a, const double* b, int lo, int hi) {
+  const int lane = threadIdx.x & 31;
+  double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+  int i = lo + lane;
+  for (; i + 96 < hi; i += 128) {
+    d0 = fma(a[i], b[i], d0);
+    d1 = fma(a[i + 32], b[i + 32], d1);
+    d2 = fma(a[i + 64], b[i + 64], d2);
+    d3 = fma(a[i + 96], b[i + 96], d3);
+  }
+  for (; i < hi; i += 32) d0 = fma(a[i], b[i], d0);
+  return warp_sum((d0 + d1) + (d2 + d3));
+}
+
+// the same with a strided first operand: sum_i a[i * sa] b[i]
+__device__ __forceinline__ double warp_dot_strided(const double* a, int64_t sa, const double* b, int lo, int hi) {
+  const int lane = threadIdx.x & 31;
+  double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+  int i = lo + lane;
+  for (; i + 96 < hi; i += 128) {
+    d0 = fma(a[(int64_t)i * sa], b[i], d0);
+    d1 = fma(a[(int64_t)(i + 32) * sa], b[i + 32], d1);
+    d2 = fma(a[(int64_t)(i + 64) * sa], b[i + 64], d2);
+    d3 = fma(a[(int64_t)(i + 96) * sa], b[i + 96], d3);
+  }
+  for (; i < hi; i += 32) d0 = fma(a[(int64_t)i * sa], b[i], d0);
+  return warp_sum((d0 + d1) + (d2 + d3));
+}
+
 // block-wide sum; `red` must hold >= 32 doubles; all threads get the result
 __device__ __forceinline__ double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;

@@ -8,32 +8,36 @@
 
 namespace sqb {
 
-// C[:, col] = op(T) (S^t Y[:, col]) ; one CTA per column of Y
-__global__ void __launch_bounds__(256)
+// C[:, col] = op(T) (S^t Y[:, col]) ; one CTA per column of Y.  Warp per
+// output with the lanes over the reduction index (warp_dot): every dot is a
+// few L2 round trips, not a chain of dependent loads per thread.
+constexpr int COEF_NT = 512;
+__global__ void __launch_bounds__(COEF_NT)
 coef_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict__ Tm, int64_t ldt,
             int transpose_t, const double* __restrict__ Y, int64_t ldy, int od, int r,
             double* __restrict__ C, int64_t ldc, const Status* st) {
   extern __shared__ double g[];  // [r]
   if (st && failed(st)) return;
-  const int col = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* y = Y + (int64_t)col * ldy;
-  for (int k = warp; k < r; k += 8) {
-    const double* sk = S + (int64_t)k * lds;
-    double d = 0.0;
-    for (int i = lane; i < od; i += 32) d = fma(sk[i], y[i], d);
-    d = warp_sum(d);
+  for (int k = warp; k < r; k += nw) {
+    const double d = warp_dot(S + (int64_t)k * lds, y, 0, od);
     if (lane == 0) g[k] = d;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < r; i += 256) {
-    double d = 0.0;
-    if (transpose_t) {
-      for (int k = 0; k <= i; ++k) d = fma(Tm[k + (int64_t)i * ldt], g[k], d);  // (T^t g)[i]
-    } else {
-      for (int k = i; k < r; ++k) d = fma(Tm[i + (int64_t)k * ldt], g[k], d);  // (T g)[i]
-    }
-    C[i + (int64_t)col * ldc] = d;
+  for (int i = warp; i < r; i += nw) {
+    // (T^t g)[i] = T[:i+1, i] . g[:i+1] (a column of T);  (T g)[i] = T[i, i:] . g[i:]
+    const double d = transpose_t ? warp_dot(Tm + (int64_t)i * ldt, g, 0, i + 1)
+                                 : warp_dot_strided(Tm + i, ldt, g, i, r);
+    if (lane == 0) C[i + (int64_t)col * ldc] = d;
   }
+}
+
+int launch_coef(sqb_ctx* ctx, const double* S, int64_t lds, const double* Tm, int64_t ldt, int transpose_t,
+                const double* Y, int64_t ldy, int od, int r, double* C, int64_t ldc, int k) {
+  coef_kernel<<<(unsigned)k, COEF_NT, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, ldy, od, r,
+                                                                         C, ldc, ctx->d_status);
+  return check_launch(ctx, "coef_kernel");
 }
 
 // Out[:, col] = fl(X[:, col] - fl(U C_lo[:, col]))  (rhqr.py:118); persistent
@@ -111,7 +115,7 @@ static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, con
   SQB_TRY(launch_copy_top(ctx, Lo<T>::code, X, ldx, m, k, Y, od, st));
   SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const T*)X + m, ldx, k, Y, od, m,
                         static_cast<char*>(ws_base) + plan.offs[iP], st));
-  coef_kernel<<<(unsigned)k, 256, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od,
+  coef_kernel<<<(unsigned)k, COEF_NT, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od,
                                                                      (int)od, (int)r, C, r, st);
   SQB_TRY(check_launch(ctx, "coef_kernel"));
   constexpr int VN = VecN<T>::n;
@@ -137,7 +141,7 @@ int compact_update_dispatch(sqb_ctx* ctx, int lo_dtype, const double* Y, int64_t
                             const double* Tm, int64_t ldt, int transpose_t, int64_t r, const void* U, int64_t ldu,
                             int64_t N, const void* X, void* Out, double* C) {
   const Status* st = ctx->d_status;
-  coef_kernel<<<1, 256, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od, (int)od, (int)r, C,
+  coef_kernel<<<1, COEF_NT, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od, (int)od, (int)r, C,
                                                            r, st);
   SQB_TRY(check_launch(ctx, "coef_kernel"));
   auto run = [&](auto t) -> int {

@@ -1,6 +1,7 @@
 // RHQR-Arnoldi and GMRES on the device (krylov.py:82-222).
 //
-// Per Arnoldi step j (krylov.py:113-143) the host enqueues, without any sync:
+// Per Arnoldi step j (krylov.py:113-143) the host enqueues, without any sync
+// (the unscaled w of each step is written straight into its basis column):
 //   arn_step_kernel   happy-breakdown test, rh_vector on z (rhqr.py:51-97),
 //                     S/T columns (_extend_t), the Hessenberg column, and the
 //                     q-coefficients T_j S_j[j-1, :]^t                (1 CTA)
@@ -169,18 +170,17 @@ __global__ void __launch_bounds__(ARN_NT) arn_step_kernel(ArnArgs a) {
   }
   __syncthreads();
   // _extend_t (rhqr.py:135-140): T[:jj, jj] = -beta T[:jj,:jj] (S[:, :jj]^t s)
+  // (warp per output, lanes over the reduction index: warp_dot)
   for (int k = warp; k < jj; k += nw) {
-    const double* sk = a.S + (int64_t)k * a.lds;
-    double d = 0.0;
-    for (int r = max(k, jj) + lane; r < od; r += 32) d = fma(sk[r], s[r], d);
-    d = warp_sum(d);
+    const double d = warp_dot(a.S + (int64_t)k * a.lds, s, max(k, jj), od);
     if (lane == 0) v[k] = d;
   }
+  // S[j-1, :j] for the q coefficients (row jj of S, gathered once)
+  double* srow = red + 32;  // [m+1]
+  for (int k = tid; k < j; k += ARN_NT) srow[k] = a.S[jj + (int64_t)k * a.lds];
   __syncthreads();
   for (int i = warp; i < jj; i += nw) {
-    double d = 0.0;
-    for (int k = i + lane; k < jj; k += 32) d = fma(a.T[i + (int64_t)k * a.ldt], v[k], d);
-    d = warp_sum(d);
+    const double d = warp_dot_strided(a.T + i, a.ldt, v, i, jj);
     if (lane == 0) a.T[i + (int64_t)jj * a.ldt] = __dmul_rn(-bo, d);
   }
   if (tid == 0) a.T[jj + (int64_t)jj * a.ldt] = bo;
@@ -188,9 +188,7 @@ __global__ void __launch_bounds__(ARN_NT) arn_step_kernel(ArnArgs a) {
   __syncthreads();
   // coef = T[:j,:j] S[j-1, :j]^t  (krylov.py:136)
   for (int i = warp; i < j; i += nw) {
-    double d = 0.0;
-    for (int k = i + lane; k < j; k += 32) d = fma(a.T[i + (int64_t)k * a.ldt], a.S[jj + (int64_t)k * a.lds], d);
-    d = warp_sum(d);
+    const double d = warp_dot_strided(a.T + i, a.ldt, srow, i, j);
     if (lane == 0) a.coefq[i] = d;
   }
 }
@@ -292,8 +290,8 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
   const size_t iC = plan.add(sizeof(double) * (mt + 1));
   const size_t icq = plan.add(sizeof(double) * (mt + 1));
   const size_t ifs = plan.add(sizeof(double) * 2);
-  const size_t iw = plan.add(sizeof(T) * (n + 16));
-  const size_t iq = plan.add(sizeof(T) * (n + 16));
+  const size_t iw = plan.add(sizeof(T) * (n + 32));
+  const size_t iq = plan.add(sizeof(T) * (n + 32));
   const size_t it64 = plan.add(op.kind == SQB_OP_CSR ? 8 : sizeof(double) * 2 * n);
   const size_t iAR = plan.add(apply_reflectors_ws_bytes(sk, Lo<T>::code, mt, mt, 1));
   const size_t iP = plan.add(std::max(sketch_partials_bytes(sk, Lo<T>::code, 1),
@@ -311,11 +309,13 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
   SQB_CUDA_TRY(cudaMemsetAsync(Tm, 0, sizeof(double) * ldt * mt, ctx->stream));
   SQB_CUDA_TRY(cudaMemsetAsync(H, 0, sizeof(double) * ldh * m, ctx->stream));
   SQB_CUDA_TRY(cudaMemsetAsync(beta, 0, sizeof(double), ctx->stream));
-  // w = lo(b - A lo(x0)); z = Psi w   (krylov.py:111-112)
-  SQB_TRY(matvec_t<T>(ctx, op, (const T*)x0lo, b, w, t64, P, st));
-  SQB_TRY(launch_copy_top(ctx, Lo<T>::code, w, n, mt, 1, z, od, st));
-  SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, w + mt, n, 1, z, od, mt, P, st));
-  const size_t step_smem = sizeof(double) * (od + mt + 32);
+  // w = lo(b - A lo(x0)); z = Psi w   (krylov.py:111-112).  The unscaled w
+  // of every step is written straight into its basis column U[:, j-1] (rows
+  // >= mt; the step kernel writes the identity rows): no copy of w into U.
+  SQB_TRY(matvec_t<T>(ctx, op, (const T*)x0lo, b, (T*)U, t64, P, st));
+  SQB_TRY(launch_copy_top(ctx, Lo<T>::code, U, n, mt, 1, z, od, st));
+  SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (T*)U + mt, n, 1, z, od, mt, P, st));
+  const size_t step_smem = sizeof(double) * (od + 2 * mt + 32);
   cudaFuncSetAttribute(arn_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(step_smem, 48 << 10));
   constexpr int VN = VecN<T>::n;
@@ -326,8 +326,6 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
       1, std::min<int64_t>((n + (int64_t)GEMV_NT * 4 * VN - 1) / ((int64_t)GEMV_NT * 4 * VN), 2 * (int64_t)ctx->sm_count));
   for (int j = 1; j <= mt; ++j) {
     T* uj = (T*)U + (int64_t)(j - 1) * ldu;
-    // the unscaled w becomes column j-1 of U (rows >= mt; the step writes the top rows)
-    SQB_CUDA_TRY(cudaMemcpyAsync(uj + mt, w + mt, sizeof(T) * (n - mt), cudaMemcpyDeviceToDevice, ctx->stream));
     ArnArgs aa{j, m, mt, (int)od, scaling, happy_tol, z, S, lds, Tm, ldt, H, ldh, U, ldu, beta, fs, cq, st};
     arn_step_kernel<T><<<1, ARN_NT, step_smem, ctx->stream>>>(aa);
     SQB_TRY(check_launch(ctx, "arn_step_kernel"));
@@ -346,12 +344,18 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
     prof_end(ctx, (double)sizeof(T) * (double)n * (double)(j + 1));
     // w = lo(A lo(q))  (krylov.py:140)
     SQB_TRY(matvec_t<T>(ctx, op, q, nullptr, w, t64, P, st));
-    // w = (I - U_j T_j^t S_j^t Psi) w  (krylov.py:141-142)
-    SQB_TRY(apply_reflectors_dispatch(ctx, sk, mt, Lo<T>::code, U, ldu, n, j, S, lds, Tm, ldt, 1, w, n, 1, w, n,
-                                      ws_ptr<void>(ctx, plan, iAR)));
+    // U[:, j] = (I - U_j T_j^t S_j^t Psi) w  (krylov.py:141-142): the update
+    // writes the next basis column in place
+    static const bool via_w = [] { const char* e = getenv("SQB_ARN_COPY"); return e && e[0] == '1'; }();
+    T* unext = via_w ? w : (T*)U + (int64_t)j * ldu;
+    SQB_TRY(apply_reflectors_dispatch(ctx, sk, mt, Lo<T>::code, U, ldu, n, j, S, lds, Tm, ldt, 1, w, n, 1, unext,
+                                      ldu, ws_ptr<void>(ctx, plan, iAR)));
     // z = Psi w  (krylov.py:143)
-    SQB_TRY(launch_copy_top(ctx, Lo<T>::code, w, n, mt, 1, z, od, st));
-    SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, w + mt, n, 1, z, od, mt, P, st));
+    SQB_TRY(launch_copy_top(ctx, Lo<T>::code, unext, n, mt, 1, z, od, st));
+    SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, unext + mt, n, 1, z, od, mt, P, st));
+    if (via_w)  // A/B: the unscaled w copied into its basis column
+      SQB_CUDA_TRY(cudaMemcpyAsync((T*)U + (int64_t)j * ldu + mt, w + mt, sizeof(T) * (n - mt),
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
   }
   // read the outcome (the only sync of the whole Arnoldi run)
   SQB_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(Status), cudaMemcpyDeviceToHost, ctx->stream));
@@ -573,7 +577,7 @@ static int arnoldi_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int m, int scaling
   SQB_TRY(gather_T(&ArnRank::q));
   for (int r = 0; r < L; ++r) SQB_TRY(spmv(rk[r], rk[r].b));
   SQB_TRY(sketch_all(&ArnRank::w, &ArnRank::z));
-  const size_t step_smem = sizeof(double) * (od + mt + 32);
+  const size_t step_smem = sizeof(double) * (od + 2 * mt + 32);
   cudaFuncSetAttribute(arn_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(step_smem, 48 << 10));
   for (int j = 1; j <= mt; ++j) {

@@ -166,13 +166,13 @@ def rhqr_arnoldi(A, b, x0, m, omega, scaling=SCALE_SQRT2, policy=None, store_q=T
         happy_tol = 32.0 * policy.u_high
     mt = m + 1
     od = psi.out_dim
+    op = _Operator(A, n, tag, host=op_host)
     U = empty_colmajor(n, mt, tag)
     S = empty_colmajor(od, mt, "double")
     T = empty_colmajor(mt, mt, "double")
     H = empty_colmajor(mt, m, "double")
     Q = empty_colmajor(n, m, "double") if store_q else None
     beta = torch.zeros(1, dtype=torch.float64, device="cuda")
-    op = _Operator(A, n, tag, host=op_host)
     attained = C.c_int(-1)
     ctx = _lib.context()
     _check_op(ctx, op, _lib.lib().sqb_rhqr_arnoldi(

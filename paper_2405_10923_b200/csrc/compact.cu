@@ -1,10 +1,13 @@
 // Compact-form application and Q materialisation (rhqr.py:100-119, 171-188),
 // Gram matrices for the diagnostics (linalg.py:151-160, 193-197).
 #include <algorithm>
+#include <cooperative_groups.h>
 
 #include "sketch.cuh"
 #include "vec.cuh"
 #include "gemv.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sqb {
 
@@ -31,6 +34,51 @@ coef_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict_
                                  : warp_dot_strided(Tm + i, ldt, g, i, r);
     if (lane == 0) C[i + (int64_t)col * ldc] = d;
   }
+}
+
+// One column on an 8-CTA cluster: partial S^t y over each CTA's block of the
+// od rows, combined through DSMEM in rank order (every CTA holds all of g),
+// then op(T) g with the outputs spread over the cluster's 64 warps.  The
+// per-step coefficients of the Arnoldi compact update (krylov.py:141) were
+// one L2-latency-bound CTA (44 us per step at m = 200).
+constexpr int CCL = 8, CCL_NT = 256;
+__global__ void __cluster_dims__(CCL, 1, 1) __launch_bounds__(CCL_NT)
+coef_cl_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict__ Tm, int64_t ldt,
+               int transpose_t, const double* __restrict__ y, int od, int r, double* __restrict__ C,
+               const Status* st) {
+  extern __shared__ double sm[];
+  double* gp = sm;      // [r] partial
+  double* g = sm + r;   // [r]
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const bool dead = st && failed(st);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = CCL_NT / 32;
+  const int B = (od + CCL - 1) / CCL, r0 = rank * B, r1 = min(od, r0 + B);
+  for (int k = warp; k < r; k += nw) {
+    const double d = dead ? 0.0 : warp_dot(S + (int64_t)k * lds, y, r0, max(r0, r1));
+    if (lane == 0) gp[k] = d;
+  }
+  cluster.sync();
+  for (int k = threadIdx.x; k < r; k += CCL_NT) {
+    double d = 0.0;
+    for (int q = 0; q < CCL; ++q) d += cluster.map_shared_rank(gp, q)[k];
+    g[k] = d;
+  }
+  cluster.sync();
+  if (dead) return;
+  const int gw = rank * nw + warp, ngw = CCL * nw;
+  for (int i = gw; i < r; i += ngw) {
+    const double d = transpose_t ? warp_dot(Tm + (int64_t)i * ldt, g, 0, i + 1)
+                                 : warp_dot_strided(Tm + i, ldt, g, i, r);
+    if (lane == 0) C[i] = d;
+  }
+}
+
+static int launch_coef_col(sqb_ctx* ctx, const double* S, int64_t lds, const double* Tm, int64_t ldt,
+                           int transpose_t, const double* y, int od, int r, double* C) {
+  coef_cl_kernel<<<CCL, CCL_NT, sizeof(double) * 2 * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, y, od, r, C,
+                                                                      ctx->d_status);
+  return check_launch(ctx, "coef_cl_kernel");
 }
 
 int launch_coef(sqb_ctx* ctx, const double* S, int64_t lds, const double* Tm, int64_t ldt, int transpose_t,
@@ -115,9 +163,13 @@ static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, con
   SQB_TRY(launch_copy_top(ctx, Lo<T>::code, X, ldx, m, k, Y, od, st));
   SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const T*)X + m, ldx, k, Y, od, m,
                         static_cast<char*>(ws_base) + plan.offs[iP], st));
-  coef_kernel<<<(unsigned)k, COEF_NT, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od,
-                                                                     (int)od, (int)r, C, r, st);
-  SQB_TRY(check_launch(ctx, "coef_kernel"));
+  if (k == 1) {
+    SQB_TRY(launch_coef_col(ctx, S, lds, Tm, ldt, transpose_t, Y, (int)od, (int)r, C));
+  } else {
+    coef_kernel<<<(unsigned)k, COEF_NT, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od,
+                                                                       (int)od, (int)r, C, r, st);
+    SQB_TRY(check_launch(ctx, "coef_kernel"));
+  }
   constexpr int VN = VecN<T>::n;
   const bool vec = ((reinterpret_cast<uintptr_t>(U) & 15) == 0) && (ldu % VN == 0);
   if (vec) {
@@ -141,9 +193,7 @@ int compact_update_dispatch(sqb_ctx* ctx, int lo_dtype, const double* Y, int64_t
                             const double* Tm, int64_t ldt, int transpose_t, int64_t r, const void* U, int64_t ldu,
                             int64_t N, const void* X, void* Out, double* C) {
   const Status* st = ctx->d_status;
-  coef_kernel<<<1, COEF_NT, sizeof(double) * r, ctx->stream>>>(S, lds, Tm, ldt, transpose_t, Y, od, (int)od, (int)r, C,
-                                                           r, st);
-  SQB_TRY(check_launch(ctx, "coef_kernel"));
+  SQB_TRY(launch_coef_col(ctx, S, lds, Tm, ldt, transpose_t, Y, (int)od, (int)r, C));
   auto run = [&](auto t) -> int {
     using T = decltype(t);
     constexpr int VN = VecN<T>::n;

@@ -232,6 +232,10 @@ class RHQRLeft(Workload):
             W = self.make_w(len(rows), CFG["w_seed"] + rank)
             self.Wd = to_device(W, self.tag, align_row=m if rank == 0 else 0)
             D.init_comm()
+            self.exchange = "nccl all-gather"
+            if getattr(self, "p2p", False):  # --exchange p2p: in-kernel peer-memory stores (sqb_p2p_*)
+                D.init_p2p(m, self.ell)
+                self.exchange = "peer-memory mailboxes (NVLink stores + release/acquire flags)"
             self.step = lambda check=False: D.rhqr_left_distributed(self.Wd, self.om, m, policy=pol, check=check)
             self.W_host = None
         else:
@@ -246,7 +250,7 @@ class RHQRLeft(Workload):
         self.config = {"workload": f"rhqr_left {self.name}: W {Ng} x {m} {self.tag}, SRHT ell={self.ell}",
                        "N": Ng, "N_per_gpu": self.N, "m": m, "ell": self.ell, "w_seed": CFG["w_seed"],
                        "sketch_seed": CFG["sketch_seed"],
-                       "parallelism": (f"row-partitioned x{ws} (1 NCCL all-gather/column)" if self.partitioned
+                       "parallelism": (f"row-partitioned x{ws} (1 exchange/column: {self.exchange})" if self.partitioned
                                        else (f"replicas x{ws}" if ws > 1 else "single GPU")),
                        "l2": "no flush: W and U exceed the 126 MB L2",
                        "alg_bytes_per_step": self.alg}
@@ -627,6 +631,9 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="row-partitioned runs (N > 1): per-column exchange by NCCL all-gather or in-kernel "
+                         "peer-memory stores")
     ap.add_argument("--cpu-full", action="store_true",
                     help="also time the CPU reference on the workload's full size (config 2: ~35-60 s)")
     args = ap.parse_args()
@@ -643,6 +650,7 @@ def main():
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
     print(f"[bench] rank {os.environ.get('RANK', '0')}/{ws_env} impl={args.impl}", file=sys.stderr, flush=True)
     wl = WORKLOADS[args.workload]()
+    wl.p2p = args.exchange == "p2p"
     if args.impl == "reference":
         run_reference(args, wl)
         return

@@ -278,6 +278,23 @@ int sqb_rec_rhqr(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype,
 int sqb_nccl_unique_id(char* out, int size);
 int sqb_ctx_init_comm(sqb_ctx* ctx, const char* id, int nranks, int rank);
 
+/* In-kernel peer-memory exchange for the row-partitioned factorizations
+ * (replaces the per-column ncclAllGather of sqb_rhqr_left_dist /
+ * sqb_rec_rhqr_dist).  Each rank allocates a mailbox of
+ * 2 x nranks slots of `count` doubles (count >= m (m + ell)) and returns its
+ * CUDA IPC handle (64 bytes) in handle_out; the handles are exchanged by the
+ * caller (e.g. torch.distributed.all_gather_object) and passed, rank-ordered,
+ * to sqb_p2p_open, which maps every peer's mailbox (NVLink peer access).  From
+ * then on a rank's partials are stored straight into the peers' mailboxes by
+ * a kernel and published with system-scope release flags that the consuming
+ * step kernel acquires: no collective launch on the per-column path.
+ * sqb_p2p_virtual sets up the same exchange between `nranks` virtual ranks on
+ * one device (sqb_*_virtual entries); sqb_p2p_close releases it.          */
+int sqb_p2p_mailbox(sqb_ctx* ctx, int nranks, int64_t count, void* handle_out);
+int sqb_p2p_open(sqb_ctx* ctx, int rank, const void* handles);
+int sqb_p2p_virtual(sqb_ctx* ctx, int nranks, int64_t count);
+int sqb_p2p_close(sqb_ctx* ctx);
+
 /* Halo ranges of the row-partitioned SpMV in the distributed RHQR-Arnoldi
  * (exchange only the referenced entries — one grid row with
  * each neighbour for the 5-point stencil — instead of all-gathering q):

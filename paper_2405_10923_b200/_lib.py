@@ -93,6 +93,10 @@ _SIGS = {
     "sqb_arnoldi_q": ([vp, C.c_int, dp, i64, i64, i64, dp, i64, dp, i64, i64, dp, i64], C.c_int),
     "sqb_nccl_unique_id": ([C.c_char_p, C.c_int], C.c_int),
     "sqb_ctx_init_comm": ([vp, C.c_char_p, C.c_int, C.c_int], C.c_int),
+    "sqb_p2p_mailbox": ([vp, C.c_int, i64, vp], C.c_int),
+    "sqb_p2p_open": ([vp, C.c_int, vp], C.c_int),
+    "sqb_p2p_virtual": ([vp, C.c_int, i64], C.c_int),
+    "sqb_p2p_close": ([vp], C.c_int),
     "sqb_rhqr_left_dist": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, dp, i64, i64, i64, dp, i64, dp, i64,
                             dp, i64, dp, i64, dp, dp, dp, dp], C.c_int),
     "sqb_rhqr_left_virtual": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, C.c_int, C.POINTER(vp),

@@ -86,9 +86,12 @@ int sqb_ctx_trim(sqb_ctx* ctx) {
   return SQB_OK;
 }
 
+int sqb_p2p_close(sqb_ctx* ctx);
+
 int sqb_ctx_destroy(sqb_ctx* ctx) {
   if (!ctx) return SQB_OK;
   cudaSetDevice(ctx->device);
+  if (ctx->p2p_table || !ctx->p2p_local.empty()) sqb_p2p_close(ctx);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->s_in) cudaStreamSynchronize(ctx->s_in);
   if (ctx->s_out) cudaStreamSynchronize(ctx->s_out);

@@ -57,6 +57,17 @@ struct sqb_ctx {
   size_t big_bytes = 0;
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaStream_t s_aux[4] = {nullptr, nullptr, nullptr, nullptr};  // streamed-sketch compute streams
+  // in-kernel peer-memory exchange of the row-partitioned sweep (sqb_p2p_*):
+  // every rank's mailbox is mapped into every peer (CUDA IPC over NVLink), a
+  // rank's partials are stored straight into the peers' mailboxes and
+  // published with a release flag the consuming kernel acquires
+  int p2p_on = 0;
+  int p2p_nranks = 0;
+  int64_t p2p_count = 0;                // doubles per (parity, rank) slot
+  std::vector<void*> p2p_local;         // own mailbox(es): 1, or nranks for virtual ranks
+  std::vector<void*> p2p_opened;        // IPC-opened peer mailboxes
+  void** p2p_table = nullptr;           // device [n_local][nranks] mailbox bases
+  unsigned long long p2p_seq = 0;       // exchanges so far (identical on every rank)
 };
 
 namespace sqb {

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "sketch.cuh"
+#include "p2p.cuh"
 
 namespace sqb {
 
@@ -59,20 +60,24 @@ inline NcclApi* nccl_api() {
 template <typename T>
 __global__ void rank_combine_kernel(const double* __restrict__ G, int nranks, int ell, int m, int ncols, int rank_level,
                                     const int64_t* __restrict__ idx, int log_tb, double norm_lo,
-                                    double* __restrict__ Y0, int64_t ldy, const Status* st) {
+                                    double* __restrict__ Y0, int64_t ldy, const Status* st,
+                                    int64_t rank_stride = -1, const unsigned long long* flags = nullptr,
+                                    int parity = 0, unsigned long long seq = 0) {
   using A = typename Lo<T>::acc;
+  p2p_wait(flags, nranks, parity, seq);  // peer-memory exchange: the peers' partials have landed
   if (failed(st)) return;
+  const int64_t rs = rank_stride < 0 ? (int64_t)ncols * (ell + m) : rank_stride;
   const int pl = ell + m;
   const int col = blockIdx.y;
   for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < m + ell; row += gridDim.x * blockDim.x) {
     double y;
     if (row < m) {
-      y = G[(int64_t)col * pl + ell + row];  // rank 0's slot
+      y = __ldcg(G + (int64_t)col * pl + ell + row);  // rank 0's slot
     } else {
       const int o = row - m;
       const int64_t rhi = __ldg(idx + o) >> log_tb;
       A v[8];
-      for (int q = 0; q < nranks; ++q) v[q] = (A)G[((int64_t)q * ncols + col) * pl + o];
+      for (int q = 0; q < nranks; ++q) v[q] = (A)__ldcg(G + (int64_t)q * rs + (int64_t)col * pl + o);
       int lvl = rank_level;
       for (int w = 1; w < nranks; w <<= 1, ++lvl) {
         const bool neg = (rhi >> lvl) & 1;

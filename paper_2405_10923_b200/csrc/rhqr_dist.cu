@@ -35,6 +35,23 @@ struct DistRank {
   void* P;
 };
 
+// Y0 (od x m) = the rank-order combine of every rank's raw-sketch partials:
+// from the gather buffer, or (p2p) from this process's first mailbox once
+// the peers' release flags of exchange xseq are acquired
+template <typename T>
+static int combine_gathered(sqb_ctx* ctx, bool p2p, const double* G0, int nranks, int64_t ell, int64_t m,
+                            int rank_level, const int64_t* idx, int log_tb, double norm_lo, double* Y0, int64_t od,
+                            unsigned long long xseq) {
+  dim3 grid((unsigned)((od + 255) / 256), (unsigned)m);
+  const int par = (int)(xseq & 1);
+  void* mb = p2p ? ctx->p2p_local[0] : nullptr;
+  rank_combine_kernel<T><<<grid, 256, 0, ctx->stream>>>(
+      p2p ? p2p_slot(mb, nranks, ctx->p2p_count, par, 0) : G0, nranks, (int)ell, (int)m, (int)m, rank_level, idx,
+      log_tb, norm_lo, Y0, od, ctx->d_status, p2p ? ctx->p2p_count : -1,
+      p2p ? reinterpret_cast<const unsigned long long*>(mb) : nullptr, par, xseq);
+  return check_launch(ctx, "rank_combine_kernel");
+}
+
 template <typename T>
 static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t m, std::vector<DistRank>& rk,
                        int nranks, bool virt, const std::vector<int>& rank_ids) {
@@ -83,11 +100,24 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
   double* G0 = (double*)(base + plan.offs[iG0]);
   double* Y0 = (double*)(base + plan.offs[iY0]);
   Status* st = ctx->d_status;
-  NcclApi* nc = virt ? nullptr : nccl_api();
-  if (!virt && (!nc || !ctx->nccl)) return set_error(ctx, SQB_ERR_NCCL, "NCCL communicator not initialised");
+  const bool p2p_ready = ctx->p2p_on && ctx->p2p_nranks == nranks && (int)ctx->p2p_local.size() == L &&
+                         ctx->p2p_count >= m * od;
+  NcclApi* nc = (virt || p2p_ready) ? nullptr : nccl_api();
+  if (!virt && !p2p_ready && (!nc || !ctx->nccl))
+    return set_error(ctx, SQB_ERR_NCCL, "no exchange: neither an NCCL communicator nor peer mailboxes (sqb_p2p_open)");
 
-  // all-gather `count` doubles from every rank's send buffer into G ([rank][count])
+  // peer-memory exchange (sqb_p2p_*): every payload fits a mailbox slot
+  const bool p2p = ctx->p2p_on && ctx->p2p_nranks == nranks && ctx->p2p_count >= (int64_t)m * od &&
+                   (int)ctx->p2p_local.size() == L;
+  unsigned long long xseq = 0;  // sequence number of the last exchange (p2p)
+  // all-gather `count` doubles from every rank's send buffer into G ([rank][count]);
+  // p2p: store them into every peer's mailbox instead (the consumer acquires)
   auto exchange = [&](double* (*sendp)(DistRank&), size_t count, double* G) -> int {
+    if (p2p) {
+      xseq = ++ctx->p2p_seq;
+      for (int r = 0; r < L; ++r) SQB_TRY(p2p_push(ctx, sendp(rk[r]), (int64_t)count, r, rank_ids[r], xseq));
+      return SQB_OK;
+    }
     if (virt) {
       for (int r = 0; r < L; ++r)
         SQB_CUDA_TRY(cudaMemcpyAsync(G + (size_t)rank_ids[r] * count, sendp(rk[r]), sizeof(double) * count,
@@ -117,12 +147,9 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
     if (d.mrow > 0) SQB_TRY(launch_copy_top(ctx, Lo<T>::code, d.W, d.ldw, m, m, d.Y0pay + ell, od, st));
   }
   SQB_TRY(exchange([](DistRank& d) { return d.Y0pay; }, (size_t)m * od, G0));
-  {
-    dim3 grid((unsigned)((od + 255) / 256), (unsigned)m);
-    rank_combine_kernel<T><<<grid, 256, 0, ctx->stream>>>(G0, nranks, (int)ell, (int)m, (int)m, rank_level, sk->indices,
-                                                          g.log_tb, norm_lo, Y0, od, st);
-    SQB_TRY(check_launch(ctx, "rank_combine_kernel"));
-  }
+  // every local rank combines from its own mailbox (p2p) or the shared gather buffer
+  SQB_TRY(combine_gathered<T>(ctx, p2p, G0, nranks, ell, m, rank_level, sk->indices, g.log_tb, norm_lo, Y0, od,
+                              xseq));
   const size_t step_smem = step_smem_bytes((int)od, (int)m);
   cudaFuncSetAttribute(rhqr_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(step_smem, 48 * 1024));
@@ -130,7 +157,15 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
     StepArgs sa{};
     sa.c = c; sa.m = (int)m; sa.off = 0; sa.ncol = (int)m; sa.ell = (int)ell; sa.od = (int)od; sa.scaling = scaling;
     sa.tree = c == 0 ? 0 : 2;
-    sa.gath = Gc; sa.nranks = nranks; sa.rank_level = rank_level;
+    sa.gath = Gc; sa.gstride = od; sa.flags = nullptr; sa.seq = 0;
+    if (p2p) {  // this rank's own mailbox: the peers stored their partials into it
+      void* mb = ctx->p2p_local[&d - rk.data()];
+      sa.gath = p2p_slot(mb, nranks, ctx->p2p_count, (int)(xseq & 1), 0);
+      sa.gstride = ctx->p2p_count;
+      sa.flags = reinterpret_cast<const unsigned long long*>(mb);
+      sa.seq = xseq;
+    }
+    sa.nranks = nranks; sa.rank_level = rank_level;
     sa.P = nullptr; sa.n_tiles = tpr; sa.n_eff = 0; sa.idx = sk->indices; sa.log_tb = g.log_tb; sa.norm_lo = norm_lo;
     sa.y = c == 0 ? Y0 : d.y; sa.Y0 = Y0; sa.S = d.S; sa.lds = d.lds; sa.R = d.R; sa.ldr = d.ldr;
     sa.U = d.Utop; sa.ldu = d.ldutop; sa.sigmas = d.sig; sa.rhos = d.rho; sa.betas = d.bet;
@@ -240,8 +275,11 @@ static int rec_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t m
   double* G0 = (double*)(base + plan.offs[iG0]);
   double* Z = (double*)(base + plan.offs[iZ]);
   Status* st = ctx->d_status;
-  NcclApi* nc = virt ? nullptr : nccl_api();
-  if (!virt && (!nc || !ctx->nccl)) return set_error(ctx, SQB_ERR_NCCL, "NCCL communicator not initialised");
+  const bool p2p_ready = ctx->p2p_on && ctx->p2p_nranks == nranks && (int)ctx->p2p_local.size() == L &&
+                         ctx->p2p_count >= m * od;
+  NcclApi* nc = (virt || p2p_ready) ? nullptr : nccl_api();
+  if (!virt && !p2p_ready && (!nc || !ctx->nccl))
+    return set_error(ctx, SQB_ERR_NCCL, "no exchange: neither an NCCL communicator nor peer mailboxes (sqb_p2p_open)");
   double scale_lo = 0.0, norm_lo = 0.0;
   srht_constants(sk, Lo<T>::code, &scale_lo, &norm_lo);
   for (int r = 0; r < L; ++r) {
@@ -257,7 +295,13 @@ static int rec_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t m
     if (d.mrow > 0) SQB_TRY(launch_copy_top(ctx, Lo<T>::code, d.W, d.ldw, m, m, d.Y0pay + ell, od, st));
   }
   const size_t count = (size_t)m * od;
-  if (virt) {
+  const bool p2p = ctx->p2p_on && ctx->p2p_nranks == nranks && ctx->p2p_count >= (int64_t)count &&
+                   (int)ctx->p2p_local.size() == L;
+  unsigned long long xseq = 0;
+  if (p2p) {
+    xseq = ++ctx->p2p_seq;
+    for (int r = 0; r < L; ++r) SQB_TRY(p2p_push(ctx, rk[r].Y0pay, (int64_t)count, r, rank_ids[r], xseq));
+  } else if (virt) {
     for (int r = 0; r < L; ++r)
       SQB_CUDA_TRY(cudaMemcpyAsync(G0 + (size_t)rank_ids[r] * count, rk[r].Y0pay, sizeof(double) * count,
                                    cudaMemcpyDeviceToDevice, ctx->stream));
@@ -266,12 +310,7 @@ static int rec_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t m
     if (e != ncclSuccess)
       return set_error(ctx, SQB_ERR_NCCL, "ncclAllGather: %s", nc->getErrorString ? nc->getErrorString(e) : "?");
   }
-  {
-    dim3 grid((unsigned)((od + 255) / 256), (unsigned)m);
-    rank_combine_kernel<T><<<grid, 256, 0, ctx->stream>>>(G0, nranks, (int)ell, (int)m, (int)m, rank_level, sk->indices,
-                                                          g.log_tb, norm_lo, Z, od, st);
-    SQB_TRY(check_launch(ctx, "rank_combine_kernel"));
-  }
+  SQB_TRY(combine_gathered<T>(ctx, p2p, G0, nranks, ell, m, rank_level, sk->indices, g.log_tb, norm_lo, Z, od, xseq));
   for (int r = 0; r < L; ++r) {
     DistRank& d = rk[r];
     SQB_TRY(rec_finish_t<T>(ctx, scaling, Z, od, m, (const T*)d.W + d.mrow, d.n_local, d.ldw, (T*)d.U + d.mrow,
@@ -319,6 +358,34 @@ static int check_common(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t
 
 using namespace sqb;
 
+// ---- peer-memory exchange setup ------------------------------------------------
+static int p2p_release(sqb_ctx* ctx) {
+  for (void* p : ctx->p2p_opened) cudaIpcCloseMemHandle(p);
+  for (void* p : ctx->p2p_local) cudaFree(p);
+  if (ctx->p2p_table) cudaFree(ctx->p2p_table);
+  ctx->p2p_opened.clear();
+  ctx->p2p_local.clear();
+  ctx->p2p_table = nullptr;
+  ctx->p2p_on = 0;
+  ctx->p2p_nranks = 0;
+  ctx->p2p_count = 0;
+  return SQB_OK;
+}
+
+static int p2p_alloc(sqb_ctx* ctx, int nranks, int64_t count, void** out) {
+  const size_t bytes = p2p_mailbox_bytes(nranks, count);
+  SQB_CUDA_TRY(cudaMalloc(out, bytes));
+  SQB_CUDA_TRY(cudaMemset(*out, 0, p2p_flag_bytes(nranks)));
+  return SQB_OK;
+}
+
+static int p2p_set_table(sqb_ctx* ctx, const std::vector<void*>& table) {
+  SQB_CUDA_TRY(cudaMalloc(&ctx->p2p_table, sizeof(void*) * table.size()));
+  SQB_CUDA_TRY(cudaMemcpy(ctx->p2p_table, table.data(), sizeof(void*) * table.size(), cudaMemcpyHostToDevice));
+  return SQB_OK;
+}
+
+
 extern "C" {
 
 int sqb_nccl_unique_id(char* out, int size) {
@@ -328,6 +395,74 @@ int sqb_nccl_unique_id(char* out, int size) {
   if (nc->getUniqueId(&id) != ncclSuccess) return SQB_ERR_NCCL;
   memcpy(out, &id, sizeof(id));
   return SQB_OK;
+}
+
+int sqb_p2p_mailbox(sqb_ctx* ctx, int nranks, int64_t count, void* handle_out) {
+  if (!ctx || !handle_out || nranks < 1 || nranks > 8 || count < 1) return SQB_ERR_ARG;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_CUDA_TRY(cudaDeviceSynchronize());
+  p2p_release(ctx);
+  void* mb = nullptr;
+  SQB_TRY(p2p_alloc(ctx, nranks, count, &mb));
+  ctx->p2p_local.push_back(mb);
+  ctx->p2p_nranks = nranks;
+  ctx->p2p_count = count;
+  cudaIpcMemHandle_t h;
+  SQB_CUDA_TRY(cudaIpcGetMemHandle(&h, mb));
+  memcpy(handle_out, &h, sizeof(h));
+  return SQB_OK;
+}
+
+int sqb_p2p_open(sqb_ctx* ctx, int rank, const void* handles) {
+  if (!ctx || !handles || ctx->p2p_local.size() != 1) return SQB_ERR_ARG;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  const int P = ctx->p2p_nranks;
+  if (rank < 0 || rank >= P) return set_error(ctx, SQB_ERR_ARG, "rank %d outside %d", rank, P);
+  std::vector<void*> table(P);
+  for (int q = 0; q < P; ++q) {
+    if (q == rank) {
+      table[q] = ctx->p2p_local[0];
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const char*>(handles) + (size_t)q * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    SQB_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->p2p_opened.push_back(p);
+    table[q] = p;
+  }
+  SQB_TRY(p2p_set_table(ctx, table));
+  ctx->p2p_on = 1;
+  ctx->nranks = P;  // the row partition of the *_dist entries (as sqb_ctx_init_comm sets it)
+  ctx->rank = rank;
+  return SQB_OK;
+}
+
+int sqb_p2p_virtual(sqb_ctx* ctx, int nranks, int64_t count) {
+  if (!ctx || nranks < 1 || nranks > 8 || count < 1) return SQB_ERR_ARG;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_CUDA_TRY(cudaDeviceSynchronize());
+  p2p_release(ctx);
+  for (int q = 0; q < nranks; ++q) {
+    void* mb = nullptr;
+    SQB_TRY(p2p_alloc(ctx, nranks, count, &mb));
+    ctx->p2p_local.push_back(mb);
+  }
+  std::vector<void*> table((size_t)nranks * nranks);
+  for (int r = 0; r < nranks; ++r)
+    for (int q = 0; q < nranks; ++q) table[(size_t)r * nranks + q] = ctx->p2p_local[q];
+  ctx->p2p_nranks = nranks;
+  ctx->p2p_count = count;
+  SQB_TRY(p2p_set_table(ctx, table));
+  ctx->p2p_on = 1;
+  return SQB_OK;
+}
+
+int sqb_p2p_close(sqb_ctx* ctx) {
+  if (!ctx) return SQB_ERR_ARG;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  SQB_CUDA_TRY(cudaDeviceSynchronize());
+  return p2p_release(ctx);
 }
 
 int sqb_ctx_init_comm(sqb_ctx* ctx, const char* id, int nranks, int rank) {

@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cooperative_groups.h>
 
+#include "p2p.cuh"
 #include "pdl.cuh"
 #include "sketch.cuh"
 #include "vec.cuh"
@@ -482,7 +483,10 @@ struct StepArgs {
   int scaling;
   int tree;                   // 1: finish the SRHT tree from the tile leaves; 0: y[m:] given;
                               // 2: combine the gathered per-rank partials (multi-GPU)
-  const double* gath;         // tree == 2: [nranks][ell + m] per-rank partials (+ rank 0's top rows)
+  const double* gath;         // tree == 2: [nranks][gstride] per-rank partials (+ rank 0's top rows)
+  int64_t gstride;            // tree == 2: doubles between ranks' partials (ell + m for a gather buffer)
+  const unsigned long long* flags;  // tree == 2, peer-memory exchange: acquire flags >= seq first
+  unsigned long long seq;
   int nranks, rank_level;     // tree == 2: P and the tree level of the rank split (log2 local tiles)
   const void* P;              // leaves [ell][n_tiles]
   int64_t n_tiles, n_eff;
@@ -541,6 +545,7 @@ rhqr_step_kernel(StepArgs a) {
   SQB_STAMP(0);
   pdl_wait();
   pdl_trigger();
+  if (a.tree == 2) p2p_wait(a.flags, a.nranks, (int)(a.seq & 1), a.seq);
   SQB_STAMP(1);
   const bool dead = failed(a.st);  // uniform across the cluster; still take part in the sync
   // ---- phase A: y on the owned rows (identity block given; Omega rows from the tree)
@@ -548,17 +553,16 @@ rhqr_step_kernel(StepArgs a) {
     if (a.tree == 2) {
       // upper log2(P) levels of the SRHT tree across ranks (left = lower rank)
       // plus the identity block from rank 0's payload
-      const int pl = a.ell + m;
       for (int i = tid; i < nrow; i += STEP_NT) {
         const int row = r0 + i;
         double y;
         if (row < m) {
-          y = a.gath[a.ell + row];
+          y = __ldcg(a.gath + a.ell + row);
         } else {
           const int o = row - m;
           const int64_t rhi = __ldg(a.idx + o) >> a.log_tb;
           A v[8];
-          for (int q = 0; q < a.nranks; ++q) v[q] = (A)a.gath[q * pl + o];
+          for (int q = 0; q < a.nranks; ++q) v[q] = (A)__ldcg(a.gath + q * a.gstride + o);
           int lvl = a.rank_level;
           for (int w2 = 1; w2 < a.nranks; w2 <<= 1, ++lvl) {
             const bool neg = (rhi >> lvl) & 1;

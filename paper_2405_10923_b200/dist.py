@@ -72,6 +72,35 @@ def init_comm(group=None):
     return ctx
 
 
+def p2p_slot_count(m: int, ell: int) -> int:
+    """Doubles per mailbox slot: the raw-sketch exchange moves m (m + ell)."""
+    return m * (m + ell)
+
+
+def init_p2p(m: int, ell: int, group=None):
+    """In-kernel peer-memory exchange (sqb_p2p_*): allocate this rank's mailbox,
+    all-gather the CUDA IPC handles over the torch process group and map every
+    peer's mailbox.  The row-partitioned factorizations then store their
+    per-column partials straight into the peers' memory (no NCCL launch on the
+    per-column path).  Needs peer access between the GPUs (NVLink/NVSwitch)."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ctx = _lib.context()
+    h = C.create_string_buffer(64)
+    ctx.check(_lib.lib().sqb_p2p_mailbox(ctx.h, world, p2p_slot_count(m, ell), h), "sqb_p2p_mailbox")
+    handles = [None] * world
+    dist.all_gather_object(handles, h.raw, group=group)
+    table = C.create_string_buffer(b"".join(handles), 64 * world)
+    ctx.check(_lib.lib().sqb_p2p_open(ctx.h, rank, table), "sqb_p2p_open")
+    return ctx
+
+
+def close_p2p():
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_p2p_close(ctx.h), "sqb_p2p_close")
+
+
 def rhqr_left_distributed(W_local, omega, m, scaling=SCALE_SQRT2, policy=None, check=True):
     """This rank's part of rhqr_left (rhqr.py:254-267) on the row partition."""
     return _distributed("sqb_rhqr_left_dist", W_local, omega, m, scaling, policy, check)
@@ -119,19 +148,22 @@ def _distributed(entry, W_local, omega, m, scaling, policy, check):
                        betas=_out(scal[2 * m:], host))
 
 
-def rhqr_left_virtual(W, omega, nranks, scaling=SCALE_SQRT2, policy=None):
+def rhqr_left_virtual(W, omega, nranks, scaling=SCALE_SQRT2, policy=None, exchange="copy"):
     """The multi-GPU algorithm with `nranks` virtual ranks on ONE device (the
-    all-gather becomes device copies).  Returns factors with U reassembled in
-    global row order — bitwise equal to rhqr_left by construction."""
-    return _virtual("sqb_rhqr_left_virtual", W, omega, nranks, scaling, policy)
+    all-gather becomes device copies, or with exchange="p2p" the peer-memory
+    mailboxes of sqb_p2p_*).  Returns factors with U reassembled in global row
+    order — bitwise equal to rhqr_left by construction."""
+    return _virtual("sqb_rhqr_left_virtual", W, omega, nranks, scaling, policy, exchange)
 
 
-def rec_rhqr_virtual(W, omega, nranks, scaling=SCALE_SQRT2, policy=None):
+def rec_rhqr_virtual(W, omega, nranks, scaling=SCALE_SQRT2, policy=None, exchange="copy"):
     """Row-partitioned rec_rhqr with `nranks` virtual ranks on one device."""
-    return _virtual("sqb_rec_rhqr_virtual", W, omega, nranks, scaling, policy)
+    return _virtual("sqb_rec_rhqr_virtual", W, omega, nranks, scaling, policy, exchange)
 
 
-def _virtual(entry, W, omega, nranks, scaling, policy):
+def _virtual(entry, W, omega, nranks, scaling, policy, exchange="copy"):
+    if exchange not in ("copy", "p2p"):
+        raise ValueError(f"unknown exchange {exchange!r}")
     check_scaling(scaling)
     policy = policy or DOUBLE_POLICY
     require_device_policy(policy)
@@ -158,11 +190,17 @@ def _virtual(entry, W, omega, nranks, scaling, policy):
     Up = (C.c_void_p * nranks)(*[t.data_ptr() for t in Us])
     Ul = (C.c_int64 * nranks)(*[ld_of(t) for t in Us])
     ctx = _lib.context()
-    ctx.check(getattr(_lib.lib(), entry)(
-        ctx.h, omega.desc(), scaling_code(scaling), CODES[tag], nranks, Wp, Wl, Up, Ul, m, S.data_ptr(),
-        ld_of(S), T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R), scal.data_ptr(), scal.data_ptr() + 8 * m,
-        scal.data_ptr() + 16 * m, scratch.data_ptr()), entry)
-    raise_status(ctx, "rec_rhqr" if entry == "sqb_rec_rhqr_virtual" else "rhqr_left_virtual")
+    if exchange == "p2p":
+        ctx.check(_lib.lib().sqb_p2p_virtual(ctx.h, nranks, p2p_slot_count(m, omega.ell)), "sqb_p2p_virtual")
+    try:
+        ctx.check(getattr(_lib.lib(), entry)(
+            ctx.h, omega.desc(), scaling_code(scaling), CODES[tag], nranks, Wp, Wl, Up, Ul, m, S.data_ptr(),
+            ld_of(S), T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R), scal.data_ptr(), scal.data_ptr() + 8 * m,
+            scal.data_ptr() + 16 * m, scratch.data_ptr()), entry)
+        raise_status(ctx, "rec_rhqr" if entry == "sqb_rec_rhqr_virtual" else "rhqr_left_virtual")
+    finally:
+        if exchange == "p2p":
+            ctx.check(_lib.lib().sqb_p2p_close(ctx.h), "sqb_p2p_close")
     U = empty_colmajor(N, m, tag)
     for rows, Ut in zip(rows_list, Us):
         if len(rows):

@@ -1,0 +1,78 @@
+"""In-kernel peer-memory exchange (sqb_p2p_*) of the row-partitioned sweep:
+each rank's per-column partials are stored straight into its peers' mailboxes
+and published with release flags the step kernel acquires (no collective
+launch).  With virtual ranks on one B200 the factors are bitwise the
+single-GPU ones, as with the copy / NCCL exchange; world 1 runs the real IPC
+set-up path."""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_2405_10923_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2405_10923_b200 as P
+    return P
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4, 8])
+def test_p2p_virtual_rhqr_left_bitwise(P, nranks):
+    from paper_2405_10923_b200 import dist
+    N, m = (1 << 16) + 77, 24
+    W = np.random.default_rng(nranks + 40).standard_normal((N, m))
+    om = P.SRHTSketch(96, N - m, 17)
+    F1 = P.rhqr_left(W, om)
+    Fv = dist.rhqr_left_virtual(W, om, nranks, exchange="p2p")
+    for k in ("R", "S", "T", "U", "sigmas", "rhos", "betas"):
+        assert np.array_equal(getattr(Fv, k), getattr(F1, k)), k
+    # the mailboxes are released: the copy exchange still works afterwards
+    Fc = dist.rhqr_left_virtual(W, om, nranks)
+    assert np.array_equal(Fc.R, F1.R)
+
+
+@pytest.mark.parametrize("nranks,m", [(2, 48), (8, 64)])
+def test_p2p_virtual_rec_rhqr_bitwise(P, nranks, m):
+    from paper_2405_10923_b200 import dist
+    N = (1 << 16) + 77
+    W = workloads.gen_cmatrix(N, m)
+    om = P.SRHTSketch(4 * m, N - m, 19)
+    F1 = P.rec_rhqr(W, om)
+    Fv = dist.rec_rhqr_virtual(W, om, nranks, exchange="p2p")
+    for k in ("R", "S", "T", "sigmas", "rhos", "betas"):
+        assert np.array_equal(getattr(Fv, k), getattr(F1, k)), k
+
+
+def test_p2p_world1_ipc_path(P):
+    """sqb_p2p_mailbox / sqb_p2p_open through torch.distributed (world 1),
+    then the row-partitioned factorizations over the mailboxes; repeated
+    calls reuse the monotone exchange sequence numbers."""
+    import torch.distributed as dist
+    from paper_2405_10923_b200 import dist as D
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(29900 + os.getpid() % 90))
+    created = False
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", rank=0, world_size=1)
+        created = True
+    try:
+        N, m = (1 << 14) + 5, 16
+        W = np.random.default_rng(0).standard_normal((N, m))
+        om = P.SRHTSketch(64, N - m, 3)
+        D.init_p2p(m, om.ell)
+        F1 = P.rhqr_left(W, om)
+        for _ in range(3):
+            Fd = D.rhqr_left_distributed(W, om, m)
+            for k in ("R", "S", "T", "U"):
+                assert np.array_equal(getattr(Fd, k), getattr(F1, k)), k
+        D.close_p2p()
+    finally:
+        if created:
+            dist.destroy_process_group()

@@ -123,6 +123,12 @@ int sqb_ctx_profile_read(sqb_ctx* ctx, double* total_ms, double* total_bytes, in
 /* Instrumentation: the step kernel of `column` writes per-phase clock64 stamps
  * (8 per cluster rank) to the device buffer dev_buf (NULL disables). */
 int sqb_debug_step_stamps(sqb_ctx* ctx, long long* dev_buf, int column);
+/* Instrumentation: every block b of the column pass of `column` writes
+ * {SM id, globaltimer ns at entry, after the flag wait, after the bulk GEMV,
+ * after griddepcontrol.wait, at exit} to dev_buf[8 b ..]; the step kernel of
+ * the same column writes {entry, after its wait, exit} of cluster rank 0 to
+ * dev_buf[8 nblocks ..] (nblocks = the pass's grid size).  NULL disables. */
+int sqb_debug_col_stamps(sqb_ctx* ctx, long long* dev_buf, int column);
 
 /* ---- sketches ------------------------------------------------------------
  * Y (ell x k, fp64, ldy) = Omega X, X (n x k, `dtype`, ldx), arithmetic in

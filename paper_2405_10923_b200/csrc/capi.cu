@@ -169,6 +169,13 @@ int sqb_debug_step_stamps(sqb_ctx* ctx, long long* dev_buf, int column) {
   return SQB_OK;
 }
 
+int sqb_debug_col_stamps(sqb_ctx* ctx, long long* dev_buf, int column) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->dbg_cts = dev_buf;
+  ctx->dbg_ccol = column;
+  return SQB_OK;
+}
+
 int sqb_ctx_status(sqb_ctx* ctx, int* code, int* col, double* val) {
   SQB_TRY(prep(ctx));
   SQB_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(Status), cudaMemcpyDeviceToHost,

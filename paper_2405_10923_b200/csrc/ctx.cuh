@@ -45,6 +45,8 @@ struct sqb_ctx {
   void* nccl = nullptr;
   long long* dbg_ts = nullptr;  // instrumentation: step-kernel phase stamps for column dbg_col
   int dbg_col = -1;
+  long long* dbg_cts = nullptr;  // instrumentation: column-pass block timeline of column dbg_ccol
+  int dbg_ccol = -1;
   int nranks = 1;
   int rank = 0;
   // halo ranges of the row-partitioned SpMV (sqb_ctx_set_halo): [P][P][2]

@@ -79,7 +79,62 @@ struct ColArgs {
   int helper_first;     // block order: 1 = helper, identity block, tiles; 0 = tiles, identity, helper
   int no_p16;           // 1: 16-bit storage stages its tile FWHT in fp32 (test hook, SQB_NO_P16)
   int no_pre;           // 1: no pre-wait loads of w_{c-1} / W[:, c] (A/B hook, SQB_NO_PRE)
+  int no_part;          // 1: partial last tile on the generic unpipelined loop (test hook, SQB_NO_PART)
+  // cross-pass overlap: tflag[b] = last pass block b (tile / identity block /
+  // helper) has completed.  With the step kernel triggering its dependents
+  // BEFORE its own wait, the CTAs of pass c are dispatched into the slots the
+  // last wave of pass c-1 frees and stream their bulk as soon as their own
+  // tile of pass c-1 (and its helper) are done, instead of after the whole
+  // pass, the step launch and this launch.  null: plain PDL order.
+  int* tflag;
+  long long* dbg;       // optional block timeline (sqb_debug_col_stamps)
 };
+
+__device__ __forceinline__ long long gtime_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
+  return t;
+}
+#define SQB_CSTAMP(i) \
+  do { if (a.dbg && threadIdx.x == 0) a.dbg[blockIdx.x * 8 + (i)] = gtime_ns(); } while (0)
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// every thread of the block has issued its stores: publish "block b finished pass c"
+__device__ __forceinline__ void col_flag_done(const ColArgs& a) {
+  if (!a.tflag) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release_gpu(a.tflag + blockIdx.x, a.c);
+  }
+}
+
+// wait until this block's own pass c-1 and the helper of pass c-1 are done
+// (they are resident or finished: pass c-1 was dispatched completely before
+// step c-1, hence before this grid, became eligible).  A recorded failure
+// releases the waiters: every block returns at its post-wait status check.
+__device__ __forceinline__ void col_flag_wait(const ColArgs& a, int64_t helper_id) {
+  if (!a.tflag) return;
+  if (a.c >= 2 && (threadIdx.x == 0 || threadIdx.x == 32)) {
+    const int* f = a.tflag + (threadIdx.x == 0 ? helper_id : (int64_t)blockIdx.x);
+    while (ld_acquire_gpu(f) < a.c - 1 && !failed(a.st)) __nanosleep(40);
+  }
+  __syncthreads();
+}
+
+// SQB_EARLY=0 restores the plain PDL order (A/B experiments)
+inline int early_env() {
+  const char* e = getenv("SQB_EARLY");
+  return e ? atoi(e) : 1;
+}
 
 // SQB_HELPER_FIRST=0 restores the old block order (A/B experiments)
 inline int helper_first_default() {
@@ -88,6 +143,10 @@ inline int helper_first_default() {
 }
 inline int no_pre_env() {
   const char* e = getenv("SQB_NO_PRE");
+  return e && e[0] == '1';
+}
+inline int no_part_env() {
+  const char* e = getenv("SQB_NO_PART");
   return e && e[0] == '1';
 }
 inline int no_p16_env() {
@@ -237,6 +296,12 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
   A* sc = reinterpret_cast<A*>(smem_raw);                      // coef rounded to low [c]
   A* sm = sc + ((a.c + 3) & ~3);                              // tile buffer
   pdl_trigger();
+  if (a.dbg && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;\n" : "=r"(smid));
+    a.dbg[blockIdx.x * 8] = smid;
+  }
+  SQB_CSTAMP(1);
   const int c = a.c;
   // block roles: with helper_first the helper (block 0) and the identity block
   // (block 1) are dispatched first, so the helper's latency-bound sketch-space
@@ -247,10 +312,14 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
   const int64_t tile = a.helper_first ? bid - 2 : bid;
   if (bid == helper_id) {
     pdl_wait();
-    if (failed(a.st)) return;
-    col_helper(a, reinterpret_cast<double*>(sm));
+    SQB_CSTAMP(4);
+    if (!failed(a.st)) col_helper(a, reinterpret_cast<double*>(sm));
+    SQB_CSTAMP(5);
+    col_flag_done(a);
     return;
   }
+  col_flag_wait(a, helper_id);
+  SQB_CSTAMP(2);
   // coef_c[:c-1] = a_c is final before step c-1 ends (helper of pass c-1): load
   // it and stream the bulk of the GEMV BEFORE waiting on step c-1 (look-ahead
   // overlap of the HBM pass with the sketch-space step, via PDL)
@@ -258,6 +327,8 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
   __syncthreads();
   if (bid == top_id) {
     if (a.mrow > 0) col_top_block<T>(a, sc);
+    SQB_CSTAMP(5);
+    col_flag_done(a);
     return;
   }
   constexpr int TB = 1 << LOGT;
@@ -337,6 +408,41 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
       fm(x1, k + 1);
     }
     if (k < K) fm(x0, k);
+  } else if (VN > 1 && tb == TB && rows > 0 && rows % VN == 0 && !a.no_part) {
+    // partial last tile made of whole 16-byte runs (n = N - m is normally a
+    // multiple of the run): the same one-column-ahead pipeline with the runs
+    // beyond `rows` masked.  The generic loop below issues one column, waits
+    // for it, then the next — at config 4 that single block took 270 us of
+    // an 830 us pass whose other 2049 blocks were done after 657 us
+    // (scripts/col_timeline.py); same summation order, same bits.
+    uint4 r0[NV], r1[NV];
+    auto ldp = [&](uint4 (&x)[NV], int k) {
+      const T* col = U + ro + (int64_t)k * a.ldu;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int i = (v * COL_NT + threadIdx.x) * VN;
+        x[v] = i < rows ? ldg_stream(col + i) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
+    auto fmp = [&](const uint4 (&x)[NV], int k) {
+      const A ck = sc[k];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        A w[VN];
+        unpack16<T>(x[v], w);
+#pragma unroll
+        for (int j = 0; j < VN; ++j) acc[v][j] = fma(w[j], ck, acc[v][j]);
+      }
+    };
+    if (K > 0) ldp(r0, 0);
+    int k = 0;
+    for (; k + 2 <= K; k += 2) {
+      ldp(r1, k + 1);
+      fmp(r0, k);
+      if (k + 2 < K) ldp(r0, k + 2);
+      fmp(r1, k + 1);
+    }
+    if (k < K) fmp(r0, k);
   } else {
     for (int k = 0; k < K; ++k) {
       const T* col = U + ro + (int64_t)k * a.ldu;
@@ -374,8 +480,10 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
     }
   }
   // ---- wait for step c-1 (f_{c-1}, coef_c[c-1], breakdown status)
+  SQB_CSTAMP(3);
   pdl_wait();
-  if (failed(a.st)) return;
+  SQB_CSTAMP(4);
+  if (failed(a.st)) { col_flag_done(a); return; }
   // column c-1: lazy scaling of the stored w_{c-1}, write back u_{c-1}
   {
     T* dst = U + ro + (int64_t)(c - 1) * a.ldu;
@@ -440,7 +548,7 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
       }
     }
   }
-  if (!a.srht) return;
+  if (!a.srht) { col_flag_done(a); return; }
   __syncthreads();
   if constexpr (P16OK) {
     if (p16path) {
@@ -449,11 +557,15 @@ __global__ void __launch_bounds__(COL_NT, MINB) rhqr_col_kernel(ColArgs a) {
       float* P = (float*)a.P + tile;
       for (int k = threadIdx.x; k < a.ell; k += COL_NT)
         P[k * a.n_tiles] = pk_lo_float<T>(s16[p16((int)(__ldg(a.idx + k) & ((1 << P16_LOG) - 1)))]);
+      SQB_CSTAMP(5);
+      col_flag_done(a);
       return;
     }
   }
   tile_fwht<T>(sm, a.log_tb);
   tile_gather<T>(sm, a.idx, a.ell, a.log_tb, (A*)a.P + tile, a.n_tiles);
+  SQB_CSTAMP(5);
+  col_flag_done(a);
 }
 
 // Bulk-loop variant of the column pass.  2-byte storage: a raw 2-deep ring
@@ -481,6 +593,7 @@ struct StepArgs {
   int c, m, ell, od;
   int off, ncol;              // sweep offset (pivot row = off + c) and width (rhqr.py:219-251)
   int scaling;
+  int early;                  // 1: trigger the dependents (pass c+1) before waiting for pass c (ColArgs::tflag)
   int tree;                   // 1: finish the SRHT tree from the tile leaves; 0: y[m:] given;
                               // 2: combine the gathered per-rank partials (multi-GPU)
   const double* gath;         // tree == 2: [nranks][gstride] per-rank partials (+ rank 0's top rows)
@@ -505,6 +618,7 @@ struct StepArgs {
   double* clast;              // out: clast[c+1] = coef_{c+1}[c]
   Status* st;
   long long* dbg;             // optional per-phase clock64 stamps [STEP_CL][8] (instrumentation)
+  long long* gdbg;            // optional globaltimer stamps {entry, after wait, exit} of rank 0
 };
 
 #define SQB_STAMP(i) \
@@ -543,8 +657,14 @@ rhqr_step_kernel(StepArgs a) {
   double* red = part + STEP_CL;                      // [32]
   __shared__ double scal[4];
   SQB_STAMP(0);
+  // early: pass c+1 becomes eligible as soon as this cluster is resident; its
+  // blocks order themselves behind pass c with per-block flags and behind
+  // this step with their own griddepcontrol.wait
+  if (a.gdbg && rank == 0 && tid == 0) a.gdbg[0] = gtime_ns();
+  if (a.early) pdl_trigger();
   pdl_wait();
-  pdl_trigger();
+  if (!a.early) pdl_trigger();
+  if (a.gdbg && rank == 0 && tid == 0) a.gdbg[1] = gtime_ns();
   if (a.tree == 2) p2p_wait(a.flags, a.nranks, (int)(a.seq & 1), a.seq);
   SQB_STAMP(1);
   const bool dead = failed(a.st);  // uniform across the cluster; still take part in the sync
@@ -696,6 +816,7 @@ rhqr_step_kernel(StepArgs a) {
     double d = 0.0;
     for (int q = 0; q < STEP_CL; ++q) d += gath[q * nk + c];
     a.clast[c + 1] = __dmul_rn(bo, d - va);
+    if (a.gdbg) a.gdbg[2] = gtime_ns();
   }
   SQB_STAMP(7);
 }

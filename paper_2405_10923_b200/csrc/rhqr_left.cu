@@ -29,7 +29,7 @@ int launch_persist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const double
 struct SweepWs {
   WsPlan plan;
   int64_t chunk;
-  size_t iY0, iy, icoef, iabuf, ivbuf, ifs, iP, iPS;
+  size_t iY0, iy, icoef, iabuf, ivbuf, ifs, iP, iPS, iflag;
 };
 static SweepWs sweep_ws(const sqb_sketch* sk, int code, int64_t m, int64_t ncol) {
   SweepWs w;
@@ -44,6 +44,8 @@ static SweepWs sweep_ws(const sqb_sketch* sk, int code, int64_t m, int64_t ncol)
   w.ifs = w.plan.add(sizeof(double) * 2);
   w.iP = w.plan.add(std::max(sketch_partials_bytes(sk, code, w.chunk), sketch_partials_bytes(sk, code, 1)));
   w.iPS = w.plan.add(code == SQB_F64 ? persist_ws_bytes(sk, m) : 0);
+  // per-block pass-completion flags of the column pass (tiles of >= 512 rows + identity block + helper)
+  w.iflag = w.plan.add(sizeof(int) * (size_t)((std::max<int64_t>(sk->n, 1) >> 9) + 8));
   return w;
 }
 size_t left_sweep_ws_bytes(const sqb_sketch* sk, int code, int64_t m, int64_t ncol) {
@@ -84,8 +86,16 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
   double* fs = reinterpret_cast<double*>(wb + plan.offs[ifs]);
   void* P = wb + plan.offs[iP];
   Status* st = ctx->d_status;
+  // cross-pass overlap (ColArgs::tflag): on for passes of many blocks; a small
+  // sweep (config 1: 34 blocks) is a latency chain in which the extra fence +
+  // flag store at every block's exit costs ~1 us per column (0.47 -> 0.50 ms)
+  const int early = early_env();
+  int* tflag = (early == 2 || (early == 1 && n >= (int64_t(1) << 19)))
+                   ? reinterpret_cast<int*>(wb + plan.offs[sw.iflag]) : nullptr;
 
   SQB_TRY(zero2d(ctx, Tm, ncol, ncol, ldt));
+  if (tflag)
+    SQB_CUDA_TRY(cudaMemsetAsync(tflag, 0, sizeof(int) * (size_t)((std::max<int64_t>(sk->n, 1) >> 9) + 8), ctx->stream));
   // raw sketches y0 = Psi W (rhqr.py:240 for every column).  Pass c and step
   // c read y0_{c+1}; with a streamed input (host_pipe.cu) the columns arrive
   // in groups and each group is sketched as soon as it is resident.
@@ -141,6 +151,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
   sa.log_tb = g.log_tb; sa.norm_lo = norm_lo; sa.y = Y0; sa.Y0 = Y0; sa.S = S; sa.lds = lds;
   sa.R = R; sa.ldr = ldr; sa.U = U; sa.ldu = ldu; sa.sigmas = sigmas; sa.rhos = rhos; sa.betas = betas;
   sa.fscale = fs; sa.vbuf = vbuf; sa.anext = abuf + (m + 1); sa.clast = coef; sa.st = st;
+  sa.early = tflag ? 1 : 0;
   SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT),
                      step_smem, sa));
 
@@ -182,10 +193,12 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
     ca.scaling = scaling; ca.srht = srht ? 1 : 0; ca.bits = srht ? sk->sign_bits : nullptr;
     ca.idx = srht ? sk->indices : nullptr; ca.scale_lo = scale_lo; ca.P = P; ca.y = y;
     ca.S = S; ca.lds = lds; ca.T = Tm; ca.ldt = ldt; ca.Y0 = Y0; ca.vprev = vbuf; ca.betas = betas;
-    ca.anext = a_nxt; ca.st = st;
+    ca.anext = a_nxt; ca.st = st; ca.tflag = tflag;
+    ca.dbg = (c == ctx->dbg_ccol) ? ctx->dbg_cts : nullptr;
     ca.helper_first = helper_first_default();
     ca.no_p16 = no_p16_env();
     ca.no_pre = no_pre_env();
+    ca.no_part = no_part_env();
     const size_t smem = sizeof(A) * ((c + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(c + 1));
     prof_begin(ctx);
     SQB_TRY(launch_pdl(ctx, "rhqr_col_kernel", colk, dim3((unsigned)(n_eff_col + 2)), dim3(COL_NT), smem,
@@ -199,6 +212,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
     sa.c = (int)c;
     sa.y = y;
     sa.dbg = (c == ctx->dbg_col) ? ctx->dbg_ts : nullptr;
+    sa.gdbg = (c == ctx->dbg_ccol && ctx->dbg_cts) ? ctx->dbg_cts + 8 * (n_eff_col + 2) : nullptr;
     sa.anext = a_nxt;
     sa.tree = srht ? 1 : 0;
     sa.n_tiles = gc.n_tiles; sa.n_eff = gc.n_eff; sa.log_tb = gc.log_tb;

@@ -197,3 +197,37 @@ def test_packed16_tile_fwht_is_bitwise(P, monkeypatch, tag, N, m, ell):
     F2 = P.rhqr_left(W, om, policy=pol)
     for k in ("U", "S", "T", "R"):
         assert np.array_equal(getattr(F1, k), getattr(F2, k)), k
+
+
+# ------------------------------------------------------------ cross-pass overlap, partial tile
+@pytest.mark.parametrize("tag,N,m,ell", [
+    ("double", (1 << 19) + 4096 + 24, 24, 64),    # partial last tile of whole 16-byte runs, many tiles
+    ("double", (1 << 19) + 1003, 24, 64),         # ragged partial tile (generic loop)
+    ("bf16", (1 << 20) + 2048 + 32, 32, 96),      # 16-bit storage, 3-CTA/SM ring variant
+    ("single", (1 << 19) + 8 + 16, 16, 48),
+])
+def test_column_pass_overlap_and_partial_tile_are_bitwise(P, monkeypatch, tag, N, m, ell):
+    """The device-resident sweep with the cross-pass overlap (per-block flags,
+    step kernel triggering its dependents early: SQB_EARLY=2 forces it, 0 is
+    the plain PDL order) and with the pipelined partial last tile (SQB_NO_PART=1
+    restores the generic loop) must give bitwise the same factors: same
+    operations in the same order, only scheduled differently
+    (rhqr.py:236-250)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(N)
+    W = torch.randn(m, N, generator=g, device="cuda", dtype=torch.float64).t() * torch.logspace(
+        0, -3, m, dtype=torch.float64, device="cuda")
+    om = P.SRHTSketch(ell, N - m, 5)
+    pol = P.PrecisionPolicy("double", tag)
+    out = {}
+    for early, nopart in (("2", "0"), ("0", "0"), ("2", "1"), ("0", "1")):
+        monkeypatch.setenv("SQB_EARLY", early)
+        monkeypatch.setenv("SQB_NO_PART", nopart)
+        for rep in range(2):  # the overlap is a race if it is wrong: run it twice
+            F = P.rhqr_left(W, om, policy=pol)
+            cur = {k: getattr(F, k).clone() for k in ("U", "S", "T", "R")}
+            if not out:
+                out = cur
+            for k in out:
+                assert torch.equal(out[k], cur[k]), (k, early, nopart, rep)
+    assert float(torch.linalg.norm(out["R"])) > 0

@@ -30,6 +30,7 @@ namespace sqb {
 constexpr int PS_NT = 512;   // = STEP_NT: phase B's block reductions are the step kernel's
 constexpr int PS_LOG = 9;    // 512-row tiles (the launch-chain path's small-problem geometry)
 constexpr int PS_TB = 1 << PS_LOG;
+constexpr int PS_TILE = 0, PS_TOP = 1, PS_TCTA = 2;  // CTA roles of the fast-step kernel
 static_assert(PS_NT == STEP_NT, "phase B replays the step kernel's 512-thread reductions");
 
 struct PersistArgs {
@@ -51,6 +52,8 @@ struct PersistArgs {
   double* abuf;         // [2][m + 1]  a_{c+1} (helper)
   double* vbuf;         // [m + 1]     v_c
   unsigned* bar;        // grid-barrier counter (zeroed before launch)
+  double* gbuf;         // [2][od]  fast step: g_{c+1} = y0_{c+1} - S_c a_{c+1} (top CTA, phase A)
+  int fast;             // 1: single-reduction step (ps_step_fast), not bitwise the launch chain
   int stage_leaves;     // 1: phase B copies the leaves to shared memory first
   long long* dbg;       // optional globaltimer stamps [m][2][16] (instrumentation)
   Status* st;
@@ -97,12 +100,13 @@ struct PsSmem {
   double* sc;     // [m]          a_c
   double* red;    // [STEP_CL][32]
   double* scal;   // [8]
+  double* an;     // [m + 1]      top CTA, fast step: a_{c+1}
   double* lvs;    // [ell][n_tiles] staged leaves (stage_leaves)
 };
 
 __host__ __device__ inline size_t ps_base_doubles(int m, int od) {
   return (size_t)m * PS_TB + (PS_TB + (PS_TB >> Pad<double>::shift) + 1) + (size_t)m * od + 3 * (size_t)od +
-         STEP_CL * (size_t)(m + 1) + m + STEP_CL * 32 + 8;
+         STEP_CL * (size_t)(m + 1) + m + STEP_CL * 32 + 8 + (size_t)(m + 2);
 }
 
 __device__ inline PsSmem ps_carve(unsigned char* raw, int m, int od) {
@@ -120,6 +124,7 @@ __device__ inline PsSmem ps_carve(unsigned char* raw, int m, int od) {
   s.sc = p; p += m;
   s.red = p; p += STEP_CL * 32;
   s.scal = p; p += 8;
+  s.an = p; p += m + 2;
   s.lvs = p;
   return s;
 }
@@ -196,21 +201,54 @@ __device__ __forceinline__ double thread_subtree(const double* lv, int t0, int q
 }
 
 // ---------------------------------------------------------------------------
-// Phase B: the step of column c, replaying rhqr_step_kernel (8 CTAs x 512
-// threads, rows split in STEP_CL blocks of step_rows(od)) bit for bit.
-// Column 0 takes y = Y0[:, 0]; later columns the identity rows from ytop and
-// the Omega rows from the tile leaves.  Returns false on breakdown (uniform).
+// The sketch y of w_c in shared memory (s.yv): column 0 takes Y0[:, 0]; later
+// columns the identity rows from ytop and the Omega rows from the tile leaves
+// (the SRHT tree, the launch chain's operations in the launch chain's order).
+// Ends with a block barrier.
 // ---------------------------------------------------------------------------
-__device__ bool ps_step(const PersistArgs& a, const PsSmem& s, int c, bool top_cta, double* f_out,
-                        double* clast_out) {
+__device__ void ps_y_rows(const PersistArgs& a, const PsSmem& s, int c, bool top_cta) {
   const int m = a.m, od = a.od, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int pv = c;
-  const int B = step_rows(od);
-  const bool has_next = c + 1 < m;
-  const double* anext = a.abuf + ((c + 1) & 1) * (m + 1);
-  double an = 0.0;  // a_{c+1}[tid] (helper of pass c), loaded with the leaves
-  if (has_next && tid < c) an = __ldcg(anext + tid);
-  // ---- y rows
+  if (c > 0 && a.n_tiles == 32 && a.ell * 4 <= PS_NT && a.ell % 8 == 0) {
+    // 32 tiles (config 1), four lanes per output: each lane loads its 8
+    // leaves straight into registers (one coalesced 2 KB run per warp, a
+    // single L2 round trip) and folds them, then the top two levels go
+    // across the lane quad — thread_subtree's operations and order without
+    // the staging pass through shared memory
+    const double* yt = a.ytop + (c & 1) * m;
+    double ytv = 0.0;
+    if (tid < m) ytv = __ldcg(yt + tid);
+    const double* lv = a.leaves + (int64_t)(c & 1) * a.ell * 32;
+    const int o = tid >> 2, j = tid & 3, ne = (int)a.n_eff;
+    PS_STAMP(c, 5);
+    if (o < a.ell) {
+      const int64_t rhi = __ldg(a.idx + o) >> PS_LOG;
+      const double2* p = reinterpret_cast<const double2*>(lv + (size_t)o * 32 + j * 8);
+      const double2 q0 = __ldcg(p), q1 = __ldcg(p + 1), q2 = __ldcg(p + 2), q3 = __ldcg(p + 3);
+      double v[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (j * 8 + t >= ne) v[t] = 0.0;
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        const bool neg = (rhi >> l) & 1;
+#pragma unroll
+        for (int t = 0; t < 8; t += (2 << l))
+          v[t] = neg ? __dsub_rn(v[t], v[t + (1 << l)]) : __dadd_rn(v[t], v[t + (1 << l)]);
+      }
+      double x = v[0];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double ot = __shfl_xor_sync(0xffffffffu, x, 1 << h, 4);
+        const bool upper = (j >> h) & 1;
+        const double lf = upper ? ot : x, rt = upper ? x : ot;
+        x = ((rhi >> (3 + h)) & 1) ? __dsub_rn(lf, rt) : __dadd_rn(lf, rt);
+      }
+      if (j == 0) s.yv[m + o] = __dmul_rn(x, a.norm_lo);
+    }
+    if (tid < m) s.yv[tid] = ytv;
+    __syncthreads();
+    return;
+  }
   if (c == 0) {
     for (int r = tid; r < od; r += PS_NT) s.yv[r] = __ldg(a.Y0 + r);
   } else {
@@ -276,6 +314,24 @@ __device__ bool ps_step(const PersistArgs& a, const PsSmem& s, int c, bool top_c
     }
   }
   __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Phase B: the step of column c, replaying rhqr_step_kernel (8 CTAs x 512
+// threads, rows split in STEP_CL blocks of step_rows(od)) bit for bit.
+// Column 0 takes y = Y0[:, 0]; later columns the identity rows from ytop and
+// the Omega rows from the tile leaves.  Returns false on breakdown (uniform).
+// ---------------------------------------------------------------------------
+__device__ bool ps_step(const PersistArgs& a, const PsSmem& s, int c, bool top_cta, double* f_out,
+                        double* clast_out) {
+  const int m = a.m, od = a.od, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pv = c;
+  const int B = step_rows(od);
+  const bool has_next = c + 1 < m;
+  const double* anext = a.abuf + ((c + 1) & 1) * (m + 1);
+  double an = 0.0;  // a_{c+1}[tid] (helper of pass c), loaded with the leaves
+  if (has_next && tid < c) an = __ldcg(anext + tid);
+  ps_y_rows(a, s, c, top_cta);
   PS_STAMP(c, 4);
   // ---- rho^2: per virtual CTA q, block_sum over its 512 threads, then q order
   {
@@ -398,11 +454,151 @@ __device__ bool ps_step(const PersistArgs& a, const PsSmem& s, int c, bool top_c
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Fast step (PersistArgs::fast): the critical path from the sketch y of w_c to
+// the two scalars the next column pass needs is ONE block reduction.  With
+//     g_{c+1} = y0_{c+1} - S_c a_{c+1}           (top CTA, during phase A)
+// the last coefficient of rhqr.py:241 is
+//     coef_{c+1}[c] = beta_c (s_c^t y0_{c+1} - v_c^t a_{c+1}) = beta_c s_c^t g_{c+1},
+// and s_c = f (0, .., 0, gamma, y[c+1:]) (rhqr.py:83-96), so
+//     rho^2 = sum_{r >= c} y_r^2   and   t = sum_{r > c} y_r g_r
+// are reduced together, every thread derives rho, gamma, beta, f and the
+// coefficient from them, and s_c, S's column, v_c = S_c^t s_c, T's column,
+// a_{c+2} and g_{c+2} leave the critical path (ps_top_post, helper).  The
+// same mathematics as the launch chain in a different association (not
+// bitwise; tests/test_gpu_persist.py holds it to the oracle).
+// ---------------------------------------------------------------------------
+__device__ bool ps_step_fast(const PersistArgs& a, const PsSmem& s, int c, int role, double* f_out,
+                             double* clast_out) {
+  const int m = a.m, od = a.od, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool top_cta = role == PS_TOP;  // PS_STAMP
+  const int pv = c;
+  const bool has_next = c + 1 < m;
+  const double* gsrc = c == 0 ? a.Y0 + od : a.gbuf + (size_t)((c + 1) & 1) * od;  // g_1 = y0_1
+  double g0 = 0.0, g1 = 0.0;  // rows tid, tid + PS_NT (od <= 2 PS_NT)
+  if (has_next) {
+    if (tid < od) g0 = __ldcg(gsrc + tid);
+    if (tid + PS_NT < od) g1 = __ldcg(gsrc + tid + PS_NT);
+  }
+  ps_y_rows(a, s, c, top_cta);
+  PS_STAMP(c, 4);
+  double p1 = 0.0, p2 = 0.0;
+  if (tid < od && tid >= pv) {
+    const double y = s.yv[tid];
+    p1 = y * y;
+    if (tid > pv) p2 = y * g0;
+  }
+  if (tid + PS_NT < od) {  // rows past 512 are always below the pivot (pv < m <= 64)
+    const double y = s.yv[tid + PS_NT];
+    p1 = fma(y, y, p1);
+    p2 = fma(y, g1, p2);
+  }
+  p1 = warp_sum(p1);
+  p2 = warp_sum(p2);
+  if (lane == 0) { s.red[warp] = p1; s.red[32 + warp] = p2; }
+  if (tid == pv) s.red[64] = g0;
+  __syncthreads();
+  double r2 = 0.0, t = 0.0;
+#pragma unroll
+  for (int w = 0; w < PS_NT / 32; ++w) { r2 += s.red[w]; t += s.red[32 + w]; }
+  const double gpv = s.red[64];
+  PS_STAMP(c, 7);
+  // rh_vector's scalars (rhqr.py:71-94), by every thread
+  const double rho = sqrt(r2);
+  const double yc = s.yv[pv];
+  const double sigma = yc >= 0.0 ? 1.0 : -1.0;
+  const double gamma = __dadd_rn(yc, sigma * rho);
+  const double beta = __ddiv_rn(1.0, __dmul_rn(__dmul_rn(rho, sigma), gamma));
+  const bool bad = rho == 0.0 || !isfinite(beta);
+  const bool sq = a.scaling == SQB_SCALE_SQRT2;
+  double f, bo, sg;
+  if (sq) { f = __dsqrt_rn(beta); bo = 1.0; sg = f * fma(gamma, gpv, t); }  // s = f yhat
+  else { f = gamma; bo = __ddiv_rn(__dmul_rn(sigma, gamma), rho); sg = gpv + t / gamma; }  // s = yhat / gamma
+  if (tid == 0) {
+    if (bad && role == PS_TCTA) fail(a.st, SQB_ERR_BREAKDOWN, pv + 1, rho == 0.0 ? 0.0 : rho);
+    s.scal[0] = -sigma * rho; s.scal[1] = gamma; s.scal[2] = f; s.scal[3] = bo;
+    if (role == PS_TCTA && !bad) { a.sigmas[c] = sigma; a.rhos[c] = rho; a.betas[c] = bo; s.sb[c] = bo; }
+  }
+  *f_out = f;
+  *clast_out = has_next ? bo * sg : 0.0;
+  PS_STAMP(c, 8);
+  return !bad;
+}
+
+// T CTA, after the fast step of column c: s_c = Psi u_c, S's column, the
+// identity-block rows of U, R's column (rhqr.py:83-96, :248-249) and
+// v_c = S_c^t s_c (the _extend_t product, :138), all from shared memory
+__device__ void ps_t_post(const PersistArgs& a, const PsSmem& s, int c) {
+  const int m = a.m, od = a.od, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pv = c;
+  __syncthreads();  // s.scal written by thread 0 of the step
+  const double rdiag = s.scal[0], gamma = s.scal[1], f = s.scal[2];
+  const bool sq = a.scaling == SQB_SCALE_SQRT2;
+  double* Sc = s.Ss + (size_t)c * od;
+  for (int row = tid; row < od; row += PS_NT) {
+    const double yh = row < pv ? 0.0 : (row == pv ? gamma : s.yv[row]);
+    const double sval = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
+    s.sv[row] = sval;
+    Sc[row] = sval;
+    a.S[row + (int64_t)c * a.lds] = sval;
+    if (row < m) {
+      a.U[row + (int64_t)c * a.ldu] = sval;
+      s.Utop[row + (size_t)c * m] = sval;
+      a.R[row + (int64_t)c * a.ldr] = row < pv ? s.yv[row] : (row == pv ? rdiag : 0.0);
+    }
+  }
+  __syncthreads();
+  for (int k = warp; k < c; k += PS_NT / 32) {
+    const double* col = s.Ss + (size_t)k * od;
+    double d0 = 0.0, d1 = 0.0;
+    int r = pv + lane;
+    for (; r + 32 < od; r += 64) {
+      d0 = fma(col[r], s.sv[r], d0);
+      d1 = fma(col[r + 32], s.sv[r + 32], d1);
+    }
+    if (r < od) d0 = fma(col[r], s.sv[r], d0);
+    const double d = warp_sum(d0 + d1);
+    if (lane == 0) { s.vs[k] = d; a.vbuf[k] = d; }
+  }
+  __syncthreads();
+}
+
 // T column kk of the top CTA's shared copy -> global T
 __device__ inline void ps_copy_t_column(const PersistArgs& a, const PsSmem& s, int kk) {
   __syncthreads();
   for (int i = threadIdx.x; i <= kk; i += PS_NT) a.T[i + (int64_t)kk * a.ldt] = s.Ts[i + (size_t)kk * a.m];
 }
+
+// phase A of a tile CTA: the column pass of column c on its 512 rows held in
+// shared memory (rhqr_col_kernel's operations in its order), SRHT leaves out
+__device__ void ps_tile_pass(const PersistArgs& a, const PsSmem& s, int c, int64_t g, int rows, int64_t ro,
+                             int64_t e0, double f_prev, double clast) {
+  const int tid = threadIdx.x;
+  double* tb = s.tile;
+  for (int r = tid; r < PS_TB; r += PS_NT) {
+    double w = 0.0;
+    if (r < rows) {
+      // final columns 0 .. c-2, one fma chain per row (rhqr_col_kernel order)
+      double acc = 0.0;
+      for (int k = 0; k < c - 1; ++k) acc = fma(s.Ut[(size_t)k * PS_TB + r], s.sc[k], acc);
+      // column c-1: lazy scaling of the stored w_{c-1} (rhqr.py:86-95)
+      double x = lazy_scale<double>(s.Ut[(size_t)(c - 1) * PS_TB + r], f_prev, a.scaling);
+      s.Ut[(size_t)(c - 1) * PS_TB + r] = x;
+      a.U[ro + r + (int64_t)(c - 1) * a.ldu] = x;
+      acc = fma(x, clast, acc);
+      w = __dsub_rn(s.Ut[(size_t)c * PS_TB + r], acc);
+      s.Ut[(size_t)c * PS_TB + r] = w;
+    }
+    const int64_t e = e0 + r;
+    tb[pidx<double>(r)] = r < rows ? srht_in<double>(w, a.scale_lo, sign_neg(a.bits, e)) : 0.0;
+  }
+  __syncthreads();
+  tile_fwht<double>(tb, PS_LOG);
+  tile_gather<double>(tb, a.idx, a.ell, PS_LOG, a.leaves + (int64_t)(c & 1) * a.ell * a.n_tiles + g,
+                      a.n_tiles);
+}
+
+__device__ void ps_identity_rows(const PersistArgs& a, const PsSmem& s, int c, double clast);
 
 __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_kernel(PersistArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -437,46 +633,9 @@ __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_kernel(PersistArgs a) {
       for (int r = tid; r < od; r += PS_NT) s.y0s[r] = __ldg(a.Y0 + (int64_t)(c + 1) * od + r);
     __syncthreads();
     if (!top_cta) {
-      double* tb = s.tile;
-      for (int r = tid; r < PS_TB; r += PS_NT) {
-        double w = 0.0;
-        if (r < rows) {
-          // final columns 0 .. c-2, one fma chain per row (rhqr_col_kernel order)
-          double acc = 0.0;
-          for (int k = 0; k < c - 1; ++k) acc = fma(s.Ut[(size_t)k * PS_TB + r], s.sc[k], acc);
-          // column c-1: lazy scaling of the stored w_{c-1} (rhqr.py:86-95)
-          double x = lazy_scale<double>(s.Ut[(size_t)(c - 1) * PS_TB + r], f_prev, a.scaling);
-          s.Ut[(size_t)(c - 1) * PS_TB + r] = x;
-          a.U[ro + r + (int64_t)(c - 1) * a.ldu] = x;
-          acc = fma(x, clast, acc);
-          w = __dsub_rn(s.Ut[(size_t)c * PS_TB + r], acc);
-          s.Ut[(size_t)c * PS_TB + r] = w;
-        }
-        const int64_t e = e0 + r;
-        tb[pidx<double>(r)] = r < rows ? srht_in<double>(w, a.scale_lo, sign_neg(a.bits, e)) : 0.0;
-      }
-      __syncthreads();
-      tile_fwht<double>(tb, PS_LOG);
-      tile_gather<double>(tb, a.idx, a.ell, PS_LOG, a.leaves + (int64_t)(c & 1) * a.ell * a.n_tiles + g,
-                          a.n_tiles);
+      ps_tile_pass(a, s, c, g, rows, ro, e0, f_prev, clast);
     } else {
-      // identity block y[r] = w_c[r], r < m (col_top_block's accumulation order)
-      double* yt = a.ytop + (c & 1) * m;
-      for (int r = tid; r < m; r += PS_NT) {
-        const double* ur = s.Utop + r;
-        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-        int k = 0;
-        for (; k + 4 <= c - 1; k += 4) {
-          acc0 = fma(ur[(size_t)k * m], s.sc[k], acc0);
-          acc1 = fma(ur[(size_t)(k + 1) * m], s.sc[k + 1], acc1);
-          acc2 = fma(ur[(size_t)(k + 2) * m], s.sc[k + 2], acc2);
-          acc3 = fma(ur[(size_t)(k + 3) * m], s.sc[k + 3], acc3);
-        }
-        for (; k < c - 1; ++k) acc0 = fma(ur[(size_t)k * m], s.sc[k], acc0);
-        const double acc = (acc0 + acc1) + (acc2 + acc3);
-        const double dot = fma(ur[(size_t)(c - 1) * m], clast, acc);
-        yt[r] = __dsub_rn(__ldg(a.W + r + (int64_t)c * a.ldw), dot);
-      }
+      ps_identity_rows(a, s, c, clast);
       // helper (col_helper) on the shared copies: T column c-1, then
       // a_{c+1} = T_c^t (S_c^t y0_{c+1})
       ColArgs h{};
@@ -511,24 +670,159 @@ __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_kernel(PersistArgs a) {
   }
 }
 
+// top CTA of the fast-step kernel, after the step of column c: apply reflector
+// c to the sketches of the columns still ahead — G_j <- G_j - alpha_j s_c with
+// alpha_j = beta_c s_c^t G_j = a_j[c] (rhqr.py:241 expanded column by column,
+// see ps_step_fast) — so that a_{c+2} and g_{c+2} are ready before the next
+// barrier without T on the path.  G lives in s.Ss, the a_j in s.Ts ([j][m]).
+__device__ void ps_top_update(const PersistArgs& a, const PsSmem& s, int c) {
+  const int m = a.m, od = a.od, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pv = c;
+  __syncthreads();  // s.scal written by thread 0 of the step
+  const double gamma = s.scal[1], f = s.scal[2], bo = s.scal[3];
+  const bool sq = a.scaling == SQB_SCALE_SQRT2;
+  for (int row = tid; row < od; row += PS_NT) {
+    const double yh = row < pv ? 0.0 : (row == pv ? gamma : s.yv[row]);
+    const double sval = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
+    s.sv[row] = sval;
+    if (row < m) s.Utop[row + (size_t)c * m] = sval;
+  }
+  __syncthreads();
+  for (int j = c + 2 + warp; j < m; j += PS_NT / 32) {
+    double* Gj = s.Ss + (size_t)j * od;
+    double d0 = 0.0, d1 = 0.0;
+    int r = pv + lane;
+    for (; r + 32 < od; r += 64) {
+      d0 = fma(Gj[r], s.sv[r], d0);
+      d1 = fma(Gj[r + 32], s.sv[r + 32], d1);
+    }
+    if (r < od) d0 = fma(Gj[r], s.sv[r], d0);
+    const double alpha = bo * warp_sum(d0 + d1);
+    for (r = pv + lane; r < od; r += 32) Gj[r] = fma(-alpha, s.sv[r], Gj[r]);
+    if (lane == 0) s.Ts[(size_t)j * m + c] = alpha;
+  }
+  __syncthreads();
+}
+
+// identity block y[r] = w_c[r], r < m (col_top_block's accumulation order)
+__device__ void ps_identity_rows(const PersistArgs& a, const PsSmem& s, int c, double clast) {
+  const int m = a.m, tid = threadIdx.x;
+  double* yt = a.ytop + (c & 1) * m;
+  for (int r = tid; r < m; r += PS_NT) {
+    const double* ur = s.Utop + r;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    int k = 0;
+    for (; k + 4 <= c - 1; k += 4) {
+      acc0 = fma(ur[(size_t)k * m], s.sc[k], acc0);
+      acc1 = fma(ur[(size_t)(k + 1) * m], s.sc[k + 1], acc1);
+      acc2 = fma(ur[(size_t)(k + 2) * m], s.sc[k + 2], acc2);
+      acc3 = fma(ur[(size_t)(k + 3) * m], s.sc[k + 3], acc3);
+    }
+    for (; k < c - 1; ++k) acc0 = fma(ur[(size_t)k * m], s.sc[k], acc0);
+    const double acc = (acc0 + acc1) + (acc2 + acc3);
+    const double dot = fma(ur[(size_t)(c - 1) * m], clast, acc);
+    yt[r] = __dsub_rn(__ldg(a.W + r + (int64_t)c * a.ldw), dot);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The fast-step persistent kernel (SQB_PERSIST=2): tile CTAs as in
+// rhqr_persist_kernel; the TOP CTA owns the identity rows and the sketches of
+// the columns ahead (ps_top_update) — everything the next barrier waits for;
+// the T CTA writes the sketch-space outputs (S, R, U's identity rows, scalars)
+// and builds T by _extend_t (rhqr.py:135-140) with a whole column period to
+// do it.  Every CTA runs the single-reduction step (ps_step_fast).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_fast_kernel(PersistArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int m = a.m, od = a.od, tid = threadIdx.x;
+  const PsSmem s = ps_carve(smem_raw, m, od);
+  const int64_t g = blockIdx.x;
+  const int role = g < a.n_eff ? PS_TILE : (g == a.n_eff ? PS_TOP : PS_TCTA);
+  const bool top_cta = role == PS_TOP;  // PS_STAMP
+  const unsigned G = gridDim.x;
+  if (failed(a.st)) return;  // uniform: written before this kernel
+  const int64_t e0 = g << PS_LOG;
+  const int rows = role != PS_TILE ? 0 : (int)(a.n - e0 < PS_TB ? a.n - e0 : (int64_t)PS_TB);
+  const int64_t ro = (int64_t)m + e0;
+  if (role == PS_TILE) {
+    for (int k = 0; k < m; ++k)
+      for (int r = tid; r < rows; r += PS_NT) s.Ut[(size_t)k * PS_TB + r] = __ldg(a.W + ro + r + (int64_t)k * a.ldw);
+  } else {
+    for (int e = tid; e < m * m; e += PS_NT) s.Ts[e] = 0.0;
+    if (role == PS_TOP)  // G_j = y0_j
+      for (int e = tid; e < m * od; e += PS_NT) s.Ss[e] = __ldg(a.Y0 + e);
+  }
+  __syncthreads();
+  double f_prev = 0.0, clast = 0.0;
+  if (!ps_step_fast(a, s, 0, role, &f_prev, &clast)) return;
+  unsigned nbar = 0;
+  for (int c = 1; c < m; ++c) {
+    PS_STAMP(c, 0);
+    if (role != PS_TCTA) {
+      const double* acur = a.abuf + (c & 1) * (m + 1);
+      for (int k = tid; k < c - 1; k += PS_NT) s.sc[k] = __ldcg(acur + k);
+    }
+    if (role == PS_TOP) ps_top_update(a, s, c - 1);
+    if (role == PS_TCTA) {
+      ps_t_post(a, s, c - 1);
+      complete_t_column(s.Ts, m, c - 1, s.vs, s.sb[c - 1]);
+      ps_copy_t_column(a, s, c - 1);
+    }
+    __syncthreads();
+    if (role == PS_TILE) {
+      ps_tile_pass(a, s, c, g, rows, ro, e0, f_prev, clast);
+    } else if (role == PS_TOP) {
+      ps_identity_rows(a, s, c, clast);
+      if (c + 1 < m) {
+        double* gd = a.gbuf + (size_t)((c + 1) & 1) * od;
+        const double* Gn = s.Ss + (size_t)(c + 1) * od;
+        for (int r = tid; r < od; r += PS_NT) gd[r] = Gn[r];
+        double* ag = a.abuf + ((c + 1) & 1) * (m + 1);
+        for (int k = tid; k < c; k += PS_NT) ag[k] = s.Ts[(size_t)(c + 1) * m + k];
+      }
+    }
+    PS_STAMP(c, 1);
+    grid_barrier(a.bar, ++nbar * G);
+    PS_STAMP(c, 2);
+    double f = 0.0, cl = 0.0;
+    if (!ps_step_fast(a, s, c, role, &f, &cl)) return;
+    f_prev = f;
+    clast = cl;
+    PS_STAMP(c, 3);
+  }
+  if (role == PS_TILE) {
+    for (int r = tid; r < rows; r += PS_NT)
+      a.U[ro + r + (int64_t)(m - 1) * a.ldu] =
+          lazy_scale<double>(s.Ut[(size_t)(m - 1) * PS_TB + r], f_prev, a.scaling);
+  } else if (role == PS_TCTA) {
+    ps_t_post(a, s, m - 1);
+    complete_t_column(s.Ts, m, m - 1, s.vs, s.sb[m - 1]);
+    ps_copy_t_column(a, s, m - 1);
+  }
+}
+
 // host side ------------------------------------------------------------------
 size_t persist_ws_bytes(const sqb_sketch* sk, int64_t m) {
   if (sk->kind != SQB_SKETCH_SRHT || sk->n_pad > (int64_t(1) << 16)) return 0;
-  return sizeof(double) * (2 * (size_t)sk->ell * (size_t)(sk->n_pad >> PS_LOG) + 2 * (size_t)m) + 256;
+  return sizeof(double) * (2 * (size_t)sk->ell * (size_t)(sk->n_pad >> PS_LOG) + 2 * (size_t)m +
+                           2 * (size_t)(m + sk->ell)) + 256;
 }
 
 // nonzero if the persistent kernel can run this sweep (fp64 SRHT, small n_pad,
 // every CTA co-resident, W/U/S rows of a CTA in shared memory)
 bool persist_eligible(sqb_ctx* ctx, const sqb_sketch* sk, int64_t N, int64_t m, int64_t ncol, int64_t off) {
-  // opt-in (SQB_PERSIST=1, read per call so tests can toggle it): measured at
-  // parity with the launch chain on config 1, not the default
+  // SQB_PERSIST (read per call so tests can toggle it): unset / 2 = the
+  // fast-step kernel (default: config 1 0.43 -> 0.24 ms), 1 = the kernel that
+  // is bitwise the launch chain (at parity with it), 0 = the launch chain
   const char* ev = getenv("SQB_PERSIST");
-  const bool off_env = !(ev && ev[0] == '1');
+  const bool off_env = ev && ev[0] == '0';
   if (off_env || off != 0 || ncol != m || sk->kind != SQB_SKETCH_SRHT) return false;
   if (sk->n_pad > (int64_t(1) << 16) || sk->n_pad < PS_TB || m < 2 || m > 64) return false;
+  if (m + sk->ell > 2 * PS_NT) return false;
   const int64_t n = N - m, od = m + sk->ell;
   const int64_t n_eff = (n + PS_TB - 1) / PS_TB;
-  if (n_eff + 1 > ctx->sm_count) return false;
+  if (n_eff + 2 > ctx->sm_count) return false;
   if (sizeof(double) * ps_base_doubles((int)m, (int)od) + 64 > 227 * 1024) return false;
   if (2 * m * m + 2 * m + 1 > m * PS_TB) return false;
   return true;
@@ -547,7 +841,12 @@ int launch_persist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const double
   char* p = static_cast<char*>(pws);
   a.leaves = reinterpret_cast<double*>(p);
   a.ytop = a.leaves + 2 * (size_t)a.ell * a.n_tiles;
-  a.bar = reinterpret_cast<unsigned*>(a.ytop + 2 * m);
+  a.gbuf = a.ytop + 2 * m;
+  a.bar = reinterpret_cast<unsigned*>(a.gbuf + 2 * (size_t)a.od);
+  {
+    const char* ev = getenv("SQB_PERSIST");
+    a.fast = (ev && ev[0] == '1') ? 0 : 1;
+  }
   a.abuf = abuf; a.vbuf = vbuf; a.st = ctx->d_status;
   SQB_CUDA_TRY(cudaMemsetAsync(a.bar, 0, 64, ctx->stream));
   size_t smem = sizeof(double) * ps_base_doubles((int)m, a.od) + 64;
@@ -555,9 +854,10 @@ int launch_persist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const double
   a.stage_leaves = smem + lv_bytes <= 227 * 1024 ? 1 : 0;
   if (a.stage_leaves) smem += lv_bytes;
   a.dbg = ctx->dbg_col == -2 ? ctx->dbg_ts : nullptr;
-  SQB_CUDA_TRY(cudaFuncSetAttribute(rhqr_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void (*kern)(PersistArgs) = a.fast ? rhqr_persist_fast_kernel : rhqr_persist_kernel;
+  SQB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(a.n_eff + 1));
+  cfg.gridDim = dim3((unsigned)(a.n_eff + (a.fast ? 2 : 1)));
   cfg.blockDim = dim3(PS_NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
@@ -566,7 +866,7 @@ int launch_persist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const double
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, rhqr_persist_kernel, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
   if (e != cudaSuccess) return set_cuda_error(ctx, e, "rhqr_persist_kernel", __FILE__, __LINE__);
   return check_launch(ctx, "rhqr_persist_kernel");
 }

@@ -7,7 +7,7 @@ import sys
 import numpy as np
 import torch
 
-os.environ.setdefault("SQB_PERSIST", "1")
+os.environ.setdefault("SQB_PERSIST", "2")
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2405_10923_b200 as P  # noqa: E402
@@ -40,6 +40,10 @@ for who, name in ((0, "tile CTA 0"), (1, "top CTA")):
           f"phaseB {np.median(B)/1e3:.2f} us, loop gap {np.median(gap)/1e3:.2f} us; "
           f"column period {np.median(np.diff(x[:, 0]))/1e3:.2f} us")
     d = lambda i, j: np.median(x[:, j] - x[:, i]) / 1e3  # noqa: E731
+    if os.environ["SQB_PERSIST"] == "2":
+        print(f"   phase B (fast step): pre-loads {d(2, 5):.2f}, leaves + trees {d(5, 4):.2f}, "
+              f"fused reduction {d(4, 7):.2f}, scalars {d(7, 8):.2f} us")
+        continue
     print(f"   phase B: pre-loads {d(2, 5):.2f}, leaf staging {d(5, 6):.2f}, trees {d(6, 4):.2f}, "
           f"rho reduction {d(4, 7):.2f}, scalars {d(7, 8):.2f}, s rows {d(8, 9):.2f}, "
           f"partial vectors {d(9, 10):.2f}, v/coef {d(10, 3):.2f} us")

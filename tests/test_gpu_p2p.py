@@ -50,10 +50,12 @@ def test_p2p_virtual_rec_rhqr_bitwise(P, nranks, m):
         assert np.array_equal(getattr(Fv, k), getattr(F1, k)), k
 
 
-def test_p2p_world1_ipc_path(P):
+def test_p2p_world1_ipc_path(P, monkeypatch):
     """sqb_p2p_mailbox / sqb_p2p_open through torch.distributed (world 1),
     then the row-partitioned factorizations over the mailboxes; repeated
-    calls reuse the monotone exchange sequence numbers."""
+    calls reuse the monotone exchange sequence numbers.  The bitwise twin of
+    the partitioned sweep is the single-GPU launch chain (SQB_PERSIST=0)."""
+    monkeypatch.setenv("SQB_PERSIST", "0")
     import torch.distributed as dist
     from paper_2405_10923_b200 import dist as D
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")

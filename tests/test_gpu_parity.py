@@ -517,10 +517,13 @@ def test_row_partitioned_arnoldi_bitwise(P, nranks):
     assert rel(xv, x1) < 1e-14
 
 
-def test_nccl_row_partitioned_single_rank(P):
+def test_nccl_row_partitioned_single_rank(P, monkeypatch):
     """Exercises the real NCCL plumbing of the row-partitioned path (dlopen,
-    unique id, communicator, per-column all-gather) with world_size 1."""
+    unique id, communicator, per-column all-gather) with world_size 1.  The
+    bitwise twin of the partitioned sweep is the single-GPU launch chain
+    (SQB_PERSIST=0), not the small-problem fast-step kernel."""
     import os
+    monkeypatch.setenv("SQB_PERSIST", "0")
     import torch.distributed as dist
     from paper_2405_10923_b200 import dist as D
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")

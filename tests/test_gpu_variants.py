@@ -112,7 +112,9 @@ def test_rhqr_block_against_oracle(P, N, m, bs, ell):
     assert fro < 1e-13
 
 
-@pytest.mark.parametrize("tag,tol", [("single", 1e-5), ("half", 3e-2), ("bf16", 1e-1)])
+# bar: 4 unit roundoffs of the storage format (measured on the B200,
+# scripts/probe_lowprec_bars.py: single 0.7-0.9 u, half bitwise, bf16 0.1-1.0 u)
+@pytest.mark.parametrize("tag,tol", [("single", 4 * 2.0 ** -24), ("half", 4 * 2.0 ** -11), ("bf16", 4 * 2.0 ** -8)])
 def test_rhqr_block_low_precision(P, tag, tol):
     # same bars as the rhqr_left mixed-precision parity (low-format GEMV
     # accumulation order differs from numpy's)
@@ -126,7 +128,7 @@ def test_rhqr_block_low_precision(P, tag, tol):
     assert np.array_equal(P.round_to(U, tag), U)
 
 
-@pytest.mark.parametrize("tag,tol", [("single", 1e-5), ("bf16", 1e-1)])
+@pytest.mark.parametrize("tag,tol", [("single", 4 * 2.0 ** -24), ("bf16", 4 * 2.0 ** -8)])
 def test_rhqr_right_low_precision(P, tag, tol):
     rng = np.random.default_rng(10)
     N, m = 8192, 12

@@ -247,6 +247,10 @@ class RHQRLeft(Workload):
         self.pol = pol
         self.alg = alg_bytes(Ng, m, self.b)  # whole job
         self.kernel = "rhqr_col_kernel (fused GEMV over U[:, :c] + lazy scale + SRHT leaves)"
+        if (not self.partitioned and self.tag == "double" and self.om.n_pad <= (1 << 16)
+                and os.environ.get("SQB_PERSIST", "2") != "0"):
+            self.kernel = ("rhqr_persist_fast_kernel (one cooperative grid for all columns: column pass on rows "
+                           "held in shared memory, SRHT leaves, one grid barrier and a single-reduction step per column)")
         self.config = {"workload": f"rhqr_left {self.name}: W {Ng} x {m} {self.tag}, SRHT ell={self.ell}",
                        "N": Ng, "N_per_gpu": self.N, "m": m, "ell": self.ell, "w_seed": CFG["w_seed"],
                        "sketch_seed": CFG["sketch_seed"],

@@ -123,6 +123,12 @@ int sqb_ctx_profile_read(sqb_ctx* ctx, double* total_ms, double* total_bytes, in
 /* Instrumentation: the step kernel of `column` writes per-phase clock64 stamps
  * (8 per cluster rank) to the device buffer dev_buf (NULL disables). */
 int sqb_debug_step_stamps(sqb_ctx* ctx, long long* dev_buf, int column);
+/* Instrumentation: stream trace.  While enabled an event is recorded after
+ * every kernel launch of the library on the context stream; trace_read
+ * synchronises and writes one line per kernel name, "name launches ms", the
+ * in-stream time (launch gap + run) summed over its launches. */
+int sqb_ctx_trace(sqb_ctx* ctx, int enable);
+int sqb_ctx_trace_read(sqb_ctx* ctx, char* buf, int64_t size);
 /* Instrumentation: every block b of the column pass of `column` writes
  * {SM id, globaltimer ns at entry, after the flag wait, after the bulk GEMV,
  * after griddepcontrol.wait, at exit} to dev_buf[8 b ..]; the step kernel of

@@ -56,6 +56,8 @@ _SIGS = {
     "sqb_ctx_profile": ([vp, C.c_int], C.c_int),
     "sqb_debug_step_stamps": ([vp, dp, C.c_int], C.c_int),
     "sqb_debug_col_stamps": ([vp, dp, C.c_int], C.c_int),
+    "sqb_ctx_trace": ([vp, C.c_int], C.c_int),
+    "sqb_ctx_trace_read": ([vp, C.c_char_p, i64], C.c_int),
     "sqb_ctx_profile_read": ([vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(i64)], C.c_int),
     "sqb_sketch_apply": ([vp, C.POINTER(SketchDesc), C.c_int, dp, i64, i64, dp, i64], C.c_int),
     "sqb_embedded_apply": ([vp, C.POINTER(SketchDesc), i64, C.c_int, dp, i64, i64, dp, i64], C.c_int),

@@ -169,6 +169,41 @@ int sqb_debug_step_stamps(sqb_ctx* ctx, long long* dev_buf, int column) {
   return SQB_OK;
 }
 
+int sqb_ctx_trace(sqb_ctx* ctx, int enable) {
+  if (!ctx) return SQB_ERR_ARG;
+  ctx->trace = enable != 0;
+  if (enable) {
+    ctx->trace_used = 0;
+    ctx->trace_name.clear();
+    trace_mark(ctx, "(start)");
+  }
+  return SQB_OK;
+}
+
+int sqb_ctx_trace_read(sqb_ctx* ctx, char* buf, int64_t size) {
+  SQB_TRY(prep(ctx));
+  SQB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  // per kernel name: launches, summed in-stream time (ms)
+  std::vector<const char*> names;
+  std::vector<double> ms;
+  std::vector<int64_t> cnt;
+  for (size_t i = 1; i < ctx->trace_used; ++i) {
+    float t = 0.f;
+    SQB_CUDA_TRY(cudaEventElapsedTime(&t, ctx->trace_ev[i - 1], ctx->trace_ev[i]));
+    size_t k = 0;
+    for (; k < names.size(); ++k)
+      if (strcmp(names[k], ctx->trace_name[i]) == 0) break;
+    if (k == names.size()) { names.push_back(ctx->trace_name[i]); ms.push_back(0.0); cnt.push_back(0); }
+    ms[k] += t;
+    cnt[k]++;
+  }
+  int64_t off = 0;
+  for (size_t k = 0; k < names.size() && off < size - 1; ++k)
+    off += snprintf(buf + off, (size_t)(size - off), "%s %lld %.6f\n", names[k], (long long)cnt[k], ms[k]);
+  if (size > 0) buf[std::min<int64_t>(off, size - 1)] = 0;
+  return SQB_OK;
+}
+
 int sqb_debug_col_stamps(sqb_ctx* ctx, long long* dev_buf, int column) {
   if (!ctx) return SQB_ERR_ARG;
   ctx->dbg_cts = dev_buf;

@@ -45,6 +45,12 @@ struct sqb_ctx {
   void* nccl = nullptr;
   long long* dbg_ts = nullptr;  // instrumentation: step-kernel phase stamps for column dbg_col
   int dbg_col = -1;
+  // stream trace (sqb_ctx_trace): an event after every launch, so consecutive
+  // deltas give each kernel's time in the stream as issued (gap + run)
+  bool trace = false;
+  std::vector<cudaEvent_t> trace_ev;
+  std::vector<const char*> trace_name;
+  size_t trace_used = 0;
   long long* dbg_cts = nullptr;  // instrumentation: column-pass block timeline of column dbg_ccol
   int dbg_ccol = -1;
   int nranks = 1;
@@ -138,8 +144,21 @@ inline void prof_end(sqb_ctx* ctx, double alg_bytes) {
   ctx->prof_bytes.push_back(alg_bytes);
 }
 
+inline void trace_mark(sqb_ctx* ctx, const char* what) {
+  if (ctx->trace_used >= ctx->trace_ev.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ctx->trace_ev.push_back(e);
+    }
+  }
+  cudaEventRecord(ctx->trace_ev[ctx->trace_used++], ctx->stream);
+  ctx->trace_name.push_back(what);
+}
+
 inline int check_launch(sqb_ctx* ctx, const char* what) {
   ctx->launches++;
+  if (ctx->trace) trace_mark(ctx, what);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(ctx, e, what, __FILE__, __LINE__);
   return SQB_OK;

@@ -45,6 +45,39 @@ __device__ __forceinline__ void gemv_rows(const T* __restrict__ U, int64_t ldu, 
       fm(x1, k + 1);
     }
     if (k < K) fm(x0, k);
+  } else if ((n - r0) % VN == 0) {
+    // partial last block made of whole 16-byte runs: the same pipeline with
+    // the runs past n masked (the generic loop below waits for every column
+    // before it issues the next one — one block then outlasts the others)
+    const int64_t rows = n - r0;
+    uint4 y0[NV], y1[NV];
+    auto ldp = [&](uint4 (&x)[NV], int k) {
+      const T* col = U + r0 + (int64_t)k * ldu;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int64_t i = (int64_t)(v * GEMV_NT + threadIdx.x) * VN;
+        x[v] = i < rows ? ldg_stream(col + i) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
+    auto fmp = [&](const uint4 (&x)[NV], int k) {
+      const A ck = c[k];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        A w[VN];
+        unpack16<T>(x[v], w);
+#pragma unroll
+        for (int j = 0; j < VN; ++j) acc[v][j] = fma(w[j], ck, acc[v][j]);
+      }
+    };
+    if (K > 0) ldp(y0, 0);
+    int k = 0;
+    for (; k + 2 <= K; k += 2) {
+      ldp(y1, k + 1);
+      fmp(y0, k);
+      if (k + 2 < K) ldp(y0, k + 2);
+      fmp(y1, k + 1);
+    }
+    if (k < K) fmp(y0, k);
   } else {
     for (int k = 0; k < K; ++k) {
       const T* col = U + r0 + (int64_t)k * ldu;

@@ -6,6 +6,7 @@
 #include "sketch.cuh"
 #include "vec.cuh"
 #include "gemv.cuh"
+#include "mma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -281,9 +282,141 @@ thin_q_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int k, const doub
   }
 }
 
+// thin Q on the FP64 tensor pipe: Q = [I;0] - U M is a tall-skinny GEMM
+// (N x K times K x nc; config 2: 2^20 x 128 x 128 = 34 GFLOP, compute-bound
+// at 37 TFLOP/s).  One CTA owns a 128-row x 64-column tile of Q; K runs in
+// 32-deep chunks, U chunk (k-major, rows contiguous as in HBM) and M chunk
+// (n-major, k contiguous) double-buffered in shared memory — cp.async for
+// fp64 storage, load + widen for the low formats — and 8 warps of 32 x 32
+// accumulate with DMMA m16n8k16.  Column blocks of the same row tile are
+// adjacent in the grid, so the second read of the U tile hits L2.  The
+// row-per-thread kernel above it replaced took 29.4 ms on config 2's factors
+// (registers spilled around u[64], broadcast shared reads): this one 1.2 ms.
+constexpr int TQ_BM = 128, TQ_BN = 64, TQ_BK = 32, TQ_AS = TQ_BM + 4, TQ_BS = TQ_BK + 4, TQ_NT = 256;
+constexpr size_t TQ_SMEM = sizeof(double) * 2 * (size_t)(TQ_BK * TQ_AS + TQ_BN * TQ_BS);
+
+__device__ __forceinline__ void cp_async8_ca(double* dst, const double* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+
+// acc (the 32 x 32 warp tile of a 128 x 64 CTA tile) = A[r0 : r0+128, :K] M[:K, c0 : c0+64]
+// A: N x K of T, column-major (lda); M: K x nc fp64, ld ldm
+template <typename T>
+__device__ __forceinline__ void tq_mainloop(double (&acc)[2][4][4], const T* __restrict__ A, int64_t lda, int64_t N,
+                                            int K, const double* __restrict__ M, int64_t ldm, int nc, int64_t r0,
+                                            int c0, double* sA, double* sB) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nk = (K + TQ_BK - 1) / TQ_BK;
+  const bool a16 = std::is_same<T, double>::value && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0) &&
+                   (r0 + TQ_BM <= N);
+  auto load_stage = [&](int st, int kt) {
+    const int k0 = kt * TQ_BK;
+    double* a = sA + st * TQ_BK * TQ_AS;
+    double* b = sB + st * TQ_BN * TQ_BS;
+    if (a16) {
+      for (int e = tid; e < TQ_BK * TQ_BM / 2; e += TQ_NT) {
+        const int k = e / (TQ_BM / 2), r = 2 * (e % (TQ_BM / 2));
+        double* d = a + k * TQ_AS + r;
+        if (k0 + k < K) cp_async16(d, reinterpret_cast<const double*>(A) + r0 + r + (int64_t)(k0 + k) * lda, 16);
+        else { d[0] = 0.0; d[1] = 0.0; }
+      }
+    } else {
+      for (int e = tid; e < TQ_BK * TQ_BM; e += TQ_NT) {
+        const int k = e / TQ_BM, r = e % TQ_BM;
+        double* d = a + k * TQ_AS + r;
+        const bool in = k0 + k < K && r0 + r < N;
+        if constexpr (std::is_same<T, double>::value) {
+          if (in) cp_async8_ca(d, reinterpret_cast<const double*>(A) + r0 + r + (int64_t)(k0 + k) * lda);
+          else *d = 0.0;
+        } else {
+          *d = in ? (double)Lo<T>::load(A[r0 + r + (int64_t)(k0 + k) * lda]) : 0.0;
+        }
+      }
+    }
+    for (int e = tid; e < TQ_BN * TQ_BK; e += TQ_NT) {
+      const int n = e / TQ_BK, k = e % TQ_BK;
+      b[n * TQ_BS + k] = (c0 + n < nc && k0 + k < K) ? __ldg(M + (k0 + k) + (int64_t)(c0 + n) * ldm) : 0.0;
+    }
+  };
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int z = 0; z < 4; ++z) acc[x][y][z] = 0.0;
+  const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+  load_stage(0, 0);
+  cp_async_commit_group();
+  for (int kt = 0; kt < nk; ++kt) {
+    if (kt + 1 < nk) load_stage((kt + 1) & 1, kt + 1);
+    cp_async_commit_group();
+    cp_async_wait_group<1>();
+    __syncthreads();
+    const double* as = sA + (kt & 1) * TQ_BK * TQ_AS + wm * 32;
+    const double* bs = sB + (kt & 1) * TQ_BN * TQ_BS + (wn * 32) * TQ_BS;
+#pragma unroll
+    for (int k16 = 0; k16 < TQ_BK / 16; ++k16) {
+      double a[2][8], b[4][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) a[mt][v] = as[(k16 * 16 + t + 4 * (v >> 1)) * TQ_AS + mt * 16 + g + 8 * (v & 1)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) b[nt][v] = bs[(nt * 8 + g) * TQ_BS + k16 * 16 + t + 4 * v];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_16x8x16(acc[mt][nt], a[mt], b[nt]);
+    }
+    __syncthreads();  // the stage is refilled two iterations on
+  }
+  cp_async_wait_group<0>();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TQ_NT, 2)
+thin_q_dmma_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int K, const double* __restrict__ M, int nc,
+                   int ncb, double* __restrict__ Q, int64_t ldq) {
+  extern __shared__ __align__(16) unsigned char tq_raw[];
+  double* sA = reinterpret_cast<double*>(tq_raw);   // [2][TQ_BK][TQ_AS]
+  double* sB = sA + 2 * TQ_BK * TQ_AS;              // [2][TQ_BN][TQ_BS]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t bid = blockIdx.x;
+  const int64_t r0 = (bid / ncb) * TQ_BM;
+  const int c0 = (int)(bid % ncb) * TQ_BN;
+  double acc[2][4][4];
+  tq_mainloop<T>(acc, U, ldu, N, K, M, K, nc, r0, c0, sA, sB);
+  const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int64_t r = r0 + wm * 32 + mt * 16 + g + h * 8;
+          const int c = c0 + wn * 32 + nt * 8 + 2 * t + q;
+          if (r < N && c < nc) Q[r + (int64_t)c * ldq] = (r == c ? 1.0 : 0.0) - acc[mt][nt][h * 2 + q];
+        }
+}
+
 template <typename T>
 static int launch_thin_q(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int64_t k, const double* M,
                          double* Q, int64_t ldq) {
+  if (k > 400) return set_error(ctx, SQB_ERR_ARG, "thin_q: k=%lld above 400", (long long)k);
+  static const bool old_path = [] { const char* e = getenv("SQB_THINQ_OLD"); return e && e[0] == '1'; }();
+  if (!old_path) {
+    cudaFuncSetAttribute(thin_q_dmma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TQ_SMEM);
+    const int ncb = (int)((k + TQ_BN - 1) / TQ_BN);
+    const int64_t tiles = (N + TQ_BM - 1) / TQ_BM;
+    thin_q_dmma_kernel<T><<<(unsigned)(tiles * ncb), TQ_NT, TQ_SMEM, ctx->stream>>>((const T*)U, ldu, N, (int)k, M,
+                                                                                  (int)k, ncb, Q, ldq);
+    return check_launch(ctx, "thin_q_dmma_kernel");
+  }
   if (k > 400) return set_error(ctx, SQB_ERR_ARG, "thin_q: k=%lld above 400", (long long)k);
   const size_t smem = sizeof(double) * k * std::min<int64_t>(64, k);
   cudaFuncSetAttribute(thin_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -367,8 +500,128 @@ __global__ void gram_reduce_kernel(const double* __restrict__ P, int nb, int k, 
   }
 }
 
+// Gram partials on the FP64 tensor pipe: CTA (b, pair) accumulates the 64 x 64
+// block G[I, J] = A[rows_b, I]^t A[rows_b, J] (I <= J) over its row range in
+// 32-row chunks.  Both operands are staged as [column][row] (rows contiguous,
+// as in HBM; stride 36 = 4 mod 16 keeps both DMMA fragment loads
+// conflict-free), double-buffered with cp.async.  The row-per-entry kernel
+// above took 34 ms for config 2's Q (2^20 x 128); this one ~1 ms.
+constexpr int GR_B = 64, GR_KC = 32, GR_ST = GR_KC + 4, GR_NT = 128;
+constexpr size_t GR_SMEM = sizeof(double) * 2 * 2 * (size_t)GR_B * GR_ST;
+
+__global__ void __launch_bounds__(GR_NT, 3)
+gram_dmma_kernel(const double* __restrict__ A, int64_t lda, int64_t N, int k, int nblk, int64_t rows_per,
+                 double* __restrict__ P) {
+  extern __shared__ __align__(16) unsigned char gr_raw[];
+  double* sI = reinterpret_cast<double*>(gr_raw);  // [2][GR_B][GR_ST]
+  double* sJ = sI + 2 * GR_B * GR_ST;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // pair index -> (bi <= bj)
+  int bi = 0, bj = 0;
+  {
+    int p = blockIdx.y;
+    for (bj = 0; bj < nblk; ++bj) {
+      if (p <= bj) { bi = p; break; }
+      p -= bj + 1;
+    }
+  }
+  const int i0 = bi * GR_B, j0 = bj * GR_B;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(N, r0 + rows_per);
+  const int nch = r1 > r0 ? (int)((r1 - r0 + GR_KC - 1) / GR_KC) : 0;
+  const bool a16 = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0) && (r0 % 2 == 0);
+  auto load_stage = [&](int st, int ch) {
+    const int64_t rb = r0 + (int64_t)ch * GR_KC;
+    double* di = sI + st * GR_B * GR_ST;
+    double* dj = sJ + st * GR_B * GR_ST;
+    for (int e = tid; e < 2 * GR_B * GR_KC / 2; e += GR_NT) {
+      const int which = e / (GR_B * GR_KC / 2), f = e % (GR_B * GR_KC / 2);
+      const int c = f / (GR_KC / 2), r = 2 * (f % (GR_KC / 2));
+      const int col = (which ? j0 : i0) + c;
+      double* d = (which ? dj : di) + c * GR_ST + r;
+      const double* src = A + rb + r + (int64_t)col * lda;
+      if (col < k && rb + r + 1 < r1 && a16) {
+        cp_async16(d, src, 16);
+      } else {
+        d[0] = (col < k && rb + r < r1) ? src[0] : 0.0;
+        d[1] = (col < k && rb + r + 1 < r1) ? src[1] : 0.0;
+      }
+    }
+  };
+  double acc[2][4][4];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int z = 0; z < 4; ++z) acc[x][y][z] = 0.0;
+  const int wm = warp & 1, wn = warp >> 1, g = lane >> 2, t = lane & 3;
+  if (nch > 0) load_stage(0, 0);
+  cp_async_commit_group();
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) load_stage((ch + 1) & 1, ch + 1);
+    cp_async_commit_group();
+    cp_async_wait_group<1>();
+    __syncthreads();
+    const double* as = sI + (ch & 1) * GR_B * GR_ST + (wm * 32) * GR_ST;
+    const double* bs = sJ + (ch & 1) * GR_B * GR_ST + (wn * 32) * GR_ST;
+#pragma unroll
+    for (int k16 = 0; k16 < GR_KC / 16; ++k16) {
+      double a[2][8], b[4][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) a[mt][v] = as[(mt * 16 + g + 8 * (v & 1)) * GR_ST + k16 * 16 + t + 4 * (v >> 1)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) b[nt][v] = bs[(nt * 8 + g) * GR_ST + k16 * 16 + t + 4 * v];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_16x8x16(acc[mt][nt], a[mt], b[nt]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait_group<0>();
+  double* p = P + (int64_t)blockIdx.x * k * k;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int i = i0 + wm * 32 + mt * 16 + g + h * 8;
+          const int j = j0 + wn * 32 + nt * 8 + 2 * t + q;
+          if (i <= j && j < k) p[i + (int64_t)j * k] = acc[mt][nt][h * 2 + q];
+        }
+}
+
 int gram_run(sqb_ctx* ctx, const double* A, int64_t lda, int64_t N, int64_t k, double* G, int64_t ldg) {
   if (k == 0) return SQB_OK;
+  static const bool old_path = [] { const char* e = getenv("SQB_GRAM_OLD"); return e && e[0] == '1'; }();
+  if (!old_path) {
+    const int nblk = (int)((k + GR_B - 1) / GR_B);
+    const int npairs = nblk * (nblk + 1) / 2;
+    int nb = (int)std::max<int64_t>(1, std::min<int64_t>((3 * (int64_t)ctx->sm_count + npairs - 1) / npairs,
+                                                        (N + 4 * GR_KC - 1) / (4 * GR_KC)));
+    int64_t rows_per = (N + nb - 1) / nb;
+    rows_per = (rows_per + GR_KC - 1) / GR_KC * GR_KC;
+    nb = (int)((N + rows_per - 1) / rows_per);
+    WsPlan plan;
+    const size_t iP = plan.add(sizeof(double) * nb * k * k);
+    SQB_TRY(ws_reserve(ctx, plan.total));
+    double* P = ws_ptr<double>(ctx, plan, iP);
+    cudaFuncSetAttribute(gram_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GR_SMEM);
+    gram_dmma_kernel<<<dim3((unsigned)nb, (unsigned)npairs), GR_NT, GR_SMEM, ctx->stream>>>(A, lda, N, (int)k, nblk,
+                                                                                          rows_per, P);
+    SQB_TRY(check_launch(ctx, "gram_dmma_kernel"));
+    gram_reduce_kernel<<<(unsigned)std::max<int64_t>(1, (k * k + 255) / 256), 256, 0, ctx->stream>>>(P, nb, (int)k, G,
+                                                                                                 ldg);
+    return check_launch(ctx, "gram_reduce_kernel");
+  }
+
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 148, (N + 1023) / 1024));
   const int64_t rows_per = (N + nb - 1) / nb;
   WsPlan plan;
@@ -417,9 +670,97 @@ __global__ void rowsum_kernel(const double* __restrict__ P, int rows, int nb, do
   }
 }
 
+// The same sums with the product Q R on the FP64 tensor pipe (tq_mainloop):
+// CTA (b, column block) walks row tiles b, b + nb, ... of 128 rows, forms
+// D = W - Q R for its 64 columns from the DMMA accumulators and keeps the
+// per-column sums of D^2 and W^2 in registers; one fixed-order reduction
+// (lane octets, then the four row warps) per CTA at the end.  The
+// row-per-thread kernel above took 23 ms on config 2 (2^20 x 128); this ~1.3.
+__global__ void __launch_bounds__(TQ_NT, 2)
+residual_dmma_kernel(const double* __restrict__ W, int64_t ldw, const double* __restrict__ Q, int64_t ldq,
+                     const double* __restrict__ R, int64_t ldr, int64_t N, int k, int kc, int ncb, int nb,
+                     double* __restrict__ P) {
+  extern __shared__ __align__(16) unsigned char tq_raw[];
+  double* sA = reinterpret_cast<double*>(tq_raw);
+  double* sB = sA + 2 * TQ_BK * TQ_AS;
+  __shared__ double red[2][4][TQ_BN];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+  const int cb = blockIdx.x % ncb, b = blockIdx.x / ncb;
+  const int c0 = cb * TQ_BN;
+  const int64_t tiles = (N + TQ_BM - 1) / TQ_BM;
+  double sd[4][2], sw[4][2];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) sd[nt][q] = sw[nt][q] = 0.0;
+  for (int64_t tile = b; tile < tiles; tile += nb) {
+    const int64_t r0 = tile * TQ_BM;
+    double acc[2][4][4];
+    tq_mainloop<double>(acc, Q, ldq, N, k, R, ldr, kc, r0, c0, sA, sB);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int64_t r = r0 + wm * 32 + mt * 16 + g + h * 8;
+            const int c = c0 + wn * 32 + nt * 8 + 2 * t + q;
+            if (r < N && c < kc) {
+              const double w = W[r + (int64_t)c * ldw];
+              const double d = w - acc[mt][nt][h * 2 + q];
+              sd[nt][q] = fma(d, d, sd[nt][q]);
+              sw[nt][q] = fma(w, w, sw[nt][q]);
+            }
+          }
+  }
+  // lanes sharing t hold the same columns: sum over g (lane bits 2..4), then over the row warps
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      double x = sd[nt][q], y = sw[nt][q];
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        x += __shfl_xor_sync(0xffffffffu, x, o);
+        y += __shfl_xor_sync(0xffffffffu, y, o);
+      }
+      if (g == 0) {
+        red[0][wm][wn * 32 + nt * 8 + 2 * t + q] = x;
+        red[1][wm][wn * 32 + nt * 8 + 2 * t + q] = y;
+      }
+    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 2 * TQ_BN; e += TQ_NT) {
+    const int which = e / TQ_BN, c = e % TQ_BN;
+    if (c0 + c < kc)
+      P[(int64_t)(which * kc + c0 + c) * nb + b] =
+          ((red[which][0][c] + red[which][1][c]) + red[which][2][c]) + red[which][3][c];
+  }
+}
+
 int residual_norms_run(sqb_ctx* ctx, const double* W, int64_t ldw, const double* Q, int64_t ldq,
                        const double* R, int64_t ldr, int64_t N, int64_t k, int64_t kc, double* out) {
   if (kc == 0) return SQB_OK;
+  static const bool old_path = [] { const char* e = getenv("SQB_RESID_OLD"); return e && e[0] == '1'; }();
+  if (!old_path) {
+    const int ncb = (int)((kc + TQ_BN - 1) / TQ_BN);
+    const int64_t tiles = (N + TQ_BM - 1) / TQ_BM;
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (2 * (int64_t)ctx->sm_count + ncb - 1) / ncb));
+    WsPlan plan;
+    const size_t iP = plan.add(sizeof(double) * 2 * kc * nb);
+    SQB_TRY(ws_reserve(ctx, plan.total));
+    double* P = ws_ptr<double>(ctx, plan, iP);
+    cudaFuncSetAttribute(residual_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TQ_SMEM);
+    residual_dmma_kernel<<<(unsigned)(nb * ncb), TQ_NT, TQ_SMEM, ctx->stream>>>(W, ldw, Q, ldq, R, ldr, N, (int)k,
+                                                                               (int)kc, ncb, nb, P);
+    SQB_TRY(check_launch(ctx, "residual_dmma_kernel"));
+    rowsum_kernel<<<(unsigned)((2 * kc + 255) / 256), 256, 0, ctx->stream>>>(P, (int)(2 * kc), nb, out);
+    return check_launch(ctx, "rowsum_kernel");
+  }
+
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(2 * 148, (N + 255) / 256));
   WsPlan plan;
   const size_t iP = plan.add(sizeof(double) * 2 * kc * nb);

@@ -138,6 +138,11 @@ update_scalar_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int r, con
   }
 }
 
+// fp64, several columns: Out = X - U C as one tall-skinny DMMA GEMM (defined
+// below, next to the thin-Q kernel whose main loop it shares)
+int launch_update_dmma(sqb_ctx* ctx, const double* U, int64_t ldu, int64_t N, int64_t r, const double* C,
+                       const double* X, int64_t ldx, int64_t k, double* Out, int64_t ldo);
+
 template <typename T>
 static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, const void* U,
                               int64_t ldu, int64_t N, int64_t r, const double* S, int64_t lds,
@@ -173,6 +178,14 @@ static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, con
   }
   constexpr int VN = VecN<T>::n;
   const bool vec = ((reinterpret_cast<uintptr_t>(U) & 15) == 0) && (ldu % VN == 0);
+  if constexpr (std::is_same<T, double>::value) {
+    // the per-column GEMV below re-reads U for every column of X (16 columns
+    // on config 2's factors: 16 GB, 2.46 ms); from 4 columns on, one DMMA
+    // GEMM reads U once
+    static const bool no_dmma = [] { const char* e = getenv("SQB_UPDATE_GEMV"); return e && e[0] == '1'; }();
+    if (k >= 4 && !no_dmma)
+      return launch_update_dmma(ctx, (const double*)U, ldu, N, r, C, (const double*)X, ldx, k, (double*)Out, ldo);
+  }
   if (vec) {
     const int64_t blocks = (N + (int64_t)GEMV_NT * 4 * VN - 1) / ((int64_t)GEMV_NT * 4 * VN);
     dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, 2 * (int64_t)ctx->sm_count)), (unsigned)k);
@@ -402,6 +415,46 @@ thin_q_dmma_kernel(const T* __restrict__ U, int64_t ldu, int64_t N, int K, const
           const int c = c0 + wn * 32 + nt * 8 + 2 * t + q;
           if (r < N && c < nc) Q[r + (int64_t)c * ldq] = (r == c ? 1.0 : 0.0) - acc[mt][nt][h * 2 + q];
         }
+}
+
+// Out = X - U C (fp64; U: N x r, C: r x k with ld r), the compact update
+// (rhqr.py:118) for several columns at once: tq_mainloop, epilogue against X
+__global__ void __launch_bounds__(TQ_NT, 2)
+update_dmma_kernel(const double* __restrict__ U, int64_t ldu, int64_t N, int r, const double* __restrict__ C, int nc,
+                   int ncb, const double* X, int64_t ldx, double* Out, int64_t ldo, const Status* st) {
+  extern __shared__ __align__(16) unsigned char tq_raw[];
+  double* sA = reinterpret_cast<double*>(tq_raw);
+  double* sB = sA + 2 * TQ_BK * TQ_AS;
+  if (st && failed(st)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t bid = blockIdx.x;
+  const int64_t r0 = (bid / ncb) * TQ_BM;
+  const int c0 = (int)(bid % ncb) * TQ_BN;
+  double acc[2][4][4];
+  tq_mainloop<double>(acc, U, ldu, N, r, C, r, nc, r0, c0, sA, sB);
+  const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int64_t row = r0 + wm * 32 + mt * 16 + g + h * 8;
+          const int c = c0 + wn * 32 + nt * 8 + 2 * t + q;
+          if (row < N && c < nc) Out[row + (int64_t)c * ldo] = __dsub_rn(X[row + (int64_t)c * ldx], acc[mt][nt][h * 2 + q]);
+        }
+}
+
+int launch_update_dmma(sqb_ctx* ctx, const double* U, int64_t ldu, int64_t N, int64_t r, const double* C,
+                       const double* X, int64_t ldx, int64_t k, double* Out, int64_t ldo) {
+  cudaFuncSetAttribute(update_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TQ_SMEM);
+  const int ncb = (int)((k + TQ_BN - 1) / TQ_BN);
+  const int64_t tiles = (N + TQ_BM - 1) / TQ_BM;
+  update_dmma_kernel<<<(unsigned)(tiles * ncb), TQ_NT, TQ_SMEM, ctx->stream>>>(U, ldu, N, (int)r, C, (int)k, ncb, X, ldx,
+                                                                              Out, ldo, ctx->d_status);
+  return check_launch(ctx, "update_dmma_kernel");
 }
 
 template <typename T>

@@ -603,6 +603,11 @@ extern "C" int sqb_upper_tri_solve(sqb_ctx* ctx, const double* R, int64_t ldr, i
   return check_launch(ctx, "upper_tri_solve_kernel");
 }
 
+namespace sqb {
+int hqr_tall(sqb_ctx* ctx, int scaling, const double* A, int64_t lda, int64_t p, int64_t m, double* U, int64_t ldu,
+             double* T, int64_t ldt, double* R, int64_t ldr, double* sigmas, double* rhos, double* betas);
+}
+
 extern "C" int sqb_householder_qr(sqb_ctx* ctx, int scaling, const double* A, int64_t lda, int64_t p, int64_t m,
                                   double* U, int64_t ldu, double* T, int64_t ldt, double* R, int64_t ldr,
                                   double* sigmas, double* rhos, double* betas) {
@@ -612,7 +617,11 @@ extern "C" int sqb_householder_qr(sqb_ctx* ctx, int scaling, const double* A, in
   if (scaling != SQB_SCALE_SQRT2 && scaling != SQB_SCALE_UNIT)
     return set_error(ctx, SQB_ERR_ARG, "unknown scaling %d", scaling);
   const size_t hsm = sizeof(double) * (p + 2 * m + 32);
-  if (hsm > 200 * 1024) return set_error(ctx, SQB_ERR_ARG, "householder_qr: p too large for the single-CTA kernel");
+  if (hsm > 200 * 1024) {  // tall matrix: the multi-CTA path (hqr_tall.cu)
+    if ((reinterpret_cast<uintptr_t>(U) & 15) != 0 || ldu % 2 != 0)
+      return set_error(ctx, SQB_ERR_ARG, "householder_qr: U must be 16-byte aligned with an even leading dimension");
+    return hqr_tall(ctx, scaling, A, lda, p, m, U, ldu, T, ldt, R, ldr, sigmas, rhos, betas);
+  }
   const size_t hsm_res = hsm + sizeof(double) * ((size_t)p * m + (size_t)m * m);
   if (hsm_res <= 227 * 1024) {
     cudaFuncSetAttribute(hqr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm_res);

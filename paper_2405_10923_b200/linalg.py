@@ -74,6 +74,30 @@ def gram(A) -> torch.Tensor:
 _GRAM_RATIO_MIN = 1e-8
 
 
+def _hqr_r(Ad) -> torch.Tensor:
+    """R factor of the library's Householder QR (baselines.py:33-89; one CTA
+    for a small matrix, the tall multi-CTA path of csrc/hqr_tall.cu
+    otherwise) — the reduction LAPACK's gesdd applies to a tall matrix before
+    its SVD, without leaving the library for the n-dimensional work.  A column
+    exactly dependent on its predecessors (HQR breakdown) makes M singular to
+    working precision: sigma_min = 0."""
+    from .devarray import empty_colmajor as _ec
+    N, k = Ad.shape
+    U = _ec(N, k, "double")
+    T = _ec(k, k, "double")
+    R = _ec(k, k, "double")
+    scal = torch.empty(3 * k, dtype=torch.float64, device=Ad.device)
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_householder_qr(ctx.h, 0, Ad.data_ptr(), ld_of(Ad), N, k, U.data_ptr(), ld_of(U),
+                                            T.data_ptr(), ld_of(T), R.data_ptr(), ld_of(R), scal.data_ptr(),
+                                            scal.data_ptr() + 8 * k, scal.data_ptr() + 16 * k), "sqb_householder_qr")
+    code, col, _ = ctx.status()
+    if code != 0:
+        R = torch.triu(R)
+        R[col - 1:, col - 1:] = 0.0  # the trailing block was never reduced
+    return R
+
+
 def cond_number(M, exact: bool = False):
     """linalg.py:151-160: 2-norm condition number; +inf if sigma_min == 0.
 
@@ -96,7 +120,7 @@ def cond_number(M, exact: bool = False):
         if lmax > 0.0 and lmin > _GRAM_RATIO_MIN * lmax:
             return float(np.sqrt(lmax) / np.sqrt(lmin))
     N, k = Ad.shape
-    B = torch.linalg.qr(Ad, mode="r")[1] if N > k else Ad
+    B = _hqr_r(Ad) if N > k else Ad
     sv = torch.linalg.svdvals(B)
     smax, smin = float(sv[0]), float(sv[-1])
     if smin == 0.0:

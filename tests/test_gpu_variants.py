@@ -10,6 +10,7 @@ import pytest
 
 from conftest import golden
 from oracle import sketchqr_oracle as O
+from paper_2405_10923_b200 import workloads
 
 pytestmark = pytest.mark.gpu
 
@@ -233,3 +234,44 @@ def test_column_pass_overlap_and_partial_tile_are_bitwise(P, monkeypatch, tag, N
             for k in out:
                 assert torch.equal(out[k], cur[k]), (k, early, nopart, rep)
     assert float(torch.linalg.norm(out["R"])) > 0
+
+
+# ------------------------------------------------------------ tall Householder QR (baseline, cond_number)
+@pytest.mark.parametrize("p,m,scaling", [(40000, 24, "sqrt2"), ((1 << 17) + 77, 33, "unit"), (30001, 5, "sqrt2")])
+def test_tall_householder_qr_matches_the_oracle(P, p, m, scaling):
+    """householder_qr beyond one CTA's shared memory (csrc/hqr_tall.cu: two
+    transposed GEMVs and one GEMV over the finished reflectors per column)
+    against the oracle's restatement of baselines.py:33-89."""
+    rng = np.random.default_rng(p)
+    A = rng.standard_normal((p, m)) * np.logspace(0, -6, m)[None, :]
+    got = P.householder_qr(A, scaling=scaling)
+    Q, R, aux = O.householder_qr(A, scaling=scaling)
+    assert rel(got.R, R) < 1e-12
+    assert rel(got.aux["U"], aux["U"]) < 1e-12 and rel(got.aux["T"], aux["T"]) < 1e-12
+    assert rel(got.Q, Q) < 1e-12
+    assert np.linalg.norm(got.Q.T @ got.Q - np.eye(m)) < 1e-13
+    assert np.linalg.norm(got.Q @ got.R - A) <= 1e-14 * np.linalg.norm(A)
+
+
+def test_tall_householder_qr_breakdown_and_singular_cond(P):
+    p, m = 50000, 4
+    A = np.random.default_rng(1).standard_normal((p, m))
+    A[:, 2] = 2.0 * A[:, 0] - A[:, 1]  # rank deficient, but not exactly in floating point
+    assert P.cond_number(A) > 1e14
+    Z = np.zeros((p, 3))
+    Z[:, 0] = 1.0
+    with pytest.raises(P.BreakdownError, match="column 2"):
+        P.householder_qr(Z)
+    assert P.cond_number(Z) == np.inf
+
+
+def test_cond_number_of_a_tall_illconditioned_matrix_uses_the_library_qr(P):
+    """linalg.py:151-160 on a tall matrix with cond 1e11: the Gram probe
+    cannot resolve it, the value comes from the library's tall Householder QR
+    and a k x k SVD — within 1e-3 of numpy's SVD of the same matrix."""
+    p, m = 1 << 17, 32
+    W = workloads.illcond_w(p, m, 3, smin_exp=-11.0)
+    ref = np.linalg.cond(W)
+    assert 1e10 < ref < 1e12
+    # sigma_min is defined to ~u cond = 1e-5 relative: two backward-stable routes agree to that
+    assert P.cond_number(W) == pytest.approx(ref, rel=1e-3)

@@ -39,7 +39,7 @@ import torch
 from . import _lib
 from .devarray import ld_of, to_device
 from .krylov import CSRMatrix, arnoldi_q, hessenberg_lstsq, rhqr_arnoldi
-from .linalg import BreakdownError, gram
+from .linalg import _hqr_r, BreakdownError, gram
 from .precision import PrecisionRangeError, policy_from_tag, require_device_policy
 from .rhqr import (apply_reflectors_compact, householder_qr, rec_rhqr, rhqr_block, rhqr_left, rhqr_right,
                    thin_q)
@@ -140,7 +140,10 @@ def _prefix_conds(A):
     k = A.shape[1]
     if not bool(torch.isfinite(A).all()):
         return [np.inf] * k
-    R = torch.linalg.qr(A, mode="r").R
+    # the R factor of the library's Householder QR (one CTA for a small A, the
+    # tall path of csrc/hqr_tall.cu otherwise): the n-dimensional work stays in
+    # the library; only the k x k SVDs of its leading blocks go to torch
+    R = _hqr_r(A) if A.shape[0] > k else torch.linalg.qr(A, mode="r").R
     out = []
     for j in range(1, k + 1):
         sv = torch.linalg.svdvals(R[:j, :j])

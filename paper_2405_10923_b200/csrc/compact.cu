@@ -895,6 +895,19 @@ static int arnoldi_q_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int6
   ts_kernel<<<(unsigned)std::max<int64_t>(1, (r * c + 255) / 256), 256, 0, ctx->stream>>>(Tm, ldt, S, lds,
                                                                                           (int)r, (int)c, M);
   SQB_TRY(check_launch(ctx, "ts_kernel"));
+  // Q = [I;0] - U M is thin Q's tall-skinny product with K = r, nc = c: the
+  // same DMMA kernel (the row-per-thread compact_q_kernel above took 2.97 ms
+  // for 2^20 x 51 and held M in shared memory, which capped r c at 25600)
+  static const bool old_path = [] { const char* e = getenv("SQB_THINQ_OLD"); return e && e[0] == '1'; }();
+  if (!old_path) {
+    cudaFuncSetAttribute(thin_q_dmma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TQ_SMEM);
+    const int ncb = (int)((c + TQ_BN - 1) / TQ_BN);
+    const int64_t tiles = (N + TQ_BM - 1) / TQ_BM;
+    thin_q_dmma_kernel<T><<<(unsigned)(tiles * std::max(ncb, 1)), TQ_NT, TQ_SMEM, ctx->stream>>>(
+        (const T*)U, ldu, N, (int)r, M, (int)c, std::max(ncb, 1), Q, ldq);
+    return check_launch(ctx, "thin_q_dmma_kernel");
+  }
+  if ((int64_t)r * c * 8 > 200 * 1024) return set_error(ctx, SQB_ERR_ARG, "arnoldi_q: r*c too large");
   const size_t smem = sizeof(double) * std::max<int64_t>(1, r * c);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(compact_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -912,7 +925,6 @@ extern "C" int sqb_arnoldi_q(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t 
   SQB_TRY(begin_entry(ctx));
   if (c < 0 || c > r) return set_error(ctx, SQB_ERR_ARG, "have %lld reflectors, cannot build %lld columns",
                                        (long long)r, (long long)c);
-  if ((int64_t)r * c * 8 > 200 * 1024) return set_error(ctx, SQB_ERR_ARG, "arnoldi_q: r*c too large");
   switch (lo_dtype) {
     case SQB_F64: return arnoldi_q_t<double>(ctx, U, ldu, N, r, T, ldt, S, lds, c, Q, ldq);
     case SQB_F32: return arnoldi_q_t<float>(ctx, U, ldu, N, r, T, ldt, S, lds, c, Q, ldq);

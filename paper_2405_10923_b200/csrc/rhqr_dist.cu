@@ -80,6 +80,10 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
     off[r * 8 + 6] = plan.add(sizeof(double) * m * od);        // raw-sketch payload
     off[r * 8 + 7] = plan.add(sizeof(A) * ell * tpr * m);      // leaves
   }
+  int64_t nl_max = 0;
+  for (auto& d : rk) nl_max = std::max(nl_max, d.n_local);
+  const size_t flag_bytes = sizeof(int) * (size_t)((nl_max >> 9) + 8);
+  const size_t iFlag = plan.add(flag_bytes);                       // column-pass block flags (fused exchange)
   const size_t iG = plan.add(sizeof(double) * nranks * od);        // per-column gather
   const size_t iG0 = plan.add(sizeof(double) * nranks * m * od);   // raw-sketch gather
   const size_t iY0 = plan.add(sizeof(double) * od * m);            // combined raw sketches (shared)
@@ -153,6 +157,18 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
   const size_t step_smem = step_smem_bytes((int)od, (int)m);
   cudaFuncSetAttribute(rhqr_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(step_smem, 48 * 1024));
+  // real ranks over peer memory: the step kernel itself folds the rank-local
+  // subtree, stores it into the peers' mailboxes and waits for theirs (tree =
+  // 3): two launches per column, as on one GPU.  Virtual ranks share one
+  // stream, where a rank's step cannot wait for ranks that have not run yet:
+  // they keep the separate subtree + push launches.
+  static const bool no_fuse = [] { const char* e = getenv("SQB_P2P_NOFUSE"); return e && e[0] == '1'; }();
+  const bool fused = p2p && !virt && L == 1 && !no_fuse;
+  // with the exchange inside the step the chain is the single-GPU one (pass,
+  // step), so the cross-pass overlap applies unchanged (ColArgs::tflag)
+  int* tflag = (fused && early_env() && rk[0].n_local >= (int64_t(1) << 19))
+                   ? reinterpret_cast<int*>(base + plan.offs[iFlag]) : nullptr;
+  if (tflag) SQB_CUDA_TRY(cudaMemsetAsync(tflag, 0, flag_bytes, ctx->stream));
   auto step_args = [&](DistRank& d, int c) {
     StepArgs sa{};
     sa.c = c; sa.m = (int)m; sa.off = 0; sa.ncol = (int)m; sa.ell = (int)ell; sa.od = (int)od; sa.scaling = scaling;
@@ -166,7 +182,16 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
       sa.seq = xseq;
     }
     sa.nranks = nranks; sa.rank_level = rank_level;
+    sa.early = tflag ? 1 : 0;
     sa.P = nullptr; sa.n_tiles = tpr; sa.n_eff = 0; sa.idx = sk->indices; sa.log_tb = g.log_tb; sa.norm_lo = norm_lo;
+    if (fused && c > 0) {
+      sa.tree = 3;
+      sa.P = d.P; sa.n_eff = (d.n_local + tb - 1) / tb;
+      sa.peers = ctx->p2p_table + (size_t)(&d - rk.data()) * nranks;
+      sa.my_rank = rank_ids[&d - rk.data()];
+      sa.slot_count = ctx->p2p_count;
+      sa.toprows = d.mrow > 0 ? d.pay + ell : nullptr;
+    }
     sa.y = c == 0 ? Y0 : d.y; sa.Y0 = Y0; sa.S = d.S; sa.lds = d.lds; sa.R = d.R; sa.ldr = d.ldr;
     sa.U = d.Utop; sa.ldu = d.ldutop; sa.sigmas = d.sig; sa.rhos = d.rho; sa.betas = d.bet;
     sa.fscale = d.fs; sa.vbuf = d.vbuf; sa.anext = d.abuf + ((c + 1) & 1) * (m + 1); sa.clast = d.coef;
@@ -194,6 +219,8 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
       ca.idx = sk->indices; ca.scale_lo = scale_lo; ca.P = d.P; ca.y = d.pay + ell;
       ca.S = d.S; ca.lds = d.lds; ca.T = d.T; ca.ldt = d.ldt; ca.Y0 = Y0; ca.vprev = d.vbuf; ca.betas = d.bet;
       ca.anext = d.abuf + ((c + 1) & 1) * (m + 1); ca.st = st;
+      ca.tflag = tflag;
+      ca.no_part = no_part_env();
       ca.helper_first = helper_first_default();
       ca.no_p16 = no_p16_env();
       ca.no_pre = no_pre_env();
@@ -206,9 +233,11 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
       // rank-local subtree of w_c's sketch -> payload[0:ell]
       SrhtGeom gl{g.log_tb, tpr, n_eff};
       if (n_eff == 0) SQB_CUDA_TRY(cudaMemsetAsync(d.P, 0, sizeof(A) * ell * tpr, ctx->stream));
-      SQB_TRY(launch_srht_tree_geom(ctx, sk, Lo<T>::code, gl, d.P, 1, d.pay, od, 0, 0, st, 1));  // column-kernel leaves
+      if (!fused)
+        SQB_TRY(launch_srht_tree_geom(ctx, sk, Lo<T>::code, gl, d.P, 1, d.pay, od, 0, 0, st, 1));  // column-kernel leaves
     }
-    SQB_TRY(exchange([](DistRank& d) { return d.pay; }, (size_t)od, Gc));
+    if (fused) xseq = ++ctx->p2p_seq;  // the step kernel is the exchange
+    else SQB_TRY(exchange([](DistRank& d) { return d.pay; }, (size_t)od, Gc));
     for (int r = 0; r < L; ++r)
       SQB_TRY(launch_pdl(ctx, "rhqr_step_kernel", rhqr_step_kernel<T>, dim3(STEP_CL), dim3(STEP_NT), step_smem,
                          step_args(rk[r], (int)c)));

@@ -595,7 +595,14 @@ struct StepArgs {
   int scaling;
   int early;                  // 1: trigger the dependents (pass c+1) before waiting for pass c (ColArgs::tflag)
   int tree;                   // 1: finish the SRHT tree from the tile leaves; 0: y[m:] given;
-                              // 2: combine the gathered per-rank partials (multi-GPU)
+                              // 2: combine the gathered per-rank partials (multi-GPU);
+                              // 3: fused exchange — this kernel folds the rank-local subtree of the
+                              //    tile leaves, stores the partials straight into every peer's mailbox
+                              //    (NVLink), releases its flags, then proceeds as 2 on its own mailbox
+  void* const* peers;         // tree == 3: mailbox base of every rank (own included), device table
+  int my_rank;                // tree == 3
+  int64_t slot_count;         // tree == 3: doubles per mailbox slot
+  const double* toprows;      // tree == 3: this rank's identity-block rows of w_c (rank 0), else null
   const double* gath;         // tree == 2: [nranks][gstride] per-rank partials (+ rank 0's top rows)
   int64_t gstride;            // tree == 2: doubles between ranks' partials (ell + m for a gather buffer)
   const unsigned long long* flags;  // tree == 2, peer-memory exchange: acquire flags >= seq first
@@ -665,12 +672,36 @@ rhqr_step_kernel(StepArgs a) {
   pdl_wait();
   if (!a.early) pdl_trigger();
   if (a.gdbg && rank == 0 && tid == 0) a.gdbg[1] = gtime_ns();
-  if (a.tree == 2) p2p_wait(a.flags, a.nranks, (int)(a.seq & 1), a.seq);
+  if (a.tree == 3) {
+    // the exchange of column c inside the step: no tree / push launches on the
+    // column's critical path.  Runs even after a recorded failure (every rank
+    // fails at the same column, and every rank still waits for the flags).
+    const int par = (int)(a.seq & 1);
+    const int rr0 = rank * step_rows(od), rr1 = min(od, rr0 + step_rows(od));
+    for (int row = max(rr0, m) + warp; row < rr1; row += nw) {
+      const int o = row - m;
+      const int64_t rhi = __ldg(a.idx + o) >> a.log_tb;
+      const A v = warp_tile_tree<T>((const A*)a.P + (int64_t)o * a.n_tiles, (int)a.n_tiles, (int)a.n_eff, rhi);
+      if (lane < a.nranks) p2p_slot(a.peers[lane], a.nranks, a.slot_count, par, a.my_rank)[o] = (double)v;
+    }
+    if (a.toprows)
+      for (int row = rr0 + tid; row < min(rr1, m); row += STEP_NT) {
+        const double y = a.toprows[row];
+        for (int q = 0; q < a.nranks; ++q) p2p_slot(a.peers[q], a.nranks, a.slot_count, par, a.my_rank)[a.ell + row] = y;
+      }
+    __threadfence_system();
+    cluster.sync();  // every CTA's stores are issued and fenced
+    if (rank == 0 && tid < a.nranks) {
+      __threadfence_system();
+      st_release_sys(reinterpret_cast<unsigned long long*>(a.peers[tid]) + par * a.nranks + a.my_rank, a.seq);
+    }
+  }
+  if (a.tree >= 2) p2p_wait(a.flags, a.nranks, (int)(a.seq & 1), a.seq);
   SQB_STAMP(1);
   const bool dead = failed(a.st);  // uniform across the cluster; still take part in the sync
   // ---- phase A: y on the owned rows (identity block given; Omega rows from the tree)
   if (!dead) {
-    if (a.tree == 2) {
+    if (a.tree >= 2) {
       // upper log2(P) levels of the SRHT tree across ranks (left = lower rank)
       // plus the identity block from rank 0's payload
       for (int i = tid; i < nrow; i += STEP_NT) {

@@ -65,16 +65,19 @@ def test_p2p_world1_ipc_path(P, monkeypatch):
         dist.init_process_group("gloo", rank=0, world_size=1)
         created = True
     try:
-        N, m = (1 << 14) + 5, 16
-        W = np.random.default_rng(0).standard_normal((N, m))
-        om = P.SRHTSketch(64, N - m, 3)
-        D.init_p2p(m, om.ell)
-        F1 = P.rhqr_left(W, om)
-        for _ in range(3):
-            Fd = D.rhqr_left_distributed(W, om, m)
-            for k in ("R", "S", "T", "U"):
-                assert np.array_equal(getattr(Fd, k), getattr(F1, k)), k
-        D.close_p2p()
+        # small: fused exchange (the step kernel folds the rank-local subtree,
+        # stores it into the mailboxes and waits); large: the same with the
+        # cross-pass overlap of the column passes (per-block flags)
+        for N, m, ell in (((1 << 14) + 5, 16, 64), ((1 << 20) + 4096 + 40, 40, 96)):
+            W = np.random.default_rng(0).standard_normal((N, m))
+            om = P.SRHTSketch(ell, N - m, 3)
+            D.init_p2p(m, om.ell)
+            F1 = P.rhqr_left(W, om)
+            for _ in range(3):
+                Fd = D.rhqr_left_distributed(W, om, m)
+                for k in ("R", "S", "T", "U"):
+                    assert np.array_equal(getattr(Fd, k), getattr(F1, k)), (k, N)
+            D.close_p2p()
     finally:
         if created:
             dist.destroy_process_group()

@@ -396,7 +396,8 @@ class RecRHQR(Workload):
         # read G (ell x n) and W, write U (sketch GEMM + reconstruction)
         self.alg = 8.0 * (ell * n + N * m + N * m)
         self.flops = 2.0 * ell * n * m
-        self.kernel = "dense_dmma_kernel (FP64 DMMA split-K sketch GEMM)"
+        self.kernel = ("dense_tma_kernel (FP64 DMMA split-K sketch GEMM: TMA tensor-map boxes on a 5-stage "
+                       "mbarrier ring, one producer warp, 16 consumer warps)")
         # the sketch GEMM is tensor-bound (AI ~12.8 flop/B): its roofline is
         # the FP64 DMMA pipe, which MEASURED_PEAKS.json does not carry
         self.roof = {"bound": "tensor", "unit": "TFLOP/s", "scale": 1e12, "peak": 37.0,

@@ -18,6 +18,7 @@
 #include "mma.cuh"
 #include "sketch.cuh"
 #include "vec.cuh"
+#include "tma.cuh"
 
 namespace sqb {
 
@@ -150,6 +151,147 @@ dense_dmma_kernel(const double* __restrict__ G, int64_t ldg, const double* __res
         }
 }
 
+// ---------------------------------------------------------------------------
+// K2 on TMA + mbarriers (round 2 session 4).  One CTA per SM owns a
+// 256 x 64 output tile of one K slab (config 3: the whole 256 x 64 sketch, so
+// X is streamed once, not once per 128-row half): a producer warp issues one
+// 2-D tensor-map box per operand and stage (16 doubles = 128 bytes of k times
+// 256 / 64 rows, SWIZZLE_128B) on a 5-stage ring of full/empty mbarriers, 16
+// consumer warps (8 x 2 of 32 x 32) wait per stage and issue DMMA m16n8k16 —
+// no block-wide barrier in the main loop.  Under the 128-byte swizzle a
+// fragment load of rows g = 0..7 would put rows g and g ^ 1 on the same banks;
+// the kernel therefore maps fragment row g to tile row pr(g) = 2 (g & 3) +
+// (g >> 2) inside every 8-row group (the MMA does not care which matrix row
+// sits in which fragment row, the epilogue applies the same map), which makes
+// every LDS.64 conflict-free.  Same slab partition and the same ascending-k
+// DMMA sequence per accumulator as dense_dmma_kernel: Z is bitwise the same.
+// ---------------------------------------------------------------------------
+constexpr int TM_BM = 256, TM_BN = 64, TM_BK = 16, TM_STAGES = 5, TM_CW = 16, TM_NT = (TM_CW + 1) * 32;
+constexpr uint32_t TM_G_BYTES = TM_BM * TM_BK * 8, TM_X_BYTES = TM_BN * TM_BK * 8;
+constexpr size_t TM_SMEM = 1024 + (size_t)TM_STAGES * (TM_G_BYTES + TM_X_BYTES) + 2 * TM_STAGES * 8;
+
+__device__ __forceinline__ int tm_pr(int g) { return ((g & 3) << 1) | (g >> 2); }
+
+__global__ void __launch_bounds__(TM_NT, 1)
+dense_tma_kernel(const __grid_constant__ CUtensorMap mapG, const __grid_constant__ CUtensorMap mapX, int64_t M,
+                 int64_t N, int64_t K, int64_t kslab, double* __restrict__ P, const Status* st) {
+  extern __shared__ __align__(1024) unsigned char tm_raw[];
+  if (st && failed(st)) return;
+  unsigned char* base = tm_raw + ((1024u - (smem_u32(tm_raw) & 1023u)) & 1023u);
+  unsigned char* sG = base;                                     // [stage][256 rows][128 B]
+  unsigned char* sX = base + (size_t)TM_STAGES * TM_G_BYTES;    // [stage][64 rows][128 B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)TM_STAGES * (TM_G_BYTES + TM_X_BYTES));
+  uint64_t* empty = full + TM_STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t m0 = (int64_t)blockIdx.x * TM_BM, n0 = (int64_t)blockIdx.y * TM_BN;
+  const int64_t z = blockIdx.z;
+  const int64_t k0 = z * kslab, k1 = min(K, k0 + kslab);
+  const int nk = (int)((k1 - k0 + TM_BK - 1) / TM_BK);
+  if (tid == 0) {
+    for (int s = 0; s < TM_STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, TM_CW); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == TM_CW) {
+    // ---- producer: one elected lane feeds the ring
+    if (lane == 0) {
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % TM_STAGES;
+        if (kt >= TM_STAGES) mbar_wait(empty + s, ((kt / TM_STAGES) - 1) & 1);
+        mbar_expect_tx(full + s, TM_G_BYTES + TM_X_BYTES);
+        const int kc = (int)(k0 + (int64_t)kt * TM_BK);
+        tma_load_2d(sG + (size_t)s * TM_G_BYTES, &mapG, kc, (int)m0, full + s);
+        tma_load_2d(sX + (size_t)s * TM_X_BYTES, &mapX, kc, (int)n0, full + s);
+      }
+    }
+    return;
+  }
+  // ---- consumers
+  double acc[2][4][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+  const int wm = warp & 7, wn = warp >> 3;  // 8 x 2 warps of 32 x 32
+  const int g = lane >> 2, t = lane & 3, pg = tm_pr(g);
+  // byte offsets inside a stage: row * 128 + ((chunk ^ (row & 7)) << 4) + (t & 1) * 8 with row & 7 = pg;
+  // the k chunk of fragment element v is (t >> 1) + 2 (v >> 1) for A and (t >> 1) + 2 v for B: four
+  // swizzled column offsets serve both, the row parts are compile-time multiples of 1024
+  uint32_t cx[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) cx[c] = (uint32_t)(((((t >> 1) + 2 * c) ^ pg) << 4) + (t & 1) * 8);
+  const uint32_t arow = (uint32_t)((wm * 32 + pg) * 128), brow = (uint32_t)((wn * 32 + pg) * 128);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % TM_STAGES;
+    mbar_wait(full + s, (kt / TM_STAGES) & 1);
+    const unsigned char* gs = sG + (size_t)s * TM_G_BYTES + arow;
+    const unsigned char* xs = sX + (size_t)s * TM_X_BYTES + brow;
+    double b[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) b[nt][v] = *reinterpret_cast<const double*>(xs + nt * 1024 + cx[v]);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      double a[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) a[v] = *reinterpret_cast<const double*>(gs + mt * 2048 + (v & 1) * 1024 + cx[v >> 1]);
+      if (mt == 1) {  // every operand of the stage is in registers: the slot can be refilled
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma_16x8x16(acc[mt][nt], a, b[nt]);
+    }
+  }
+  // epilogue: partial tile -> P[slab] (M x N column-major), fragment rows / columns through pr()
+  double* p = P + z * M * N;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int64_t r = m0 + wm * 32 + mt * 16 + h * 8 + pg;
+          const int64_t c = n0 + wn * 32 + nt * 8 + tm_pr(2 * t + q);
+          if (r < M && c < N) p[r + c * M] = acc[mt][nt][h * 2 + q];
+        }
+}
+
+typedef CUresult (*TmEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmEncodeFn tm_encode() {
+  static TmEncodeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<TmEncodeFn>(p);
+  }
+  return fn;
+}
+
+// rows x K fp64 matrix with K contiguous (ld doubles between rows), box 16 x box_rows, 128-byte swizzle
+static bool tm_make_map(CUtensorMap* map, const double* A, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+  TmEncodeFn enc = tm_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)TM_BK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 __global__ void dense_reduce_kernel(const double* __restrict__ P, int64_t M, int64_t N, int S,
                                     double* __restrict__ Y, int64_t ldy, int64_t row_off,
                                     const Status* st) {
@@ -224,9 +366,28 @@ int launch_dense<double>(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int6
   }
   dim3 grid((unsigned)((sk->ell + DBM - 1) / DBM), (unsigned)((k + DBN - 1) / DBN), (unsigned)S);
   prof_begin(ctx);
-  dense_dmma_kernel<<<grid, DNT, DSMEM, ctx->stream>>>(sk->G, sk->ldg, (const double*)X, ldx, sk->ell,
-                                                        k, sk->n, ks, (double*)ws, st, 0);
-  SQB_TRY(check_launch(ctx, "dense_dmma_kernel"));
+  // TMA + mbarrier kernel (256-row tiles): same slabs, same bits.  Needs 16-byte aligned operands with
+  // 16-byte row strides; SQB_DENSE_CPASYNC=1 keeps the cp.async kernel (A/B)
+  static const bool no_tma = [] { const char* e = getenv("SQB_DENSE_CPASYNC"); return e && e[0] == '1'; }();
+  CUtensorMap mapG, mapX;
+  const bool tma_ok = !no_tma && sk->ell > DBM && ks % TM_BK == 0 && (sk->ldg % 2 == 0) && (ldx % 2 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(sk->G) | reinterpret_cast<uintptr_t>(X)) & 15) == 0 &&
+                      tm_make_map(&mapG, sk->G, sk->ell, sk->n, sk->ldg, TM_BM) &&
+                      tm_make_map(&mapX, (const double*)X, k, sk->n, ldx, TM_BN);
+  if (tma_ok) {
+    static bool attr_t = false;
+    if (!attr_t) {
+      cudaFuncSetAttribute(dense_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TM_SMEM);
+      attr_t = true;
+    }
+    dim3 gt((unsigned)((sk->ell + TM_BM - 1) / TM_BM), (unsigned)((k + TM_BN - 1) / TM_BN), (unsigned)S);
+    dense_tma_kernel<<<gt, TM_NT, TM_SMEM, ctx->stream>>>(mapG, mapX, sk->ell, k, sk->n, ks, (double*)ws, st);
+    SQB_TRY(check_launch(ctx, "dense_tma_kernel"));
+  } else {
+    dense_dmma_kernel<<<grid, DNT, DSMEM, ctx->stream>>>(sk->G, sk->ldg, (const double*)X, ldx, sk->ell,
+                                                          k, sk->n, ks, (double*)ws, st, 0);
+    SQB_TRY(check_launch(ctx, "dense_dmma_kernel"));
+  }
   prof_end(ctx, 2.0 * (double)sk->ell * (double)sk->n * (double)k);  // flops (bench.py: tensor roofline)
   const int64_t MN = sk->ell * k;
   const unsigned rb = (unsigned)std::min<int64_t>((MN + 255) / 256, 4096);

@@ -238,9 +238,29 @@ class RHQRLeft(Workload):
             self.Wd = to_device(W, self.tag, align_row=m if rank == 0 else 0)
             D.init_comm()
             self.exchange = "nccl all-gather"
-            if getattr(self, "p2p", False):  # --exchange p2p: in-kernel peer-memory stores (sqb_p2p_*)
-                D.init_p2p(m, self.ell)
-                self.exchange = "peer-memory mailboxes (NVLink stores + release/acquire flags)"
+            mode = getattr(self, "exchange_mode", "auto")
+            if mode in ("p2p", "auto"):
+                # the exchange inside the step kernel (sqb_p2p_*: IPC mailboxes, NVLink stores, release/acquire
+                # flags): two launches per column instead of four; "auto" falls back to NCCL when the mailboxes
+                # cannot be set up (no peer access / IPC) — agreed on by every rank
+                import torch.distributed as dist
+                ok = 1
+                try:
+                    D.init_p2p(m, self.ell)
+                except Exception as exc:  # noqa: BLE001
+                    if mode == "p2p":
+                        raise
+                    ok = 0
+                    sys.stderr.write(f"[bench] rank {rank}: peer-memory exchange unavailable ({exc}); using NCCL\n")
+                flag = torch.tensor([ok], device="cuda")
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+                if int(flag.item()) == 1:
+                    self.exchange = "peer-memory mailboxes, exchange inside the step kernel (NVLink stores + release/acquire flags)"
+                else:
+                    try:
+                        D.close_p2p()
+                    except Exception:  # noqa: BLE001
+                        pass
             self.step = lambda check=False: D.rhqr_left_distributed(self.Wd, self.om, m, policy=pol, check=check)
             self.W_host = None
         else:
@@ -742,7 +762,7 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"],
                     help="row-partitioned runs (N > 1): per-column exchange by NCCL all-gather or in-kernel "
                          "peer-memory stores")
     ap.add_argument("--no-other-configs", action="store_true",
@@ -763,7 +783,7 @@ def main():
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
     print(f"[bench] rank {os.environ.get('RANK', '0')}/{ws_env} impl={args.impl}", file=sys.stderr, flush=True)
     wl = WORKLOADS[args.workload]()
-    wl.p2p = args.exchange == "p2p"
+    wl.exchange_mode = args.exchange
     if args.impl == "reference":
         run_reference(args, wl)
         return

@@ -87,12 +87,30 @@ def init_p2p(m: int, ell: int, group=None):
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     ctx = _lib.context()
+    # every step that can fail locally is followed by a collective on its
+    # outcome, so a failure on one rank raises on all of them instead of
+    # leaving the others inside a collective
     h = C.create_string_buffer(64)
-    ctx.check(_lib.lib().sqb_p2p_mailbox(ctx.h, world, p2p_slot_count(m, ell), h), "sqb_p2p_mailbox")
+    err = None
+    try:
+        ctx.check(_lib.lib().sqb_p2p_mailbox(ctx.h, world, p2p_slot_count(m, ell), h), "sqb_p2p_mailbox")
+    except Exception as exc:  # noqa: BLE001
+        err = repr(exc)
     handles = [None] * world
-    dist.all_gather_object(handles, h.raw, group=group)
+    dist.all_gather_object(handles, None if err else h.raw, group=group)
+    if any(x is None for x in handles):
+        close_p2p()
+        raise RuntimeError(f"peer-memory mailbox allocation failed on a rank ({err or 'another rank'})")
     table = C.create_string_buffer(b"".join(handles), 64 * world)
-    ctx.check(_lib.lib().sqb_p2p_open(ctx.h, rank, table), "sqb_p2p_open")
+    try:
+        ctx.check(_lib.lib().sqb_p2p_open(ctx.h, rank, table), "sqb_p2p_open")
+    except Exception as exc:  # noqa: BLE001
+        err = repr(exc)
+    oks = [None] * world
+    dist.all_gather_object(oks, err is None, group=group)
+    if not all(oks):
+        close_p2p()
+        raise RuntimeError(f"peer-memory mailboxes could not be mapped on a rank ({err or 'another rank'})")
     return ctx
 
 

@@ -415,7 +415,9 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
   double* z = ws_ptr<double>(ctx, plan, iz);
   double* fs = ws_ptr<double>(ctx, plan, ifs);
   double* cq = ws_ptr<double>(ctx, plan, icq);
-  T* w = ws_ptr<T>(ctx, plan, iw);
+  // w is sketched from row mt on (apply_reflectors): shift it so that w + mt is 16-byte aligned and the
+  // sketch takes the TMA kernels instead of the scalar-load tile kernel (mt = m + 1 is odd for even m)
+  T* w = ws_ptr<T>(ctx, plan, iw) + (VecN<T>::n - mt % VecN<T>::n) % VecN<T>::n;
   T* q = ws_ptr<T>(ctx, plan, iq);
   double* t64 = ws_ptr<double>(ctx, plan, it64);
   void* P = ws_ptr<void>(ctx, plan, iP);

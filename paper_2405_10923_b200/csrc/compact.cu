@@ -166,9 +166,10 @@ static int apply_reflectors_t(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, con
                                      cudaMemcpyDeviceToDevice, ctx->stream));
     return SQB_OK;
   }
-  SQB_TRY(launch_copy_top(ctx, Lo<T>::code, X, ldx, m, k, Y, od, st));
+  defer_copy_top(ctx, Lo<T>::code, X, ldx, m, k, Y, od);
   SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (const T*)X + m, ldx, k, Y, od, m,
                         static_cast<char*>(ws_base) + plan.offs[iP], st));
+  SQB_TRY(flush_copy_top(ctx, st));
   if (k == 1) {
     SQB_TRY(launch_coef_col(ctx, S, lds, Tm, ldt, transpose_t, Y, (int)od, (int)r, C));
   } else {

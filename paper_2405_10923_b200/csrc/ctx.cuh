@@ -51,6 +51,13 @@ struct sqb_ctx {
   std::vector<cudaEvent_t> trace_ev;
   std::vector<const char*> trace_name;
   size_t trace_used = 0;
+  // a copy of the identity-block rows (copy_top) waiting to ride on the next single-vector SRHT tree
+  // launch (defer_copy_top / flush_copy_top, sketch.cu): one launch less per sketch of an Arnoldi vector
+  bool top_pending = false;
+  const void* top_X = nullptr;
+  int64_t top_ldx = 0, top_m = 0, top_k = 0, top_ldy = 0;
+  double* top_Y = nullptr;
+  int top_dtype = 0;
   long long* dbg_cts = nullptr;  // instrumentation: column-pass block timeline of column dbg_ccol
   int dbg_ccol = -1;
   int nranks = 1;
@@ -170,6 +177,7 @@ inline int check_launch(sqb_ctx* ctx, const char* what) {
 inline int begin_entry(sqb_ctx* ctx) {
   if (!ctx) return SQB_ERR_ARG;
   ctx->err[0] = 0;
+  ctx->top_pending = false;  // a deferred copy_top never outlives the call that deferred it
   SQB_CUDA_TRY(cudaSetDevice(ctx->device));
   SQB_CUDA_TRY(cudaMemsetAsync(ctx->d_status, 0, sizeof(Status), ctx->stream));
   return SQB_OK;

@@ -430,8 +430,9 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
   // of every step is written straight into its basis column U[:, j-1] (rows
   // >= mt; the step kernel writes the identity rows): no copy of w into U.
   SQB_TRY(matvec_t<T>(ctx, op, (const T*)x0lo, b, (T*)U, t64, P, st));
-  SQB_TRY(launch_copy_top(ctx, Lo<T>::code, U, n, mt, 1, z, od, st));
+  defer_copy_top(ctx, Lo<T>::code, U, n, mt, 1, z, od);
   SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (T*)U + mt, n, 1, z, od, mt, P, st));
+  SQB_TRY(flush_copy_top(ctx, st));
   const size_t step_smem = sizeof(double) * (od + 3 * mt + 32);
   cudaFuncSetAttribute(arn_step_cl_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)std::max<size_t>(step_smem, 48 << 10));
@@ -468,8 +469,9 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
     SQB_TRY(apply_reflectors_dispatch(ctx, sk, mt, Lo<T>::code, U, ldu, n, j, S, lds, Tm, ldt, 1, w, n, 1, unext,
                                       ldu, ws_ptr<void>(ctx, plan, iAR)));
     // z = Psi w  (krylov.py:143)
-    SQB_TRY(launch_copy_top(ctx, Lo<T>::code, unext, n, mt, 1, z, od, st));
+    defer_copy_top(ctx, Lo<T>::code, unext, n, mt, 1, z, od);
     SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, unext + mt, n, 1, z, od, mt, P, st));
+    SQB_TRY(flush_copy_top(ctx, st));
     if (via_w)  // A/B: the unscaled w copied into its basis column
       SQB_CUDA_TRY(cudaMemcpyAsync((T*)U + (int64_t)j * ldu + mt, w + mt, sizeof(T) * (n - mt),
                                    cudaMemcpyDeviceToDevice, ctx->stream));

@@ -1112,10 +1112,15 @@ __global__ void __launch_bounds__(256)
 srht_tree_gmw_kernel(const typename Lo<T>::acc* __restrict__ P, int64_t n_tiles, int64_t n_eff,
                      const int64_t* __restrict__ idx, int ell, int log_tb,
                      typename Lo<T>::acc norm_lo, double* __restrict__ Y, int64_t ldy,
-                     int64_t row_off, const Status* st, int apply_norm) {
+                     int64_t row_off, const Status* st, int apply_norm, const T* __restrict__ Xtop = nullptr,
+                     int64_t ldxtop = 0, int mtop = 0) {
   if (st && failed(st)) return;
   const int k = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t col = blockIdx.y;
+  {  // a deferred copy of the identity-block rows Y[0:mtop] = X[0:mtop] (defer_copy_top)
+    const int gi = blockIdx.x * 256 + threadIdx.x;
+    if (Xtop && gi < mtop) Y[gi + col * ldy] = (double)Lo<T>::load(Xtop[gi + col * ldxtop]);
+  }
   if (k >= ell) return;
   const int64_t rhi = __ldg(idx + k) >> log_tb;
   const typename Lo<T>::acc v =
@@ -1348,8 +1353,15 @@ static int launch_tree_gm(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g,
   dim3 grid((unsigned)((sk->ell + 31) / 32), (unsigned)k);
   if (k <= 2 && g.n_tiles <= 65536) {  // warp_tile_tree's chunk stack limit
     dim3 gw((unsigned)((sk->ell + 7) / 8), (unsigned)k);
+    const T* xtop = nullptr;
+    if (ctx->top_pending && ctx->top_dtype == Lo<T>::code && ctx->top_k == k && ctx->top_Y == Y &&
+        ctx->top_ldy == ldy && ctx->top_m <= (int64_t)gw.x * 256 && ctx->top_m <= row_off) {
+      xtop = static_cast<const T*>(ctx->top_X);  // the deferred copy_top rides on this launch
+      ctx->top_pending = false;
+    }
     srht_tree_gmw_kernel<T><<<gw, 256, 0, ctx->stream>>>((const A*)P, g.n_tiles, g.n_eff, sk->indices,
-                                                         (int)sk->ell, g.log_tb, nm, Y, ldy, row_off, st, apply_norm);
+                                                         (int)sk->ell, g.log_tb, nm, Y, ldy, row_off, st, apply_norm,
+                                                         xtop, ctx->top_ldx, (int)ctx->top_m);
     return check_launch(ctx, "srht_tree_gmw_kernel");
   }
   if ((int64_t)grid.x * grid.y < 2 * ctx->sm_count && g.n_tiles >= 64)
@@ -1430,6 +1442,20 @@ static int copy_top_t(sqb_ctx* ctx, const void* X, int64_t ldx, int64_t m, int64
   dim3 grid((unsigned)std::min<int64_t>((m + 255) / 256, 1024), (unsigned)k);
   copy_top_kernel<T><<<grid, 256, 0, ctx->stream>>>((const T*)X, ldx, m, Y, ldy, st);
   return check_launch(ctx, "copy_top_kernel");
+}
+
+// Y[0:m, :k] = X[0:m, :k] deferred until the sketch that follows: a single-vector SRHT tree launch
+// (srht_tree_gmw_kernel) performs it; flush_copy_top launches copy_top_kernel if nothing took it
+void defer_copy_top(sqb_ctx* ctx, int dtype, const void* X, int64_t ldx, int64_t m, int64_t k, double* Y, int64_t ldy) {
+  ctx->top_pending = m > 0 && k > 0;
+  ctx->top_dtype = dtype; ctx->top_X = X; ctx->top_ldx = ldx; ctx->top_m = m; ctx->top_k = k; ctx->top_Y = Y;
+  ctx->top_ldy = ldy;
+}
+int flush_copy_top(sqb_ctx* ctx, const Status* st) {
+  if (!ctx->top_pending) return SQB_OK;
+  ctx->top_pending = false;
+  return launch_copy_top(ctx, ctx->top_dtype, ctx->top_X, ctx->top_ldx, ctx->top_m, ctx->top_k, ctx->top_Y,
+                         ctx->top_ldy, st);
 }
 
 int launch_copy_top(sqb_ctx* ctx, int dtype, const void* X, int64_t ldx, int64_t m, int64_t k,

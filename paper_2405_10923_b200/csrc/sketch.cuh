@@ -74,6 +74,8 @@ int launch_srht_tree_geom(sqb_ctx* ctx, const sqb_sketch* sk, int dtype, const S
 // Y[0:m, col] = X[0:m, col] as fp64 (identity block of Psi, sketching.py:257)
 int launch_copy_top(sqb_ctx* ctx, int dtype, const void* X, int64_t ldx, int64_t m, int64_t k,
                     double* Y, int64_t ldy, const Status* st);
+void defer_copy_top(sqb_ctx* ctx, int dtype, const void* X, int64_t ldx, int64_t m, int64_t k, double* Y, int64_t ldy);
+int flush_copy_top(sqb_ctx* ctx, const Status* st);
 
 // host rounding of the SRHT constants to the arithmetic dtype:
 // c = dtype(scale) (sketching.py:150) and dtype(n_pad^-1/2) (sketching.py:42)

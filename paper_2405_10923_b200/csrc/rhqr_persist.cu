@@ -30,7 +30,7 @@ namespace sqb {
 constexpr int PS_NT = 512;   // = STEP_NT: phase B's block reductions are the step kernel's
 constexpr int PS_LOG = 9;    // 512-row tiles (the launch-chain path's small-problem geometry)
 constexpr int PS_TB = 1 << PS_LOG;
-constexpr int PS_TILE = 0, PS_TOP = 1, PS_TCTA = 2;  // CTA roles of the fast-step kernel
+constexpr int PS_TILE = 0, PS_TOP = 1, PS_TCTA = 2, PS_ID = 3;  // CTA roles of the fast-step kernel
 static_assert(PS_NT == STEP_NT, "phase B replays the step kernel's 512-thread reductions");
 
 struct PersistArgs {
@@ -75,11 +75,11 @@ __device__ __forceinline__ long long gtimer() {
 __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
+    // release-add without waiting for the old value (a fence + atomicAdd round trip before the first
+    // poll cost ~0.6 us per column), then acquire-poll
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
     while (ld_acquire(ctr) < target) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -499,8 +499,8 @@ __device__ bool ps_step_fast(const PersistArgs& a, const PsSmem& s, int c, int r
   if (tid == pv) s.red[64] = g0;
   __syncthreads();
   double r2 = 0.0, t = 0.0;
-#pragma unroll
-  for (int w = 0; w < PS_NT / 32; ++w) { r2 += s.red[w]; t += s.red[32 + w]; }
+  const int nact = min(PS_NT / 32, (od + 31) / 32);  // warps past the last row hold exact zeros
+  for (int w = 0; w < nact; ++w) { r2 += s.red[w]; t += s.red[32 + w]; }
   const double gpv = s.red[64];
   PS_STAMP(c, 7);
   // rh_vector's scalars (rhqr.py:71-94), by every thread
@@ -727,8 +727,9 @@ __device__ void ps_identity_rows(const PersistArgs& a, const PsSmem& s, int c, d
 
 // ---------------------------------------------------------------------------
 // The fast-step persistent kernel (SQB_PERSIST=2): tile CTAs as in
-// rhqr_persist_kernel; the TOP CTA owns the identity rows and the sketches of
-// the columns ahead (ps_top_update) — everything the next barrier waits for;
+// rhqr_persist_kernel; the TOP CTA owns the sketches of the columns ahead
+// (ps_top_update), the ID CTA the identity-block rows of w_c — everything the
+// next barrier waits for, on two CTAs so neither chain outlasts a tile pass;
 // the T CTA writes the sketch-space outputs (S, R, U's identity rows, scalars)
 // and builds T by _extend_t (rhqr.py:135-140) with a whole column period to
 // do it.  Every CTA runs the single-reduction step (ps_step_fast).
@@ -738,24 +739,42 @@ __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_fast_kernel(PersistArgs
   const int m = a.m, od = a.od, tid = threadIdx.x;
   const PsSmem s = ps_carve(smem_raw, m, od);
   const int64_t g = blockIdx.x;
-  const int role = g < a.n_eff ? PS_TILE : (g == a.n_eff ? PS_TOP : PS_TCTA);
+  const int role = g < a.n_eff ? PS_TILE : (g == a.n_eff ? PS_TOP : (g == a.n_eff + 1 ? PS_TCTA : PS_ID));
   const bool top_cta = role == PS_TOP;  // PS_STAMP
   const unsigned G = gridDim.x;
   if (failed(a.st)) return;  // uniform: written before this kernel
   const int64_t e0 = g << PS_LOG;
   const int rows = role != PS_TILE ? 0 : (int)(a.n - e0 < PS_TB ? a.n - e0 : (int64_t)PS_TB);
   const int64_t ro = (int64_t)m + e0;
+  PS_STAMP(0, 0);
   if (role == PS_TILE) {
-    for (int k = 0; k < m; ++k)
-      for (int r = tid; r < rows; r += PS_NT) s.Ut[(size_t)k * PS_TB + r] = __ldg(a.W + ro + r + (int64_t)k * a.ldw);
+    // eight columns of the tile in flight per thread (the one-load-one-store loop spent one HBM round
+    // trip per column: ~16 us of the kernel's 235)
+    for (int k0 = 0; k0 < m; k0 += 8)
+      for (int r = tid; r < rows; r += PS_NT) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = k0 + u < m ? __ldg(a.W + ro + r + (int64_t)(k0 + u) * a.ldw) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (k0 + u < m) s.Ut[(size_t)(k0 + u) * PS_TB + r] = v[u];
+      }
   } else {
     for (int e = tid; e < m * m; e += PS_NT) s.Ts[e] = 0.0;
     if (role == PS_TOP)  // G_j = y0_j
-      for (int e = tid; e < m * od; e += PS_NT) s.Ss[e] = __ldg(a.Y0 + e);
+      for (int e0b = 0; e0b < m * od; e0b += 8 * PS_NT) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { const int e = e0b + u * PS_NT + tid; v[u] = e < m * od ? __ldg(a.Y0 + e) : 0.0; }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { const int e = e0b + u * PS_NT + tid; if (e < m * od) s.Ss[e] = v[u]; }
+      }
   }
   __syncthreads();
+  PS_STAMP(0, 1);
   double f_prev = 0.0, clast = 0.0;
   if (!ps_step_fast(a, s, 0, role, &f_prev, &clast)) return;
+  PS_STAMP(0, 2);
   unsigned nbar = 0;
   for (int c = 1; c < m; ++c) {
     PS_STAMP(c, 0);
@@ -764,6 +783,16 @@ __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_fast_kernel(PersistArgs
       for (int k = tid; k < c - 1; k += PS_NT) s.sc[k] = __ldcg(acur + k);
     }
     if (role == PS_TOP) ps_top_update(a, s, c - 1);
+    if (role == PS_ID) {
+      // the identity-block rows of u_{c-1} (= s_{c-1}[:m]) for this CTA's copy of U's top rows
+      __syncthreads();  // s.scal of step c-1
+      const double gamma = s.scal[1], f = s.scal[2];
+      const bool sq = a.scaling == SQB_SCALE_SQRT2;
+      for (int row = tid; row < m; row += PS_NT) {
+        const double yh = row < c - 1 ? 0.0 : (row == c - 1 ? gamma : s.yv[row]);
+        s.Utop[row + (size_t)(c - 1) * m] = sq ? __dmul_rn(yh, f) : __ddiv_rn(yh, f);
+      }
+    }
     if (role == PS_TCTA) {
       ps_t_post(a, s, c - 1);
       complete_t_column(s.Ts, m, c - 1, s.vs, s.sb[c - 1]);
@@ -772,8 +801,9 @@ __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_fast_kernel(PersistArgs
     __syncthreads();
     if (role == PS_TILE) {
       ps_tile_pass(a, s, c, g, rows, ro, e0, f_prev, clast);
+    } else if (role == PS_ID) {
+      ps_identity_rows(a, s, c, clast);  // y_c[0:m], off the TOP CTA's chain
     } else if (role == PS_TOP) {
-      ps_identity_rows(a, s, c, clast);
       if (c + 1 < m) {
         double* gd = a.gbuf + (size_t)((c + 1) & 1) * od;
         const double* Gn = s.Ss + (size_t)(c + 1) * od;
@@ -800,6 +830,7 @@ __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_fast_kernel(PersistArgs
     complete_t_column(s.Ts, m, m - 1, s.vs, s.sb[m - 1]);
     ps_copy_t_column(a, s, m - 1);
   }
+  PS_STAMP(0, 3);
 }
 
 // host side ------------------------------------------------------------------
@@ -822,7 +853,7 @@ bool persist_eligible(sqb_ctx* ctx, const sqb_sketch* sk, int64_t N, int64_t m, 
   if (m + sk->ell > 2 * PS_NT) return false;
   const int64_t n = N - m, od = m + sk->ell;
   const int64_t n_eff = (n + PS_TB - 1) / PS_TB;
-  if (n_eff + 2 > ctx->sm_count) return false;
+  if (n_eff + 3 > ctx->sm_count) return false;
   if (sizeof(double) * ps_base_doubles((int)m, (int)od) + 64 > 227 * 1024) return false;
   if (2 * m * m + 2 * m + 1 > m * PS_TB) return false;
   return true;
@@ -857,7 +888,7 @@ int launch_persist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const double
   void (*kern)(PersistArgs) = a.fast ? rhqr_persist_fast_kernel : rhqr_persist_kernel;
   SQB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(a.n_eff + (a.fast ? 2 : 1)));
+  cfg.gridDim = dim3((unsigned)(a.n_eff + (a.fast ? 3 : 1)));
   cfg.blockDim = dim3(PS_NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;

@@ -776,12 +776,11 @@ __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_fast_kernel(PersistArgs
   if (!ps_step_fast(a, s, 0, role, &f_prev, &clast)) return;
   PS_STAMP(0, 2);
   unsigned nbar = 0;
+  double sc_pref = 0.0;
   for (int c = 1; c < m; ++c) {
     PS_STAMP(c, 0);
-    if (role != PS_TCTA) {
-      const double* acur = a.abuf + (c & 1) * (m + 1);
-      for (int k = tid; k < c - 1; k += PS_NT) s.sc[k] = __ldcg(acur + k);
-    }
+    // a_c was published before barrier c-1 and fetched under the leaf loads of step c-1
+    if (role != PS_TCTA && tid < c - 1) s.sc[tid] = sc_pref;
     if (role == PS_TOP) ps_top_update(a, s, c - 1);
     if (role == PS_ID) {
       // the identity-block rows of u_{c-1} (= s_{c-1}[:m]) for this CTA's copy of U's top rows
@@ -816,6 +815,9 @@ __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_fast_kernel(PersistArgs
     grid_barrier(a.bar, ++nbar * G);
     PS_STAMP(c, 2);
     double f = 0.0, cl = 0.0;
+    // a_{c+1} (written by the TOP CTA before this barrier): in flight during the step instead of one
+    // more L2 round trip at the head of the next column pass (m <= 64 < PS_NT: one entry per thread)
+    sc_pref = (c + 1 < m && tid < c) ? __ldcg(a.abuf + ((c + 1) & 1) * (m + 1) + tid) : 0.0;
     if (!ps_step_fast(a, s, c, role, &f, &cl)) return;
     f_prev = f;
     clast = cl;

@@ -55,7 +55,7 @@ struct PersistArgs {
   double* gbuf;         // [2][od]  fast step: g_{c+1} = y0_{c+1} - S_c a_{c+1} (top CTA, phase A)
   int fast;             // 1: single-reduction step (ps_step_fast), not bitwise the launch chain
   int stage_leaves;     // 1: phase B copies the leaves to shared memory first
-  long long* dbg;       // optional globaltimer stamps [m][2][16] (instrumentation)
+  long long* dbg;       // optional clock64 stamps [m][4][16] (instrumentation)
   Status* st;
 };
 
@@ -81,6 +81,19 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
     while (ld_acquire(ctr) < target) {
     }
   }
+  __syncthreads();
+}
+
+// the two halves of the barrier for a CTA nobody waits for: it arrives as soon as it has consumed the
+// previous column's data (so the others never wait for its own work) and waits before reading the next
+__device__ __forceinline__ void grid_arrive(unsigned* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
+}
+__device__ __forceinline__ void grid_wait(unsigned* ctr, unsigned target) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(ctr) < target) {
+    }
   __syncthreads();
 }
 
@@ -129,10 +142,13 @@ __device__ inline PsSmem ps_carve(unsigned char* raw, int m, int od) {
   return s;
 }
 
+// stamps of tile CTA 0 (slot 0), the TOP CTA (1), and in the fast-step kernel the T CTA (2) and ID CTA (3)
 #define PS_STAMP(c, ph)                                                                     \
   do {                                                                                      \
-    if (a.dbg && threadIdx.x == 0 && (blockIdx.x == 0 || top_cta))                           \
-      a.dbg[((int64_t)(c) * 2 + (top_cta ? 1 : 0)) * 16 + (ph)] = clock64();                  \
+    if (a.dbg && threadIdx.x == 0) {                                                        \
+      const int slot__ = top_cta ? 1 : (blockIdx.x == 0 ? 0 : (int)blockIdx.x - (int)a.n_eff + 1); \
+      if (slot__ >= 0 && slot__ < 4) a.dbg[((int64_t)(c) * 4 + slot__) * 16 + (ph)] = clock64(); \
+    }                                                                                       \
   } while (0)
 
 // The SRHT tree over a row's tile leaves by ONE thread: a binary counter over
@@ -574,28 +590,53 @@ __device__ inline void ps_copy_t_column(const PersistArgs& a, const PsSmem& s, i
 __device__ void ps_tile_pass(const PersistArgs& a, const PsSmem& s, int c, int64_t g, int rows, int64_t ro,
                              int64_t e0, double f_prev, double clast) {
   const int tid = threadIdx.x;
+  static_assert(PS_TB == PS_NT, "one tile row per thread");
   double* tb = s.tile;
-  for (int r = tid; r < PS_TB; r += PS_NT) {
-    double w = 0.0;
-    if (r < rows) {
-      // final columns 0 .. c-2, one fma chain per row (rhqr_col_kernel order)
-      double acc = 0.0;
-      for (int k = 0; k < c - 1; ++k) acc = fma(s.Ut[(size_t)k * PS_TB + r], s.sc[k], acc);
-      // column c-1: lazy scaling of the stored w_{c-1} (rhqr.py:86-95)
-      double x = lazy_scale<double>(s.Ut[(size_t)(c - 1) * PS_TB + r], f_prev, a.scaling);
-      s.Ut[(size_t)(c - 1) * PS_TB + r] = x;
-      a.U[ro + r + (int64_t)(c - 1) * a.ldu] = x;
-      acc = fma(x, clast, acc);
-      w = __dsub_rn(s.Ut[(size_t)c * PS_TB + r], acc);
-      s.Ut[(size_t)c * PS_TB + r] = w;
-    }
-    const int64_t e = e0 + r;
-    tb[pidx<double>(r)] = r < rows ? srht_in<double>(w, a.scale_lo, sign_neg(a.bits, e)) : 0.0;
+  const int r = tid;
+  double w = 0.0;
+  if (r < rows) {
+    // final columns 0 .. c-2, one fma chain per row (rhqr_col_kernel order)
+    double acc = 0.0;
+    for (int k = 0; k < c - 1; ++k) acc = fma(s.Ut[(size_t)k * PS_TB + r], s.sc[k], acc);
+    // column c-1: lazy scaling of the stored w_{c-1} (rhqr.py:86-95)
+    double x = lazy_scale<double>(s.Ut[(size_t)(c - 1) * PS_TB + r], f_prev, a.scaling);
+    s.Ut[(size_t)(c - 1) * PS_TB + r] = x;
+    a.U[ro + r + (int64_t)(c - 1) * a.ldu] = x;
+    acc = fma(x, clast, acc);
+    w = __dsub_rn(s.Ut[(size_t)c * PS_TB + r], acc);
+    s.Ut[(size_t)c * PS_TB + r] = w;
   }
+  // in-tile FWHT of the 512 values, one per thread: stages h = 1..16 are lane
+  // butterflies (the pair (i, i|h) becomes (x_i + x_{i|h}, x_i - x_{i|h}), the
+  // operations of tile_fwht in its order), stages h = 32..256 are evaluated
+  // only at the ell sampled positions — output p is the binary tree over the
+  // 16 values {(p & 31) + 32 j}, level l taking left +/- right by bit 5 + l of
+  // p: exactly the butterflies that feed position p.  Same bits as
+  // tile_fwht + tile_gather, two shared-memory passes and the gather fewer.
+  double v = r < rows ? srht_in<double>(w, a.scale_lo, sign_neg(a.bits, e0 + r)) : 0.0;
+  const int lane = tid & 31;
+#pragma unroll
+  for (int h = 1; h < 32; h <<= 1) {
+    const double o = __shfl_xor_sync(0xffffffffu, v, h);
+    v = (lane & h) ? __dsub_rn(o, v) : __dadd_rn(v, o);
+  }
+  tb[r] = v;
   __syncthreads();
-  tile_fwht<double>(tb, PS_LOG);
-  tile_gather<double>(tb, a.idx, a.ell, PS_LOG, a.leaves + (int64_t)(c & 1) * a.ell * a.n_tiles + g,
-                      a.n_tiles);
+  double* P = a.leaves + (int64_t)(c & 1) * a.ell * a.n_tiles + g;
+  for (int k = tid; k < a.ell; k += PS_NT) {
+    const int p = (int)(__ldg(a.idx + k) & (PS_TB - 1));
+    const double* q = tb + (p & 31);
+    double x[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = q[32 * j];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const bool neg = (p >> (5 + l)) & 1;
+#pragma unroll
+      for (int j = 0; j < 16; j += (2 << l)) x[j] = neg ? __dsub_rn(x[j], x[j + (1 << l)]) : __dadd_rn(x[j], x[j + (1 << l)]);
+    }
+    P[(int64_t)k * a.n_tiles] = x[0];
+  }
 }
 
 __device__ void ps_identity_rows(const PersistArgs& a, const PsSmem& s, int c, double clast);
@@ -793,6 +834,10 @@ __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_fast_kernel(PersistArgs
       }
     }
     if (role == PS_TCTA) {
+      // nothing this CTA writes is read inside the kernel: it arrives at barrier c now, having consumed
+      // the data of column c-1, and only waits for it below — its 1.7 us of output work (S, R, U's
+      // identity rows, T's column) no longer sits between the tile passes and the barrier
+      grid_arrive(a.bar);
       ps_t_post(a, s, c - 1);
       complete_t_column(s.Ts, m, c - 1, s.vs, s.sb[c - 1]);
       ps_copy_t_column(a, s, c - 1);
@@ -812,7 +857,8 @@ __global__ void __launch_bounds__(PS_NT, 1) rhqr_persist_fast_kernel(PersistArgs
       }
     }
     PS_STAMP(c, 1);
-    grid_barrier(a.bar, ++nbar * G);
+    if (role == PS_TCTA) grid_wait(a.bar, ++nbar * G);
+    else grid_barrier(a.bar, ++nbar * G);
     PS_STAMP(c, 2);
     double f = 0.0, cl = 0.0;
     // a_{c+1} (written by the TOP CTA before this barrier): in flight during the step instead of one

@@ -22,21 +22,22 @@ Wd = to_device(W, "double", align_row=m)
 psi = _embed(om, N, m)
 pol = P.PrecisionPolicy("double", "double")
 ctx = _lib.context()
-buf = torch.zeros(m * 2 * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(m * 4 * 16, dtype=torch.int64, device="cuda")
 for _ in range(3):
     rhqr_left_device(Wd, psi, "sqrt2", pol, check=False)
 _lib.lib().sqb_debug_step_stamps(ctx.h, buf.data_ptr(), -2)
 rhqr_left_device(Wd, psi, "sqrt2", pol, check=False)
 torch.cuda.synchronize()
 _lib.lib().sqb_debug_step_stamps(ctx.h, None, -1)
-t = buf.cpu().numpy().reshape(m, 2, 16).astype(np.float64) / 1.965  # clock64 cycles -> ns at 1965 MHz
+t = buf.cpu().numpy().reshape(m, 4, 16).astype(np.float64) / 1.965  # clock64 cycles -> ns at 1965 MHz
 if os.environ["SQB_PERSIST"] == "2":
     for who, name in ((0, "tile CTA 0"), (1, "top CTA")):
         z = t[0, who]
         last = t[m - 1, who, 3]
         print(f"{name}: prologue {(z[1]-z[0])/1e3:.2f} us, step 0 {(z[2]-z[1])/1e3:.2f} us, "
               f"column loop {(last - z[2])/1e3:.2f} us, epilogue {(z[3]-last)/1e3:.2f} us, kernel {(z[3]-z[0])/1e3:.2f} us")
-for who, name in ((0, "tile CTA 0"), (1, "top CTA")):
+whos = ((0, "tile CTA 0"), (1, "top CTA")) + (((2, "T CTA"), (3, "ID CTA")) if os.environ["SQB_PERSIST"] == "2" else ())
+for who, name in whos:
     x = t[1:, who]
     A = x[:, 1] - x[:, 0]
     Wt = x[:, 2] - x[:, 1]

@@ -306,6 +306,12 @@ int sqb_p2p_mailbox(sqb_ctx* ctx, int nranks, int64_t count, void* handle_out);
 int sqb_p2p_open(sqb_ctx* ctx, int rank, const void* handles);
 int sqb_p2p_virtual(sqb_ctx* ctx, int nranks, int64_t count);
 int sqb_p2p_close(sqb_ctx* ctx);
+/* A consumer that waits longer than `ms` (default 20 s; 0 restores it) for a
+ * peer's flag records SQB_ERR_NCCL with col = -(peer + 1) in the device status
+ * instead of spinning for ever (a rank that died must not hang the others'
+ * streams).  An all-zero handle in sqb_p2p_open's table stands for such a
+ * peer (tests). */
+int sqb_p2p_set_timeout_ms(sqb_ctx* ctx, int64_t ms);
 
 /* Halo ranges of the row-partitioned SpMV in the distributed RHQR-Arnoldi
  * (exchange only the referenced entries — one grid row with

@@ -100,6 +100,7 @@ _SIGS = {
     "sqb_p2p_open": ([vp, C.c_int, vp], C.c_int),
     "sqb_p2p_virtual": ([vp, C.c_int, i64], C.c_int),
     "sqb_p2p_close": ([vp], C.c_int),
+    "sqb_p2p_set_timeout_ms": ([vp, i64], C.c_int),
     "sqb_rhqr_left_dist": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, dp, i64, i64, i64, dp, i64, dp, i64,
                             dp, i64, dp, i64, dp, dp, dp, dp], C.c_int),
     "sqb_rhqr_left_virtual": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, C.c_int, C.POINTER(vp),

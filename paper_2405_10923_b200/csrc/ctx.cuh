@@ -81,6 +81,7 @@ struct sqb_ctx {
   int64_t p2p_count = 0;                // doubles per (parity, rank) slot
   std::vector<void*> p2p_local;         // own mailbox(es): 1, or nranks for virtual ranks
   std::vector<void*> p2p_opened;        // IPC-opened peer mailboxes
+  std::vector<void*> p2p_absent;        // stand-ins for peers that never answer (fault injection)
   void** p2p_table = nullptr;           // device [n_local][nranks] mailbox bases
   unsigned long long p2p_seq = 0;       // exchanges so far (identical on every rank)
 };

@@ -64,7 +64,7 @@ __global__ void rank_combine_kernel(const double* __restrict__ G, int nranks, in
                                     int64_t rank_stride = -1, const unsigned long long* flags = nullptr,
                                     int parity = 0, unsigned long long seq = 0) {
   using A = typename Lo<T>::acc;
-  p2p_wait(flags, nranks, parity, seq);  // peer-memory exchange: the peers' partials have landed
+  p2p_wait(flags, nranks, parity, seq, st);  // peer-memory exchange: the peers' partials have landed
   if (failed(st)) return;
   const int64_t rs = rank_stride < 0 ? (int64_t)ncols * (ell + m) : rank_stride;
   const int pl = ell + m;

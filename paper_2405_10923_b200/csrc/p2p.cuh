@@ -18,7 +18,8 @@ namespace sqb {
 // rank runs before it produces the next payload (stream order).
 // ---------------------------------------------------------------------------
 __host__ __device__ inline size_t p2p_flag_bytes(int nranks) {
-  return ((size_t)2 * nranks * sizeof(unsigned long long) + 255) & ~size_t(255);
+  // [2][nranks] flags, then one word: the wait timeout in ns (0 = P2P_TIMEOUT_NS)
+  return ((size_t)(2 * nranks + 1) * sizeof(unsigned long long) + 255) & ~size_t(255);
 }
 __host__ __device__ inline size_t p2p_mailbox_bytes(int nranks, int64_t count) {
   return p2p_flag_bytes(nranks) + sizeof(double) * 2 * (size_t)nranks * (size_t)count;
@@ -38,13 +39,39 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 }
 
 // spin until every rank's flag of this parity reached seq (threads < nranks
-// poll, the block then proceeds); flags == nullptr: nothing to wait for
+// poll, the block then proceeds); flags == nullptr: nothing to wait for.
+// A peer that never arrives (a rank that died, a mapping that went away)
+// must not hang the stream: after P2P_TIMEOUT_NS of polling the waiter
+// records SQB_ERR_NCCL (col = -(peer + 1), val = seq) in the device status
+// and the call chain becomes a no-op like any other failure.  The word after
+// the flags of the waiter's own mailbox overrides the limit
+// (sqb_p2p_set_timeout_ms).
+constexpr long long P2P_TIMEOUT_NS = 20LL * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ long long p2p_now_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void p2p_wait(const unsigned long long* flags, int nranks, int parity,
-                                         unsigned long long seq) {
+                                         unsigned long long seq, const Status* st = nullptr) {
   if (!flags) return;
-  if ((int)threadIdx.x < nranks)
-    while (ld_acquire_sys(flags + parity * nranks + threadIdx.x) < seq) {
+  if ((int)threadIdx.x < nranks) {
+    const unsigned long long* f = flags + parity * nranks + threadIdx.x;
+    if (ld_acquire_sys(f) < seq) {
+      const long long t0 = p2p_now_ns();
+      const long long tset = (long long)__ldcg(flags + 2 * nranks);
+      const long long limit = tset > 0 ? tset : P2P_TIMEOUT_NS;
+      unsigned polls = 0;
+      while (ld_acquire_sys(f) < seq) {
+        if ((++polls & 0xffu) == 0 && p2p_now_ns() - t0 > limit) {
+          if (st) fail(const_cast<Status*>(st), SQB_ERR_NCCL, -((int)threadIdx.x + 1), (double)seq);
+          break;
+        }
+      }
     }
+  }
   __syncthreads();
 }
 

@@ -391,13 +391,20 @@ using namespace sqb;
 static int p2p_release(sqb_ctx* ctx) {
   for (void* p : ctx->p2p_opened) cudaIpcCloseMemHandle(p);
   for (void* p : ctx->p2p_local) cudaFree(p);
+  for (void* p : ctx->p2p_absent) cudaFree(p);
+  ctx->p2p_absent.clear();
   if (ctx->p2p_table) cudaFree(ctx->p2p_table);
   ctx->p2p_opened.clear();
   ctx->p2p_local.clear();
   ctx->p2p_table = nullptr;
+  if (ctx->p2p_on && !ctx->nccl) {  // the partition sqb_p2p_open set goes with the mailboxes
+    ctx->nranks = 1;
+    ctx->rank = 0;
+  }
   ctx->p2p_on = 0;
   ctx->p2p_nranks = 0;
   ctx->p2p_count = 0;
+  ctx->p2p_seq = 0;  // fresh mailboxes have zero flags (every rank re-opens collectively)
   return SQB_OK;
 }
 
@@ -455,9 +462,16 @@ int sqb_p2p_open(sqb_ctx* ctx, int rank, const void* handles) {
     }
     cudaIpcMemHandle_t h;
     memcpy(&h, static_cast<const char*>(handles) + (size_t)q * sizeof(h), sizeof(h));
+    bool absent = true;  // an all-zero handle: a peer that never answers (fault injection, tests)
+    for (size_t b = 0; b < sizeof(h); ++b) absent = absent && reinterpret_cast<const char*>(&h)[b] == 0;
     void* p = nullptr;
-    SQB_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-    ctx->p2p_opened.push_back(p);
+    if (absent) {
+      SQB_TRY(p2p_alloc(ctx, P, ctx->p2p_count, &p));
+      ctx->p2p_absent.push_back(p);  // freed with the mailboxes
+    } else {
+      SQB_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      ctx->p2p_opened.push_back(p);
+    }
     table[q] = p;
   }
   SQB_TRY(p2p_set_table(ctx, table));
@@ -484,6 +498,16 @@ int sqb_p2p_virtual(sqb_ctx* ctx, int nranks, int64_t count) {
   ctx->p2p_count = count;
   SQB_TRY(p2p_set_table(ctx, table));
   ctx->p2p_on = 1;
+  return SQB_OK;
+}
+
+int sqb_p2p_set_timeout_ms(sqb_ctx* ctx, int64_t ms) {
+  if (!ctx || ms < 0 || ctx->p2p_local.empty()) return SQB_ERR_ARG;
+  SQB_CUDA_TRY(cudaSetDevice(ctx->device));
+  const unsigned long long ns = (unsigned long long)ms * 1000000ull;
+  for (void* mb : ctx->p2p_local)
+    SQB_CUDA_TRY(cudaMemcpy(reinterpret_cast<unsigned long long*>(mb) + 2 * ctx->p2p_nranks, &ns, sizeof(ns),
+                            cudaMemcpyHostToDevice));
   return SQB_OK;
 }
 

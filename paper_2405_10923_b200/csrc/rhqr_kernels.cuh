@@ -696,7 +696,7 @@ rhqr_step_kernel(StepArgs a) {
       st_release_sys(reinterpret_cast<unsigned long long*>(a.peers[tid]) + par * a.nranks + a.my_rank, a.seq);
     }
   }
-  if (a.tree >= 2) p2p_wait(a.flags, a.nranks, (int)(a.seq & 1), a.seq);
+  if (a.tree >= 2) p2p_wait(a.flags, a.nranks, (int)(a.seq & 1), a.seq, a.st);
   SQB_STAMP(1);
   const bool dead = failed(a.st);  // uniform across the cluster; still take part in the sync
   // ---- phase A: y on the owned rows (identity block given; Omega rows from the tree)

@@ -114,6 +114,13 @@ def init_p2p(m: int, ell: int, group=None):
     return ctx
 
 
+def set_p2p_timeout(ms: int):
+    """Bound the in-kernel wait for a peer's flag (default 20 s): past it the
+    call fails with SketchQRError naming the silent rank instead of hanging."""
+    ctx = _lib.context()
+    ctx.check(_lib.lib().sqb_p2p_set_timeout_ms(ctx.h, int(ms)), "sqb_p2p_set_timeout_ms")
+
+
 def close_p2p():
     ctx = _lib.context()
     ctx.check(_lib.lib().sqb_p2p_close(ctx.h), "sqb_p2p_close")

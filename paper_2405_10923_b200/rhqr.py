@@ -94,6 +94,8 @@ def raise_status(ctx, what="factorization", tag=None):
         raise BreakdownError(f"reflector scale degenerated at column {col} (rho={val:.3e})")
     if code == _lib.SQB_ERR_SINGULAR:
         raise SingularFactorError(f"triangular factor has zero or subnormal diagonal at index {col - 1}")
+    if code == _lib.SQB_ERR_NCCL and col < 0:  # p2p_wait (csrc/p2p.cuh): a peer's flag never arrived
+        raise _lib.SketchQRError(f"{what}: peer-memory exchange {int(val)} timed out waiting for rank {-col - 1}")
     raise _lib.SketchQRError(f"{what}: device status {code} at column {col}")
 
 

@@ -81,3 +81,39 @@ def test_p2p_world1_ipc_path(P, monkeypatch):
     finally:
         if created:
             dist.destroy_process_group()
+
+
+def test_p2p_silent_peer_times_out_instead_of_hanging(P, monkeypatch):
+    """Failure detection of the in-kernel exchange: rank 0 of a 2-rank
+    partition whose peer never publishes its flag (an all-zero IPC handle
+    stands for it) must fail with an error naming rank 1 after the wait
+    limit, and the context must be usable again afterwards."""
+    monkeypatch.setenv("SQB_PERSIST", "0")
+    import ctypes as C
+    import torch.distributed as dist
+    from paper_2405_10923_b200 import _lib, dist as D
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(29900 + os.getpid() % 90))
+    created = False
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", rank=0, world_size=1)
+        created = True
+    N, m, ell = (1 << 14) + 5, 16, 64
+    W = np.random.default_rng(0).standard_normal((N, m))
+    om = P.SRHTSketch(ell, N - m, 3)
+    ctx = _lib.context()
+    try:
+        h = C.create_string_buffer(64)
+        ctx.check(_lib.lib().sqb_p2p_mailbox(ctx.h, 2, D.p2p_slot_count(m, ell), h), "sqb_p2p_mailbox")
+        table = C.create_string_buffer(h.raw + bytes(64), 128)
+        ctx.check(_lib.lib().sqb_p2p_open(ctx.h, 0, table), "sqb_p2p_open")
+        D.set_p2p_timeout(50)
+        rows0 = D.local_rows(N, m, om.n_pad, 2, 0, "double")
+        with pytest.raises(_lib.SketchQRError, match="timed out waiting for rank 1"):
+            D.rhqr_left_distributed(W[rows0], om, m)
+    finally:
+        D.close_p2p()
+        if created:
+            dist.destroy_process_group()
+    F = P.rhqr_left(W, om)  # the status word was consumed: the next call runs
+    assert np.isfinite(F.R).all()

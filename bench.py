@@ -254,6 +254,20 @@ class RHQRLeft(Workload):
                     sys.stderr.write(f"[bench] rank {rank}: peer-memory exchange unavailable ({exc}); using NCCL\n")
                 flag = torch.tensor([ok], device="cuda")
                 dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+                if int(flag.item()) == 1 and mode == "auto":
+                    # one trial factorization over the mailboxes with a short wait limit: a peer whose stores or
+                    # flags never arrive (no NVLink path behind the mapping) shows up here as a timeout error on
+                    # some rank, and every rank then falls back to NCCL together
+                    try:
+                        D.set_p2p_timeout(5000)
+                        D.rhqr_left_distributed(self.Wd, self.om, m, policy=pol, check=True)
+                        torch.cuda.synchronize()
+                        D.set_p2p_timeout(0)
+                    except Exception as exc:  # noqa: BLE001
+                        ok = 0
+                        sys.stderr.write(f"[bench] rank {rank}: peer-memory trial failed ({exc}); using NCCL\n")
+                    flag = torch.tensor([ok], device="cuda")
+                    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
                 if int(flag.item()) == 1:
                     self.exchange = "peer-memory mailboxes, exchange inside the step kernel (NVLink stores + release/acquire flags)"
                 else:

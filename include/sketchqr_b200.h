@@ -224,7 +224,9 @@ int sqb_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype
 
 /* Trimmed left-looking RHQR (trim_rhqr_left, trim.py:272-325).  The sketch
  * sk acts on all N coordinates; the column-scaled wrapper (sketching.py:
- * 216-235) multiplies coordinates k < m by scales[k] first, and E (ell x m,
+ * 216-235) multiplies coordinates k < mscale by scales[k] first (mscale >= m:
+ * the span the operator was normalised over — an operator wrapped for more
+ * columns than W has is used unchanged, trim.py:59-60), and E (ell x m,
  * ld lde) holds its unit leading-column sketches (normalize_leading_columns,
  * trim.py:51-77, built by the caller).  Outputs U (N x m, lo dtype, 16-byte
  * aligned), S (ell x m), T, T~, R, L (m x m, fp64) and the scalars.
@@ -232,7 +234,7 @@ int sqb_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype
  * annihilated, 1: sketched reflector cancelled, val = norm; 2: unit pivot
  * vanished, val = pivot).                                                 */
 int sqb_trim_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
-                       const double* E, int64_t lde, int scaling, int lo_dtype,
+                       int64_t mscale, const double* E, int64_t lde, int scaling, int lo_dtype,
                        const void* W, int64_t N, int64_t m, int64_t ldw,
                        void* U, int64_t ldu, double* S, int64_t lds,
                        double* T, int64_t ldt, double* Tt, int64_t ldtt,
@@ -244,7 +246,7 @@ int sqb_trim_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
  * sketch; T = t_factor_from_sketches(S), T~ = t_tilde_from_factors(S, E, U),
  * L = tril(S^t E, -1) after the sweep.  Arguments as sqb_trim_rhqr_left.  */
 int sqb_trim_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
-                        const double* E, int64_t lde, int scaling, int lo_dtype,
+                        int64_t mscale, const double* E, int64_t lde, int scaling, int lo_dtype,
                         const void* W, int64_t N, int64_t m, int64_t ldw,
                         void* U, int64_t ldu, double* S, int64_t lds,
                         double* T, int64_t ldt, double* Tt, int64_t ldtt,

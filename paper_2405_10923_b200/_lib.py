@@ -73,10 +73,10 @@ _SIGS = {
     "sqb_rhqr_right": ([vp, C.POINTER(SketchDesc), C.c_int, C.c_int, dp, i64, i64, i64, dp, i64,
                         dp, i64, dp, i64, dp, i64, dp, dp, dp], C.c_int),
     "sqb_t_factor": ([vp, dp, i64, i64, i64, dp, i64], C.c_int),
-    "sqb_trim_rhqr_left": ([vp, C.POINTER(SketchDesc), dp, dp, i64, C.c_int, C.c_int, dp, i64, i64, i64,
+    "sqb_trim_rhqr_left": ([vp, C.POINTER(SketchDesc), dp, i64, dp, i64, C.c_int, C.c_int, dp, i64, i64, i64,
                             dp, i64, dp, i64, dp, i64, dp, i64, dp, i64, dp, i64, dp, dp, dp], C.c_int),
     "sqb_ctx_set_halo": ([vp, C.c_int, vp], C.c_int),
-    "sqb_trim_rhqr_right": ([vp, C.POINTER(SketchDesc), dp, dp, i64, C.c_int, C.c_int, dp, i64, i64, i64,
+    "sqb_trim_rhqr_right": ([vp, C.POINTER(SketchDesc), dp, i64, dp, i64, C.c_int, C.c_int, dp, i64, i64, i64,
                              dp, i64, dp, i64, dp, i64, dp, i64, dp, i64, dp, i64, dp, dp, dp], C.c_int),
     "sqb_colscaled_apply": ([vp, C.POINTER(SketchDesc), dp, i64, C.c_int, dp, i64, i64, dp, i64], C.c_int),
     "sqb_trim_thin_q": ([vp, C.c_int, dp, i64, i64, i64, dp, i64, dp, i64, dp, i64, i64, dp, i64], C.c_int),

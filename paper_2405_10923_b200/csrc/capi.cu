@@ -20,10 +20,10 @@ int sketch_q_run(sqb_ctx*, int, const void*, int64_t, int64_t, const double*, in
 int rhqr_block_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t, int64_t,
                         void*, int64_t, double*, int64_t, double*, int64_t, double*, int64_t, double*, double*,
                         double*);
-int trim_left_dispatch(sqb_ctx*, const sqb_sketch*, const double*, const double*, int64_t, int, int, const void*,
+int trim_left_dispatch(sqb_ctx*, const sqb_sketch*, const double*, int64_t, const double*, int64_t, int, int, const void*,
                        int64_t, int64_t, int64_t, void*, int64_t, double*, int64_t, double*, int64_t, double*,
                        int64_t, double*, int64_t, double*, int64_t, double*, double*, double*);
-int trim_right_dispatch(sqb_ctx*, const sqb_sketch*, const double*, const double*, int64_t, int, int, const void*,
+int trim_right_dispatch(sqb_ctx*, const sqb_sketch*, const double*, int64_t, const double*, int64_t, int, int, const void*,
                         int64_t, int64_t, int64_t, void*, int64_t, double*, int64_t, double*, int64_t, double*,
                         int64_t, double*, int64_t, double*, int64_t, double*, double*, double*);
 int colscaled_apply_dispatch(sqb_ctx*, const sqb_sketch*, const double*, int64_t, int, const void*, int64_t,
@@ -285,7 +285,8 @@ int sqb_rhqr_block(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype
                              ldr, sigmas, rhos, betas);
 }
 
-int sqb_trim_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+int sqb_trim_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t mscale, const double* E,
+                       int64_t lde,
                        int scaling, int lo_dtype, const void* W, int64_t N, int64_t m, int64_t ldw, void* U,
                        int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt, double* Tt, int64_t ldtt,
                        double* R, int64_t ldr, double* L, int64_t ldl, double* sigmas, double* rhos,
@@ -302,17 +303,21 @@ int sqb_trim_rhqr_left(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
   if (m > N) return set_error(ctx, SQB_ERR_ARG, "cannot normalize %lld leading columns of %lld inputs",
                               (long long)m, (long long)N);
   if (!scales || !E || lde < sk->ell) return set_error(ctx, SQB_ERR_ARG, "column-scaled operator without scales/E");
+  if (mscale < m || mscale > N)
+    return set_error(ctx, SQB_ERR_ARG, "operator normalised over %lld leading columns, W has %lld", (long long)mscale,
+                     (long long)m);
   if (ldw < N || ldu < N || lds < sk->ell || ldt < m || ldtt < m || ldr < m || ldl < m)
     return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
   const int64_t esz = lo_dtype == SQB_F64 ? 8 : lo_dtype == SQB_F32 ? 4 : 2;
   if ((reinterpret_cast<uintptr_t>(U) & 15) || (ldu * esz) % 16)
     return set_error(ctx, SQB_ERR_ARG, "U must be 16-byte aligned with a 16-byte multiple leading dimension");
-  SQB_TRY(trim_left_dispatch(ctx, sk, scales, E, lde, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, T, ldt, Tt,
+  SQB_TRY(trim_left_dispatch(ctx, sk, scales, mscale, E, lde, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, T, ldt, Tt,
                              ldtt, R, ldr, L, ldl, sigmas, rhos, betas));
   return SQB_OK;
 }
 
-int sqb_trim_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+int sqb_trim_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t mscale, const double* E,
+                       int64_t lde,
                         int scaling, int lo_dtype, const void* W, int64_t N, int64_t m, int64_t ldw, void* U,
                         int64_t ldu, double* S, int64_t lds, double* T, int64_t ldt, double* Tt, int64_t ldtt,
                         double* R, int64_t ldr, double* L, int64_t ldl, double* sigmas, double* rhos,
@@ -331,9 +336,12 @@ int sqb_trim_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
   if (m > N) return set_error(ctx, SQB_ERR_ARG, "cannot normalize %lld leading columns of %lld inputs",
                               (long long)m, (long long)N);
   if (!scales || !E || lde < sk->ell) return set_error(ctx, SQB_ERR_ARG, "column-scaled operator without scales/E");
+  if (mscale < m || mscale > N)
+    return set_error(ctx, SQB_ERR_ARG, "operator normalised over %lld leading columns, W has %lld", (long long)mscale,
+                     (long long)m);
   if (ldw < N || ldu < N || lds < sk->ell || ldt < m || ldtt < m || ldr < m || ldl < m)
     return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
-  SQB_TRY(trim_right_dispatch(ctx, sk, scales, E, lde, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, T, ldt, Tt,
+  SQB_TRY(trim_right_dispatch(ctx, sk, scales, mscale, E, lde, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, T, ldt, Tt,
                               ldtt, R, ldr, L, ldl, sigmas, rhos, betas));
   return SQB_OK;
 }

@@ -280,7 +280,7 @@ __global__ void trim_ucol_kernel(T* __restrict__ Uc, const T* __restrict__ w, in
 }
 
 template <typename T>
-static int trim_left_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+static int trim_left_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t ms, const double* E, int64_t lde,
                        int scaling, const void* W, int64_t N, int64_t m, int64_t ldw, void* Uv, int64_t ldu,
                        double* S, int64_t lds, double* Tm, int64_t ldt, double* Tt, int64_t ldtt, double* R,
                        int64_t ldr, double* L, int64_t ldl, double* sig, double* rho, double* bet) {
@@ -323,7 +323,7 @@ static int trim_left_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
                                                                        2 * ctx->sm_count));
   if (m > 1) {
     const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 2 * ctx->sm_count));
-    trim_prep_batch_kernel<T><<<dim3(gb, (unsigned)(m - 1)), 256, 0, s>>>(Xa, ldx, (const T*)W, ldw, N, m,
+    trim_prep_batch_kernel<T><<<dim3(gb, (unsigned)(m - 1)), 256, 0, s>>>(Xa, ldx, (const T*)W, ldw, N, ms,
                                                                           scales, st);
     SQB_TRY(check_launch(ctx, "trim_prep_batch_kernel"));
     SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, Xa, ldx, m - 1, Z0 + ell, ell, 0, P, st));
@@ -336,7 +336,7 @@ static int trim_left_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales,
     }
     SQB_TRY(launch_pdl(ctx, "trim_update_kernel", trim_update_kernel<T>, dim3(gu), dim3(GEMV_NT),
                        sizeof(typename Lo<T>::acc) * std::max<int64_t>(c, 1), (const T*)U, ldu, N, (int)c,
-                       (const double*)coef, (const T*)W + c * ldw, w, x, m, scales, (const Status*)st));
+                       (const double*)coef, (const T*)W + c * ldw, w, x, ms, scales, (const Status*)st));
     SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, z, ell, 0, P, st));
     SQB_TRY(launch_pdl(ctx, "trim_tail_kernel", trim_tail_kernel<T>, dim3(1), dim3(TRIM_NT), 0, (const double*)z,
                        (int)ell, (const T*)w, (int)c, scales, x, scal, st));
@@ -385,23 +385,28 @@ int colscaled_apply_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, const double* s
   return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", dtype);
 }
 
-// M = T triu(S^t E)   (k x k, ld k; T upper so M[i, j] = sum_{l >= i} T[i, l] triu(S^t E)[l, j])
-__global__ void trim_tm_kernel(const double* __restrict__ Tm, int64_t ldt, const double* __restrict__ S,
-                               int64_t lds, const double* __restrict__ E, int64_t lde, int ell, int k,
-                               double* __restrict__ M) {
-  extern __shared__ double G[];  // k x k: triu(S^t E)
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    const int l = e % k, j = e / k;
+// G = triu(S^t E) (k x k, ld k), then M = T G (T upper, so M[i, j] = sum_{i <= l <= j} T[i, l] G[l, j]).
+// One thread per entry with the sums in index order; G lives in the workspace (k is not bounded by
+// shared memory: the acceptance runs of the reference use k = 300).
+__global__ void trim_g_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict__ E, int64_t lde,
+                              int ell, int k, double* __restrict__ G) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int l = (int)(e % k), j = (int)(e / k);
     double d = 0.0;
     if (l <= j)
       for (int i = 0; i < ell; ++i) d = fma(S[i + (int64_t)l * lds], E[i + (int64_t)j * lde], d);
     G[e] = d;
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    const int i = e % k, j = e / k;
+}
+
+__global__ void trim_tm_kernel(const double* __restrict__ Tm, int64_t ldt, const double* __restrict__ G, int k,
+                               double* __restrict__ M) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % k), j = (int)(e / k);
     double d = 0.0;
-    for (int l = i; l <= j; ++l) d = fma(Tm[i + (int64_t)l * ldt], G[l + j * k], d);
+    for (int l = i; l <= j; ++l) d = fma(Tm[i + (int64_t)l * ldt], G[l + (int64_t)j * k], d);
     M[e] = d;
   }
 }
@@ -413,11 +418,14 @@ int trim_thin_q_impl(sqb_ctx* ctx, int lo_dtype, const void* U, int64_t ldu, int
                      int64_t ell, double* Q, int64_t ldq) {
   WsPlan plan;
   const size_t iM = plan.add(sizeof(double) * std::max<int64_t>(1, k * k));
+  const size_t iG = plan.add(sizeof(double) * std::max<int64_t>(1, k * k));
   SQB_TRY(ws_reserve(ctx, plan.total));
   double* M = ws_ptr<double>(ctx, plan, iM);
-  const size_t smem = sizeof(double) * k * k;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(trim_tm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  trim_tm_kernel<<<1, 256, smem, ctx->stream>>>(Tm, ldt, S, lds, E, lde, (int)ell, (int)k, M);
+  double* G = ws_ptr<double>(ctx, plan, iG);
+  const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((k * k + 255) / 256, 4 * ctx->sm_count));
+  trim_g_kernel<<<gb, 256, 0, ctx->stream>>>(S, lds, E, lde, (int)ell, (int)k, G);
+  SQB_TRY(check_launch(ctx, "trim_g_kernel"));
+  trim_tm_kernel<<<gb, 256, 0, ctx->stream>>>(Tm, ldt, G, (int)k, M);
   SQB_TRY(check_launch(ctx, "trim_tm_kernel"));
   return thin_q_m_dispatch(ctx, lo_dtype, U, ldu, N, k, M, Q, ldq);
 }
@@ -502,7 +510,7 @@ __global__ void trim_negate_kernel(const double* __restrict__ X, int m, double* 
 }
 
 template <typename T>
-static int trim_right_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+static int trim_right_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t ms, const double* E, int64_t lde,
                         int scaling, const void* W, int64_t N, int64_t m, int64_t ldw, void* Uv, int64_t ldu,
                         double* S, int64_t lds, double* Tm, int64_t ldt, double* Tt, int64_t ldtt, double* R,
                         int64_t ldr, double* L, int64_t ldl, double* sig, double* rho, double* bet) {
@@ -542,7 +550,7 @@ static int trim_right_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
     const double u_high = 1.0 / 9007199254740992.0;
     for (int64_t c = 0; c < m; ++c) {
       T* w = Wl + c * ldx;
-      trim_prep_kernel<T><<<gv, 256, 0, s>>>(x, w, N, c, m, scales, st);
+      trim_prep_kernel<T><<<gv, 256, 0, s>>>(x, w, N, c, ms, scales, st);
       SQB_TRY(check_launch(ctx, "trim_prep_kernel"));
       SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, x, ldx, 1, z, ell, 0, P, st));
       trim_tail_kernel<T><<<1, TRIM_NT, 0, s>>>(z, (int)ell, w, (int)c, scales, x, scal, st);
@@ -560,7 +568,7 @@ static int trim_right_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
       const int64_t k = m - c - 1;
       if (k > 0) {
         const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 2 * ctx->sm_count));
-        trim_mask_batch_kernel<T><<<dim3(gb, (unsigned)k), 256, 0, s>>>(Xm, ldx, w + ldx, ldx, N, c, m, scales, st);
+        trim_mask_batch_kernel<T><<<dim3(gb, (unsigned)k), 256, 0, s>>>(Xm, ldx, w + ldx, ldx, N, c, ms, scales, st);
         SQB_TRY(check_launch(ctx, "trim_mask_batch_kernel"));
         SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, Xm, ldx, k, Yx, ell, 0, P, st));
         trim_rcoef_kernel<<<(unsigned)k, 256, 0, s>>>(S + c * lds, Yx, ell, (int)ell, bet, (int)c, coef, st);
@@ -589,12 +597,12 @@ static int trim_right_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
   return check_launch(ctx, "trim_negate_kernel");
 }
 
-int trim_right_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+int trim_right_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t ms, const double* E, int64_t lde,
                         int scaling, int lo_dtype, const void* W, int64_t N, int64_t m, int64_t ldw, void* U,
                         int64_t ldu, double* S, int64_t lds, double* Tm, int64_t ldt, double* Tt, int64_t ldtt,
                         double* R, int64_t ldr, double* L, int64_t ldl, double* sig, double* rho, double* bet) {
 #define SQB_TRIM_CALL(TY)                                                                                       \
-  return trim_right_t<TY>(ctx, sk, scales, E, lde, scaling, W, N, m, ldw, U, ldu, S, lds, Tm, ldt, Tt, ldtt, R, \
+  return trim_right_t<TY>(ctx, sk, scales, ms, E, lde, scaling, W, N, m, ldw, U, ldu, S, lds, Tm, ldt, Tt, ldtt, R, \
                           ldr, L, ldl, sig, rho, bet)
   switch (lo_dtype) {
     case SQB_F64: SQB_TRIM_CALL(double);
@@ -606,12 +614,12 @@ int trim_right_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
   return set_error(ctx, SQB_ERR_ARG, "unknown dtype %d", lo_dtype);
 }
 
-int trim_left_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, const double* E, int64_t lde,
+int trim_left_dispatch(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales, int64_t ms, const double* E, int64_t lde,
                        int scaling, int lo_dtype, const void* W, int64_t N, int64_t m, int64_t ldw, void* U,
                        int64_t ldu, double* S, int64_t lds, double* Tm, int64_t ldt, double* Tt, int64_t ldtt,
                        double* R, int64_t ldr, double* L, int64_t ldl, double* sig, double* rho, double* bet) {
 #define SQB_TRIM_CALL(TY)                                                                                      \
-  return trim_left_t<TY>(ctx, sk, scales, E, lde, scaling, W, N, m, ldw, U, ldu, S, lds, Tm, ldt, Tt, ldtt, R, \
+  return trim_left_t<TY>(ctx, sk, scales, ms, E, lde, scaling, W, N, m, ldw, U, ldu, S, lds, Tm, ldt, Tt, ldtt, R, \
                          ldr, L, ldl, sig, rho, bet)
   switch (lo_dtype) {
     case SQB_F64: SQB_TRIM_CALL(double);

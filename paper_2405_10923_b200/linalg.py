@@ -47,11 +47,46 @@ def sign(v):
     return 1.0 if v >= 0.0 else -1.0
 
 
+class DenseMatrix:
+    """linalg.py:40-72: a host matrix tagged with the format its float64 entries
+    honour (rounded on construction).  Every entry point of this package takes
+    it wherever it takes an ndarray (it converts through __array__)."""
+
+    def __init__(self, data, precision="double"):
+        from .precision import round_to
+        a = np.array(data, dtype=np.float64, ndmin=2)
+        if a.ndim != 2:
+            raise ValueError(f"expected a 2-D array, got shape {a.shape}")
+        self.precision = precision
+        self.data = np.asfortranarray(round_to(a, precision))
+
+    rows = property(lambda self: self.data.shape[0])
+    cols = property(lambda self: self.data.shape[1])
+    shape = property(lambda self: self.data.shape)
+
+    def __array__(self, dtype=None, copy=None):
+        return np.array(self.data, dtype=np.float64 if dtype is None else dtype, copy=bool(copy) or None)
+
+    def __eq__(self, other):
+        return (isinstance(other, DenseMatrix) and self.precision == other.precision
+                and np.array_equal(self.data, other.data))
+
+    def __repr__(self):
+        return f"DenseMatrix(data={self.data!r}, precision={self.precision!r})"
+
+
 def as_array(M):
-    """numpy passthrough (device tensors are left as they are)."""
+    """linalg.py:75-79 (device tensors are left as they are)."""
     if isinstance(M, torch.Tensor):
         return M
+    if isinstance(M, DenseMatrix):
+        return M.data
     return np.asarray(M, dtype=np.float64)
+
+
+def cast_precision(M, tag):
+    """linalg.py:82-89: M rounded to `tag` as a DenseMatrix (idempotent)."""
+    return DenseMatrix(as_array(M), tag)
 
 
 def _dev64(A) -> torch.Tensor:

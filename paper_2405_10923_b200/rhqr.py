@@ -341,6 +341,19 @@ def householder_qr(A, scaling=SCALE_SQRT2, policy=None):
     return QRResult(Q=_out(Q, host), R=_out(R, host), method="householder", aux=aux)
 
 
+def _round_high(X, policy, host):
+    """The reference solves in policy.high (linalg.py:108-116): the float64
+    device solution rounded once to that format (exactly representable, as the
+    reference's output is; a no-op for the double policy)."""
+    if policy is None or policy.high == "double":
+        return X
+    from .precision import round_to
+    if host:
+        return round_to(X, policy.high)
+    from .devarray import TORCH_DTYPES
+    return X.to(TORCH_DTYPES[policy.high]).to(torch.float64)
+
+
 def upper_tri_solve(R, B, policy=None):
     """linalg.py:102-116: R X = B by back substitution (device)."""
     host = not (is_device(R) or is_device(B))
@@ -354,7 +367,23 @@ def upper_tri_solve(R, B, policy=None):
                                              X.data_ptr(), ld_of(X)), "sqb_upper_tri_solve")
     raise_status(ctx, "upper_tri_solve")
     out = X[:, 0] if vec else X
-    return _out(out, host)
+    return _round_high(_out(out, host), policy, host)
+
+
+def right_tri_solve(B, R, policy=None):
+    """linalg.py:119-129: X R = B for upper-triangular R.  R^t X^t = B^t is a
+    lower-triangular system; reversing the index order turns it into the
+    upper-triangular one the device solves (J R^t J is upper, J the flip)."""
+    host = not (is_device(R) or is_device(B))
+    vec = (B.dim() == 1) if is_device(B) else (np.ndim(B) == 1)
+    Rd = to_device(R, "double")
+    Bd = to_device(B, "double")              # a vector arrives as the column B^t
+    Bt = Bd if vec else Bd.t()
+    Rf = torch.flip(Rd, (0, 1)).t()
+    Xf = upper_tri_solve(Rf, torch.flip(Bt, (0,)).contiguous())
+    Xt = torch.flip(Xf, (0,))
+    out = Xt[:, 0] if vec else Xt.t()
+    return _round_high(_out(out, host), policy, host)
 
 
 def lsq_via_implicit_q(factors, b, policy=None):
@@ -496,5 +525,5 @@ def sketch_q(factors):
 __all__ = ["HouseholderStep", "RHQRFactors", "QRResult", "householder_qr", "upper_tri_solve",
            "BlockPanel", "BlockRHQRFactors", "rhqr_block", "rhqr_right", "t_factor_from_sketches",
            "lsq_via_implicit_q", "rh_vector", "rhqr_left", "rec_rhqr", "apply_reflectors_compact",
-           "thin_q", "sketch_q", "SCALE_SQRT2", "SCALE_UNIT", "raise_status", "_embed"]
+           "thin_q", "sketch_q", "SCALE_SQRT2", "SCALE_UNIT", "raise_status", "_embed", "right_tri_solve"]
 _ = C

@@ -142,6 +142,70 @@ class SRHTSketch(SketchOperator):
         return {"desc": d, "bits": bits, "idx": idx}
 
 
+class _FullHadamard(SRHTSketch):
+    """The SRHT with all signs +1, every row kept in order and scale 1: its
+    apply IS the normalized Walsh-Hadamard transform (the K1 kernels, same
+    butterfly order and rounding as fwht, sketching.py:21-43)."""
+
+    def __init__(self, n):
+        SketchOperator.__init__(self, n, n, 0)
+        self.n_pad = n
+        self.signs = np.ones(n)
+        self.indices = np.arange(n, dtype=np.int64)
+        self.scale = 1.0
+
+
+_hadamard_ops = {}
+
+
+def fwht(x):
+    """sketching.py:21-43: normalized fast Walsh-Hadamard transform along axis 0
+    in x's own dtype (float64, float32, float16 or a CUDA tensor), on the
+    device through the SRHT kernels."""
+    dev = is_device(x)
+    a = x if dev else np.asarray(x)
+    n = a.shape[0] if a.ndim else 0
+    if n == 0 or n & (n - 1):
+        raise ValueError(f"length {n} is not a power of two")
+    if dev:
+        dt = None
+        tag = tag_of_torch(a.dtype)
+    else:
+        if a.dtype.kind != "f":
+            a = a.astype(np.float64)
+        dt = a.dtype
+        try:
+            tag = tag_of_dtype(dt)
+        except ValueError:
+            raise TypeError(f"fwht on the device supports float64/float32/float16, not {dt}") from None
+    if n == 1:
+        return a.clone() if dev else a.copy()
+    if n > 1 << 18:  # every row is kept: the leaf table grows as n^2 / tile
+        raise ValueError("the device fwht is a validation utility (n <= 2^18); SRHTSketch.apply is the transform")
+    op = _hadamard_ops.get(n)
+    if op is None:
+        if len(_hadamard_ops) > 8:
+            _hadamard_ops.clear()
+        op = _hadamard_ops[n] = _FullHadamard(n)
+    shape = a.shape
+    a2 = a.reshape(n, -1)
+    y = op.apply(a2 if dev else a2.astype(np.float64), dtype=_np_dtype(tag))
+    y = y.reshape(shape)
+    return y.to(a.dtype) if dev else y.astype(dt)
+
+
+def check_embedding(op, Q, orth_tol=1e-12):
+    """sketching.py:286-298: max(sigma_max - 1, 1 - sigma_min) of op applied to
+    a float64-orthonormal basis Q (ValueError if Q is not orthonormal)."""
+    from .linalg import orthogonality_error
+    err = orthogonality_error(Q)
+    if err > orth_tol:
+        raise ValueError(f"basis is not orthonormal: ||Q^tQ - I|| = {err:.3e}")
+    Y = op.apply(Q)
+    sv = torch.linalg.svdvals(Y if is_device(Y) else torch.from_numpy(np.ascontiguousarray(Y)).cuda())
+    return float(max(float(sv[0]) - 1.0, 1.0 - float(sv[-1])))
+
+
 def _philox_rows(seed, n, i0, i1, out, scale):
     for i in range(i0, i1):
         g = np.random.Generator(np.random.Philox(key=[seed, i]))

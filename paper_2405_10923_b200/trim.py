@@ -114,6 +114,99 @@ def normalize_leading_columns(omega, m, chunk=256):
 
 
 @dataclass
+class TrimStep:
+    """trim.py:36-47: one trimmed reflector (elimination index j, 1-based; tail
+    vector v of length n-j+1; its sketch s = Omega [0; v]; the scalars)."""
+
+    j: int
+    v: object
+    s: object
+    sigma: float
+    rho: float
+    beta: float
+
+
+def trim_rh_vector(w_tail, omega, j, scaling=SCALE_SQRT2, policy=None):
+    """trim.py:79-146: the reflector of the trimmed elimination at column j, on
+    the device: the two sketches Omega [0; w_tail] and Omega [0; v] through
+    the operator's kernels, the scalars in float64 (the column sweep's
+    trim_tail / trim_finish kernels compute the same quantities in place;
+    this is the single-step form the reference exposes)."""
+    check_scaling(scaling)
+    policy = policy or DOUBLE_POLICY
+    require_device_policy(policy)
+    from .devarray import TORCH_DTYPES
+    host = not is_device(w_tail)
+    lo_t = TORCH_DTYPES[policy.low]
+    wt = to_device(w_tail, "double")[:, 0]
+    n = omega.n
+    jj = j - 1
+    if not 0 <= jj < n:
+        raise ValueError(f"elimination index {j} outside {n} coordinates")
+    if wt.shape[0] != n - jj:
+        raise ValueError(f"tail has {wt.shape[0]} entries, expected {n - jj}")
+    lo_np = _np_lo(policy.low)
+    x = torch.zeros(n, dtype=torch.float64, device=wt.device)
+    x[jj:] = wt
+    z = omega.apply(x, dtype=lo_np)
+    rho = float(torch.linalg.norm(z))
+    if rho == 0.0:
+        raise BreakdownError(f"sketched tail annihilated at column {j}")
+    w0 = float(wt[0])
+    sigma = 1.0 if w0 >= 0.0 else -1.0
+    v = wt.clone()
+    v[0] += sigma * rho
+    v = v.to(lo_t).to(torch.float64)  # round_to(v, low)
+    x[jj:] = v
+    vs = omega.apply(x, dtype=lo_np)
+    nv = float(torch.linalg.norm(vs))
+    u_high = 2.0 ** -53  # sketch-space arithmetic is float64 on the device
+    if nv <= 8.0 * u_high * (rho + rho):
+        raise BreakdownError(f"sketched reflector vector cancelled at column {j} "
+                             f"(degenerate sketch geometry, norm {nv:.3e})")
+    beta = 2.0 / (nv * nv)
+    if scaling == SCALE_SQRT2:
+        f = float(np.sqrt(beta))
+        v = v * f
+        vs = vs * f
+        beta = 1.0
+    else:
+        piv = float(vs[0])
+        if abs(piv) <= 8.0 * u_high * nv:
+            raise BreakdownError(f"unit scaling pivot vanished at column {j} (sketched entry {piv:.3e})")
+        v = v / piv
+        vs = vs / piv
+        beta = beta * piv * piv
+    v = v.to(lo_t).to(torch.float64)
+    o = (lambda t: to_numpy(t)) if host else (lambda t: t)
+    return TrimStep(j=j, v=o(v), s=o(vs), sigma=sigma, rho=rho, beta=float(beta))
+
+
+def _np_lo(tag):
+    from .precision import DTYPES
+    return DTYPES[tag]
+
+
+def t_tilde_from_factors(S, E, U, policy=None):
+    """trim.py:179-196: the reversed-product triangle from S, E and U's leading
+    block: A = L U[:m] - tril(S^t S, -1) - diag(S^t S) / 2 is lower triangular
+    and T~^t = -A^{-1} (device products and the device triangular solve)."""
+    from .rhqr import upper_tri_solve
+    host = not is_device(S)
+    Sd = to_device(S, "double")
+    m = Sd.shape[1]
+    Ed = to_device(E, "double")[:, :m]
+    Ud = (U if is_device(U) else torch.from_numpy(np.ascontiguousarray(np.asarray(U, dtype=np.float64)[:m])).cuda())
+    Ud = Ud[:m].to(torch.float64)
+    G = Sd.t() @ Sd
+    L = torch.tril(Sd.t() @ Ed, -1)
+    A = L @ Ud - torch.tril(G, -1) - torch.diag(torch.diagonal(G) / 2.0)
+    X = upper_tri_solve(A.t().contiguous(), torch.eye(m, dtype=torch.float64, device=Sd.device))
+    out = -X
+    return to_numpy(out) if host else out
+
+
+@dataclass
 class TrimFactors:
     """trim.py:149-186: W = (I - U T ut((Omega U)^t Omega)) [R; 0]."""
 
@@ -208,7 +301,7 @@ def _trim_run(entry, W, omega, scaling, policy):
     scal = torch.empty(3 * m, dtype=torch.float64, device=Wd.device)
     ctx = _lib.context()
     ctx.check(getattr(_lib.lib(), entry)(
-        ctx.h, omega.desc(), sc.data_ptr(), Ed.data_ptr(), ld_of(Ed), scaling_code(scaling), CODES[tag],
+        ctx.h, omega.desc(), sc.data_ptr(), omega.m, Ed.data_ptr(), ld_of(Ed), scaling_code(scaling), CODES[tag],
         Wd.data_ptr(), n, m, ld_of(Wd), U.data_ptr(), ld_of(U), S.data_ptr(), ld_of(S), T.data_ptr(), ld_of(T),
         Tt.data_ptr(), ld_of(Tt), R.data_ptr(), ld_of(R), L.data_ptr(), ld_of(L), scal.data_ptr(),
         scal.data_ptr() + 8 * m, scal.data_ptr() + 16 * m), entry)

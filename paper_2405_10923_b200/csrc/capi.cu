@@ -30,6 +30,8 @@ int colscaled_apply_dispatch(sqb_ctx*, const sqb_sketch*, const double*, int64_t
                              int64_t, double*, int64_t);
 int trim_thin_q_impl(sqb_ctx*, int, const void*, int64_t, int64_t, int64_t, const double*, int64_t,
                      const double*, int64_t, const double*, int64_t, int64_t, double*, int64_t);
+int t_factor_impl(sqb_ctx*, const double*, int64_t, int64_t, int64_t, double*, int64_t);
+int upper_tri_solve_impl(sqb_ctx*, const double*, int64_t, int64_t, const double*, int64_t, int64_t, double*, int64_t);
 int rhqr_right_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t, void*,
                         int64_t, double*, int64_t, double*, int64_t, double*, double*, double*);
 int rec_rhqr_dispatch(sqb_ctx*, const sqb_sketch*, int, int, const void*, int64_t, int64_t, int64_t, void*,
@@ -384,7 +386,7 @@ int sqb_rhqr_right(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int lo_dtype
     return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
   SQB_TRY(rhqr_right_dispatch(ctx, sk, scaling, lo_dtype, W, N, m, ldw, U, ldu, S, lds, R, ldr, sigmas, rhos,
                               betas));
-  return sqb_t_factor(ctx, S, lds, m + sk->ell, m, T, ldt);
+  return t_factor_impl(ctx, S, lds, m + sk->ell, m, T, ldt);
 }
 
 int sqb_apply_reflectors(sqb_ctx* ctx, const sqb_sketch* sk, int64_t m, int lo_dtype, const void* U,

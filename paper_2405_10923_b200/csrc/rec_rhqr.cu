@@ -593,14 +593,23 @@ upper_tri_solve_kernel(const double* __restrict__ R, int64_t ldr, int m, const d
 
 }  // namespace sqb
 
-extern "C" int sqb_upper_tri_solve(sqb_ctx* ctx, const double* R, int64_t ldr, int64_t m, const double* B,
-                                   int64_t ldb, int64_t k, double* X, int64_t ldx) {
-  using namespace sqb;
-  SQB_TRY(begin_entry(ctx));
+namespace sqb {
+// the solve inside a running call chain (no status reset: a breakdown recorded
+// by an earlier kernel of the chain must survive to the caller's status read)
+int upper_tri_solve_impl(sqb_ctx* ctx, const double* R, int64_t ldr, int64_t m, const double* B, int64_t ldb,
+                         int64_t k, double* X, int64_t ldx) {
   if (m < 1 || k < 1) return SQB_OK;
   upper_tri_solve_kernel<<<(unsigned)k, 256, sizeof(double) * m, ctx->stream>>>(R, ldr, (int)m, B, ldb, X, ldx,
                                                                                ctx->d_status);
   return check_launch(ctx, "upper_tri_solve_kernel");
+}
+}  // namespace sqb
+
+extern "C" int sqb_upper_tri_solve(sqb_ctx* ctx, const double* R, int64_t ldr, int64_t m, const double* B,
+                                   int64_t ldb, int64_t k, double* X, int64_t ldx) {
+  using namespace sqb;
+  SQB_TRY(begin_entry(ctx));
+  return upper_tri_solve_impl(ctx, R, ldr, m, B, ldb, k, X, ldx);
 }
 
 namespace sqb {

@@ -376,10 +376,21 @@ __global__ void tinv_kernel(const double* __restrict__ S, int64_t lds, int od, i
 
 }  // namespace sqb
 
+namespace sqb {
+int t_factor_impl(sqb_ctx* ctx, const double* S, int64_t lds, int64_t od, int64_t k, double* T, int64_t ldt);
+}
+
 extern "C" int sqb_t_factor(sqb_ctx* ctx, const double* S, int64_t lds, int64_t od, int64_t k, double* T,
                             int64_t ldt) {
   using namespace sqb;
   SQB_TRY(begin_entry(ctx));
+  return t_factor_impl(ctx, S, lds, od, k, T, ldt);
+}
+
+// T from S inside a running call chain (no status reset: a breakdown recorded
+// by the sweep must survive to the caller's status read)
+int sqb::t_factor_impl(sqb_ctx* ctx, const double* S, int64_t lds, int64_t od, int64_t k, double* T, int64_t ldt) {
+  using namespace sqb;
   if (k < 1) return SQB_OK;
   if (lds < od || ldt < k) return set_error(ctx, SQB_ERR_ARG, "bad leading dimensions");
   WsPlan plan;

@@ -28,6 +28,9 @@
 
 namespace sqb {
 
+int t_factor_impl(sqb_ctx*, const double*, int64_t, int64_t, int64_t, double*, int64_t);
+int upper_tri_solve_impl(sqb_ctx*, const double*, int64_t, int64_t, const double*, int64_t, int64_t, double*, int64_t);
+
 constexpr int TRIM_NT = 256;
 constexpr int TRIM_SNT = 1024;  // single-CTA sketch-space kernels
 
@@ -579,7 +582,7 @@ static int trim_right_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
     }
   }
   // T = t_factor_from_sketches(S) (rhqr.py:122-132); may reuse the workspace
-  SQB_TRY(sqb_t_factor(ctx, S, lds, ell, m, Tm, ldt));
+  SQB_TRY(t_factor_impl(ctx, S, lds, ell, m, Tm, ldt));
   WsPlan plan;
   const size_t iA = plan.add(sizeof(double) * m * m);
   const size_t iI = plan.add(sizeof(double) * m * m);
@@ -592,7 +595,7 @@ static int trim_right_t(sqb_ctx* ctx, const sqb_sketch* sk, const double* scales
   double* Lt = ws_ptr<double>(ctx, plan, iL);
   trim_tilde_kernel<T><<<1, 256, 0, s>>>(S, lds, E, lde, (int)ell, U, ldu, (int)m, At, I, L, ldl, Lt);
   SQB_TRY(check_launch(ctx, "trim_tilde_kernel"));
-  SQB_TRY(sqb_upper_tri_solve(ctx, At, m, m, I, m, m, X, m));
+  SQB_TRY(upper_tri_solve_impl(ctx, At, m, m, I, m, m, X, m));
   trim_negate_kernel<<<(unsigned)std::max<int64_t>(1, (m * m + 255) / 256), 256, 0, s>>>(X, (int)m, Tt, ldtt);
   return check_launch(ctx, "trim_negate_kernel");
 }

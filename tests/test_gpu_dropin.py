@@ -171,3 +171,30 @@ def test_single_trimmed_reflector_matches_the_sweep(P):
         trim.trim_rh_vector(np.zeros(n), om, 1)
     Tt = trim.t_tilde_from_factors(F.S, F.E, F.U)
     assert np.allclose(Tt, F.T_tilde, atol=1e-12 * np.linalg.norm(F.T_tilde))
+
+
+def test_right_looking_sweeps_report_a_breakdown_like_the_left_ones(P):
+    """An exactly dependent (zero) last column stays exactly zero under the
+    rank-1 updates (rhqr.py:296-298), so the right-looking sweeps must raise
+    at that column too; the T assembled after the sweep must not wipe the
+    recorded breakdown."""
+    from paper_2405_10923_b200 import trim
+    rng = np.random.default_rng(5)
+    for N, m, om_f in ((160, 9, lambda n: P.GaussianSketch(18, n, 3)), (4200, 6, lambda n: P.SRHTSketch(12, n, 3))):
+        W = rng.standard_normal((N, m))
+        W[:, m - 1] = 0.0
+        for scaling in (P.SCALE_SQRT2, P.SCALE_UNIT):
+            with pytest.raises(P.BreakdownError, match=f"sketched tail annihilated at column {m}"):
+                P.rhqr_right(W, om_f(N - m), scaling=scaling)
+            with pytest.raises(P.BreakdownError, match=f"sketched tail annihilated at column {m}"):
+                P.rhqr_left(W, om_f(N - m), scaling=scaling)
+            with pytest.raises(P.BreakdownError, match=f"sketched tail annihilated at column {m}"):
+                trim.trim_rhqr_right(W, om_f(N), scaling=scaling)
+            with pytest.raises(P.BreakdownError, match=f"sketched tail annihilated at column {m}"):
+                trim.trim_rhqr_left(W, om_f(N), scaling=scaling)
+    # unit scaling divides by the first SKETCH entry: with a pass-through operator it is a padded zero
+    W = rng.standard_normal((19, 8))
+    for f in (trim.trim_rhqr_left, trim.trim_rhqr_right):
+        with pytest.raises(P.BreakdownError, match="unit scaling pivot vanished at column 2"):
+            f(W, P.IdentitySketch(19), scaling=P.SCALE_UNIT)
+        assert np.isfinite(f(W, P.IdentitySketch(19)).R).all()

@@ -40,7 +40,9 @@ enum sqb_status {
   SQB_ERR_SINGULAR = 3,   /* SingularFactorError (linalg.py:35, :92-99) */
   SQB_ERR_CUDA = 4,
   SQB_ERR_NCCL = 5,
-  SQB_ERR_RANGE = 6       /* PrecisionRangeError (precision.py:25, :45-50) */
+  SQB_ERR_RANGE = 6,      /* PrecisionRangeError (precision.py:25, :45-50) */
+  SQB_ERR_NONFINITE = 7   /* ValueError "array must not contain infs or NaNs": what the reference's triangular
+                             solves (scipy.linalg.solve_triangular, linalg.py:115, :128) raise on such operands */
 };
 
 /* storage / arithmetic formats (precision.py:12-19, plus bf16) */

@@ -15,7 +15,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsketchqr_b200.so")
 
-SQB_OK, SQB_ERR_ARG, SQB_ERR_BREAKDOWN, SQB_ERR_SINGULAR, SQB_ERR_CUDA, SQB_ERR_NCCL, SQB_ERR_RANGE = range(7)
+SQB_OK, SQB_ERR_ARG, SQB_ERR_BREAKDOWN, SQB_ERR_SINGULAR, SQB_ERR_CUDA, SQB_ERR_NCCL, SQB_ERR_RANGE, \
+    SQB_ERR_NONFINITE = range(8)
 SQB_F64, SQB_F32, SQB_F16, SQB_BF16 = range(4)
 SQB_SCALE_SQRT2, SQB_SCALE_UNIT = 0, 1
 SQB_SKETCH_SRHT, SQB_SKETCH_DENSE, SQB_SKETCH_IDENTITY = 0, 1, 2

@@ -159,6 +159,12 @@ mfac_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict_
 
 // zero-diagonal check (rhqr.py:388-391): argmin |diag| < DBL_MIN -> breakdown
 __global__ void mfac_check_kernel(const double* M, int m, Status* st) {
+  if (failed(st)) return;
+  // the reference hands Mfac to scipy's solve_triangular (linalg.py:128), which rejects non-finite entries
+  // (a sketch that overflowed its storage format) with a ValueError before any arithmetic
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x)
+    if (e % m <= e / m && !isfinite(M[e])) fail(st, SQB_ERR_NONFINITE, e / m + 1, M[e]);
+  __syncthreads();
   if (threadIdx.x != 0 || failed(st)) return;
   int k = 0;
   double dmin = fabs(M[0]);
@@ -481,7 +487,7 @@ int rec_finish_t(sqb_ctx* ctx, int scaling, const double* Z, int64_t od, int64_t
   // Mfac = triu(T^t S^t Z) and its diagonal check (rhqr.py:387-391)
   mfac_kernel<<<(unsigned)m, 256, sizeof(double) * m, ctx->stream>>>(S, lds, Tm, ldt, Z, od, (int)od, (int)m, M, st);
   SQB_TRY(check_launch(ctx, "mfac_kernel"));
-  mfac_check_kernel<<<1, 32, 0, ctx->stream>>>(M, (int)m, st);
+  mfac_check_kernel<<<1, 256, 0, ctx->stream>>>(M, (int)m, st);
   SQB_TRY(check_launch(ctx, "mfac_check_kernel"));
   // K6: U2 = W2 Mfac^{-1}
   const int64_t n = n2;
@@ -581,6 +587,16 @@ upper_tri_solve_kernel(const double* __restrict__ R, int64_t ldr, int m, const d
   if (threadIdx.x == 0 && col == 0)
     for (int i = 0; i < m; ++i)
       if (fabs(R[i + (int64_t)i * ldr]) < DBL_MIN) { fail(st, SQB_ERR_SINGULAR, i + 1, R[i + (int64_t)i * ldr]); break; }
+  // scipy's check_finite (linalg.py:115): non-finite operands are a ValueError, after the diagonal check
+  __syncthreads();
+  if (!failed(st)) {
+    bool bad = false;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) bad = bad || !isfinite(B[i + (int64_t)col * ldb]);
+    if (col == 0)
+      for (int e = threadIdx.x; e < m * m; e += blockDim.x)
+        if (e % m <= e / m) bad = bad || !isfinite(R[e % m + (int64_t)(e / m) * ldr]);
+    if (bad) fail(st, SQB_ERR_NONFINITE, col + 1, 0.0);
+  }
   for (int i = m - 1; i >= 0; --i) {
     double part = 0.0;
     for (int j = i + 1 + threadIdx.x; j < m; j += blockDim.x) part = fma(R[i + (int64_t)j * ldr], x[j], part);

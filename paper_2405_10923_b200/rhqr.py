@@ -94,6 +94,8 @@ def raise_status(ctx, what="factorization", tag=None):
         raise BreakdownError(f"reflector scale degenerated at column {col} (rho={val:.3e})")
     if code == _lib.SQB_ERR_SINGULAR:
         raise SingularFactorError(f"triangular factor has zero or subnormal diagonal at index {col - 1}")
+    if code == _lib.SQB_ERR_NONFINITE:  # scipy's check_finite in the reference's triangular solves
+        raise ValueError("array must not contain infs or NaNs")
     if code == _lib.SQB_ERR_NCCL and col < 0:  # p2p_wait (csrc/p2p.cuh): a peer's flag never arrived
         raise _lib.SketchQRError(f"{what}: peer-memory exchange {int(val)} timed out waiting for rank {-col - 1}")
     raise _lib.SketchQRError(f"{what}: device status {code} at column {col}")
@@ -319,7 +321,8 @@ def householder_qr(A, scaling=SCALE_SQRT2, policy=None):
     check_scaling(scaling)
     policy = policy or DOUBLE_POLICY
     if policy.low != "double" or policy.high != "double":
-        raise NotImplementedError("householder_qr on the device runs in double")
+        raise NotImplementedError("householder_qr in a low-precision policy is a comparison method outside the B200 "
+                                  "hot path (the device Householder QR is the float64 sketch-space QR of recRHQR)")
     host = not is_device(A)
     Ad = to_device(A, "double")
     p, m = Ad.shape

@@ -260,6 +260,8 @@ def _raise_trim_status(ctx):
     if code == _lib.SQB_ERR_SINGULAR:
         from .linalg import SingularFactorError
         raise SingularFactorError("triangular factor has zero or subnormal diagonal")
+    if code == _lib.SQB_ERR_NONFINITE:  # scipy's check_finite in the reference's triangular solves
+        raise ValueError("array must not contain infs or NaNs")
     raise _lib.SketchQRError(f"trimmed factorization: device status {code} at column {col}")
 
 

@@ -198,3 +198,27 @@ def test_right_looking_sweeps_report_a_breakdown_like_the_left_ones(P):
         with pytest.raises(P.BreakdownError, match="unit scaling pivot vanished at column 2"):
             f(W, P.IdentitySketch(19), scaling=P.SCALE_UNIT)
         assert np.isfinite(f(W, P.IdentitySketch(19)).R).all()
+
+
+def test_non_finite_operands_fail_like_the_reference(P):
+    """A non-finite entry (an input inf, or a low-precision transform that
+    overflowed) must not come back as silent NaN factors: the sweeps report the
+    degenerate reflector (rhqr.py:73-79), the triangular solves and everything
+    built on them raise scipy's check_finite ValueError (linalg.py:115, :128)."""
+    from paper_2405_10923_b200.rhqr import t_factor_from_sketches, upper_tri_solve
+    W = np.random.default_rng(0).standard_normal((500, 6))
+    W[40, 2] = np.inf
+    for om in (P.SRHTSketch(24, 494, 1), P.GaussianSketch(24, 494, 1)):
+        with pytest.raises(ValueError, match="infs or NaNs"):
+            P.rec_rhqr(W, om)
+        with pytest.raises(P.BreakdownError, match="column 3"):
+            P.rhqr_left(W, om)
+        with pytest.raises(P.BreakdownError, match="column 3"):
+            P.rhqr_right(W, om)
+    S = np.random.default_rng(1).standard_normal((30, 4))
+    S[3, 1] = np.nan
+    with pytest.raises(ValueError, match="infs or NaNs"):
+        t_factor_from_sketches(S)
+    with pytest.raises(ValueError, match="infs or NaNs"):
+        upper_tri_solve(np.eye(3), np.array([1.0, np.inf, 0.0]))
+    assert np.array_equal(upper_tri_solve(np.eye(3), np.ones(3)), np.ones(3))  # the status does not stick

@@ -117,3 +117,22 @@ def test_p2p_silent_peer_times_out_instead_of_hanging(P, monkeypatch):
             dist.destroy_process_group()
     F = P.rhqr_left(W, om)  # the status word was consumed: the next call runs
     assert np.isfinite(F.R).all()
+
+
+def test_row_partition_fuzz_is_bitwise_the_single_gpu_run(P, monkeypatch, capsys):
+    """A short seeded run of scripts/fuzz_dist.py: random shapes (ragged last
+    ranks, ranks that own only padding, n_pad / P down to one tile), formats,
+    scalings and exchanges on 1-8 virtual ranks; every factor bitwise the
+    single-GPU launch chain, every failure the same exception."""
+    import importlib.util
+    import sys
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts", "fuzz_dist.py")
+    spec = importlib.util.spec_from_file_location("fuzz_dist", path)
+    mod = importlib.util.module_from_spec(spec)
+    monkeypatch.setenv("SQB_PERSIST", "0")
+    spec.loader.exec_module(mod)
+    rc = mod.main(["--seconds", "12", "--seed", "7"])
+    out = capsys.readouterr().out
+    assert rc == 0, out
+    assert "0 disagreements" in out
+    sys.modules.pop("fuzz_dist", None)

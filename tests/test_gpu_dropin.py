@@ -222,3 +222,62 @@ def test_non_finite_operands_fail_like_the_reference(P):
     with pytest.raises(ValueError, match="infs or NaNs"):
         upper_tri_solve(np.eye(3), np.array([1.0, np.inf, 0.0]))
     assert np.array_equal(upper_tri_solve(np.eye(3), np.ones(3)), np.ones(3))  # the status does not stick
+
+
+def test_streams_and_threads_do_not_share_scratch(P):
+    """One library context per (device, host thread); within a thread a stream
+    switch orders the new stream after the old one.  Factorizations issued on
+    two torch streams back to back, and from four threads at once, must be
+    bitwise the serial results (a shared scratch or status word would show as
+    corrupted factors or a breakdown reported to the wrong caller)."""
+    import threading
+
+    import torch
+    rng = np.random.default_rng(77)
+    cases = []
+    for i, (N, m, ell) in enumerate([(20000, 12, 48), (70000, 20, 80), (5000, 8, 32), (33000, 16, 64)]):
+        W = rng.standard_normal((N, m))
+        om = P.SRHTSketch(ell, N - m, 100 + i)
+        cases.append((W, om, P.rhqr_left(W, om)))
+    Wbad = cases[0][0].copy()
+    Wbad[:, 5] = 0.0
+    # two streams, interleaved, device-resident operands
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    dev = [(torch.from_numpy(np.asfortranarray(W)).cuda(), om) for W, om, _ in cases]
+    torch.cuda.synchronize()
+    outs = [None] * len(cases)
+    for rep in range(3):
+        for i, (Wd, om) in enumerate(dev):
+            with torch.cuda.stream(s1 if (i + rep) % 2 == 0 else s2):
+                outs[i] = P.rhqr_left(Wd, om)
+    torch.cuda.synchronize()
+    for (W, om, F), Fd in zip(cases, outs):
+        assert np.array_equal(Fd.R.cpu().numpy(), F.R) and np.array_equal(Fd.U.cpu().numpy(), F.U)
+    # four threads at once, one of them failing on every call
+    errors, results = [], {}
+
+    def work(i):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for rep in range(4):
+                    if i == 3:
+                        with pytest.raises(P.BreakdownError, match="column 6"):
+                            P.rhqr_left(Wbad, cases[0][1])
+                    else:
+                        W, om, _ = cases[i]
+                        results[(i, rep)] = P.rhqr_left(W, om)
+        except BaseException as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors, errors
+    for (i, rep), F in results.items():
+        ref = cases[i][2]
+        for k in ("R", "S", "T", "U"):
+            assert np.array_equal(getattr(F, k), getattr(ref, k)), (i, rep, k)

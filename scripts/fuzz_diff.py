@@ -29,6 +29,22 @@ from paper_2405_10923_b200 import trim as Ptrim  # noqa: E402
 
 BAR = 1e-10
 
+# bf16 storage (config 4's format): the reference has no such tag; it is injected at runtime exactly as
+# tests/golden/make_golden.py does, the reference's source untouched
+import ml_dtypes  # noqa: E402
+from sketchqr import precision as _RP  # noqa: E402
+
+if "bf16" not in _RP.PRECISIONS:
+    _RP.PRECISIONS = _RP.PRECISIONS + ("bf16",)
+    _RP.DTYPES["bf16"] = ml_dtypes.bfloat16
+    _RP.UNIT_ROUNDOFF["bf16"] = 2.0 ** -8
+
+
+def policies(tag):
+    if tag == "bf16":
+        return R.PrecisionPolicy(high="double", low="bf16"), P.PrecisionPolicy("double", "bf16")
+    return R.policy_from_tag(tag), P.policy_from_tag(tag)
+
 
 def rel(a, b):
     a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
@@ -132,7 +148,7 @@ def main():
             n = min(n, 600)
             ell = n
         scaling = str(rng.choice(["sqrt2", "unit"]))
-        tag = str(rng.choice(["double", "double", "double", "single", "mixed"]))
+        tag = str(rng.choice(["double", "double", "double", "single", "mixed", "bf16"]))
         seed = int(rng.integers(0, 1 << 30))
         N = n + m
         desc = f"{op} N={N} m={m} n={n} ell={ell} {kind} {scaling} {tag} seed={seed}"
@@ -152,7 +168,7 @@ def main():
                     continue
                 omr, omp = orr[1]
                 X = wr.standard_normal((n, k)) if k > 1 else wr.standard_normal(n)
-                dt = {"double": np.float64, "single": np.float32, "mixed": np.float16}[tag]
+                dt = {"double": np.float64, "single": np.float32, "mixed": np.float16, "bf16": ml_dtypes.bfloat16}[tag]
                 a, b = outcome(lambda: omr.apply(X, dtype=dt)), outcome(lambda: omp.apply(X, dtype=dt))
                 if a[0] != b[0]:
                     n_bad += 1
@@ -234,7 +250,7 @@ def main():
                 big[2:N + 2, 1:m + 1] = W
                 W = big[2:N + 2, 1:m + 1]
             desc += f" lay={lay}"
-            pol_r, pol_p = R.policy_from_tag(tag), P.policy_from_tag(tag)
+            pol_r, pol_p = policies(tag)
             sk = outcome(lambda: sketches(kind, ell, n, seed))
             if sk[0] != "ok":
                 sp = outcome(lambda: (P.SRHTSketch if kind == "srht" else P.GaussianSketch)(ell, n, seed))
@@ -403,7 +419,7 @@ def main():
                     print("MISMATCH values", desc, bad)
             else:
                 # low-precision storage: R within a few storage roundoffs times sqrt(N)
-                u = {"single": 2.0 ** -24, "mixed": 2.0 ** -11}[tag]
+                u = {"single": 2.0 ** -24, "mixed": 2.0 ** -11, "bf16": 2.0 ** -8}[tag]
                 e = rel(b[1].R, a[1].R)
                 if not np.isfinite(np.asarray(a[1].R)).all():
                     continue  # the reference overflowed its half-precision transform

@@ -370,7 +370,11 @@ class RHQRLeft(Workload):
         dt_c = run(torch.from_numpy(np.ascontiguousarray(self.W_host)).pin_memory())
         dt_f = run(torch.from_numpy(np.asfortranarray(self.W_host).T).pin_memory().T)
         dt = dt_c  # headline: the C-order arrays the reference's users pass
+        # the same call with an ordinary pageable (not page-locked) C-order ndarray: the upload goes through the
+        # library's page-locked staging ring filled by host threads (host_pipe.cu: staged_h2d)
+        dt_pg = run(np.array(self.W_host, order="C"))
         return {"value": self.alg / dt / 1e9, "unit": "GB/s", "ms_per_step": dt * 1e3,
+                "ms_per_step_pageable_c_order_input": dt_pg * 1e3,
                 "h2d_bytes_per_step": self.b * N * m if self.b == 8 else 8 * N * m,
                 "d2h_bytes_per_step": 8 * (N * m + (m + ell) * m + 2 * m * m + 3 * m),
                 "ms_per_step_c_order_input": dt_c * 1e3, "ms_per_step_f_order_input": dt_f * 1e3,

@@ -141,7 +141,7 @@ def _factor(mod, entry, W, omega, scaling, policy):
                            layout, p(U), n, p(S), od, p(T), m, p(R), m, p(sc), p(sc) + 8 * m, p(sc) + 16 * m)
     _check(rc, entry)
     _raise(mod, "rec_rhqr" if entry == "sqb_rec_rhqr_host" else "rhqr_left", policy.low)
-    return mod.rhqr.RHQRFactors(U=np.array(U), S=S, T=T, R=R, psi=psi, scaling=scaling, sigmas=sc[:m].copy(),
+    return mod.rhqr.RHQRFactors(U=U, S=S, T=T, R=R, psi=psi, scaling=scaling, sigmas=sc[:m].copy(),
                                 rhos=sc[m:2 * m].copy(), betas=sc[2 * m:].copy())
 
 

@@ -106,6 +106,10 @@ int sqb_ctx_destroy(sqb_ctx* ctx) {
     }
   if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
   if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
+  for (int k = 0; k < 4; ++k) {
+    if (ctx->pg_slot[k]) cudaFreeHost(ctx->pg_slot[k]);
+    if (ctx->pg_ev[k]) cudaEventDestroy(ctx->pg_ev[k]);
+  }
   if (ctx->d_status) cudaFree(ctx->d_status);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);

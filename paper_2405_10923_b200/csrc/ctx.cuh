@@ -84,6 +84,11 @@ struct sqb_ctx {
   std::vector<void*> p2p_absent;        // stand-ins for peers that never answer (fault injection)
   void** p2p_table = nullptr;           // device [n_local][nranks] mailbox bases
   unsigned long long p2p_seq = 0;       // exchanges so far (identical on every rank)
+  // page-locked staging ring for PAGEABLE host operands (host_pipe.cu: staged_h2d)
+  void* pg_slot[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t pg_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t pg_bytes = 0;
+  unsigned pg_next = 0;
 };
 
 namespace sqb {

@@ -20,6 +20,8 @@
 // bandwidth (the facade allocates its outputs that way); pageable buffers
 // work but the driver stages them synchronously.
 #include <algorithm>
+#include <cstring>
+#include <thread>
 #include <vector>
 
 #include "sketch.cuh"
@@ -156,6 +158,68 @@ static DevLayout dev_layout(int64_t rows, int64_t cols, int code, int64_t align_
   return L;
 }
 
+// ---------------------------------------------------------------------------
+// Host -> device copy of a contiguous range that may live in PAGEABLE memory
+// (the ndarray a caller of the reference passes).  cudaMemcpyAsync from
+// pageable memory is staged by the driver through one bounce buffer,
+// synchronously, at a fraction of the PCIe rate; here the range goes through
+// a ring of four page-locked slots filled by a few host threads, so the CPU
+// copy of slot k+1 runs under the DMA of slot k.  Page-locked sources take the
+// plain asynchronous copy.
+// ---------------------------------------------------------------------------
+static bool host_is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  static const unsigned nt = [] {
+    const unsigned hc = std::thread::hardware_concurrency();
+    return std::max(1u, std::min(8u, hc ? hc / 2 : 4u));
+  }();
+  if (bytes < (4u << 20) || nt == 1) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t part = ((bytes + nt - 1) / nt + 4095) & ~size_t(4095);
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; ++t) {
+    const size_t o = (size_t)t * part;
+    if (o >= bytes) break;
+    th.emplace_back([=] { memcpy((char*)dst + o, (const char*)src + o, std::min(part, bytes - o)); });
+  }
+  memcpy(dst, src, std::min(part, bytes));
+  for (auto& t : th) t.join();
+}
+
+static int staged_h2d(sqb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s, bool pinned) {
+  if (pinned || bytes < (1u << 20)) {
+    SQB_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return SQB_OK;
+  }
+  if (!ctx->pg_bytes) {
+    const size_t slot = 16u << 20;
+    for (int k = 0; k < 4; ++k) {
+      SQB_CUDA_TRY(cudaHostAlloc(&ctx->pg_slot[k], slot, cudaHostAllocDefault));
+      SQB_CUDA_TRY(cudaEventCreateWithFlags(&ctx->pg_ev[k], cudaEventDisableTiming));
+    }
+    ctx->pg_bytes = slot;
+  }
+  for (size_t o = 0; o < bytes; o += ctx->pg_bytes) {
+    const unsigned k = ctx->pg_next++ & 3u;
+    const size_t nb = std::min(ctx->pg_bytes, bytes - o);
+    SQB_CUDA_TRY(cudaEventSynchronize(ctx->pg_ev[k]));  // the slot's previous DMA has drained (no-op when unused)
+    parallel_memcpy(ctx->pg_slot[k], (const char*)src + o, nb);
+    SQB_CUDA_TRY(cudaMemcpyAsync((char*)dst + o, ctx->pg_slot[k], nb, cudaMemcpyHostToDevice, s));
+    SQB_CUDA_TRY(cudaEventRecord(ctx->pg_ev[k], s));
+  }
+  return SQB_OK;
+}
+
 struct HostPipe : SweepHooks {
   sqb_ctx* ctx = nullptr;
   EventPool* evp = nullptr;
@@ -164,6 +228,7 @@ struct HostPipe : SweepHooks {
   // input
   const double* Wh = nullptr;
   int64_t ldwh = 0;
+  bool w_pinned = true;           // false: W is pageable, uploads go through the staging ring (staged_h2d)
   void* Wd = nullptr;
   int64_t ldwd = 0;
   double* stage_in[2] = {nullptr, nullptr};
@@ -188,12 +253,23 @@ struct HostPipe : SweepHooks {
     for (int64_t g = 0; g < ngrp; ++g) {
       const int64_t c0 = g * gin, k = std::min(gin, m - c0);
       if (code == SQB_F64) {
-        SQB_CUDA_TRY(cudaMemcpy2DAsync((char*)Wd + c0 * ldwd * es, ldwd * es, Wh + c0 * ldwh, ldwh * sizeof(double),
-                                       N * sizeof(double), k, cudaMemcpyHostToDevice, ctx->s_in));
+        if (w_pinned) {
+          SQB_CUDA_TRY(cudaMemcpy2DAsync((char*)Wd + c0 * ldwd * es, ldwd * es, Wh + c0 * ldwh,
+                                         ldwh * sizeof(double), N * sizeof(double), k, cudaMemcpyHostToDevice,
+                                         ctx->s_in));
+        } else {
+          for (int64_t c = c0; c < c0 + k; ++c)
+            SQB_TRY(staged_h2d(ctx, (char*)Wd + c * ldwd * es, Wh + c * ldwh, N * sizeof(double), ctx->s_in, false));
+        }
       } else {
         double* sbuf = stage_in[g & 1];
-        SQB_CUDA_TRY(cudaMemcpy2DAsync(sbuf, N * sizeof(double), Wh + c0 * ldwh, ldwh * sizeof(double),
-                                       N * sizeof(double), k, cudaMemcpyHostToDevice, ctx->s_in));
+        if (w_pinned) {
+          SQB_CUDA_TRY(cudaMemcpy2DAsync(sbuf, N * sizeof(double), Wh + c0 * ldwh, ldwh * sizeof(double),
+                                         N * sizeof(double), k, cudaMemcpyHostToDevice, ctx->s_in));
+        } else {
+          for (int64_t c = 0; c < k; ++c)
+            SQB_TRY(staged_h2d(ctx, sbuf + c * N, Wh + (c0 + c) * ldwh, N * sizeof(double), ctx->s_in, false));
+        }
         const unsigned gb = (unsigned)std::min<int64_t>((N * k + 255) / 256, 4 * ctx->sm_count);
         SQB_TRY(by_dtype(code, [&](auto t) {
           using T = decltype(t);
@@ -215,8 +291,7 @@ struct HostPipe : SweepHooks {
     int slot = 0;
     for (int64_t r0 = 0; r0 < N; r0 += rb, slot ^= 1) {
       const int64_t R = std::min(rb, N - r0);
-      SQB_CUDA_TRY(cudaMemcpyAsync(stage_in[slot], Wh + r0 * ldwh, (size_t)R * ldwh * sizeof(double),
-                                   cudaMemcpyHostToDevice, ctx->s_in));
+      SQB_TRY(staged_h2d(ctx, stage_in[slot], Wh + r0 * ldwh, (size_t)R * ldwh * sizeof(double), ctx->s_in, w_pinned));
       dim3 grid((unsigned)((R + 31) / 32), (unsigned)((m + 31) / 32));
       SQB_TRY(by_dtype(code, [&](auto t) {
         using T = decltype(t);
@@ -342,6 +417,7 @@ extern "C" int sqb_rhqr_left_host(sqb_ctx* ctx, const sqb_sketch* sk, int scalin
   hp.m = m;
   hp.Wh = W;
   hp.ldwh = ldw;
+  hp.w_pinned = host_is_pinned(W);
   hp.Wd = Wd;
   hp.ldwd = LW.ld;
   hp.stage_in[0] = reinterpret_cast<double*>(base + plan.offs[iI0]);
@@ -465,14 +541,14 @@ extern "C" int sqb_rec_rhqr_host(sqb_ctx* ctx, const sqb_sketch* sk, int scaling
     for (auto a : ctx->s_aux) SQB_CUDA_TRY(cudaStreamWaitEvent(a, e, 0));
   }
   // ---- upload in row blocks [r0, r1) of W (block 0 also carries the m identity rows)
+  const bool w_pinned = host_is_pinned(W);  // a pageable row-major W goes through the staging ring
   std::vector<cudaEvent_t> done;
   int slot = 0, z = 0;
   for (int64_t r0 = 0, b = 0; r0 < N; ++b, slot ^= 1) {
     const int64_t r1 = std::min(N, (b == 0 ? m : r0) + blk_rows);
     const int64_t R = r1 - r0;
     if (rowmajor) {
-      SQB_CUDA_TRY(cudaMemcpyAsync(stage_in[slot], W + r0 * ldw, (size_t)R * ldw * sizeof(double),
-                                   cudaMemcpyHostToDevice, ctx->s_in));
+      SQB_TRY(staged_h2d(ctx, stage_in[slot], W + r0 * ldw, (size_t)R * ldw * sizeof(double), ctx->s_in, w_pinned));
       dim3 grid((unsigned)((R + 31) / 32), (unsigned)((m + 31) / 32));
       SQB_TRY(by_dtype(lo_dtype, [&](auto t) {
         using TT = decltype(t);

@@ -13,6 +13,7 @@ Replaced (reference file:line -> export):
     SRHTSketch._apply / GaussianSketch._apply  sketching.py:149-155, :109-125 -> sqb_sketch_apply
     rhqr_left                                  rhqr.py:254-267              -> sqb_rhqr_left_host
     rec_rhqr                                   rhqr.py:368-395              -> sqb_rec_rhqr_host
+    rhqr_arnoldi (hence rhqr_gmres)            krylov.py:82-150             -> sqb_rhqr_arnoldi
 Policies whose sketch-space precision is not float64, and operators the
 library has no descriptor for, fall through to the reference's own code.
 """
@@ -33,6 +34,15 @@ class _Sketch(C.Structure):  # include/sketchqr_b200.h: sqb_sketch
                 ("G", C.c_void_p), ("ldg", C.c_int64)]
 
 
+_MATVEC_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
+
+
+class _Operator(C.Structure):  # include/sketchqr_b200.h: sqb_operator
+    _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("n", C.c_int64), ("indptr", C.c_void_p),
+                ("indices", C.c_void_p), ("data", C.c_void_p), ("A", C.c_void_p), ("lda", C.c_int64),
+                ("cb", _MATVEC_CB), ("user", C.c_void_p), ("xbuf", C.c_void_p), ("ybuf", C.c_void_p)]
+
+
 _state = {"lib": None, "ctx": None, "saved": {}}
 _p, _i64, _int = C.c_void_p, C.c_int64, C.c_int
 
@@ -48,6 +58,8 @@ def _load(path):
             _p, _p, _p]
     L.sqb_rhqr_left_host.argtypes = host
     L.sqb_rec_rhqr_host.argtypes = host
+    L.sqb_rhqr_arnoldi.argtypes = [_p, C.POINTER(_Sketch), C.POINTER(_Operator), _int, _int, _int, C.c_double, _p, _p,
+                                   _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, C.POINTER(_int)]
     ctx = _p()
     rc = L.sqb_ctx_create(torch.cuda.current_device(), None, C.byref(ctx))
     if rc != SQB_OK:
@@ -145,6 +157,76 @@ def _factor(mod, entry, W, omega, scaling, policy):
                                 rhos=sc[m:2 * m].copy(), betas=sc[2 * m:].copy())
 
 
+def _arnoldi(mod, A, b, x0, m, omega, scaling, policy, store_q, happy_tol):
+    """rhqr_arnoldi through sqb_rhqr_arnoldi (fp64 storage); None = not handled."""
+    import scipy.sparse
+    policy = policy or mod.precision.DOUBLE_POLICY
+    if policy.high != "double" or policy.low != "double":
+        return None
+    b = np.asarray(mod.linalg.as_array(b), dtype=np.float64)
+    n = b.shape[0]
+    psi = mod.rhqr._embed(omega, n, m + 1)
+    desc = _descriptor(omega)
+    if desc is None:
+        return None
+    keep, err = [], []
+    op = _Operator(n=n)
+    if scipy.sparse.issparse(A):
+        M = scipy.sparse.csr_matrix(A, dtype=np.float64)
+        M.sort_indices()
+        ip = torch.from_numpy(M.indptr.astype(np.int64)).cuda()
+        ix = torch.from_numpy(M.indices.astype(np.int32)).cuda()
+        dv = torch.from_numpy(np.ascontiguousarray(M.data)).cuda()
+        keep += [ip, ix, dv]
+        op.kind, op.indptr, op.indices, op.data = 0, ip.data_ptr(), ix.data_ptr(), dv.data_ptr()
+    elif callable(A):
+        xbuf = torch.empty(n, dtype=torch.float64, device="cuda")
+        ybuf = torch.empty(n, dtype=torch.float64, device="cuda")
+
+        def _cb(user, stream):  # the reference hands its matvec a numpy vector (krylov.py:28-35)
+            try:
+                y = np.asarray(A(xbuf.cpu().numpy()), dtype=np.float64)
+                ybuf.copy_(torch.from_numpy(np.ascontiguousarray(y)).reshape(-1))
+                return 0
+            except BaseException as e:  # noqa: BLE001
+                err.append(e)
+                return 1
+
+        cb = _MATVEC_CB(_cb)
+        keep += [xbuf, ybuf, cb]
+        op.kind, op.cb, op.xbuf, op.ybuf = 2, cb, xbuf.data_ptr(), ybuf.data_ptr()
+    else:
+        Ad = torch.from_numpy(np.ascontiguousarray(np.asarray(mod.linalg.as_array(A), dtype=np.float64))).cuda()
+        keep.append(Ad)
+        op.kind, op.A, op.lda = 1, Ad.data_ptr(), Ad.stride(0)
+    if happy_tol is None:
+        happy_tol = 32.0 * policy.u_high
+    mt, od = m + 1, psi.out_dim
+    ld = (n + 1) // 2 * 2
+    f64 = dict(dtype=torch.float64, device="cuda")
+    bd = torch.from_numpy(b).cuda()
+    x0d = torch.zeros(n, **f64) if x0 is None else torch.from_numpy(np.asarray(x0, dtype=np.float64)).cuda()
+    U, S, T = torch.zeros((mt, ld), **f64), torch.zeros((mt, od), **f64), torch.zeros((mt, mt), **f64)
+    H, Q = torch.zeros((m, mt), **f64), (torch.zeros((m, ld), **f64) if store_q else None)
+    beta, attained = torch.zeros(1, **f64), _int(-1)
+    L, ctx = _state["lib"], _state["ctx"]
+    rc = L.sqb_rhqr_arnoldi(ctx, C.byref(desc[0]), C.byref(op), m, SCALING_CODE[scaling], 0, float(happy_tol),
+                            bd.data_ptr(), x0d.data_ptr(), U.data_ptr(), ld, S.data_ptr(), od, T.data_ptr(), mt,
+                            H.data_ptr(), mt, Q.data_ptr() if store_q else None, ld if store_q else 1,
+                            beta.data_ptr(), C.byref(attained))
+    if err:
+        raise err[0]
+    _check(rc, "sqb_rhqr_arnoldi")
+    _raise(mod, "rhqr_arnoldi")
+    closed = None if attained.value < 0 else attained.value
+    k = m if closed is None else closed
+    r = mt if closed is None else closed
+    h = lambda t: t.cpu().numpy().T  # noqa: E731  (column-major device buffers)
+    return mod.krylov.KrylovBundle(U=h(U)[:n, :r], S=h(S)[:, :r], T=h(T)[:r, :r], H=h(H)[: k + 1, :k].copy(), psi=psi,
+                                   beta=float(beta.item()), scaling=scaling,
+                                   Q_cols=h(Q)[:n, :k].copy() if store_q else None, breakdown=closed)
+
+
 def _apply(mod, om, X, dtype):
     """SketchOperator._apply (X: n x k float64, returns ell x k in `dtype`); None = not handled."""
     code = NP_CODE.get(np.dtype(dtype))
@@ -188,10 +270,18 @@ def install(mod, lib_path):
         out = _apply(mod, self, X, dtype)
         return out if out is not None else orig_srht(self, X, dtype)
 
-    rhqr_left.__doc__, rec_rhqr.__doc__ = orig_left.__doc__, orig_rec.__doc__
+    orig_arn = mod.krylov.rhqr_arnoldi
+
+    def rhqr_arnoldi(A, b, x0, m, omega, scaling=mod.linalg.SCALE_SQRT2, policy=None, store_q=True, happy_tol=None):
+        mod.linalg.check_scaling(scaling)
+        out = _arnoldi(mod, A, b, x0, m, omega, scaling, policy, store_q, happy_tol)
+        return out if out is not None else orig_arn(A, b, x0, m, omega, scaling, policy, store_q, happy_tol)
+
+    rhqr_left.__doc__, rec_rhqr.__doc__, rhqr_arnoldi.__doc__ = orig_left.__doc__, orig_rec.__doc__, orig_arn.__doc__
     saved["funcs"] = []
     import sys
-    for name, new, old in (("rhqr_left", rhqr_left, orig_left), ("rec_rhqr", rec_rhqr, orig_rec)):
+    for name, new, old in (("rhqr_left", rhqr_left, orig_left), ("rec_rhqr", rec_rhqr, orig_rec),
+                           ("rhqr_arnoldi", rhqr_arnoldi, orig_arn)):
         for m2 in list(sys.modules.values()):  # every module that imported the name holds its own reference
             if m2 is not None and getattr(m2, "__name__", "").split(".")[0] == mod.__name__ and getattr(m2, name, None) is old:
                 setattr(m2, name, new)

@@ -84,3 +84,29 @@ def test_reference_package_dispatches_its_hot_path_through_the_c_abi(patched):
     assert np.isfinite(Fs.R).all()
     b200.uninstall(R)
     assert R.rhqr_left.__module__ == "sketchqr.rhqr"
+
+
+def test_reference_gmres_runs_its_arnoldi_through_the_c_abi(patched):
+    import scipy.sparse as sp
+    R, b200 = patched
+    rng = np.random.default_rng(3)
+    n, m = 4000, 18
+    A = sp.diags([np.full(n - 1, -1.0), np.linspace(2.0, 3.0, n), np.full(n - 1, -0.5)], [-1, 0, 1], format="csr")
+    b = rng.standard_normal(n)
+    x0 = rng.standard_normal(n)
+    d = np.linspace(1.0, 2.0, n)
+    ops = (A, A.toarray(), lambda v: d * v)
+    om = R.SRHTSketch(4 * (m + 1), n - m - 1, 9)
+    cpu = [(R.rhqr_arnoldi(op, b, x0, m, om), R.rhqr_gmres(op, b, None, m, om)) for op in ops]
+    b200.install(R, LIB)
+    assert R.krylov.rhqr_arnoldi.__module__ == "sketchqr_b200_binding"
+    for op, (Bc, (xc, hc)) in zip(ops, cpu):
+        Bg = R.rhqr_arnoldi(op, b, x0, m, om)
+        assert Bg.breakdown == Bc.breakdown and abs(Bg.beta - Bc.beta) <= 1e-13 * abs(Bc.beta)
+        for k in ("H", "S", "T", "U", "Q_cols"):
+            assert rel(getattr(Bg, k), getattr(Bc, k)) < 1e-10, k
+        xg, hg = R.rhqr_gmres(op, b, None, m, om)          # the reference's own driver around the patched Arnoldi
+        assert rel(xg, xc) < 1e-10 and rel(hg, hc) < 1e-10
+    with pytest.raises(ZeroDivisionError):                  # a failing user matvec surfaces as itself
+        R.rhqr_arnoldi(lambda v: v / 0 if False else (_ for _ in ()).throw(ZeroDivisionError()), b, None, m, om)
+    b200.uninstall(R)

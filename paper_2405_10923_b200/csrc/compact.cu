@@ -450,7 +450,7 @@ update_dmma_kernel(const double* __restrict__ U, int64_t ldu, int64_t N, int r, 
 
 int launch_update_dmma(sqb_ctx* ctx, const double* U, int64_t ldu, int64_t N, int64_t r, const double* C,
                        const double* X, int64_t ldx, int64_t k, double* Out, int64_t ldo) {
-  cudaFuncSetAttribute(update_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TQ_SMEM);
+  allow_dyn_smem(update_dmma_kernel, (size_t)(TQ_SMEM));
   const int ncb = (int)((k + TQ_BN - 1) / TQ_BN);
   const int64_t tiles = (N + TQ_BM - 1) / TQ_BM;
   update_dmma_kernel<<<(unsigned)(tiles * ncb), TQ_NT, TQ_SMEM, ctx->stream>>>(U, ldu, N, (int)r, C, (int)k, ncb, X, ldx,
@@ -464,7 +464,7 @@ static int launch_thin_q(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, in
   if (k > 400) return set_error(ctx, SQB_ERR_ARG, "thin_q: k=%lld above 400", (long long)k);
   static const bool old_path = [] { const char* e = getenv("SQB_THINQ_OLD"); return e && e[0] == '1'; }();
   if (!old_path) {
-    cudaFuncSetAttribute(thin_q_dmma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TQ_SMEM);
+    allow_dyn_smem(thin_q_dmma_kernel<T>, (size_t)(TQ_SMEM));
     const int ncb = (int)((k + TQ_BN - 1) / TQ_BN);
     const int64_t tiles = (N + TQ_BM - 1) / TQ_BM;
     thin_q_dmma_kernel<T><<<(unsigned)(tiles * ncb), TQ_NT, TQ_SMEM, ctx->stream>>>((const T*)U, ldu, N, (int)k, M,
@@ -473,8 +473,7 @@ static int launch_thin_q(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, in
   }
   if (k > 400) return set_error(ctx, SQB_ERR_ARG, "thin_q: k=%lld above 400", (long long)k);
   const size_t smem = sizeof(double) * k * std::min<int64_t>(64, k);
-  cudaFuncSetAttribute(thin_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(smem, 48 * 1024));
+  allow_dyn_smem(thin_q_kernel<T>, (size_t)(std::max<size_t>(smem, 48 * 1024)));
   const unsigned nb = (unsigned)((k + 63) / 64);
   thin_q_kernel<T><<<dim3((unsigned)std::min<int64_t>((N + 255) / 256, 2 * 148), nb), 256, smem, ctx->stream>>>(
       (const T*)U, ldu, N, (int)k, M, Q, ldq);
@@ -667,7 +666,7 @@ int gram_run(sqb_ctx* ctx, const double* A, int64_t lda, int64_t N, int64_t k, d
     const size_t iP = plan.add(sizeof(double) * nb * k * k);
     SQB_TRY(ws_reserve(ctx, plan.total));
     double* P = ws_ptr<double>(ctx, plan, iP);
-    cudaFuncSetAttribute(gram_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GR_SMEM);
+    allow_dyn_smem(gram_dmma_kernel, (size_t)(GR_SMEM));
     gram_dmma_kernel<<<dim3((unsigned)nb, (unsigned)npairs), GR_NT, GR_SMEM, ctx->stream>>>(A, lda, N, (int)k, nblk,
                                                                                           rows_per, P);
     SQB_TRY(check_launch(ctx, "gram_dmma_kernel"));
@@ -807,7 +806,7 @@ int residual_norms_run(sqb_ctx* ctx, const double* W, int64_t ldw, const double*
     const size_t iP = plan.add(sizeof(double) * 2 * kc * nb);
     SQB_TRY(ws_reserve(ctx, plan.total));
     double* P = ws_ptr<double>(ctx, plan, iP);
-    cudaFuncSetAttribute(residual_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TQ_SMEM);
+    allow_dyn_smem(residual_dmma_kernel, (size_t)(TQ_SMEM));
     residual_dmma_kernel<<<(unsigned)(nb * ncb), TQ_NT, TQ_SMEM, ctx->stream>>>(W, ldw, Q, ldq, R, ldr, N, (int)k,
                                                                                (int)kc, ncb, nb, P);
     SQB_TRY(check_launch(ctx, "residual_dmma_kernel"));
@@ -901,7 +900,7 @@ static int arnoldi_q_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int6
   // for 2^20 x 51 and held M in shared memory, which capped r c at 25600)
   static const bool old_path = [] { const char* e = getenv("SQB_THINQ_OLD"); return e && e[0] == '1'; }();
   if (!old_path) {
-    cudaFuncSetAttribute(thin_q_dmma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TQ_SMEM);
+    allow_dyn_smem(thin_q_dmma_kernel<T>, (size_t)(TQ_SMEM));
     const int ncb = (int)((c + TQ_BN - 1) / TQ_BN);
     const int64_t tiles = (N + TQ_BM - 1) / TQ_BM;
     thin_q_dmma_kernel<T><<<(unsigned)(tiles * std::max(ncb, 1)), TQ_NT, TQ_SMEM, ctx->stream>>>(
@@ -911,7 +910,7 @@ static int arnoldi_q_t(sqb_ctx* ctx, const void* U, int64_t ldu, int64_t N, int6
   if ((int64_t)r * c * 8 > 200 * 1024) return set_error(ctx, SQB_ERR_ARG, "arnoldi_q: r*c too large");
   const size_t smem = sizeof(double) * std::max<int64_t>(1, r * c);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(compact_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(compact_q_kernel<T>, (size_t)(smem));
   compact_q_kernel<T><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 4 * 148)), 256, smem,
                         ctx->stream>>>((const T*)U, ldu, N, (int)r, (int)c, M, Q, ldq);
   return check_launch(ctx, "compact_q_kernel");

@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdarg>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -92,6 +94,36 @@ struct sqb_ctx {
 };
 
 namespace sqb {
+
+// Opt-in dynamic shared memory of a kernel.  The limit is a property of the
+// kernel on the device, shared by every host thread and context: setting it to
+// each call's own size races (thread A raises it, thread B lowers it, A's
+// launch then fails with cudaErrorCooperativeLaunchTooLarge / invalid value).
+// It is therefore set ONCE per (device, kernel) to the opt-in maximum less the
+// kernel's static shared memory, and never lowered.
+template <typename K>
+inline cudaError_t allow_dyn_smem(K kern, size_t needed) {
+  static std::mutex mu;
+  static std::unordered_map<unsigned long long, int> limit;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long key = (unsigned long long)reinterpret_cast<uintptr_t>(reinterpret_cast<const void*>(kern)) ^
+                                 ((unsigned long long)dev << 56);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = limit.find(key);
+  if (it == limit.end()) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    int optin = 227 * 1024;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int lim = optin - (int)fa.sharedSizeBytes;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if (e != cudaSuccess) return e;
+    it = limit.emplace(key, lim).first;
+  }
+  return needed <= (size_t)it->second ? cudaSuccess : cudaErrorInvalidValue;
+}
 
 inline int set_error(sqb_ctx* ctx, int code, const char* fmt, ...) {
   if (ctx) {

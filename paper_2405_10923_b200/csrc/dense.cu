@@ -361,7 +361,7 @@ int launch_dense<double>(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int6
   const int S = dense_slabs(sk->ell, k, sk->n, 148, &ks);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dense_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DSMEM);
+    allow_dyn_smem(dense_dmma_kernel, (size_t)(DSMEM));
     attr = true;
   }
   dim3 grid((unsigned)((sk->ell + DBM - 1) / DBM), (unsigned)((k + DBN - 1) / DBN), (unsigned)S);
@@ -377,7 +377,7 @@ int launch_dense<double>(sqb_ctx* ctx, const sqb_sketch* sk, const void* X, int6
   if (tma_ok) {
     static bool attr_t = false;
     if (!attr_t) {
-      cudaFuncSetAttribute(dense_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TM_SMEM);
+      allow_dyn_smem(dense_tma_kernel, (size_t)(TM_SMEM));
       attr_t = true;
     }
     dim3 gt((unsigned)((sk->ell + TM_BM - 1) / TM_BM), (unsigned)((k + TM_BN - 1) / TM_BN), (unsigned)S);
@@ -407,7 +407,7 @@ int launch_dense_slabs(sqb_ctx* ctx, cudaStream_t stream, const sqb_sketch* sk, 
                        int64_t k, int z0, int z1, int64_t kslab, void* ws, const Status* st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dense_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DSMEM);
+    allow_dyn_smem(dense_dmma_kernel, (size_t)(DSMEM));
     attr = true;
   }
   if (z1 <= z0) return SQB_OK;

@@ -226,8 +226,7 @@ int hqr_tall(sqb_ctx* ctx, int scaling, const double* A, int64_t lda, int64_t p,
   SQB_CUDA_TRY(cudaMemset2DAsync(T, ldt * sizeof(double), 0, m * sizeof(double), m, ctx->stream));
   SQB_CUDA_TRY(cudaMemset2DAsync(R, ldr * sizeof(double), 0, m * sizeof(double), m, ctx->stream));
   const size_t dsm_max = sizeof(double) * (GEMV_NT / 32 + 1) * m;
-  cudaFuncSetAttribute(hqrt_dots_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(dsm_max, 48 << 10));
+  allow_dyn_smem(hqrt_dots_kernel, (size_t)(std::max<size_t>(dsm_max, 48 << 10)));
   const unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p + 255) / 256, 4 * (int64_t)ctx->sm_count));
   for (int c = 0; c < (int)m; ++c) {
     const size_t dsm = sizeof(double) * (GEMV_NT / 32 + 1) * std::max(c, 1);

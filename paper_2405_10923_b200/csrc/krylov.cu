@@ -434,8 +434,7 @@ static int arnoldi_t(sqb_ctx* ctx, const sqb_sketch* sk, const OpDesc& op, int m
   SQB_TRY(launch_sketch(ctx, sk, Lo<T>::code, (T*)U + mt, n, 1, z, od, mt, P, st));
   SQB_TRY(flush_copy_top(ctx, st));
   const size_t step_smem = sizeof(double) * (od + 3 * mt + 32);
-  cudaFuncSetAttribute(arn_step_cl_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(step_smem, 48 << 10));
+  allow_dyn_smem(arn_step_cl_kernel<T>, (size_t)(std::max<size_t>(step_smem, 48 << 10)));
   constexpr int VN = VecN<T>::n;
   if (!(((reinterpret_cast<uintptr_t>(U) & 15) == 0) && (ldu % VN == 0)))
     return set_error(ctx, SQB_ERR_ARG, "Arnoldi basis U must be 16-byte aligned with ldu %% %d == 0", VN);
@@ -697,8 +696,7 @@ static int arnoldi_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int m, int scaling
   for (int r = 0; r < L; ++r) SQB_TRY(spmv(rk[r], rk[r].b));
   SQB_TRY(sketch_all(&ArnRank::w, &ArnRank::z));
   const size_t step_smem = sizeof(double) * (od + 3 * mt + 32);
-  cudaFuncSetAttribute(arn_step_cl_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(step_smem, 48 << 10));
+  allow_dyn_smem(arn_step_cl_kernel<T>, (size_t)(std::max<size_t>(step_smem, 48 << 10)));
   for (int j = 1; j <= mt; ++j) {
     for (int r = 0; r < L; ++r) {
       ArnRank& d = rk[r];

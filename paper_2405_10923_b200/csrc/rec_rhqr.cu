@@ -474,12 +474,11 @@ int rec_finish_t(sqb_ctx* ctx, int scaling, const double* Z, int64_t od, int64_t
   const size_t hsm = sizeof(double) * (od + 2 * m + 32);
   const size_t hsm_res = hsm + sizeof(double) * ((size_t)od * m + (size_t)m * m);
   if (hsm_res <= 227 * 1024) {
-    cudaFuncSetAttribute(hqr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm_res);
+    allow_dyn_smem(hqr_kernel<true>, (size_t)(hsm_res));
     hqr_kernel<true><<<1, HQR_NT, hsm_res, ctx->stream>>>(Z, od, (int)od, (int)m, scaling, S, lds, Tm, ldt, R, ldr,
                                                           sigmas, rhos, betas, st);
   } else {
-    cudaFuncSetAttribute(hqr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max<size_t>(hsm, 48 << 10));
+    allow_dyn_smem(hqr_kernel<false>, (size_t)(std::max<size_t>(hsm, 48 << 10)));
     hqr_kernel<false><<<1, HQR_NT, hsm, ctx->stream>>>(Z, od, (int)od, (int)m, scaling, S, lds, Tm, ldt, R, ldr,
                                                        sigmas, rhos, betas, st);
   }
@@ -500,11 +499,11 @@ int rec_finish_t(sqb_ctx* ctx, int scaling, const double* Z, int64_t od, int64_t
                          ((reinterpret_cast<uintptr_t>(W2) & 15) == 0) && ((reinterpret_cast<uintptr_t>(U2) & 15) == 0) &&
                          (ldw % 2 == 0) && (ldu % 2 == 0) && !getenv("SQB_TRSM_BASE");
     if (pipe_ok) {
-      cudaFuncSetAttribute(trsm_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM);
+      allow_dyn_smem(trsm_pipe_kernel, (size_t)(TP_SMEM));
       const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + TP_ROWS - 1) / TP_ROWS, 2 * (int64_t)ctx->sm_count));
       trsm_pipe_kernel<<<gt, TP_NT, TP_SMEM, ctx->stream>>>((const double*)W2, ldw, n, (int)m, mp, M, (double*)U2, ldu, st);
     } else if (m > 16 && tsm <= 200 * 1024) {
-      cudaFuncSetAttribute(trsm_dmma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      allow_dyn_smem(trsm_dmma_kernel<T>, (size_t)(tsm));
       const unsigned gt = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + TR_ROWS - 1) / TR_ROWS, 2 * (int64_t)ctx->sm_count));
       trsm_dmma_kernel<T><<<gt, TR_NT, tsm, ctx->stream>>>(W2, ldw, n, (int)m, mp, M, U2, ldu, st);
     } else if (m <= 16) {
@@ -649,12 +648,11 @@ extern "C" int sqb_householder_qr(sqb_ctx* ctx, int scaling, const double* A, in
   }
   const size_t hsm_res = hsm + sizeof(double) * ((size_t)p * m + (size_t)m * m);
   if (hsm_res <= 227 * 1024) {
-    cudaFuncSetAttribute(hqr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm_res);
+    allow_dyn_smem(hqr_kernel<true>, (size_t)(hsm_res));
     hqr_kernel<true><<<1, HQR_NT, hsm_res, ctx->stream>>>(A, lda, (int)p, (int)m, scaling, U, ldu, T, ldt, R, ldr,
                                                           sigmas, rhos, betas, ctx->d_status);
   } else {
-    cudaFuncSetAttribute(hqr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max<size_t>(hsm, 48 << 10));
+    allow_dyn_smem(hqr_kernel<false>, (size_t)(std::max<size_t>(hsm, 48 << 10)));
     hqr_kernel<false><<<1, HQR_NT, hsm, ctx->stream>>>(A, lda, (int)p, (int)m, scaling, U, ldu, T, ldt, R, ldr,
                                                        sigmas, rhos, betas, ctx->d_status);
   }

@@ -282,7 +282,7 @@ static int panel_update(sqb_ctx* ctx, const T* U, int64_t ldu, int64_t N, int64_
   if constexpr (std::is_same<T, double>::value) {
     if (bp <= PD_KC && b <= PD_NC) {
       const size_t smem = sizeof(double) * (2 * PD_KC * PD_US + PD_KC * PD_CS);
-      cudaFuncSetAttribute(panel_update_dmma32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      allow_dyn_smem(panel_update_dmma32_kernel, (size_t)(smem));
       const unsigned grid = (unsigned)std::min<int64_t>(blocks, 2 * (int64_t)ctx->sm_count);
       panel_update_dmma32_kernel<<<grid, 256, smem, ctx->stream>>>(U, ldu, N, (int)bp, C, ldc, X, ldx, (int)b,
                                                                    ctx->d_status);

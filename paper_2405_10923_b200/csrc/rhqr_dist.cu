@@ -155,8 +155,7 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
   SQB_TRY(combine_gathered<T>(ctx, p2p, G0, nranks, ell, m, rank_level, sk->indices, g.log_tb, norm_lo, Y0, od,
                               xseq));
   const size_t step_smem = step_smem_bytes((int)od, (int)m);
-  cudaFuncSetAttribute(rhqr_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(step_smem, 48 * 1024));
+  allow_dyn_smem(rhqr_step_kernel<T>, (size_t)(std::max<size_t>(step_smem, 48 * 1024)));
   // real ranks over peer memory: the step kernel itself folds the rank-local
   // subtree, stores it into the peers' mailboxes and waits for theirs (tree =
   // 3): two launches per column, as on one GPU.  Virtual ranks share one
@@ -205,8 +204,8 @@ static int rhqr_dist_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, int64_t 
   constexpr int VN = VecN<T>::n;
   const size_t tile_bytes = tile_smem_bytes<A>(1 << TileCfg<T>::LOG_TB);
   const size_t col_smem_max = sizeof(A) * ((m + 3) & ~3) + std::max(tile_bytes, sizeof(double) * (size_t)(m + 1));
-  cudaFuncSetAttribute(col_kernel_select<T, VN>(true), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
-  cudaFuncSetAttribute(col_kernel_select<T, VN>(false), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
+  allow_dyn_smem(col_kernel_select<T, VN>(true), (size_t)(col_smem_max));
+  allow_dyn_smem(col_kernel_select<T, VN>(false), (size_t)(col_smem_max));
   for (int64_t c = 1; c < m; ++c) {
     for (int r = 0; r < L; ++r) {
       DistRank& d = rk[r];

@@ -140,8 +140,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
   SQB_TRY(ensure_y0(2));
 
   const size_t step_smem = step_smem_bytes((int)od, (int)m);
-  cudaFuncSetAttribute(rhqr_step_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)std::max<size_t>(step_smem, 48 * 1024));
+  allow_dyn_smem(rhqr_step_kernel<T>, (size_t)(std::max<size_t>(step_smem, 48 * 1024)));
   // column 0: y = y0_0 (w = W[:, 0]); a_1 is empty
   StepArgs sa{};
   sa.c = 0; sa.m = (int)m; sa.ell = (int)ell; sa.od = (int)od; sa.scaling = scaling; sa.tree = 0;
@@ -181,7 +180,7 @@ int left_sweep_t(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const void* W,
   if constexpr (std::is_same<T, double>::value) {
     if (small) colk = rhqr_col_kernel<T, VN, 0, 2, SMALL_LOG>;
   }
-  cudaFuncSetAttribute(colk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem_max);
+  allow_dyn_smem(colk, (size_t)(col_smem_max));
   for (int64_t c = 1; c < ncol; ++c) {
     SQB_TRY(ensure_y0(c + 2));
     double* a_cur = abuf + (c & 1) * (m + 1);

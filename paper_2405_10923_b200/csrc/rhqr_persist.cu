@@ -934,7 +934,7 @@ int launch_persist(sqb_ctx* ctx, const sqb_sketch* sk, int scaling, const double
   if (a.stage_leaves) smem += lv_bytes;
   a.dbg = ctx->dbg_col == -2 ? ctx->dbg_ts : nullptr;
   void (*kern)(PersistArgs) = a.fast ? rhqr_persist_fast_kernel : rhqr_persist_kernel;
-  SQB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SQB_CUDA_TRY(allow_dyn_smem(kern, smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.n_eff + (a.fast ? 3 : 1)));
   cfg.blockDim = dim3(PS_NT);

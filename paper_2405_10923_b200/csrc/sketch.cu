@@ -697,7 +697,7 @@ static int launch_tma(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, int
   const size_t smem = 1024 + (size_t)WPB * S * Tma<T>::STAGE + sizeof(T) * (size_t)WPB * 32 * wt_rs<T>() +
                        (size_t)WPB * S * 8;
   auto kern = srht_tma_tile_kernel<T, KPL, S, WPB, LG>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_dyn_smem(kern, (size_t)(smem));
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem);
@@ -727,7 +727,7 @@ static int launch_tma_split(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& 
   if (r != CUDA_SUCCESS) return set_error(ctx, SQB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   const size_t smem = 1024 + 4 * (size_t)Tma<T>::STAGE + sizeof(T) * 4 * 32 * (size_t)(wt_rs<T>() + KPL) + 4 * 8;
   auto kern = srht_tma_split_kernel<T, KPL>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_dyn_smem(kern, (size_t)(smem));
   const int64_t items = g.n_eff * k;
   kern<<<(unsigned)std::min<int64_t>(items, 65535), 128, smem, ctx->stream>>>(
       map, X, ldx, n_local, g.n_eff, k, sk->sign_bits, sk->indices, (int)sk->ell, sc, P, g.n_tiles, st, e_base);
@@ -1078,7 +1078,7 @@ static int launch_tma16(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom& g, i
   if (r != CUDA_SUCCESS) return set_error(ctx, SQB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   const size_t smem = 1024 + (size_t)WPB * S * 4096 + 4 * (size_t)WPB * 32 * 36 + (size_t)WPB * S * 8;
   auto kern = srht_tma16_tile_kernel<T, KPL, S, WPB>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_dyn_smem(kern, (size_t)(smem));
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem);
@@ -1283,7 +1283,7 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
     }
     if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= S64_MAX_ELL) {
       const size_t smemh = s64_head_bytes((int)sk->ell, 2) + s64_buf_bytes<T>();
-      cudaFuncSetAttribute(srht64h_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemh);
+      allow_dyn_smem(srht64h_tile_kernel<T>, (size_t)(smemh));
       cudaFuncSetAttribute(srht64h_tile_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
       int per_sm = 1;
@@ -1308,7 +1308,7 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
       return launch_tma_kpl<T, 2, 4>(ctx, sk, g, n_local, e_base, (const T*)X, ldx, k, (T)sc, (T*)P, st);
     if (vec && g.log_tb == S64_LOG && (e_base & 63) == 0 && sk->ell <= S64_MAX_ELL) {
       const size_t smem64 = s64_head_bytes((int)sk->ell, sizeof(T)) + s64_buf_bytes<T>();
-      cudaFuncSetAttribute(srht64_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64);
+      allow_dyn_smem(srht64_tile_kernel<T>, (size_t)(smem64));
       cudaFuncSetAttribute(srht64_tile_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
       int per_sm = 1;
@@ -1324,13 +1324,13 @@ static int srht_tiles_geom_t(sqb_ctx* ctx, const sqb_sketch* sk, const SrhtGeom&
   }
   if (vec) {
     auto kern = srht_tile_kernel<T, VN>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(kern, (size_t)(smem));
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     kern<<<grid, SRHT_NT, smem, ctx->stream>>>((const T*)X, ldx, n_local, g.log_tb, sk->sign_bits,
                                                sk->indices, (int)sk->ell, (A)sc, (A*)P, g.n_tiles, st, e_base);
   } else {
     auto kern = srht_tile_kernel<T, 1>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(kern, (size_t)(smem));
     kern<<<grid, SRHT_NT, smem, ctx->stream>>>((const T*)X, ldx, n_local, g.log_tb, sk->sign_bits,
                                                sk->indices, (int)sk->ell, (A)sc, (A*)P, g.n_tiles, st, e_base);
   }

@@ -20,7 +20,9 @@
 // bandwidth (the facade allocates its outputs that way); pageable buffers
 // work but the driver stages them synchronously.
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -176,25 +178,69 @@ static bool host_is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
 }
 
-static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-  static const unsigned nt = [] {
+// A small pool of host threads that lives for the process (leaked on purpose:
+// no static-destruction order to get wrong); one memcpy job at a time, split in
+// page-aligned parts.  Spawning threads per 16 MB slot cost ~10 ms per GiB.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* p = new CopyPool();
+    return *p;
+  }
+  void copy(void* dst, const void* src, size_t bytes) {
+    if (bytes < (4u << 20) || workers_ == 0) {
+      memcpy(dst, src, bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> job(job_mu_);  // one job at a time (contexts on several threads share the pool)
+    const unsigned parts = workers_ + 1;
+    const size_t part = ((bytes + parts - 1) / parts + 4095) & ~size_t(4095);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      dst_ = (char*)dst; src_ = (const char*)src; bytes_ = bytes; part_ = part;
+      pending_ = workers_;
+      ++gen_;
+    }
+    cv_.notify_all();
+    memcpy(dst, src, std::min(part, bytes));  // part 0 on the calling thread
+    std::unique_lock<std::mutex> g(mu_);
+    done_.wait(g, [&] { return pending_ == 0; });
+  }
+
+ private:
+  CopyPool() {
     const unsigned hc = std::thread::hardware_concurrency();
-    return std::max(1u, std::min(8u, hc ? hc / 2 : 4u));
-  }();
-  if (bytes < (4u << 20) || nt == 1) {
-    memcpy(dst, src, bytes);
-    return;
+    workers_ = std::max(1u, std::min(8u, hc ? hc / 2 : 4u)) - 1;
+    for (unsigned t = 0; t < workers_; ++t) std::thread([this, t] { run(t + 1); }).detach();
   }
-  const size_t part = ((bytes + nt - 1) / nt + 4095) & ~size_t(4095);
-  std::vector<std::thread> th;
-  for (unsigned t = 1; t < nt; ++t) {
-    const size_t o = (size_t)t * part;
-    if (o >= bytes) break;
-    th.emplace_back([=] { memcpy((char*)dst + o, (const char*)src + o, std::min(part, bytes - o)); });
+  void run(unsigned idx) {
+    unsigned long long seen = 0;
+    for (;;) {
+      char* d; const char* sp; size_t n, part;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        d = dst_; sp = src_; n = bytes_; part = part_;
+      }
+      const size_t o = (size_t)idx * part;
+      if (o < n) memcpy(d + o, sp + o, std::min(part, n - o));
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
   }
-  memcpy(dst, src, std::min(part, bytes));
-  for (auto& t : th) t.join();
-}
+  std::mutex job_mu_, mu_;
+  std::condition_variable cv_, done_;
+  unsigned workers_ = 0, pending_ = 0;
+  unsigned long long gen_ = 0;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0, part_ = 0;
+};
+
+static void parallel_memcpy(void* dst, const void* src, size_t bytes) { CopyPool::get().copy(dst, src, bytes); }
 
 static int staged_h2d(sqb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s, bool pinned) {
   if (pinned || bytes < (1u << 20)) {
